@@ -1,0 +1,258 @@
+/*
+ * pf_gpu.h — C-ABI of the B200 (sm_100a) geometric-multigrid V-cycle hot path.
+ *
+ * This is the drop-in boundary for the data-parallel hot path of the reference
+ * `parfem` library (arXiv:1609.04809 restated as /root/reference/proj).  Every
+ * entry point below replaces one reference C++ function, named in its comment
+ * as `file:line` relative to /root/reference/proj.  The reference keeps its own
+ * mesh / partition / ParFEMapper construction; it hands each MultigridLevel to
+ * pf_hierarchy_set_level() once and then calls the pf_* operations instead of
+ * the CPU loops.  The C++ shim that rethrows the reference's exception types is
+ * include/parfem_b200.hpp; the reference-side binding is shown in
+ * INTEGRATION.md and built in integration/parfem_gpu_bridge.cpp.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; no torch / CUDA types in signatures;
+ *  - every function returns a pf_status; on failure pf_last_error() returns a
+ *    thread-local message.  Status codes map 1:1 onto the reference's
+ *    exception hierarchy (include/parfem/errors.hpp:9-42);
+ *  - "host order" means the reference's rank-local consecutive dof numbering
+ *    (class-sorted, own dofs [0, n_own_dofs) first — femapper.hpp:16-25).
+ *    The device keeps its own permuted layout; vectors cross the boundary in
+ *    host order through pf_vector_upload / pf_vector_download;
+ *  - a hierarchy holds `n_subdomains` consecutive ranks [rank_base,
+ *    rank_base + n_subdomains) of a `world_size`-rank decomposition.  With one
+ *    process per GPU n_subdomains = 1; several subdomains on one device are the
+ *    single-GPU stand-in for several ranks (exchanges become device copies);
+ *  - all arithmetic is fp64 with the reference's per-row summation order and
+ *    no fused multiply-add, so damped Jacobi reproduces the reference
+ *    iterate for iterate.
+ */
+#ifndef PF_GPU_H
+#define PF_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PF_OK = 0,
+  PF_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (linalg.cpp:46-48, fecomm.cpp:18-23) */
+  PF_ERR_SINGULAR_DIAGONAL = 2, /* SingularDiagonalError (solvers.cpp:10-15)                */
+  PF_ERR_NO_CONVERGENCE = 3,    /* NoConvergenceError (multigrid.cpp:241-244)              */
+  PF_ERR_TRANSPORT = 4,         /* TransportError (transport.cpp:49-60)                    */
+  PF_ERR_CUDA = 5,              /* Error: device / driver failure                          */
+  PF_ERR_STATE = 6              /* Error: API used out of order                            */
+} pf_status;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* pf_last_error(void);
+/* Library version string and build flags (arch, compiler). */
+const char* pf_version(void);
+
+/* ---------------------------------------------------------------- enums -- */
+
+/* parfem::ChannelKind (femapper.hpp:27). */
+enum { PF_CH_MASTER_SLAVE = 0, PF_CH_HALO1 = 1, PF_CH_HALO2 = 2, PF_NUM_CHANNEL_KINDS = 3 };
+
+/* parfem::UpdateMode (fecomm.hpp:28). */
+enum { PF_UPDATE_SCATTER = 0, PF_UPDATE_ACCUMULATE_THEN_SCATTER = 1 };
+
+/* parfem::SmootherKind (solvers.hpp:7) plus the B200 multicolour SOR.
+ * PF_SMOOTHER_GAUSS_SEIDEL on the device is multicolour Gauss-Seidel (omega = 1)
+ * in the explicit colour order given at upload. */
+enum { PF_SMOOTHER_JACOBI = 0, PF_SMOOTHER_GAUSS_SEIDEL = 1, PF_SMOOTHER_MULTICOLOR_SOR = 2 };
+
+/* ---------------------------------------------------------------- types -- */
+
+/* One peer of one ParFECommunicator channel (femapper.hpp:38-41): the i-th entry
+ * of send_dofs here and of recv_dofs on `peer` name the same carrier. */
+typedef struct {
+  int32_t kind;  /* PF_CH_* */
+  int32_t peer;  /* global rank, != own rank */
+  int32_t n_send;
+  int32_t n_recv;
+  const int32_t* send_dofs; /* host order */
+  const int32_t* recv_dofs; /* host order */
+} pf_channel_desc;
+
+/* One rank's view of one MultigridLevel (multigrid.hpp:15-31) in host order. */
+typedef struct {
+  int32_t n_dofs;     /* ParFEMapper::n_dofs */
+  int32_t n_own_dofs; /* ParFEMapper::n_own_dofs: rows [0, n_own) are swept and normed */
+  /* level operator `system` (Dirichlet rows applied), full local CSR, n_dofs rows,
+   * columns sorted ascending per row (linalg.hpp:12-22) */
+  const int64_t* row_offsets; /* n_dofs + 1 */
+  const int32_t* col_indices;
+  const double* values;
+  const uint8_t* owns_row;     /* n_dofs, ParFEMapper::owns_row            */
+  const uint8_t* is_dirichlet; /* n_dofs, class_of == DofClass::Dirichlet  */
+  /* colour of each own row for the coloured smoothers, or NULL: greedy colouring
+   * of the own-row graph in host order */
+  const int32_t* color;
+  int32_t n_channels;
+  const pf_channel_desc* channels;
+  /* MultigridLevel::prolong_map (multigrid.cpp:35-72) as CSR over the n_dofs fine
+   * rows, entries in the reference's (coarse dof, weight) order; NULL on level 0 */
+  const int64_t* p_offsets;
+  const int32_t* p_cols;
+  const double* p_weights;
+} pf_level_desc;
+
+/* parfem::SmootherConfig (solvers.hpp:9-14). `damping` is the Jacobi damping and
+ * the SOR relaxation factor; ignored for Gauss-Seidel. */
+typedef struct {
+  int32_t kind;
+  int32_t sweeps;
+  int32_t local_sweeps;
+  double damping;
+} pf_smoother_config;
+
+/* parfem::MultigridConfig (multigrid.hpp:53-62). */
+typedef struct {
+  int32_t cycles;
+  pf_smoother_config smoother;
+  int32_t pre_smooth;
+  int32_t post_smooth;
+  double coarse_tol;
+  int32_t coarse_max_iter;
+  double outer_tol;
+  int32_t outer_max_cycles;
+} pf_multigrid_config;
+
+/* parfem::SolveStats (linalg.hpp:37-45) minus the residual vector, which the
+ * solve functions write to a caller array. */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double initial_residual;
+  double final_residual;
+  double solve_seconds;
+  double comm_seconds;
+} pf_solve_stats;
+
+typedef struct pf_hierarchy pf_hierarchy;
+typedef struct pf_vector pf_vector;
+
+/* Defaults of the reference structs. */
+void pf_default_smoother_config(pf_smoother_config* out);
+void pf_default_multigrid_config(pf_multigrid_config* out);
+
+/* ------------------------------------------------------------ hierarchy -- */
+
+/* Replaces the device side of build_hierarchy (multigrid.cpp:76-119). */
+pf_status pf_hierarchy_create(int device, int n_levels, int n_subdomains, int rank_base,
+                              int world_size, pf_hierarchy** out);
+/* Copies one rank's level data; arrays may be freed after the call. */
+pf_status pf_hierarchy_set_level(pf_hierarchy* h, int level, int subdomain,
+                                 const pf_level_desc* desc);
+/* Uploads all levels: device layout, colour permutation, R = P^T, exchange plans.
+ * Raises PF_ERR_SINGULAR_DIAGONAL for a zero or missing own-row diagonal — the check
+ * smooth() repeats on every call in the reference (solvers.cpp:10-15, :57). */
+pf_status pf_hierarchy_finalize(pf_hierarchy* h);
+/* Multi-process: join the NCCL communicator of `world_size` ranks (one hierarchy per
+ * process).  `unique_id` is the 128-byte ncclUniqueId from pf_nccl_unique_id() on
+ * rank 0, broadcast by the caller. */
+pf_status pf_nccl_unique_id(void* out, int nbytes);
+pf_status pf_hierarchy_init_nccl(pf_hierarchy* h, const void* unique_id, int nbytes);
+pf_status pf_hierarchy_destroy(pf_hierarchy* h);
+
+/* Device bytes held by the hierarchy (matrices, transfers, plans, scratch). */
+pf_status pf_hierarchy_device_bytes(const pf_hierarchy* h, int64_t* out);
+
+/* -------------------------------------------------------------- vectors -- */
+
+/* DistributedVector (fecomm.hpp:16-26) on one level: one device array per subdomain. */
+pf_status pf_vector_create(pf_hierarchy* h, int level, pf_vector** out);
+pf_status pf_vector_destroy(pf_vector* v);
+/* Host order in/out.  Pinned host memory (pf_host_alloc) makes these asynchronous-
+ * fast; pageable memory works but is staged. */
+pf_status pf_vector_upload(pf_vector* v, int subdomain, const double* host, int64_t n);
+pf_status pf_vector_download(const pf_vector* v, int subdomain, double* host, int64_t n);
+pf_status pf_vector_fill(pf_vector* v, double value);
+pf_status pf_host_alloc(void** out, int64_t bytes);
+pf_status pf_host_free(void* p);
+
+/* ------------------------------------------------------------ operations -- */
+
+/* spmv (linalg.cpp:45-57): y = A x on every local row. */
+pf_status pf_spmv(pf_hierarchy* h, int level, const pf_vector* x, pf_vector* y);
+
+/* residual_norm (linalg.cpp:59-74): sqrt of the ascending-rank sum of per-rank
+ * sum_{r < n_own} (b_r - A_r x)^2. */
+pf_status pf_residual_norm(pf_hierarchy* h, int level, const pf_vector* x, const pf_vector* b,
+                           double* out);
+
+/* smooth (solvers.cpp:56-68): `sweeps` x [local_sweeps x sweep on own rows, then
+ * update_master_slave(Scatter) and update_halo1]. */
+pf_status pf_smooth(pf_hierarchy* h, int level, pf_vector* x, const pf_vector* b,
+                    const pf_smoother_config* cfg);
+
+/* coarse_solve (solvers.cpp:70-92): Gauss-Seidel + residual_norm until
+ * <= tol * r0 or max_iter; non-convergence is reported in stats, not raised. */
+pf_status pf_coarse_solve(pf_hierarchy* h, int level, pf_vector* x, const pf_vector* b,
+                          double tol, int max_iter, pf_solve_stats* stats);
+
+/* prolongate (multigrid.cpp:121-129): out = P xc on every local fine dof. */
+pf_status pf_prolongate(pf_hierarchy* h, int fine_level, const pf_vector* coarse, pf_vector* out);
+
+/* restrict_residual (multigrid.cpp:131-146): rc = P^T r over owns_row fine rows,
+ * then update_master_slave(AccumulateThenScatter) on the coarse level. */
+pf_status pf_restrict_residual(pf_hierarchy* h, int fine_level, const pf_vector* r, pf_vector* rc);
+
+/* ParFECommunicator (fecomm.cpp:41-72). */
+pf_status pf_update_master_slave(pf_hierarchy* h, int level, pf_vector* v, int mode);
+pf_status pf_update_halo1(pf_hierarchy* h, int level, pf_vector* v);
+pf_status pf_update_halo2(pf_hierarchy* h, int level, pf_vector* v);
+
+/* allreduce_sum(Transport&, double) (transport.cpp:139-165): one value per local
+ * subdomain in, ascending-rank sum out (identical on every rank). */
+pf_status pf_allreduce_sum(pf_hierarchy* h, const double* per_subdomain, double* out);
+
+/* v_cycle (multigrid.cpp:194-208) on the finest level; stats = coarse-solve stats. */
+pf_status pf_v_cycle(pf_hierarchy* h, pf_vector* x, const pf_vector* b,
+                     const pf_multigrid_config* cfg, pf_solve_stats* stats);
+
+/* solve_outer (multigrid.cpp:210-246).  residuals[i] = residual after outer cycle i+1
+ * (at most max_residuals written).  Returns PF_ERR_NO_CONVERGENCE after
+ * outer_max_cycles, with stats filled. */
+pf_status pf_solve_outer(pf_hierarchy* h, pf_vector* x, const pf_vector* b,
+                         const pf_multigrid_config* cfg, pf_solve_stats* stats,
+                         double* residuals, int max_residuals);
+
+/* End-to-end solve_outer from host memory: per local subdomain s, x_host[s] (in: start
+ * vector, out: solution) and b_host[s], host order.  Host->device copies, the solve and
+ * the device->host copy all happen inside this call. */
+pf_status pf_solve_outer_host(pf_hierarchy* h, double* const* x_host, const double* const* b_host,
+                              const pf_multigrid_config* cfg, pf_solve_stats* stats,
+                              double* residuals, int max_residuals);
+
+/* ------------------------------------------------------------- profiling -- */
+
+/* Number of this library's kernels launched since the last reset (graph nodes
+ * count once per graph launch). */
+pf_status pf_launch_count(const pf_hierarchy* h, int64_t* out);
+pf_status pf_reset_launch_count(pf_hierarchy* h);
+
+/* Times `iters` back-to-back launches of one smoother sweep of `kind` on `level`
+ * (subdomain 0) with CUDA events on the library stream; writes the mean kernel time
+ * in milliseconds and the algorithmic bytes one sweep moves. */
+pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double* mean_ms,
+                        double* algorithmic_bytes);
+
+/* Mean time of one full V-cycle (graph replay) over `iters` cycles, CUDA events. */
+pf_status pf_time_vcycle(pf_hierarchy* h, pf_vector* x, const pf_vector* b,
+                         const pf_multigrid_config* cfg, int iters, double* mean_ms);
+
+/* Level geometry as uploaded (for diagnostics and tests). */
+pf_status pf_level_info(const pf_hierarchy* h, int level, int subdomain, int64_t* n_dofs,
+                        int64_t* n_own, int64_t* nnz, int64_t* n_colors);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PF_GPU_H */

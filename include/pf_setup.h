@@ -1,0 +1,68 @@
+/*
+ * pf_setup.h — structured, communication-free setup of the GMG hierarchy data that the
+ * hot path consumes ("scalable setup").
+ *
+ * For the unit square/cube Q1 Poisson problem on n_coarse^d cells refined n_levels-1
+ * times and partitioned by coordinate bisection of the coarse cells (the reference's
+ * only data-parallel decomposition, partition.cpp:35-142, ownership inherited by
+ * children, partition.cpp:255-265), it computes for one rank and every level exactly
+ * what the reference's setup pipeline computes with std::map and a cross-rank
+ * handshake:
+ *   - the subdomain (own cells + one-layer halo closure)     partition.cpp:156-365
+ *   - dof classes Master/Independent/Dependent1/Dependent2/Slave/Halo1/Halo2/Dirichlet,
+ *     including the greedy master balance in key order     femapper.cpp:66-165
+ *   - the MasterSlave / Halo1 / Halo2 channels in key order  femapper.cpp:222-351
+ *   - the Q1 stiffness with Dirichlet rows set to identity   assembly.cpp:48-170
+ *   - the load vector (own cells + accumulate) and rhs       assembly.cpp:144-160
+ *   - the multilinear prolongation map                       multigrid.cpp:35-72
+ * but from closed-form lattice rules, so each rank builds its own data (and its
+ * neighbours' requests) without talking to anyone, in O(local dofs).
+ *
+ * The local numbering is the product's own: own dofs first in lexicographic lattice
+ * order, then Slave, Halo1, Halo2, Dirichlet (each lexicographic) — the reference's
+ * class-sorted layout (femapper.hpp:16-25) with a different order inside each class.
+ * Own rows carry the lattice-parity colour (2^d colours) used by the coloured smoothers.
+ * Results are compared with the reference per carrier key (Key4, tests/support.hpp:18-21).
+ */
+#ifndef PF_SETUP_H
+#define PF_SETUP_H
+
+#include "pf_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pf_setup pf_setup;
+
+/* Problems: 0 = BASELINE (f = d pi^2 prod_a sin(pi x_a), g = 0);
+ *           1 = the reference's PoissonProblem (model.cpp:33-43: sin(pi x) cos(pi y)
+ *               [cos(pi z)], Dirichlet data from the exact solution);
+ *           2 = f = 1, g = 0. */
+enum { PF_PROBLEM_BASELINE = 0, PF_PROBLEM_REFERENCE_POISSON = 1, PF_PROBLEM_UNIT_SOURCE = 2 };
+
+pf_status pf_setup_create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem,
+                          pf_setup** out);
+pf_status pf_setup_destroy(pf_setup* s);
+
+/* Level data in the layout pf_hierarchy_set_level takes; pointers stay valid until
+ * pf_setup_destroy. level 0 = coarsest. */
+pf_status pf_setup_level(const pf_setup* s, int level, pf_level_desc* out);
+/* Per-dof carrier key (entity kind 0 = vertex, lattice x, y, z), 4 int64 per dof, and
+ * DofClass value (femapper.hpp:16-25) per dof. */
+pf_status pf_setup_level_keys(const pf_setup* s, int level, const int64_t** keys4,
+                              const uint8_t** class_of);
+/* Finest-level right-hand side (load with Dirichlet rhs applied) and start vector
+ * (zero except Dirichlet entries = boundary data), app.cpp:253-260. */
+pf_status pf_setup_rhs(const pf_setup* s, const double** b, const double** x0, int64_t* n);
+/* Global dof count of the finest level ((N+1)^d) and this rank's local counts. */
+pf_status pf_setup_counts(const pf_setup* s, int level, int64_t* n_global, int64_t* n_dofs,
+                          int64_t* n_own, int64_t* nnz);
+/* Seconds spent in pf_setup_create. */
+pf_status pf_setup_seconds(const pf_setup* s, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PF_SETUP_H */

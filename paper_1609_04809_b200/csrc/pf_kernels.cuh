@@ -1,0 +1,394 @@
+// pf_kernels.cuh — sm_100a kernels of the GMG V-cycle hot path.
+//
+// Storage: every level operator is SELL-32 — slices of 32 consecutive device rows,
+// column-major inside a slice (entry j of the slice's lane l at
+// slice_ptr[s] + 32*j + l), so a warp's load of entry j of its 32 rows is one
+// 256 B (values) + 128 B (columns) contiguous transaction.  Entries of a row keep
+// the reference's CSR order (linalg.hpp:12-22), which fixes the summation order.
+//
+// Arithmetic: every product and sum is rounded separately (__dmul_rn / __dadd_rn /
+// __dsub_rn / __ddiv_rn, never an FMA), reproducing the reference's x86-64 SSE2
+// evaluation of the same expressions, so Jacobi iterates match bit for bit.
+//
+// HBM behaviour: matrix values/columns are read exactly once per sweep with
+// streaming loads (evict-first: they are 12 B/nnz and never reused inside a sweep);
+// the x gather goes through the read-only path and stays L2-resident (the whole
+// finest x at 128^3 is 17 MB of a 126 MB L2).
+#pragma once
+
+#include <cstdint>
+
+#include "pf_types.hpp"
+
+namespace pf {
+
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
+
+// acc := acc - sum_{c != row} a_rc x_c over the row's entries in stored order; diag := a_rr.
+// This is the inner loop of one_local_sweep (solvers.cpp:21-51).
+template <bool kReadOnlyX>
+__device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, const double* x,
+                                            double& acc, double& diag) {
+  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
+  const int len = A.row_len[row];
+  int j = 0;
+  for (; j + kUnroll <= len; j += kUnroll) {
+    int32_t c[kUnroll];
+    double v[kUnroll], xv[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const int64_t e = base + static_cast<int64_t>(j + k) * kSlice;
+      c[k] = ld_stream(A.cols + e);
+      v[k] = ld_stream(A.vals + e);
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k)
+      xv[k] = (c[k] == row) ? 0.0 : (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]);
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      if (c[k] == row)
+        diag = v[k];
+      else
+        acc = __dsub_rn(acc, __dmul_rn(v[k], xv[k]));
+    }
+  }
+  for (; j < len; ++j) {
+    const int64_t e = base + static_cast<int64_t>(j) * kSlice;
+    const int32_t c = ld_stream(A.cols + e);
+    const double v = ld_stream(A.vals + e);
+    if (c == row)
+      diag = v;
+    else
+      acc = __dsub_rn(acc, __dmul_rn(v, kReadOnlyX ? __ldg(x + c) : x[c]));
+  }
+}
+
+// acc := acc op sum_c a_rc x_c over all entries in stored order.
+//   kSubtract: acc -= a x   (residual_norm, linalg.cpp:64-73: acc starts at b)
+//   else:      acc += a x   (spmv, linalg.cpp:49-56: acc starts at 0)
+template <bool kSubtract>
+__device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const double* __restrict__ x,
+                                          double acc) {
+  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
+  const int len = A.row_len[row];
+  int j = 0;
+  for (; j + kUnroll <= len; j += kUnroll) {
+    int32_t c[kUnroll];
+    double v[kUnroll], xv[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const int64_t e = base + static_cast<int64_t>(j + k) * kSlice;
+      c[k] = ld_stream(A.cols + e);
+      v[k] = ld_stream(A.vals + e);
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) xv[k] = __ldg(x + c[k]);
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k)
+      acc = kSubtract ? __dsub_rn(acc, __dmul_rn(v[k], xv[k])) : __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
+  }
+  for (; j < len; ++j) {
+    const int64_t e = base + static_cast<int64_t>(j) * kSlice;
+    const double p = __dmul_rn(ld_stream(A.vals + e), __ldg(x + ld_stream(A.cols + e)));
+    acc = kSubtract ? __dsub_rn(acc, p) : __dadd_rn(acc, p);
+  }
+  return acc;
+}
+
+// Damped Jacobi sweep (solvers.cpp:35-51) with ping-pong buffers instead of the
+// reference's full scratch copy: own rows [0, n_own) are relaxed from x_old into
+// x_new; every other row is carried over unchanged (the sweep never writes Slave,
+// Halo or Dirichlet entries, solvers.hpp:16-20).
+__global__ void __launch_bounds__(kBlock) k_jacobi(SellView A, const double* __restrict__ x_old,
+                                                   double* __restrict__ x_new,
+                                                   const double* __restrict__ b, int32_t n_own,
+                                                   int32_t n, double omega) {
+  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  if (row >= n) return;
+  const double xo = x_old[row];
+  if (row >= n_own) {
+    x_new[row] = xo;
+    return;
+  }
+  double acc = b[row], diag = 0.0;
+  row_offdiag<true>(A, row, x_old, acc, diag);
+  x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
+}
+
+// One colour of multicolour Gauss-Seidel / SOR, in place, rows [row0, row1).  Rows of
+// one colour never couple, so the result does not depend on the order in which the
+// threads of this launch run.  kSor=false: x = acc/diag (solvers.cpp:21-34);
+// kSor=true: x = (1-w) x + w acc/diag.
+template <bool kSor>
+__global__ void __launch_bounds__(kBlock) k_color_sweep(SellView A, double* x,
+                                                        const double* __restrict__ b, int32_t row0,
+                                                        int32_t row1, double omega) {
+  const int32_t row = row0 + blockIdx.x * kBlock + threadIdx.x;
+  if (row >= row1) return;
+  double acc = b[row], diag = 0.0;
+  // Other colours are read-only during this launch and this row's own entry is
+  // skipped by row_offdiag, so the read-only path is safe for the gather.
+  row_offdiag<true>(A, row, x, acc, diag);
+  if (kSor)
+    x[row] = __dadd_rn(__dmul_rn(1.0 - omega, x[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
+  else
+    x[row] = __ddiv_rn(acc, diag);
+}
+
+// Residual of the cycle (multigrid.cpp:166-167): y = A x (spmv order, acc from 0), r = b - y,
+// on rows [0, n).
+__global__ void __launch_bounds__(kBlock) k_residual(SellView A, const double* __restrict__ x,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ r, int32_t n) {
+  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  if (row >= n) return;
+  r[row] = __dsub_rn(b[row], row_dot<false>(A, row, x, 0.0));
+}
+
+// y = A x on every row (linalg.cpp:45-57).
+__global__ void __launch_bounds__(kBlock) k_spmv(SellView A, const double* __restrict__ x,
+                                                 double* __restrict__ y, int32_t n) {
+  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  if (row >= n) return;
+  y[row] = row_dot<false>(A, row, x, 0.0);
+}
+
+// Deterministic block sum: fixed shuffle tree inside each warp, then warp 0 sums the
+// per-warp values in warp order.  No floating-point atomics anywhere.
+__device__ __forceinline__ double block_sum(double v, double* smem /* kBlock/32 */) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (warp == 0) {
+    s = lane < (kBlock / 32) ? smem[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+  }
+  return s;  // valid in thread 0
+}
+
+// sum_{r < n_own} (b_r - A_r x)^2 (residual_norm's local part, linalg.cpp:64-73).  Every
+// block writes its partial; the last block to finish (ticket counter, integer atomic
+// only) sums the partials in index order, stores the rank sum in *sumsq and, when
+// `norm_out` is set (single-subdomain case: the ascending-rank allreduce of one value
+// is 0.0 + s, transport.cpp:139-149), sqrt of it.  The ticket is reset for the next use.
+__global__ void __launch_bounds__(kBlock) k_resnorm(SellView A, const double* __restrict__ x,
+                                                    const double* __restrict__ b, int32_t n_own,
+                                                    double* __restrict__ partials,
+                                                    unsigned int* ticket, double* sumsq,
+                                                    double* norm_out) {
+  __shared__ double smem[kBlock / 32];
+  __shared__ bool last;
+  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  double sq = 0.0;
+  if (row < n_own) {
+    const double acc = row_dot<true>(A, row, x, b[row]);
+    sq = __dmul_rn(acc, acc);
+  }
+  const double s = block_sum(sq, smem);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (unsigned int i = threadIdx.x; i < gridDim.x; i += kBlock) t = __dadd_rn(t, partials[i]);
+  __syncthreads();
+  t = block_sum(t, smem);
+  if (threadIdx.x == 0) {
+    *sumsq = t;
+    if (norm_out) *norm_out = sqrt(__dadd_rn(0.0, t));
+    *ticket = 0u;
+  }
+}
+
+// Ordered allreduce of per-subdomain sums: out = sqrt(((0 + s_0) + s_1) + ...)
+// (ascending rank, transport.cpp:139-149), optionally without the sqrt.
+__global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* out, int take_sqrt) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s = __dadd_rn(s, parts[i]);
+  *out = take_sqrt ? sqrt(s) : s;
+}
+
+// x_f += P x_c over every local fine dof (multigrid.cpp:121-129 + :183-184): the
+// correction is accumulated from 0 in P's entry order, then added.
+__global__ void __launch_bounds__(kBlock) k_prolong_add(const int64_t* __restrict__ p_off,
+                                                        const int32_t* __restrict__ p_col,
+                                                        const double* __restrict__ p_w,
+                                                        const double* __restrict__ xc,
+                                                        double* __restrict__ xf, int32_t n_f,
+                                                        int add) {
+  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  if (row >= n_f) return;
+  double acc = 0.0;
+  for (int64_t e = p_off[row], e1 = p_off[row + 1]; e < e1; ++e)
+    acc = __dadd_rn(acc, __dmul_rn(ld_stream(p_w + e), __ldg(xc + ld_stream(p_col + e))));
+  xf[row] = add ? __dadd_rn(xf[row], acc) : acc;
+}
+
+// rc = R r_f with R = P^T restricted to owns_row fine rows (multigrid.cpp:131-146), as a
+// gather: each coarse row sums its fine contributions in ascending fine host index,
+// i.e. exactly the order of the reference's scatter-add.  Fused epilogue of the cycle
+// (multigrid.cpp:172-179): Dirichlet coarse entries of b become 0 and the coarse x is
+// zeroed.  (Zeroing before the master/slave accumulate is equivalent: Dirichlet
+// carriers are Dirichlet on every rank, so they only ever accumulate zeros.)
+__global__ void __launch_bounds__(kBlock) k_restrict(const int64_t* __restrict__ r_off,
+                                                     const int32_t* __restrict__ r_col,
+                                                     const double* __restrict__ r_w,
+                                                     const double* __restrict__ rf,
+                                                     double* __restrict__ bc,
+                                                     double* __restrict__ xc,
+                                                     const uint8_t* __restrict__ is_dir_c,
+                                                     int32_t n_c, int zero_dirichlet) {
+  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  if (row >= n_c) return;
+  double acc = 0.0;
+  for (int64_t e = r_off[row], e1 = r_off[row + 1]; e < e1; ++e)
+    acc = __dadd_rn(acc, __dmul_rn(ld_stream(r_w + e), __ldg(rf + ld_stream(r_col + e))));
+  bc[row] = (zero_dirichlet && is_dir_c[row]) ? 0.0 : acc;
+  if (xc) xc[row] = 0.0;
+}
+
+// Sequential coarse solve (solvers.cpp:70-92) of every subdomain held on this device:
+// per iteration, in-place Gauss-Seidel over each subdomain's own rows in the
+// reference's host order (host_of_own[i] = device row of host own dof i), then the
+// communicating part of smooth() — update_master_slave(Scatter) and update_halo1
+// (solvers.cpp:65-66) as level-global index copies — then residual_norm with the
+// ascending-rank sum; stop at <= tol * r0 or max_iter.  One thread: the coarse level of
+// the n_coarse=2 hierarchies holds one unknown, and a sequential sweep is the only way
+// to keep the reference's exact ordering.  stats: [iterations, converged, r0, final].
+__global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, double* x,
+                            const double* __restrict__ b, const int32_t* __restrict__ ms_dst,
+                            const int32_t* __restrict__ ms_src, int32_t ms_n,
+                            const int32_t* __restrict__ h1_dst, const int32_t* __restrict__ h1_src,
+                            int32_t h1_n, double tol, int32_t max_iter, double* stats) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  auto norm = [&]() {
+    double total = 0.0;
+    for (int s = 0; s < n_sub; ++s) {
+      const CoarseSub& S = subs[s];
+      const double* xs = x + S.offset;
+      const double* bs = b + S.offset;
+      double local = 0.0;
+      for (int32_t i = 0; i < S.n_own; ++i) {
+        const int32_t d = S.host_of_own[i];
+        const int64_t base = S.A.slice_ptr[d >> 5] + (d & 31);
+        double acc = bs[d];
+        for (int j = 0; j < S.A.row_len[d]; ++j) {
+          const int64_t e = base + static_cast<int64_t>(j) * kSlice;
+          acc = __dsub_rn(acc, __dmul_rn(S.A.vals[e], xs[S.A.cols[e]]));
+        }
+        local = __dadd_rn(local, __dmul_rn(acc, acc));
+      }
+      total = __dadd_rn(total, local);
+    }
+    return sqrt(total);
+  };
+  const double r0 = norm();
+  stats[0] = 0;
+  stats[1] = 1;
+  stats[2] = r0;
+  stats[3] = r0;
+  if (r0 == 0.0) return;
+  const double target = __dmul_rn(tol, r0);
+  int it = 0;
+  while (it < max_iter) {
+    for (int s = 0; s < n_sub; ++s) {
+      const CoarseSub& S = subs[s];
+      double* xs = x + S.offset;
+      const double* bs = b + S.offset;
+      for (int32_t i = 0; i < S.n_own; ++i) {
+        const int32_t d = S.host_of_own[i];
+        const int64_t base = S.A.slice_ptr[d >> 5] + (d & 31);
+        double acc = bs[d], diag = 0.0;
+        for (int j = 0; j < S.A.row_len[d]; ++j) {
+          const int64_t e = base + static_cast<int64_t>(j) * kSlice;
+          const int32_t c = S.A.cols[e];
+          if (c == d)
+            diag = S.A.vals[e];
+          else
+            acc = __dsub_rn(acc, __dmul_rn(S.A.vals[e], xs[c]));
+        }
+        xs[d] = __ddiv_rn(acc, diag);
+      }
+    }
+    for (int32_t i = 0; i < ms_n; ++i) x[ms_dst[i]] = x[ms_src[i]];
+    for (int32_t i = 0; i < h1_n; ++i) x[h1_dst[i]] = x[h1_src[i]];
+    ++it;
+    const double fr = norm();
+    stats[0] = it;
+    stats[3] = fr;
+    if (fr <= target) return;
+  }
+  stats[1] = 0;
+}
+
+// ------------------------------------------------------------- vector utilities --
+
+// Host order -> device order: dev[perm[i]] = host[i].
+__global__ void k_scatter_perm(const double* __restrict__ host, const int32_t* __restrict__ perm,
+                               double* __restrict__ dev, int32_t n) {
+  const int32_t i = blockIdx.x * kBlock + threadIdx.x;
+  if (i < n) dev[perm[i]] = host[i];
+}
+// Device order -> host order: host[i] = dev[perm[i]].
+__global__ void k_gather_perm(const double* __restrict__ dev, const int32_t* __restrict__ perm,
+                              double* __restrict__ host, int32_t n) {
+  const int32_t i = blockIdx.x * kBlock + threadIdx.x;
+  if (i < n) host[i] = dev[perm[i]];
+}
+__global__ void k_fill(double* __restrict__ v, double value, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+  if (i < n) v[i] = value;
+}
+__global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
+
+// ------------------------------------------------------------- exchange kernels --
+// A channel plan flattens every (peer, entry) of one exchange of one subdomain.
+
+// Local transport of one scatter: v[dst[i]] = v[src[i]] (pack + send + recv + unpack of
+// fecomm.cpp:25-39 when every peer lives on this device).
+__global__ void k_copy_idx(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                           double* v, int32_t n) {
+  const int32_t i = blockIdx.x * kBlock + threadIdx.x;
+  if (i < n) v[dst[i]] = v[src[i]];
+}
+// Pack: buf[i] = v[idx[i]] (send side of scatter, fecomm.cpp:28-32).
+__global__ void k_pack(const double* __restrict__ v, const int32_t* __restrict__ idx,
+                       double* __restrict__ buf, int32_t n) {
+  const int32_t i = blockIdx.x * kBlock + threadIdx.x;
+  if (i < n) buf[i] = v[idx[i]];
+}
+// Unpack: v[idx[i]] = buf[i] (receive side of scatter, fecomm.cpp:33-38).
+__global__ void k_unpack(const double* __restrict__ buf, const int32_t* __restrict__ idx,
+                         double* __restrict__ v, int32_t n) {
+  const int32_t i = blockIdx.x * kBlock + threadIdx.x;
+  if (i < n) v[idx[i]] = buf[i];
+}
+// Accumulate (fecomm.cpp:43-59): master entry m receives its slave partials in ascending
+// peer order: v[dst[m]] = ((v + p_a) + p_b) + ...  with the partials' buffer positions
+// listed per master in src[acc_off[m] .. acc_off[m+1]).
+__global__ void k_unpack_accumulate(const double* __restrict__ buf,
+                                    const int32_t* __restrict__ acc_off,
+                                    const int32_t* __restrict__ src,
+                                    const int32_t* __restrict__ dst, double* __restrict__ v,
+                                    int32_t n_masters) {
+  const int32_t m = blockIdx.x * kBlock + threadIdx.x;
+  if (m >= n_masters) return;
+  double acc = v[dst[m]];
+  for (int32_t e = acc_off[m]; e < acc_off[m + 1]; ++e) acc = __dadd_rn(acc, buf[src[e]]);
+  v[dst[m]] = acc;
+}
+
+}  // namespace pf

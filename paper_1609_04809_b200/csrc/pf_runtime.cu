@@ -1,0 +1,1287 @@
+// pf_runtime.cu — host runtime and C-ABI of the B200 GMG V-cycle hot path.
+//
+// Maps the reference's hot-path API onto sm_100a kernels:
+//   spmv / residual_norm            linalg.cpp:45-74     -> k_spmv / k_resnorm
+//   smooth (Jacobi, GS)             solvers.cpp:17-68    -> k_jacobi / k_color_sweep
+//   coarse_solve                    solvers.cpp:70-92    -> k_coarse_gs
+//   prolongate / restrict_residual  multigrid.cpp:121-146 -> k_prolong_add / k_restrict
+//   v_cycle / solve_outer           multigrid.cpp:150-246 -> one CUDA graph per outer cycle
+//   ParFECommunicator updates       fecomm.cpp:25-72     -> exchange plans (device copies
+//                                                           or NCCL send/recv)
+//   allreduce_sum                   transport.cpp:139-165 -> ordered device sum
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "pf_kernels.cuh"
+#include "pf_nccl.hpp"
+#include "pf_runtime.hpp"
+
+using namespace pf;
+
+namespace pf {
+
+thread_local std::string g_last_error;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(PF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+double wall_now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+inline unsigned grid_for(int64_t n) { return static_cast<unsigned>((n + kBlock - 1) / kBlock); }
+
+[[noreturn]] void invalid(const std::string& m) { throw Error(PF_ERR_INVALID_ARGUMENT, m); }
+[[noreturn]] void state(const std::string& m) { throw Error(PF_ERR_STATE, m); }
+
+struct Launcher {
+  pf_hierarchy* h;
+  int64_t* counter;
+  template <typename Kern, typename... Args>
+  void operator()(unsigned grid, unsigned block, Kern kern, Args... args) {
+    if (grid == 0) return;
+    kern<<<grid, block, 0, h->stream>>>(args...);
+    PF_CUDA(cudaGetLastError());
+    ++*counter;
+  }
+};
+
+// While a graph is being captured, kernel launches are counted into the graph entry.
+int64_t* g_capture_counter = nullptr;
+
+Launcher launcher(pf_hierarchy* h) { return Launcher{h, g_capture_counter ? g_capture_counter : &h->launches}; }
+
+SellView view(const DevSell& s) { return SellView{s.vals.p, s.cols.p, s.slice_ptr.p, s.row_len.p}; }
+
+void check_level(const pf_hierarchy* h, int level) {
+  if (!h) invalid("null hierarchy");
+  if (!h->finalized) state("hierarchy not finalized");
+  if (level < 0 || level >= h->n_levels) invalid("level " + std::to_string(level) + " out of range");
+}
+
+void check_vec(const pf_hierarchy* h, const pf_vector* v, int level, const char* what) {
+  if (!v) invalid(std::string(what) + ": null vector");
+  if (v->h != h) invalid(std::string(what) + ": vector belongs to another hierarchy");
+  if (v->level != level)
+    invalid(std::string("vector length does not match mapper dof count (") + what + ": level " +
+            std::to_string(v->level) + " vs " + std::to_string(level) + ")");
+}
+
+// ------------------------------------------------------------------ upload --
+
+// Device layout of one subdomain level: own rows colour-major (stable in host order),
+// then every other row in host order; SELL-32 operator; P (rows of this level).
+void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
+  const int32_t n = H.n, n_own = H.n_own;
+  D.n = n;
+  D.n_own = n_own;
+  // --- diagonal check (check_diagonal, solvers.cpp:10-15) and column sanity
+  for (int32_t r = 0; r < n; ++r) {
+    if (H.rowptr[r + 1] < H.rowptr[r]) invalid("row offsets must be non-decreasing");
+  }
+  for (int64_t k = 0; k < H.rowptr[n]; ++k)
+    if (H.cols[k] < 0 || H.cols[k] >= n) invalid("column index out of range");
+  for (int32_t r = 0; r < n_own; ++r) {
+    double diag = 0.0;
+    for (int64_t k = H.rowptr[r]; k < H.rowptr[r + 1]; ++k)
+      if (H.cols[k] == r) diag = H.vals[k];
+    if (diag == 0.0)
+      throw Error(PF_ERR_SINGULAR_DIAGONAL, "zero diagonal at own dof " + std::to_string(r) +
+                                                " (level " + std::to_string(level) + ")");
+  }
+  // --- colours of own rows
+  std::vector<int32_t> color(static_cast<size_t>(n_own), 0);
+  if (!H.color.empty()) {
+    for (int32_t i = 0; i < n_own; ++i) {
+      if (H.color[i] < 0) invalid("negative colour");
+      color[i] = H.color[i];
+    }
+    // a colour class must be an independent set of the own-row graph
+    for (int32_t i = 0; i < n_own; ++i)
+      for (int64_t k = H.rowptr[i]; k < H.rowptr[i + 1]; ++k) {
+        const int32_t c = H.cols[k];
+        if (c != i && c < n_own && color[c] == color[i] && H.vals[k] != 0.0)
+          invalid("colouring couples rows " + std::to_string(i) + " and " + std::to_string(c));
+      }
+  } else {
+    std::vector<int32_t> seen;
+    for (int32_t i = 0; i < n_own; ++i) {
+      seen.clear();
+      for (int64_t k = H.rowptr[i]; k < H.rowptr[i + 1]; ++k) {
+        const int32_t c = H.cols[k];
+        if (c < i) seen.push_back(color[c]);
+      }
+      std::sort(seen.begin(), seen.end());
+      int32_t pick = 0;
+      for (int32_t s : seen) {
+        if (s == pick) ++pick;
+        else if (s > pick) break;
+      }
+      color[i] = pick;
+    }
+  }
+  int32_t n_colors = 0;
+  for (int32_t c : color) n_colors = std::max(n_colors, c + 1);
+  D.n_colors = n_colors;
+  D.color_start.assign(static_cast<size_t>(n_colors) + 1, 0);
+  for (int32_t c : color) ++D.color_start[c + 1];
+  for (int32_t c = 0; c < n_colors; ++c) D.color_start[c + 1] += D.color_start[c];
+  // --- permutation host -> device
+  D.perm.assign(static_cast<size_t>(n), 0);
+  std::vector<int32_t> inv(static_cast<size_t>(n), 0);
+  {
+    std::vector<int32_t> next(D.color_start.begin(), D.color_start.end() - 1);
+    for (int32_t i = 0; i < n_own; ++i) D.perm[i] = next[color[i]]++;
+    for (int32_t i = n_own; i < n; ++i) D.perm[i] = i;
+    for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
+  }
+  D.d_perm.upload(D.perm);
+  // --- SELL-32
+  const int64_t n_slices = (n + kSlice - 1) / kSlice;
+  std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
+  std::vector<int32_t> rlen(static_cast<size_t>(n_slices * kSlice), 0);
+  for (int32_t d = 0; d < n; ++d) {
+    const int32_t hr = inv[d];
+    rlen[d] = static_cast<int32_t>(H.rowptr[hr + 1] - H.rowptr[hr]);
+  }
+  for (int64_t s = 0; s < n_slices; ++s) {
+    int32_t w = 0;
+    for (int l = 0; l < kSlice; ++l) w = std::max(w, rlen[s * kSlice + l]);
+    sptr[s + 1] = sptr[s] + static_cast<int64_t>(w) * kSlice;
+  }
+  std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
+  std::vector<int32_t> sc(static_cast<size_t>(sptr[n_slices]), 0);
+  for (int64_t s = 0; s < n_slices; ++s) {
+    const int64_t w = (sptr[s + 1] - sptr[s]) / kSlice;
+    for (int l = 0; l < kSlice; ++l) {
+      const int64_t d = s * kSlice + l;
+      const int32_t len = d < n ? rlen[d] : 0;
+      const int32_t hr = d < n ? inv[d] : 0;
+      for (int64_t j = 0; j < w; ++j) {
+        const int64_t e = sptr[s] + j * kSlice + l;
+        if (j < len) {
+          const int64_t k = H.rowptr[hr] + j;
+          sc[e] = D.perm[H.cols[k]];
+          sv[e] = H.vals[k];
+        } else {
+          sc[e] = static_cast<int32_t>(std::min<int64_t>(d, n > 0 ? n - 1 : 0));
+          sv[e] = 0.0;
+        }
+      }
+    }
+  }
+  D.A.slice_ptr.upload(sptr);
+  D.A.row_len.upload(rlen);
+  D.A.vals.upload(sv);
+  D.A.cols.upload(sc);
+  D.A.nnz = H.rowptr[n];
+  D.A.own_nnz = H.rowptr[n_own];
+  D.A.stored = sptr[n_slices];
+  {
+    std::vector<uint8_t> touched(static_cast<size_t>(n), 0);
+    for (int64_t k = 0; k < H.rowptr[n_own]; ++k) touched[H.cols[k]] = 1;
+    D.own_cols_touched = std::count(touched.begin(), touched.end(), 1);
+  }
+  // --- Dirichlet mask in device order
+  std::vector<uint8_t> isdir(static_cast<size_t>(n), 0);
+  for (int32_t i = 0; i < n; ++i) isdir[D.perm[i]] = H.is_dir.empty() ? 0 : H.is_dir[i];
+  D.d_is_dir.upload(isdir);
+  // --- residual-norm scratch
+  D.resnorm_blocks = std::max<int>(1, static_cast<int>(grid_for(n_own)));
+  D.partials.alloc(D.resnorm_blocks);
+  D.ticket.alloc(1);
+  PF_CUDA(cudaMemset(D.ticket.p, 0, sizeof(unsigned int)));
+}
+
+// P rows of the fine level in device order; R = P^T over owns_row fine rows as a
+// parent-row gather with entries in ascending fine host index.
+void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const DevLevel& DC) {
+  const int32_t nf = F.n, nc = Cc.n;
+  if (F.p_off.size() != static_cast<size_t>(nf) + 1) invalid("prolongation needs n_dofs + 1 offsets");
+  for (int64_t e = 0; e < F.p_off[nf]; ++e)
+    if (F.p_col[e] < 0 || F.p_col[e] >= nc) invalid("prolongation column out of the parent level");
+  std::vector<int32_t> inv_f(static_cast<size_t>(nf));
+  for (int32_t i = 0; i < nf; ++i) inv_f[DF.perm[i]] = i;
+  std::vector<int64_t> poff(static_cast<size_t>(nf) + 1, 0);
+  std::vector<int32_t> pcol;
+  std::vector<double> pw;
+  pcol.reserve(static_cast<size_t>(F.p_off[nf]));
+  pw.reserve(static_cast<size_t>(F.p_off[nf]));
+  for (int32_t d = 0; d < nf; ++d) {
+    const int32_t hr = inv_f[d];
+    for (int64_t e = F.p_off[hr]; e < F.p_off[hr + 1]; ++e) {
+      pcol.push_back(DC.perm[F.p_col[e]]);
+      pw.push_back(F.p_w[e]);
+    }
+    poff[d + 1] = static_cast<int64_t>(pcol.size());
+  }
+  DF.p_off.upload(poff);
+  DF.p_col.upload(pcol);
+  DF.p_w.upload(pw);
+  DF.p_nnz = static_cast<int64_t>(pcol.size());
+  // R by counting sort over parent host rows; iterating fine host rows ascending keeps
+  // each parent row's contributions in the reference's scatter-add order.
+  std::vector<int64_t> cnt(static_cast<size_t>(nc) + 1, 0);
+  for (int32_t f = 0; f < nf; ++f)
+    if (F.owns_row[f])
+      for (int64_t e = F.p_off[f]; e < F.p_off[f + 1]; ++e) ++cnt[F.p_col[e] + 1];
+  std::vector<int64_t> start(static_cast<size_t>(nc) + 1, 0);
+  for (int32_t c = 0; c < nc; ++c) start[c + 1] = start[c] + cnt[c + 1];
+  std::vector<int32_t> rf(static_cast<size_t>(start[nc]));
+  std::vector<double> rw(static_cast<size_t>(start[nc]));
+  {
+    std::vector<int64_t> pos(start.begin(), start.end() - 1);
+    for (int32_t f = 0; f < nf; ++f)
+      if (F.owns_row[f])
+        for (int64_t e = F.p_off[f]; e < F.p_off[f + 1]; ++e) {
+          const int64_t q = pos[F.p_col[e]]++;
+          rf[q] = DF.perm[f];
+          rw[q] = F.p_w[e];
+        }
+  }
+  // reorder parent rows into device order
+  std::vector<int32_t> inv_c(static_cast<size_t>(nc));
+  for (int32_t i = 0; i < nc; ++i) inv_c[DC.perm[i]] = i;
+  std::vector<int64_t> roff(static_cast<size_t>(nc) + 1, 0);
+  std::vector<int32_t> rcol;
+  std::vector<double> rwt;
+  rcol.reserve(rf.size());
+  rwt.reserve(rf.size());
+  for (int32_t d = 0; d < nc; ++d) {
+    const int32_t hc = inv_c[d];
+    for (int64_t q = start[hc]; q < start[hc + 1]; ++q) {
+      rcol.push_back(rf[q]);
+      rwt.push_back(rw[q]);
+    }
+    roff[d + 1] = static_cast<int64_t>(rcol.size());
+  }
+  DF.r_off.upload(roff);
+  DF.r_col.upload(rcol);
+  DF.r_w.upload(rwt);
+  DF.r_nnz = static_cast<int64_t>(rcol.size());
+}
+
+const HostChannel* find_channel(const HostLevel& H, int kind, int peer) {
+  for (const HostChannel& c : H.channels)
+    if (c.kind == kind && c.peer == peer) return &c;
+  return nullptr;
+}
+
+void build_plans(pf_hierarchy* h, int l) {
+  Level& L = h->levels[l];
+  const bool local = h->world == h->n_sub;
+  for (int kind = 0; kind < PF_NUM_CHANNEL_KINDS; ++kind) {
+    ExchangePlan& P = L.scatter[kind];
+    if (local) {
+      std::vector<int32_t> dst, src;
+      for (int s = 0; s < h->n_sub; ++s) {
+        const int R = h->rank_base + s;
+        for (const HostChannel& c : L.host[s].channels) {
+          if (c.kind != kind || c.recv.empty()) continue;
+          const int p = c.peer - h->rank_base;
+          if (p < 0 || p >= h->n_sub || p == s) invalid("channel peer " + std::to_string(c.peer) + " out of range");
+          const HostChannel* pc = find_channel(L.host[p], kind, R);
+          if (!pc || pc->send.size() != c.recv.size())
+            throw Error(PF_ERR_TRANSPORT, "channel lists of kind " + std::to_string(kind) +
+                                              " between ranks " + std::to_string(c.peer) + " and " +
+                                              std::to_string(R) + " do not pair up");
+          for (size_t i = 0; i < c.recv.size(); ++i) {
+            dst.push_back(static_cast<int32_t>(L.sub[s].offset + L.sub[s].perm[c.recv[i]]));
+            src.push_back(static_cast<int32_t>(L.sub[p].offset + L.sub[p].perm[pc->send[i]]));
+          }
+        }
+      }
+      P.n = static_cast<int64_t>(dst.size());
+      P.dst.upload(dst);
+      P.src.upload(src);
+    } else {
+      const DevLevel& D = L.sub[0];
+      std::vector<int32_t> pk, up;
+      for (const HostChannel& c : L.host[0].channels) {
+        if (c.kind != kind) continue;
+        if (!c.send.empty()) {
+          P.send_segs.push_back({c.peer, static_cast<int64_t>(pk.size()), static_cast<int64_t>(c.send.size())});
+          for (int32_t d : c.send) pk.push_back(D.perm[d]);
+        }
+        if (!c.recv.empty()) {
+          P.recv_segs.push_back({c.peer, static_cast<int64_t>(up.size()), static_cast<int64_t>(c.recv.size())});
+          for (int32_t d : c.recv) up.push_back(D.perm[d]);
+        }
+      }
+      P.n = static_cast<int64_t>(up.size());
+      P.pack_idx.upload(pk);
+      P.unpack_idx.upload(up);
+      P.sendbuf.alloc(static_cast<int64_t>(pk.size()));
+      P.recvbuf.alloc(static_cast<int64_t>(up.size()));
+    }
+  }
+  // master/slave accumulate: slaves push v[recv_dofs], masters add in ascending peer order
+  ExchangePlan& A = L.accumulate;
+  std::map<int32_t, std::vector<int32_t>> contrib;  // master dst -> sources, peer-ascending
+  if (local) {
+    for (int s = 0; s < h->n_sub; ++s) {
+      const int R = h->rank_base + s;
+      std::vector<const HostChannel*> ms;
+      for (const HostChannel& c : L.host[s].channels)
+        if (c.kind == PF_CH_MASTER_SLAVE && !c.send.empty()) ms.push_back(&c);
+      std::sort(ms.begin(), ms.end(), [](const HostChannel* a, const HostChannel* b) { return a->peer < b->peer; });
+      for (const HostChannel* c : ms) {
+        const int p = c->peer - h->rank_base;
+        const HostChannel* pc = find_channel(L.host[p], PF_CH_MASTER_SLAVE, R);
+        if (!pc || pc->recv.size() != c->send.size())
+          throw Error(PF_ERR_TRANSPORT, "master/slave lists do not pair up");
+        for (size_t i = 0; i < c->send.size(); ++i)
+          contrib[static_cast<int32_t>(L.sub[s].offset + L.sub[s].perm[c->send[i]])].push_back(
+              static_cast<int32_t>(L.sub[p].offset + L.sub[p].perm[pc->recv[i]]));
+      }
+    }
+  } else {
+    const DevLevel& D = L.sub[0];
+    std::vector<const HostChannel*> ms;
+    for (const HostChannel& c : L.host[0].channels)
+      if (c.kind == PF_CH_MASTER_SLAVE) ms.push_back(&c);
+    std::sort(ms.begin(), ms.end(), [](const HostChannel* a, const HostChannel* b) { return a->peer < b->peer; });
+    std::vector<int32_t> pk;
+    int64_t rpos = 0;
+    for (const HostChannel* c : ms) {
+      if (!c->recv.empty()) {  // slave side: push partial sums to the master
+        A.send_segs.push_back({c->peer, static_cast<int64_t>(pk.size()), static_cast<int64_t>(c->recv.size())});
+        for (int32_t d : c->recv) pk.push_back(D.perm[d]);
+      }
+      if (!c->send.empty()) {  // master side
+        A.recv_segs.push_back({c->peer, rpos, static_cast<int64_t>(c->send.size())});
+        for (size_t i = 0; i < c->send.size(); ++i)
+          contrib[D.perm[c->send[i]]].push_back(static_cast<int32_t>(rpos + static_cast<int64_t>(i)));
+        rpos += static_cast<int64_t>(c->send.size());
+      }
+    }
+    A.pack_idx.upload(pk);
+    A.sendbuf.alloc(static_cast<int64_t>(pk.size()));
+    A.recvbuf.alloc(rpos);
+  }
+  std::vector<int32_t> off{0}, srcs, dsts;
+  for (const auto& [d, list] : contrib) {
+    dsts.push_back(d);
+    srcs.insert(srcs.end(), list.begin(), list.end());
+    off.push_back(static_cast<int32_t>(srcs.size()));
+  }
+  A.n_masters = static_cast<int32_t>(dsts.size());
+  A.n = static_cast<int64_t>(srcs.size());
+  A.acc_off.upload(off);
+  A.acc_src.upload(srcs);
+  A.acc_dst.upload(dsts);
+}
+
+// ------------------------------------------------------------------ enqueue --
+
+void enq_scatter(pf_hierarchy* h, int l, int kind, double* v) {
+  ExchangePlan& P = h->levels[l].scatter[kind];
+  auto launch = launcher(h);
+  if (h->world == h->n_sub) {
+    if (P.n == 0) return;
+    // pack, transport and unpack in one device copy: sends and receives of one
+    // channel kind touch disjoint entries (masters/owners vs slaves/halos)
+    launch(grid_for(P.n), kBlock, k_copy_idx, static_cast<const int32_t*>(P.src.p),
+           static_cast<const int32_t*>(P.dst.p), v, static_cast<int32_t>(P.n));
+    return;
+  }
+  if (P.send_segs.empty() && P.recv_segs.empty()) return;
+  launch(grid_for(P.pack_idx.n), kBlock, k_pack, static_cast<const double*>(v),
+         static_cast<const int32_t*>(P.pack_idx.p), P.sendbuf.p, static_cast<int32_t>(P.pack_idx.n));
+  h->nccl->group_start();
+  for (const PeerSeg& s : P.send_segs) h->nccl->send(P.sendbuf.p + s.off, s.len, s.peer, h->stream);
+  for (const PeerSeg& s : P.recv_segs) h->nccl->recv(P.recvbuf.p + s.off, s.len, s.peer, h->stream);
+  h->nccl->group_end();
+  launch(grid_for(P.unpack_idx.n), kBlock, k_unpack, static_cast<const double*>(P.recvbuf.p),
+         static_cast<const int32_t*>(P.unpack_idx.p), v, static_cast<int32_t>(P.unpack_idx.n));
+}
+
+void enq_accumulate(pf_hierarchy* h, int l, double* v) {
+  ExchangePlan& A = h->levels[l].accumulate;
+  auto launch = launcher(h);
+  if (h->world == h->n_sub) {
+    if (A.n_masters == 0) return;
+    launch(grid_for(A.n_masters), kBlock, k_unpack_accumulate, static_cast<const double*>(v),
+           static_cast<const int32_t*>(A.acc_off.p), static_cast<const int32_t*>(A.acc_src.p),
+           static_cast<const int32_t*>(A.acc_dst.p), v, A.n_masters);
+    return;
+  }
+  if (A.send_segs.empty() && A.recv_segs.empty()) return;
+  launch(grid_for(A.pack_idx.n), kBlock, k_pack, static_cast<const double*>(v),
+         static_cast<const int32_t*>(A.pack_idx.p), A.sendbuf.p, static_cast<int32_t>(A.pack_idx.n));
+  h->nccl->group_start();
+  for (const PeerSeg& s : A.send_segs) h->nccl->send(A.sendbuf.p + s.off, s.len, s.peer, h->stream);
+  for (const PeerSeg& s : A.recv_segs) h->nccl->recv(A.recvbuf.p + s.off, s.len, s.peer, h->stream);
+  h->nccl->group_end();
+  launch(grid_for(A.n_masters), kBlock, k_unpack_accumulate, static_cast<const double*>(A.recvbuf.p),
+         static_cast<const int32_t*>(A.acc_off.p), static_cast<const int32_t*>(A.acc_src.p),
+         static_cast<const int32_t*>(A.acc_dst.p), v, A.n_masters);
+}
+
+void enq_update_ms(pf_hierarchy* h, int l, double* v, int mode) {
+  if (mode == PF_UPDATE_ACCUMULATE_THEN_SCATTER) enq_accumulate(h, l, v);
+  enq_scatter(h, l, PF_CH_MASTER_SLAVE, v);
+}
+
+// ascending-rank allreduce of the per-subdomain sums in L.sumsq into L.norm
+void enq_allreduce(pf_hierarchy* h, Level& L, bool take_sqrt) {
+  auto launch = launcher(h);
+  if (h->world == h->n_sub) {
+    launch(1, 32, k_ordered_sum, static_cast<const double*>(L.sumsq.p), h->n_sub, L.norm.p,
+           take_sqrt ? 1 : 0);
+  } else {
+    h->nccl->allgather(L.sumsq.p, L.sumsq.p + 1, 1, h->stream);
+    launch(1, 32, k_ordered_sum, static_cast<const double*>(L.sumsq.p + 1), h->world, L.norm.p,
+           take_sqrt ? 1 : 0);
+  }
+}
+
+void enq_resnorm(pf_hierarchy* h, int l, const double* x, const double* b) {
+  Level& L = h->levels[l];
+  auto launch = launcher(h);
+  const bool single = h->world == 1;
+  for (int s = 0; s < h->n_sub; ++s) {
+    DevLevel& D = L.sub[s];
+    launch(static_cast<unsigned>(D.resnorm_blocks), kBlock, k_resnorm, view(D.A), x + D.offset,
+           b + D.offset, D.n_own, D.partials.p, D.ticket.p, L.sumsq.p + s, single ? L.norm.p : nullptr);
+  }
+  if (!single) enq_allreduce(h, L, true);
+}
+
+void enq_residual(pf_hierarchy* h, int l, const double* x, const double* b, double* r) {
+  Level& L = h->levels[l];
+  auto launch = launcher(h);
+  for (DevLevel& D : L.sub)
+    launch(grid_for(D.n), kBlock, k_residual, view(D.A), x + D.offset, b + D.offset, r + D.offset, D.n);
+}
+
+void enq_spmv(pf_hierarchy* h, int l, const double* x, double* y) {
+  Level& L = h->levels[l];
+  auto launch = launcher(h);
+  for (DevLevel& D : L.sub)
+    launch(grid_for(D.n), kBlock, k_spmv, view(D.A), x + D.offset, y + D.offset, D.n);
+}
+
+void enq_copy(pf_hierarchy* h, const double* src, double* dst, int64_t n) {
+  launcher(h)(grid_for(n), kBlock, k_copy, src, dst, n);
+}
+
+// smooth (solvers.cpp:56-68) on x (primary buffer) with b.
+void enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_smoother_config& sc) {
+  Level& L = h->levels[l];
+  auto launch = launcher(h);
+  double* bufs[2] = {xv->cur(), xv->alt()};
+  int cur = 0;
+  for (int sweep = 0; sweep < sc.sweeps; ++sweep) {
+    for (int local = 0; local < sc.local_sweeps; ++local) {
+      if (sc.kind == PF_SMOOTHER_JACOBI) {
+        for (DevLevel& D : L.sub)
+          launch(grid_for(D.n), kBlock, k_jacobi, view(D.A), static_cast<const double*>(bufs[cur] + D.offset),
+                 bufs[cur ^ 1] + D.offset, b + D.offset, D.n_own, D.n, sc.damping);
+        cur ^= 1;
+      } else {
+        const bool sor = sc.kind == PF_SMOOTHER_MULTICOLOR_SOR;
+        int max_colors = 0;
+        for (DevLevel& D : L.sub) max_colors = std::max(max_colors, D.n_colors);
+        for (int c = 0; c < max_colors; ++c)
+          for (DevLevel& D : L.sub) {
+            if (c >= D.n_colors) continue;
+            const int32_t r0 = D.color_start[c], r1 = D.color_start[c + 1];
+            if (sor)
+              launch(grid_for(r1 - r0), kBlock, k_color_sweep<true>, view(D.A), bufs[cur] + D.offset,
+                     b + D.offset, r0, r1, sc.damping);
+            else
+              launch(grid_for(r1 - r0), kBlock, k_color_sweep<false>, view(D.A), bufs[cur] + D.offset,
+                     b + D.offset, r0, r1, 1.0);
+          }
+      }
+    }
+    enq_update_ms(h, l, bufs[cur], PF_UPDATE_SCATTER);
+    enq_scatter(h, l, PF_CH_HALO1, bufs[cur]);
+  }
+  if (cur) enq_copy(h, bufs[1], bufs[0], L.total);
+}
+
+void enq_prolong(pf_hierarchy* h, int fine, const double* xc, double* xf, int add) {
+  Level& F = h->levels[fine];
+  Level& Cl = h->levels[fine - 1];
+  auto launch = launcher(h);
+  for (int s = 0; s < h->n_sub; ++s) {
+    DevLevel& D = F.sub[s];
+    launch(grid_for(D.n), kBlock, k_prolong_add, static_cast<const int64_t*>(D.p_off.p),
+           static_cast<const int32_t*>(D.p_col.p), static_cast<const double*>(D.p_w.p),
+           xc + Cl.sub[s].offset, xf + D.offset, D.n, add);
+  }
+}
+
+// rc = R rf over owns_row rows; optional zeroing of Dirichlet b and of the coarse x.
+void enq_restrict(pf_hierarchy* h, int fine, const double* rf, double* bc, double* xc, int zero_dir) {
+  Level& F = h->levels[fine];
+  Level& Cl = h->levels[fine - 1];
+  auto launch = launcher(h);
+  for (int s = 0; s < h->n_sub; ++s) {
+    DevLevel& D = F.sub[s];
+    DevLevel& DC = Cl.sub[s];
+    launch(grid_for(DC.n), kBlock, k_restrict, static_cast<const int64_t*>(D.r_off.p),
+           static_cast<const int32_t*>(D.r_col.p), static_cast<const double*>(D.r_w.p),
+           rf + D.offset, bc + DC.offset, xc ? xc + DC.offset : nullptr,
+           static_cast<const uint8_t*>(DC.d_is_dir.p), DC.n, zero_dir);
+  }
+}
+
+void enq_coarse(pf_hierarchy* h, int l, double* x, const double* b, double tol, int max_iter) {
+  Level& L = h->levels[l];
+  if (h->world != h->n_sub)
+    state("multi-process coarse solve needs the replicated coarse level (not built)");
+  auto launch = launcher(h);
+  const ExchangePlan& ms = L.scatter[PF_CH_MASTER_SLAVE];
+  const ExchangePlan& h1 = L.scatter[PF_CH_HALO1];
+  launch(1, 32, k_coarse_gs, L.coarse_subs.p, h->n_sub, x, b, static_cast<const int32_t*>(ms.dst.p),
+         static_cast<const int32_t*>(ms.src.p), static_cast<int32_t>(ms.n),
+         static_cast<const int32_t*>(h1.dst.p), static_cast<const int32_t*>(h1.src.p),
+         static_cast<int32_t>(h1.n), tol, max_iter, L.coarse_stats.p);
+}
+
+// cycle (multigrid.cpp:150-190)
+void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_multigrid_config& cfg) {
+  Level& L = h->levels[l];
+  double* x = xv->cur();
+  if (l == 0) {
+    enq_coarse(h, 0, x, b, cfg.coarse_tol, cfg.coarse_max_iter);
+    enq_scatter(h, 0, PF_CH_HALO2, x);
+    return;
+  }
+  pf_smoother_config pre = cfg.smoother;
+  pre.sweeps = cfg.pre_smooth;
+  enq_smooth(h, l, xv, b, pre);
+  enq_scatter(h, l, PF_CH_HALO2, x);
+  enq_residual(h, l, x, b, L.r.p);
+  Level& Cl = h->levels[l - 1];
+  enq_restrict(h, l, L.r.p, Cl.b->cur(), Cl.x->cur(), 1);
+  enq_update_ms(h, l - 1, Cl.b->cur(), PF_UPDATE_ACCUMULATE_THEN_SCATTER);
+  enq_cycle(h, l - 1, Cl.x, Cl.b->cur(), cfg);
+  enq_prolong(h, l, Cl.x->cur(), x, 1);
+  pf_smoother_config post = cfg.smoother;
+  post.sweeps = cfg.post_smooth;
+  enq_smooth(h, l, xv, b, post);
+  enq_scatter(h, l, PF_CH_HALO2, x);
+}
+
+// v_cycle (multigrid.cpp:194-208)
+void enq_vcycle(pf_hierarchy* h, pf_vector* x, const double* b, const pf_multigrid_config& cfg) {
+  const int top = h->n_levels - 1;
+  enq_scatter(h, top, PF_CH_HALO2, x->cur());
+  enq_cycle(h, top, x, b, cfg);
+}
+
+void sync(pf_hierarchy* h) {
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  if (h->nccl) h->nccl->check_async();
+}
+
+double read_norm(pf_hierarchy* h, int l) {
+  PF_CUDA(cudaMemcpyAsync(h->pinned, h->levels[l].norm.p, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  return h->pinned[0];
+}
+
+void validate_cfg(const pf_multigrid_config& c) {
+  if (c.cycles < 1) invalid("cycles must be >= 1");
+  if (c.pre_smooth < 0 || c.post_smooth < 0) invalid("smoothing steps must be >= 0");
+  if (c.smoother.local_sweeps < 1) invalid("local_sweeps must be >= 1");
+  if (c.smoother.kind < 0 || c.smoother.kind > 2) invalid("unknown smoother kind");
+  if (c.outer_max_cycles < 1) invalid("outer_max_cycles must be >= 1");
+}
+
+std::string graph_key(const char* tag, const void* x, const void* b, const pf_multigrid_config& c) {
+  std::ostringstream os;
+  os << tag << ':' << x << ':' << b << ':' << c.cycles << ':' << c.smoother.kind << ':'
+     << c.smoother.local_sweeps << ':' << c.smoother.damping << ':' << c.pre_smooth << ':'
+     << c.post_smooth << ':' << c.coarse_tol << ':' << c.coarse_max_iter;
+  return os.str();
+}
+
+// One outer iteration of solve_outer as a graph: cfg.cycles V-cycles, the finest
+// residual norm, and its copy into pinned host memory.
+pf_hierarchy::GraphEntry& outer_graph(pf_hierarchy* h, pf_vector* x, const pf_vector* b,
+                                      const pf_multigrid_config& cfg, bool with_norm) {
+  const std::string key = graph_key(with_norm ? "outer" : "vcycle", x, b, cfg);
+  auto it = h->graphs.find(key);
+  if (it != h->graphs.end()) return it->second;
+  pf_hierarchy::GraphEntry e;
+  cudaGraph_t g = nullptr;
+  PF_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  g_capture_counter = &e.kernels;
+  try {
+    for (int j = 0; j < cfg.cycles; ++j) enq_vcycle(h, x, b->cur(), cfg);
+    if (with_norm) {
+      const int top = h->n_levels - 1;
+      enq_resnorm(h, top, x->cur(), b->cur());
+      PF_CUDA(cudaMemcpyAsync(h->pinned, h->levels[top].norm.p, sizeof(double),
+                              cudaMemcpyDeviceToHost, h->stream));
+    }
+  } catch (...) {
+    g_capture_counter = nullptr;
+    cudaStreamEndCapture(h->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  g_capture_counter = nullptr;
+  PF_CUDA(cudaStreamEndCapture(h->stream, &g));
+  PF_CUDA(cudaGraphInstantiate(&e.exec, g, 0));
+  PF_CUDA(cudaGraphDestroy(g));
+  return h->graphs.emplace(key, e).first->second;
+}
+
+void graph_launch(pf_hierarchy* h, pf_hierarchy::GraphEntry& e) {
+  PF_CUDA(cudaGraphLaunch(e.exec, h->stream));
+  h->launches += e.kernels;
+}
+
+void solve_outer_dev(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf_multigrid_config& cfg,
+                     pf_solve_stats* st, double* residuals, int max_res) {
+  validate_cfg(cfg);
+  const int top = h->n_levels - 1;
+  const double t0 = wall_now();
+  pf_solve_stats s{};
+  enq_resnorm(h, top, x->cur(), b->cur());
+  const double r0 = read_norm(h, top);
+  s.initial_residual = r0;
+  s.final_residual = r0;
+  s.converged = 1;
+  if (r0 != 0.0) {
+    s.converged = 0;
+    auto& g = outer_graph(h, x, b, cfg, true);
+    for (int outer = 1; outer <= cfg.outer_max_cycles; ++outer) {
+      graph_launch(h, g);
+      sync(h);
+      const double r = h->pinned[0];
+      s.iterations = outer;
+      if (residuals && outer <= max_res) residuals[outer - 1] = r;
+      s.final_residual = r;
+      if (r <= cfg.outer_tol * r0) {
+        s.converged = 1;
+        break;
+      }
+    }
+  }
+  s.solve_seconds = wall_now() - t0;
+  if (st) *st = s;
+  if (!s.converged) {
+    std::ostringstream os;
+    os << "multigrid stalled at relative residual " << s.final_residual / r0;
+    throw Error(PF_ERR_NO_CONVERGENCE, os.str());
+  }
+}
+
+void upload_vec(pf_hierarchy* h, pf_vector* v, int s, const double* host, int64_t n) {
+  DevLevel& D = h->levels[v->level].sub[s];
+  if (n != D.n)
+    invalid("vector length " + std::to_string(n) + " does not match mapper dof count " + std::to_string(D.n));
+  PF_CUDA(cudaMemcpyAsync(h->staging.p, host, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+  launcher(h)(grid_for(n), kBlock, k_scatter_perm, static_cast<const double*>(h->staging.p),
+              static_cast<const int32_t*>(D.d_perm.p), v->cur() + D.offset, D.n);
+}
+
+void download_vec(pf_hierarchy* h, const pf_vector* v, int s, double* host, int64_t n) {
+  DevLevel& D = h->levels[v->level].sub[s];
+  if (n != D.n)
+    invalid("vector length " + std::to_string(n) + " does not match mapper dof count " + std::to_string(D.n));
+  launcher(h)(grid_for(n), kBlock, k_gather_perm, static_cast<const double*>(v->cur() + D.offset),
+              static_cast<const int32_t*>(D.d_perm.p), h->staging.p, D.n);
+  PF_CUDA(cudaMemcpyAsync(host, h->staging.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+}
+
+pf_vector* new_vector(pf_hierarchy* h, int level) {
+  auto* v = new pf_vector;
+  v->h = h;
+  v->level = level;
+  v->total = h->levels[level].total;
+  v->data.alloc(2 * std::max<int64_t>(v->total, 1));
+  PF_CUDA(cudaMemsetAsync(v->data.p, 0, sizeof(double) * 2 * std::max<int64_t>(v->total, 1), h->stream));
+  return v;
+}
+
+void set_error(const char* m) { g_last_error = m; }
+
+}  // namespace
+}  // namespace pf
+
+pf_hierarchy::~pf_hierarchy() {
+  cudaSetDevice(device);
+  for (auto& [k, e] : graphs)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+  for (pf::Level& L : levels) {
+    delete L.x;
+    delete L.b;
+  }
+  levels.clear();
+  nccl.reset();
+  if (pinned) cudaFreeHost(pinned);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+#define PF_API_BEGIN try {
+#define PF_API_END                                   \
+  }                                                  \
+  catch (const pf::Error& e) {                       \
+    pf::set_error(e.what());                         \
+    return e.code;                                   \
+  }                                                  \
+  catch (const std::bad_alloc&) {                    \
+    pf::set_error("host out of memory");             \
+    return PF_ERR_STATE;                             \
+  }                                                  \
+  catch (const std::exception& e) {                  \
+    pf::set_error(e.what());                         \
+    return PF_ERR_STATE;                             \
+  }                                                  \
+  return PF_OK;
+
+extern "C" {
+
+const char* pf_last_error(void) { return pf::g_last_error.c_str(); }
+
+const char* pf_version(void) {
+  return "paper_1609_04809_b200 pf_gpu 0.1 (sm_100a, SELL-32 fp64)";
+}
+
+void pf_default_smoother_config(pf_smoother_config* o) {
+  o->kind = PF_SMOOTHER_GAUSS_SEIDEL;  // solvers.hpp:10
+  o->sweeps = 3;
+  o->local_sweeps = 1;
+  o->damping = 0.8;
+}
+
+void pf_default_multigrid_config(pf_multigrid_config* o) {
+  o->cycles = 1;  // multigrid.hpp:53-62
+  pf_default_smoother_config(&o->smoother);
+  o->pre_smooth = 3;
+  o->post_smooth = 3;
+  o->coarse_tol = 1e-12;
+  o->coarse_max_iter = 20000;
+  o->outer_tol = 1e-9;
+  o->outer_max_cycles = 100;
+}
+
+pf_status pf_hierarchy_create(int device, int n_levels, int n_subdomains, int rank_base,
+                              int world_size, pf_hierarchy** out) {
+  PF_API_BEGIN
+  if (!out) invalid("null output");
+  if (n_levels < 1) invalid("hierarchy needs at least one level");
+  if (n_subdomains < 1 || world_size < n_subdomains || rank_base < 0 ||
+      rank_base + n_subdomains > world_size)
+    invalid("bad subdomain / rank layout");
+  if (n_subdomains != world_size && n_subdomains != 1)
+    invalid("several subdomains per device are only supported when all ranks are local");
+  PF_CUDA(cudaSetDevice(device));
+  auto h = std::make_unique<pf_hierarchy>();
+  h->device = device;
+  h->n_levels = n_levels;
+  h->n_sub = n_subdomains;
+  h->rank_base = rank_base;
+  h->world = world_size;
+  h->levels.resize(static_cast<size_t>(n_levels));
+  for (auto& L : h->levels) L.host.resize(static_cast<size_t>(n_subdomains));
+  PF_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  PF_CUDA(cudaEventCreate(&h->ev0));
+  PF_CUDA(cudaEventCreate(&h->ev1));
+  PF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->pinned), 64 * sizeof(double)));
+  *out = h.release();
+  PF_API_END
+}
+
+pf_status pf_hierarchy_set_level(pf_hierarchy* h, int level, int sub, const pf_level_desc* d) {
+  PF_API_BEGIN
+  if (!h || !d) invalid("null argument");
+  if (h->finalized) state("hierarchy already finalized");
+  if (level < 0 || level >= h->n_levels) invalid("level out of range");
+  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
+  if (d->n_dofs < 0 || d->n_own_dofs < 0 || d->n_own_dofs > d->n_dofs) invalid("bad dof counts");
+  if (!d->row_offsets || (d->n_dofs > 0 && (!d->owns_row))) invalid("missing level arrays");
+  HostLevel& H = h->levels[level].host[sub];
+  H = HostLevel{};
+  H.set = true;
+  H.n = d->n_dofs;
+  H.n_own = d->n_own_dofs;
+  const int64_t nnz = d->row_offsets[d->n_dofs];
+  if (d->row_offsets[0] != 0 || nnz < 0) invalid("row offsets must start at 0");
+  if (nnz > 0 && (!d->col_indices || !d->values)) invalid("missing matrix arrays");
+  H.rowptr.assign(d->row_offsets, d->row_offsets + d->n_dofs + 1);
+  H.cols.assign(d->col_indices, d->col_indices + nnz);
+  H.vals.assign(d->values, d->values + nnz);
+  H.owns_row.assign(d->owns_row, d->owns_row + d->n_dofs);
+  if (d->is_dirichlet) H.is_dir.assign(d->is_dirichlet, d->is_dirichlet + d->n_dofs);
+  else H.is_dir.assign(static_cast<size_t>(d->n_dofs), 0);
+  if (d->color) H.color.assign(d->color, d->color + d->n_own_dofs);
+  const int me = h->rank_base + sub;
+  for (int i = 0; i < d->n_channels; ++i) {
+    const pf_channel_desc& c = d->channels[i];
+    if (c.kind < 0 || c.kind >= PF_NUM_CHANNEL_KINDS) invalid("bad channel kind");
+    if (c.peer < 0 || c.peer >= h->world || c.peer == me) invalid("bad channel peer");
+    HostChannel hc;
+    hc.kind = c.kind;
+    hc.peer = c.peer;
+    hc.send.assign(c.send_dofs, c.send_dofs + c.n_send);
+    hc.recv.assign(c.recv_dofs, c.recv_dofs + c.n_recv);
+    for (int32_t v : hc.send)
+      if (v < 0 || v >= d->n_dofs) invalid("channel send dof out of range");
+    for (int32_t v : hc.recv)
+      if (v < 0 || v >= d->n_dofs) invalid("channel recv dof out of range");
+    H.channels.push_back(std::move(hc));
+  }
+  std::sort(H.channels.begin(), H.channels.end(), [](const HostChannel& a, const HostChannel& b) {
+    return a.kind != b.kind ? a.kind < b.kind : a.peer < b.peer;
+  });
+  if (level > 0) {
+    if (!d->p_offsets) invalid("level > 0 needs a prolongation map");
+    H.p_off.assign(d->p_offsets, d->p_offsets + d->n_dofs + 1);
+    const int64_t pn = H.p_off.back();
+    H.p_col.assign(d->p_cols, d->p_cols + pn);
+    H.p_w.assign(d->p_weights, d->p_weights + pn);
+  }
+  PF_API_END
+}
+
+pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
+  PF_API_BEGIN
+  if (!h) invalid("null hierarchy");
+  if (h->finalized) state("hierarchy already finalized");
+  PF_CUDA(cudaSetDevice(h->device));
+  int64_t max_total = 1;
+  for (int l = 0; l < h->n_levels; ++l) {
+    Level& L = h->levels[l];
+    L.sub.resize(static_cast<size_t>(h->n_sub));
+    int64_t off = 0;
+    for (int s = 0; s < h->n_sub; ++s) {
+      if (!L.host[s].set)
+        state("level " + std::to_string(l) + " subdomain " + std::to_string(s) + " not set");
+      build_dev_level(L.host[s], L.sub[s], l);
+      L.sub[s].offset = off;
+      off += L.sub[s].n;
+      max_total = std::max<int64_t>(max_total, L.sub[s].n);
+    }
+    L.total = off;
+    if (off >= (int64_t(1) << 31)) invalid("level too large for int32 device indices");
+    if (l > 0)
+      for (int s = 0; s < h->n_sub; ++s)
+        build_transfer(L.host[s], L.sub[s], h->levels[l - 1].host[s], h->levels[l - 1].sub[s]);
+    build_plans(h, l);
+    L.r.alloc(std::max<int64_t>(off, 1));
+    L.sumsq.alloc(1 + std::max(h->world, h->n_sub));
+    L.norm.alloc(1);
+    L.coarse_stats.alloc(4);
+    PF_CUDA(cudaMemset(L.coarse_stats.p, 0, 4 * sizeof(double)));
+    if (l == 0) {
+      std::vector<CoarseSub> cs;
+      for (DevLevel& D : L.sub) cs.push_back(CoarseSub{view(D.A), D.d_perm.p, D.n_own, D.offset});
+      L.coarse_subs.upload(cs);
+    }
+  }
+  h->staging.alloc(max_total);
+  for (int l = 0; l < h->n_levels; ++l) {
+    h->levels[l].x = new_vector(h, l);
+    h->levels[l].b = new_vector(h, l);
+  }
+  for (Level& L : h->levels) L.host.clear();
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  h->finalized = true;
+  PF_API_END
+}
+
+pf_status pf_nccl_unique_id(void* out, int nbytes) {
+  PF_API_BEGIN
+  pf::nccl_unique_id(out, nbytes);
+  PF_API_END
+}
+
+pf_status pf_hierarchy_init_nccl(pf_hierarchy* h, const void* id, int nbytes) {
+  PF_API_BEGIN
+  if (!h) invalid("null hierarchy");
+  if (h->world == h->n_sub) state("NCCL is only used when ranks live in separate processes");
+  PF_CUDA(cudaSetDevice(h->device));
+  h->nccl = pf::nccl_init(h->rank_base, h->world, id, nbytes);
+  PF_API_END
+}
+
+pf_status pf_hierarchy_destroy(pf_hierarchy* h) {
+  PF_API_BEGIN
+  delete h;
+  PF_API_END
+}
+
+pf_status pf_hierarchy_device_bytes(const pf_hierarchy* h, int64_t* out) {
+  PF_API_BEGIN
+  if (!h || !out) invalid("null argument");
+  int64_t b = 0;
+  for (const Level& L : h->levels) {
+    for (const DevLevel& D : L.sub)
+      b += D.A.vals.bytes() + D.A.cols.bytes() + D.A.slice_ptr.bytes() + D.A.row_len.bytes() +
+           D.p_off.bytes() + D.p_col.bytes() + D.p_w.bytes() + D.r_off.bytes() + D.r_col.bytes() +
+           D.r_w.bytes() + D.d_perm.bytes() + D.d_is_dir.bytes();
+    b += L.r.bytes() + (L.x ? L.x->data.bytes() : 0) + (L.b ? L.b->data.bytes() : 0);
+  }
+  *out = b;
+  PF_API_END
+}
+
+pf_status pf_vector_create(pf_hierarchy* h, int level, pf_vector** out) {
+  PF_API_BEGIN
+  check_level(h, level);
+  if (!out) invalid("null output");
+  PF_CUDA(cudaSetDevice(h->device));
+  *out = new_vector(h, level);
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  PF_API_END
+}
+
+pf_status pf_vector_destroy(pf_vector* v) {
+  PF_API_BEGIN
+  if (v) cudaSetDevice(v->h->device);
+  delete v;
+  PF_API_END
+}
+
+pf_status pf_vector_upload(pf_vector* v, int sub, const double* host, int64_t n) {
+  PF_API_BEGIN
+  if (!v || !host) invalid("null argument");
+  pf_hierarchy* h = v->h;
+  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
+  PF_CUDA(cudaSetDevice(h->device));
+  upload_vec(h, v, sub, host, n);
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_vector_download(const pf_vector* v, int sub, double* host, int64_t n) {
+  PF_API_BEGIN
+  if (!v || !host) invalid("null argument");
+  pf_hierarchy* h = v->h;
+  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
+  PF_CUDA(cudaSetDevice(h->device));
+  download_vec(h, v, sub, host, n);
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_vector_fill(pf_vector* v, double value) {
+  PF_API_BEGIN
+  if (!v) invalid("null vector");
+  PF_CUDA(cudaSetDevice(v->h->device));
+  launcher(v->h)(grid_for(2 * v->total), kBlock, k_fill, v->data.p, value, 2 * v->total);
+  sync(v->h);
+  PF_API_END
+}
+
+pf_status pf_host_alloc(void** out, int64_t bytes) {
+  PF_API_BEGIN
+  if (!out || bytes < 0) invalid("bad argument");
+  PF_CUDA(cudaMallocHost(out, static_cast<size_t>(std::max<int64_t>(bytes, 8))));
+  PF_API_END
+}
+
+pf_status pf_host_free(void* p) {
+  PF_API_BEGIN
+  if (p) PF_CUDA(cudaFreeHost(p));
+  PF_API_END
+}
+
+pf_status pf_spmv(pf_hierarchy* h, int level, const pf_vector* x, pf_vector* y) {
+  PF_API_BEGIN
+  check_level(h, level);
+  check_vec(h, x, level, "x");
+  check_vec(h, y, level, "y");
+  PF_CUDA(cudaSetDevice(h->device));
+  enq_spmv(h, level, x->cur(), y->cur());
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_residual_norm(pf_hierarchy* h, int level, const pf_vector* x, const pf_vector* b, double* out) {
+  PF_API_BEGIN
+  check_level(h, level);
+  check_vec(h, x, level, "x");
+  check_vec(h, b, level, "b");
+  if (!out) invalid("null output");
+  PF_CUDA(cudaSetDevice(h->device));
+  enq_resnorm(h, level, x->cur(), b->cur());
+  *out = read_norm(h, level);
+  PF_API_END
+}
+
+pf_status pf_smooth(pf_hierarchy* h, int level, pf_vector* x, const pf_vector* b, const pf_smoother_config* cfg) {
+  PF_API_BEGIN
+  check_level(h, level);
+  check_vec(h, x, level, "x");
+  check_vec(h, b, level, "b");
+  if (!cfg) invalid("null config");
+  if (cfg->kind < 0 || cfg->kind > 2) invalid("unknown smoother kind");
+  if (cfg->sweeps < 0 || cfg->local_sweeps < 0) invalid("negative sweep count");
+  PF_CUDA(cudaSetDevice(h->device));
+  enq_smooth(h, level, x, b->cur(), *cfg);
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_coarse_solve(pf_hierarchy* h, int level, pf_vector* x, const pf_vector* b, double tol,
+                          int max_iter, pf_solve_stats* stats) {
+  PF_API_BEGIN
+  check_level(h, level);
+  check_vec(h, x, level, "x");
+  check_vec(h, b, level, "b");
+  PF_CUDA(cudaSetDevice(h->device));
+  const double t0 = wall_now();
+  enq_coarse(h, level, x->cur(), b->cur(), tol, max_iter);
+  double st[4];
+  PF_CUDA(cudaMemcpyAsync(h->pinned, h->levels[level].coarse_stats.p, 4 * sizeof(double),
+                          cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  std::memcpy(st, h->pinned, sizeof st);
+  if (stats) {
+    stats->iterations = static_cast<int32_t>(st[0]);
+    stats->converged = static_cast<int32_t>(st[1]);
+    stats->initial_residual = st[2];
+    stats->final_residual = st[3];
+    stats->solve_seconds = wall_now() - t0;
+    stats->comm_seconds = 0;
+  }
+  PF_API_END
+}
+
+pf_status pf_prolongate(pf_hierarchy* h, int fine, const pf_vector* coarse, pf_vector* out) {
+  PF_API_BEGIN
+  check_level(h, fine);
+  if (fine == 0) invalid("level 0 has no parent");
+  check_vec(h, coarse, fine - 1, "coarse");
+  check_vec(h, out, fine, "out");
+  PF_CUDA(cudaSetDevice(h->device));
+  enq_prolong(h, fine, coarse->cur(), out->cur(), 0);
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_restrict_residual(pf_hierarchy* h, int fine, const pf_vector* r, pf_vector* rc) {
+  PF_API_BEGIN
+  check_level(h, fine);
+  if (fine == 0) invalid("level 0 has no parent");
+  check_vec(h, r, fine, "r");
+  check_vec(h, rc, fine - 1, "rc");
+  PF_CUDA(cudaSetDevice(h->device));
+  enq_restrict(h, fine, r->cur(), rc->cur(), nullptr, 0);
+  enq_update_ms(h, fine - 1, rc->cur(), PF_UPDATE_ACCUMULATE_THEN_SCATTER);
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_update_master_slave(pf_hierarchy* h, int level, pf_vector* v, int mode) {
+  PF_API_BEGIN
+  check_level(h, level);
+  check_vec(h, v, level, "v");
+  if (mode != PF_UPDATE_SCATTER && mode != PF_UPDATE_ACCUMULATE_THEN_SCATTER) invalid("bad update mode");
+  PF_CUDA(cudaSetDevice(h->device));
+  enq_update_ms(h, level, v->cur(), mode);
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_update_halo1(pf_hierarchy* h, int level, pf_vector* v) {
+  PF_API_BEGIN
+  check_level(h, level);
+  check_vec(h, v, level, "v");
+  PF_CUDA(cudaSetDevice(h->device));
+  enq_scatter(h, level, PF_CH_HALO1, v->cur());
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_update_halo2(pf_hierarchy* h, int level, pf_vector* v) {
+  PF_API_BEGIN
+  check_level(h, level);
+  check_vec(h, v, level, "v");
+  PF_CUDA(cudaSetDevice(h->device));
+  enq_scatter(h, level, PF_CH_HALO2, v->cur());
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_allreduce_sum(pf_hierarchy* h, const double* per_sub, double* out) {
+  PF_API_BEGIN
+  check_level(h, 0);
+  if (!per_sub || !out) invalid("null argument");
+  PF_CUDA(cudaSetDevice(h->device));
+  Level& L = h->levels[0];
+  PF_CUDA(cudaMemcpyAsync(L.sumsq.p, per_sub, sizeof(double) * h->n_sub, cudaMemcpyHostToDevice, h->stream));
+  enq_allreduce(h, L, false);
+  *out = read_norm(h, 0);
+  PF_API_END
+}
+
+pf_status pf_v_cycle(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf_multigrid_config* cfg,
+                     pf_solve_stats* stats) {
+  PF_API_BEGIN
+  check_level(h, h ? h->n_levels - 1 : 0);
+  check_vec(h, x, h->n_levels - 1, "x");
+  check_vec(h, b, h->n_levels - 1, "b");
+  if (!cfg) invalid("null config");
+  validate_cfg(*cfg);
+  PF_CUDA(cudaSetDevice(h->device));
+  const double t0 = wall_now();
+  enq_vcycle(h, x, b->cur(), *cfg);
+  PF_CUDA(cudaMemcpyAsync(h->pinned, h->levels[0].coarse_stats.p, 4 * sizeof(double),
+                          cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  if (stats) {
+    stats->iterations = static_cast<int32_t>(h->pinned[0]);
+    stats->converged = static_cast<int32_t>(h->pinned[1]);
+    stats->initial_residual = h->pinned[2];
+    stats->final_residual = h->pinned[3];
+    stats->solve_seconds = wall_now() - t0;
+    stats->comm_seconds = 0;
+  }
+  PF_API_END
+}
+
+pf_status pf_solve_outer(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf_multigrid_config* cfg,
+                         pf_solve_stats* stats, double* residuals, int max_residuals) {
+  PF_API_BEGIN
+  check_level(h, h ? h->n_levels - 1 : 0);
+  check_vec(h, x, h->n_levels - 1, "x");
+  check_vec(h, b, h->n_levels - 1, "b");
+  if (!cfg) invalid("null config");
+  PF_CUDA(cudaSetDevice(h->device));
+  solve_outer_dev(h, x, b, *cfg, stats, residuals, max_residuals);
+  PF_API_END
+}
+
+pf_status pf_solve_outer_host(pf_hierarchy* h, double* const* x_host, const double* const* b_host,
+                              const pf_multigrid_config* cfg, pf_solve_stats* stats, double* residuals,
+                              int max_residuals) {
+  PF_API_BEGIN
+  check_level(h, h ? h->n_levels - 1 : 0);
+  if (!x_host || !b_host || !cfg) invalid("null argument");
+  PF_CUDA(cudaSetDevice(h->device));
+  const int top = h->n_levels - 1;
+  Level& T = h->levels[top];
+  // the finest level's own scratch vectors carry the user's x and b
+  for (int s = 0; s < h->n_sub; ++s) {
+    upload_vec(h, T.x, s, x_host[s], T.sub[s].n);
+    upload_vec(h, T.b, s, b_host[s], T.sub[s].n);
+  }
+  pf_status rc = PF_OK;
+  std::string msg;
+  try {
+    solve_outer_dev(h, T.x, T.b, *cfg, stats, residuals, max_residuals);
+  } catch (const pf::Error& e) {
+    if (e.code != PF_ERR_NO_CONVERGENCE) throw;
+    rc = e.code;
+    msg = e.what();
+  }
+  for (int s = 0; s < h->n_sub; ++s) {
+    download_vec(h, T.x, s, x_host[s], T.sub[s].n);
+    sync(h);  // staging buffer is shared between subdomains
+  }
+  if (rc != PF_OK) throw pf::Error(rc, msg);
+  PF_API_END
+}
+
+pf_status pf_launch_count(const pf_hierarchy* h, int64_t* out) {
+  PF_API_BEGIN
+  if (!h || !out) invalid("null argument");
+  *out = h->launches;
+  PF_API_END
+}
+
+pf_status pf_reset_launch_count(pf_hierarchy* h) {
+  PF_API_BEGIN
+  if (!h) invalid("null hierarchy");
+  h->launches = 0;
+  PF_API_END
+}
+
+pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double* mean_ms, double* bytes) {
+  PF_API_BEGIN
+  check_level(h, level);
+  if (iters < 1) invalid("iters must be >= 1");
+  PF_CUDA(cudaSetDevice(h->device));
+  Level& L = h->levels[level];
+  DevLevel& D = L.sub[0];
+  pf_vector* x = L.x;
+  const double* b = L.b->cur();
+  auto launch = launcher(h);
+  auto one = [&](int i) {
+    if (kind == PF_SMOOTHER_JACOBI) {
+      const double* src = (i & 1) ? x->alt() : x->cur();
+      double* dst = (i & 1) ? x->cur() : x->alt();
+      launch(grid_for(D.n), kBlock, k_jacobi, view(D.A), src, dst, b, D.n_own, D.n, 0.8);
+    } else {
+      for (int c = 0; c < D.n_colors; ++c)
+        launch(grid_for(D.color_start[c + 1] - D.color_start[c]), kBlock, k_color_sweep<true>, view(D.A),
+               x->cur(), b, D.color_start[c], D.color_start[c + 1], kind == PF_SMOOTHER_MULTICOLOR_SOR ? 1.2 : 1.0);
+    }
+  };
+  for (int i = 0; i < 3; ++i) one(i);  // warm-up
+  PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+  for (int i = 0; i < iters; ++i) one(i);
+  PF_CUDA(cudaEventRecord(h->ev1, h->stream));
+  sync(h);
+  float ms = 0;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (mean_ms) *mean_ms = ms / iters;
+  // B = 12 z + 4 n + 8 m + 8 n (b) + 8 n (out), n = own rows,
+  // z = own nnz, m = distinct columns the own rows touch.
+  if (bytes)
+    *bytes = 12.0 * D.A.own_nnz + 4.0 * D.n_own + 8.0 * D.own_cols_touched + 16.0 * D.n_own;
+  PF_API_END
+}
+
+pf_status pf_time_vcycle(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf_multigrid_config* cfg,
+                         int iters, double* mean_ms) {
+  PF_API_BEGIN
+  check_level(h, h ? h->n_levels - 1 : 0);
+  check_vec(h, x, h->n_levels - 1, "x");
+  check_vec(h, b, h->n_levels - 1, "b");
+  if (!cfg || iters < 1) invalid("bad argument");
+  validate_cfg(*cfg);
+  PF_CUDA(cudaSetDevice(h->device));
+  pf_multigrid_config one = *cfg;
+  one.cycles = 1;
+  auto& g = outer_graph(h, x, b, one, false);
+  graph_launch(h, g);
+  PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+  for (int i = 0; i < iters; ++i) graph_launch(h, g);
+  PF_CUDA(cudaEventRecord(h->ev1, h->stream));
+  sync(h);
+  float ms = 0;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  *mean_ms = ms / iters;
+  PF_API_END
+}
+
+pf_status pf_level_info(const pf_hierarchy* h, int level, int sub, int64_t* n_dofs, int64_t* n_own,
+                        int64_t* nnz, int64_t* n_colors) {
+  PF_API_BEGIN
+  check_level(h, level);
+  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
+  const DevLevel& D = h->levels[level].sub[sub];
+  if (n_dofs) *n_dofs = D.n;
+  if (n_own) *n_own = D.n_own;
+  if (nnz) *nnz = D.A.nnz;
+  if (n_colors) *n_colors = D.n_colors;
+  PF_API_END
+}
+
+}  // extern "C"

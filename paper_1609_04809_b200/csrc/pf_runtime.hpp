@@ -1,0 +1,180 @@
+// pf_runtime.hpp — host-side runtime of the B200 GMG hot path (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "pf_gpu.h"
+#include "pf_types.hpp"
+
+namespace pf {
+
+struct Error : std::runtime_error {
+  pf_status code;
+  Error(pf_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define PF_CUDA(x) ::pf::cuda_check((x), #x)
+
+// Owning device buffer.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { reset(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(int64_t count) {
+    reset();
+    n = count;
+    if (count > 0) PF_CUDA(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
+  }
+  void upload(const std::vector<T>& v) {
+    alloc(static_cast<int64_t>(v.size()));
+    if (!v.empty()) PF_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  }
+  int64_t bytes() const { return n * static_cast<int64_t>(sizeof(T)); }
+};
+
+struct HostChannel {
+  int kind = 0, peer = 0;
+  std::vector<int32_t> send, recv;
+};
+
+// Deep copy of one pf_level_desc.
+struct HostLevel {
+  bool set = false;
+  int32_t n = 0, n_own = 0;
+  std::vector<int64_t> rowptr;
+  std::vector<int32_t> cols;
+  std::vector<double> vals;
+  std::vector<uint8_t> owns_row, is_dir;
+  std::vector<int32_t> color;
+  std::vector<HostChannel> channels;
+  std::vector<int64_t> p_off;
+  std::vector<int32_t> p_col;
+  std::vector<double> p_w;
+};
+
+// SELL-32 operator on the device.
+struct DevSell {
+  DevBuf<double> vals;
+  DevBuf<int32_t> cols;
+  DevBuf<int64_t> slice_ptr;
+  DevBuf<int32_t> row_len;
+  int64_t nnz = 0, own_nnz = 0, stored = 0;
+};
+
+// One subdomain of one level on the device.
+struct DevLevel {
+  int32_t n = 0, n_own = 0;
+  int64_t offset = 0;  // position of this subdomain inside the level's vectors
+  int n_colors = 0;
+  std::vector<int32_t> color_start;  // device rows, n_colors + 1 (own rows only)
+  std::vector<int32_t> perm;         // host index -> device index
+  DevBuf<int32_t> d_perm;
+  DevSell A;
+  DevBuf<uint8_t> d_is_dir;
+  int64_t own_cols_touched = 0;  // distinct columns referenced by own rows
+  // prolongation from the parent level (rows = this level's device rows)
+  DevBuf<int64_t> p_off;
+  DevBuf<int32_t> p_col;  // parent device index (+ parent offset)
+  DevBuf<double> p_w;
+  int64_t p_nnz = 0;
+  // restriction to the parent level (rows = parent device rows)
+  DevBuf<int64_t> r_off;
+  DevBuf<int32_t> r_col;  // this level's device index (+ own offset)
+  DevBuf<double> r_w;
+  int64_t r_nnz = 0;
+  // residual-norm scratch
+  int resnorm_blocks = 0;
+  DevBuf<double> partials;
+  DevBuf<unsigned int> ticket;
+};
+
+struct PeerSeg {
+  int peer = 0;
+  int64_t off = 0, len = 0;
+};
+
+// One exchange (scatter of one channel kind, or the master/slave accumulate) on one
+// level.  Indices are level-global device indices (subdomain offset included).
+struct ExchangePlan {
+  int64_t n = 0;  // entries moved
+  // local transport (all peers on this device): v[dst[i]] = v[src[i]]
+  DevBuf<int32_t> dst, src;
+  // accumulate: per master m: v[acc_dst[m]] += sum over acc_src[acc_off[m]..acc_off[m+1])
+  int32_t n_masters = 0;
+  DevBuf<int32_t> acc_off, acc_src, acc_dst;
+  // remote transport (NCCL; one subdomain per process)
+  DevBuf<int32_t> pack_idx, unpack_idx;
+  std::vector<PeerSeg> send_segs, recv_segs;
+  DevBuf<double> sendbuf, recvbuf;
+};
+
+struct Level {
+  std::vector<HostLevel> host;  // per local subdomain (freed after finalize)
+  std::vector<DevLevel> sub;    // per local subdomain
+  int64_t total = 0;            // sum of subdomain sizes
+  std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS> scatter;
+  ExchangePlan accumulate;
+  DevBuf<double> r;             // residual scratch
+  DevBuf<double> sumsq;         // per-subdomain sums of squares
+  DevBuf<double> norm;          // allreduced norm
+  DevBuf<double> coarse_stats;  // [iterations, converged, r0, final]
+  DevBuf<CoarseSub> coarse_subs;  // level 0 only
+  pf_vector* x = nullptr;       // MultigridLevel::x, b (cycle scratch)
+  pf_vector* b = nullptr;
+};
+
+struct Nccl;  // pf_nccl.cpp
+
+}  // namespace pf
+
+struct pf_vector {
+  pf_hierarchy* h = nullptr;
+  int level = 0;
+  pf::DevBuf<double> data;  // [2 * total]: primary then Jacobi ping-pong partner
+  double* cur() const { return data.p; }
+  double* alt() const { return data.p + total; }
+  int64_t total = 0;
+};
+
+struct pf_hierarchy {
+  int device = 0;
+  int n_levels = 0, n_sub = 1, rank_base = 0, world = 1;
+  bool finalized = false;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<pf::Level> levels;
+  pf::DevBuf<double> staging;  // host-order staging for uploads/downloads
+  double* pinned = nullptr;    // pinned host slots for scalars read back each cycle
+  int64_t launches = 0;
+  std::unique_ptr<pf::Nccl> nccl;
+  // graph cache of one outer cycle (cycles x V-cycle + finest residual norm)
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
+  };
+  std::map<std::string, GraphEntry> graphs;
+  ~pf_hierarchy();
+};

@@ -1,0 +1,127 @@
+"""Host-side level data: the Python form of ``pf_level_desc`` (include/pf_gpu.h).
+
+A ``LevelArrays`` is one rank's view of one ``MultigridLevel``
+(/root/reference/proj/include/parfem/multigrid.hpp:15-31) in the reference's host
+order: the level operator as CSR, the ParFEMapper fields the hot path reads
+(n_own_dofs, owns_row, the Dirichlet class, the channels, femapper.hpp:45-70) and the
+prolongation map (multigrid.cpp:35-72).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+
+@dataclass
+class Channel:
+    kind: int
+    peer: int
+    send: np.ndarray  # int32, host order
+    recv: np.ndarray  # int32, host order
+
+
+@dataclass
+class LevelArrays:
+    n: int
+    n_own: int
+    row_offsets: np.ndarray
+    cols: np.ndarray
+    vals: np.ndarray
+    owns_row: np.ndarray
+    is_dir: np.ndarray
+    color: np.ndarray | None = None
+    channels: list = field(default_factory=list)
+    p_offsets: np.ndarray | None = None
+    p_cols: np.ndarray | None = None
+    p_w: np.ndarray | None = None
+    keys: np.ndarray | None = None      # (n, 4) int64: entity kind, lattice key
+    class_of: np.ndarray | None = None  # uint8 DofClass
+
+    def normalized(self) -> "LevelArrays":
+        def a(x, t):
+            return None if x is None else np.ascontiguousarray(x, dtype=t)
+        chans = [Channel(int(c.kind), int(c.peer), a(c.send, np.int32), a(c.recv, np.int32))
+                 for c in self.channels]
+        return LevelArrays(int(self.n), int(self.n_own), a(self.row_offsets, np.int64),
+                           a(self.cols, np.int32), a(self.vals, np.float64),
+                           a(self.owns_row, np.uint8), a(self.is_dir, np.uint8),
+                           a(self.color, np.int32), chans, a(self.p_offsets, np.int64),
+                           a(self.p_cols, np.int32), a(self.p_w, np.float64),
+                           a(self.keys, np.int64), a(self.class_of, np.uint8))
+
+    def desc(self):
+        """(LevelDesc, keepalive) pointing into this object's arrays."""
+        L = self.normalized()
+        chans = (_lib.ChannelDesc * max(len(L.channels), 1))()
+        for i, c in enumerate(L.channels):
+            chans[i] = _lib.ChannelDesc(c.kind, c.peer, len(c.send), len(c.recv),
+                                        c.send.ctypes.data, c.recv.ctypes.data)
+        p = lambda x: None if x is None else x.ctypes.data  # noqa: E731
+        d = _lib.LevelDesc(L.n, L.n_own, p(L.row_offsets), p(L.cols), p(L.vals), p(L.owns_row),
+                           p(L.is_dir), p(L.color), len(L.channels), chans, p(L.p_offsets),
+                           p(L.p_cols), p(L.p_w))
+        return d, (L, chans)
+
+
+def _arr(ptr, n, ctype, dtype):
+    if n == 0:
+        return np.zeros(0, dtype)
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(n,)).astype(dtype, copy=True)
+
+
+class StructuredSetup:
+    """The product's communication-free setup (include/pf_setup.h) for one rank."""
+
+    def __init__(self, dim: int, n_coarse: int, n_levels: int, n_ranks: int = 1, rank: int = 0,
+                 problem: int = _lib.PF_PROBLEM_BASELINE):
+        L = _lib.lib()
+        self._h = C.c_void_p()
+        _lib.check(L.pf_setup_create(dim, n_coarse, n_levels, n_ranks, rank, problem,
+                                     C.byref(self._h)), setup=True)
+        self.dim, self.n_coarse, self.n_levels = dim, n_coarse, n_levels
+        self.n_ranks, self.rank, self.problem = n_ranks, rank, problem
+        self.levels = [self._level(l) for l in range(n_levels)]
+        bp, xp, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        _lib.check(L.pf_setup_rhs(self._h, C.byref(bp), C.byref(xp), C.byref(n)), setup=True)
+        self.b = _arr(bp, n.value, C.c_double, np.float64)
+        self.x0 = _arr(xp, n.value, C.c_double, np.float64)
+        ng = C.c_int64()
+        _lib.check(L.pf_setup_counts(self._h, n_levels - 1, C.byref(ng), None, None, None), setup=True)
+        self.n_global = ng.value
+        s = C.c_double()
+        _lib.check(L.pf_setup_seconds(self._h, C.byref(s)), setup=True)
+        self.seconds = s.value
+        L.pf_setup_destroy(self._h)
+        self._h = None
+
+    def _level(self, l: int) -> LevelArrays:
+        L = _lib.lib()
+        d = _lib.LevelDesc()
+        _lib.check(L.pf_setup_level(self._h, l, C.byref(d)), setup=True)
+        n, n_own = d.n_dofs, d.n_own_dofs
+        rp = _arr(d.row_offsets, n + 1, C.c_int64, np.int64)
+        nnz = int(rp[-1])
+        chans = []
+        for i in range(d.n_channels):
+            c = d.channels[i]
+            chans.append(Channel(c.kind, c.peer, _arr(c.send_dofs, c.n_send, C.c_int32, np.int32),
+                                 _arr(c.recv_dofs, c.n_recv, C.c_int32, np.int32)))
+        kp, cp = C.c_void_p(), C.c_void_p()
+        _lib.check(L.pf_setup_level_keys(self._h, l, C.byref(kp), C.byref(cp)), setup=True)
+        out = LevelArrays(n, n_own, rp, _arr(d.col_indices, nnz, C.c_int32, np.int32),
+                          _arr(d.values, nnz, C.c_double, np.float64),
+                          _arr(d.owns_row, n, C.c_uint8, np.uint8),
+                          _arr(d.is_dirichlet, n, C.c_uint8, np.uint8),
+                          _arr(d.color, n_own, C.c_int32, np.int32), chans,
+                          keys=_arr(kp, 4 * n, C.c_int64, np.int64).reshape(n, 4),
+                          class_of=_arr(cp, n, C.c_uint8, np.uint8))
+        if l > 0:
+            out.p_offsets = _arr(d.p_offsets, n + 1, C.c_int64, np.int64)
+            pn = int(out.p_offsets[-1])
+            out.p_cols = _arr(d.p_cols, pn, C.c_int32, np.int32)
+            out.p_w = _arr(d.p_weights, pn, C.c_double, np.float64)
+        return out
