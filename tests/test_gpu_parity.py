@@ -1,0 +1,185 @@
+"""GPU parity: every hot-path operation of libpf_gpu.so against the C restatement (bit for
+bit, same input bytes) and against the compiled reference itself.
+
+The restatement (oracle/gmg_oracle.c) is pinned bit-exactly to the reference by
+tests/test_oracle.py, so "GPU == oracle" on the reference's own level data means
+"GPU == reference".  Jacobi iterates, coloured GS/SOR iterates, the cycle residual,
+restriction (+ accumulate), prolongation, the exchanges and the coarse solve are
+compared with ==; norms (device tree reduction vs sequential sum) within 1e-13.
+"""
+import numpy as np
+import pytest
+
+from helpers import cfg, download, key_noise, keyed, structured, upload
+from oracle.restated import Oracle
+from paper_1609_04809_b200 import _lib, gmg
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [gmg.PF_SMOOTHER_JACOBI, gmg.PF_SMOOTHER_GAUSS_SEIDEL, gmg.PF_SMOOTHER_MULTICOLOR_SOR]
+CASES = [(3, 2, 4, 1), (3, 2, 4, 2), (3, 2, 4, 4), (3, 2, 3, 8), (2, 4, 3, 6), (3, 2, 3, 3)]
+
+
+def exact(a_list, b_list):
+    return all(np.array_equal(a, b) for a, b in zip(a_list, b_list))
+
+
+@pytest.fixture(scope="module", params=CASES, ids=lambda c: "d%d_nc%d_L%d_K%d" % c)
+def system(request, cuda):
+    dim, nc, L, K = request.param
+    setups, levels = structured(dim, nc, L, K)
+    h = gmg.Hierarchy(levels)
+    o = Oracle(levels)
+    return dict(h=h, o=o, levels=levels, setups=setups, K=K, L=L)
+
+
+@pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
+def test_smooth_bit_exact(system, kind):
+    h, o, levels, K, L = system["h"], system["o"], system["levels"], system["K"], system["L"]
+    top = L - 1
+    tl = [lv[top] for lv in levels]
+    x0 = key_noise(tl, 11)
+    b = key_noise(tl, 12)
+    omega = 1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8
+    for sweeps in (1, 2, 3):
+        x = upload(h, top, x0)
+        bb = upload(h, top, b)
+        gmg.smooth(h, top, x, bb, gmg.SmootherConfig(kind=kind, sweeps=sweeps, damping=omega))
+        got = download(h, x, K)
+        want = o.smooth(top, x0, b, kind, sweeps=sweeps, damping=omega)
+        assert exact(got, want), f"sweeps={sweeps}"
+
+
+def test_spmv_residual_transfers_bit_exact(system):
+    h, o, levels, K, L = system["h"], system["o"], system["levels"], system["K"], system["L"]
+    for l in range(L):
+        lv = [s[l] for s in levels]
+        x = key_noise(lv, 21 + l)
+        b = key_noise(lv, 31 + l)
+        xd, bd, yd = upload(h, l, x), upload(h, l, b), h.vector(l)
+        gmg.spmv(h, l, xd, yd)
+        assert exact(download(h, yd, K), o.spmv(l, x))
+        rn = gmg.residual_norm(h, l, xd, bd)
+        assert rn == pytest.approx(o.residual_norm(l, x, b), rel=1e-13)
+        for kind in (0, 1, 2):
+            v = upload(h, l, x)
+            {0: lambda: gmg.update_master_slave(h, l, v, gmg.PF_UPDATE_SCATTER),
+             1: lambda: gmg.update_halo1(h, l, v), 2: lambda: gmg.update_halo2(h, l, v)}[kind]()
+            want = (o.update_master_slave(l, x, 0) if kind == 0 else o.update_halo(l, kind, x))
+            assert exact(download(h, v, K), want), f"scatter kind {kind}"
+        v = upload(h, l, x)
+        gmg.update_master_slave(h, l, v, gmg.PF_UPDATE_ACCUMULATE_THEN_SCATTER)
+        assert exact(download(h, v, K), o.update_master_slave(l, x, 1))
+        if l > 0:
+            lc = [s[l - 1] for s in levels]
+            xc = key_noise(lc, 41 + l)
+            out = h.vector(l)
+            gmg.prolongate(h, l, upload(h, l - 1, xc), out)
+            assert exact(download(h, out, K), o.prolongate(l, xc))
+            rc = h.vector(l - 1)
+            gmg.restrict_residual(h, l, upload(h, l, x), rc)
+            assert exact(download(h, rc, K), o.restrict_residual(l, x))
+
+
+@pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
+def test_vcycle_and_solve_bit_exact(system, kind):
+    h, o, levels, setups, K, L = (system[k] for k in ("h", "o", "levels", "setups", "K", "L"))
+    c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
+    b = [s.b for s in setups]
+    x0 = [s.x0 for s in setups]
+    x = upload(h, L - 1, x0)
+    bd = upload(h, L - 1, b)
+    gmg.v_cycle(h, x, bd, c)
+    xo, _ = o.v_cycle(x0, b, c)
+    assert exact(download(h, x, K), xo)
+    x = upload(h, L - 1, x0)
+    st = gmg.solve_outer(h, x, bd, c)
+    xs, res, ost, rc = o.solve_outer(x0, b, c)
+    assert rc == 0 and st.converged
+    assert st.iterations == ost.iterations
+    np.testing.assert_allclose(st.residuals, res, rtol=1e-12)
+    assert exact(download(h, x, K), xs)
+    assert st.final_residual <= 1e-10 * st.initial_residual
+
+
+def test_coarse_solve_matches_oracle(system):
+    h, o, levels, K = system["h"], system["o"], system["levels"], system["K"]
+    lv = [s[0] for s in levels]
+    b = key_noise(lv, 5)
+    x0 = [np.zeros(l.n) for l in lv]
+    xd, bd = upload(h, 0, x0), upload(h, 0, b)
+    st = gmg.coarse_solve(h, 0, xd, bd, 1e-12, 20000)
+    xo, ost = o.coarse_solve(0, x0, b, 1e-12, 20000)
+    assert st.iterations == ost.iterations and st.converged == bool(ost.converged)
+    assert st.initial_residual == ost.initial_residual and st.final_residual == ost.final_residual
+    assert exact(download(h, xd, K), xo)
+
+
+def test_reference_level_data_bit_exact(cuda, ref_lib):
+    """The drop-in path: the reference's own CSR / P / channels (host order, class-sorted,
+    Z-order first touch) through the GPU library; solve_outer must reproduce the
+    reference's residual history and solution bit for bit (Jacobi, C1 = 32^3)."""
+    for K in (1, 2, 8):
+        R = ref_lib.build(3, 2, 5 if K == 1 else 4, K)
+        levels = [[lv.to_level_arrays() for lv in R.ranks[r]] for r in range(K)]
+        h = gmg.Hierarchy(levels)
+        c = cfg(gmg.PF_SMOOTHER_JACOBI)
+        x = upload(h, h.finest, R.x0)
+        b = upload(h, h.finest, R.b)
+        st = gmg.solve_outer(h, x, b, c)
+        xr, resr, sr = ref_lib.run(3, 2, h.n_levels, K, smoother=0, pre=2, post=2, outer_tol=1e-10)
+        assert st.iterations == sr["iterations"]
+        np.testing.assert_allclose(st.residuals, resr, rtol=1e-13, atol=0)
+        assert exact(download(h, x, K), xr), f"K={K}: solution differs from the reference"
+
+
+def test_structured_solution_matches_reference_by_key(cuda, ref_lib):
+    """Product setup + GPU solve vs the reference's solve, compared per carrier key:
+    identical cycle count, residual history within 1e-9, solution within 1e-12."""
+    for K, L in ((1, 5), (8, 4), (4, 4)):
+        setups, levels = structured(3, 2, L, K)
+        h = gmg.Hierarchy(levels)
+        x = upload(h, L - 1, [s.x0 for s in setups])
+        b = upload(h, L - 1, [s.b for s in setups])
+        st = gmg.solve_outer(h, x, b, cfg())
+        R = ref_lib.build(3, 2, L, K)
+        xr, resr, sr = ref_lib.run(3, 2, L, K, smoother=0, pre=2, post=2, outer_tol=1e-10)
+        assert st.iterations == sr["iterations"]
+        np.testing.assert_allclose(st.residuals, resr, rtol=1e-9)
+        got = keyed([s[-1] for s in levels], download(h, x, K))
+        want = keyed([R.ranks[r][-1].to_level_arrays() for r in range(K)], xr)
+        assert got.keys() == want.keys()
+        diff = max(abs(got[k] - want[k]) for k in want)
+        assert diff <= 1e-12 * max(abs(v) for v in want.values())
+
+
+def test_host_entry_point_matches_device_solve(cuda):
+    setups, levels = structured(3, 2, 5, 1)
+    h = gmg.Hierarchy(levels)
+    c = cfg()
+    x = upload(h, 4, [setups[0].x0])
+    st = gmg.solve_outer(h, x, upload(h, 4, [setups[0].b]), c)
+    xh = [setups[0].x0.copy()]
+    st2 = gmg.solve_outer_host(h, xh, [setups[0].b], c)
+    assert st2.iterations == st.iterations
+    assert np.array_equal(xh[0], x.download())
+
+
+def test_errors_are_raised(cuda):
+    setups, levels = structured(3, 2, 3, 1)
+    h = gmg.Hierarchy(levels)
+    x = upload(h, 2, [setups[0].x0])
+    b = upload(h, 2, [setups[0].b])
+    with pytest.raises(gmg.NoConvergenceError):
+        gmg.solve_outer(h, x, b, cfg(tol=1e-14, max_cycles=1))
+    with pytest.raises(_lib.InvalidArgument):
+        gmg.spmv(h, 2, h.vector(1), h.vector(2))
+    bad = levels[0][2].normalized()
+    bad.vals = bad.vals.copy()
+    for k in range(bad.row_offsets[0], bad.row_offsets[1]):
+        if bad.cols[k] == 0:
+            bad.vals[k] = 0.0
+    lv = list(levels[0])
+    lv[2] = bad
+    with pytest.raises(gmg.SingularDiagonalError):
+        gmg.Hierarchy([lv])
