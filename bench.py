@@ -1,0 +1,329 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 GMG V-cycle hot path (BASELINE.json metric on configs[1] = C2).
+
+One step = one complete solve_outer (multigrid.cpp:210-246) of the C2 problem — 3D Q1
+Poisson on 128^3 cells (2,146,689 DOFs), 7 levels from 2^3, f = 3 pi^2 sin sin sin,
+g = 0, V(2,2) damped Jacobi omega = 0.8, stop at 1e-10 relative residual — from x0 = 0.
+value = DOFs/s = n_global * steps / (device time of the steps), max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N > 1 runs under torchrun (one process per GPU, NCCL halo exchange and allreduce),
+partitioning the same global problem into N boxes (strong scaling).  --impl
+reference times the reference's own CPU solver (oracle/_ref, the unmodified
+/root/reference/proj library) on the host cores on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(dim=3, n_coarse=2, levels=7, pre=2, post=2, omega=0.8, tol=1e-10)
+METRIC = "GMG solve DOFs/s (solve_outer to 1e-10 rel. residual, V(2,2) damped Jacobi w=0.8)"
+CONFIG = {
+    "workload": "C2: 3D Poisson -Lap u = f, unit cube, 128^3 hex cells (2,146,689 DOFs), conforming "
+                "Q1, fp64, 7 levels from 2^3, V(2,2) damped Jacobi w=0.8, coarse GS, stop at 1e-10",
+    "n_dofs": 2146689,
+    "levels": 7,
+    "cells": "128^3",
+    "smoother": "damped_jacobi_0.8",
+    "l2_flush": "no flush: the finest-level operator (0.69 GB) and the whole hierarchy (~0.8 GB) "
+                "exceed the 126 MB L2, so every step streams the matrices from HBM",
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join("/tmp", f"pf_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 7 or not f[0].isdigit():
+                    continue
+                sm.append(int(f[0]))
+                mx = int(f[1])
+                for n, v in zip(names, f[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        except OSError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ncu_traffic():
+    """DRAM bytes per finest-level Jacobi launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s.get("k_jacobi_c2", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(steps_hint: int = 1):
+    """The reference CPU solver (oracle/_ref) on this host, bounded to one solve of C2."""
+    from oracle import ref
+    ranks = max(1, min(8, os.cpu_count() or 1))
+    if ref.available():
+        r = ref.bench(3, 2, WORKLOAD["levels"], ranks, smoother=0, damping=WORKLOAD["omega"],
+                      pre=2, post=2, outer_tol=WORKLOAD["tol"], warmup=0, steps=steps_hint)
+        t = float(min(r["step_seconds"]))
+        return {"value": r["n_global"] / t, "unit": "DOF/s", "cores": ranks, "kind": "reference",
+                "sample": f"{steps_hint} full solve_outer of C2 (128^3, {r['iterations']} V(2,2) "
+                          f"Jacobi cycles) on {ranks} reference ranks (threads); setup "
+                          f"{r['setup_seconds']:.1f}s excluded",
+                "solve_seconds": t}
+    from oracle.restated import Oracle
+    from paper_1609_04809_b200.levels import StructuredSetup
+    from paper_1609_04809_b200.gmg import MultigridConfig, SmootherConfig
+    s = StructuredSetup(3, 2, WORKLOAD["levels"], 1, 0)
+    o = Oracle([s.levels])
+    cfg = MultigridConfig(smoother=SmootherConfig(kind=0, damping=0.8), pre_smooth=2, post_smooth=2,
+                          outer_tol=1e-10)
+    t0 = time.perf_counter()
+    _, res, st, _ = o.solve_outer([s.x0], [s.b], cfg)
+    t = time.perf_counter() - t0
+    return {"value": s.n_global / t, "unit": "DOF/s", "cores": 1, "kind": "port",
+            "sample": f"1 solve_outer of C2 ({st.iterations} cycles) with the C restatement",
+            "solve_seconds": t}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU solver, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparfem_ref.so not built"}))
+        return
+    ranks = max(1, min(8, os.cpu_count() or 1))
+    r = ref.bench(3, 2, WORKLOAD["levels"], ranks, smoother=0, damping=WORKLOAD["omega"], pre=2, post=2,
+                  outer_tol=WORKLOAD["tol"], warmup=args.warmup, steps=args.steps)
+    total = float(sum(r["step_seconds"]))
+    value = r["n_global"] * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic manufactured problem (f = 3 pi^2 sin sin sin, g = 0)",
+        "config": dict(CONFIG, parallelism=f"{ranks} reference ranks (std::thread) on host cores"),
+        "cycles": r["iterations"],
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": ranks, "kind": "reference",
+                         "sample": f"{args.steps} full C2 solves after {args.warmup} warm-up, "
+                                   f"setup {r['setup_seconds']:.1f}s excluded"},
+        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+
+    from paper_1609_04809_b200 import gmg
+    from paper_1609_04809_b200.levels import StructuredSetup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    W = WORKLOAD
+    t0 = time.time()
+    setup = StructuredSetup(W["dim"], W["n_coarse"], W["levels"], world, rank)
+    h = gmg.Hierarchy([setup.levels], device=local, rank_base=rank, world_size=world)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(gmg.Hierarchy.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        h.init_nccl(bytes(uid.cpu().numpy().tobytes()))
+    setup_s = time.time() - t0
+    top = h.finest
+    cfg = gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=gmg.PF_SMOOTHER_JACOBI, damping=W["omega"]),
+                              pre_smooth=W["pre"], post_smooth=W["post"], outer_tol=W["tol"])
+    x0 = h.vector(top, setup.x0)
+    b = h.vector(top, setup.b)
+    x = h.vector(top)
+    stream = torch.cuda.ExternalStream(h.stream_handle(), device=torch.device("cuda", local))
+
+    def step(c):
+        x.copy_from(x0)
+        return gmg.solve_outer(h, x, b, c)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def timed(c, steps):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st = None
+        for _ in range(steps):
+            st = step(c)
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, st
+
+    for _ in range(args.warmup):
+        st = step(cfg)
+    n0 = h.launch_count()
+    with Clocks(local) as clk:
+        ms, st = timed(cfg, args.steps)
+    launches = h.launch_count() - n0
+    clocks = clk.summary()
+    value = setup.n_global * args.steps / (ms / 1e3)
+
+    # e2e: the same solve through the host-buffer entry point (pinned host x0/b in,
+    # solution out, copies inside the timed region)
+    xh = torch.empty(len(setup.x0), dtype=torch.float64).pin_memory().numpy()
+    bh = torch.from_numpy(setup.b.copy()).pin_memory().numpy()
+    for _ in range(max(1, args.warmup)):
+        xh[:] = setup.x0
+        gmg.solve_outer_host(h, [xh], [bh], cfg)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        xh[:] = setup.x0
+        gmg.solve_outer_host(h, [xh], [bh], cfg)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = setup.n_global * args.steps / (e2e_ms / 1e3)
+
+    # dominant kernel: finest-level Jacobi sweep (4 of the ~5.5 matrix passes per cycle)
+    sweep_ms, sweep_bytes = h.time_sweep(top, gmg.PF_SMOOTHER_JACOBI, 50)
+    sor_ms, _ = h.time_sweep(top, gmg.PF_SMOOTHER_MULTICOLOR_SOR, 20)
+    vcycle_ms = h.time_vcycle(x, b, cfg, 20)
+    peak, peak_src = peaks()
+    achieved = sweep_bytes / (sweep_ms / 1e3) / 1e9
+
+    # multicolour SOR w=1.2 variant of the same config (BASELINE configs[1])
+    sor = gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=gmg.PF_SMOOTHER_MULTICOLOR_SOR, damping=1.2),
+                              pre_smooth=2, post_smooth=2, outer_tol=W["tol"])
+    for _ in range(2):
+        st_sor = step(sor)
+    sor_ms_total, st_sor = timed(sor, max(3, args.steps // 2))
+    sor_steps = max(3, args.steps // 2)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline()
+        except Exception as e:  # reported, never fatal for the GPU number
+            cpu = {"value": None, "unit": "DOF/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic manufactured problem (f = 3 pi^2 sin sin sin, g = 0), product setup",
+        "config": dict(CONFIG, parallelism=f"{world} box subdomain(s), one per GPU" if world > 1 else "1 GPU"),
+        "cycles": st.iterations, "final_rel_residual": st.final_residual / st.initial_residual,
+        "vcycle_ms": vcycle_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(),
+                     "kernel": "k_jacobi (finest-level damped-Jacobi sweep, SELL-32 fp64)",
+                     "kernel_us": sweep_ms * 1e3, "algorithmic_bytes_per_launch": sweep_bytes,
+                     "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "DOF/s", "h2d_bytes_per_step": 16 * len(setup.x0),
+                "d2h_bytes_per_step": 8 * len(setup.x0), "ms_per_step": e2e_ms / args.steps},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "setup_seconds": setup_s,
+        "variants": {"multicolor_sor_1.2": {
+            "value": setup.n_global * sor_steps / (sor_ms_total / 1e3), "unit": "DOF/s",
+            "cycles": st_sor.iterations, "ms_per_step": sor_ms_total / sor_steps,
+            "sweep_us": sor_ms * 1e3,
+            "sweep_frac": sweep_bytes / (sor_ms / 1e3) / 1e9 / peak}},
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

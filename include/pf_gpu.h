@@ -173,6 +173,8 @@ pf_status pf_vector_destroy(pf_vector* v);
 pf_status pf_vector_upload(pf_vector* v, int subdomain, const double* host, int64_t n);
 pf_status pf_vector_download(const pf_vector* v, int subdomain, double* host, int64_t n);
 pf_status pf_vector_fill(pf_vector* v, double value);
+/* dst = src (same level), on the device. */
+pf_status pf_vector_copy(const pf_vector* src, pf_vector* dst);
 pf_status pf_host_alloc(void** out, int64_t bytes);
 pf_status pf_host_free(void* p);
 
@@ -246,6 +248,10 @@ pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double*
 /* Mean time of one full V-cycle (graph replay) over `iters` cycles, CUDA events. */
 pf_status pf_time_vcycle(pf_hierarchy* h, pf_vector* x, const pf_vector* b,
                          const pf_multigrid_config* cfg, int iters, double* mean_ms);
+
+/* The cudaStream_t (as void*) every operation of this hierarchy is issued on, so a
+ * caller can bracket work with its own CUDA events on the right stream. */
+pf_status pf_hierarchy_stream(const pf_hierarchy* h, void** stream);
 
 /* Level geometry as uploaded (for diagnostics and tests). */
 pf_status pf_level_info(const pf_hierarchy* h, int level, int subdomain, int64_t* n_dofs,

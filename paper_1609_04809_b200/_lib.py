@@ -99,11 +99,11 @@ EXPORTS = [
     "pf_hierarchy_create", "pf_hierarchy_set_level", "pf_hierarchy_finalize", "pf_nccl_unique_id",
     "pf_hierarchy_init_nccl", "pf_hierarchy_destroy", "pf_hierarchy_device_bytes",
     "pf_vector_create", "pf_vector_destroy", "pf_vector_upload", "pf_vector_download",
-    "pf_vector_fill", "pf_host_alloc", "pf_host_free", "pf_spmv", "pf_residual_norm", "pf_smooth",
+    "pf_vector_fill", "pf_vector_copy", "pf_host_alloc", "pf_host_free", "pf_spmv", "pf_residual_norm", "pf_smooth",
     "pf_coarse_solve", "pf_prolongate", "pf_restrict_residual", "pf_update_master_slave",
     "pf_update_halo1", "pf_update_halo2", "pf_allreduce_sum", "pf_v_cycle", "pf_solve_outer",
     "pf_solve_outer_host", "pf_launch_count", "pf_reset_launch_count", "pf_time_sweep",
-    "pf_time_vcycle", "pf_level_info",
+    "pf_time_vcycle", "pf_hierarchy_stream", "pf_level_info",
     "pf_setup_create", "pf_setup_destroy", "pf_setup_level", "pf_setup_level_keys",
     "pf_setup_rhs", "pf_setup_counts", "pf_setup_seconds",
 ]
@@ -141,6 +141,7 @@ def lib():
         "pf_vector_upload": [P, C.c_int, P, C.c_int64],
         "pf_vector_download": [P, C.c_int, P, C.c_int64],
         "pf_vector_fill": [P, C.c_double],
+        "pf_vector_copy": [P, P],
         "pf_host_alloc": [PP, C.c_int64],
         "pf_host_free": [P],
         "pf_spmv": [P, C.c_int, P, P],
@@ -162,6 +163,7 @@ def lib():
         "pf_time_sweep": [P, C.c_int, C.c_int, C.c_int, dp, dp],
         "pf_time_vcycle": [P, P, P, C.POINTER(MultigridConfig), C.c_int, dp],
         "pf_level_info": [P, C.c_int, C.c_int, i64p, i64p, i64p, i64p],
+        "pf_hierarchy_stream": [P, PP],
         "pf_setup_create": [C.c_int] * 6 + [PP],
         "pf_setup_destroy": [P],
         "pf_setup_level": [P, C.c_int, C.POINTER(LevelDesc)],

@@ -987,6 +987,16 @@ pf_status pf_vector_fill(pf_vector* v, double value) {
   PF_API_END
 }
 
+pf_status pf_vector_copy(const pf_vector* src, pf_vector* dst) {
+  PF_API_BEGIN
+  if (!src || !dst) invalid("null vector");
+  if (src->h != dst->h || src->level != dst->level) invalid("vectors of different levels");
+  PF_CUDA(cudaSetDevice(src->h->device));
+  enq_copy(src->h, src->cur(), dst->cur(), src->total);
+  sync(src->h);
+  PF_API_END
+}
+
 pf_status pf_host_alloc(void** out, int64_t bytes) {
   PF_API_BEGIN
   if (!out || bytes < 0) invalid("bad argument");
@@ -1268,6 +1278,13 @@ pf_status pf_time_vcycle(pf_hierarchy* h, pf_vector* x, const pf_vector* b, cons
   float ms = 0;
   PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   *mean_ms = ms / iters;
+  PF_API_END
+}
+
+pf_status pf_hierarchy_stream(const pf_hierarchy* h, void** stream) {
+  PF_API_BEGIN
+  if (!h || !stream) invalid("null argument");
+  *stream = static_cast<void*>(h->stream);
   PF_API_END
 }
 

@@ -108,6 +108,10 @@ class DeviceVector:
         _lib.check(_lib.lib().pf_vector_fill(self._p, value))
         return self
 
+    def copy_from(self, src: "DeviceVector") -> "DeviceVector":
+        _lib.check(_lib.lib().pf_vector_copy(src._p, self._p))
+        return self
+
     def close(self):
         if self._p:
             _lib.lib().pf_vector_destroy(self._p)
@@ -186,6 +190,12 @@ class Hierarchy:
         _lib.check(_lib.lib().pf_level_info(self._h, level, sub, C.byref(a), C.byref(b), C.byref(c),
                                             C.byref(d)))
         return dict(n_dofs=a.value, n_own=b.value, nnz=c.value, n_colors=d.value)
+
+    def stream_handle(self) -> int:
+        """cudaStream_t of this hierarchy (an int for torch.cuda.ExternalStream)."""
+        out = C.c_void_p()
+        _lib.check(_lib.lib().pf_hierarchy_stream(self._h, C.byref(out)))
+        return out.value or 0
 
     def launch_count(self) -> int:
         out = C.c_int64()
