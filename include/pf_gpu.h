@@ -158,7 +158,23 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h);
  * rank 0, broadcast by the caller. */
 pf_status pf_nccl_unique_id(void* out, int nbytes);
 pf_status pf_hierarchy_init_nccl(pf_hierarchy* h, const void* unique_id, int nbytes);
+/* Multi-process: level 0 (coarsest) of every rank r in [0, world_size), set before
+ * pf_hierarchy_finalize.  Each GPU replays the reference's communicating coarse
+ * Gauss-Seidel of all ranks on this replica after one allgather of the coarse rhs,
+ * instead of one allreduce and two halo exchanges per coarse iteration; the result is
+ * the same bit for bit (same sequential order, same exchange order). */
+pf_status pf_hierarchy_set_coarse_replica(pf_hierarchy* h, int rank, const pf_level_desc* desc);
 pf_status pf_hierarchy_destroy(pf_hierarchy* h);
+
+/* Single-GPU test bench of the multi-process path: `world_size` single-subdomain
+ * hierarchies on one device, each driven by its own host thread, exchange through a
+ * shared loopback hub (device copies ordered by CUDA events) instead of NCCL.  Every
+ * pack / unpack / accumulate / allgather / replicated-coarse code path is the one NCCL
+ * runs; only the transport differs.  A rank that never reaches an exchange raises
+ * PF_ERR_TRANSPORT after the watchdog (transport.cpp:44-65 semantics). */
+pf_status pf_loopback_create(int world_size, void** hub);
+pf_status pf_loopback_destroy(void* hub);
+pf_status pf_hierarchy_init_loopback(pf_hierarchy* h, void* hub);
 
 /* Device bytes held by the hierarchy (matrices, transfers, plans, scratch). */
 pf_status pf_hierarchy_device_bytes(const pf_hierarchy* h, int64_t* out);

@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstring>
 #include <string>
 
@@ -85,7 +86,7 @@ std::unique_ptr<Nccl> nccl_init(int rank, int world, const void* id, int nbytes)
 }
 
 void Nccl::group_start() { ck(api().GroupStart(), "ncclGroupStart"); }
-void Nccl::group_end() { ck(api().GroupEnd(), "ncclGroupEnd"); }
+void Nccl::group_end(cudaStream_t) { ck(api().GroupEnd(), "ncclGroupEnd"); }
 void Nccl::send(const double* buf, int64_t count, int peer, cudaStream_t s) {
   ck(api().Send(buf, static_cast<size_t>(count), ncclFloat64, peer, static_cast<ncclComm_t>(comm), s),
      "ncclSend");
@@ -106,6 +107,109 @@ void Nccl::check_async() {
 }
 Nccl::~Nccl() {
   if (comm) api().CommDestroy(static_cast<ncclComm_t>(comm));
+}
+
+// ---------------------------------------------------------------- loopback --
+
+LoopbackHub::LoopbackHub(int w) : world(w), posts(static_cast<size_t>(w)) {
+  for (Post& p : posts) {
+    cuda_check(cudaEventCreateWithFlags(&p.ready, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming), "cudaEventCreate");
+  }
+}
+
+LoopbackHub::~LoopbackHub() {
+  for (Post& p : posts) {
+    if (p.ready) cudaEventDestroy(p.ready);
+    if (p.done) cudaEventDestroy(p.done);
+  }
+}
+
+// Host barrier of all loopback ranks with the reference fabric's watchdog
+// (transport.cpp:44-65): a missing rank surfaces as TransportError.
+void LoopbackHub::barrier() {
+  std::unique_lock<std::mutex> lock(mu);
+  if (aborted) throw Error(PF_ERR_TRANSPORT, "loopback fabric aborted");
+  const int64_t gen = generation;
+  if (++arrived == world) {
+    arrived = 0;
+    ++generation;
+    cv.notify_all();
+    return;
+  }
+  if (!cv.wait_for(lock, std::chrono::duration<double>(watchdog_s),
+                   [&] { return generation != gen || aborted; })) {
+    aborted = true;
+    cv.notify_all();
+    throw Error(PF_ERR_TRANSPORT, "loopback watchdog: a rank did not reach the exchange");
+  }
+  if (aborted) throw Error(PF_ERR_TRANSPORT, "loopback fabric aborted");
+}
+
+void LoopbackHub::abort() {
+  std::lock_guard<std::mutex> lock(mu);
+  aborted = true;
+  cv.notify_all();
+}
+
+void Loopback::group_start() {
+  auto& p = hub->posts[static_cast<size_t>(rank)];
+  p.sends.clear();
+  p.recvs.clear();
+}
+
+void Loopback::send(const double* buf, int64_t count, int peer, cudaStream_t) {
+  hub->posts[static_cast<size_t>(rank)].sends.push_back({peer, buf, nullptr, count});
+}
+
+void Loopback::recv(double* buf, int64_t count, int peer, cudaStream_t) {
+  hub->posts[static_cast<size_t>(rank)].recvs.push_back({peer, nullptr, buf, count});
+}
+
+// B1: every rank's sends are posted and their data ready-event recorded; each rank pulls
+// its receives behind the senders' events; B2: done-events recorded; every sender waits
+// for its receivers before it may overwrite its send buffers; B3: posts may be reused.
+void Loopback::group_end(cudaStream_t s) {
+  auto& mine = hub->posts[static_cast<size_t>(rank)];
+  cuda_check(cudaEventRecord(mine.ready, s), "cudaEventRecord");
+  hub->barrier();
+  for (const auto& r : mine.recvs) {
+    const auto& src = hub->posts[static_cast<size_t>(r.peer)];
+    const LoopbackHub::Msg* m = nullptr;
+    for (const auto& snd : src.sends)
+      if (snd.peer == rank) m = &snd;
+    if (!m || m->n != r.n) {
+      hub->abort();
+      throw Error(PF_ERR_TRANSPORT, "loopback: unmatched receive from rank " + std::to_string(r.peer));
+    }
+    cuda_check(cudaStreamWaitEvent(s, src.ready, 0), "cudaStreamWaitEvent");
+    cuda_check(cudaMemcpyAsync(r.dst, m->src, sizeof(double) * static_cast<size_t>(r.n),
+                               cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync");
+  }
+  cuda_check(cudaEventRecord(mine.done, s), "cudaEventRecord");
+  hub->barrier();
+  for (const auto& snd : mine.sends)
+    cuda_check(cudaStreamWaitEvent(s, hub->posts[static_cast<size_t>(snd.peer)].done, 0), "cudaStreamWaitEvent");
+  hub->barrier();
+}
+
+void Loopback::allgather(const double* send, double* recv, int64_t count, cudaStream_t s) {
+  auto& mine = hub->posts[static_cast<size_t>(rank)];
+  mine.gather_src = send;
+  cuda_check(cudaEventRecord(mine.ready, s), "cudaEventRecord");
+  hub->barrier();
+  for (int q = 0; q < hub->world; ++q) {
+    const auto& src = hub->posts[static_cast<size_t>(q)];
+    cuda_check(cudaStreamWaitEvent(s, src.ready, 0), "cudaStreamWaitEvent");
+    cuda_check(cudaMemcpyAsync(recv + static_cast<int64_t>(q) * count, src.gather_src,
+                               sizeof(double) * static_cast<size_t>(count), cudaMemcpyDeviceToDevice, s),
+               "cudaMemcpyAsync");
+  }
+  cuda_check(cudaEventRecord(mine.done, s), "cudaEventRecord");
+  hub->barrier();
+  for (int q = 0; q < hub->world; ++q)
+    cuda_check(cudaStreamWaitEvent(s, hub->posts[static_cast<size_t>(q)].done, 0), "cudaStreamWaitEvent");
+  hub->barrier();
 }
 
 }  // namespace pf

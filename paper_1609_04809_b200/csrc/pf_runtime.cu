@@ -279,27 +279,30 @@ const HostChannel* find_channel(const HostLevel& H, int kind, int peer) {
   return nullptr;
 }
 
-void build_plans(pf_hierarchy* h, int l) {
-  Level& L = h->levels[l];
-  const bool local = h->world == h->n_sub;
+// Exchange plans of one level from the per-subdomain channel lists.  local: every peer
+// is one of the subdomains in H (ranks rank_base + s); else one subdomain whose peers
+// live in other processes (NCCL segments).
+void build_exchange(const std::vector<HostLevel>& H, const std::vector<DevLevel>& D, int rank_base,
+                    bool local, std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS>& scatter, ExchangePlan& A) {
+  const int n_sub = static_cast<int>(H.size());
   for (int kind = 0; kind < PF_NUM_CHANNEL_KINDS; ++kind) {
-    ExchangePlan& P = L.scatter[kind];
+    ExchangePlan& P = scatter[kind];
     if (local) {
       std::vector<int32_t> dst, src;
-      for (int s = 0; s < h->n_sub; ++s) {
-        const int R = h->rank_base + s;
-        for (const HostChannel& c : L.host[s].channels) {
+      for (int s = 0; s < n_sub; ++s) {
+        const int R = rank_base + s;
+        for (const HostChannel& c : H[s].channels) {
           if (c.kind != kind || c.recv.empty()) continue;
-          const int p = c.peer - h->rank_base;
-          if (p < 0 || p >= h->n_sub || p == s) invalid("channel peer " + std::to_string(c.peer) + " out of range");
-          const HostChannel* pc = find_channel(L.host[p], kind, R);
+          const int p = c.peer - rank_base;
+          if (p < 0 || p >= n_sub || p == s) invalid("channel peer " + std::to_string(c.peer) + " out of range");
+          const HostChannel* pc = find_channel(H[p], kind, R);
           if (!pc || pc->send.size() != c.recv.size())
             throw Error(PF_ERR_TRANSPORT, "channel lists of kind " + std::to_string(kind) +
                                               " between ranks " + std::to_string(c.peer) + " and " +
                                               std::to_string(R) + " do not pair up");
           for (size_t i = 0; i < c.recv.size(); ++i) {
-            dst.push_back(static_cast<int32_t>(L.sub[s].offset + L.sub[s].perm[c.recv[i]]));
-            src.push_back(static_cast<int32_t>(L.sub[p].offset + L.sub[p].perm[pc->send[i]]));
+            dst.push_back(static_cast<int32_t>(D[s].offset + D[s].perm[c.recv[i]]));
+            src.push_back(static_cast<int32_t>(D[p].offset + D[p].perm[pc->send[i]]));
           }
         }
       }
@@ -307,17 +310,17 @@ void build_plans(pf_hierarchy* h, int l) {
       P.dst.upload(dst);
       P.src.upload(src);
     } else {
-      const DevLevel& D = L.sub[0];
+      const DevLevel& D0 = D[0];
       std::vector<int32_t> pk, up;
-      for (const HostChannel& c : L.host[0].channels) {
+      for (const HostChannel& c : H[0].channels) {
         if (c.kind != kind) continue;
         if (!c.send.empty()) {
           P.send_segs.push_back({c.peer, static_cast<int64_t>(pk.size()), static_cast<int64_t>(c.send.size())});
-          for (int32_t d : c.send) pk.push_back(D.perm[d]);
+          for (int32_t d : c.send) pk.push_back(D0.perm[d]);
         }
         if (!c.recv.empty()) {
           P.recv_segs.push_back({c.peer, static_cast<int64_t>(up.size()), static_cast<int64_t>(c.recv.size())});
-          for (int32_t d : c.recv) up.push_back(D.perm[d]);
+          for (int32_t d : c.recv) up.push_back(D0.perm[d]);
         }
       }
       P.n = static_cast<int64_t>(up.size());
@@ -328,29 +331,28 @@ void build_plans(pf_hierarchy* h, int l) {
     }
   }
   // master/slave accumulate: slaves push v[recv_dofs], masters add in ascending peer order
-  ExchangePlan& A = L.accumulate;
   std::map<int32_t, std::vector<int32_t>> contrib;  // master dst -> sources, peer-ascending
   if (local) {
-    for (int s = 0; s < h->n_sub; ++s) {
-      const int R = h->rank_base + s;
+    for (int s = 0; s < n_sub; ++s) {
+      const int R = rank_base + s;
       std::vector<const HostChannel*> ms;
-      for (const HostChannel& c : L.host[s].channels)
+      for (const HostChannel& c : H[s].channels)
         if (c.kind == PF_CH_MASTER_SLAVE && !c.send.empty()) ms.push_back(&c);
       std::sort(ms.begin(), ms.end(), [](const HostChannel* a, const HostChannel* b) { return a->peer < b->peer; });
       for (const HostChannel* c : ms) {
-        const int p = c->peer - h->rank_base;
-        const HostChannel* pc = find_channel(L.host[p], PF_CH_MASTER_SLAVE, R);
+        const int p = c->peer - rank_base;
+        const HostChannel* pc = find_channel(H[p], PF_CH_MASTER_SLAVE, R);
         if (!pc || pc->recv.size() != c->send.size())
           throw Error(PF_ERR_TRANSPORT, "master/slave lists do not pair up");
         for (size_t i = 0; i < c->send.size(); ++i)
-          contrib[static_cast<int32_t>(L.sub[s].offset + L.sub[s].perm[c->send[i]])].push_back(
-              static_cast<int32_t>(L.sub[p].offset + L.sub[p].perm[pc->recv[i]]));
+          contrib[static_cast<int32_t>(D[s].offset + D[s].perm[c->send[i]])].push_back(
+              static_cast<int32_t>(D[p].offset + D[p].perm[pc->recv[i]]));
       }
     }
   } else {
-    const DevLevel& D = L.sub[0];
+    const DevLevel& D0 = D[0];
     std::vector<const HostChannel*> ms;
-    for (const HostChannel& c : L.host[0].channels)
+    for (const HostChannel& c : H[0].channels)
       if (c.kind == PF_CH_MASTER_SLAVE) ms.push_back(&c);
     std::sort(ms.begin(), ms.end(), [](const HostChannel* a, const HostChannel* b) { return a->peer < b->peer; });
     std::vector<int32_t> pk;
@@ -358,12 +360,12 @@ void build_plans(pf_hierarchy* h, int l) {
     for (const HostChannel* c : ms) {
       if (!c->recv.empty()) {  // slave side: push partial sums to the master
         A.send_segs.push_back({c->peer, static_cast<int64_t>(pk.size()), static_cast<int64_t>(c->recv.size())});
-        for (int32_t d : c->recv) pk.push_back(D.perm[d]);
+        for (int32_t d : c->recv) pk.push_back(D0.perm[d]);
       }
       if (!c->send.empty()) {  // master side
         A.recv_segs.push_back({c->peer, rpos, static_cast<int64_t>(c->send.size())});
         for (size_t i = 0; i < c->send.size(); ++i)
-          contrib[D.perm[c->send[i]]].push_back(static_cast<int32_t>(rpos + static_cast<int64_t>(i)));
+          contrib[D0.perm[c->send[i]]].push_back(static_cast<int32_t>(rpos + static_cast<int64_t>(i)));
         rpos += static_cast<int64_t>(c->send.size());
       }
     }
@@ -384,6 +386,84 @@ void build_plans(pf_hierarchy* h, int l) {
   A.acc_dst.upload(dsts);
 }
 
+void build_plans(pf_hierarchy* h, int l) {
+  Level& L = h->levels[l];
+  build_exchange(L.host, L.sub, h->rank_base, h->world == h->n_sub, L.scatter, L.accumulate);
+}
+
+HostLevel parse_desc(const pf_level_desc& dd, int me, int world, bool need_p) {
+  const pf_level_desc* d = &dd;
+  if (d->n_dofs < 0 || d->n_own_dofs < 0 || d->n_own_dofs > d->n_dofs) invalid("bad dof counts");
+  if (!d->row_offsets || (d->n_dofs > 0 && (!d->owns_row))) invalid("missing level arrays");
+  HostLevel H;
+  H.set = true;
+  H.n = d->n_dofs;
+  H.n_own = d->n_own_dofs;
+  const int64_t nnz = d->row_offsets[d->n_dofs];
+  if (d->row_offsets[0] != 0 || nnz < 0) invalid("row offsets must start at 0");
+  if (nnz > 0 && (!d->col_indices || !d->values)) invalid("missing matrix arrays");
+  H.rowptr.assign(d->row_offsets, d->row_offsets + d->n_dofs + 1);
+  H.cols.assign(d->col_indices, d->col_indices + nnz);
+  H.vals.assign(d->values, d->values + nnz);
+  H.owns_row.assign(d->owns_row, d->owns_row + d->n_dofs);
+  if (d->is_dirichlet) H.is_dir.assign(d->is_dirichlet, d->is_dirichlet + d->n_dofs);
+  else H.is_dir.assign(static_cast<size_t>(d->n_dofs), 0);
+  if (d->color) H.color.assign(d->color, d->color + d->n_own_dofs);
+  for (int i = 0; i < d->n_channels; ++i) {
+    const pf_channel_desc& c = d->channels[i];
+    if (c.kind < 0 || c.kind >= PF_NUM_CHANNEL_KINDS) invalid("bad channel kind");
+    if (c.peer < 0 || c.peer >= world || c.peer == me) invalid("bad channel peer");
+    HostChannel hc;
+    hc.kind = c.kind;
+    hc.peer = c.peer;
+    hc.send.assign(c.send_dofs, c.send_dofs + c.n_send);
+    hc.recv.assign(c.recv_dofs, c.recv_dofs + c.n_recv);
+    for (int32_t v : hc.send)
+      if (v < 0 || v >= d->n_dofs) invalid("channel send dof out of range");
+    for (int32_t v : hc.recv)
+      if (v < 0 || v >= d->n_dofs) invalid("channel recv dof out of range");
+    H.channels.push_back(std::move(hc));
+  }
+  std::sort(H.channels.begin(), H.channels.end(), [](const HostChannel& a, const HostChannel& b) {
+    return a.kind != b.kind ? a.kind < b.kind : a.peer < b.peer;
+  });
+  if (need_p) {
+    if (!d->p_offsets) invalid("level > 0 needs a prolongation map");
+    H.p_off.assign(d->p_offsets, d->p_offsets + d->n_dofs + 1);
+    const int64_t pn = H.p_off.back();
+    H.p_col.assign(d->p_cols, d->p_cols + pn);
+    H.p_w.assign(d->p_weights, d->p_weights + pn);
+  }
+  return H;
+}
+
+void build_replica(pf_hierarchy* h) {
+  auto& R = h->rep;
+  if (R.host.size() != static_cast<size_t>(h->world))
+    state("multi-process hierarchy needs pf_hierarchy_set_coarse_replica for every rank");
+  R.sub.resize(static_cast<size_t>(h->world));
+  int64_t stride = 1;
+  for (int r = 0; r < h->world; ++r) {
+    if (!R.host[r].set) state("coarse replica of rank " + std::to_string(r) + " not set");
+    build_dev_level(R.host[r], R.sub[r], 0);
+    stride = std::max<int64_t>(stride, R.sub[r].n);
+  }
+  R.stride = stride;
+  for (int r = 0; r < h->world; ++r) R.sub[r].offset = r * stride;
+  const DevLevel& mine = h->levels[0].sub[0];
+  if (R.sub[h->rank_base].n != mine.n || R.sub[h->rank_base].perm != mine.perm)
+    invalid("coarse replica of this rank differs from its level 0");
+  build_exchange(R.host, R.sub, 0, true, R.scatter, R.acc);
+  std::vector<CoarseSub> cs;
+  for (DevLevel& D : R.sub) cs.push_back(CoarseSub{view(D.A), D.d_perm.p, D.n_own, D.offset});
+  R.subs.upload(cs);
+  R.x.alloc(stride * h->world);
+  R.b.alloc(stride * h->world);
+  R.send.alloc(stride);
+  PF_CUDA(cudaMemset(R.send.p, 0, sizeof(double) * stride));
+  R.active = true;
+}
+
 // ------------------------------------------------------------------ enqueue --
 
 void enq_scatter(pf_hierarchy* h, int l, int kind, double* v) {
@@ -397,13 +477,14 @@ void enq_scatter(pf_hierarchy* h, int l, int kind, double* v) {
            static_cast<const int32_t*>(P.dst.p), v, static_cast<int32_t>(P.n));
     return;
   }
-  if (P.send_segs.empty() && P.recv_segs.empty()) return;
+  // collective on every rank, even one with nothing to move on this channel
+  if (!h->xport) state("multi-process hierarchy used before pf_hierarchy_init_nccl");
   launch(grid_for(P.pack_idx.n), kBlock, k_pack, static_cast<const double*>(v),
          static_cast<const int32_t*>(P.pack_idx.p), P.sendbuf.p, static_cast<int32_t>(P.pack_idx.n));
-  h->nccl->group_start();
-  for (const PeerSeg& s : P.send_segs) h->nccl->send(P.sendbuf.p + s.off, s.len, s.peer, h->stream);
-  for (const PeerSeg& s : P.recv_segs) h->nccl->recv(P.recvbuf.p + s.off, s.len, s.peer, h->stream);
-  h->nccl->group_end();
+  h->xport->group_start();
+  for (const PeerSeg& s : P.send_segs) h->xport->send(P.sendbuf.p + s.off, s.len, s.peer, h->stream);
+  for (const PeerSeg& s : P.recv_segs) h->xport->recv(P.recvbuf.p + s.off, s.len, s.peer, h->stream);
+  h->xport->group_end(h->stream);
   launch(grid_for(P.unpack_idx.n), kBlock, k_unpack, static_cast<const double*>(P.recvbuf.p),
          static_cast<const int32_t*>(P.unpack_idx.p), v, static_cast<int32_t>(P.unpack_idx.n));
 }
@@ -418,13 +499,13 @@ void enq_accumulate(pf_hierarchy* h, int l, double* v) {
            static_cast<const int32_t*>(A.acc_dst.p), v, A.n_masters);
     return;
   }
-  if (A.send_segs.empty() && A.recv_segs.empty()) return;
+  if (!h->xport) state("multi-process hierarchy used before pf_hierarchy_init_nccl");
   launch(grid_for(A.pack_idx.n), kBlock, k_pack, static_cast<const double*>(v),
          static_cast<const int32_t*>(A.pack_idx.p), A.sendbuf.p, static_cast<int32_t>(A.pack_idx.n));
-  h->nccl->group_start();
-  for (const PeerSeg& s : A.send_segs) h->nccl->send(A.sendbuf.p + s.off, s.len, s.peer, h->stream);
-  for (const PeerSeg& s : A.recv_segs) h->nccl->recv(A.recvbuf.p + s.off, s.len, s.peer, h->stream);
-  h->nccl->group_end();
+  h->xport->group_start();
+  for (const PeerSeg& s : A.send_segs) h->xport->send(A.sendbuf.p + s.off, s.len, s.peer, h->stream);
+  for (const PeerSeg& s : A.recv_segs) h->xport->recv(A.recvbuf.p + s.off, s.len, s.peer, h->stream);
+  h->xport->group_end(h->stream);
   launch(grid_for(A.n_masters), kBlock, k_unpack_accumulate, static_cast<const double*>(A.recvbuf.p),
          static_cast<const int32_t*>(A.acc_off.p), static_cast<const int32_t*>(A.acc_src.p),
          static_cast<const int32_t*>(A.acc_dst.p), v, A.n_masters);
@@ -442,7 +523,8 @@ void enq_allreduce(pf_hierarchy* h, Level& L, bool take_sqrt) {
     launch(1, 32, k_ordered_sum, static_cast<const double*>(L.sumsq.p), h->n_sub, L.norm.p,
            take_sqrt ? 1 : 0);
   } else {
-    h->nccl->allgather(L.sumsq.p, L.sumsq.p + 1, 1, h->stream);
+    if (!h->xport) state("multi-process hierarchy used before pf_hierarchy_init_nccl");
+    h->xport->allgather(L.sumsq.p, L.sumsq.p + 1, 1, h->stream);
     launch(1, 32, k_ordered_sum, static_cast<const double*>(L.sumsq.p + 1), h->world, L.norm.p,
            take_sqrt ? 1 : 0);
   }
@@ -541,17 +623,48 @@ void enq_restrict(pf_hierarchy* h, int fine, const double* rf, double* bc, doubl
   }
 }
 
-void enq_coarse(pf_hierarchy* h, int l, double* x, const double* b, double tol, int max_iter) {
+// coarse_solve on level l.  cycle_mode: x enters as zero and update_halo2 follows
+// (multigrid.cpp:153-158); returns true when that halo update was already done.
+bool enq_coarse(pf_hierarchy* h, int l, double* x, const double* b, double tol, int max_iter,
+                bool cycle_mode) {
   Level& L = h->levels[l];
-  if (h->world != h->n_sub)
-    state("multi-process coarse solve needs the replicated coarse level (not built)");
   auto launch = launcher(h);
-  const ExchangePlan& ms = L.scatter[PF_CH_MASTER_SLAVE];
-  const ExchangePlan& h1 = L.scatter[PF_CH_HALO1];
-  launch(1, 32, k_coarse_gs, L.coarse_subs.p, h->n_sub, x, b, static_cast<const int32_t*>(ms.dst.p),
+  if (h->world == h->n_sub) {
+    const ExchangePlan& ms = L.scatter[PF_CH_MASTER_SLAVE];
+    const ExchangePlan& h1 = L.scatter[PF_CH_HALO1];
+    launch(1, 32, k_coarse_gs, static_cast<const CoarseSub*>(L.coarse_subs.p), h->n_sub, x, b,
+           static_cast<const int32_t*>(ms.dst.p), static_cast<const int32_t*>(ms.src.p),
+           static_cast<int32_t>(ms.n), static_cast<const int32_t*>(h1.dst.p),
+           static_cast<const int32_t*>(h1.src.p), static_cast<int32_t>(h1.n), tol, max_iter,
+           L.coarse_stats.p);
+    return false;
+  }
+  if (l != 0) state("multi-process coarse solve runs on level 0 only");
+  auto& R = h->rep;
+  const DevLevel& D = L.sub[0];
+  if (!h->xport) state("multi-process hierarchy used before pf_hierarchy_init_nccl");
+  // every rank's coarse rhs (and start vector) on every GPU: one allgather each
+  enq_copy(h, b, R.send.p, D.n);
+  h->xport->allgather(R.send.p, R.b.p, R.stride, h->stream);
+  if (cycle_mode) {
+    PF_CUDA(cudaMemsetAsync(R.x.p, 0, sizeof(double) * R.stride * h->world, h->stream));
+  } else {
+    enq_copy(h, x, R.send.p, D.n);
+    h->xport->allgather(R.send.p, R.x.p, R.stride, h->stream);
+  }
+  const ExchangePlan& ms = R.scatter[PF_CH_MASTER_SLAVE];
+  const ExchangePlan& h1 = R.scatter[PF_CH_HALO1];
+  const ExchangePlan& h2 = R.scatter[PF_CH_HALO2];
+  launch(1, 32, k_coarse_gs, static_cast<const CoarseSub*>(R.subs.p), h->world, R.x.p,
+         static_cast<const double*>(R.b.p), static_cast<const int32_t*>(ms.dst.p),
          static_cast<const int32_t*>(ms.src.p), static_cast<int32_t>(ms.n),
          static_cast<const int32_t*>(h1.dst.p), static_cast<const int32_t*>(h1.src.p),
          static_cast<int32_t>(h1.n), tol, max_iter, L.coarse_stats.p);
+  if (cycle_mode && h2.n > 0)
+    launch(grid_for(h2.n), kBlock, k_copy_idx, static_cast<const int32_t*>(h2.src.p),
+           static_cast<const int32_t*>(h2.dst.p), R.x.p, static_cast<int32_t>(h2.n));
+  enq_copy(h, R.x.p + h->rank_base * R.stride, x, D.n);
+  return cycle_mode;
 }
 
 // cycle (multigrid.cpp:150-190)
@@ -559,8 +672,8 @@ void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_
   Level& L = h->levels[l];
   double* x = xv->cur();
   if (l == 0) {
-    enq_coarse(h, 0, x, b, cfg.coarse_tol, cfg.coarse_max_iter);
-    enq_scatter(h, 0, PF_CH_HALO2, x);
+    if (!enq_coarse(h, 0, x, b, cfg.coarse_tol, cfg.coarse_max_iter, true))
+      enq_scatter(h, 0, PF_CH_HALO2, x);
     return;
   }
   pf_smoother_config pre = cfg.smoother;
@@ -588,7 +701,7 @@ void enq_vcycle(pf_hierarchy* h, pf_vector* x, const double* b, const pf_multigr
 
 void sync(pf_hierarchy* h) {
   PF_CUDA(cudaStreamSynchronize(h->stream));
-  if (h->nccl) h->nccl->check_async();
+  if (h->xport) h->xport->check_async();
 }
 
 double read_norm(pf_hierarchy* h, int l) {
@@ -663,9 +776,17 @@ void solve_outer_dev(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf
   s.converged = 1;
   if (r0 != 0.0) {
     s.converged = 0;
-    auto& g = outer_graph(h, x, b, cfg, true);
+    const bool eager = h->xport && !h->xport->capturable();
+    pf_hierarchy::GraphEntry* g = eager ? nullptr : &outer_graph(h, x, b, cfg, true);
     for (int outer = 1; outer <= cfg.outer_max_cycles; ++outer) {
-      graph_launch(h, g);
+      if (g) {
+        graph_launch(h, *g);
+      } else {
+        for (int j = 0; j < cfg.cycles; ++j) enq_vcycle(h, x, b->cur(), cfg);
+        enq_resnorm(h, top, x->cur(), b->cur());
+        PF_CUDA(cudaMemcpyAsync(h->pinned, h->levels[top].norm.p, sizeof(double),
+                                cudaMemcpyDeviceToHost, h->stream));
+      }
       sync(h);
       const double r = h->pinned[0];
       s.iterations = outer;
@@ -728,7 +849,7 @@ pf_hierarchy::~pf_hierarchy() {
     delete L.b;
   }
   levels.clear();
-  nccl.reset();
+  xport.reset();
   if (pinned) cudaFreeHost(pinned);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
@@ -811,49 +932,17 @@ pf_status pf_hierarchy_set_level(pf_hierarchy* h, int level, int sub, const pf_l
   if (h->finalized) state("hierarchy already finalized");
   if (level < 0 || level >= h->n_levels) invalid("level out of range");
   if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
-  if (d->n_dofs < 0 || d->n_own_dofs < 0 || d->n_own_dofs > d->n_dofs) invalid("bad dof counts");
-  if (!d->row_offsets || (d->n_dofs > 0 && (!d->owns_row))) invalid("missing level arrays");
-  HostLevel& H = h->levels[level].host[sub];
-  H = HostLevel{};
-  H.set = true;
-  H.n = d->n_dofs;
-  H.n_own = d->n_own_dofs;
-  const int64_t nnz = d->row_offsets[d->n_dofs];
-  if (d->row_offsets[0] != 0 || nnz < 0) invalid("row offsets must start at 0");
-  if (nnz > 0 && (!d->col_indices || !d->values)) invalid("missing matrix arrays");
-  H.rowptr.assign(d->row_offsets, d->row_offsets + d->n_dofs + 1);
-  H.cols.assign(d->col_indices, d->col_indices + nnz);
-  H.vals.assign(d->values, d->values + nnz);
-  H.owns_row.assign(d->owns_row, d->owns_row + d->n_dofs);
-  if (d->is_dirichlet) H.is_dir.assign(d->is_dirichlet, d->is_dirichlet + d->n_dofs);
-  else H.is_dir.assign(static_cast<size_t>(d->n_dofs), 0);
-  if (d->color) H.color.assign(d->color, d->color + d->n_own_dofs);
-  const int me = h->rank_base + sub;
-  for (int i = 0; i < d->n_channels; ++i) {
-    const pf_channel_desc& c = d->channels[i];
-    if (c.kind < 0 || c.kind >= PF_NUM_CHANNEL_KINDS) invalid("bad channel kind");
-    if (c.peer < 0 || c.peer >= h->world || c.peer == me) invalid("bad channel peer");
-    HostChannel hc;
-    hc.kind = c.kind;
-    hc.peer = c.peer;
-    hc.send.assign(c.send_dofs, c.send_dofs + c.n_send);
-    hc.recv.assign(c.recv_dofs, c.recv_dofs + c.n_recv);
-    for (int32_t v : hc.send)
-      if (v < 0 || v >= d->n_dofs) invalid("channel send dof out of range");
-    for (int32_t v : hc.recv)
-      if (v < 0 || v >= d->n_dofs) invalid("channel recv dof out of range");
-    H.channels.push_back(std::move(hc));
-  }
-  std::sort(H.channels.begin(), H.channels.end(), [](const HostChannel& a, const HostChannel& b) {
-    return a.kind != b.kind ? a.kind < b.kind : a.peer < b.peer;
-  });
-  if (level > 0) {
-    if (!d->p_offsets) invalid("level > 0 needs a prolongation map");
-    H.p_off.assign(d->p_offsets, d->p_offsets + d->n_dofs + 1);
-    const int64_t pn = H.p_off.back();
-    H.p_col.assign(d->p_cols, d->p_cols + pn);
-    H.p_w.assign(d->p_weights, d->p_weights + pn);
-  }
+  h->levels[level].host[sub] = parse_desc(*d, h->rank_base + sub, h->world, level > 0);
+  PF_API_END
+}
+
+pf_status pf_hierarchy_set_coarse_replica(pf_hierarchy* h, int rank, const pf_level_desc* d) {
+  PF_API_BEGIN
+  if (!h || !d) invalid("null argument");
+  if (h->finalized) state("hierarchy already finalized");
+  if (rank < 0 || rank >= h->world) invalid("rank out of range");
+  if (h->rep.host.empty()) h->rep.host.resize(static_cast<size_t>(h->world));
+  h->rep.host[rank] = parse_desc(*d, rank, h->world, false);
   PF_API_END
 }
 
@@ -892,6 +981,7 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
       L.coarse_subs.upload(cs);
     }
   }
+  if (h->world != h->n_sub) build_replica(h);
   h->staging.alloc(max_total);
   for (int l = 0; l < h->n_levels; ++l) {
     h->levels[l].x = new_vector(h, l);
@@ -914,7 +1004,35 @@ pf_status pf_hierarchy_init_nccl(pf_hierarchy* h, const void* id, int nbytes) {
   if (!h) invalid("null hierarchy");
   if (h->world == h->n_sub) state("NCCL is only used when ranks live in separate processes");
   PF_CUDA(cudaSetDevice(h->device));
-  h->nccl = pf::nccl_init(h->rank_base, h->world, id, nbytes);
+  if (h->xport) state("transport already initialized");
+  h->xport = pf::nccl_init(h->rank_base, h->world, id, nbytes);
+  PF_API_END
+}
+
+pf_status pf_loopback_create(int world_size, void** hub) {
+  PF_API_BEGIN
+  if (!hub || world_size < 1) invalid("bad argument");
+  *hub = new pf::LoopbackHub(world_size);
+  PF_API_END
+}
+
+pf_status pf_loopback_destroy(void* hub) {
+  PF_API_BEGIN
+  delete static_cast<pf::LoopbackHub*>(hub);
+  PF_API_END
+}
+
+pf_status pf_hierarchy_init_loopback(pf_hierarchy* h, void* hub) {
+  PF_API_BEGIN
+  if (!h || !hub) invalid("null argument");
+  if (h->world == h->n_sub) state("loopback is only used when ranks live in separate hierarchies");
+  if (h->xport) state("transport already initialized");
+  auto* H = static_cast<pf::LoopbackHub*>(hub);
+  if (H->world != h->world) invalid("loopback hub size differs from the world size");
+  auto t = std::make_unique<pf::Loopback>();
+  t->hub = H;
+  t->rank = h->rank_base;
+  h->xport = std::move(t);
   PF_API_END
 }
 
@@ -1055,7 +1173,7 @@ pf_status pf_coarse_solve(pf_hierarchy* h, int level, pf_vector* x, const pf_vec
   check_vec(h, b, level, "b");
   PF_CUDA(cudaSetDevice(h->device));
   const double t0 = wall_now();
-  enq_coarse(h, level, x->cur(), b->cur(), tol, max_iter);
+  enq_coarse(h, level, x->cur(), b->cur(), tol, max_iter, false);
   double st[4];
   PF_CUDA(cudaMemcpyAsync(h->pinned, h->levels[level].coarse_stats.p, 4 * sizeof(double),
                           cudaMemcpyDeviceToHost, h->stream));

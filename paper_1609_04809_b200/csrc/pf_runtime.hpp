@@ -146,7 +146,7 @@ struct Level {
   pf_vector* b = nullptr;
 };
 
-struct Nccl;  // pf_nccl.cpp
+struct Transport;  // pf_nccl.hpp
 
 }  // namespace pf
 
@@ -169,12 +169,25 @@ struct pf_hierarchy {
   pf::DevBuf<double> staging;  // host-order staging for uploads/downloads
   double* pinned = nullptr;    // pinned host slots for scalars read back each cycle
   int64_t launches = 0;
-  std::unique_ptr<pf::Nccl> nccl;
+  std::unique_ptr<pf::Transport> xport;  // multi-process exchanges (NCCL or loopback)
   // graph cache of one outer cycle (cycles x V-cycle + finest residual norm)
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     int64_t kernels = 0;
   };
   std::map<std::string, GraphEntry> graphs;
+  // Multi-process runs: level 0 of every rank, replicated on each GPU, so the coarse
+  // solve (solvers.cpp:70-92, which communicates every iteration) runs without any
+  // per-iteration collective; one allgather of the coarse rhs feeds it.
+  struct Replica {
+    bool active = false;
+    std::vector<pf::HostLevel> host;  // per world rank
+    std::vector<pf::DevLevel> sub;
+    int64_t stride = 0;               // rank r's entries at [r * stride, r * stride + n_r)
+    std::array<pf::ExchangePlan, PF_NUM_CHANNEL_KINDS> scatter;
+    pf::ExchangePlan acc;
+    pf::DevBuf<pf::CoarseSub> subs;
+    pf::DevBuf<double> x, b, send;
+  } rep;
   ~pf_hierarchy();
 };

@@ -124,6 +124,20 @@ class DeviceVector:
             pass
 
 
+class LoopbackHub:
+    """Shared transport of several single-subdomain hierarchies on one GPU (the
+    single-GPU test bench of the multi-process path, include/pf_gpu.h)."""
+
+    def __init__(self, world_size: int):
+        self._p = C.c_void_p()
+        _lib.check(_lib.lib().pf_loopback_create(world_size, C.byref(self._p)))
+
+    def close(self):
+        if self._p:
+            _lib.lib().pf_loopback_destroy(self._p)
+            self._p = C.c_void_p()
+
+
 class Hierarchy:
     """Device mirror of MultigridHierarchy (multigrid.hpp:43-51).
 
@@ -133,7 +147,7 @@ class Hierarchy:
     """
 
     def __init__(self, levels, device: int = 0, rank_base: int = 0, world_size: int | None = None,
-                 finalize: bool = True):
+                 finalize: bool = True, coarse_replicas=None):
         n_sub = len(levels)
         n_levels = len(levels[0])
         world = n_sub if world_size is None else world_size
@@ -147,6 +161,11 @@ class Hierarchy:
                 d, keep = lv.desc()
                 _lib.check(L.pf_hierarchy_set_level(self._h, l, s, C.byref(d)))
                 del keep
+        if coarse_replicas is not None:  # level 0 of every rank (multi-process runs)
+            for r, lv in enumerate(coarse_replicas):
+                d, keep = lv.desc()
+                _lib.check(L.pf_hierarchy_set_coarse_replica(self._h, r, C.byref(d)))
+                del keep
         if finalize:
             self.finalize()
 
@@ -156,6 +175,9 @@ class Hierarchy:
     def init_nccl(self, unique_id: bytes):
         buf = C.create_string_buffer(unique_id, len(unique_id))
         _lib.check(_lib.lib().pf_hierarchy_init_nccl(self._h, buf, len(unique_id)))
+
+    def init_loopback(self, hub: "LoopbackHub"):
+        _lib.check(_lib.lib().pf_hierarchy_init_loopback(self._h, hub._p))
 
     @staticmethod
     def nccl_unique_id() -> bytes:

@@ -188,3 +188,60 @@ def test_errors_are_raised(cuda):
     lv[2] = bad
     with pytest.raises(gmg.SingularDiagonalError):
         gmg.Hierarchy([lv])
+
+
+def _run_ranks(K, body):
+    """Run body(rank) on K host threads (ctypes releases the GIL inside the library)."""
+    import threading
+    out, errs = [None] * K, []
+
+    def wrap(r):
+        try:
+            out[r] = body(r)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+    th = [threading.Thread(target=wrap, args=(r,)) for r in range(K)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("K,L", [(2, 4), (4, 4), (8, 3), (3, 3)])
+@pytest.mark.parametrize("kind", [gmg.PF_SMOOTHER_JACOBI, gmg.PF_SMOOTHER_MULTICOLOR_SOR], ids=["jacobi", "sor"])
+def test_multiprocess_path_loopback(cuda, K, L, kind):
+    """The one-subdomain-per-process code path (pack/unpack kernels, segment transport,
+    master accumulate from a receive buffer, allgather-based allreduce, replicated coarse
+    solve) with the loopback transport standing in for NCCL: K hierarchies on K threads
+    must reproduce the oracle's K-rank solve bit for bit."""
+    setups, levels = structured(3, 2, L, K)
+    c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
+    replicas = [s[0] for s in levels]
+    hub = gmg.LoopbackHub(K)
+
+    def body(r):
+        h = gmg.Hierarchy([levels[r]], rank_base=r, world_size=K, coarse_replicas=replicas)
+        h.init_loopback(hub)
+        x = h.vector(L - 1, setups[r].x0)
+        b = h.vector(L - 1, setups[r].b)
+        st = gmg.solve_outer(h, x, b, c)
+        rn = gmg.residual_norm(h, L - 1, x, b)
+        v = h.vector(L - 2, key_noise([levels[r][L - 2]], 3)[0])
+        gmg.update_master_slave(h, L - 2, v, gmg.PF_UPDATE_ACCUMULATE_THEN_SCATTER)
+        return st, x.download(), rn, v.download()
+
+    res = _run_ranks(K, body)
+    hub.close()
+    o = Oracle(levels)
+    xs, resid, ost, rc = o.solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
+    acc = o.update_master_slave(L - 2, key_noise([lv[L - 2] for lv in levels], 3), 1)
+    for r in range(K):
+        st, x, rn, v = res[r]
+        assert st.iterations == ost.iterations
+        np.testing.assert_allclose(st.residuals, resid, rtol=1e-12)
+        assert np.array_equal(x, xs[r]), f"rank {r}"
+        assert np.array_equal(v, acc[r]), f"accumulate rank {r}"
+        assert rn == pytest.approx(res[0][2], rel=0, abs=0)
