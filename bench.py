@@ -182,7 +182,11 @@ def run_b200(args):
     W = WORKLOAD
     t0 = time.time()
     setup = StructuredSetup(W["dim"], W["n_coarse"], W["levels"], world, rank)
-    h = gmg.Hierarchy([setup.levels], device=local, rank_base=rank, world_size=world)
+    # multi-process: every rank's level 0 (27 coarse dofs) for the replicated coarse solve
+    replicas = ([StructuredSetup(W["dim"], W["n_coarse"], 1, world, q).levels[0] for q in range(world)]
+                if world > 1 else None)
+    h = gmg.Hierarchy([setup.levels], device=local, rank_base=rank, world_size=world,
+                      coarse_replicas=replicas)
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:

@@ -1,0 +1,112 @@
+"""CPU: the product's communication-free setup (include/pf_setup.h) reproduces the
+reference's setup pipeline (partition.cpp, fespace.cpp, femapper.cpp, assembly.cpp,
+multigrid.cpp:35-72) per carrier key: dof classes, owns_row, the ordered channel key
+lists, the matrix pattern and values, the prolongation map, the rhs and start vector —
+against the live compiled reference and against the committed golden structure tables.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from paper_1609_04809_b200 import _lib
+from paper_1609_04809_b200.levels import StructuredSetup
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def compare(R, S):
+    K, levels = R.K, R.n_levels
+    for r in range(K):
+        for l in range(levels):
+            a, b = R.ranks[r][l], S[r].levels[l]
+            ka, kb = [tuple(k) for k in a.keys], [tuple(k) for k in b.keys]
+            ia, ib = {k: i for i, k in enumerate(ka)}, {k: i for i, k in enumerate(kb)}
+            assert set(ka) == set(kb), (r, l)
+            assert a.n_own == b.n_own
+            for k in ka:
+                assert a.class_of[ia[k]] == b.class_of[ib[k]], (r, l, k)
+                assert a.owns_row[ia[k]] == b.owns_row[ib[k]], (r, l, k)
+            cha = {(c.kind, c.peer): ([ka[i] for i in c.send], [ka[i] for i in c.recv])
+                   for c in a.channels if len(c.send) or len(c.recv)}
+            chb = {(c.kind, c.peer): ([kb[i] for i in c.send], [kb[i] for i in c.recv])
+                   for c in b.channels if len(c.send) or len(c.recv)}
+            assert cha == chb, (r, l)
+
+            def mat(x, kk):
+                return {(kk[i], kk[x.cols[e]]): x.vals[e]
+                        for i in range(x.n) for e in range(x.row_offsets[i], x.row_offsets[i + 1])}
+            ma, mb = mat(a.to_level_arrays(), ka), mat(b, kb)
+            assert ma.keys() == mb.keys()
+            scale = max(abs(v) for v in ma.values())
+            assert max(abs(ma[k] - mb[k]) for k in ma) <= 1e-14 * scale
+            if l > 0:
+                kca = [tuple(k) for k in R.ranks[r][l - 1].keys]
+                kcb = [tuple(k) for k in S[r].levels[l - 1].keys]
+                pa = {ka[i]: {kca[a.p_cols[e]]: a.p_w[e] for e in range(a.p_offsets[i], a.p_offsets[i + 1])}
+                      for i in range(a.n_dofs)}
+                pb = {kb[i]: {kcb[b.p_cols[e]]: b.p_w[e] for e in range(b.p_offsets[i], b.p_offsets[i + 1])}
+                      for i in range(b.n)}
+                assert pa == pb
+        ka = [tuple(k) for k in R.ranks[r][-1].keys]
+        ib = {tuple(k): i for i, k in enumerate(S[r].levels[-1].keys)}
+        bb = np.array([S[r].b[ib[k]] for k in ka])
+        assert np.abs(R.b[r] - bb).max() <= 1e-13 * max(np.abs(R.b[r]).max(), 1e-300)
+        assert np.array_equal(R.x0[r], np.array([S[r].x0[ib[k]] for k in ka]))
+
+
+@pytest.mark.parametrize("dim,nc,L,K,prob", [
+    (2, 2, 3, 1, 0), (2, 2, 3, 2, 0), (2, 4, 3, 4, 0), (2, 4, 2, 6, 0), (3, 2, 3, 1, 0),
+    (3, 2, 3, 2, 0), (3, 2, 3, 4, 0), (3, 2, 4, 8, 0), (3, 2, 2, 3, 0), (3, 2, 3, 8, 1),
+    (2, 3, 3, 5, 1), (3, 3, 2, 7, 2)])
+def test_setup_matches_reference(ref_lib, dim, nc, L, K, prob):
+    R = ref_lib.build(dim, nc, L, K, prob)
+    S = [StructuredSetup(dim, nc, L, K, r, prob) for r in range(K)]
+    compare(R, S)
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "*.npz"))), ids=os.path.basename)
+def test_setup_structure_matches_golden(path):
+    """Class counts, n_own, nnz and channel sizes per rank and level equal the reference's
+    (golden structure tables; no reference needed)."""
+    g = np.load(path)
+    if "structure" not in g.files:
+        pytest.skip("sweep fixture")
+    dim, nc, L, K, prob = (int(g[k]) for k in ("dim", "n_coarse", "levels", "K", "problem"))
+    if L > 5:
+        pytest.skip("C2 structure is checked on the GPU box (setup takes seconds)")
+    S = [StructuredSetup(dim, nc, L, K, r, prob) for r in range(K)]
+    rows = []
+    chans = []
+    for r in range(K):
+        for l, lv in enumerate(S[r].levels):
+            rows.append([r, l, lv.n, lv.n_own, int(lv.row_offsets[-1])] +
+                        np.bincount(lv.class_of, minlength=8).tolist())
+            for c in lv.channels:
+                chans.append([r, l, c.kind, c.peer, len(c.send), len(c.recv)])
+    assert np.array_equal(np.array(rows), g["structure"])
+    assert np.array_equal(np.array(chans).reshape(-1, 6), g["channels"])
+    assert S[0].n_global == int(g["n_global"])
+
+
+def test_setup_rejects_bad_arguments():
+    """Mirrors the reference's validation (mesh.cpp:11-14, partition.cpp:104-111)."""
+    with pytest.raises(_lib.InvalidArgument, match="dimension"):
+        StructuredSetup(7, 2, 2)
+    with pytest.raises(_lib.InvalidArgument, match="at least one cell per rank"):
+        StructuredSetup(3, 2, 2, n_ranks=9)
+    with pytest.raises(_lib.InvalidArgument):
+        StructuredSetup(3, 2, 0)
+
+
+def test_setup_counts_at_c1():
+    """C1 sizes of SURVEY.md §8: 35,937 DOFs, 29,791 own rows, 804,357 own-row nnz,
+    912,673 full nnz on one rank; colours are the 8 lattice parities."""
+    s = StructuredSetup(3, 2, 5)
+    top = s.levels[-1]
+    assert s.n_global == 35937 and top.n == 35937 and top.n_own == 29791
+    assert int(top.row_offsets[top.n_own]) == 804357 and int(top.row_offsets[-1]) == 912673
+    assert sorted(set(top.color.tolist())) == list(range(8))
+    k = top.keys[:top.n_own, 1:]
+    assert np.array_equal(top.color, (k[:, 0] & 1) * 4 + (k[:, 1] & 1) * 2 + (k[:, 2] & 1))
