@@ -1,0 +1,245 @@
+// pf_bottom.cuh — the bottom of the V-cycle in one cooperative persistent kernel.
+//
+// Levels 0..Lc of the hierarchy are tiny: at C2 they hold 27, 125, 729, 4,913 and
+// 35,937 dofs.  Run as separate launches, every phase of cycle() on them is one
+// latency-bound kernel (launch + a chain of dependent L2 round trips), so the five
+// bottom levels cost ~30 % of a V-cycle while holding 1.7 % of the dofs.  k_bottom runs
+// the whole of cycle(Lc) (multigrid.cpp:150-190) — pre-smoothing, halo refreshes,
+// residual, restriction, master/slave accumulate, the coarse Gauss-Seidel, prolongation,
+// post-smoothing — in one launch, with a grid barrier between dependent phases.  Every
+// phase runs the same per-row code as the standalone kernels (row_offdiag / row_dot,
+// separate rounding, reference entry order), so the result is bit-identical to the
+// multi-launch path; only the launch structure changes.
+//
+// The launch is cooperative (all blocks co-resident), which is what makes the grid
+// barrier legal; blocks never wait on another launch.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "pf_kernels.cuh"
+
+namespace pf {
+
+namespace cg = cooperative_groups;
+
+constexpr int kBotMaxLevels = 8;
+constexpr int kBotMaxSubs = 8;
+
+struct BotSub {
+  SellView A;
+  const int32_t* host_of_own;
+  const int32_t* color_start;  // n_colors + 1, subdomain-local device rows
+  const int64_t* p_off;        // P of this level (rows: this level; cols: parent, local)
+  const int32_t* p_col;
+  const double* p_w;
+  const int64_t* r_off;        // R to the parent (rows: parent, local; cols: this level, local)
+  const int32_t* r_col;
+  const double* r_w;
+  const uint8_t* is_dir;
+  int32_t n, n_own, n_colors;
+  int32_t off;                 // position in the level vectors
+};
+
+struct BotPlan {
+  const int32_t* dst;
+  const int32_t* src;
+  int32_t n;
+};
+
+struct BotLevel {
+  double* x;   // primary
+  double* xa;  // Jacobi ping-pong partner
+  double* b;
+  double* r;
+  int32_t total;
+  int32_t max_colors;
+  BotPlan ms, h1, h2;
+  const int32_t* acc_off;
+  const int32_t* acc_src;
+  const int32_t* acc_dst;
+  int32_t acc_n;
+};
+
+struct BotDesc {
+  int n_sub;
+  int n_levels;  // Lc + 1
+  const CoarseSub* coarse;  // level 0 in CoarseSub form
+  double* coarse_stats;
+  BotLevel lev[kBotMaxLevels];
+  BotSub sub[kBotMaxLevels][kBotMaxSubs];
+};
+
+struct BotCfg {
+  int kind, pre, post, local_sweeps, coarse_max_iter;
+  double omega, coarse_tol;
+};
+
+__device__ __forceinline__ int bot_find(const BotDesc& D, int l, int32_t row) {
+  int s = D.n_sub - 1;
+  while (s > 0 && row < D.sub[l][s].off) --s;
+  return s;
+}
+
+__device__ __forceinline__ void bot_copy_plan(const BotPlan& P, double* v, int64_t t, int64_t stride) {
+  for (int64_t i = t; i < P.n; i += stride) v[P.dst[i]] = v[P.src[i]];
+}
+
+__device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps, cg::grid_group& g,
+                           int64_t t, int64_t stride) {
+  const BotLevel& L = D.lev[l];
+  double* bufs[2] = {L.x, L.xa};
+  int cur = 0;
+  for (int sw = 0; sw < sweeps; ++sw) {
+    for (int loc = 0; loc < c.local_sweeps; ++loc) {
+      if (c.kind == 0) {  // damped Jacobi, ping-pong (k_jacobi)
+        const double* src = bufs[cur];
+        double* dst = bufs[cur ^ 1];
+        for (int64_t r = t; r < L.total; r += stride) {
+          const BotSub& S = D.sub[l][bot_find(D, l, static_cast<int32_t>(r))];
+          const int32_t lr = static_cast<int32_t>(r - S.off);
+          const double xo = src[r];
+          if (lr >= S.n_own) {
+            dst[r] = xo;
+            continue;
+          }
+          double acc = L.b[r], diag = 0.0;
+          row_offdiag<false>(S.A, lr, src + S.off, acc, diag);
+          dst[r] = __dadd_rn(__dmul_rn(1.0 - c.omega, xo), __ddiv_rn(__dmul_rn(c.omega, acc), diag));
+        }
+        cur ^= 1;
+        g.sync();
+      } else {  // coloured GS / SOR, in place (k_color_sweep)
+        const bool sor = c.kind == 2;
+        double* x = bufs[cur];
+        for (int col = 0; col < L.max_colors; ++col) {
+          for (int s = 0; s < D.n_sub; ++s) {
+            const BotSub& S = D.sub[l][s];
+            if (col >= S.n_colors) continue;
+            const int32_t r0 = S.color_start[col], r1 = S.color_start[col + 1];
+            double* xs = x + S.off;
+            const double* bs = L.b + S.off;
+            for (int64_t lr = r0 + t; lr < r1; lr += stride) {
+              const int32_t row = static_cast<int32_t>(lr);
+              double acc = bs[row], diag = 0.0;
+              row_offdiag<false>(S.A, row, xs, acc, diag);
+              xs[row] = sor ? __dadd_rn(__dmul_rn(1.0 - c.omega, xs[row]),
+                                        __ddiv_rn(__dmul_rn(c.omega, acc), diag))
+                            : __ddiv_rn(acc, diag);
+            }
+          }
+          g.sync();
+        }
+      }
+    }
+    if (L.ms.n) {
+      bot_copy_plan(L.ms, bufs[cur], t, stride);
+      g.sync();
+    }
+    if (L.h1.n) {
+      bot_copy_plan(L.h1, bufs[cur], t, stride);
+      g.sync();
+    }
+  }
+  if (cur) {
+    for (int64_t r = t; r < L.total; r += stride) L.x[r] = L.xa[r];
+    g.sync();
+  }
+}
+
+// master/slave AccumulateThenScatter on level l (fecomm.cpp:41-62)
+__device__ void bot_accumulate_scatter(const BotDesc& D, int l, double* v, cg::grid_group& g, int64_t t,
+                                       int64_t stride) {
+  const BotLevel& L = D.lev[l];
+  if (L.acc_n) {
+    for (int64_t m = t; m < L.acc_n; m += stride) {
+      double acc = v[L.acc_dst[m]];
+      for (int32_t e = L.acc_off[m]; e < L.acc_off[m + 1]; ++e) acc = __dadd_rn(acc, v[L.acc_src[e]]);
+      v[L.acc_dst[m]] = acc;
+    }
+    g.sync();
+  }
+  if (L.ms.n) {
+    bot_copy_plan(L.ms, v, t, stride);
+    g.sync();
+  }
+}
+
+// cycle(Lc) (multigrid.cpp:150-190) on levels 0..Lc.  On entry lev[Lc].b holds the
+// restricted residual (Dirichlet entries zeroed, before the master/slave accumulate when
+// `accumulate_top`) and lev[Lc].x is zero.
+__global__ void __launch_bounds__(kBlock) k_bottom(const BotDesc* __restrict__ Dp, BotCfg c,
+                                                   int accumulate_top) {
+  cg::grid_group g = cg::this_grid();
+  const BotDesc& D = *Dp;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int top = D.n_levels - 1;
+  if (accumulate_top) bot_accumulate_scatter(D, top, D.lev[top].b, g, t, stride);
+  // descend
+  for (int l = top; l >= 1; --l) {
+    const BotLevel& L = D.lev[l];
+    bot_smooth(D, l, c, c.pre, g, t, stride);
+    if (L.h2.n) {
+      bot_copy_plan(L.h2, L.x, t, stride);
+      g.sync();
+    }
+    // r = b - A x on every row (k_residual)
+    for (int64_t r = t; r < L.total; r += stride) {
+      const BotSub& S = D.sub[l][bot_find(D, l, static_cast<int32_t>(r))];
+      const int32_t lr = static_cast<int32_t>(r - S.off);
+      L.r[r] = __dsub_rn(L.b[r], row_dot<false, false>(S.A, lr, L.x + S.off, 0.0));
+    }
+    g.sync();
+    // b_c = R r, Dirichlet zeroed, x_c = 0 (k_restrict)
+    const BotLevel& C = D.lev[l - 1];
+    for (int64_t pr = t; pr < C.total; pr += stride) {
+      const int s = bot_find(D, l - 1, static_cast<int32_t>(pr));
+      const BotSub& F = D.sub[l][s];
+      const BotSub& Sc = D.sub[l - 1][s];
+      const int32_t lr = static_cast<int32_t>(pr - Sc.off);
+      double acc = 0.0;
+      for (int64_t e = F.r_off[lr], e1 = F.r_off[lr + 1]; e < e1; ++e)
+        acc = __dadd_rn(acc, __dmul_rn(F.r_w[e], L.r[F.off + F.r_col[e]]));
+      C.b[pr] = Sc.is_dir[lr] ? 0.0 : acc;
+      C.x[pr] = 0.0;
+    }
+    g.sync();
+    bot_accumulate_scatter(D, l - 1, C.b, g, t, stride);
+  }
+  // level 0: coarse_solve + update_halo2 (multigrid.cpp:153-158)
+  {
+    const BotLevel& L0 = D.lev[0];
+    if (t == 0)
+      coarse_gs_body(D.coarse, D.n_sub, L0.x, L0.b, L0.ms.dst, L0.ms.src, L0.ms.n, L0.h1.dst, L0.h1.src,
+                     L0.h1.n, c.coarse_tol, c.coarse_max_iter, D.coarse_stats);
+    g.sync();
+    if (L0.h2.n) {
+      bot_copy_plan(L0.h2, L0.x, t, stride);
+      g.sync();
+    }
+  }
+  // ascend
+  for (int l = 1; l <= top; ++l) {
+    const BotLevel& L = D.lev[l];
+    const BotLevel& C = D.lev[l - 1];
+    for (int64_t r = t; r < L.total; r += stride) {  // x += P x_c (k_prolong_add)
+      const int s = bot_find(D, l, static_cast<int32_t>(r));
+      const BotSub& S = D.sub[l][s];
+      const int32_t lr = static_cast<int32_t>(r - S.off);
+      const double* xc = C.x + D.sub[l - 1][s].off;
+      double acc = 0.0;
+      for (int64_t e = S.p_off[lr], e1 = S.p_off[lr + 1]; e < e1; ++e)
+        acc = __dadd_rn(acc, __dmul_rn(S.p_w[e], xc[S.p_col[e]]));
+      L.x[r] = __dadd_rn(L.x[r], acc);
+    }
+    g.sync();
+    bot_smooth(D, l, c, c.post, g, t, stride);
+    if (L.h2.n) {
+      bot_copy_plan(L.h2, L.x, t, stride);
+      g.sync();
+    }
+  }
+}
+
+}  // namespace pf

@@ -67,7 +67,7 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
 // acc := acc op sum_c a_rc x_c over all entries in stored order.
 //   kSubtract: acc -= a x   (residual_norm, linalg.cpp:64-73: acc starts at b)
 //   else:      acc += a x   (spmv, linalg.cpp:49-56: acc starts at 0)
-template <bool kSubtract>
+template <bool kSubtract, bool kReadOnlyX = true>
 __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const double* __restrict__ x,
                                           double acc) {
   const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
@@ -83,14 +83,15 @@ __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const 
       v[k] = ld_stream(A.vals + e);
     }
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) xv[k] = __ldg(x + c[k]);
+    for (int k = 0; k < kUnroll; ++k) xv[k] = kReadOnlyX ? __ldg(x + c[k]) : x[c[k]];
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k)
       acc = kSubtract ? __dsub_rn(acc, __dmul_rn(v[k], xv[k])) : __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
   }
   for (; j < len; ++j) {
     const int64_t e = base + static_cast<int64_t>(j) * kSlice;
-    const double p = __dmul_rn(ld_stream(A.vals + e), __ldg(x + ld_stream(A.cols + e)));
+    const int32_t c = ld_stream(A.cols + e);
+    const double p = __dmul_rn(ld_stream(A.vals + e), kReadOnlyX ? __ldg(x + c) : x[c]);
     acc = kSubtract ? __dsub_rn(acc, p) : __dadd_rn(acc, p);
   }
   return acc;
@@ -265,12 +266,11 @@ __global__ void __launch_bounds__(kBlock) k_restrict(const int64_t* __restrict__
 // ascending-rank sum; stop at <= tol * r0 or max_iter.  One thread: the coarse level of
 // the n_coarse=2 hierarchies holds one unknown, and a sequential sweep is the only way
 // to keep the reference's exact ordering.  stats: [iterations, converged, r0, final].
-__global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, double* x,
-                            const double* __restrict__ b, const int32_t* __restrict__ ms_dst,
-                            const int32_t* __restrict__ ms_src, int32_t ms_n,
-                            const int32_t* __restrict__ h1_dst, const int32_t* __restrict__ h1_src,
-                            int32_t h1_n, double tol, int32_t max_iter, double* stats) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void coarse_gs_body(const CoarseSub* __restrict__ subs, int n_sub, double* x,
+                               const double* __restrict__ b, const int32_t* __restrict__ ms_dst,
+                               const int32_t* __restrict__ ms_src, int32_t ms_n,
+                               const int32_t* __restrict__ h1_dst, const int32_t* __restrict__ h1_src,
+                               int32_t h1_n, double tol, int32_t max_iter, double* stats) {
   auto norm = [&]() {
     double total = 0.0;
     for (int s = 0; s < n_sub; ++s) {
@@ -329,6 +329,15 @@ __global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, doubl
     if (fr <= target) return;
   }
   stats[1] = 0;
+}
+
+__global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, double* x,
+                            const double* __restrict__ b, const int32_t* __restrict__ ms_dst,
+                            const int32_t* __restrict__ ms_src, int32_t ms_n,
+                            const int32_t* __restrict__ h1_dst, const int32_t* __restrict__ h1_src,
+                            int32_t h1_n, double tol, int32_t max_iter, double* stats) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  coarse_gs_body(subs, n_sub, x, b, ms_dst, ms_src, ms_n, h1_dst, h1_src, h1_n, tol, max_iter, stats);
 }
 
 // ------------------------------------------------------------- vector utilities --

@@ -14,12 +14,14 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <sstream>
 #include <string>
 #include <vector>
 
+#include "pf_bottom.cuh"
 #include "pf_kernels.cuh"
 #include "pf_nccl.hpp"
 #include "pf_runtime.hpp"
@@ -464,6 +466,74 @@ void build_replica(pf_hierarchy* h) {
   R.active = true;
 }
 
+// Levels whose total row count stays below PF_BOTTOM_ROWS (default 65536; 0 disables)
+// run as one cooperative kernel.  Only when every rank of the level lives on this device.
+void build_bottom(pf_hierarchy* h) {
+  int64_t limit = 65536;
+  if (const char* e = std::getenv("PF_BOTTOM_ROWS")) limit = std::atoll(e);
+  if (h->world != h->n_sub || h->n_sub > kBotMaxSubs || limit <= 0) return;
+  int top = -1;
+  for (int l = 0; l < h->n_levels - 1 && l < kBotMaxLevels; ++l)
+    if (h->levels[l].total <= limit) top = l;
+  if (top < 1) return;
+  BotDesc d;
+  std::memset(&d, 0, sizeof d);
+  d.n_sub = h->n_sub;
+  d.n_levels = top + 1;
+  d.coarse = h->levels[0].coarse_subs.p;
+  d.coarse_stats = h->levels[0].coarse_stats.p;
+  auto plan = [](const ExchangePlan& P) { return BotPlan{P.dst.p, P.src.p, static_cast<int32_t>(P.n)}; };
+  int64_t max_total = 0;
+  for (int l = 0; l <= top; ++l) {
+    Level& L = h->levels[l];
+    BotLevel& B = d.lev[l];
+    B.x = L.x->cur();
+    B.xa = L.x->alt();
+    B.b = L.b->cur();
+    B.r = L.r.p;
+    B.total = static_cast<int32_t>(L.total);
+    max_total = std::max(max_total, L.total);
+    B.ms = plan(L.scatter[PF_CH_MASTER_SLAVE]);
+    B.h1 = plan(L.scatter[PF_CH_HALO1]);
+    B.h2 = plan(L.scatter[PF_CH_HALO2]);
+    B.acc_off = L.accumulate.acc_off.p;
+    B.acc_src = L.accumulate.acc_src.p;
+    B.acc_dst = L.accumulate.acc_dst.p;
+    B.acc_n = L.accumulate.n_masters;
+    for (int s = 0; s < h->n_sub; ++s) {
+      DevLevel& D = L.sub[s];
+      BotSub& S = d.sub[l][s];
+      B.max_colors = std::max(B.max_colors, D.n_colors);
+      h->bot.color_bufs.emplace_back();
+      h->bot.color_bufs.back().upload(D.color_start);
+      S.A = view(D.A);
+      S.host_of_own = D.d_perm.p;
+      S.color_start = h->bot.color_bufs.back().p;
+      S.p_off = D.p_off.p;
+      S.p_col = D.p_col.p;
+      S.p_w = D.p_w.p;
+      S.r_off = D.r_off.p;
+      S.r_col = D.r_col.p;
+      S.r_w = D.r_w.p;
+      S.is_dir = D.d_is_dir.p;
+      S.n = D.n;
+      S.n_own = D.n_own;
+      S.n_colors = D.n_colors;
+      S.off = static_cast<int32_t>(D.offset);
+    }
+  }
+  PF_CUDA(cudaMalloc(&h->bot.desc, sizeof(BotDesc)));
+  PF_CUDA(cudaMemcpy(h->bot.desc, &d, sizeof d, cudaMemcpyHostToDevice));
+  int sms = 0, occ = 0;
+  PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+  PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bottom, kBlock, 0));
+  if (occ < 1) return;
+  const int64_t want = std::max<int64_t>(sms, (max_total + kBlock - 1) / kBlock);
+  h->bot.grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(occ) * sms));
+  h->bot.top = top;
+  h->bot.active = true;
+}
+
 // ------------------------------------------------------------------ enqueue --
 
 void enq_scatter(pf_hierarchy* h, int l, int kind, double* v) {
@@ -667,6 +737,24 @@ bool enq_coarse(pf_hierarchy* h, int l, double* x, const double* b, double tol, 
   return cycle_mode;
 }
 
+// cycle(bot.top) in one cooperative launch; lev[top].b holds the restricted residual
+// (before the master/slave accumulate when accumulate_top) and lev[top].x is zero.
+void enq_bottom(pf_hierarchy* h, const pf_multigrid_config& cfg, int accumulate_top) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(static_cast<unsigned>(h->bot.grid));
+  lc.blockDim = dim3(kBlock);
+  lc.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  const BotCfg c{cfg.smoother.kind, cfg.pre_smooth, cfg.post_smooth, cfg.smoother.local_sweeps,
+                 cfg.coarse_max_iter, cfg.smoother.damping, cfg.coarse_tol};
+  PF_CUDA(cudaLaunchKernelEx(&lc, k_bottom, static_cast<const BotDesc*>(h->bot.desc), c, accumulate_top));
+  ++*(g_capture_counter ? g_capture_counter : &h->launches);
+}
+
 // cycle (multigrid.cpp:150-190)
 void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_multigrid_config& cfg) {
   Level& L = h->levels[l];
@@ -683,8 +771,12 @@ void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_
   enq_residual(h, l, x, b, L.r.p);
   Level& Cl = h->levels[l - 1];
   enq_restrict(h, l, L.r.p, Cl.b->cur(), Cl.x->cur(), 1);
-  enq_update_ms(h, l - 1, Cl.b->cur(), PF_UPDATE_ACCUMULATE_THEN_SCATTER);
-  enq_cycle(h, l - 1, Cl.x, Cl.b->cur(), cfg);
+  if (h->bot.active && l - 1 == h->bot.top) {
+    enq_bottom(h, cfg, 1);  // accumulate, cycle(top) ... down to the coarse solve and back
+  } else {
+    enq_update_ms(h, l - 1, Cl.b->cur(), PF_UPDATE_ACCUMULATE_THEN_SCATTER);
+    enq_cycle(h, l - 1, Cl.x, Cl.b->cur(), cfg);
+  }
   enq_prolong(h, l, Cl.x->cur(), x, 1);
   pf_smoother_config post = cfg.smoother;
   post.sweeps = cfg.post_smooth;
@@ -828,6 +920,7 @@ void download_vec(pf_hierarchy* h, const pf_vector* v, int s, double* host, int6
 pf_vector* new_vector(pf_hierarchy* h, int level) {
   auto* v = new pf_vector;
   v->h = h;
+  v->device = h->device;
   v->level = level;
   v->total = h->levels[level].total;
   v->data.alloc(2 * std::max<int64_t>(v->total, 1));
@@ -849,6 +942,7 @@ pf_hierarchy::~pf_hierarchy() {
     delete L.b;
   }
   levels.clear();
+  if (bot.desc) cudaFree(bot.desc);
   xport.reset();
   if (pinned) cudaFreeHost(pinned);
   if (ev0) cudaEventDestroy(ev0);
@@ -856,7 +950,11 @@ pf_hierarchy::~pf_hierarchy() {
   if (stream) cudaStreamDestroy(stream);
 }
 
-#define PF_API_BEGIN try {
+// Clear any runtime error left on this thread by unrelated code, so the launch checks
+// below report only this call's failures.
+#define PF_API_BEGIN \
+  (void)cudaGetLastError(); \
+  try {
 #define PF_API_END                                   \
   }                                                  \
   catch (const pf::Error& e) {                       \
@@ -987,6 +1085,7 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
     h->levels[l].x = new_vector(h, l);
     h->levels[l].b = new_vector(h, l);
   }
+  build_bottom(h);
   for (Level& L : h->levels) L.host.clear();
   PF_CUDA(cudaStreamSynchronize(h->stream));
   h->finalized = true;
@@ -1069,7 +1168,7 @@ pf_status pf_vector_create(pf_hierarchy* h, int level, pf_vector** out) {
 
 pf_status pf_vector_destroy(pf_vector* v) {
   PF_API_BEGIN
-  if (v) cudaSetDevice(v->h->device);
+  if (v) cudaSetDevice(v->device);
   delete v;
   PF_API_END
 }

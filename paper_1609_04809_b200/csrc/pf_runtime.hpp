@@ -152,6 +152,7 @@ struct Transport;  // pf_nccl.hpp
 
 struct pf_vector {
   pf_hierarchy* h = nullptr;
+  int device = 0;  // kept here so destruction never reads the hierarchy
   int level = 0;
   pf::DevBuf<double> data;  // [2 * total]: primary then Jacobi ping-pong partner
   double* cur() const { return data.p; }
@@ -189,5 +190,13 @@ struct pf_hierarchy {
     pf::DevBuf<pf::CoarseSub> subs;
     pf::DevBuf<double> x, b, send;
   } rep;
+  // Levels 0..top of the V-cycle run in one cooperative kernel (pf_bottom.cuh).
+  struct Bottom {
+    bool active = false;
+    int top = -1;
+    int grid = 0;
+    void* desc = nullptr;  // device BotDesc
+    std::vector<pf::DevBuf<int32_t>> color_bufs;
+  } bot;
   ~pf_hierarchy();
 };

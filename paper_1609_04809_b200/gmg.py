@@ -25,6 +25,7 @@ reference's exception (``_lib.SingularDiagonalError``, ``_lib.NoConvergenceError
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -93,6 +94,7 @@ class DeviceVector:
         self.h, self.level = h, level
         self._p = C.c_void_p()
         _lib.check(_lib.lib().pf_vector_create(h._h, level, C.byref(self._p)))
+        h._vectors.add(self)
 
     def upload(self, values, sub: int = 0) -> "DeviceVector":
         a = np.ascontiguousarray(values, np.float64)
@@ -153,6 +155,7 @@ class Hierarchy:
         world = n_sub if world_size is None else world_size
         L = _lib.lib()
         self._h = C.c_void_p()
+        self._vectors = weakref.WeakSet()
         _lib.check(L.pf_hierarchy_create(device, n_levels, n_sub, rank_base, world, C.byref(self._h)))
         self.n_levels, self.n_sub, self.rank_base, self.world = n_levels, n_sub, rank_base, world
         self._sizes = [[lv.n for lv in sub] for sub in levels]
@@ -240,6 +243,9 @@ class Hierarchy:
 
     def close(self):
         if getattr(self, "_h", None):
+            # vectors first: a vector must never outlive the hierarchy it was made from
+            for v in list(getattr(self, "_vectors", ())):
+                v.close()
             _lib.lib().pf_hierarchy_destroy(self._h)
             self._h = None
 

@@ -245,3 +245,21 @@ def test_multiprocess_path_loopback(cuda, K, L, kind):
         assert np.array_equal(x, xs[r]), f"rank {r}"
         assert np.array_equal(v, acc[r]), f"accumulate rank {r}"
         assert rn == pytest.approx(res[0][2], rel=0, abs=0)
+
+
+@pytest.mark.parametrize("bottom_rows", ["0", "65536", "1000000"], ids=["multilaunch", "bottom", "bottom-all"])
+@pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
+def test_bottom_kernel_equals_multilaunch(cuda, monkeypatch, bottom_rows, kind):
+    """The cooperative bottom-of-cycle kernel is a launch-structure change only: with it
+    disabled, covering the default levels, or covering every level below the finest, the
+    solve must equal the oracle bit for bit (1 and 4 subdomains)."""
+    monkeypatch.setenv("PF_BOTTOM_ROWS", bottom_rows)
+    c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
+    for K in (1, 4):
+        setups, levels = structured(3, 2, 5, K)
+        h = gmg.Hierarchy(levels)
+        x = upload(h, 4, [s.x0 for s in setups])
+        st = gmg.solve_outer(h, x, upload(h, 4, [s.b for s in setups]), c)
+        xo, res, ost, rc = Oracle(levels).solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
+        assert st.iterations == ost.iterations
+        assert exact(download(h, x, K), xo)
