@@ -27,12 +27,18 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p
 
 // acc := acc - sum_{c != row} a_rc x_c over the row's entries in stored order; diag := a_rr.
 // This is the inner loop of one_local_sweep (solvers.cpp:21-51).
-template <bool kReadOnlyX>
+template <bool kReadOnlyX, bool kRes = false>
 __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, const double* x,
-                                            double& acc, double& diag) {
+                                            double& acc, double& diag, double* res = nullptr,
+                                            double x_row = 0.0) {
+  // kRes: *res (starting at b_r) also subtracts every product in stored order, the
+  // diagonal included — the reference's residual_norm row (linalg.cpp:66-70) bit for bit.
   const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
   const int len = A.row_len[row];
+  double r = kRes ? *res : 0.0;
   int j = 0;
+  // (measured: a branch-free variant that also gathers x for the diagonal needs 40
+  // registers and runs the C2 sweep 17 % slower — occupancy beats per-thread ILP here)
   for (; j + kUnroll <= len; j += kUnroll) {
     int32_t c[kUnroll];
     double v[kUnroll], xv[kUnroll];
@@ -44,24 +50,29 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
     }
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k)
-      xv[k] = (c[k] == row) ? 0.0 : (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]);
+      xv[k] = (c[k] == row) ? x_row : (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]);
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
+      const double p = __dmul_rn(v[k], xv[k]);
+      if (kRes) r = __dsub_rn(r, p);
       if (c[k] == row)
         diag = v[k];
       else
-        acc = __dsub_rn(acc, __dmul_rn(v[k], xv[k]));
+        acc = __dsub_rn(acc, p);
     }
   }
   for (; j < len; ++j) {
     const int64_t e = base + static_cast<int64_t>(j) * kSlice;
     const int32_t c = ld_stream(A.cols + e);
     const double v = ld_stream(A.vals + e);
+    const double p = __dmul_rn(v, c == row ? x_row : (kReadOnlyX ? __ldg(x + c) : x[c]));
+    if (kRes) r = __dsub_rn(r, p);
     if (c == row)
       diag = v;
     else
-      acc = __dsub_rn(acc, __dmul_rn(v, kReadOnlyX ? __ldg(x + c) : x[c]));
+      acc = __dsub_rn(acc, p);
   }
+  if (kRes) *res = r;
 }
 
 // acc := acc op sum_c a_rc x_c over all entries in stored order.
@@ -115,6 +126,47 @@ __global__ void __launch_bounds__(kBlock) k_jacobi(SellView A, const double* __r
   double acc = b[row], diag = 0.0;
   row_offdiag<true>(A, row, x_old, acc, diag);
   x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
+}
+
+// State of a device-driven solve_outer (multigrid.cpp:210-246).
+struct SolveState {
+  double r0;
+  double last;
+  int32_t launches;  // outer iterations started (the norm just computed is of x_{launches})
+  int32_t stop;
+  int32_t converged;
+  int32_t pad;
+  double hist[1];  // [outer_max_cycles]
+};
+
+// The convergence test of solve_outer on the device: the ascending-rank sum of the
+// per-subdomain squares (transport.cpp:139-149) gives ||b - A x_m||; m = 0 records r0,
+// m >= 1 records the residual after cycle m and stops at <= tol * r0 or after max cycles.
+// Sets the WHILE (next iteration) and IF (rest of the cycle) conditions of the graph.
+__global__ void k_decide(const double* __restrict__ sumsq, int n_parts, double tol, int max_cycles,
+                         SolveState* st, cudaGraphConditionalHandle h_while,
+                         cudaGraphConditionalHandle h_if) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  for (int i = 0; i < n_parts; ++i) s = __dadd_rn(s, sumsq[i]);
+  const double norm = sqrt(s);
+  const int m = st->launches;
+  int stop, conv;
+  if (m == 0) {
+    st->r0 = norm;
+    conv = norm == 0.0;
+    stop = conv;
+  } else {
+    st->hist[m - 1] = norm;
+    conv = norm <= __dmul_rn(tol, st->r0);
+    stop = conv || m >= max_cycles;
+  }
+  st->last = norm;
+  st->launches = m + 1;
+  st->stop = stop;
+  st->converged = conv;
+  cudaGraphSetConditional(h_while, stop ? 0u : 1u);
+  cudaGraphSetConditional(h_if, stop ? 0u : 1u);
 }
 
 // One colour of multicolour Gauss-Seidel / SOR, in place, rows [row0, row1).  Rows of
@@ -206,6 +258,52 @@ __global__ void __launch_bounds__(kBlock) k_resnorm(SellView A, const double* __
   if (threadIdx.x == 0) {
     *sumsq = t;
     if (norm_out) *norm_out = sqrt(__dadd_rn(0.0, t));
+    *ticket = 0u;
+  }
+}
+
+// k_jacobi that also returns the residual norm of its input iterate: each own row's
+// b - A x_old is accumulated alongside the sweep from the same loaded entries (in the
+// reference's order, so each row's residual is bit-identical), so solve_outer's convergence
+// test of the previous cycle (multigrid.cpp:230) costs no extra pass over the matrix.
+// Deterministic block sums + last-block finish exactly as k_resnorm; *sumsq gets this
+// subdomain's sum of squares.
+__global__ void __launch_bounds__(kBlock) k_jacobi_norm(SellView A, const double* __restrict__ x_old,
+                                                        double* __restrict__ x_new,
+                                                        const double* __restrict__ b, int32_t n_own,
+                                                        int32_t n, double omega,
+                                                        double* __restrict__ partials,
+                                                        unsigned int* ticket, double* sumsq) {
+  __shared__ double smem[kBlock / 32];
+  __shared__ bool last;
+  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  double sq = 0.0;
+  if (row < n) {
+    const double xo = x_old[row];
+    if (row >= n_own) {
+      x_new[row] = xo;
+    } else {
+      double acc = b[row], diag = 0.0, res = b[row];
+      row_offdiag<true, true>(A, row, x_old, acc, diag, &res, xo);
+      sq = __dmul_rn(res, res);
+      x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
+    }
+  }
+  const double s = block_sum(sq, smem);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (unsigned int i = threadIdx.x; i < gridDim.x; i += kBlock) t = __dadd_rn(t, partials[i]);
+  __syncthreads();
+  t = block_sum(t, smem);
+  if (threadIdx.x == 0) {
+    *sumsq = t;
     *ticket = 0u;
   }
 }

@@ -528,7 +528,8 @@ void build_bottom(pf_hierarchy* h) {
   PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bottom, kBlock, 0));
   if (occ < 1) return;
-  const int64_t want = std::max<int64_t>(sms, (max_total + kBlock - 1) / kBlock);
+  int64_t want = std::max<int64_t>(sms, (max_total + kBlock - 1) / kBlock);
+  if (const char* e = std::getenv("PF_BOTTOM_GRID")) want = std::max<int64_t>(1, std::atoll(e));
   h->bot.grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(occ) * sms));
   h->bot.top = top;
   h->bot.active = true;
@@ -631,7 +632,9 @@ void enq_copy(pf_hierarchy* h, const double* src, double* dst, int64_t n) {
 }
 
 // smooth (solvers.cpp:56-68) on x (primary buffer) with b.
-void enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_smoother_config& sc) {
+// first_done: the first Jacobi sweep already ran (k_jacobi_norm in the solve graph).
+void enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_smoother_config& sc,
+                bool first_done = false) {
   Level& L = h->levels[l];
   auto launch = launcher(h);
   double* bufs[2] = {xv->cur(), xv->alt()};
@@ -639,9 +642,10 @@ void enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
   for (int sweep = 0; sweep < sc.sweeps; ++sweep) {
     for (int local = 0; local < sc.local_sweeps; ++local) {
       if (sc.kind == PF_SMOOTHER_JACOBI) {
-        for (DevLevel& D : L.sub)
-          launch(grid_for(D.n), kBlock, k_jacobi, view(D.A), static_cast<const double*>(bufs[cur] + D.offset),
-                 bufs[cur ^ 1] + D.offset, b + D.offset, D.n_own, D.n, sc.damping);
+        if (!(first_done && sweep == 0 && local == 0))
+          for (DevLevel& D : L.sub)
+            launch(grid_for(D.n), kBlock, k_jacobi, view(D.A), static_cast<const double*>(bufs[cur] + D.offset),
+                   bufs[cur ^ 1] + D.offset, b + D.offset, D.n_own, D.n, sc.damping);
         cur ^= 1;
       } else {
         const bool sor = sc.kind == PF_SMOOTHER_MULTICOLOR_SOR;
@@ -756,7 +760,8 @@ void enq_bottom(pf_hierarchy* h, const pf_multigrid_config& cfg, int accumulate_
 }
 
 // cycle (multigrid.cpp:150-190)
-void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_multigrid_config& cfg) {
+void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_multigrid_config& cfg,
+               bool first_done = false) {
   Level& L = h->levels[l];
   double* x = xv->cur();
   if (l == 0) {
@@ -766,7 +771,7 @@ void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_
   }
   pf_smoother_config pre = cfg.smoother;
   pre.sweeps = cfg.pre_smooth;
-  enq_smooth(h, l, xv, b, pre);
+  enq_smooth(h, l, xv, b, pre, first_done && cfg.pre_smooth > 0);
   enq_scatter(h, l, PF_CH_HALO2, x);
   enq_residual(h, l, x, b, L.r.p);
   Level& Cl = h->levels[l - 1];
@@ -789,6 +794,138 @@ void enq_vcycle(pf_hierarchy* h, pf_vector* x, const double* b, const pf_multigr
   const int top = h->n_levels - 1;
   enq_scatter(h, top, PF_CH_HALO2, x->cur());
   enq_cycle(h, top, x, b, cfg);
+}
+
+// The norm-producing head of one outer iteration of the device-driven solve: for damped
+// Jacobi the first pre-smoothing sweep of the next cycle (k_jacobi_norm), otherwise a
+// k_resnorm pass; per-subdomain squares land in L.sumsq for k_decide.
+bool fused_head(const pf_multigrid_config& cfg) {
+  return cfg.smoother.kind == PF_SMOOTHER_JACOBI && cfg.pre_smooth > 0 && cfg.smoother.local_sweeps >= 1;
+}
+
+void enq_norm_head(pf_hierarchy* h, pf_vector* x, const double* b, const pf_multigrid_config& cfg) {
+  const int top = h->n_levels - 1;
+  Level& L = h->levels[top];
+  auto launch = launcher(h);
+  for (int s = 0; s < h->n_sub; ++s) {
+    DevLevel& D = L.sub[s];
+    if (fused_head(cfg))
+      launch(grid_for(D.n), kBlock, k_jacobi_norm, view(D.A), static_cast<const double*>(x->cur() + D.offset),
+             x->alt() + D.offset, b + D.offset, D.n_own, D.n, cfg.smoother.damping, D.partials.p,
+             D.ticket.p, L.sumsq.p + s);
+    else
+      launch(static_cast<unsigned>(D.resnorm_blocks), kBlock, k_resnorm, view(D.A),
+             static_cast<const double*>(x->cur() + D.offset), b + D.offset, D.n_own, D.partials.p,
+             D.ticket.p, L.sumsq.p + s, static_cast<double*>(nullptr));
+  }
+}
+
+void sync(pf_hierarchy* h);
+std::string graph_key(const char* tag, const void* x, const void* b, const pf_multigrid_config& c);
+
+cudaGraphNode_t single_leaf(cudaGraph_t g) {
+  size_t n = 0;
+  PF_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  PF_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+  cudaGraphNode_t leaf = nullptr;
+  for (cudaGraphNode_t v : nodes) {
+    size_t nd = 0;
+    PF_CUDA(cudaGraphNodeGetDependentNodes(v, nullptr, &nd));
+    if (nd == 0) {
+      if (leaf) state("solve graph head has several leaves");
+      leaf = v;
+    }
+  }
+  return leaf;
+}
+
+// solve_outer as ONE graph launch: WHILE(continue) { halo2(x); norm head; k_decide;
+// IF(continue) { rest of the V-cycle(s) } }, then the solve state copied to pinned host
+// memory.  No host round trip between cycles.
+pf_hierarchy::GraphEntry& solve_graph(pf_hierarchy* h, pf_vector* x, const pf_vector* b,
+                                      const pf_multigrid_config& cfg) {
+  const std::string key = graph_key("solve", x, b, cfg) + ":" + std::to_string(cfg.outer_max_cycles) +
+                          ":" + std::to_string(cfg.outer_tol);
+  auto it = h->graphs.find(key);
+  if (it != h->graphs.end()) return it->second;
+  pf_hierarchy::GraphEntry e;
+  const int top = h->n_levels - 1;
+  const size_t state_bytes = sizeof(SolveState) + sizeof(double) * static_cast<size_t>(cfg.outer_max_cycles);
+  PF_CUDA(cudaMalloc(&e.state, state_bytes));
+  PF_CUDA(cudaMallocHost(&e.host_state, state_bytes));
+  e.state_bytes = state_bytes;
+  cudaGraph_t G = nullptr;
+  PF_CUDA(cudaGraphCreate(&G, 0));
+  try {
+    cudaGraphConditionalHandle hw, hi;
+    PF_CUDA(cudaGraphConditionalHandleCreate(&hw, G, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t reset = nullptr;
+    cudaMemsetParams mp = {};
+    mp.dst = e.state;
+    mp.value = 0;
+    mp.elementSize = 1;
+    mp.width = state_bytes;
+    mp.height = 1;
+    PF_CUDA(cudaGraphAddMemsetNode(&reset, G, nullptr, 0, &mp));
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hw;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode = nullptr;
+    PF_CUDA(cudaGraphAddNode(&wnode, G, &reset, 1, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    PF_CUDA(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
+    // head: halo2(x) of v_cycle entry, norm head, decision
+    int64_t head = 0, rest = 0;
+    PF_CUDA(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    g_capture_counter = &head;
+    try {
+      enq_scatter(h, top, PF_CH_HALO2, x->cur());
+      enq_norm_head(h, x, b->cur(), cfg);
+      launcher(h)(1, 32, k_decide, static_cast<const double*>(h->levels[top].sumsq.p), h->n_sub,
+                  cfg.outer_tol, cfg.outer_max_cycles, static_cast<SolveState*>(e.state), hw, hi);
+    } catch (...) {
+      g_capture_counter = nullptr;
+      cudaStreamEndCapture(h->stream, &body);
+      throw;
+    }
+    g_capture_counter = nullptr;
+    PF_CUDA(cudaStreamEndCapture(h->stream, &body));
+    cudaGraphNode_t leaf = single_leaf(body);
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hi;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode = nullptr;
+    PF_CUDA(cudaGraphAddNode(&inode, body, &leaf, 1, &ip));
+    cudaGraph_t rest_g = ip.conditional.phGraph_out[0];
+    PF_CUDA(cudaStreamBeginCaptureToGraph(h->stream, rest_g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    g_capture_counter = &rest;
+    try {
+      enq_cycle(h, top, x, b->cur(), cfg, fused_head(cfg));
+      for (int j = 1; j < cfg.cycles; ++j) enq_vcycle(h, x, b->cur(), cfg);
+    } catch (...) {
+      g_capture_counter = nullptr;
+      cudaStreamEndCapture(h->stream, &rest_g);
+      throw;
+    }
+    g_capture_counter = nullptr;
+    PF_CUDA(cudaStreamEndCapture(h->stream, &rest_g));
+    cudaGraphNode_t copy = nullptr;
+    PF_CUDA(cudaGraphAddMemcpyNode1D(&copy, G, &wnode, 1, e.host_state, e.state, state_bytes,
+                                     cudaMemcpyDeviceToHost));
+    PF_CUDA(cudaGraphInstantiate(&e.exec, G, 0));
+    e.head_kernels = head;
+    e.kernels = rest;
+  } catch (...) {
+    cudaGraphDestroy(G);
+    throw;
+  }
+  PF_CUDA(cudaGraphDestroy(G));
+  return h->graphs.emplace(key, e).first->second;
 }
 
 void sync(pf_hierarchy* h) {
@@ -861,6 +998,28 @@ void solve_outer_dev(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf
   const int top = h->n_levels - 1;
   const double t0 = wall_now();
   pf_solve_stats s{};
+  const char* mode = std::getenv("PF_SOLVE_MODE");
+  if (h->world == h->n_sub && !(mode && std::string(mode) == "host")) {
+    auto& g = solve_graph(h, x, b, cfg);
+    PF_CUDA(cudaGraphLaunch(g.exec, h->stream));
+    sync(h);
+    const auto* ss = static_cast<const SolveState*>(g.host_state);
+    const int m = ss->launches - 1;  // cycles completed
+    h->launches += g.head_kernels * ss->launches + g.kernels * m;
+    s.initial_residual = ss->r0;
+    s.iterations = m;
+    s.final_residual = ss->last;
+    s.converged = ss->converged;
+    for (int i = 0; i < m && residuals && i < max_res; ++i) residuals[i] = ss->hist[i];
+    s.solve_seconds = wall_now() - t0;
+    if (st) *st = s;
+    if (!s.converged) {
+      std::ostringstream os;
+      os << "multigrid stalled at relative residual " << s.final_residual / s.initial_residual;
+      throw Error(PF_ERR_NO_CONVERGENCE, os.str());
+    }
+    return;
+  }
   enq_resnorm(h, top, x->cur(), b->cur());
   const double r0 = read_norm(h, top);
   s.initial_residual = r0;
@@ -935,8 +1094,11 @@ void set_error(const char* m) { g_last_error = m; }
 
 pf_hierarchy::~pf_hierarchy() {
   cudaSetDevice(device);
-  for (auto& [k, e] : graphs)
+  for (auto& [k, e] : graphs) {
     if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (e.state) cudaFree(e.state);
+    if (e.host_state) cudaFreeHost(e.host_state);
+  }
   for (pf::Level& L : levels) {
     delete L.x;
     delete L.b;

@@ -174,7 +174,11 @@ struct pf_hierarchy {
   // graph cache of one outer cycle (cycles x V-cycle + finest residual norm)
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
-    int64_t kernels = 0;
+    int64_t kernels = 0;       // kernels per replay (solve graph: per executed IF body)
+    int64_t head_kernels = 0;  // solve graph: kernels per WHILE iteration head
+    void* state = nullptr;      // solve graph: device SolveState
+    void* host_state = nullptr; // pinned copy written at the end of the graph
+    size_t state_bytes = 0;
   };
   std::map<std::string, GraphEntry> graphs;
   // Multi-process runs: level 0 of every rank, replicated on each GPU, so the coarse

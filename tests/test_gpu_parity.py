@@ -263,3 +263,27 @@ def test_bottom_kernel_equals_multilaunch(cuda, monkeypatch, bottom_rows, kind):
         xo, res, ost, rc = Oracle(levels).solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
         assert st.iterations == ost.iterations
         assert exact(download(h, x, K), xo)
+
+
+@pytest.mark.parametrize("mode", ["host", "graph"])
+@pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
+def test_solve_drivers_agree(cuda, monkeypatch, mode, kind):
+    """solve_outer driven from the host (one graph per outer cycle + host convergence
+    test) and as one device-driven graph (WHILE/IF conditional nodes, the Jacobi norm
+    fused into the next cycle's first sweep) give the oracle's iterate and cycle count."""
+    monkeypatch.setenv("PF_SOLVE_MODE", mode)
+    c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
+    for K in (1, 2):
+        setups, levels = structured(3, 2, 4, K)
+        h = gmg.Hierarchy(levels)
+        x = upload(h, 3, [s.x0 for s in setups])
+        st = gmg.solve_outer(h, x, upload(h, 3, [s.b for s in setups]), c)
+        xo, res, ost, rc = Oracle(levels).solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
+        assert st.iterations == ost.iterations and len(st.residuals) == st.iterations
+        np.testing.assert_allclose(st.residuals, res, rtol=1e-12)
+        assert st.initial_residual == pytest.approx(ost.initial_residual, rel=1e-13)
+        assert exact(download(h, x, K), xo)
+        # zero rhs converges in zero cycles (test_multigrid.cpp:164-174)
+        z = h.vector(3)
+        st0 = gmg.solve_outer(h, z, h.vector(3), c)
+        assert st0.iterations == 0 and st0.converged
