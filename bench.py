@@ -50,42 +50,57 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling (B200_PROFILING.md clocks line), started before the run and
+    filtered to the timed region by timestamp."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
         self.path = os.path.join("/tmp", f"pf_clocks_{os.getpid()}.csv")
+        self.windows = []
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,"
-                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "50"],
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            time.sleep(0.15)
         except Exception:
             self.proc = None
         return self
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc:
+            time.sleep(0.1)
             self.proc.terminate()
             self.proc.wait()
 
+    def window(self, t0, t1):
+        self.windows.append((t0, t1))
+
     def summary(self):
+        import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, n_all = [], None, set(), 0
         try:
             for line in open(self.path):
                 f = [x.strip() for x in line.split(",")]
-                if len(f) < 7 or not f[0].isdigit():
+                if len(f) < 8 or not f[1].isdigit():
                     continue
-                sm.append(int(f[0]))
-                mx = int(f[1])
-                for n, v in zip(names, f[3:7]):
+                n_all += 1
+                try:
+                    ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                if not any(t0 - 0.02 <= ts <= t1 + 0.02 for t0, t1 in self.windows):
+                    continue
+                sm.append(int(f[1]))
+                mx = int(f[2])
+                for n, v in zip(names, f[4:8]):
                     if v.lower() == "active":
                         reasons.add(n)
         except OSError:
@@ -171,6 +186,7 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    clk = Clocks(local).start()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
@@ -214,12 +230,14 @@ def run_b200(args):
     def timed(c, steps):
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.time()
         e0.record(stream)
         st = None
         for _ in range(steps):
             st = step(c)
         e1.record(stream)
         barrier()
+        clk.window(w0, time.time())
         ms = e0.elapsed_time(e1)
         if dist:
             t = torch.tensor([ms], device="cuda")
@@ -230,10 +248,8 @@ def run_b200(args):
     for _ in range(args.warmup):
         st = step(cfg)
     n0 = h.launch_count()
-    with Clocks(local) as clk:
-        ms, st = timed(cfg, args.steps)
+    ms, st = timed(cfg, args.steps)
     launches = h.launch_count() - n0
-    clocks = clk.summary()
     value = setup.n_global * args.steps / (ms / 1e3)
 
     # e2e: the same solve through the host-buffer entry point (pinned host x0/b in,
@@ -273,6 +289,8 @@ def run_b200(args):
     sor_ms_total, st_sor = timed(sor, max(3, args.steps // 2))
     sor_steps = max(3, args.steps // 2)
 
+    clk.stop()
+    clocks = clk.summary()
     if rank != 0:
         if dist:
             dist.destroy_process_group()

@@ -30,12 +30,8 @@ struct BotSub {
   SellView A;
   const int32_t* host_of_own;
   const int32_t* color_start;  // n_colors + 1, subdomain-local device rows
-  const int64_t* p_off;        // P of this level (rows: this level; cols: parent, local)
-  const int32_t* p_col;
-  const double* p_w;
-  const int64_t* r_off;        // R to the parent (rows: parent, local; cols: this level, local)
-  const int32_t* r_col;
-  const double* r_w;
+  SellView P;                  // P of this level (rows: this level; cols: parent, local)
+  SellView R;                  // R to the parent (rows: parent, local; cols: this level, local)
   const uint8_t* is_dir;
   int32_t n, n_own, n_colors;
   int32_t off;                 // position in the level vectors
@@ -198,9 +194,7 @@ __global__ void __launch_bounds__(kBlock) k_bottom(const BotDesc* __restrict__ D
       const BotSub& F = D.sub[l][s];
       const BotSub& Sc = D.sub[l - 1][s];
       const int32_t lr = static_cast<int32_t>(pr - Sc.off);
-      double acc = 0.0;
-      for (int64_t e = F.r_off[lr], e1 = F.r_off[lr + 1]; e < e1; ++e)
-        acc = __dadd_rn(acc, __dmul_rn(F.r_w[e], L.r[F.off + F.r_col[e]]));
+      const double acc = row_dot<false, false>(F.R, lr, L.r + F.off, 0.0);
       C.b[pr] = Sc.is_dir[lr] ? 0.0 : acc;
       C.x[pr] = 0.0;
     }
@@ -228,9 +222,7 @@ __global__ void __launch_bounds__(kBlock) k_bottom(const BotDesc* __restrict__ D
       const BotSub& S = D.sub[l][s];
       const int32_t lr = static_cast<int32_t>(r - S.off);
       const double* xc = C.x + D.sub[l - 1][s].off;
-      double acc = 0.0;
-      for (int64_t e = S.p_off[lr], e1 = S.p_off[lr + 1]; e < e1; ++e)
-        acc = __dadd_rn(acc, __dmul_rn(S.p_w[e], xc[S.p_col[e]]));
+      const double acc = row_dot<false, false>(S.P, lr, xc, 0.0);
       L.x[r] = __dadd_rn(L.x[r], acc);
     }
     g.sync();

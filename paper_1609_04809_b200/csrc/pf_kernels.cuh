@@ -319,17 +319,11 @@ __global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* o
 
 // x_f += P x_c over every local fine dof (multigrid.cpp:121-129 + :183-184): the
 // correction is accumulated from 0 in P's entry order, then added.
-__global__ void __launch_bounds__(kBlock) k_prolong_add(const int64_t* __restrict__ p_off,
-                                                        const int32_t* __restrict__ p_col,
-                                                        const double* __restrict__ p_w,
-                                                        const double* __restrict__ xc,
-                                                        double* __restrict__ xf, int32_t n_f,
-                                                        int add) {
+__global__ void __launch_bounds__(kBlock) k_prolong_add(SellView P, const double* __restrict__ xc,
+                                                        double* __restrict__ xf, int32_t n_f, int add) {
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_f) return;
-  double acc = 0.0;
-  for (int64_t e = p_off[row], e1 = p_off[row + 1]; e < e1; ++e)
-    acc = __dadd_rn(acc, __dmul_rn(ld_stream(p_w + e), __ldg(xc + ld_stream(p_col + e))));
+  const double acc = row_dot<false>(P, row, xc, 0.0);
   xf[row] = add ? __dadd_rn(xf[row], acc) : acc;
 }
 
@@ -339,19 +333,14 @@ __global__ void __launch_bounds__(kBlock) k_prolong_add(const int64_t* __restric
 // (multigrid.cpp:172-179): Dirichlet coarse entries of b become 0 and the coarse x is
 // zeroed.  (Zeroing before the master/slave accumulate is equivalent: Dirichlet
 // carriers are Dirichlet on every rank, so they only ever accumulate zeros.)
-__global__ void __launch_bounds__(kBlock) k_restrict(const int64_t* __restrict__ r_off,
-                                                     const int32_t* __restrict__ r_col,
-                                                     const double* __restrict__ r_w,
-                                                     const double* __restrict__ rf,
+__global__ void __launch_bounds__(kBlock) k_restrict(SellView R, const double* __restrict__ rf,
                                                      double* __restrict__ bc,
                                                      double* __restrict__ xc,
                                                      const uint8_t* __restrict__ is_dir_c,
                                                      int32_t n_c, int zero_dirichlet) {
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_c) return;
-  double acc = 0.0;
-  for (int64_t e = r_off[row], e1 = r_off[row + 1]; e < e1; ++e)
-    acc = __dadd_rn(acc, __dmul_rn(ld_stream(r_w + e), __ldg(rf + ld_stream(r_col + e))));
+  const double acc = row_dot<false>(R, row, rf, 0.0);
   bc[row] = (zero_dirichlet && is_dir_c[row]) ? 0.0 : acc;
   if (xc) xc[row] = 0.0;
 }

@@ -83,6 +83,45 @@ void check_vec(const pf_hierarchy* h, const pf_vector* v, int level, const char*
 
 // ------------------------------------------------------------------ upload --
 
+// SELL-32 from rows already in device order (entry order inside a row is preserved).
+void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vector<int32_t>& col,
+                    const std::vector<double>& val, DevSell& out) {
+  const int64_t n_slices = (n + kSlice - 1) / kSlice;
+  std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
+  std::vector<int32_t> rlen(static_cast<size_t>(std::max<int64_t>(n_slices, 1) * kSlice), 0);
+  for (int32_t d = 0; d < n; ++d) rlen[d] = static_cast<int32_t>(off[d + 1] - off[d]);
+  for (int64_t s = 0; s < n_slices; ++s) {
+    int32_t w = 0;
+    for (int l = 0; l < kSlice; ++l) w = std::max(w, rlen[s * kSlice + l]);
+    sptr[s + 1] = sptr[s] + static_cast<int64_t>(w) * kSlice;
+  }
+  std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
+  std::vector<int32_t> sc(static_cast<size_t>(sptr[n_slices]), 0);
+  for (int64_t s = 0; s < n_slices; ++s) {
+    const int64_t w = (sptr[s + 1] - sptr[s]) / kSlice;
+    for (int l = 0; l < kSlice; ++l) {
+      const int64_t d = s * kSlice + l;
+      const int32_t len = d < n ? rlen[d] : 0;
+      for (int64_t j = 0; j < w; ++j) {
+        const int64_t e = sptr[s] + j * kSlice + l;
+        if (j < len) {
+          sc[e] = col[off[d] + j];
+          sv[e] = val[off[d] + j];
+        } else {  // padding, never read (row_len bounds every loop)
+          sc[e] = 0;
+          sv[e] = 0.0;
+        }
+      }
+    }
+  }
+  out.slice_ptr.upload(sptr);
+  out.row_len.upload(rlen);
+  out.vals.upload(sv);
+  out.cols.upload(sc);
+  out.nnz = n > 0 ? off[n] : 0;
+  out.stored = sptr[n_slices];
+}
+
 // Device layout of one subdomain level: own rows colour-major (stable in host order),
 // then every other row in host order; SELL-32 operator; P (rows of this level).
 void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
@@ -150,47 +189,24 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
     for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
   }
   D.d_perm.upload(D.perm);
-  // --- SELL-32
-  const int64_t n_slices = (n + kSlice - 1) / kSlice;
-  std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
-  std::vector<int32_t> rlen(static_cast<size_t>(n_slices * kSlice), 0);
-  for (int32_t d = 0; d < n; ++d) {
-    const int32_t hr = inv[d];
-    rlen[d] = static_cast<int32_t>(H.rowptr[hr + 1] - H.rowptr[hr]);
-  }
-  for (int64_t s = 0; s < n_slices; ++s) {
-    int32_t w = 0;
-    for (int l = 0; l < kSlice; ++l) w = std::max(w, rlen[s * kSlice + l]);
-    sptr[s + 1] = sptr[s] + static_cast<int64_t>(w) * kSlice;
-  }
-  std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
-  std::vector<int32_t> sc(static_cast<size_t>(sptr[n_slices]), 0);
-  for (int64_t s = 0; s < n_slices; ++s) {
-    const int64_t w = (sptr[s + 1] - sptr[s]) / kSlice;
-    for (int l = 0; l < kSlice; ++l) {
-      const int64_t d = s * kSlice + l;
-      const int32_t len = d < n ? rlen[d] : 0;
-      const int32_t hr = d < n ? inv[d] : 0;
-      for (int64_t j = 0; j < w; ++j) {
-        const int64_t e = sptr[s] + j * kSlice + l;
-        if (j < len) {
-          const int64_t k = H.rowptr[hr] + j;
-          sc[e] = D.perm[H.cols[k]];
-          sv[e] = H.vals[k];
-        } else {
-          sc[e] = static_cast<int32_t>(std::min<int64_t>(d, n > 0 ? n - 1 : 0));
-          sv[e] = 0.0;
-        }
+  // --- SELL-32 operator: rows in device order, columns mapped, entries in CSR order
+  {
+    std::vector<int64_t> off(static_cast<size_t>(n) + 1, 0);
+    std::vector<int32_t> col;
+    std::vector<double> val;
+    col.reserve(H.cols.size());
+    val.reserve(H.vals.size());
+    for (int32_t d = 0; d < n; ++d) {
+      const int32_t hr = inv[d];
+      for (int64_t k = H.rowptr[hr]; k < H.rowptr[hr + 1]; ++k) {
+        col.push_back(D.perm[H.cols[k]]);
+        val.push_back(H.vals[k]);
       }
+      off[d + 1] = static_cast<int64_t>(col.size());
     }
+    sell_from_rows(n, off, col, val, D.A);
   }
-  D.A.slice_ptr.upload(sptr);
-  D.A.row_len.upload(rlen);
-  D.A.vals.upload(sv);
-  D.A.cols.upload(sc);
-  D.A.nnz = H.rowptr[n];
   D.A.own_nnz = H.rowptr[n_own];
-  D.A.stored = sptr[n_slices];
   {
     std::vector<uint8_t> touched(static_cast<size_t>(n), 0);
     for (int64_t k = 0; k < H.rowptr[n_own]; ++k) touched[H.cols[k]] = 1;
@@ -229,10 +245,7 @@ void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const
     }
     poff[d + 1] = static_cast<int64_t>(pcol.size());
   }
-  DF.p_off.upload(poff);
-  DF.p_col.upload(pcol);
-  DF.p_w.upload(pw);
-  DF.p_nnz = static_cast<int64_t>(pcol.size());
+  sell_from_rows(nf, poff, pcol, pw, DF.P);
   // R by counting sort over parent host rows; iterating fine host rows ascending keeps
   // each parent row's contributions in the reference's scatter-add order.
   std::vector<int64_t> cnt(static_cast<size_t>(nc) + 1, 0);
@@ -269,10 +282,7 @@ void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const
     }
     roff[d + 1] = static_cast<int64_t>(rcol.size());
   }
-  DF.r_off.upload(roff);
-  DF.r_col.upload(rcol);
-  DF.r_w.upload(rwt);
-  DF.r_nnz = static_cast<int64_t>(rcol.size());
+  sell_from_rows(nc, roff, rcol, rwt, DF.R);
 }
 
 const HostChannel* find_channel(const HostLevel& H, int kind, int peer) {
@@ -509,12 +519,8 @@ void build_bottom(pf_hierarchy* h) {
       S.A = view(D.A);
       S.host_of_own = D.d_perm.p;
       S.color_start = h->bot.color_bufs.back().p;
-      S.p_off = D.p_off.p;
-      S.p_col = D.p_col.p;
-      S.p_w = D.p_w.p;
-      S.r_off = D.r_off.p;
-      S.r_col = D.r_col.p;
-      S.r_w = D.r_w.p;
+      S.P = view(D.P);
+      S.R = view(D.R);
       S.is_dir = D.d_is_dir.p;
       S.n = D.n;
       S.n_own = D.n_own;
@@ -676,9 +682,7 @@ void enq_prolong(pf_hierarchy* h, int fine, const double* xc, double* xf, int ad
   auto launch = launcher(h);
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = F.sub[s];
-    launch(grid_for(D.n), kBlock, k_prolong_add, static_cast<const int64_t*>(D.p_off.p),
-           static_cast<const int32_t*>(D.p_col.p), static_cast<const double*>(D.p_w.p),
-           xc + Cl.sub[s].offset, xf + D.offset, D.n, add);
+    launch(grid_for(D.n), kBlock, k_prolong_add, view(D.P), xc + Cl.sub[s].offset, xf + D.offset, D.n, add);
   }
 }
 
@@ -690,9 +694,7 @@ void enq_restrict(pf_hierarchy* h, int fine, const double* rf, double* bc, doubl
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = F.sub[s];
     DevLevel& DC = Cl.sub[s];
-    launch(grid_for(DC.n), kBlock, k_restrict, static_cast<const int64_t*>(D.r_off.p),
-           static_cast<const int32_t*>(D.r_col.p), static_cast<const double*>(D.r_w.p),
-           rf + D.offset, bc + DC.offset, xc ? xc + DC.offset : nullptr,
+    launch(grid_for(DC.n), kBlock, k_restrict, view(D.R), rf + D.offset, bc + DC.offset, xc ? xc + DC.offset : nullptr,
            static_cast<const uint8_t*>(DC.d_is_dir.p), DC.n, zero_dir);
   }
 }
@@ -1310,8 +1312,9 @@ pf_status pf_hierarchy_device_bytes(const pf_hierarchy* h, int64_t* out) {
   for (const Level& L : h->levels) {
     for (const DevLevel& D : L.sub)
       b += D.A.vals.bytes() + D.A.cols.bytes() + D.A.slice_ptr.bytes() + D.A.row_len.bytes() +
-           D.p_off.bytes() + D.p_col.bytes() + D.p_w.bytes() + D.r_off.bytes() + D.r_col.bytes() +
-           D.r_w.bytes() + D.d_perm.bytes() + D.d_is_dir.bytes();
+           D.P.vals.bytes() + D.P.cols.bytes() + D.P.slice_ptr.bytes() + D.P.row_len.bytes() +
+           D.R.vals.bytes() + D.R.cols.bytes() + D.R.slice_ptr.bytes() + D.R.row_len.bytes() +
+           D.d_perm.bytes() + D.d_is_dir.bytes();
     b += L.r.bytes() + (L.x ? L.x->data.bytes() : 0) + (L.b ? L.b->data.bytes() : 0);
   }
   *out = b;

@@ -95,16 +95,12 @@ struct DevLevel {
   DevSell A;
   DevBuf<uint8_t> d_is_dir;
   int64_t own_cols_touched = 0;  // distinct columns referenced by own rows
-  // prolongation from the parent level (rows = this level's device rows)
-  DevBuf<int64_t> p_off;
-  DevBuf<int32_t> p_col;  // parent device index (+ parent offset)
-  DevBuf<double> p_w;
-  int64_t p_nnz = 0;
-  // restriction to the parent level (rows = parent device rows)
-  DevBuf<int64_t> r_off;
-  DevBuf<int32_t> r_col;  // this level's device index (+ own offset)
-  DevBuf<double> r_w;
-  int64_t r_nnz = 0;
+  // prolongation from the parent level (rows: this level's device rows; columns: parent
+  // device rows of the same subdomain), SELL-32 like the operator
+  DevSell P;
+  // restriction to the parent level (rows: parent device rows; columns: this level's
+  // device rows), entries in ascending fine host index
+  DevSell R;
   // residual-norm scratch
   int resnorm_blocks = 0;
   DevBuf<double> partials;
