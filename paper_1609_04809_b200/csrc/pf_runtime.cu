@@ -218,7 +218,8 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
   D.d_is_dir.upload(isdir);
   // --- residual-norm scratch
   D.resnorm_blocks = std::max<int>(1, static_cast<int>(grid_for(n_own)));
-  D.partials.alloc(D.resnorm_blocks);
+  // partials serve k_resnorm (grid over own rows) and k_jacobi_norm (grid over all rows)
+  D.partials.alloc(std::max<int64_t>(D.resnorm_blocks, grid_for(n)));
   D.ticket.alloc(1);
   PF_CUDA(cudaMemset(D.ticket.p, 0, sizeof(unsigned int)));
 }

@@ -287,3 +287,30 @@ def test_solve_drivers_agree(cuda, monkeypatch, mode, kind):
         z = h.vector(3)
         st0 = gmg.solve_outer(h, z, h.vector(3), c)
         assert st0.iterations == 0 and st0.converged
+
+
+def test_repeated_solves_at_c2(cuda):
+    """C2 (128^3) solved three times through the same cached solve graph: 9 Jacobi cycles,
+    the reference's residual history (golden, 8 reference ranks) within the roundoff gate,
+    identical iterates every time."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c2_jacobi_k8.npz"))
+    setups, levels = structured(3, 2, 7, 1)
+    h = gmg.Hierarchy(levels)
+    x = h.vector(6)
+    b = upload(h, 6, [setups[0].b])
+    first = None
+    for _ in range(3):
+        x.upload(setups[0].x0)
+        st = gmg.solve_outer(h, x, b, cfg())
+        assert st.iterations == int(g["iterations"]) == 9
+        np.testing.assert_allclose(st.residuals, g["residuals"], rtol=1e-6,
+                                   atol=1e-14 * float(g["initial_residual"]))
+        sol = x.download()
+        if first is None:
+            first = sol
+        assert np.array_equal(sol, first)
+    got = keyed([levels[0][-1]], [first])
+    want = dict(zip(map(tuple, g["keys"]), g["values"]))
+    scale = np.abs(g["values"]).max()
+    assert max(abs(got[k] - want[k]) for k in want) <= 1e-11 * scale
