@@ -52,6 +52,8 @@ typedef enum {
 const char* pf_last_error(void);
 /* Library version string and build flags (arch, compiler). */
 const char* pf_version(void);
+/* Number of CUDA devices visible to this process. */
+pf_status pf_device_count(int* out);
 
 /* ---------------------------------------------------------------- enums -- */
 

@@ -16,20 +16,40 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_ref", "libparfem_ref.so")
+BRIDGE_PATH = os.path.join(HERE, "_ref", "libparfem_bridge.so")
 
 _lib = None
+_bridge = None
 
 
 def available() -> bool:
     return os.path.exists(LIB_PATH)
 
 
-def lib():
-    global _lib
+def bridge_available() -> bool:
+    return os.path.exists(BRIDGE_PATH)
+
+
+def lib(bridge: bool = False):
+    """The reference library; bridge=True: the same reference with solve_outer routed
+    through integration/parfem_gpu_bridge.cpp into libpf_gpu.so (ref_set_gpu(1))."""
+    global _lib, _bridge
+    if bridge:
+        if _bridge is None:
+            if not bridge_available():
+                raise FileNotFoundError(f"{BRIDGE_PATH} not built (make -C oracle bridge)")
+            _bridge = _bind(C.CDLL(BRIDGE_PATH))
+            _bridge.ref_set_gpu(1)
+        return _bridge
     if _lib is None:
         if not available():
             raise FileNotFoundError(f"reference oracle not built: {LIB_PATH} (run make -C oracle)")
-        L = C.CDLL(LIB_PATH)
+        _lib = _bind(C.CDLL(LIB_PATH))
+    return _lib
+
+
+def _bind(L):
+    if True:
         P = C.c_void_p
         i64p = C.POINTER(C.c_int64)
         L.ref_last_error.restype = C.c_char_p
@@ -46,8 +66,8 @@ def lib():
                                               P, P, P, C.c_int, C.POINTER(C.c_int), P]
         L.ref_bench.argtypes = [C.c_int] * 6 + [C.c_double, C.c_int, C.c_int, C.c_double,
                                                 C.c_int, C.c_int, P, P, i64p, C.POINTER(C.c_int)]
-        _lib = L
-    return _lib
+        L.ref_set_gpu.argtypes = [C.c_int]
+    return L
 
 
 def _ptr(a: np.ndarray):
@@ -160,9 +180,10 @@ OP_SOLVE, OP_SMOOTH, OP_VCYCLE, OP_RESNORM, OP_RESIDUAL = range(5)
 
 
 def run(dim, n_coarse, levels, K, *, problem=0, op=OP_SOLVE, n_ops=1, smoother=0, damping=0.8,
-        pre=2, post=2, outer_tol=1e-10, max_cycles=100, x_in=None, sizes=None):
-    """Run the reference hot path; returns (x_per_rank, residuals, stats dict)."""
-    L = lib()
+        pre=2, post=2, outer_tol=1e-10, max_cycles=100, x_in=None, sizes=None, gpu=False):
+    """Run the reference hot path; returns (x_per_rank, residuals, stats dict).
+    gpu=True: the unmodified reference with its solve_outer replaced by the GPU bridge."""
+    L = lib(bridge=gpu)
     if sizes is None:
         hb = build(dim, n_coarse, levels, K, problem)
         sizes = [hb.ranks[r][-1].n_dofs for r in range(K)]

@@ -28,12 +28,32 @@
 
 #include "parfem/app.hpp"
 #include "parfem/multigrid.hpp"
+#ifdef PF_BRIDGE
+// the reference-side binding of the GPU hot path (integration/parfem_gpu_bridge.hpp)
+#include "parfem_gpu_bridge.hpp"
+#endif
 
 using namespace parfem;
 
 namespace {
 
 thread_local std::string g_err;
+int g_use_gpu = 0;  // PF_BRIDGE builds: solve_outer goes through parfem::gpu::solve_outer
+
+SolveStats outer(MultigridHierarchy& h, DistributedVector& x, const DistributedVector& b,
+                 const MultigridConfig& cfg) {
+#ifdef PF_BRIDGE
+  if (g_use_gpu) return parfem::gpu::solve_outer(h, x, b, cfg);
+#endif
+  return solve_outer(h, x, b, cfg);
+}
+
+void done_with(MultigridHierarchy& h) {
+#ifdef PF_BRIDGE
+  if (g_use_gpu) parfem::gpu::release(h);
+#endif
+  (void)h;
+}
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -183,6 +203,16 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
+// 1: solve_outer calls go through the GPU bridge (only in libparfem_bridge.so).
+int ref_set_gpu(int on) {
+#ifdef PF_BRIDGE
+  g_use_gpu = on;
+  return 0;
+#else
+  return on ? 1 : 0;
+#endif
+}
+
 double ref_key_noise(const std::int64_t* k4, std::uint64_t salt) { return key_noise(k4, salt); }
 
 // Build the reference hierarchy on K logical ranks and keep a plain copy of every
@@ -316,7 +346,7 @@ int ref_run(int dim, int n_coarse, int levels, int K, int problem, int op, int n
       if (op == 0) {
         barrier(tp);
         t2 = now_s();
-        st = solve_outer(h, x, b, cfg);
+        st = outer(h, x, b, cfg);
         t3 = now_s();
       } else if (op == 1) {
         SmootherConfig sc = cfg.smoother;
@@ -336,6 +366,7 @@ int ref_run(int dim, int n_coarse, int levels, int K, int problem, int op, int n
         for (std::size_t i = 0; i < y.size(); ++i) x.values[i] = b.values[i] - y[i];
       }
       const double cs = tp.comm_seconds() - c0;
+      done_with(h);
       if (x_out && x_out[r]) std::copy(x.values.begin(), x.values.end(), x_out[r]);
       std::lock_guard<std::mutex> lock(mu);
       solve_s = std::max(solve_s, t3 - t2);
@@ -389,11 +420,12 @@ int ref_bench(int dim, int n_coarse, int levels, int K, int problem, int smoothe
         start_vectors(h, x, b);
         barrier(tp);
         const double a = now_s();
-        const SolveStats st = solve_outer(h, x, b, cfg);
+        const SolveStats st = outer(h, x, b, cfg);
         const double e = now_s();
         it = st.iterations;
         if (s >= warmup) mine[static_cast<std::size_t>(s - warmup)] = e - a;
       }
+      done_with(h);
       std::lock_guard<std::mutex> lock(mu);
       for (int s = 0; s < steps; ++s)
         per[static_cast<std::size_t>(s)] = std::max(per[static_cast<std::size_t>(s)], mine[static_cast<std::size_t>(s)]);

@@ -95,7 +95,7 @@ class SolveStats(C.Structure):
 
 # Every symbol include/pf_gpu.h and include/pf_setup.h declare (checked by the CPU tests).
 EXPORTS = [
-    "pf_last_error", "pf_version", "pf_default_smoother_config", "pf_default_multigrid_config",
+    "pf_last_error", "pf_version", "pf_device_count", "pf_default_smoother_config", "pf_default_multigrid_config",
     "pf_hierarchy_create", "pf_hierarchy_set_level", "pf_hierarchy_finalize", "pf_nccl_unique_id",
     "pf_hierarchy_init_nccl", "pf_hierarchy_set_coarse_replica", "pf_hierarchy_destroy",
     "pf_loopback_create", "pf_loopback_destroy", "pf_hierarchy_init_loopback", "pf_hierarchy_device_bytes",
@@ -130,6 +130,7 @@ def lib():
     L.pf_default_smoother_config.argtypes = [C.POINTER(SmootherConfig)]
     L.pf_default_multigrid_config.argtypes = [C.POINTER(MultigridConfig)]
     sigs = {
+        "pf_device_count": [C.POINTER(C.c_int)],
         "pf_hierarchy_create": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, PP],
         "pf_hierarchy_set_level": [P, C.c_int, C.c_int, C.POINTER(LevelDesc)],
         "pf_hierarchy_finalize": [P],

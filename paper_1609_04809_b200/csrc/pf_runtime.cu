@@ -61,7 +61,7 @@ struct Launcher {
 };
 
 // While a graph is being captured, kernel launches are counted into the graph entry.
-int64_t* g_capture_counter = nullptr;
+thread_local int64_t* g_capture_counter = nullptr;
 
 Launcher launcher(pf_hierarchy* h) { return Launcher{h, g_capture_counter ? g_capture_counter : &h->launches}; }
 
@@ -1142,6 +1142,13 @@ const char* pf_last_error(void) { return pf::g_last_error.c_str(); }
 
 const char* pf_version(void) {
   return "paper_1609_04809_b200 pf_gpu 0.1 (sm_100a, SELL-32 fp64)";
+}
+
+pf_status pf_device_count(int* out) {
+  PF_API_BEGIN
+  if (!out) invalid("null output");
+  PF_CUDA(cudaGetDeviceCount(out));
+  PF_API_END
 }
 
 void pf_default_smoother_config(pf_smoother_config* o) {

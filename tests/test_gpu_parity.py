@@ -314,3 +314,32 @@ def test_repeated_solves_at_c2(cuda):
     want = dict(zip(map(tuple, g["keys"]), g["values"]))
     scale = np.abs(g["values"]).max()
     assert max(abs(got[k] - want[k]) for k in want) <= 1e-11 * scale
+
+
+@pytest.mark.parametrize("K", [1, 2, 4, 8])
+@pytest.mark.parametrize("smoother", [0, 1], ids=["jacobi", "gs"])
+def test_drop_in_bridge_inside_the_reference(cuda, ref_lib, K, smoother):
+    """The drop-in: the UNMODIFIED reference builds its hierarchy on K rank threads
+    (run_on_ranks) and calls parfem::gpu::solve_outer (integration/parfem_gpu_bridge.cpp)
+    where it would call parfem::solve_outer.  Jacobi must equal the reference's own solve
+    bit for bit; Gauss-Seidel (device: multicolour) must converge to the same solution
+    within the SURVEY §8d gate with +-1 cycle."""
+    if not ref_lib.bridge_available():
+        pytest.skip("oracle/_ref/libparfem_bridge.so not built")
+    L = 5 if K == 1 else 4
+    R = ref_lib.build(3, 2, L, K)
+    sizes = [R.ranks[r][-1].n_dofs for r in range(K)]
+    xr, resr, sr = ref_lib.run(3, 2, L, K, smoother=smoother, pre=2, post=2, outer_tol=1e-10, sizes=sizes)
+    xg, resg, sg = ref_lib.run(3, 2, L, K, smoother=smoother, pre=2, post=2, outer_tol=1e-10, sizes=sizes,
+                               gpu=True)
+    assert sg["status"] == 0, sg["error"]
+    if smoother == 0:
+        assert sg["iterations"] == sr["iterations"]
+        np.testing.assert_allclose(resg, resr, rtol=1e-13)
+        assert all(np.array_equal(a, b) for a, b in zip(xg, xr))
+    else:
+        assert abs(sg["iterations"] - sr["iterations"]) <= 1
+        assert resg[-1] <= 1e-10 * sg["initial_residual"]
+        num = sum(float(np.sum((a - b) ** 2)) for a, b in zip(xg, xr))
+        den = sum(float(np.sum(b ** 2)) for b in xr)
+        assert np.sqrt(num) <= 1e-8 * np.sqrt(den)
