@@ -7,6 +7,8 @@
 // cross in the reference's host order.
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -183,6 +185,7 @@ inline SolveStats solve_outer(Hierarchy& h, DeviceVector& x, const DeviceVector&
   pf_solve_stats s{};
   std::vector<double> res(static_cast<size_t>(cfg.outer_max_cycles > 0 ? cfg.outer_max_cycles : 1));
   const pf_status st = pf_solve_outer(h.raw(), x.raw(), b.raw(), &c, &s, res.data(), static_cast<int>(res.size()));
+  if (std::getenv("PF_BRIDGE_TRACE")) std::fprintf(stderr, "[shim] pf_solve_outer -> %d, %d iterations\n", static_cast<int>(st), s.iterations);
   SolveStats out{s.iterations, s.initial_residual, s.final_residual, s.converged != 0,
                  std::vector<double>(res.begin(), res.begin() + s.iterations), s.solve_seconds, s.comm_seconds};
   check(st);

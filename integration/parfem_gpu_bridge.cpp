@@ -1,6 +1,10 @@
 // parfem_gpu_bridge.cpp — see parfem_gpu_bridge.hpp.
 #include "parfem_gpu_bridge.hpp"
 
+#include <csignal>
+#include <cstdio>
+#include <execinfo.h>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -12,6 +16,22 @@
 namespace parfem::gpu {
 
 namespace {
+
+void on_segv(int) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  backtrace_symbols_fd(frames, n, 2);
+  std::_Exit(139);
+}
+
+void trace(const char* what) {
+  static const bool on = [] {
+    const bool t = std::getenv("PF_BRIDGE_TRACE") != nullptr;
+    if (t) std::signal(SIGSEGV, on_segv);
+    return t;
+  }();
+  if (on) std::fprintf(stderr, "[parfem::gpu] %s\n", what);
+}
 
 // Plain storage behind one pf_level_desc.
 struct LevelStore {
@@ -163,10 +183,13 @@ Mirror& mirror(MultigridHierarchy& h) {
   int n_dev = 0;
   if (pf_device_count(&n_dev) != PF_OK || n_dev < 1) throw Error("parfem::gpu: no CUDA device");
   auto m = std::make_unique<Mirror>();
+  trace("create");
   m->dev = std::make_unique<parfem_b200::Hierarchy>(rank % n_dev, L, 1, rank, K);
+  trace("created");
   std::vector<LevelStore> stores;
   for (const MultigridLevel& lv : h.levels) stores.push_back(from_level(lv));
   for (int l = 0; l < L; ++l) m->dev->set_level(l, 0, stores[static_cast<size_t>(l)].desc());
+  trace("levels set");
   if (K > 1) {
     // every rank's coarse level, over the reference's own transport (setup only)
     std::vector<Bytes> all = allgather(tp, serialize(stores[0]));
@@ -176,6 +199,7 @@ Mirror& mirror(MultigridHierarchy& h) {
     }
   }
   m->dev->finalize();
+  trace("finalized");
   if (K > 1) {
     ByteWriter w;
     if (rank == 0) {
@@ -214,8 +238,10 @@ SolveStats solve_outer(MultigridHierarchy& h, DistributedVector& x, const Distri
   c.coarse_max_iter = cfg.coarse_max_iter;
   c.outer_tol = cfg.outer_tol;
   c.outer_max_cycles = cfg.outer_max_cycles;
+  trace("upload");
   m.x->upload(x.values);
   m.b->upload(b.values);
+  trace("solve");
   SolveStats out;
   try {
     const parfem_b200::SolveStats s = parfem_b200::solve_outer(*m.dev, *m.x, *m.b, c);
@@ -234,8 +260,10 @@ SolveStats solve_outer(MultigridHierarchy& h, DistributedVector& x, const Distri
   } catch (const parfem_b200::SingularDiagonalError& e) {
     throw SingularDiagonalError(e.what());
   }
+  trace("download");
   m.x->download(x.values);
   x.state = ConsistencyState::Consistent;
+  trace("done");
   return out;
 }
 

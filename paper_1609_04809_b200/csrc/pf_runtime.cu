@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -46,6 +47,12 @@ double wall_now() {
 inline unsigned grid_for(int64_t n) { return static_cast<unsigned>((n + kBlock - 1) / kBlock); }
 
 [[noreturn]] void invalid(const std::string& m) { throw Error(PF_ERR_INVALID_ARGUMENT, m); }
+
+// PF_TRACE=1: one stderr line per major host step (debugging integrations).
+void trace(const char* what) {
+  static const bool on = std::getenv("PF_TRACE") != nullptr;
+  if (on) std::fprintf(stderr, "[pf] %s\n", what);
+}
 [[noreturn]] void state(const std::string& m) { throw Error(PF_ERR_STATE, m); }
 
 struct Launcher {
@@ -852,6 +859,7 @@ pf_hierarchy::GraphEntry& solve_graph(pf_hierarchy* h, pf_vector* x, const pf_ve
                           ":" + std::to_string(cfg.outer_tol);
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) return it->second;
+  trace("solve graph: build");
   pf_hierarchy::GraphEntry e;
   const int top = h->n_levels - 1;
   const size_t state_bytes = sizeof(SolveState) + sizeof(double) * static_cast<size_t>(cfg.outer_max_cycles);
@@ -896,6 +904,7 @@ pf_hierarchy::GraphEntry& solve_graph(pf_hierarchy* h, pf_vector* x, const pf_ve
     }
     g_capture_counter = nullptr;
     PF_CUDA(cudaStreamEndCapture(h->stream, &body));
+    trace("solve graph: head captured");
     cudaGraphNode_t leaf = single_leaf(body);
     cudaGraphNodeParams ip = {};
     ip.type = cudaGraphNodeTypeConditional;
@@ -917,10 +926,12 @@ pf_hierarchy::GraphEntry& solve_graph(pf_hierarchy* h, pf_vector* x, const pf_ve
     }
     g_capture_counter = nullptr;
     PF_CUDA(cudaStreamEndCapture(h->stream, &rest_g));
+    trace("solve graph: body captured");
     cudaGraphNode_t copy = nullptr;
     PF_CUDA(cudaGraphAddMemcpyNode1D(&copy, G, &wnode, 1, e.host_state, e.state, state_bytes,
                                      cudaMemcpyDeviceToHost));
     PF_CUDA(cudaGraphInstantiate(&e.exec, G, 0));
+    trace("solve graph: instantiated");
     e.head_kernels = head;
     e.kernels = rest;
   } catch (...) {
@@ -997,6 +1008,7 @@ void graph_launch(pf_hierarchy* h, pf_hierarchy::GraphEntry& e) {
 
 void solve_outer_dev(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf_multigrid_config& cfg,
                      pf_solve_stats* st, double* residuals, int max_res) {
+  trace("solve_outer_dev");
   validate_cfg(cfg);
   const int top = h->n_levels - 1;
   const double t0 = wall_now();
@@ -1004,8 +1016,10 @@ void solve_outer_dev(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf
   const char* mode = std::getenv("PF_SOLVE_MODE");
   if (h->world == h->n_sub && !(mode && std::string(mode) == "host")) {
     auto& g = solve_graph(h, x, b, cfg);
+    trace("solve graph: launch");
     PF_CUDA(cudaGraphLaunch(g.exec, h->stream));
     sync(h);
+    trace("solve graph: done");
     const auto* ss = static_cast<const SolveState*>(g.host_state);
     const int m = ss->launches - 1;  // cycles completed
     h->launches += g.head_kernels * ss->launches + g.kernels * m;
@@ -1557,6 +1571,7 @@ pf_status pf_v_cycle(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf
 
 pf_status pf_solve_outer(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf_multigrid_config* cfg,
                          pf_solve_stats* stats, double* residuals, int max_residuals) {
+  trace("pf_solve_outer");
   PF_API_BEGIN
   check_level(h, h ? h->n_levels - 1 : 0);
   check_vec(h, x, h->n_levels - 1, "x");
