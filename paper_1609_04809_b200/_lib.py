@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpf_gpu.so")
+LIB_PATH = os.environ.get("PF_LIB_PATH") or os.path.join(HERE, "libpf_gpu.so")  # override: experiments only
 
 # pf_status
 PF_OK = 0

@@ -60,7 +60,8 @@ struct BotLevel {
 struct BotDesc {
   int n_sub;
   int n_levels;  // Lc + 1
-  const CoarseSub* coarse;  // level 0 in CoarseSub form
+  unsigned long long* stamps;  // optional (PF_BOTTOM_PROFILE): globaltimer after each phase
+  CoarsePack coarse;        // level 0 packed for the shared-memory coarse solve
   double* coarse_stats;
   BotLevel lev[kBotMaxLevels];
   BotSub sub[kBotMaxLevels][kBotMaxSubs];
@@ -70,6 +71,56 @@ struct BotCfg {
   int kind, pre, post, local_sweeps, coarse_max_iter;
   double omega, coarse_tol;
 };
+
+// Latency-oriented row routines for the bottom levels, where each phase is a chain of
+// dependent L2 round trips rather than a bandwidth problem: all entries of a row (up to
+// kBotChunk) are loaded in one round, then all x gathers in one round.  Same operations
+// in the same order as row_offdiag / row_dot, so results are bit-identical.
+constexpr int kBotChunk = 28;  // a Q1 row has 27 entries
+
+__device__ __forceinline__ void bot_row_offdiag(const SellView& A, int32_t row, const double* x, double& acc,
+                                                double& diag) {
+  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
+  const int len = A.row_len[row];
+  if (len > kBotChunk) {  // long rows: the bandwidth kernel's loop
+    row_offdiag<false>(A, row, x, acc, diag);
+    return;
+  }
+  int32_t c[kBotChunk];
+  double v[kBotChunk], xv[kBotChunk];
+#pragma unroll
+  for (int k = 0; k < kBotChunk; ++k) {
+    const int64_t e = base + static_cast<int64_t>(k < len ? k : 0) * kSlice;
+    c[k] = A.cols[e];
+    v[k] = A.vals[e];
+  }
+#pragma unroll
+  for (int k = 0; k < kBotChunk; ++k) xv[k] = x[c[k]];
+#pragma unroll
+  for (int k = 0; k < kBotChunk; ++k)
+    if (k < len) {
+      if (c[k] == row)
+        diag = v[k];
+      else
+        acc = __dsub_rn(acc, __dmul_rn(v[k], xv[k]));
+    }
+}
+
+// (measured: the 28-wide unrolled form that helps the sweeps makes the residual,
+// restriction and prolongation phases 2-3x slower; they keep the bandwidth loop)
+__device__ __forceinline__ double bot_row_dot(const SellView& A, int32_t row, const double* x, double acc) {
+  return row_dot<false, false>(A, row, x, acc);
+}
+
+// grid barrier + optional phase timestamp (block 0, thread 0)
+__device__ __forceinline__ void bsync(cg::grid_group& g, const BotDesc& D, int& phase) {
+  g.sync();
+  if (D.stamps && blockIdx.x == 0 && threadIdx.x == 0 && phase < 255) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    D.stamps[++phase] = t;
+  }
+}
 
 __device__ __forceinline__ int bot_find(const BotDesc& D, int l, int32_t row) {
   int s = D.n_sub - 1;
@@ -82,7 +133,7 @@ __device__ __forceinline__ void bot_copy_plan(const BotPlan& P, double* v, int64
 }
 
 __device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps, cg::grid_group& g,
-                           int64_t t, int64_t stride) {
+                           int64_t t, int64_t stride, int& ph) {
   const BotLevel& L = D.lev[l];
   double* bufs[2] = {L.x, L.xa};
   int cur = 0;
@@ -100,11 +151,11 @@ __device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps,
             continue;
           }
           double acc = L.b[r], diag = 0.0;
-          row_offdiag<false>(S.A, lr, src + S.off, acc, diag);
+          bot_row_offdiag(S.A, lr, src + S.off, acc, diag);
           dst[r] = __dadd_rn(__dmul_rn(1.0 - c.omega, xo), __ddiv_rn(__dmul_rn(c.omega, acc), diag));
         }
         cur ^= 1;
-        g.sync();
+        bsync(g, D, ph);
       } else {  // coloured GS / SOR, in place (k_color_sweep)
         const bool sor = c.kind == 2;
         double* x = bufs[cur];
@@ -118,34 +169,34 @@ __device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps,
             for (int64_t lr = r0 + t; lr < r1; lr += stride) {
               const int32_t row = static_cast<int32_t>(lr);
               double acc = bs[row], diag = 0.0;
-              row_offdiag<false>(S.A, row, xs, acc, diag);
+              bot_row_offdiag(S.A, row, xs, acc, diag);
               xs[row] = sor ? __dadd_rn(__dmul_rn(1.0 - c.omega, xs[row]),
                                         __ddiv_rn(__dmul_rn(c.omega, acc), diag))
                             : __ddiv_rn(acc, diag);
             }
           }
-          g.sync();
+          bsync(g, D, ph);
         }
       }
     }
     if (L.ms.n) {
       bot_copy_plan(L.ms, bufs[cur], t, stride);
-      g.sync();
+      bsync(g, D, ph);
     }
     if (L.h1.n) {
       bot_copy_plan(L.h1, bufs[cur], t, stride);
-      g.sync();
+      bsync(g, D, ph);
     }
   }
   if (cur) {
     for (int64_t r = t; r < L.total; r += stride) L.x[r] = L.xa[r];
-    g.sync();
+    bsync(g, D, ph);
   }
 }
 
 // master/slave AccumulateThenScatter on level l (fecomm.cpp:41-62)
 __device__ void bot_accumulate_scatter(const BotDesc& D, int l, double* v, cg::grid_group& g, int64_t t,
-                                       int64_t stride) {
+                                       int64_t stride, int& ph) {
   const BotLevel& L = D.lev[l];
   if (L.acc_n) {
     for (int64_t m = t; m < L.acc_n; m += stride) {
@@ -153,40 +204,56 @@ __device__ void bot_accumulate_scatter(const BotDesc& D, int l, double* v, cg::g
       for (int32_t e = L.acc_off[m]; e < L.acc_off[m + 1]; ++e) acc = __dadd_rn(acc, v[L.acc_src[e]]);
       v[L.acc_dst[m]] = acc;
     }
-    g.sync();
+    bsync(g, D, ph);
   }
   if (L.ms.n) {
     bot_copy_plan(L.ms, v, t, stride);
-    g.sync();
+    bsync(g, D, ph);
   }
 }
 
 // cycle(Lc) (multigrid.cpp:150-190) on levels 0..Lc.  On entry lev[Lc].b holds the
 // restricted residual (Dirichlet entries zeroed, before the master/slave accumulate when
 // `accumulate_top`) and lev[Lc].x is zero.
-__global__ void __launch_bounds__(kBlock) k_bottom(const BotDesc* __restrict__ Dp, BotCfg c,
-                                                   int accumulate_top) {
+__global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __restrict__ Dp, BotCfg c,
+                                                      int accumulate_top) {
   cg::grid_group g = cg::this_grid();
-  const BotDesc& D = *Dp;
+  // The descriptor is read on every row of every phase: keep a per-block copy in
+  // shared memory (the grid barrier invalidates L1, so global reads would go to L2).
+  extern __shared__ __align__(16) unsigned char smem_b[];
+  {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(Dp);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(smem_b);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(BotDesc) / 8); i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+  }
+  const BotDesc& D = *reinterpret_cast<const BotDesc*>(smem_b);
+  unsigned char* smem_coarse = smem_b + ((sizeof(BotDesc) + 15) / 16) * 16;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int top = D.n_levels - 1;
-  if (accumulate_top) bot_accumulate_scatter(D, top, D.lev[top].b, g, t, stride);
+  int ph = 0;
+  if (D.stamps && t == 0) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    D.stamps[0] = t0;
+  }
+  if (accumulate_top) bot_accumulate_scatter(D, top, D.lev[top].b, g, t, stride, ph);
   // descend
   for (int l = top; l >= 1; --l) {
     const BotLevel& L = D.lev[l];
-    bot_smooth(D, l, c, c.pre, g, t, stride);
+    bot_smooth(D, l, c, c.pre, g, t, stride, ph);
     if (L.h2.n) {
       bot_copy_plan(L.h2, L.x, t, stride);
-      g.sync();
+      bsync(g, D, ph);
     }
     // r = b - A x on every row (k_residual)
     for (int64_t r = t; r < L.total; r += stride) {
       const BotSub& S = D.sub[l][bot_find(D, l, static_cast<int32_t>(r))];
       const int32_t lr = static_cast<int32_t>(r - S.off);
-      L.r[r] = __dsub_rn(L.b[r], row_dot<false, false>(S.A, lr, L.x + S.off, 0.0));
+      L.r[r] = __dsub_rn(L.b[r], bot_row_dot(S.A, lr, L.x + S.off, 0.0));
     }
-    g.sync();
+    bsync(g, D, ph);
     // b_c = R r, Dirichlet zeroed, x_c = 0 (k_restrict)
     const BotLevel& C = D.lev[l - 1];
     for (int64_t pr = t; pr < C.total; pr += stride) {
@@ -194,25 +261,25 @@ __global__ void __launch_bounds__(kBlock) k_bottom(const BotDesc* __restrict__ D
       const BotSub& F = D.sub[l][s];
       const BotSub& Sc = D.sub[l - 1][s];
       const int32_t lr = static_cast<int32_t>(pr - Sc.off);
-      const double acc = row_dot<false, false>(F.R, lr, L.r + F.off, 0.0);
+      const double acc = bot_row_dot(F.R, lr, L.r + F.off, 0.0);
       C.b[pr] = Sc.is_dir[lr] ? 0.0 : acc;
       C.x[pr] = 0.0;
     }
-    g.sync();
-    bot_accumulate_scatter(D, l - 1, C.b, g, t, stride);
+    bsync(g, D, ph);
+    bot_accumulate_scatter(D, l - 1, C.b, g, t, stride, ph);
   }
   // level 0: coarse_solve + update_halo2 (multigrid.cpp:153-158)
   {
     const BotLevel& L0 = D.lev[0];
-    if (t == 0)
-      coarse_gs_body(D.coarse, D.n_sub, L0.x, L0.b, L0.ms.dst, L0.ms.src, L0.ms.n, L0.h1.dst, L0.h1.src,
-                     L0.h1.n, c.coarse_tol, c.coarse_max_iter, D.coarse_stats);
-    g.sync();
+    if (blockIdx.x == 0)
+      coarse_gs_smem(D.coarse, L0.x, L0.b, c.coarse_tol, c.coarse_max_iter, D.coarse_stats, smem_coarse);
+    bsync(g, D, ph);
     if (L0.h2.n) {
       bot_copy_plan(L0.h2, L0.x, t, stride);
-      g.sync();
+      bsync(g, D, ph);
     }
   }
+
   // ascend
   for (int l = 1; l <= top; ++l) {
     const BotLevel& L = D.lev[l];
@@ -222,16 +289,17 @@ __global__ void __launch_bounds__(kBlock) k_bottom(const BotDesc* __restrict__ D
       const BotSub& S = D.sub[l][s];
       const int32_t lr = static_cast<int32_t>(r - S.off);
       const double* xc = C.x + D.sub[l - 1][s].off;
-      const double acc = row_dot<false, false>(S.P, lr, xc, 0.0);
+      const double acc = bot_row_dot(S.P, lr, xc, 0.0);
       L.x[r] = __dadd_rn(L.x[r], acc);
     }
-    g.sync();
-    bot_smooth(D, l, c, c.post, g, t, stride);
+    bsync(g, D, ph);
+    bot_smooth(D, l, c, c.post, g, t, stride, ph);
     if (L.h2.n) {
       bot_copy_plan(L.h2, L.x, t, stride);
-      g.sync();
+      bsync(g, D, ph);
     }
   }
+  if (D.stamps && t == 0) D.stamps[255] = static_cast<unsigned long long>(ph);
 }
 
 }  // namespace pf

@@ -418,6 +418,102 @@ __device__ void coarse_gs_body(const CoarseSub* __restrict__ subs, int n_sub, do
   stats[1] = 0;
 }
 
+// coarse_gs_body on a block: all threads stage the packed level in shared memory (one
+// round of parallel loads), thread 0 runs the sequential algorithm there, all threads
+// write x back.  Same operations in the same order as coarse_gs_body.
+__device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __restrict__ b, double tol,
+                               int32_t max_iter, double* stats, unsigned char* smem) {
+  double* sx = reinterpret_cast<double*>(smem);
+  double* sb = sx + P.n_total;
+  double* sv = sb + P.n_rows;
+  int32_t* srp = reinterpret_cast<int32_t*>(sv + P.nnz);
+  int32_t* srd = srp + P.n_rows + 1;
+  int32_t* sc = srd + P.n_rows;
+  int32_t* ssr = sc + P.nnz;
+  int32_t* smd = ssr + P.n_sub + 1;
+  int32_t* sms = smd + P.ms_n;
+  int32_t* shd = sms + P.ms_n;
+  int32_t* shs = shd + P.h1_n;
+  for (int i = threadIdx.x; i < P.n_total; i += blockDim.x) sx[i] = x[i];
+  for (int i = threadIdx.x; i < P.n_rows; i += blockDim.x) {
+    srd[i] = P.rowdev[i];
+    sb[i] = b[P.rowdev[i]];
+  }
+  for (int i = threadIdx.x; i <= P.n_rows; i += blockDim.x) srp[i] = P.rowptr[i];
+  for (int i = threadIdx.x; i < P.nnz; i += blockDim.x) {
+    sv[i] = P.vals[i];
+    sc[i] = P.cols[i];
+  }
+  for (int i = threadIdx.x; i <= P.n_sub; i += blockDim.x) ssr[i] = P.sub_rows[i];
+  for (int i = threadIdx.x; i < P.ms_n; i += blockDim.x) {
+    smd[i] = P.ms_dst[i];
+    sms[i] = P.ms_src[i];
+  }
+  for (int i = threadIdx.x; i < P.h1_n; i += blockDim.x) {
+    shd[i] = P.h1_dst[i];
+    shs[i] = P.h1_src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    auto norm = [&]() {
+      double total = 0.0;
+      for (int s = 0; s < P.n_sub; ++s) {
+        double local = 0.0;
+        for (int32_t i = ssr[s]; i < ssr[s + 1]; ++i) {
+          double acc = sb[i];
+          for (int32_t e = srp[i]; e < srp[i + 1]; ++e) acc = __dsub_rn(acc, __dmul_rn(sv[e], sx[sc[e]]));
+          local = __dadd_rn(local, __dmul_rn(acc, acc));
+        }
+        total = __dadd_rn(total, local);
+      }
+      return sqrt(total);
+    };
+    const double r0 = norm();
+    stats[0] = 0;
+    stats[1] = 1;
+    stats[2] = r0;
+    stats[3] = r0;
+    if (r0 != 0.0) {
+      const double target = __dmul_rn(tol, r0);
+      int it = 0;
+      bool conv = false;
+      while (it < max_iter) {
+        for (int32_t i = 0; i < P.n_rows; ++i) {
+          const int32_t d = srd[i];
+          double acc = sb[i], diag = 0.0;
+          for (int32_t e = srp[i]; e < srp[i + 1]; ++e) {
+            const int32_t c = sc[e];
+            if (c == d)
+              diag = sv[e];
+            else
+              acc = __dsub_rn(acc, __dmul_rn(sv[e], sx[c]));
+          }
+          sx[d] = __ddiv_rn(acc, diag);
+        }
+        for (int32_t i = 0; i < P.ms_n; ++i) sx[smd[i]] = sx[sms[i]];
+        for (int32_t i = 0; i < P.h1_n; ++i) sx[shd[i]] = sx[shs[i]];
+        ++it;
+        const double fr = norm();
+        stats[0] = it;
+        stats[3] = fr;
+        if (fr <= target) {
+          conv = true;
+          break;
+        }
+      }
+      if (!conv) stats[1] = 0;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P.n_total; i += blockDim.x) x[i] = sx[i];
+}
+
+__global__ void k_coarse_smem(CoarsePack P, double* x, const double* __restrict__ b, double tol,
+                              int32_t max_iter, double* stats) {
+  extern __shared__ __align__(16) unsigned char smem_c[];
+  coarse_gs_smem(P, x, b, tol, max_iter, stats, smem_c);
+}
+
 __global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, double* x,
                             const double* __restrict__ b, const int32_t* __restrict__ ms_dst,
                             const int32_t* __restrict__ ms_src, int32_t ms_n,

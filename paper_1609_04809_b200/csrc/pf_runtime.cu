@@ -411,6 +411,55 @@ void build_plans(pf_hierarchy* h, int l) {
   build_exchange(L.host, L.sub, h->rank_base, h->world == h->n_sub, L.scatter, L.accumulate);
 }
 
+// Pack a coarse level (all subdomains of H/D, level-global indices) for the shared-memory
+// coarse solve: own rows per subdomain in host order, entries in stored order.
+CoarsePack make_coarse_pack(const std::vector<HostLevel>& H, const std::vector<DevLevel>& D,
+                            const std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS>& plans,
+                            DevBuf<int32_t>& sub_rows, DevBuf<int32_t>& rowptr, DevBuf<int32_t>& rowdev,
+                            DevBuf<int32_t>& cols, DevBuf<double>& vals) {
+  std::vector<int32_t> sr{0}, rp{0}, rd, cc;
+  std::vector<double> vv;
+  int64_t total = 0;
+  for (size_t s = 0; s < H.size(); ++s) {
+    const HostLevel& h = H[s];
+    const DevLevel& d = D[s];
+    for (int32_t i = 0; i < h.n_own; ++i) {
+      rd.push_back(static_cast<int32_t>(d.offset + d.perm[i]));
+      for (int64_t k = h.rowptr[i]; k < h.rowptr[i + 1]; ++k) {
+        cc.push_back(static_cast<int32_t>(d.offset + d.perm[h.cols[k]]));
+        vv.push_back(h.vals[k]);
+      }
+      rp.push_back(static_cast<int32_t>(cc.size()));
+    }
+    sr.push_back(static_cast<int32_t>(rd.size()));
+    total = std::max<int64_t>(total, d.offset + d.n);
+  }
+  sub_rows.upload(sr);
+  rowptr.upload(rp);
+  rowdev.upload(rd);
+  cols.upload(cc);
+  vals.upload(vv);
+  CoarsePack P{};
+  P.n_total = static_cast<int32_t>(total);
+  P.n_rows = static_cast<int32_t>(rd.size());
+  P.nnz = static_cast<int32_t>(cc.size());
+  P.n_sub = static_cast<int32_t>(H.size());
+  P.sub_rows = sub_rows.p;
+  P.rowptr = rowptr.p;
+  P.rowdev = rowdev.p;
+  P.cols = cols.p;
+  P.vals = vals.p;
+  P.ms_dst = plans[PF_CH_MASTER_SLAVE].dst.p;
+  P.ms_src = plans[PF_CH_MASTER_SLAVE].src.p;
+  P.ms_n = static_cast<int32_t>(plans[PF_CH_MASTER_SLAVE].n);
+  P.h1_dst = plans[PF_CH_HALO1].dst.p;
+  P.h1_src = plans[PF_CH_HALO1].src.p;
+  P.h1_n = static_cast<int32_t>(plans[PF_CH_HALO1].n);
+  return P;
+}
+
+constexpr size_t kCoarseSmemMax = 160 * 1024;  // opt-in shared memory for the coarse pack
+
 HostLevel parse_desc(const pf_level_desc& dd, int me, int world, bool need_p) {
   const pf_level_desc* d = &dd;
   if (d->n_dofs < 0 || d->n_own_dofs < 0 || d->n_own_dofs > d->n_dofs) invalid("bad dof counts");
@@ -477,6 +526,8 @@ void build_replica(pf_hierarchy* h) {
   std::vector<CoarseSub> cs;
   for (DevLevel& D : R.sub) cs.push_back(CoarseSub{view(D.A), D.d_perm.p, D.n_own, D.offset});
   R.subs.upload(cs);
+  R.cpack = make_coarse_pack(R.host, R.sub, R.scatter, R.cp_sub_rows, R.cp_rowptr, R.cp_rowdev, R.cp_cols,
+                             R.cp_vals);
   R.x.alloc(stride * h->world);
   R.b.alloc(stride * h->world);
   R.send.alloc(stride);
@@ -498,7 +549,8 @@ void build_bottom(pf_hierarchy* h) {
   std::memset(&d, 0, sizeof d);
   d.n_sub = h->n_sub;
   d.n_levels = top + 1;
-  d.coarse = h->levels[0].coarse_subs.p;
+  d.coarse = h->levels[0].cpack;
+  if (coarse_pack_smem(d.coarse) > kCoarseSmemMax) return;
   d.coarse_stats = h->levels[0].coarse_stats.p;
   auto plan = [](const ExchangePlan& P) { return BotPlan{P.dst.p, P.src.p, static_cast<int32_t>(P.n)}; };
   int64_t max_total = 0;
@@ -536,11 +588,20 @@ void build_bottom(pf_hierarchy* h) {
       S.off = static_cast<int32_t>(D.offset);
     }
   }
+  if (std::getenv("PF_BOTTOM_PROFILE")) {
+    PF_CUDA(cudaMalloc(&h->bot.stamps, 256 * sizeof(unsigned long long)));
+    PF_CUDA(cudaMemset(h->bot.stamps, 0, 256 * sizeof(unsigned long long)));
+    d.stamps = static_cast<unsigned long long*>(h->bot.stamps);
+  }
   PF_CUDA(cudaMalloc(&h->bot.desc, sizeof(BotDesc)));
   PF_CUDA(cudaMemcpy(h->bot.desc, &d, sizeof d, cudaMemcpyHostToDevice));
   int sms = 0, occ = 0;
   PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-  PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bottom, kBlock, 0));
+  h->bot.smem = ((sizeof(BotDesc) + 15) / 16) * 16 + coarse_pack_smem(d.coarse);
+  if (h->bot.smem > 48 * 1024)
+    PF_CUDA(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(h->bot.smem)));
+  PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bottom, kBlock, h->bot.smem));
   if (occ < 1) return;
   int64_t want = std::max<int64_t>(sms, (max_total + kBlock - 1) / kBlock);
   if (const char* e = std::getenv("PF_BOTTOM_GRID")) want = std::max<int64_t>(1, std::atoll(e));
@@ -707,12 +768,27 @@ void enq_restrict(pf_hierarchy* h, int fine, const double* rf, double* bc, doubl
   }
 }
 
+void enq_coarse_smem(pf_hierarchy* h, const CoarsePack& P, double* x, const double* b, double tol,
+                     int max_iter, double* stats) {
+  const size_t bytes = coarse_pack_smem(P);
+  if (bytes > 48 * 1024)
+    PF_CUDA(cudaFuncSetAttribute(k_coarse_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+  k_coarse_smem<<<1, kBlock, bytes, h->stream>>>(P, x, b, tol, max_iter, stats);
+  PF_CUDA(cudaGetLastError());
+  ++*(g_capture_counter ? g_capture_counter : &h->launches);
+}
+
 // coarse_solve on level l.  cycle_mode: x enters as zero and update_halo2 follows
 // (multigrid.cpp:153-158); returns true when that halo update was already done.
 bool enq_coarse(pf_hierarchy* h, int l, double* x, const double* b, double tol, int max_iter,
                 bool cycle_mode) {
   Level& L = h->levels[l];
   auto launch = launcher(h);
+  if (h->world == h->n_sub && l == 0 && coarse_pack_smem(L.cpack) <= kCoarseSmemMax) {
+    enq_coarse_smem(h, L.cpack, x, b, tol, max_iter, L.coarse_stats.p);
+    return false;
+  }
   if (h->world == h->n_sub) {
     const ExchangePlan& ms = L.scatter[PF_CH_MASTER_SLAVE];
     const ExchangePlan& h1 = L.scatter[PF_CH_HALO1];
@@ -739,11 +815,14 @@ bool enq_coarse(pf_hierarchy* h, int l, double* x, const double* b, double tol, 
   const ExchangePlan& ms = R.scatter[PF_CH_MASTER_SLAVE];
   const ExchangePlan& h1 = R.scatter[PF_CH_HALO1];
   const ExchangePlan& h2 = R.scatter[PF_CH_HALO2];
-  launch(1, 32, k_coarse_gs, static_cast<const CoarseSub*>(R.subs.p), h->world, R.x.p,
-         static_cast<const double*>(R.b.p), static_cast<const int32_t*>(ms.dst.p),
-         static_cast<const int32_t*>(ms.src.p), static_cast<int32_t>(ms.n),
-         static_cast<const int32_t*>(h1.dst.p), static_cast<const int32_t*>(h1.src.p),
-         static_cast<int32_t>(h1.n), tol, max_iter, L.coarse_stats.p);
+  if (coarse_pack_smem(R.cpack) <= kCoarseSmemMax)
+    enq_coarse_smem(h, R.cpack, R.x.p, R.b.p, tol, max_iter, L.coarse_stats.p);
+  else
+    launch(1, 32, k_coarse_gs, static_cast<const CoarseSub*>(R.subs.p), h->world, R.x.p,
+           static_cast<const double*>(R.b.p), static_cast<const int32_t*>(ms.dst.p),
+           static_cast<const int32_t*>(ms.src.p), static_cast<int32_t>(ms.n),
+           static_cast<const int32_t*>(h1.dst.p), static_cast<const int32_t*>(h1.src.p),
+           static_cast<int32_t>(h1.n), tol, max_iter, L.coarse_stats.p);
   if (cycle_mode && h2.n > 0)
     launch(grid_for(h2.n), kBlock, k_copy_idx, static_cast<const int32_t*>(h2.src.p),
            static_cast<const int32_t*>(h2.dst.p), R.x.p, static_cast<int32_t>(h2.n));
@@ -757,6 +836,7 @@ void enq_bottom(pf_hierarchy* h, const pf_multigrid_config& cfg, int accumulate_
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(static_cast<unsigned>(h->bot.grid));
   lc.blockDim = dim3(kBlock);
+  lc.dynamicSmemBytes = h->bot.smem;
   lc.stream = h->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -1122,6 +1202,7 @@ pf_hierarchy::~pf_hierarchy() {
   }
   levels.clear();
   if (bot.desc) cudaFree(bot.desc);
+  if (bot.stamps) cudaFree(bot.stamps);
   xport.reset();
   if (pinned) cudaFreeHost(pinned);
   if (ev0) cudaEventDestroy(ev0);
@@ -1263,6 +1344,9 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
       std::vector<CoarseSub> cs;
       for (DevLevel& D : L.sub) cs.push_back(CoarseSub{view(D.A), D.d_perm.p, D.n_own, D.offset});
       L.coarse_subs.upload(cs);
+      if (h->world == h->n_sub)
+        L.cpack = make_coarse_pack(L.host, L.sub, L.scatter, L.cp_sub_rows, L.cp_rowptr, L.cp_rowdev,
+                                   L.cp_cols, L.cp_vals);
     }
   }
   if (h->world != h->n_sub) build_replica(h);
@@ -1683,6 +1767,14 @@ pf_status pf_time_vcycle(pf_hierarchy* h, pf_vector* x, const pf_vector* b, cons
   float ms = 0;
   PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   *mean_ms = ms / iters;
+  if (h->bot.stamps) {  // PF_BOTTOM_PROFILE: per-phase times of the last bottom launch
+    unsigned long long st[256];
+    PF_CUDA(cudaMemcpy(st, h->bot.stamps, sizeof st, cudaMemcpyDeviceToHost));
+    const int n = static_cast<int>(st[255]);
+    std::fprintf(stderr, "[pf] bottom: %d phases, total %.2f us:", n, (st[n] - st[0]) / 1e3);
+    for (int i = 1; i <= n; ++i) std::fprintf(stderr, " %.2f", (st[i] - st[i - 1]) / 1e3);
+    std::fprintf(stderr, "\n");
+  }
   PF_API_END
 }
 

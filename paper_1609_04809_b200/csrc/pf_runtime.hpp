@@ -138,6 +138,10 @@ struct Level {
   DevBuf<double> norm;          // allreduced norm
   DevBuf<double> coarse_stats;  // [iterations, converged, r0, final]
   DevBuf<CoarseSub> coarse_subs;  // level 0 only
+  // level 0 packed for the shared-memory coarse solve (k_coarse_smem / k_bottom)
+  DevBuf<int32_t> cp_sub_rows, cp_rowptr, cp_rowdev, cp_cols;
+  DevBuf<double> cp_vals;
+  CoarsePack cpack{};
   pf_vector* x = nullptr;       // MultigridLevel::x, b (cycle scratch)
   pf_vector* b = nullptr;
 };
@@ -189,13 +193,18 @@ struct pf_hierarchy {
     pf::ExchangePlan acc;
     pf::DevBuf<pf::CoarseSub> subs;
     pf::DevBuf<double> x, b, send;
+    pf::DevBuf<int32_t> cp_sub_rows, cp_rowptr, cp_rowdev, cp_cols;
+    pf::DevBuf<double> cp_vals;
+    pf::CoarsePack cpack{};
   } rep;
   // Levels 0..top of the V-cycle run in one cooperative kernel (pf_bottom.cuh).
   struct Bottom {
     bool active = false;
     int top = -1;
     int grid = 0;
+    size_t smem = 0;       // dynamic shared memory: descriptor copy + coarse pack
     void* desc = nullptr;  // device BotDesc
+    void* stamps = nullptr;  // PF_BOTTOM_PROFILE phase timestamps
     std::vector<pf::DevBuf<int32_t>> color_bufs;
   } bot;
   ~pf_hierarchy();
