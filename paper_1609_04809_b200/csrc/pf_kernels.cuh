@@ -24,26 +24,16 @@ namespace pf {
 
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
-__device__ __forceinline__ uint16_t ld_stream(const uint16_t* p) { return __ldcs(p); }
 
 // acc := acc - sum_{c != row} a_rc x_c over the row's entries in stored order; diag := a_rr.
 // This is the inner loop of one_local_sweep (solvers.cpp:21-51).
-// Column of entry j of a row whose entry 0 sits at `e0 = slice_ptr[s] + lane`.
-__device__ __forceinline__ int32_t sell_col(const SellView& A, bool packed, int64_t sb, int64_t e, int j) {
-  return packed ? __ldg(A.sbase + sb + j) + static_cast<int32_t>(ld_stream(A.cols16 + e))
-                : ld_stream(A.cols + e);
-}
-
 template <bool kReadOnlyX, bool kRes = false>
 __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, const double* x,
                                             double& acc, double& diag, double* res = nullptr,
                                             double x_row = 0.0) {
   // kRes: *res (starting at b_r) also subtracts every product in stored order, the
   // diagonal included — the reference's residual_norm row (linalg.cpp:66-70) bit for bit.
-  const int64_t sp = A.slice_ptr[row >> 5];
-  const int64_t base = sp + (row & 31);
-  const int64_t sb = sp >> 5;
-  const bool packed = A.smode && A.smode[row >> 5];
+  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
   const int len = A.row_len[row];
   double r = kRes ? *res : 0.0;
   int j = 0;
@@ -55,7 +45,7 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
       const int64_t e = base + static_cast<int64_t>(j + k) * kSlice;
-      c[k] = sell_col(A, packed, sb, e, j + k);
+      c[k] = ld_stream(A.cols + e);
       v[k] = ld_stream(A.vals + e);
     }
 #pragma unroll
@@ -73,7 +63,7 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
   }
   for (; j < len; ++j) {
     const int64_t e = base + static_cast<int64_t>(j) * kSlice;
-    const int32_t c = sell_col(A, packed, sb, e, j);
+    const int32_t c = ld_stream(A.cols + e);
     const double v = ld_stream(A.vals + e);
     const double p = __dmul_rn(v, c == row ? x_row : (kReadOnlyX ? __ldg(x + c) : x[c]));
     if (kRes) r = __dsub_rn(r, p);
@@ -91,10 +81,7 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
 template <bool kSubtract, bool kReadOnlyX = true>
 __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const double* __restrict__ x,
                                           double acc) {
-  const int64_t sp = A.slice_ptr[row >> 5];
-  const int64_t base = sp + (row & 31);
-  const int64_t sb = sp >> 5;
-  const bool packed = A.smode && A.smode[row >> 5];
+  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
   const int len = A.row_len[row];
   int j = 0;
   for (; j + kUnroll <= len; j += kUnroll) {
@@ -103,7 +90,7 @@ __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const 
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
       const int64_t e = base + static_cast<int64_t>(j + k) * kSlice;
-      c[k] = sell_col(A, packed, sb, e, j + k);
+      c[k] = ld_stream(A.cols + e);
       v[k] = ld_stream(A.vals + e);
     }
 #pragma unroll
@@ -114,7 +101,7 @@ __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const 
   }
   for (; j < len; ++j) {
     const int64_t e = base + static_cast<int64_t>(j) * kSlice;
-    const int32_t c = sell_col(A, packed, sb, e, j);
+    const int32_t c = ld_stream(A.cols + e);
     const double p = __dmul_rn(ld_stream(A.vals + e), kReadOnlyX ? __ldg(x + c) : x[c]);
     acc = kSubtract ? __dsub_rn(acc, p) : __dadd_rn(acc, p);
   }

@@ -72,9 +72,7 @@ thread_local int64_t* g_capture_counter = nullptr;
 
 Launcher launcher(pf_hierarchy* h) { return Launcher{h, g_capture_counter ? g_capture_counter : &h->launches}; }
 
-SellView view(const DevSell& s) {
-  return SellView{s.vals.p, s.cols.p, s.slice_ptr.p, s.row_len.p, s.cols16.p, s.sbase.p, s.smode.p};
-}
+SellView view(const DevSell& s) { return SellView{s.vals.p, s.cols.p, s.slice_ptr.p, s.row_len.p}; }
 
 void check_level(const pf_hierarchy* h, int level) {
   if (!h) invalid("null hierarchy");
@@ -129,47 +127,6 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
   out.cols.upload(sc);
   out.nnz = n > 0 ? off[n] : 0;
   out.stored = sptr[n_slices];
-  out.slices = n_slices;
-  // column compression: per (slice, entry position) a base, per entry a 16-bit offset,
-  // for every slice whose columns of each entry position span < 65536
-  bool compress = true;
-  if (const char* e = std::getenv("PF_SELL_COMPRESS")) compress = std::atoi(e) != 0;
-  if (!compress || n_slices == 0) return;
-  std::vector<uint16_t> c16(static_cast<size_t>(sptr[n_slices]), 0);
-  std::vector<int32_t> base(static_cast<size_t>(sptr[n_slices] / kSlice), 0);
-  std::vector<uint8_t> mode(static_cast<size_t>(n_slices), 0);
-  int64_t nc = 0;
-  for (int64_t s = 0; s < n_slices; ++s) {
-    const int64_t w = (sptr[s + 1] - sptr[s]) / kSlice;
-    bool ok = true;
-    for (int64_t j = 0; j < w && ok; ++j) {
-      int64_t lo = INT64_MAX, hi = INT64_MIN;
-      for (int l = 0; l < kSlice; ++l) {
-        const int64_t d = s * kSlice + l;
-        if (d >= n || j >= rlen[d]) continue;
-        const int64_t c = sc[sptr[s] + j * kSlice + l];
-        lo = std::min(lo, c);
-        hi = std::max(hi, c);
-      }
-      if (lo == INT64_MAX) lo = hi = 0;
-      if (hi - lo > 65535) ok = false;
-      base[sptr[s] / kSlice + j] = static_cast<int32_t>(lo);
-    }
-    if (!ok) continue;
-    for (int64_t j = 0; j < w; ++j)
-      for (int l = 0; l < kSlice; ++l) {
-        const int64_t e = sptr[s] + j * kSlice + l;
-        const int64_t d = s * kSlice + l;
-        c16[e] = (d < n && j < rlen[d]) ? static_cast<uint16_t>(sc[e] - base[sptr[s] / kSlice + j]) : 0;
-      }
-    mode[s] = 1;
-    ++nc;
-  }
-  out.compressed_slices = nc;
-  if (nc == 0) return;
-  out.cols16.upload(c16);
-  out.sbase.upload(base);
-  out.smode.upload(mode);
 }
 
 // Device layout of one subdomain level: own rows colour-major (stable in host order),
@@ -233,27 +190,8 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
   D.perm.assign(static_cast<size_t>(n), 0);
   std::vector<int32_t> inv(static_cast<size_t>(n), 0);
   {
-    // inside a colour, rows are grouped by their "non-own pattern" (which entry positions
-    // reference non-own dofs, i.e. Dirichlet / slave / halo columns numbered after the own
-    // block) and keep host order within a group: interior rows form long runs whose
-    // columns per entry position are close together, which is what the 16-bit column
-    // compression needs.  Row order never changes results (Jacobi reads only the old
-    // iterate; rows of one colour never couple).
-    std::vector<uint64_t> key(static_cast<size_t>(n_own), 0);
-    for (int32_t i = 0; i < n_own; ++i) {
-      uint64_t m = 0;
-      const int64_t len = H.rowptr[i + 1] - H.rowptr[i];
-      for (int64_t j = 0; j < len && j < 56; ++j)
-        if (H.cols[H.rowptr[i] + j] >= n_own) m |= uint64_t(1) << j;
-      key[i] = (m << 6) | static_cast<uint64_t>(std::min<int64_t>(len, 63));
-    }
-    std::vector<int32_t> order(static_cast<size_t>(n_own));
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-      if (color[a] != color[b]) return color[a] < color[b];
-      return key[a] < key[b];
-    });
-    for (int32_t pos = 0; pos < n_own; ++pos) D.perm[order[pos]] = pos;
+    std::vector<int32_t> next(D.color_start.begin(), D.color_start.end() - 1);
+    for (int32_t i = 0; i < n_own; ++i) D.perm[i] = next[color[i]]++;
     for (int32_t i = n_own; i < n; ++i) D.perm[i] = i;
     for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
   }
@@ -274,9 +212,6 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
       off[d + 1] = static_cast<int64_t>(col.size());
     }
     sell_from_rows(n, off, col, val, D.A);
-    if (std::getenv("PF_TRACE"))
-      std::fprintf(stderr, "[pf] level %d: %d rows, %lld/%lld slices column-compressed\n", level, n,
-                   static_cast<long long>(D.A.compressed_slices), static_cast<long long>(D.A.slices));
   }
   D.A.own_nnz = H.rowptr[n_own];
   {

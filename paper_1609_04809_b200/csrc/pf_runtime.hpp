@@ -81,11 +81,7 @@ struct DevSell {
   DevBuf<int32_t> cols;
   DevBuf<int64_t> slice_ptr;
   DevBuf<int32_t> row_len;
-  DevBuf<uint16_t> cols16;  // compressed columns (see SellView)
-  DevBuf<int32_t> sbase;
-  DevBuf<uint8_t> smode;
   int64_t nnz = 0, own_nnz = 0, stored = 0;
-  int64_t compressed_slices = 0, slices = 0;
 };
 
 // One subdomain of one level on the device.

@@ -25,12 +25,6 @@ struct SellView {
   const int32_t* __restrict__ cols;
   const int64_t* __restrict__ slice_ptr;
   const int32_t* __restrict__ row_len;
-  // Column compression (null when off): slice s with smode[s] = 1 stores entry e's column
-  // as sbase[slice_ptr[s] / 32 + j] + cols16[e] (j = entry position inside the row);
-  // the bandwidth kernels then read 2 B instead of 4 B per entry.
-  const uint16_t* __restrict__ cols16;
-  const int32_t* __restrict__ sbase;
-  const uint8_t* __restrict__ smode;
 };
 
 // One subdomain of the coarse level, for the sequential coarse solve.
