@@ -59,7 +59,8 @@ struct BotLevel {
 
 struct BotDesc {
   int n_sub;
-  int n_levels;  // Lc + 1
+  int n_levels;   // Lc + 1
+  int block_top;  // highest level small enough for block 0 alone (block barriers), -1: none
   unsigned long long* stamps;  // optional (PF_BOTTOM_PROFILE): globaltimer after each phase
   CoarsePack coarse;        // level 0 packed for the shared-memory coarse solve
   double* coarse_stats;
@@ -70,6 +71,7 @@ struct BotDesc {
 struct BotCfg {
   int kind, pre, post, local_sweeps, coarse_max_iter;
   double omega, coarse_tol;
+  int block_top;  // levels 0..block_top inside block 0 (-1: none); chosen per smoother
 };
 
 // Latency-oriented row routines for the bottom levels, where each phase is a chain of
@@ -122,6 +124,18 @@ __device__ __forceinline__ void bsync(cg::grid_group& g, const BotDesc& D, int& 
   }
 }
 
+// A team is whoever executes a phase: the whole grid (grid barrier between phases) or,
+// for the tiniest levels, block 0 alone (__syncthreads, ~20x cheaper than a grid barrier).
+struct GridTeam {
+  cg::grid_group g;
+  int64_t t, stride;
+  __device__ void sync(const BotDesc& D, int& ph) { bsync(g, D, ph); }
+};
+struct BlockTeam {
+  int64_t t, stride;
+  __device__ void sync(const BotDesc&, int&) { __syncthreads(); }
+};
+
 __device__ __forceinline__ int bot_find(const BotDesc& D, int l, int32_t row) {
   int s = D.n_sub - 1;
   while (s > 0 && row < D.sub[l][s].off) --s;
@@ -132,8 +146,9 @@ __device__ __forceinline__ void bot_copy_plan(const BotPlan& P, double* v, int64
   for (int64_t i = t; i < P.n; i += stride) v[P.dst[i]] = v[P.src[i]];
 }
 
-__device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps, cg::grid_group& g,
-                           int64_t t, int64_t stride, int& ph) {
+template <class Team>
+__device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps, Team& T, int& ph) {
+  const int64_t t = T.t, stride = T.stride;
   const BotLevel& L = D.lev[l];
   double* bufs[2] = {L.x, L.xa};
   int cur = 0;
@@ -155,7 +170,7 @@ __device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps,
           dst[r] = __dadd_rn(__dmul_rn(1.0 - c.omega, xo), __ddiv_rn(__dmul_rn(c.omega, acc), diag));
         }
         cur ^= 1;
-        bsync(g, D, ph);
+        T.sync(D, ph);
       } else {  // coloured GS / SOR, in place (k_color_sweep)
         const bool sor = c.kind == 2;
         double* x = bufs[cur];
@@ -175,28 +190,29 @@ __device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps,
                             : __ddiv_rn(acc, diag);
             }
           }
-          bsync(g, D, ph);
+          T.sync(D, ph);
         }
       }
     }
     if (L.ms.n) {
       bot_copy_plan(L.ms, bufs[cur], t, stride);
-      bsync(g, D, ph);
+      T.sync(D, ph);
     }
     if (L.h1.n) {
       bot_copy_plan(L.h1, bufs[cur], t, stride);
-      bsync(g, D, ph);
+      T.sync(D, ph);
     }
   }
   if (cur) {
     for (int64_t r = t; r < L.total; r += stride) L.x[r] = L.xa[r];
-    bsync(g, D, ph);
+    T.sync(D, ph);
   }
 }
 
 // master/slave AccumulateThenScatter on level l (fecomm.cpp:41-62)
-__device__ void bot_accumulate_scatter(const BotDesc& D, int l, double* v, cg::grid_group& g, int64_t t,
-                                       int64_t stride, int& ph) {
+template <class Team>
+__device__ void bot_accumulate_scatter(const BotDesc& D, int l, double* v, Team& T, int& ph) {
+  const int64_t t = T.t, stride = T.stride;
   const BotLevel& L = D.lev[l];
   if (L.acc_n) {
     for (int64_t m = t; m < L.acc_n; m += stride) {
@@ -204,20 +220,86 @@ __device__ void bot_accumulate_scatter(const BotDesc& D, int l, double* v, cg::g
       for (int32_t e = L.acc_off[m]; e < L.acc_off[m + 1]; ++e) acc = __dadd_rn(acc, v[L.acc_src[e]]);
       v[L.acc_dst[m]] = acc;
     }
-    bsync(g, D, ph);
+    T.sync(D, ph);
   }
   if (L.ms.n) {
     bot_copy_plan(L.ms, v, t, stride);
-    bsync(g, D, ph);
+    T.sync(D, ph);
+  }
+}
+
+// Descending half of cycle(l) (multigrid.cpp:160-179): pre-smooth, halo2, residual,
+// restriction to l-1 (Dirichlet zeroed, coarse x = 0), master/slave accumulate on l-1.
+template <class Team>
+__device__ void bot_descend(const BotDesc& D, int l, const BotCfg& c, Team& T, int& ph) {
+  const int64_t t = T.t, stride = T.stride;
+  const BotLevel& L = D.lev[l];
+  bot_smooth(D, l, c, c.pre, T, ph);
+  if (L.h2.n) {
+    bot_copy_plan(L.h2, L.x, t, stride);
+    T.sync(D, ph);
+  }
+  for (int64_t r = t; r < L.total; r += stride) {  // r = b - A x on every row (k_residual)
+    const BotSub& S = D.sub[l][bot_find(D, l, static_cast<int32_t>(r))];
+    const int32_t lr = static_cast<int32_t>(r - S.off);
+    L.r[r] = __dsub_rn(L.b[r], bot_row_dot(S.A, lr, L.x + S.off, 0.0));
+  }
+  T.sync(D, ph);
+  const BotLevel& C = D.lev[l - 1];
+  for (int64_t pr = t; pr < C.total; pr += stride) {  // b_c = R r (k_restrict)
+    const int s = bot_find(D, l - 1, static_cast<int32_t>(pr));
+    const BotSub& F = D.sub[l][s];
+    const BotSub& Sc = D.sub[l - 1][s];
+    const int32_t lr = static_cast<int32_t>(pr - Sc.off);
+    const double acc = bot_row_dot(F.R, lr, L.r + F.off, 0.0);
+    C.b[pr] = Sc.is_dir[lr] ? 0.0 : acc;
+    C.x[pr] = 0.0;
+  }
+  T.sync(D, ph);
+  bot_accumulate_scatter(D, l - 1, C.b, T, ph);
+}
+
+// Ascending half of cycle(l) (multigrid.cpp:183-189): x += P x_c, post-smooth, halo2.
+template <class Team>
+__device__ void bot_ascend(const BotDesc& D, int l, const BotCfg& c, Team& T, int& ph) {
+  const int64_t t = T.t, stride = T.stride;
+  const BotLevel& L = D.lev[l];
+  const BotLevel& C = D.lev[l - 1];
+  for (int64_t r = t; r < L.total; r += stride) {
+    const int s = bot_find(D, l, static_cast<int32_t>(r));
+    const BotSub& S = D.sub[l][s];
+    const int32_t lr = static_cast<int32_t>(r - S.off);
+    const double acc = bot_row_dot(S.P, lr, C.x + D.sub[l - 1][s].off, 0.0);
+    L.x[r] = __dadd_rn(L.x[r], acc);
+  }
+  T.sync(D, ph);
+  bot_smooth(D, l, c, c.post, T, ph);
+  if (L.h2.n) {
+    bot_copy_plan(L.h2, L.x, t, stride);
+    T.sync(D, ph);
+  }
+}
+
+// Level 0: coarse_solve + update_halo2 (multigrid.cpp:153-158).  Block 0 runs the
+// shared-memory solve; every thread of the team then meets at the team barrier.
+template <class Team>
+__device__ void bot_coarse(const BotDesc& D, const BotCfg& c, Team& T, int& ph, unsigned char* smem_coarse) {
+  const BotLevel& L0 = D.lev[0];
+  if (blockIdx.x == 0)
+    coarse_gs_smem(D.coarse, L0.x, L0.b, c.coarse_tol, c.coarse_max_iter, D.coarse_stats, smem_coarse);
+  T.sync(D, ph);
+  if (L0.h2.n) {
+    bot_copy_plan(L0.h2, L0.x, T.t, T.stride);
+    T.sync(D, ph);
   }
 }
 
 // cycle(Lc) (multigrid.cpp:150-190) on levels 0..Lc.  On entry lev[Lc].b holds the
 // restricted residual (Dirichlet entries zeroed, before the master/slave accumulate when
-// `accumulate_top`) and lev[Lc].x is zero.
+// `accumulate_top`) and lev[Lc].x is zero.  Levels above block_top run with the whole
+// grid; levels 0..block_top (at most a few hundred rows each) run inside block 0.
 __global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __restrict__ Dp, BotCfg c,
                                                       int accumulate_top) {
-  cg::grid_group g = cg::this_grid();
   // The descriptor is read on every row of every phase: keep a per-block copy in
   // shared memory (the grid barrier invalidates L1, so global reads would go to L2).
   extern __shared__ __align__(16) unsigned char smem_b[];
@@ -229,77 +311,32 @@ __global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __restrict_
   }
   const BotDesc& D = *reinterpret_cast<const BotDesc*>(smem_b);
   unsigned char* smem_coarse = smem_b + ((sizeof(BotDesc) + 15) / 16) * 16;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  GridTeam G{cg::this_grid(), static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+             static_cast<int64_t>(gridDim.x) * blockDim.x};
   const int top = D.n_levels - 1;
   int ph = 0;
-  if (D.stamps && t == 0) {
+  if (D.stamps && G.t == 0) {
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     D.stamps[0] = t0;
   }
-  if (accumulate_top) bot_accumulate_scatter(D, top, D.lev[top].b, g, t, stride, ph);
-  // descend
-  for (int l = top; l >= 1; --l) {
-    const BotLevel& L = D.lev[l];
-    bot_smooth(D, l, c, c.pre, g, t, stride, ph);
-    if (L.h2.n) {
-      bot_copy_plan(L.h2, L.x, t, stride);
-      bsync(g, D, ph);
+  if (accumulate_top) bot_accumulate_scatter(D, top, D.lev[top].b, G, ph);
+  const int bt = c.block_top < D.block_top ? c.block_top : D.block_top;
+  for (int l = top; l > bt && l >= 1; --l) bot_descend(D, l, c, G, ph);
+  if (bt >= 0) {
+    if (blockIdx.x == 0) {
+      BlockTeam B{threadIdx.x, blockDim.x};
+      int bph = 0;
+      for (int l = bt; l >= 1; --l) bot_descend(D, l, c, B, bph);
+      bot_coarse(D, c, B, bph, smem_coarse);
+      for (int l = 1; l <= bt; ++l) bot_ascend(D, l, c, B, bph);
     }
-    // r = b - A x on every row (k_residual)
-    for (int64_t r = t; r < L.total; r += stride) {
-      const BotSub& S = D.sub[l][bot_find(D, l, static_cast<int32_t>(r))];
-      const int32_t lr = static_cast<int32_t>(r - S.off);
-      L.r[r] = __dsub_rn(L.b[r], bot_row_dot(S.A, lr, L.x + S.off, 0.0));
-    }
-    bsync(g, D, ph);
-    // b_c = R r, Dirichlet zeroed, x_c = 0 (k_restrict)
-    const BotLevel& C = D.lev[l - 1];
-    for (int64_t pr = t; pr < C.total; pr += stride) {
-      const int s = bot_find(D, l - 1, static_cast<int32_t>(pr));
-      const BotSub& F = D.sub[l][s];
-      const BotSub& Sc = D.sub[l - 1][s];
-      const int32_t lr = static_cast<int32_t>(pr - Sc.off);
-      const double acc = bot_row_dot(F.R, lr, L.r + F.off, 0.0);
-      C.b[pr] = Sc.is_dir[lr] ? 0.0 : acc;
-      C.x[pr] = 0.0;
-    }
-    bsync(g, D, ph);
-    bot_accumulate_scatter(D, l - 1, C.b, g, t, stride, ph);
+    G.sync(D, ph);
+  } else {
+    bot_coarse(D, c, G, ph, smem_coarse);
   }
-  // level 0: coarse_solve + update_halo2 (multigrid.cpp:153-158)
-  {
-    const BotLevel& L0 = D.lev[0];
-    if (blockIdx.x == 0)
-      coarse_gs_smem(D.coarse, L0.x, L0.b, c.coarse_tol, c.coarse_max_iter, D.coarse_stats, smem_coarse);
-    bsync(g, D, ph);
-    if (L0.h2.n) {
-      bot_copy_plan(L0.h2, L0.x, t, stride);
-      bsync(g, D, ph);
-    }
-  }
-
-  // ascend
-  for (int l = 1; l <= top; ++l) {
-    const BotLevel& L = D.lev[l];
-    const BotLevel& C = D.lev[l - 1];
-    for (int64_t r = t; r < L.total; r += stride) {  // x += P x_c (k_prolong_add)
-      const int s = bot_find(D, l, static_cast<int32_t>(r));
-      const BotSub& S = D.sub[l][s];
-      const int32_t lr = static_cast<int32_t>(r - S.off);
-      const double* xc = C.x + D.sub[l - 1][s].off;
-      const double acc = bot_row_dot(S.P, lr, xc, 0.0);
-      L.x[r] = __dadd_rn(L.x[r], acc);
-    }
-    bsync(g, D, ph);
-    bot_smooth(D, l, c, c.post, g, t, stride, ph);
-    if (L.h2.n) {
-      bot_copy_plan(L.h2, L.x, t, stride);
-      bsync(g, D, ph);
-    }
-  }
-  if (D.stamps && t == 0) D.stamps[255] = static_cast<unsigned long long>(ph);
+  for (int l = (bt >= 0 ? bt + 1 : 1); l <= top; ++l) bot_ascend(D, l, c, G, ph);
+  if (D.stamps && G.t == 0) D.stamps[255] = static_cast<unsigned long long>(ph);
 }
 
 }  // namespace pf
