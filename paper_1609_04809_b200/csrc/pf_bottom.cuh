@@ -300,6 +300,7 @@ __device__ void bot_coarse(const BotDesc& D, const BotCfg& c, Team& T, int& ph, 
 // grid; levels 0..block_top (at most a few hundred rows each) run inside block 0.
 __global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __restrict__ Dp, BotCfg c,
                                                       int accumulate_top) {
+  PF_PDL_ENTRY();
   // The descriptor is read on every row of every phase: keep a per-block copy in
   // shared memory (the grid barrier invalidates L1, so global reads would go to L2).
   extern __shared__ __align__(16) unsigned char smem_b[];

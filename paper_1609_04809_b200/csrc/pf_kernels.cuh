@@ -22,6 +22,16 @@
 
 namespace pf {
 
+// Programmatic dependent launch: every kernel of the chain waits for its predecessor's
+// memory (griddepcontrol.wait — a no-op when launched without the PDL attribute) and then
+// lets its own successor's blocks be scheduled, so launch latency overlaps the previous
+// kernel's tail instead of adding to it.
+#define PF_PDL_ENTRY()                                         \
+  do {                                                         \
+    asm volatile("griddepcontrol.wait;" ::: "memory");         \
+    asm volatile("griddepcontrol.launch_dependents;" :::);     \
+  } while (0)
+
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
 
@@ -116,6 +126,7 @@ __global__ void __launch_bounds__(kBlock) k_jacobi(SellView A, const double* __r
                                                    double* __restrict__ x_new,
                                                    const double* __restrict__ b, int32_t n_own,
                                                    int32_t n, double omega) {
+  PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n) return;
   const double xo = x_old[row];
@@ -146,6 +157,7 @@ struct SolveState {
 __global__ void k_decide(const double* __restrict__ sumsq, int n_parts, double tol, int max_cycles,
                          SolveState* st, cudaGraphConditionalHandle h_while,
                          cudaGraphConditionalHandle h_if) {
+  PF_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0.0;
   for (int i = 0; i < n_parts; ++i) s = __dadd_rn(s, sumsq[i]);
@@ -177,6 +189,7 @@ template <bool kSor>
 __global__ void __launch_bounds__(kBlock) k_color_sweep(SellView A, double* x,
                                                         const double* __restrict__ b, int32_t row0,
                                                         int32_t row1, double omega) {
+  PF_PDL_ENTRY();
   const int32_t row = row0 + blockIdx.x * kBlock + threadIdx.x;
   if (row >= row1) return;
   double acc = b[row], diag = 0.0;
@@ -194,6 +207,7 @@ __global__ void __launch_bounds__(kBlock) k_color_sweep(SellView A, double* x,
 __global__ void __launch_bounds__(kBlock) k_residual(SellView A, const double* __restrict__ x,
                                                      const double* __restrict__ b,
                                                      double* __restrict__ r, int32_t n) {
+  PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n) return;
   r[row] = __dsub_rn(b[row], row_dot<false>(A, row, x, 0.0));
@@ -202,6 +216,7 @@ __global__ void __launch_bounds__(kBlock) k_residual(SellView A, const double* _
 // y = A x on every row (linalg.cpp:45-57).
 __global__ void __launch_bounds__(kBlock) k_spmv(SellView A, const double* __restrict__ x,
                                                  double* __restrict__ y, int32_t n) {
+  PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n) return;
   y[row] = row_dot<false>(A, row, x, 0.0);
@@ -234,6 +249,7 @@ __global__ void __launch_bounds__(kBlock) k_resnorm(SellView A, const double* __
                                                     double* __restrict__ partials,
                                                     unsigned int* ticket, double* sumsq,
                                                     double* norm_out) {
+  PF_PDL_ENTRY();
   __shared__ double smem[kBlock / 32];
   __shared__ bool last;
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
@@ -274,6 +290,7 @@ __global__ void __launch_bounds__(kBlock) k_jacobi_norm(SellView A, const double
                                                         int32_t n, double omega,
                                                         double* __restrict__ partials,
                                                         unsigned int* ticket, double* sumsq) {
+  PF_PDL_ENTRY();
   __shared__ double smem[kBlock / 32];
   __shared__ bool last;
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
@@ -311,6 +328,7 @@ __global__ void __launch_bounds__(kBlock) k_jacobi_norm(SellView A, const double
 // Ordered allreduce of per-subdomain sums: out = sqrt(((0 + s_0) + s_1) + ...)
 // (ascending rank, transport.cpp:139-149), optionally without the sqrt.
 __global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* out, int take_sqrt) {
+  PF_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0.0;
   for (int i = 0; i < n; ++i) s = __dadd_rn(s, parts[i]);
@@ -321,6 +339,7 @@ __global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* o
 // correction is accumulated from 0 in P's entry order, then added.
 __global__ void __launch_bounds__(kBlock) k_prolong_add(SellView P, const double* __restrict__ xc,
                                                         double* __restrict__ xf, int32_t n_f, int add) {
+  PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_f) return;
   const double acc = row_dot<false>(P, row, xc, 0.0);
@@ -338,6 +357,7 @@ __global__ void __launch_bounds__(kBlock) k_restrict(SellView R, const double* _
                                                      double* __restrict__ xc,
                                                      const uint8_t* __restrict__ is_dir_c,
                                                      int32_t n_c, int zero_dirichlet) {
+  PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_c) return;
   const double acc = row_dot<false>(R, row, rf, 0.0);
@@ -510,6 +530,7 @@ __device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __r
 
 __global__ void k_coarse_smem(CoarsePack P, double* x, const double* __restrict__ b, double tol,
                               int32_t max_iter, double* stats) {
+  PF_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem_c[];
   coarse_gs_smem(P, x, b, tol, max_iter, stats, smem_c);
 }
@@ -519,6 +540,7 @@ __global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, doubl
                             const int32_t* __restrict__ ms_src, int32_t ms_n,
                             const int32_t* __restrict__ h1_dst, const int32_t* __restrict__ h1_src,
                             int32_t h1_n, double tol, int32_t max_iter, double* stats) {
+  PF_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   coarse_gs_body(subs, n_sub, x, b, ms_dst, ms_src, ms_n, h1_dst, h1_src, h1_n, tol, max_iter, stats);
 }
@@ -528,20 +550,24 @@ __global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, doubl
 // Host order -> device order: dev[perm[i]] = host[i].
 __global__ void k_scatter_perm(const double* __restrict__ host, const int32_t* __restrict__ perm,
                                double* __restrict__ dev, int32_t n) {
+  PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i < n) dev[perm[i]] = host[i];
 }
 // Device order -> host order: host[i] = dev[perm[i]].
 __global__ void k_gather_perm(const double* __restrict__ dev, const int32_t* __restrict__ perm,
                               double* __restrict__ host, int32_t n) {
+  PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i < n) host[i] = dev[perm[i]];
 }
 __global__ void k_fill(double* __restrict__ v, double value, int64_t n) {
+  PF_PDL_ENTRY();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
   if (i < n) v[i] = value;
 }
 __global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst, int64_t n) {
+  PF_PDL_ENTRY();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
   if (i < n) dst[i] = src[i];
 }
@@ -553,18 +579,21 @@ __global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst,
 // fecomm.cpp:25-39 when every peer lives on this device).
 __global__ void k_copy_idx(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                            double* v, int32_t n) {
+  PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i < n) v[dst[i]] = v[src[i]];
 }
 // Pack: buf[i] = v[idx[i]] (send side of scatter, fecomm.cpp:28-32).
 __global__ void k_pack(const double* __restrict__ v, const int32_t* __restrict__ idx,
                        double* __restrict__ buf, int32_t n) {
+  PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i < n) buf[i] = v[idx[i]];
 }
 // Unpack: v[idx[i]] = buf[i] (receive side of scatter, fecomm.cpp:33-38).
 __global__ void k_unpack(const double* __restrict__ buf, const int32_t* __restrict__ idx,
                          double* __restrict__ v, int32_t n) {
+  PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i < n) v[idx[i]] = buf[i];
 }
@@ -576,6 +605,7 @@ __global__ void k_unpack_accumulate(const double* __restrict__ buf,
                                     const int32_t* __restrict__ src,
                                     const int32_t* __restrict__ dst, double* __restrict__ v,
                                     int32_t n_masters) {
+  PF_PDL_ENTRY();
   const int32_t m = blockIdx.x * kBlock + threadIdx.x;
   if (m >= n_masters) return;
   double acc = v[dst[m]];

@@ -55,14 +55,30 @@ void trace(const char* what) {
 }
 [[noreturn]] void state(const std::string& m) { throw Error(PF_ERR_STATE, m); }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 struct Launcher {
   pf_hierarchy* h;
   int64_t* counter;
-  template <typename Kern, typename... Args>
-  void operator()(unsigned grid, unsigned block, Kern kern, Args... args) {
+  template <typename... KArgs, typename... Args>
+  void operator()(unsigned grid, unsigned block, void (*kern)(KArgs...), Args... args) {
     if (grid == 0) return;
-    kern<<<grid, block, 0, h->stream>>>(args...);
-    PF_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(block);
+    lc.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = pdl_enabled() ? 1 : 0;
+    PF_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...));
     ++*counter;
   }
 };
