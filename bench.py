@@ -198,9 +198,9 @@ def run_b200(args):
     W = WORKLOAD
     t0 = time.time()
     setup = StructuredSetup(W["dim"], W["n_coarse"], W["levels"], world, rank)
-    # multi-process: every rank's level 0 (27 coarse dofs) for the replicated coarse solve
-    replicas = ([StructuredSetup(W["dim"], W["n_coarse"], 1, world, q).levels[0] for q in range(world)]
-                if world > 1 else None)
+    # multi-process: every rank's bottom levels, replicated on each GPU (one allgather per
+    # cycle feeds a redundant bottom V-cycle instead of per-sweep exchanges on tiny levels)
+    replicas = (gmg.replica_levels(W["dim"], W["n_coarse"], W["levels"], world) if world > 1 else None)
     h = gmg.Hierarchy([setup.levels], device=local, rank_base=rank, world_size=world,
                       coarse_replicas=replicas)
     if world > 1:

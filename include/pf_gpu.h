@@ -166,6 +166,12 @@ pf_status pf_hierarchy_init_nccl(pf_hierarchy* h, const void* unique_id, int nby
  * instead of one allreduce and two halo exchanges per coarse iteration; the result is
  * the same bit for bit (same sequential order, same exchange order). */
 pf_status pf_hierarchy_set_coarse_replica(pf_hierarchy* h, int rank, const pf_level_desc* desc);
+/* Multi-process: level `level` of every rank (levels 0..top, all ranks each, set before
+ * finalize; level 0 == pf_hierarchy_set_coarse_replica).  When every replicated level is
+ * small, each GPU runs the whole bottom of the V-cycle (levels 0..top) for all ranks
+ * after ONE allgather of the restricted residual, instead of the per-sweep halo
+ * exchanges the reference performs on those latency-bound levels; bit-identical. */
+pf_status pf_hierarchy_set_replica_level(pf_hierarchy* h, int level, int rank, const pf_level_desc* desc);
 pf_status pf_hierarchy_destroy(pf_hierarchy* h);
 
 /* Single-GPU test bench of the multi-process path: `world_size` single-subdomain

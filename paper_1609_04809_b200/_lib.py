@@ -97,7 +97,8 @@ class SolveStats(C.Structure):
 EXPORTS = [
     "pf_last_error", "pf_version", "pf_device_count", "pf_default_smoother_config", "pf_default_multigrid_config",
     "pf_hierarchy_create", "pf_hierarchy_set_level", "pf_hierarchy_finalize", "pf_nccl_unique_id",
-    "pf_hierarchy_init_nccl", "pf_hierarchy_set_coarse_replica", "pf_hierarchy_destroy",
+    "pf_hierarchy_init_nccl", "pf_hierarchy_set_coarse_replica", "pf_hierarchy_set_replica_level",
+    "pf_hierarchy_destroy",
     "pf_loopback_create", "pf_loopback_destroy", "pf_hierarchy_init_loopback", "pf_hierarchy_device_bytes",
     "pf_vector_create", "pf_vector_destroy", "pf_vector_upload", "pf_vector_download",
     "pf_vector_fill", "pf_vector_copy", "pf_host_alloc", "pf_host_free", "pf_spmv", "pf_residual_norm", "pf_smooth",
@@ -137,6 +138,7 @@ def lib():
         "pf_nccl_unique_id": [P, C.c_int],
         "pf_hierarchy_init_nccl": [P, P, C.c_int],
         "pf_hierarchy_set_coarse_replica": [P, C.c_int, C.POINTER(LevelDesc)],
+        "pf_hierarchy_set_replica_level": [P, C.c_int, C.c_int, C.POINTER(LevelDesc)],
         "pf_loopback_create": [C.c_int, PP],
         "pf_loopback_destroy": [P],
         "pf_hierarchy_init_loopback": [P, P],

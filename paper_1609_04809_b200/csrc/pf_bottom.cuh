@@ -161,7 +161,7 @@ __device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps,
           const BotSub& S = D.sub[l][bot_find(D, l, static_cast<int32_t>(r))];
           const int32_t lr = static_cast<int32_t>(r - S.off);
           const double xo = src[r];
-          if (lr >= S.n_own) {
+          if (lr >= S.n_own) {  // non-own rows (and replica padding) carry over
             dst[r] = xo;
             continue;
           }
@@ -242,6 +242,7 @@ __device__ void bot_descend(const BotDesc& D, int l, const BotCfg& c, Team& T, i
   for (int64_t r = t; r < L.total; r += stride) {  // r = b - A x on every row (k_residual)
     const BotSub& S = D.sub[l][bot_find(D, l, static_cast<int32_t>(r))];
     const int32_t lr = static_cast<int32_t>(r - S.off);
+    if (lr >= S.n) continue;  // padding of a replicated (strided) level
     L.r[r] = __dsub_rn(L.b[r], bot_row_dot(S.A, lr, L.x + S.off, 0.0));
   }
   T.sync(D, ph);
@@ -251,6 +252,7 @@ __device__ void bot_descend(const BotDesc& D, int l, const BotCfg& c, Team& T, i
     const BotSub& F = D.sub[l][s];
     const BotSub& Sc = D.sub[l - 1][s];
     const int32_t lr = static_cast<int32_t>(pr - Sc.off);
+    if (lr >= Sc.n) continue;
     const double acc = bot_row_dot(F.R, lr, L.r + F.off, 0.0);
     C.b[pr] = Sc.is_dir[lr] ? 0.0 : acc;
     C.x[pr] = 0.0;
@@ -269,6 +271,7 @@ __device__ void bot_ascend(const BotDesc& D, int l, const BotCfg& c, Team& T, in
     const int s = bot_find(D, l, static_cast<int32_t>(r));
     const BotSub& S = D.sub[l][s];
     const int32_t lr = static_cast<int32_t>(r - S.off);
+    if (lr >= S.n) continue;
     const double acc = bot_row_dot(S.P, lr, C.x + D.sub[l - 1][s].off, 0.0);
     L.x[r] = __dadd_rn(L.x[r], acc);
   }

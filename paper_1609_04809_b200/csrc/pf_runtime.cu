@@ -524,82 +524,106 @@ HostLevel parse_desc(const pf_level_desc& dd, int me, int world, bool need_p) {
 
 void build_replica(pf_hierarchy* h) {
   auto& R = h->rep;
-  if (R.host.size() != static_cast<size_t>(h->world))
+  if (R.lv.empty() || R.lv[0].host.size() != static_cast<size_t>(h->world))
     state("multi-process hierarchy needs pf_hierarchy_set_coarse_replica for every rank");
-  R.sub.resize(static_cast<size_t>(h->world));
-  int64_t stride = 1;
-  for (int r = 0; r < h->world; ++r) {
-    if (!R.host[r].set) state("coarse replica of rank " + std::to_string(r) + " not set");
-    build_dev_level(R.host[r], R.sub[r], 0);
-    stride = std::max<int64_t>(stride, R.sub[r].n);
+  const int top = static_cast<int>(R.lv.size()) - 1;
+  if (top >= h->n_levels) invalid("more replicated levels than the hierarchy has");
+  int64_t max_stride = 1;
+  for (int l = 0; l <= top; ++l) {
+    auto& RL = R.lv[static_cast<size_t>(l)];
+    if (RL.host.size() != static_cast<size_t>(h->world)) state("replica level " + std::to_string(l) + " incomplete");
+    RL.sub.resize(static_cast<size_t>(h->world));
+    int64_t stride = 1;
+    for (int r = 0; r < h->world; ++r) {
+      if (!RL.host[r].set)
+        state("replica of rank " + std::to_string(r) + " level " + std::to_string(l) + " not set");
+      build_dev_level(RL.host[r], RL.sub[r], l);
+      stride = std::max<int64_t>(stride, RL.sub[r].n);
+    }
+    RL.stride = stride;
+    max_stride = std::max(max_stride, stride);
+    for (int r = 0; r < h->world; ++r) RL.sub[r].offset = r * stride;
+    const DevLevel& mine = h->levels[l].sub[0];
+    if (RL.sub[h->rank_base].n != mine.n || RL.sub[h->rank_base].perm != mine.perm)
+      invalid("replica of this rank differs from its own level " + std::to_string(l));
+    if (l > 0)
+      for (int r = 0; r < h->world; ++r)
+        build_transfer(RL.host[r], RL.sub[r], R.lv[static_cast<size_t>(l - 1)].host[r],
+                       R.lv[static_cast<size_t>(l - 1)].sub[r]);
+    build_exchange(RL.host, RL.sub, 0, true, RL.scatter, RL.acc);
+    RL.x.alloc(2 * stride * h->world);
+    RL.b.alloc(stride * h->world);
+    RL.r.alloc(stride * h->world);
+    PF_CUDA(cudaMemset(RL.x.p, 0, sizeof(double) * 2 * stride * h->world));
+    PF_CUDA(cudaMemset(RL.b.p, 0, sizeof(double) * stride * h->world));
   }
-  R.stride = stride;
-  for (int r = 0; r < h->world; ++r) R.sub[r].offset = r * stride;
-  const DevLevel& mine = h->levels[0].sub[0];
-  if (R.sub[h->rank_base].n != mine.n || R.sub[h->rank_base].perm != mine.perm)
-    invalid("coarse replica of this rank differs from its level 0");
-  build_exchange(R.host, R.sub, 0, true, R.scatter, R.acc);
+  auto& R0 = R.lv[0];
   std::vector<CoarseSub> cs;
-  for (DevLevel& D : R.sub) cs.push_back(CoarseSub{view(D.A), D.d_perm.p, D.n_own, D.offset});
+  for (DevLevel& D : R0.sub) cs.push_back(CoarseSub{view(D.A), D.d_perm.p, D.n_own, D.offset});
   R.subs.upload(cs);
-  R.cpack = make_coarse_pack(R.host, R.sub, R.scatter, R.cp_sub_rows, R.cp_rowptr, R.cp_rowdev, R.cp_cols,
+  R.cpack = make_coarse_pack(R0.host, R0.sub, R0.scatter, R.cp_sub_rows, R.cp_rowptr, R.cp_rowdev, R.cp_cols,
                              R.cp_vals);
-  R.x.alloc(stride * h->world);
-  R.b.alloc(stride * h->world);
-  R.send.alloc(stride);
-  PF_CUDA(cudaMemset(R.send.p, 0, sizeof(double) * stride));
+  R.send.alloc(max_stride);
+  PF_CUDA(cudaMemset(R.send.p, 0, sizeof(double) * max_stride));
+  R.coarse_stats.alloc(4);
+  PF_CUDA(cudaMemset(R.coarse_stats.p, 0, 4 * sizeof(double)));
   R.active = true;
 }
 
-// Levels whose total row count stays below PF_BOTTOM_ROWS (default 65536; 0 disables)
-// run as one cooperative kernel.  Only when every rank of the level lives on this device.
-void build_bottom(pf_hierarchy* h) {
-  int64_t limit = 65536;
-  if (const char* e = std::getenv("PF_BOTTOM_ROWS")) limit = std::atoll(e);
-  if (h->world != h->n_sub || h->n_sub > kBotMaxSubs || limit <= 0) return;
-  int top = -1;
-  for (int l = 0; l < h->n_levels - 1 && l < kBotMaxLevels; ++l)
-    if (h->levels[l].total <= limit) top = l;
-  if (top < 1) return;
+// One level as the bottom kernel sees it.
+struct BotSrc {
+  const std::vector<DevLevel>* sub;
+  int64_t total;
+  const std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS>* scatter;
+  const ExchangePlan* acc;
+  double *x, *xa, *b, *r;
+};
+
+// Fill and upload a BotDesc for levels 0..top = src.size()-1; false if unsupported.
+bool fill_bottom(pf_hierarchy* h, pf_hierarchy::Bottom& bot, const std::vector<BotSrc>& src,
+                 const CoarsePack& pack, double* coarse_stats) {
+  const int top = static_cast<int>(src.size()) - 1;
+  const int n_sub = static_cast<int>(src[0].sub->size());
+  if (top < 1 || top >= kBotMaxLevels || n_sub > kBotMaxSubs) return false;
+  if (coarse_pack_smem(pack) > kCoarseSmemMax) return false;
   BotDesc d;
   std::memset(&d, 0, sizeof d);
-  d.n_sub = h->n_sub;
+  d.n_sub = n_sub;
   d.n_levels = top + 1;
   int64_t block_rows = 1024;
   if (const char* e = std::getenv("PF_BOTTOM_BLOCK_ROWS")) block_rows = std::atoll(e);
   d.block_top = -1;
   for (int l = 0; l <= top; ++l)
-    if (h->levels[l].total <= block_rows) d.block_top = l;
-  d.coarse = h->levels[0].cpack;
-  if (coarse_pack_smem(d.coarse) > kCoarseSmemMax) return;
-  d.coarse_stats = h->levels[0].coarse_stats.p;
+    if (src[l].total <= block_rows) d.block_top = l;
+  d.coarse = pack;
+  d.coarse_stats = coarse_stats;
   auto plan = [](const ExchangePlan& P) { return BotPlan{P.dst.p, P.src.p, static_cast<int32_t>(P.n)}; };
   int64_t max_total = 0;
   for (int l = 0; l <= top; ++l) {
-    Level& L = h->levels[l];
+    const BotSrc& L = src[l];
     BotLevel& B = d.lev[l];
-    B.x = L.x->cur();
-    B.xa = L.x->alt();
-    B.b = L.b->cur();
-    B.r = L.r.p;
+    B.x = L.x;
+    B.xa = L.xa;
+    B.b = L.b;
+    B.r = L.r;
     B.total = static_cast<int32_t>(L.total);
     max_total = std::max(max_total, L.total);
-    B.ms = plan(L.scatter[PF_CH_MASTER_SLAVE]);
-    B.h1 = plan(L.scatter[PF_CH_HALO1]);
-    B.h2 = plan(L.scatter[PF_CH_HALO2]);
-    B.acc_off = L.accumulate.acc_off.p;
-    B.acc_src = L.accumulate.acc_src.p;
-    B.acc_dst = L.accumulate.acc_dst.p;
-    B.acc_n = L.accumulate.n_masters;
-    for (int s = 0; s < h->n_sub; ++s) {
-      DevLevel& D = L.sub[s];
+    B.ms = plan((*L.scatter)[PF_CH_MASTER_SLAVE]);
+    B.h1 = plan((*L.scatter)[PF_CH_HALO1]);
+    B.h2 = plan((*L.scatter)[PF_CH_HALO2]);
+    B.acc_off = L.acc->acc_off.p;
+    B.acc_src = L.acc->acc_src.p;
+    B.acc_dst = L.acc->acc_dst.p;
+    B.acc_n = L.acc->n_masters;
+    for (int s = 0; s < n_sub; ++s) {
+      const DevLevel& D = (*L.sub)[s];
       BotSub& S = d.sub[l][s];
       B.max_colors = std::max(B.max_colors, D.n_colors);
-      h->bot.color_bufs.emplace_back();
-      h->bot.color_bufs.back().upload(D.color_start);
+      bot.color_bufs.emplace_back();
+      bot.color_bufs.back().upload(D.color_start);
       S.A = view(D.A);
       S.host_of_own = D.d_perm.p;
-      S.color_start = h->bot.color_bufs.back().p;
+      S.color_start = bot.color_bufs.back().p;
       S.P = view(D.P);
       S.R = view(D.R);
       S.is_dir = D.d_is_dir.p;
@@ -610,25 +634,66 @@ void build_bottom(pf_hierarchy* h) {
     }
   }
   if (std::getenv("PF_BOTTOM_PROFILE")) {
-    PF_CUDA(cudaMalloc(&h->bot.stamps, 256 * sizeof(unsigned long long)));
-    PF_CUDA(cudaMemset(h->bot.stamps, 0, 256 * sizeof(unsigned long long)));
-    d.stamps = static_cast<unsigned long long*>(h->bot.stamps);
+    PF_CUDA(cudaMalloc(&bot.stamps, 256 * sizeof(unsigned long long)));
+    PF_CUDA(cudaMemset(bot.stamps, 0, 256 * sizeof(unsigned long long)));
+    d.stamps = static_cast<unsigned long long*>(bot.stamps);
   }
-  PF_CUDA(cudaMalloc(&h->bot.desc, sizeof(BotDesc)));
-  PF_CUDA(cudaMemcpy(h->bot.desc, &d, sizeof d, cudaMemcpyHostToDevice));
+  PF_CUDA(cudaMalloc(&bot.desc, sizeof(BotDesc)));
+  PF_CUDA(cudaMemcpy(bot.desc, &d, sizeof d, cudaMemcpyHostToDevice));
   int sms = 0, occ = 0;
   PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-  h->bot.smem = ((sizeof(BotDesc) + 15) / 16) * 16 + coarse_pack_smem(d.coarse);
-  if (h->bot.smem > 48 * 1024)
+  bot.smem = ((sizeof(BotDesc) + 15) / 16) * 16 + coarse_pack_smem(d.coarse);
+  if (bot.smem > 48 * 1024)
     PF_CUDA(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(h->bot.smem)));
-  PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bottom, kBlock, h->bot.smem));
-  if (occ < 1) return;
+                                 static_cast<int>(bot.smem)));
+  PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bottom, kBlock, bot.smem));
+  if (occ < 1) return false;
   int64_t want = std::max<int64_t>(sms, (max_total + kBlock - 1) / kBlock);
   if (const char* e = std::getenv("PF_BOTTOM_GRID")) want = std::max<int64_t>(1, std::atoll(e));
-  h->bot.grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(occ) * sms));
-  h->bot.top = top;
-  h->bot.active = true;
+  bot.grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(occ) * sms));
+  bot.top = top;
+  bot.active = true;
+  return true;
+}
+
+int64_t bottom_row_limit() {
+  int64_t limit = 65536;
+  if (const char* e = std::getenv("PF_BOTTOM_ROWS")) limit = std::atoll(e);
+  return limit;
+}
+
+// Levels whose total row count stays below PF_BOTTOM_ROWS (default 65536; 0 disables)
+// run as one cooperative kernel when every rank of the level lives on this device.
+void build_bottom(pf_hierarchy* h) {
+  const int64_t limit = bottom_row_limit();
+  if (h->world != h->n_sub || limit <= 0) return;
+  int top = -1;
+  for (int l = 0; l < h->n_levels - 1 && l < kBotMaxLevels; ++l)
+    if (h->levels[l].total <= limit) top = l;
+  if (top < 1) return;
+  std::vector<BotSrc> src;
+  for (int l = 0; l <= top; ++l) {
+    Level& L = h->levels[l];
+    src.push_back(BotSrc{&L.sub, L.total, &L.scatter, &L.accumulate, L.x->cur(), L.x->alt(), L.b->cur(), L.r.p});
+  }
+  fill_bottom(h, h->bot, src, h->levels[0].cpack, h->levels[0].coarse_stats.p);
+}
+
+// Multi-process: the bottom kernel over the replicated levels (all ranks on every GPU),
+// if they are all small enough; otherwise only the coarse replica is used.
+void build_rep_bottom(pf_hierarchy* h) {
+  auto& R = h->rep;
+  const int top = static_cast<int>(R.lv.size()) - 1;
+  const int64_t limit = bottom_row_limit();
+  if (top < 1 || top >= h->n_levels - 1 || limit <= 0) return;
+  std::vector<BotSrc> src;
+  for (int l = 0; l <= top; ++l) {
+    auto& RL = R.lv[static_cast<size_t>(l)];
+    const int64_t total = RL.stride * h->world;
+    if (total > limit) return;
+    src.push_back(BotSrc{&RL.sub, total, &RL.scatter, &RL.acc, RL.x.p, RL.x.p + total, RL.b.p, RL.r.p});
+  }
+  fill_bottom(h, R.bot, src, R.cpack, h->levels[0].coarse_stats.p);
 }
 
 // ------------------------------------------------------------------ enqueue --
@@ -822,42 +887,44 @@ bool enq_coarse(pf_hierarchy* h, int l, double* x, const double* b, double tol, 
   }
   if (l != 0) state("multi-process coarse solve runs on level 0 only");
   auto& R = h->rep;
+  auto& R0 = R.lv[0];
   const DevLevel& D = L.sub[0];
   if (!h->xport) state("multi-process hierarchy used before pf_hierarchy_init_nccl");
   // every rank's coarse rhs (and start vector) on every GPU: one allgather each
   enq_copy(h, b, R.send.p, D.n);
-  h->xport->allgather(R.send.p, R.b.p, R.stride, h->stream);
+  h->xport->allgather(R.send.p, R0.b.p, R0.stride, h->stream);
   if (cycle_mode) {
-    PF_CUDA(cudaMemsetAsync(R.x.p, 0, sizeof(double) * R.stride * h->world, h->stream));
+    PF_CUDA(cudaMemsetAsync(R0.x.p, 0, sizeof(double) * R0.stride * h->world, h->stream));
   } else {
     enq_copy(h, x, R.send.p, D.n);
-    h->xport->allgather(R.send.p, R.x.p, R.stride, h->stream);
+    h->xport->allgather(R.send.p, R0.x.p, R0.stride, h->stream);
   }
-  const ExchangePlan& ms = R.scatter[PF_CH_MASTER_SLAVE];
-  const ExchangePlan& h1 = R.scatter[PF_CH_HALO1];
-  const ExchangePlan& h2 = R.scatter[PF_CH_HALO2];
+  const ExchangePlan& ms = R0.scatter[PF_CH_MASTER_SLAVE];
+  const ExchangePlan& h1 = R0.scatter[PF_CH_HALO1];
+  const ExchangePlan& h2 = R0.scatter[PF_CH_HALO2];
   if (coarse_pack_smem(R.cpack) <= kCoarseSmemMax)
-    enq_coarse_smem(h, R.cpack, R.x.p, R.b.p, tol, max_iter, L.coarse_stats.p);
+    enq_coarse_smem(h, R.cpack, R0.x.p, R0.b.p, tol, max_iter, L.coarse_stats.p);
   else
-    launch(1, 32, k_coarse_gs, static_cast<const CoarseSub*>(R.subs.p), h->world, R.x.p,
-           static_cast<const double*>(R.b.p), static_cast<const int32_t*>(ms.dst.p),
+    launch(1, 32, k_coarse_gs, static_cast<const CoarseSub*>(R.subs.p), h->world, R0.x.p,
+           static_cast<const double*>(R0.b.p), static_cast<const int32_t*>(ms.dst.p),
            static_cast<const int32_t*>(ms.src.p), static_cast<int32_t>(ms.n),
            static_cast<const int32_t*>(h1.dst.p), static_cast<const int32_t*>(h1.src.p),
            static_cast<int32_t>(h1.n), tol, max_iter, L.coarse_stats.p);
   if (cycle_mode && h2.n > 0)
     launch(grid_for(h2.n), kBlock, k_copy_idx, static_cast<const int32_t*>(h2.src.p),
-           static_cast<const int32_t*>(h2.dst.p), R.x.p, static_cast<int32_t>(h2.n));
-  enq_copy(h, R.x.p + h->rank_base * R.stride, x, D.n);
+           static_cast<const int32_t*>(h2.dst.p), R0.x.p, static_cast<int32_t>(h2.n));
+  enq_copy(h, R0.x.p + h->rank_base * R0.stride, x, D.n);
   return cycle_mode;
 }
 
 // cycle(bot.top) in one cooperative launch; lev[top].b holds the restricted residual
 // (before the master/slave accumulate when accumulate_top) and lev[top].x is zero.
-void enq_bottom(pf_hierarchy* h, const pf_multigrid_config& cfg, int accumulate_top) {
+void enq_bottom(pf_hierarchy* h, const pf_hierarchy::Bottom& bot, const pf_multigrid_config& cfg,
+                int accumulate_top) {
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(static_cast<unsigned>(h->bot.grid));
+  lc.gridDim = dim3(static_cast<unsigned>(bot.grid));
   lc.blockDim = dim3(kBlock);
-  lc.dynamicSmemBytes = h->bot.smem;
+  lc.dynamicSmemBytes = bot.smem;
   lc.stream = h->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -870,7 +937,7 @@ void enq_bottom(pf_hierarchy* h, const pf_multigrid_config& cfg, int accumulate_
   const int block_top = cfg.smoother.kind == PF_SMOOTHER_JACOBI ? -1 : 1 << 20;
   const BotCfg c{cfg.smoother.kind, cfg.pre_smooth, cfg.post_smooth, cfg.smoother.local_sweeps,
                  cfg.coarse_max_iter, cfg.smoother.damping, cfg.coarse_tol, block_top};
-  PF_CUDA(cudaLaunchKernelEx(&lc, k_bottom, static_cast<const BotDesc*>(h->bot.desc), c, accumulate_top));
+  PF_CUDA(cudaLaunchKernelEx(&lc, k_bottom, static_cast<const BotDesc*>(bot.desc), c, accumulate_top));
   ++*(g_capture_counter ? g_capture_counter : &h->launches);
 }
 
@@ -892,7 +959,19 @@ void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_
   Level& Cl = h->levels[l - 1];
   enq_restrict(h, l, L.r.p, Cl.b->cur(), Cl.x->cur(), 1);
   if (h->bot.active && l - 1 == h->bot.top) {
-    enq_bottom(h, cfg, 1);  // accumulate, cycle(top) ... down to the coarse solve and back
+    enq_bottom(h, h->bot, cfg, 1);  // accumulate, cycle(top) ... down to the coarse solve and back
+  } else if (h->rep.bot.active && l - 1 == h->rep.bot.top) {
+    // multi-process: the restricted partial sums of every rank in one allgather, then the
+    // bottom V-cycle of ALL ranks replayed on this GPU (accumulate included), then this
+    // rank's part of the result (halo2 already consistent) back into the local level
+    auto& RL = h->rep.lv[static_cast<size_t>(l - 1)];
+    const DevLevel& D = Cl.sub[0];
+    if (!h->xport) state("multi-process hierarchy used before pf_hierarchy_init_nccl");
+    enq_copy(h, Cl.b->cur(), h->rep.send.p, D.n);
+    h->xport->allgather(h->rep.send.p, RL.b.p, RL.stride, h->stream);
+    PF_CUDA(cudaMemsetAsync(RL.x.p, 0, sizeof(double) * RL.stride * h->world, h->stream));
+    enq_bottom(h, h->rep.bot, cfg, 1);
+    enq_copy(h, RL.x.p + h->rank_base * RL.stride, Cl.x->cur(), D.n);
   } else {
     enq_update_ms(h, l - 1, Cl.b->cur(), PF_UPDATE_ACCUMULATE_THEN_SCATTER);
     enq_cycle(h, l - 1, Cl.x, Cl.b->cur(), cfg);
@@ -1226,8 +1305,6 @@ pf_hierarchy::~pf_hierarchy() {
     delete L.b;
   }
   levels.clear();
-  if (bot.desc) cudaFree(bot.desc);
-  if (bot.stamps) cudaFree(bot.stamps);
   xport.reset();
   if (pinned) cudaFreeHost(pinned);
   if (ev0) cudaEventDestroy(ev0);
@@ -1326,14 +1403,22 @@ pf_status pf_hierarchy_set_level(pf_hierarchy* h, int level, int sub, const pf_l
   PF_API_END
 }
 
-pf_status pf_hierarchy_set_coarse_replica(pf_hierarchy* h, int rank, const pf_level_desc* d) {
+pf_status pf_hierarchy_set_replica_level(pf_hierarchy* h, int level, int rank, const pf_level_desc* d) {
   PF_API_BEGIN
   if (!h || !d) invalid("null argument");
   if (h->finalized) state("hierarchy already finalized");
   if (rank < 0 || rank >= h->world) invalid("rank out of range");
-  if (h->rep.host.empty()) h->rep.host.resize(static_cast<size_t>(h->world));
-  h->rep.host[rank] = parse_desc(*d, rank, h->world, false);
+  if (level < 0 || level >= h->n_levels) invalid("level out of range");
+  auto& R = h->rep;
+  if (R.lv.size() <= static_cast<size_t>(level)) R.lv.resize(static_cast<size_t>(level) + 1);
+  auto& RL = R.lv[static_cast<size_t>(level)];
+  if (RL.host.empty()) RL.host.resize(static_cast<size_t>(h->world));
+  RL.host[rank] = parse_desc(*d, rank, h->world, level > 0);
   PF_API_END
+}
+
+pf_status pf_hierarchy_set_coarse_replica(pf_hierarchy* h, int rank, const pf_level_desc* d) {
+  return pf_hierarchy_set_replica_level(h, 0, rank, d);
 }
 
 pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
@@ -1381,7 +1466,9 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
     h->levels[l].b = new_vector(h, l);
   }
   build_bottom(h);
+  if (h->world != h->n_sub) build_rep_bottom(h);
   for (Level& L : h->levels) L.host.clear();
+  for (auto& RL : h->rep.lv) RL.host.clear();
   PF_CUDA(cudaStreamSynchronize(h->stream));
   h->finalized = true;
   PF_API_END

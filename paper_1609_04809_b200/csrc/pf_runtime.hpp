@@ -181,22 +181,6 @@ struct pf_hierarchy {
     size_t state_bytes = 0;
   };
   std::map<std::string, GraphEntry> graphs;
-  // Multi-process runs: level 0 of every rank, replicated on each GPU, so the coarse
-  // solve (solvers.cpp:70-92, which communicates every iteration) runs without any
-  // per-iteration collective; one allgather of the coarse rhs feeds it.
-  struct Replica {
-    bool active = false;
-    std::vector<pf::HostLevel> host;  // per world rank
-    std::vector<pf::DevLevel> sub;
-    int64_t stride = 0;               // rank r's entries at [r * stride, r * stride + n_r)
-    std::array<pf::ExchangePlan, PF_NUM_CHANNEL_KINDS> scatter;
-    pf::ExchangePlan acc;
-    pf::DevBuf<pf::CoarseSub> subs;
-    pf::DevBuf<double> x, b, send;
-    pf::DevBuf<int32_t> cp_sub_rows, cp_rowptr, cp_rowdev, cp_cols;
-    pf::DevBuf<double> cp_vals;
-    pf::CoarsePack cpack{};
-  } rep;
   // Levels 0..top of the V-cycle run in one cooperative kernel (pf_bottom.cuh).
   struct Bottom {
     bool active = false;
@@ -206,6 +190,36 @@ struct pf_hierarchy {
     void* desc = nullptr;  // device BotDesc
     void* stamps = nullptr;  // PF_BOTTOM_PROFILE phase timestamps
     std::vector<pf::DevBuf<int32_t>> color_bufs;
+    Bottom() = default;
+    Bottom(const Bottom&) = delete;
+    Bottom& operator=(const Bottom&) = delete;
+    ~Bottom() {
+      if (desc) cudaFree(desc);
+      if (stamps) cudaFree(stamps);
+    }
   } bot;
+  // Multi-process runs: the bottom levels 0..top of EVERY rank, replicated on each GPU.
+  // One allgather of the restricted residual feeds a redundant bottom V-cycle (or, with
+  // only level 0 replicated, the coarse solve), instead of the per-sweep and
+  // per-coarse-iteration exchanges the reference does on those latency-bound levels.
+  struct RepLevel {
+    std::vector<pf::HostLevel> host;  // per world rank
+    std::vector<pf::DevLevel> sub;
+    int64_t stride = 0;               // rank r's entries at [r * stride, r * stride + n_r)
+    std::array<pf::ExchangePlan, PF_NUM_CHANNEL_KINDS> scatter;
+    pf::ExchangePlan acc;
+    pf::DevBuf<double> x, b, r;       // x holds [2 * world * stride] (Jacobi ping-pong)
+  };
+  struct Replica {
+    bool active = false;
+    std::vector<RepLevel> lv;         // levels 0..top
+    pf::DevBuf<pf::CoarseSub> subs;   // level 0, sequential coarse solve fallback
+    pf::DevBuf<int32_t> cp_sub_rows, cp_rowptr, cp_rowdev, cp_cols;
+    pf::DevBuf<double> cp_vals;
+    pf::CoarsePack cpack{};
+    pf::DevBuf<double> send;          // max stride
+    pf::DevBuf<double> coarse_stats;
+    Bottom bot;                       // bottom kernel over the replicated levels
+  } rep;
   ~pf_hierarchy();
 };

@@ -164,11 +164,14 @@ class Hierarchy:
                 d, keep = lv.desc()
                 _lib.check(L.pf_hierarchy_set_level(self._h, l, s, C.byref(d)))
                 del keep
-        if coarse_replicas is not None:  # level 0 of every rank (multi-process runs)
-            for r, lv in enumerate(coarse_replicas):
-                d, keep = lv.desc()
-                _lib.check(L.pf_hierarchy_set_coarse_replica(self._h, r, C.byref(d)))
-                del keep
+        if coarse_replicas is not None:
+            # multi-process runs: coarse_replicas[r] = rank r's level 0, or the list of its
+            # levels 0..top (the replicated bottom of the V-cycle)
+            for r, lvs in enumerate(coarse_replicas):
+                for l, lv in enumerate(lvs if isinstance(lvs, (list, tuple)) else [lvs]):
+                    d, keep = lv.desc()
+                    _lib.check(L.pf_hierarchy_set_replica_level(self._h, l, r, C.byref(d)))
+                    del keep
         if finalize:
             self.finalize()
 
@@ -351,6 +354,20 @@ def solve_outer_host(h: Hierarchy, x_host: list, b_host: list, cfg: MultigridCon
         raise err
     _lib.check(rc)
     return stats
+
+
+def replica_levels(dim: int, n_coarse: int, n_levels: int, world: int, problem: int = 0,
+                   max_rows: int = 65536):
+    """Every rank's bottom levels 0..top for a multi-process hierarchy (coarse_replicas):
+    top is the highest level below the finest whose rows over all ranks stay <= max_rows
+    (those levels then run redundantly on every GPU after one allgather)."""
+    per_rank = [StructuredSetup(dim, n_coarse, max(1, n_levels - 1), world, q, problem).levels
+                for q in range(world)]
+    top = 0
+    for l in range(len(per_rank[0])):
+        if sum(p[l].n for p in per_rank) <= max_rows:
+            top = l
+    return [p[:top + 1] for p in per_rank]
 
 
 def structured_hierarchy(dim: int, n_coarse: int, n_levels: int, n_ranks: int = 1,

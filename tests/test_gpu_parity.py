@@ -210,16 +210,18 @@ def _run_ranks(K, body):
     return out
 
 
-@pytest.mark.parametrize("K,L", [(2, 4), (4, 4), (8, 3), (3, 3)])
+@pytest.mark.parametrize("K,L", [(2, 4), (4, 4), (8, 3), (3, 3), (8, 4)])
 @pytest.mark.parametrize("kind", [gmg.PF_SMOOTHER_JACOBI, gmg.PF_SMOOTHER_MULTICOLOR_SOR], ids=["jacobi", "sor"])
-def test_multiprocess_path_loopback(cuda, K, L, kind):
+@pytest.mark.parametrize("rep", ["coarse", "bottom"])
+def test_multiprocess_path_loopback(cuda, K, L, kind, rep):
     """The one-subdomain-per-process code path (pack/unpack kernels, segment transport,
-    master accumulate from a receive buffer, allgather-based allreduce, replicated coarse
-    solve) with the loopback transport standing in for NCCL: K hierarchies on K threads
-    must reproduce the oracle's K-rank solve bit for bit."""
+    master accumulate from a receive buffer, allgather-based allreduce, the replicated
+    coarse solve or the replicated bottom V-cycle) with the loopback transport standing in
+    for NCCL: K hierarchies on K threads must reproduce the oracle's K-rank solve bit for
+    bit."""
     setups, levels = structured(3, 2, L, K)
     c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
-    replicas = [s[0] for s in levels]
+    replicas = [s[0] for s in levels] if rep == "coarse" else [s[:L - 1] for s in levels]
     hub = gmg.LoopbackHub(K)
 
     def body(r):
