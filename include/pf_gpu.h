@@ -139,6 +139,28 @@ typedef struct {
 typedef struct pf_hierarchy pf_hierarchy;
 typedef struct pf_vector pf_vector;
 
+/* One rank's finest-level load f(t, x) = s(t) * profile(x), profile = F0(pi x) F1(pi y)
+ * [F2(pi z)] multiplied left to right (model.cpp:11-31), as assemble_load evaluates it
+ * over the rank's own cells (assembly.cpp:60-88, :144-160).  Host order; the per-axis
+ * tables make every product the reference forms available bit for bit. */
+typedef struct {
+  int32_t dim;
+  int32_t n_cells;          /* N: cells per axis (table length) */
+  int32_t n_dofs;
+  const int32_t* lattice;   /* [3 * n_dofs] vertex lattice coordinates x, y, z */
+  /* [n_dofs] own cells around the vertex in ascending global cell number: bits 0-3 the
+   * count, cell k in bits 4+3k .. 6+3k, bit a set = the cell's low corner along axis a is
+   * the vertex itself (else vertex - 1).  Rows without own cells, and Dirichlet rows,
+   * have count 0 (their load is never read: apply_dirichlet_rhs overwrites it). */
+  const uint32_t* cells;
+  const double* factor;     /* [3][N][2]: F_a(pi * (lo_a(c) + p_k * h_a(c))) */
+  const double* extent;     /* [3][N]: h_a(c) = hi - lo (volume = (h0 h1) h2) */
+  const double* phi;        /* [8][8]: value of ring vertex v at Gauss point q, phi[q * 8 + v] */
+  double qweight;           /* Gauss weight product: 0.25 (2D) or 0.125 (3D) */
+  const double* boundary;   /* [n_dofs]: profile at the dof coordinates (read on Dirichlet rows) */
+  const uint8_t* is_dirichlet;  /* [n_dofs] */
+} pf_load_desc;
+
 /* Defaults of the reference structs. */
 void pf_default_smoother_config(pf_smoother_config* out);
 void pf_default_multigrid_config(pf_multigrid_config* out);
@@ -255,6 +277,54 @@ pf_status pf_solve_outer(pf_hierarchy* h, pf_vector* x, const pf_vector* b,
 pf_status pf_solve_outer_host(pf_hierarchy* h, double* const* x_host, const double* const* b_host,
                               const pf_multigrid_config* cfg, pf_solve_stats* stats,
                               double* residuals, int max_residuals);
+
+/* ----------------------------------------------------- heat (Crank-Nicolson) -- */
+/* The reference's heat run (heat_rank_body, app.cpp:146-230) on the
+ * device.  Per time step t_{k+1}:
+ *   load_next = assemble_load(f, t_{k+1})                 assembly.cpp:144-160
+ *   b = (M - dt/2 K) u + dt/2 (load_now + load_next)      app.cpp:191-194
+ *   b_D = g(t_{k+1}), u_D = b_D                           app.cpp:195-200
+ *   solve_outer(h, u, b)                                  app.cpp:202-209
+ * Scalars that involve exp() are computed by the caller with the host libm (the
+ * reference's), so each device product equals the reference's. */
+
+typedef struct pf_operator pf_operator;
+/* A second matrix on the sparsity pattern of `level` (all local subdomains), e.g. the CN
+ * right-hand-side operator M - dt/2 K (app.cpp:185-189). */
+pf_status pf_operator_create(pf_hierarchy* h, int level, pf_operator** out);
+/* Values of one subdomain in the CSR entry order of its pf_level_desc. */
+pf_status pf_operator_set_values(pf_operator* op, int subdomain, const double* values, int64_t nnz);
+/* spmv (linalg.cpp:45-57) with this operator: y = Op x on every local row. */
+pf_status pf_operator_apply(pf_operator* op, const pf_vector* x, pf_vector* y);
+pf_status pf_operator_destroy(pf_operator* op);
+
+typedef struct pf_load pf_load;
+pf_status pf_load_create(pf_hierarchy* h, int level, pf_load** out);
+pf_status pf_load_set(pf_load* ld, int subdomain, const pf_load_desc* desc);
+/* assemble_load (assembly.cpp:144-160) with f = source_scale * profile: own-cell Gauss
+ * quadrature per dof, then update_master_slave(AccumulateThenScatter). */
+pf_status pf_load_assemble(pf_load* ld, double source_scale, pf_vector* out);
+/* apply_dirichlet_rhs (assembly.cpp:172-179) with g = dirichlet_scale * profile
+ * (has_dirichlet = 0: g = 0); with u != NULL also u_D = b_D (app.cpp:196-200). */
+pf_status pf_load_apply_dirichlet(pf_load* ld, int has_dirichlet, double dirichlet_scale, pf_vector* b,
+                                  pf_vector* u);
+pf_status pf_load_destroy(pf_load* ld);
+
+/* b = Op u + half_dt (load_now + load_next) on every local row, then the Dirichlet rows
+ * of b and u as pf_load_apply_dirichlet (app.cpp:191-200); one pass over the matrix. */
+pf_status pf_cn_rhs(pf_operator* op, pf_load* ld, const pf_vector* u_in, const pf_vector* load_now,
+                    const pf_vector* load_next, double half_dt, int has_dirichlet, double dirichlet_scale,
+                    pf_vector* b, pf_vector* u);
+
+/* The whole loop (app.cpp:180-213): steps first_step+1 .. first_step+steps from u (in:
+ * u(t_first), out: u(t_last)); load_now in: load(t_first), out: load(t_last).
+ * source_scale[k] / dirichlet_scale[k] belong to step first_step+k+1.  stats / residuals:
+ * the last step's solve.  A step that does not converge returns PF_ERR_NO_CONVERGENCE
+ * with *failed_step = its 1-based index (app.cpp:205-207). */
+pf_status pf_heat_run(pf_hierarchy* h, pf_operator* op, pf_load* ld, pf_vector* u, pf_vector* load_now,
+                      int first_step, int steps, double half_dt, const double* source_scale, int has_dirichlet,
+                      const double* dirichlet_scale, const pf_multigrid_config* cfg,
+                      pf_solve_stats* stats, double* residuals, int max_residuals, int* failed_step);
 
 /* ------------------------------------------------------------- profiling -- */
 

@@ -39,10 +39,17 @@ typedef struct pf_setup pf_setup;
  *           1 = the reference's PoissonProblem (model.cpp:33-43: sin(pi x) cos(pi y)
  *               [cos(pi z)], Dirichlet data from the exact solution);
  *           2 = f = 1, g = 0. */
-enum { PF_PROBLEM_BASELINE = 0, PF_PROBLEM_REFERENCE_POISSON = 1, PF_PROBLEM_UNIT_SOURCE = 2 };
+/*           3 = the reference's HeatProblem (model.cpp:19-31): u = exp(-t/10) sin(pi x)
+ *               cos(pi y) [cos(pi z)], f = (d pi^2 - 1/10) u; every level's system is the
+ *               Crank-Nicolson matrix M + dt/2 K (multigrid.cpp:18-28). */
+enum { PF_PROBLEM_BASELINE = 0, PF_PROBLEM_REFERENCE_POISSON = 1, PF_PROBLEM_UNIT_SOURCE = 2,
+       PF_PROBLEM_HEAT = 3 };
 
 pf_status pf_setup_create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem,
                           pf_setup** out);
+/* Same, with the time step of the heat problem (AppConfig::dt, config.hpp:22). */
+pf_status pf_setup_create_heat(int dim, int n_coarse, int n_levels, int n_ranks, int rank, double dt,
+                               pf_setup** out);
 pf_status pf_setup_destroy(pf_setup* s);
 
 /* Level data in the layout pf_hierarchy_set_level takes; pointers stay valid until
@@ -58,6 +65,19 @@ pf_status pf_setup_rhs(const pf_setup* s, const double** b, const double** x0, i
 /* Global dof count of the finest level ((N+1)^d) and this rank's local counts. */
 pf_status pf_setup_counts(const pf_setup* s, int level, int64_t* n_global, int64_t* n_dofs,
                           int64_t* n_own, int64_t* nnz);
+/* Heat: the finest-level right-hand-side operator M - dt/2 K (app.cpp:185-189), raw rows,
+ * in the CSR entry order of pf_setup_level(finest). */
+pf_status pf_setup_rhs_operator(const pf_setup* s, const double** values, int64_t* nnz);
+/* Finest-level load at time t (assemble_load, assembly.cpp:144-160, after the master /
+ * slave accumulate), host order; Dirichlet rows 0.  n must equal the finest n_dofs. */
+pf_status pf_setup_load_at(const pf_setup* s, double t, double* out, int64_t n);
+/* The device description of the same load (pf_load_set).  Pointers stay valid until
+ * pf_setup_destroy. */
+pf_status pf_setup_load_desc(const pf_setup* s, pf_load_desc* out);
+/* f(t) = source_scale * profile, g(t) = dirichlet_scale * profile (or 0 when
+ * !has_dirichlet), evaluated with this library's libm exactly as model.cpp does. */
+pf_status pf_setup_scales(const pf_setup* s, double t, double* source_scale, int32_t* has_dirichlet,
+                          double* dirichlet_scale);
 /* Seconds spent in pf_setup_create. */
 pf_status pf_setup_seconds(const pf_setup* s, double* out);
 

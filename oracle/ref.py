@@ -67,6 +67,14 @@ def _bind(L):
         L.ref_bench.argtypes = [C.c_int] * 6 + [C.c_double, C.c_int, C.c_int, C.c_double,
                                                 C.c_int, C.c_int, P, P, i64p, C.POINTER(C.c_int)]
         L.ref_set_gpu.argtypes = [C.c_int]
+        L.ref_heat.restype = P
+        L.ref_heat.argtypes = [C.c_int] * 4 + [C.c_double, C.c_double, C.c_int, C.c_double,
+                                               C.c_int, C.c_int, C.c_double]
+        L.ref_heat_info.argtypes = [P, i64p, C.POINTER(C.c_int), P, P, P]
+        L.ref_heat_copy.argtypes = [P, P, P, P]
+        L.ref_heat_free.argtypes = [P]
+        L.ref_set_heat.argtypes = [C.c_double, C.c_int]
+        L.ref_heat_data.argtypes = [P, C.c_int, P, P]
     return L
 
 
@@ -124,12 +132,18 @@ class RefHierarchy:
     K: int
     problem: int
     ranks: list  # ranks[r] = list of RefLevel, 0 = coarsest
-    b: list      # finest rhs per rank
-    x0: list     # finest start vector per rank
+    b: list      # finest rhs per rank (heat: load at t = 0)
+    x0: list     # finest start vector per rank (heat: exact solution at t = 0)
+    rhs_op: list | None = None  # heat: finest M - dt/2 K values per rank
+    loads: list | None = None   # heat: per rank, [n_loads, n_dofs] loads at t_k = k dt
 
 
-def build(dim: int, n_coarse: int, levels: int, K: int, problem: int = 0) -> RefHierarchy:
+def build(dim: int, n_coarse: int, levels: int, K: int, problem: int = 0, *, dt: float = 0.01,
+          n_loads: int = 2) -> RefHierarchy:
+    """problem 3 (heat): the HeatCrankNicolson hierarchy with time step dt, plus the rhs
+    operator and the loads at t_k = k dt, k = 1..n_loads."""
     L = lib()
+    L.ref_set_heat(dt, n_loads)
     h = L.ref_build(dim, n_coarse, levels, K, problem)
     if not h:
         raise RuntimeError(L.ref_last_error().decode())
@@ -171,7 +185,17 @@ def build(dim: int, n_coarse: int, levels: int, K: int, problem: int = 0) -> Ref
             L.ref_rhs(h, r, _ptr(b), _ptr(x0))
             bs.append(b)
             xs.append(x0)
-        return RefHierarchy(dim, n_coarse, levels, K, problem, ranks, bs, xs)
+        out = RefHierarchy(dim, n_coarse, levels, K, problem, ranks, bs, xs)
+        if problem == 3:
+            out.rhs_op, out.loads = [], []
+            for r in range(K):
+                top = ranks[r][-1]
+                op = np.zeros(len(top.vals))
+                ld = np.zeros((n_loads, top.n_dofs))
+                L.ref_heat_data(h, r, _ptr(op), _ptr(ld))
+                out.rhs_op.append(op)
+                out.loads.append(ld)
+        return out
     finally:
         L.ref_free(h)
 
@@ -228,3 +252,29 @@ def key_noise(keys: np.ndarray, salt: int) -> np.ndarray:
     for i in range(len(keys)):
         out[i] = L.ref_key_noise(keys[i].ctypes.data_as(C.POINTER(C.c_int64)), salt)
     return out
+
+
+def heat(dim, n_coarse, levels, K, *, dt=0.01, end_time=0.05, smoother=0, damping=0.8, pre=2,
+         post=2, outer_tol=1e-10):
+    """The reference's own run_heat (app.cpp:146-230, :299-305): Crank-Nicolson over
+    round(end_time/dt) steps.  Returns dict(solution={Key4: value} over all ranks,
+    residuals=last solve's history, l2, linf, phases={...})."""
+    L = lib()
+    hv = L.ref_heat(dim, n_coarse, levels, K, dt, end_time, smoother, damping, pre, post, outer_tol)
+    if not hv:
+        raise RuntimeError(L.ref_last_error().decode())
+    try:
+        n = C.c_int64(0)
+        nr = C.c_int(0)
+        l2, linf, ph = np.zeros(1), np.zeros(1), np.zeros(5)
+        L.ref_heat_info(hv, C.byref(n), C.byref(nr), _ptr(l2), _ptr(linf), _ptr(ph))
+        keys = np.zeros((n.value, 4), np.int64)
+        vals = np.zeros(n.value)
+        res = np.zeros(max(nr.value, 1))
+        L.ref_heat_copy(hv, _ptr(keys), _ptr(vals), _ptr(res))
+    finally:
+        L.ref_heat_free(hv)
+    sol = {tuple(int(v) for v in k): float(x) for k, x in zip(keys, vals)}
+    names = ("initialization", "assembling", "solving", "communication", "total")
+    return dict(solution=sol, residuals=res[:nr.value], l2=float(l2[0]), linf=float(linf[0]),
+                phases=dict(zip(names, ph.tolist())))

@@ -61,7 +61,13 @@ double now_s() {
 
 const double kPi = std::acos(-1.0);
 
+// problem 3 = HeatProblem (model.cpp:19-31) with the CN system M + dt/2 K; dt and the
+// number of extra load times (t_k = k dt, k = 1..n) come from ref_set_heat.
+double g_heat_dt = 0.01;
+int g_heat_loads = 2;
+
 ScalarField problem_source(int problem, int dim) {
+  if (problem == 3) return HeatProblem{dim}.source();
   if (problem == 0)
     return [dim](double, const std::array<double, 3>& x) {
       double u = std::sin(kPi * x[0]) * std::sin(kPi * x[1]);
@@ -74,6 +80,7 @@ ScalarField problem_source(int problem, int dim) {
 
 ScalarField problem_dirichlet(int problem, int dim) {
   if (problem == 1) return PoissonProblem{dim}.dirichlet();
+  if (problem == 3) return HeatProblem{dim}.dirichlet();
   return [](double, const std::array<double, 3>&) { return 0.0; };
 }
 
@@ -100,6 +107,9 @@ struct LevelData {
 struct RankData {
   std::vector<LevelData> levels;
   std::vector<double> b, x0;  // finest
+  // heat: M - dt/2 K (app.cpp:185-189) and assemble_load at t_k = k dt, k = 1..n
+  std::vector<double> rhs_op;
+  std::vector<std::vector<double>> loads;
 };
 
 struct Built {
@@ -113,7 +123,8 @@ MultigridHierarchy build(int dim, int n_coarse, int levels, int problem, Transpo
       partition_cells(coarse, tp.size(), PartitionStrategy::CoordinateBisection);
   HierarchyOptions opt;
   opt.n_levels = levels;
-  opt.kind = SystemKind::PoissonStiffness;
+  opt.kind = problem == 3 ? SystemKind::HeatCrankNicolson : SystemKind::PoissonStiffness;
+  opt.dt = g_heat_dt;
   opt.source = problem_source(problem, dim);
   opt.dirichlet = problem_dirichlet(problem, dim);
   return build_hierarchy(coarse, pmap, opt, tp);
@@ -230,6 +241,21 @@ void* ref_build(int dim, int n_coarse, int levels, int K, int problem) {
       MultigridHierarchy h = build(dim, n_coarse, levels, problem, tp);
       RankData rd;
       for (const MultigridLevel& L : h.levels) rd.levels.push_back(extract(L));
+      if (problem == 3) {
+        // heat_rank_body's start (app.cpp:173-185): rhs operator, u(0) everywhere, load(0)
+        const MultigridLevel& top = h.finest();
+        const ParFEMapper& m = *top.mapper;
+        rd.rhs_op.resize(top.stiffness.values.size());
+        for (std::size_t i = 0; i < rd.rhs_op.size(); ++i)
+          rd.rhs_op[i] = top.mass.values[i] - 0.5 * g_heat_dt * top.stiffness.values[i];
+        const ScalarField uex = HeatProblem{dim}.exact();
+        rd.x0.resize(static_cast<std::size_t>(m.n_dofs));
+        for (int i = 0; i < m.n_dofs; ++i) rd.x0[static_cast<std::size_t>(i)] = uex(0.0, m.dofs[static_cast<std::size_t>(i)].coords);
+        rd.b = top.load.values;
+        for (int k = 1; k <= g_heat_loads; ++k)
+          rd.loads.push_back(assemble_load(m, *top.comm, h.options.source, k * g_heat_dt).values);
+        return rd;
+      }
       DistributedVector x, bb;
       start_vectors(h, x, bb);
       rd.b = bb.values;
@@ -294,6 +320,28 @@ int ref_level_channels(void* hv, int rank, int level, int* meta, int* entries) {
     meta[4 * i + 3] = static_cast<int>(c.recv.size());
     for (int v : c.send) entries[e++] = v;
     for (int v : c.recv) entries[e++] = v;
+  }
+  return 0;
+}
+
+void ref_set_heat(double dt, int n_loads) {
+  g_heat_dt = dt;
+  g_heat_loads = n_loads;
+}
+
+// heat builds: rhs operator (nnz of the finest level) and the loads, n_loads x n_dofs
+int ref_heat_data(void* hv, int rank, double* rhs_op, double* loads) {
+  const Built* h = static_cast<const Built*>(hv);
+  const RankData& rd = h->ranks.at(static_cast<std::size_t>(rank));
+  if (rd.rhs_op.empty()) {
+    g_err = "not a heat build";
+    return 1;
+  }
+  std::copy(rd.rhs_op.begin(), rd.rhs_op.end(), rhs_op);
+  std::size_t at = 0;
+  for (const auto& l : rd.loads) {
+    std::copy(l.begin(), l.end(), loads + at);
+    at += l.size();
   }
   return 0;
 }
@@ -442,5 +490,55 @@ int ref_bench(int dim, int n_coarse, int levels, int K, int problem, int smoothe
   }
   return rc;
 }
+
+// The reference's own Crank-Nicolson heat run (run_heat, app.cpp:146-230,
+// :299-305), unmodified: returns a handle to its SolveReport (NULL on failure).
+void* ref_heat(int dim, int n_coarse, int levels, int K, double dt, double end_time, int smoother_kind,
+               double damping, int pre, int post, double outer_tol) {
+  SolveReport* out = nullptr;
+  const int rc = guarded([&] {
+    AppConfig cfg;
+    cfg.dimension = dim;
+    cfg.n_coarse = n_coarse;
+    cfg.ranks = K;
+    cfg.levels = levels;
+    cfg.pre_smooth = pre;
+    cfg.post_smooth = post;
+    cfg.dt = dt;
+    cfg.end_time = end_time;
+    cfg.outer_tol = outer_tol;
+    cfg.smoother = smoother_kind == 0 ? "jacobi" : "gauss_seidel";
+    cfg.damping = damping;
+    out = new SolveReport(run_heat(cfg));
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+// entries of solution_by_key, residual count, errors, phases {init, assembling, solving,
+// communication, total}
+int ref_heat_info(void* hv, std::int64_t* n_entries, int* n_res, double* l2, double* linf, double* phases) {
+  const SolveReport& r = *static_cast<SolveReport*>(hv);
+  *n_entries = static_cast<std::int64_t>(r.solution_by_key.size());
+  *n_res = static_cast<int>(r.cycle_residuals.size());
+  *l2 = r.l2_error;
+  *linf = r.linf_error;
+  const PhaseTimes& p = r.metrics.phases;
+  const double ph[5] = {p.initialization, p.assembling, p.solving, p.communication, p.total};
+  std::copy(ph, ph + 5, phases);
+  return 0;
+}
+
+int ref_heat_copy(void* hv, std::int64_t* keys, double* values, double* residuals) {
+  const SolveReport& r = *static_cast<SolveReport*>(hv);
+  std::size_t i = 0;
+  for (const auto& [k, v] : r.solution_by_key) {
+    for (int a = 0; a < 4; ++a) keys[4 * i + static_cast<std::size_t>(a)] = k[static_cast<std::size_t>(a)];
+    values[i++] = v;
+  }
+  std::copy(r.cycle_residuals.begin(), r.cycle_residuals.end(), residuals);
+  return 0;
+}
+
+void ref_heat_free(void* hv) { delete static_cast<SolveReport*>(hv); }
 
 }  // extern "C"

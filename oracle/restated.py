@@ -163,3 +163,61 @@ class Oracle:
                 self._h = None
         except Exception:
             pass
+
+
+# ------------------------------------------------------------ heat (Crank-Nicolson) --
+
+def csr_spmv(row_offsets, cols, vals, x):
+    """spmv (linalg.cpp:45-57): every row summed serially in stored order from 0.0
+    (numpy elementwise products and sums are single IEEE operations, no contraction)."""
+    n = len(row_offsets) - 1
+    lens = np.diff(row_offsets)
+    y = np.zeros(n)
+    for j in range(int(lens.max()) if n else 0):
+        m = lens > j
+        e = row_offsets[:-1][m] + j
+        y[m] = y[m] + vals[e] * x[cols[e]]
+    return y
+
+
+def heat_exact(keys, denom, dim, t):
+    """HeatProblem::exact (model.cpp:11-22) at the dof coordinates key / denom
+    (fespace.cpp:66-70), with the host libm like the reference."""
+    import math
+    out = np.empty(len(keys))
+    e = math.exp(-0.1 * t)
+    for i, k in enumerate(keys):
+        x = [float(k[1]) / denom, float(k[2]) / denom, float(k[3]) / denom]
+        u = math.sin(math.pi * x[0]) * math.cos(math.pi * x[1])
+        if dim == 3:
+            u *= math.cos(math.pi * x[2])
+        out[i] = e * u
+    return out
+
+
+def heat_loop(oracle, tops, rhs_ops, u0, load0, loads, dt, steps, cfg, dim, denom):
+    """heat_rank_body's time loop (app.cpp:180-213) composed from the restated pieces:
+    the reference's own rhs operator values and loads (per rank: loads[r][k] at t_{k+1}),
+    csr_spmv, the Dirichlet rows from heat_exact, and Oracle.solve_outer.
+    Returns (u per rank, last residual history)."""
+    K = len(tops)
+    u = [np.array(a, np.float64) for a in u0]
+    ln = [np.array(a, np.float64) for a in load0]
+    res = None
+    for k in range(steps):
+        t = float(k + 1) * dt
+        b = []
+        for r in range(K):
+            lv = tops[r]
+            br = csr_spmv(lv.row_offsets, lv.cols, rhs_ops[r], u[r])
+            br = br + 0.5 * dt * (ln[r] + loads[r][k])
+            dir_rows = np.flatnonzero(lv.class_of == 7)
+            g = heat_exact(lv.keys[dir_rows], denom, dim, t)
+            br[dir_rows] = g
+            u[r][dir_rows] = g
+            b.append(br)
+        u, res, st, rc = oracle.solve_outer(u, b, cfg)
+        if rc == 3:
+            raise RuntimeError(f"time step {k + 1}: no convergence")
+        ln = [loads[r][k] for r in range(K)]
+    return u, res

@@ -25,7 +25,7 @@ PF_ERR_STATE = 6
 PF_CH_MASTER_SLAVE, PF_CH_HALO1, PF_CH_HALO2 = 0, 1, 2
 PF_UPDATE_SCATTER, PF_UPDATE_ACCUMULATE_THEN_SCATTER = 0, 1
 PF_SMOOTHER_JACOBI, PF_SMOOTHER_GAUSS_SEIDEL, PF_SMOOTHER_MULTICOLOR_SOR = 0, 1, 2
-PF_PROBLEM_BASELINE, PF_PROBLEM_REFERENCE_POISSON, PF_PROBLEM_UNIT_SOURCE = 0, 1, 2
+PF_PROBLEM_BASELINE, PF_PROBLEM_REFERENCE_POISSON, PF_PROBLEM_UNIT_SOURCE, PF_PROBLEM_HEAT = 0, 1, 2, 3
 
 
 class PfError(RuntimeError):
@@ -75,6 +75,13 @@ class LevelDesc(C.Structure):
                 ("p_offsets", C.c_void_p), ("p_cols", C.c_void_p), ("p_weights", C.c_void_p)]
 
 
+class LoadDesc(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("n_cells", C.c_int32), ("n_dofs", C.c_int32),
+                ("lattice", C.c_void_p), ("cells", C.c_void_p), ("factor", C.c_void_p),
+                ("extent", C.c_void_p), ("phi", C.c_void_p), ("qweight", C.c_double),
+                ("boundary", C.c_void_p), ("is_dirichlet", C.c_void_p)]
+
+
 class SmootherConfig(C.Structure):
     _fields_ = [("kind", C.c_int32), ("sweeps", C.c_int32), ("local_sweeps", C.c_int32),
                 ("damping", C.c_double)]
@@ -106,8 +113,12 @@ EXPORTS = [
     "pf_update_halo1", "pf_update_halo2", "pf_allreduce_sum", "pf_v_cycle", "pf_solve_outer",
     "pf_solve_outer_host", "pf_launch_count", "pf_reset_launch_count", "pf_time_sweep",
     "pf_time_vcycle", "pf_hierarchy_stream", "pf_level_info",
-    "pf_setup_create", "pf_setup_destroy", "pf_setup_level", "pf_setup_level_keys",
-    "pf_setup_rhs", "pf_setup_counts", "pf_setup_seconds",
+    "pf_operator_create", "pf_operator_set_values", "pf_operator_apply", "pf_operator_destroy",
+    "pf_load_create", "pf_load_set", "pf_load_assemble", "pf_load_apply_dirichlet", "pf_load_destroy",
+    "pf_cn_rhs", "pf_heat_run",
+    "pf_setup_create", "pf_setup_create_heat", "pf_setup_destroy", "pf_setup_level", "pf_setup_level_keys",
+    "pf_setup_rhs", "pf_setup_counts", "pf_setup_seconds", "pf_setup_rhs_operator", "pf_setup_load_at",
+    "pf_setup_load_desc", "pf_setup_scales",
 ]
 
 _lib = None
@@ -172,7 +183,25 @@ def lib():
         "pf_time_vcycle": [P, P, P, C.POINTER(MultigridConfig), C.c_int, dp],
         "pf_level_info": [P, C.c_int, C.c_int, i64p, i64p, i64p, i64p],
         "pf_hierarchy_stream": [P, PP],
+        "pf_operator_create": [P, C.c_int, PP],
+        "pf_operator_set_values": [P, C.c_int, P, C.c_int64],
+        "pf_operator_apply": [P, P, P],
+        "pf_operator_destroy": [P],
+        "pf_load_create": [P, C.c_int, PP],
+        "pf_load_set": [P, C.c_int, C.POINTER(LoadDesc)],
+        "pf_load_assemble": [P, C.c_double, P],
+        "pf_load_apply_dirichlet": [P, C.c_int, C.c_double, P, P],
+        "pf_load_destroy": [P],
+        "pf_cn_rhs": [P, P, P, P, P, C.c_double, C.c_int, C.c_double, P, P],
+        "pf_heat_run": [P, P, P, P, P, C.c_int, C.c_int, C.c_double, dp, C.c_int, dp,
+                        C.POINTER(MultigridConfig), C.POINTER(SolveStats), dp, C.c_int,
+                        C.POINTER(C.c_int)],
         "pf_setup_create": [C.c_int] * 6 + [PP],
+        "pf_setup_create_heat": [C.c_int] * 5 + [C.c_double, PP],
+        "pf_setup_rhs_operator": [P, PP, i64p],
+        "pf_setup_load_at": [P, C.c_double, P, C.c_int64],
+        "pf_setup_load_desc": [P, C.POINTER(LoadDesc)],
+        "pf_setup_scales": [P, C.c_double, dp, C.POINTER(C.c_int32), dp],
         "pf_setup_destroy": [P],
         "pf_setup_level": [P, C.c_int, C.POINTER(LevelDesc)],
         "pf_setup_level_keys": [P, C.c_int, PP, PP],

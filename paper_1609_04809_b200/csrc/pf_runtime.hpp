@@ -93,6 +93,9 @@ struct DevLevel {
   std::vector<int32_t> perm;         // host index -> device index
   DevBuf<int32_t> d_perm;
   DevSell A;
+  // host copies to place further value sets on A's pattern (pf_operator_set_values)
+  std::vector<int64_t> csr_rowptr;   // the level desc's row offsets (host order)
+  std::vector<int64_t> sell_ptr;     // A.slice_ptr
   DevBuf<uint8_t> d_is_dir;
   int64_t own_cols_touched = 0;  // distinct columns referenced by own rows
   // prolongation from the parent level (rows: this level's device rows; columns: parent

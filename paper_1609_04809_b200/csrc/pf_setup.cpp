@@ -114,9 +114,36 @@ struct Geo {
   const std::vector<int>* coarse_owner = nullptr;
   std::unordered_map<int64_t, int> master;  // interface vertex -> master rank
 
+  // Vertex coordinate along one axis as the reference stores it: level 0 from the unit
+  // mesh (mesh.cpp:73,87: i * (1/n)), refined levels from the lattice (partition.cpp:331).
+  double coord(int64_t i) const {
+    return level == 0 ? static_cast<double>(i) * (1.0 / static_cast<double>(N))
+                      : static_cast<double>(i) / static_cast<double>(N);
+  }
+  // Cell extent (element_matrices takes hi - lo per axis, assembly.cpp:51-58).
+  double extent(int64_t c) const { return coord(c + 1) - coord(c); }
+  // Global cell number: coarse cells lexicographic (mesh.cpp:93-100), children
+  // nc * parent + child index with child offset (c/4, c/2 % 2, c % 2) (mesh.cpp:36-42,
+  // :170-176).  Local cells are visited in ascending gcn (partition.cpp:184-186, :296-298),
+  // which fixes the order every assembled sum is accumulated in.
+  int64_t gcn(int64_t x, int64_t y, int64_t z) const {
+    const int64_t n = n_coarse;
+    int64_t g = d == 3 ? ((x / S) * n + (y / S)) * n + (z / S) : (x / S) * n + (y / S);
+    for (int b = level - 1; b >= 0; --b) {
+      const int64_t ci = d == 3 ? (((x >> b) & 1) << 2) | (((y >> b) & 1) << 1) | ((z >> b) & 1)
+                                : (((x >> b) & 1) << 1) | ((y >> b) & 1);
+      g = g * (int64_t(1) << d) + ci;
+    }
+    return g;
+  }
   int64_t nzc() const { return d == 3 ? N : 1; }     // cells along z
   int64_t nzv() const { return d == 3 ? N + 1 : 1; } // vertices along z
   int64_t vkey(int64_t x, int64_t y, int64_t z) const { return (x * (N + 1) + y) * nzv() + z; }
+  void unpack(int64_t key, int64_t& x, int64_t& y, int64_t& z) const {
+    z = key % nzv();
+    y = (key / nzv()) % (N + 1);
+    x = key / (nzv() * (N + 1));
+  }
   bool cell_in(int64_t x, int64_t y, int64_t z) const {
     return x >= 0 && y >= 0 && z >= 0 && x < N && y < N && z < nzc();
   }
@@ -315,47 +342,30 @@ struct OwnedChannel {
   std::vector<int32_t> send, recv;
 };
 
-struct SetupLevel {
-  Geo geo;
-  int32_t n = 0, n_own = 0;
-  Box vbox;                       // vertex box of the local vertices
-  std::vector<int32_t> index;     // over vbox: local index or -1
-  std::vector<int64_t> vert;      // per local dof: packed vertex key
-  std::vector<int64_t> rowptr;
-  std::vector<int32_t> cols;
-  std::vector<double> vals;
-  std::vector<uint8_t> owns_row, is_dir, class_of;
-  std::vector<int32_t> color;
-  std::vector<int64_t> keys4;
-  std::vector<OwnedChannel> channels;
-  std::vector<pf_channel_desc> descs;
-  std::vector<int64_t> p_off;
-  std::vector<int32_t> p_col;
-  std::vector<double> p_w;
-  int32_t lookup(int64_t x, int64_t y, int64_t z) const {
-    return vbox.in(x, y, z) ? index[vbox.idx(x, y, z)] : -1;
-  }
-};
-
-// Q1 element stiffness on a cube of side h, 2-point Gauss (assembly.cpp:11-92).
+// Q1 element matrices on an axis-aligned cell with extents h[0..d), 2-point Gauss
+// (assembly.cpp:11-92): stiffness K, mass M, and what the load needs per quadrature point.
 struct Element {
-  int nv = 8;
+  int nv = 8, nq = 8;
   double K[8][8] = {};
+  double M[8][8] = {};
   double qp[8][3] = {};   // quadrature points (reference cell)
   double qw[8] = {};      // weight * volume
   double phi[8][8] = {};  // phi[q][v]
+  double h[3] = {1.0, 1.0, 1.0};
 };
 
-Element make_element(int d, double h) {
+Element make_element(int d, const double* hx) {
   Element E;
   E.nv = 1 << d;
+  E.nq = 1 << d;
   const double off = 0.5 / std::sqrt(3.0);
   const double pts[2] = {0.5 - off, 0.5 + off};
-  double hh[3] = {1.0, 1.0, 1.0}, volume = 1.0;
+  double volume = 1.0;
   for (int a = 0; a < d; ++a) {
-    hh[a] = h;
-    volume *= hh[a];
+    E.h[a] = hx[a];
+    volume *= E.h[a];
   }
+  const double* hh = E.h;
   int q = 0;
   const int nz = d == 3 ? 2 : 1;
   for (int ix = 0; ix < 2; ++ix)
@@ -389,10 +399,42 @@ Element make_element(int d, double h) {
             double gsum = 0.0;
             for (int a = 0; a < d; ++a) gsum += grad[i][a] * grad[j][a] / (hh[a] * hh[a]);
             E.K[i][j] += E.qw[q] * gsum;
+            E.M[i][j] += E.qw[q] * E.phi[q][i] * E.phi[q][j];
           }
       }
   return E;
 }
+
+struct SetupLevel {
+  Geo geo;
+  int32_t n = 0, n_own = 0;
+  Box vbox;                       // vertex box of the local vertices
+  std::vector<int32_t> index;     // over vbox: local index or -1
+  std::vector<int64_t> vert;      // per local dof: packed vertex key
+  std::vector<int64_t> rowptr;
+  std::vector<int32_t> cols;
+  std::vector<double> vals;
+  std::vector<uint8_t> owns_row, is_dir, class_of;
+  std::vector<int32_t> color;
+  std::vector<int64_t> keys4;
+  std::vector<OwnedChannel> channels;
+  std::vector<pf_channel_desc> descs;
+  std::vector<int64_t> p_off;
+  std::vector<int32_t> p_col;
+  std::vector<double> p_w;
+  // element matrices per distinct cell shape (extents differ in the last bit across cells
+  // unless N is a power of two)
+  std::vector<Element> elems;
+  std::vector<int> hid;  // per cell index along an axis: its extent's slot
+  int nh = 0;
+  int32_t lookup(int64_t x, int64_t y, int64_t z) const {
+    return vbox.in(x, y, z) ? index[vbox.idx(x, y, z)] : -1;
+  }
+  const Element& elem(int64_t cx, int64_t cy, int64_t cz) const {
+    const int e = geo.d == 3 ? (hid[cx] * nh + hid[cy]) * nh + hid[cz] : hid[cx] * nh + hid[cy];
+    return elems[static_cast<size_t>(e)];
+  }
+};
 
 int ring_slot(int d, int ox, int oy, int oz) {
   for (int v = 0; v < (1 << d); ++v)
@@ -400,24 +442,37 @@ int ring_slot(int d, int ox, int oy, int oz) {
   return -1;
 }
 
+// The manufactured fields as the reference evaluates them.  Every source and boundary
+// field here is "scalar(t) * profile(x)" with profile = F0(pi x) * F1(pi y) [* F2(pi z)]
+// multiplied left to right, so a device kernel holding per-axis factor tables and the
+// host-computed scalar reproduces each product bit for bit.
 struct Problem {
   int kind = 0, d = 3;
-  double f(const double* x) const {
-    if (kind == PF_PROBLEM_UNIT_SOURCE) return 1.0;
-    if (kind == PF_PROBLEM_BASELINE) {
-      double u = std::sin(kPi * x[0]) * std::sin(kPi * x[1]);
-      if (d == 3) u *= std::sin(kPi * x[2]);
-      return d * kPi * kPi * u;
-    }
-    double u = std::sin(kPi * x[0]) * std::cos(kPi * x[1]);  // model.cpp:12-16
-    if (d == 3) u *= std::cos(kPi * x[2]);
-    return d * kPi * kPi * u;
-  }
-  double g(const double* x) const {
-    if (kind != PF_PROBLEM_REFERENCE_POISSON) return 0.0;
-    double u = std::sin(kPi * x[0]) * std::cos(kPi * x[1]);
-    if (d == 3) u *= std::cos(kPi * x[2]);
+  double dt = 0.0;
+  bool unit() const { return kind == PF_PROBLEM_UNIT_SOURCE; }
+  // axis factor a of the profile: sin for axis 0 (and every axis of BASELINE), else cos
+  bool axis_sin(int a) const { return a == 0 || kind == PF_PROBLEM_BASELINE; }
+  double profile(const double* x) const {
+    if (unit()) return 1.0;
+    double u = (axis_sin(0) ? std::sin(kPi * x[0]) : std::cos(kPi * x[0])) *
+               (axis_sin(1) ? std::sin(kPi * x[1]) : std::cos(kPi * x[1]));  // model.cpp:12-16
+    if (d == 3) u *= axis_sin(2) ? std::sin(kPi * x[2]) : std::cos(kPi * x[2]);
     return u;
+  }
+  // f(t, x) = source_scale(t) * profile(x)
+  double source_scale(double t) const {
+    if (unit()) return 1.0;
+    if (kind == PF_PROBLEM_HEAT) return (-0.1 + d * kPi * kPi) * std::exp(-0.1 * t);  // model.cpp:24-29
+    return d * kPi * kPi;                                                                // model.cpp:38-41
+  }
+  // g(t, x) = dirichlet_scale(t) * profile(x), or exactly 0 when !has_dirichlet()
+  bool has_dirichlet() const { return kind == PF_PROBLEM_REFERENCE_POISSON || kind == PF_PROBLEM_HEAT; }
+  double dirichlet_scale(double t) const { return kind == PF_PROBLEM_HEAT ? std::exp(-0.1 * t) : 1.0; }
+  double f(double t, const double* x) const { return source_scale(t) * profile(x); }
+  double g(double t, const double* x) const {
+    if (!has_dirichlet()) return 0.0;
+    if (kind == PF_PROBLEM_HEAT) return std::exp(-0.1 * t) * profile(x);  // model.cpp:19-22
+    return profile(x);
   }
 };
 
@@ -429,6 +484,11 @@ struct pf_setup {
   std::vector<int> coarse_owner;
   std::vector<std::unique_ptr<SetupLevel>> levels;
   std::vector<double> b, x0;
+  std::vector<double> rhs_op;  // heat: finest-level M - dt/2 K in the system's CSR order
+  // device load description of the finest level (pf_load_desc)
+  std::vector<int32_t> ld_lattice;
+  std::vector<uint32_t> ld_cells;
+  std::vector<double> ld_factor, ld_extent, ld_phi, ld_boundary;
   double seconds = 0;
 };
 
@@ -473,6 +533,68 @@ Box expand(const Box& b, int64_t by, const Geo& g, bool vertices) {
   return o;
 }
 
+// Cells given as (x, y, z) triples, reordered by ascending gcn (at most 8).
+void sort_cells_by_gcn(const Geo& g, int64_t* cells, int nc) {
+  int64_t key[8];
+  for (int c = 0; c < nc; ++c) key[c] = g.gcn(cells[3 * c], cells[3 * c + 1], cells[3 * c + 2]);
+  for (int i = 1; i < nc; ++i)
+    for (int j = i; j > 0 && key[j - 1] > key[j]; --j) {
+      std::swap(key[j - 1], key[j]);
+      for (int a = 0; a < 3; ++a) std::swap(cells[3 * (j - 1) + a], cells[3 * j + a]);
+    }
+}
+
+// The cells around vertex (x, y, z) owned by rank q, in gcn order; returns the count.
+int owned_cells_around(const Geo& g, int q, int64_t x, int64_t y, int64_t z, int64_t* cells) {
+  int nc = 0;
+  const int zlo = g.d == 3 ? -1 : 0;
+  for (int dx = -1; dx <= 0; ++dx)
+    for (int dy = -1; dy <= 0; ++dy)
+      for (int dz = zlo; dz <= 0; ++dz) {
+        const int64_t cx = x + dx, cy = y + dy, cz = z + dz;
+        if (!g.cell_in(cx, cy, cz) || g.owner(cx, cy, cz) != q) continue;
+        cells[3 * nc] = cx;
+        cells[3 * nc + 1] = cy;
+        cells[3 * nc + 2] = cz;
+        ++nc;
+      }
+  sort_cells_by_gcn(g, cells, nc);
+  return nc;
+}
+
+// Rank q's share of the load at vertex (x, y, z) at time t: its own cells in gcn order,
+// each cell's element load summed over the quadrature points (assembly.cpp:60-88,
+// :144-160).
+double load_partial(const Problem& P, const SetupLevel& L, int q, int64_t x, int64_t y, int64_t z, double t) {
+  const Geo& g = L.geo;
+  const int d = g.d;
+  int64_t cells[24];
+  const int nc = owned_cells_around(g, q, x, y, z, cells);
+  double acc = 0.0;
+  for (int c = 0; c < nc; ++c) {
+    const int64_t* cc = &cells[3 * c];
+    const Element& E = L.elem(cc[0], cc[1], cc[2]);
+    const int slot = ring_slot(d, static_cast<int>(x - cc[0]), static_cast<int>(y - cc[1]),
+                               static_cast<int>(z - cc[2]));
+    const double lo[3] = {g.coord(cc[0]), g.coord(cc[1]), d == 3 ? g.coord(cc[2]) : 0.0};
+    double load = 0.0;
+    for (int q2 = 0; q2 < E.nq; ++q2) {
+      double xq[3];
+      for (int a = 0; a < 3; ++a) xq[a] = lo[a] + E.qp[q2][a] * E.h[a];
+      const double fq = P.f(t, xq);
+      load += E.qw[q2] * fq * E.phi[q2][slot];
+    }
+    acc += load;
+  }
+  return acc;
+}
+
+// Finest-level load at time t after the master/slave accumulate-then-scatter
+// (fecomm.cpp:41-62: masters add the slaves' parts in ascending rank order, slaves take
+// the sum).  Dirichlet rows are left 0: the caller overwrites them with boundary data.
+void finest_load(const pf_setup& s, double t, double* out);
+void finish_finest(pf_setup& s);
+
 void build_level(pf_setup& s, int l) {
   auto L = std::make_unique<SetupLevel>();
   Geo& g = L->geo;
@@ -512,7 +634,13 @@ void build_level(pf_setup& s, int l) {
     for (int64_t y = vb.lo[1]; y < vb.hi[1]; ++y)
       for (int64_t z = vb.lo[2]; z < vb.hi[2]; ++z) info[vb.idx(x, y, z)] = classify(V, x, y, z);
 
-  // --- numbering: own (lexicographic), then Slave, Halo1, Halo2, Dirichlet
+  // --- numbering: the reference's own.  build_fespace numbers vertices at first touch
+  // over the local cells in gcn order, ring-slot order inside a cell (fespace.cpp:47-85);
+  // build_parfemapper then stable-sorts that numbering by DofClass value
+  // (femapper.cpp:167-199).  So local index order = (class, gcn of the lowest local cell
+  // containing the vertex, the vertex's slot in it) — which makes every row's column
+  // order, the restriction's scatter-add order and the coarse Gauss-Seidel order the
+  // reference's, and with them the floating-point results.
   L->index.assign(static_cast<size_t>(nvb), -1);
   int64_t count[8] = {};
   for (const VInfo& v : info)
@@ -521,9 +649,37 @@ void build_level(pf_setup& s, int l) {
   int64_t total = 0;
   for (int64_t c : count) total += c;
   if (total >= (int64_t(1) << 31)) invalid("local level too large for int32 indices");
-  int64_t next[5] = {0, n_own, n_own + count[kSlave], n_own + count[kSlave] + count[kHalo1],
-                     n_own + count[kSlave] + count[kHalo1] + count[kHalo2]};
-  auto group = [](uint8_t c) { return c <= kDep2 ? 0 : c - 3; };
+  struct Order {
+    int64_t key;  // class << 60 | first-touch rank
+    int64_t bi;
+  };
+  std::vector<Order> order;
+  order.reserve(static_cast<size_t>(total));
+  for (int64_t bi = 0; bi < nvb; ++bi)
+    if (info[static_cast<size_t>(bi)].local) order.push_back({0, bi});
+  const int zlo = d == 3 ? -1 : 0;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < static_cast<int64_t>(order.size()); ++k) {
+    const int64_t bi = order[static_cast<size_t>(k)].bi;
+    const int64_t ez = vb.ext(2), ey = vb.ext(1);
+    const int64_t x = vb.lo[0] + bi / (ey * ez), y = vb.lo[1] + (bi / ez) % ey, z = vb.lo[2] + bi % ez;
+    int64_t best = -1;
+    int slot = 0;
+    for (int dx = -1; dx <= 0; ++dx)
+      for (int dy = -1; dy <= 0; ++dy)
+        for (int dz = zlo; dz <= 0; ++dz) {
+          const int64_t cx = x + dx, cy = y + dy, cz = z + dz;
+          if (!V.cell_local(cx, cy, cz)) continue;
+          const int64_t gc = g.gcn(cx, cy, cz);
+          if (best < 0 || gc < best) {
+            best = gc;
+            slot = ring_slot(d, -dx, -dy, -dz);
+          }
+        }
+    order[static_cast<size_t>(k)].key =
+        (static_cast<int64_t>(info[static_cast<size_t>(bi)].cls) << 59) | (best * 8 + slot);
+  }
+  std::sort(order.begin(), order.end(), [](const Order& a, const Order& b) { return a.key < b.key; });
   L->n = static_cast<int32_t>(total);
   L->n_own = static_cast<int32_t>(n_own);
   L->vert.resize(static_cast<size_t>(total));
@@ -531,31 +687,25 @@ void build_level(pf_setup& s, int l) {
   L->owns_row.resize(static_cast<size_t>(total));
   L->is_dir.resize(static_cast<size_t>(total));
   L->keys4.resize(static_cast<size_t>(4 * total));
-  for (int64_t x = vb.lo[0]; x < vb.hi[0]; ++x)
-    for (int64_t y = vb.lo[1]; y < vb.hi[1]; ++y)
-      for (int64_t z = vb.lo[2]; z < vb.hi[2]; ++z) {
-        const int64_t bi = vb.idx(x, y, z);
-        const VInfo& v = info[static_cast<size_t>(bi)];
-        if (!v.local) continue;
-        const int64_t li = next[group(v.cls)]++;
-        L->index[static_cast<size_t>(bi)] = static_cast<int32_t>(li);
-        L->vert[static_cast<size_t>(li)] = g.vkey(x, y, z);
-        L->class_of[static_cast<size_t>(li)] = v.cls;
-        L->is_dir[static_cast<size_t>(li)] = v.cls == kDirichlet;
-        L->owns_row[static_cast<size_t>(li)] = v.cls <= kDep2 || (v.cls == kDirichlet && v.diri_authority == me);
-        int64_t* k4 = &L->keys4[static_cast<size_t>(4 * li)];
-        k4[0] = 0;
-        k4[1] = x;
-        k4[2] = y;
-        k4[3] = d == 3 ? z : 0;
-      }
+#pragma omp parallel for schedule(static)
+  for (int64_t li = 0; li < total; ++li) {
+    const int64_t bi = order[static_cast<size_t>(li)].bi;
+    const int64_t ez = vb.ext(2), ey = vb.ext(1);
+    const int64_t x = vb.lo[0] + bi / (ey * ez), y = vb.lo[1] + (bi / ez) % ey, z = vb.lo[2] + bi % ez;
+    const VInfo& v = info[static_cast<size_t>(bi)];
+    L->index[static_cast<size_t>(bi)] = static_cast<int32_t>(li);
+    L->vert[static_cast<size_t>(li)] = g.vkey(x, y, z);
+    L->class_of[static_cast<size_t>(li)] = v.cls;
+    L->is_dir[static_cast<size_t>(li)] = v.cls == kDirichlet;
+    L->owns_row[static_cast<size_t>(li)] = v.cls <= kDep2 || (v.cls == kDirichlet && v.diri_authority == me);
+    int64_t* k4 = &L->keys4[static_cast<size_t>(4 * li)];
+    k4[0] = 0;
+    k4[1] = x;
+    k4[2] = y;
+    k4[3] = d == 3 ? z : 0;
+  }
   const int32_t n = L->n;
-  auto unpack = [&](int64_t key, int64_t& x, int64_t& y, int64_t& z) {
-    const int64_t nzv = g.nzv();
-    z = key % nzv;
-    y = (key / nzv) % (g.N + 1);
-    x = key / (nzv * (g.N + 1));
-  };
+  auto unpack = [&](int64_t key, int64_t& x, int64_t& y, int64_t& z) { g.unpack(key, x, y, z); };
   // lattice-parity colour of own rows: 2^d independent sets of the Q1 stencil
   L->color.resize(static_cast<size_t>(n_own));
   for (int32_t i = 0; i < L->n_own; ++i) {
@@ -565,9 +715,32 @@ void build_level(pf_setup& s, int l) {
                                               : ((x & 1) << 1) | (y & 1));
   }
 
-  // --- stiffness (assembly over own + halo cells, Dirichlet rows -> identity)
-  const double h = 1.0 / static_cast<double>(g.N);
-  const Element E = make_element(d, h);
+  // --- element matrices per distinct cell shape
+  std::vector<double> hvals;
+  L->hid.assign(static_cast<size_t>(g.N), 0);
+  for (int64_t c = 0; c < g.N; ++c) {
+    const double e = g.extent(c);
+    size_t k = 0;
+    while (k < hvals.size() && hvals[k] != e) ++k;
+    if (k == hvals.size()) hvals.push_back(e);
+    L->hid[static_cast<size_t>(c)] = static_cast<int>(k);
+  }
+  L->nh = static_cast<int>(hvals.size());
+  for (int a = 0; a < L->nh; ++a)
+    for (int b = 0; b < L->nh; ++b)
+      for (int c = 0; c < (d == 3 ? L->nh : 1); ++c) {
+        const double hx[3] = {hvals[a], hvals[b], d == 3 ? hvals[c] : 1.0};
+        L->elems.push_back(make_element(d, hx));
+      }
+  const SetupLevel& LC = *L;
+  auto elem = [&](int64_t cx, int64_t cy, int64_t cz) -> const Element& { return LC.elem(cx, cy, cz); };
+  auto sort_by_gcn = [&](int64_t* cells, int nc) { sort_cells_by_gcn(g, cells, nc); };
+  const bool heat = s.prob.kind == PF_PROBLEM_HEAT;
+  const bool finest = l == s.n_levels - 1;
+  const double half_dt = 0.5 * s.prob.dt;
+
+  // --- system (assembly over own + halo cells in gcn order, assembly.cpp:114-131);
+  // heat: M + dt/2 K (multigrid.cpp:18-28); Dirichlet rows -> identity (:162-170)
   const int zr = d == 3 ? 1 : 0;
   std::vector<int64_t> rowlen(static_cast<size_t>(n) + 1, 0);
   auto shared_cells = [&](int64_t x, int64_t y, int64_t z, int dx, int dy, int dz, int64_t* cells) {
@@ -583,6 +756,7 @@ void build_level(pf_setup& s, int l) {
           cells[3 * nc + 2] = cz;
           ++nc;
         }
+    sort_by_gcn(cells, nc);
     return nc;
   };
 #pragma omp parallel for schedule(static)
@@ -599,13 +773,18 @@ void build_level(pf_setup& s, int l) {
   }
   L->rowptr.assign(static_cast<size_t>(n) + 1, 0);
   for (int32_t i = 0; i < n; ++i) L->rowptr[i + 1] = L->rowptr[i] + rowlen[i + 1];
-  L->cols.resize(static_cast<size_t>(L->rowptr[n]));
-  L->vals.resize(static_cast<size_t>(L->rowptr[n]));
+  const int64_t nnz = L->rowptr[n];
+  L->cols.resize(static_cast<size_t>(nnz));
+  L->vals.resize(static_cast<size_t>(nnz));
+  if (heat && finest) s.rhs_op.resize(static_cast<size_t>(nnz));
 #pragma omp parallel for schedule(static)
   for (int32_t i = 0; i < n; ++i) {
     int64_t x, y, z;
     unpack(L->vert[i], x, y, z);
-    std::pair<int32_t, double> row[27];
+    struct Ent {
+      int32_t j;
+      double sys, rhs;
+    } row[27];
     int nr = 0;
     int64_t cells[24];
     const bool dir = L->is_dir[i];
@@ -616,21 +795,29 @@ void build_level(pf_setup& s, int l) {
           if (j < 0) continue;
           const int nc = shared_cells(x, y, z, dx, dy, dz, cells);
           if (nc == 0) continue;
-          double v = 0.0;
+          double k = 0.0, m = 0.0;
           for (int c = 0; c < nc; ++c) {
-            const int si = ring_slot(d, static_cast<int>(x - cells[3 * c]), static_cast<int>(y - cells[3 * c + 1]),
-                                     static_cast<int>(z - cells[3 * c + 2]));
-            const int sj = ring_slot(d, static_cast<int>(x + dx - cells[3 * c]), static_cast<int>(y + dy - cells[3 * c + 1]),
-                                     static_cast<int>(z + dz - cells[3 * c + 2]));
-            v += E.K[si][sj];
+            const int64_t* cc = &cells[3 * c];
+            const int si = ring_slot(d, static_cast<int>(x - cc[0]), static_cast<int>(y - cc[1]),
+                                     static_cast<int>(z - cc[2]));
+            const int sj = ring_slot(d, static_cast<int>(x + dx - cc[0]), static_cast<int>(y + dy - cc[1]),
+                                     static_cast<int>(z + dz - cc[2]));
+            const Element& E = elem(cc[0], cc[1], cc[2]);
+            k += E.K[si][sj];
+            if (heat) m += E.M[si][sj];
           }
+          double v = heat ? m + half_dt * k : k;
+          // heat rhs operator M - dt/2 K on raw rows (app.cpp:185-189)
+          const double r = heat ? m - half_dt * k : 0.0;
           if (dir) v = (j == i) ? 1.0 : 0.0;  // apply_dirichlet_rows, assembly.cpp:162-170
-          row[nr++] = {j, v};
+          row[nr++] = {j, v, r};
         }
-    std::sort(row, row + nr, [](const auto& a, const auto& b) { return a.first < b.first; });
-    for (int k = 0; k < nr; ++k) {
-      L->cols[static_cast<size_t>(L->rowptr[i] + k)] = row[k].first;
-      L->vals[static_cast<size_t>(L->rowptr[i] + k)] = row[k].second;
+    std::sort(row, row + nr, [](const Ent& a, const Ent& b) { return a.j < b.j; });
+    for (int e = 0; e < nr; ++e) {
+      const size_t at = static_cast<size_t>(L->rowptr[i] + e);
+      L->cols[at] = row[e].j;
+      L->vals[at] = row[e].sys;
+      if (heat && finest) s.rhs_op[at] = row[e].rhs;
     }
   }
 
@@ -681,9 +868,25 @@ void build_level(pf_setup& s, int l) {
     for (int32_t i = 0; i < n; ++i) {
       int64_t X[3];
       unpack(L->vert[i], X[0], X[1], X[2]);
+      // parent of the dof's home cell: the lowest-gcn local fine cell containing it
+      // (multigrid.cpp:43-55); its ring order fixes the order of the row's entries
+      int64_t home[3] = {0, 0, 0}, best = -1;
+      for (int dx = -1; dx <= 0; ++dx)
+        for (int dy = -1; dy <= 0; ++dy)
+          for (int dz = (d == 3 ? -1 : 0); dz <= 0; ++dz) {
+            const int64_t cx = X[0] + dx, cy = X[1] + dy, cz = X[2] + dz;
+            if (!V.cell_local(cx, cy, cz)) continue;
+            const int64_t gc = g.gcn(cx, cy, cz);
+            if (best < 0 || gc < best) {
+              best = gc;
+              home[0] = cx;
+              home[1] = cy;
+              home[2] = cz;
+            }
+          }
+      if (best < 0) bad = true;
       int64_t c[3] = {0, 0, 0};
-      for (int a = 0; a < d; ++a)
-        c[a] = (X[a] & 1) ? (X[a] - 1) / 2 : std::min<int64_t>(X[a] / 2, C.geo.N - 1);
+      for (int a = 0; a < d; ++a) c[a] = home[a] >> 1;
       for (int v = 0; v < (1 << d); ++v) {
         double w = 1.0;
         int64_t corner[3] = {0, 0, 0};
@@ -709,59 +912,106 @@ void build_level(pf_setup& s, int l) {
       }
   }
 
-  // --- finest level: load (own cells + master/slave accumulate) and rhs
-  if (l == s.n_levels - 1) {
-    s.b.assign(static_cast<size_t>(n), 0.0);
-    s.x0.assign(static_cast<size_t>(n), 0.0);
-    const double denom = static_cast<double>(g.N);
-    auto partial = [&](int q, int64_t x, int64_t y, int64_t z) {
-      // sum over cells around (x,y,z) owned by q, lexicographic, of the element load
-      double acc = 0.0;
-      const int zlo = d == 3 ? -1 : 0;
-      for (int dx = -1; dx <= 0; ++dx)
-        for (int dy = -1; dy <= 0; ++dy)
-          for (int dz = zlo; dz <= 0; ++dz) {
-            const int64_t cx = x + dx, cy = y + dy, cz = z + dz;
-            if (!g.cell_in(cx, cy, cz) || g.owner(cx, cy, cz) != q) continue;
-            const int slot = ring_slot(d, -dx, -dy, -dz);
-            const double lo[3] = {static_cast<double>(cx) / denom, static_cast<double>(cy) / denom,
-                                  d == 3 ? static_cast<double>(cz) / denom : 0.0};
-            double load = 0.0;
-            for (int q2 = 0; q2 < (1 << d); ++q2) {
-              double xq[3] = {0.0, 0.0, 0.0};
-              for (int a = 0; a < 3; ++a) xq[a] = lo[a] + E.qp[q2][a] * (a < d ? h : 1.0);
-              const double fq = s.prob.f(xq);
-              load += E.qw[q2] * fq * E.phi[q2][slot];
-            }
-            acc += load;
-          }
-      return acc;
-    };
+  s.levels.push_back(std::move(L));
+  if (l == s.n_levels - 1) finish_finest(s);
+}
+
+void finest_load(const pf_setup& s, double t, double* out) {
+  const SetupLevel& L = *s.levels.back();
+  const Geo& g = L.geo;
+  const int me = s.rank;
 #pragma omp parallel for schedule(static)
-    for (int32_t i = 0; i < n; ++i) {
-      int64_t x, y, z;
-      unpack(L->vert[i], x, y, z);
-      const uint8_t c = L->class_of[i];
-      double bi = 0.0;
-      if (c == kDirichlet) {
-        const double xc[3] = {static_cast<double>(x) / denom, static_cast<double>(y) / denom,
-                              d == 3 ? static_cast<double>(z) / denom : 0.0};
-        bi = s.prob.g(xc);  // apply_dirichlet_rhs, assembly.cpp:172-179
-        s.x0[i] = bi;
-      } else if (c == kMaster || c == kSlave) {
-        const int m = g.master_of(x, y, z);
-        int owners[8];
-        const int no = g.owners_around(x, y, z, owners);
-        bi = partial(m, x, y, z);
-        for (int k = 0; k < no; ++k)
-          if (owners[k] != m) bi += partial(owners[k], x, y, z);
-      } else if (c <= kDep2) {
-        bi = partial(me, x, y, z);
-      }
-      s.b[i] = bi;
+  for (int32_t i = 0; i < L.n; ++i) {
+    int64_t x, y, z;
+    g.unpack(L.vert[i], x, y, z);
+    const uint8_t c = L.class_of[i];
+    double bi = 0.0;
+    if (c == kMaster || c == kSlave) {
+      const int m = g.master_of(x, y, z);
+      int owners[8];
+      const int no = g.owners_around(x, y, z, owners);
+      bi = load_partial(s.prob, L, m, x, y, z, t);
+      for (int k = 0; k < no; ++k)
+        if (owners[k] != m) bi += load_partial(s.prob, L, owners[k], x, y, z, t);
+    } else if (c <= kDep2) {
+      bi = load_partial(s.prob, L, me, x, y, z, t);
+    }
+    out[i] = bi;
+  }
+}
+
+// Finest level: rhs and start vector.  Poisson kinds: b = load with the Dirichlet rhs
+// applied, x0 = boundary data on Dirichlet rows, 0 elsewhere (app.cpp:253-260).  Heat:
+// b = the load at t = 0 (app.cpp:178), x0 = the exact solution at t = 0 on every dof
+// (app.cpp:173-176).
+void finish_finest(pf_setup& s) {
+  const SetupLevel& L = *s.levels.back();
+  const Geo& g = L.geo;
+  const int32_t n = L.n;
+  s.b.assign(static_cast<size_t>(n), 0.0);
+  s.x0.assign(static_cast<size_t>(n), 0.0);
+  finest_load(s, 0.0, s.b.data());
+  const bool heat = s.prob.kind == PF_PROBLEM_HEAT;
+  const double denom = static_cast<double>(g.N);
+#pragma omp parallel for schedule(static)
+  for (int32_t i = 0; i < n; ++i) {
+    int64_t x, y, z;
+    g.unpack(L.vert[i], x, y, z);
+    // dof coordinates key / denom (fespace.cpp:66-70)
+    const double xc[3] = {static_cast<double>(x) / denom, static_cast<double>(y) / denom,
+                          g.d == 3 ? static_cast<double>(z) / denom : 0.0};
+    if (heat) {
+      s.x0[i] = s.prob.g(0.0, xc);
+    } else if (L.class_of[i] == kDirichlet) {
+      s.b[i] = s.prob.g(0.0, xc);  // apply_dirichlet_rhs, assembly.cpp:172-179
+      s.x0[i] = s.b[i];
     }
   }
-  s.levels.push_back(std::move(L));
+
+  // --- device load description (pf_load_desc)
+  const int d = g.d;
+  const int64_t N = g.N;
+  s.ld_lattice.resize(static_cast<size_t>(3 * n));
+  s.ld_cells.assign(static_cast<size_t>(n), 0u);
+  s.ld_boundary.assign(static_cast<size_t>(n), 0.0);
+#pragma omp parallel for schedule(static)
+  for (int32_t i = 0; i < n; ++i) {
+    int64_t x, y, z;
+    g.unpack(L.vert[i], x, y, z);
+    s.ld_lattice[3 * static_cast<size_t>(i)] = static_cast<int32_t>(x);
+    s.ld_lattice[3 * static_cast<size_t>(i) + 1] = static_cast<int32_t>(y);
+    s.ld_lattice[3 * static_cast<size_t>(i) + 2] = static_cast<int32_t>(z);
+    const double xc[3] = {static_cast<double>(x) / denom, static_cast<double>(y) / denom,
+                          d == 3 ? static_cast<double>(z) / denom : 0.0};
+    s.ld_boundary[i] = s.prob.profile(xc);
+    if (L.class_of[i] == kDirichlet) continue;
+    int64_t cells[24];
+    const int nc = owned_cells_around(g, s.rank, x, y, z, cells);
+    uint32_t w = static_cast<uint32_t>(nc);
+    for (int c = 0; c < nc; ++c) {
+      const uint32_t bits = (cells[3 * c] == x ? 1u : 0u) | (cells[3 * c + 1] == y ? 2u : 0u) |
+                            (d == 3 && cells[3 * c + 2] == z ? 4u : 0u);
+      w |= bits << (4 + 3 * c);
+    }
+    s.ld_cells[i] = w;
+  }
+  s.ld_factor.assign(static_cast<size_t>(3 * N * 2), 1.0);
+  s.ld_extent.assign(static_cast<size_t>(3 * N), 1.0);
+  const Element& E0 = L.elems.front();
+  for (int a = 0; a < d; ++a)
+    for (int64_t c = 0; c < N; ++c) {
+      const double lo = g.coord(c), h = g.extent(c);
+      s.ld_extent[static_cast<size_t>(a * N + c)] = h;
+      for (int k = 0; k < 2; ++k) {
+        const double xq = lo + E0.qp[k == 0 ? 0 : E0.nq - 1][0] * h;  // Gauss point k (q = 0 / last)
+        double f = 1.0;
+        if (!s.prob.unit()) f = s.prob.axis_sin(a) ? std::sin(kPi * xq) : std::cos(kPi * xq);
+        s.ld_factor[static_cast<size_t>((a * N + c) * 2 + k)] = f;
+      }
+    }
+  s.ld_phi.assign(64, 0.0);
+  for (int q = 0; q < E0.nq; ++q)
+    for (int v = 0; v < E0.nv; ++v) s.ld_phi[static_cast<size_t>(q * 8 + v)] = E0.phi[q][v];
 }
 
 template <typename F>
@@ -778,21 +1028,16 @@ pf_status guard(F&& f) {
   }
 }
 
-}  // namespace
-
-extern "C" {
-
-const char* pf_setup_last_error(void) { return g_setup_err.c_str(); }
-
-pf_status pf_setup_create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem,
-                          pf_setup** out) {
+pf_status create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem, double dt,
+                 pf_setup** out) {
   return guard([&] {
     if (!out) invalid("null output");
     if (dim != 2 && dim != 3) invalid("dimension must be 2 or 3, got " + std::to_string(dim));
     if (n_coarse < 1) invalid("n_coarse must be >= 1");
     if (n_levels < 1) invalid("hierarchy needs at least one level");
     if (rank < 0 || rank >= n_ranks) invalid("rank out of range");
-    if (problem < 0 || problem > 2) invalid("unknown problem");
+    if (problem < 0 || problem > 3) invalid("unknown problem");
+    if (problem == PF_PROBLEM_HEAT && !(dt > 0.0)) invalid("dt must be positive");  // config.cpp:86
     const auto t0 = std::chrono::steady_clock::now();
     auto s = std::make_unique<pf_setup>();
     s->d = dim;
@@ -802,11 +1047,32 @@ pf_status pf_setup_create(int dim, int n_coarse, int n_levels, int n_ranks, int 
     s->rank = rank;
     s->prob.kind = problem;
     s->prob.d = dim;
+    s->prob.dt = problem == PF_PROBLEM_HEAT ? dt : 0.0;
     s->coarse_owner = coarse_partition(dim, n_coarse, n_ranks);
     for (int l = 0; l < n_levels; ++l) build_level(*s, l);
     s->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = s.release();
   });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pf_setup_last_error(void) { return g_setup_err.c_str(); }
+
+pf_status pf_setup_create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem,
+                          pf_setup** out) {
+  if (problem == PF_PROBLEM_HEAT) {
+    g_setup_err = "the heat problem needs dt: use pf_setup_create_heat";
+    return PF_ERR_INVALID_ARGUMENT;
+  }
+  return create(dim, n_coarse, n_levels, n_ranks, rank, problem, 0.0, out);
+}
+
+pf_status pf_setup_create_heat(int dim, int n_coarse, int n_levels, int n_ranks, int rank, double dt,
+                               pf_setup** out) {
+  return create(dim, n_coarse, n_levels, n_ranks, rank, PF_PROBLEM_HEAT, dt, out);
 }
 
 pf_status pf_setup_destroy(pf_setup* s) {
@@ -868,6 +1134,52 @@ pf_status pf_setup_counts(const pf_setup* s, int level, int64_t* n_global, int64
     if (n_dofs) *n_dofs = L.n;
     if (n_own) *n_own = L.n_own;
     if (nnz) *nnz = L.rowptr.empty() ? 0 : L.rowptr.back();
+  });
+}
+
+pf_status pf_setup_rhs_operator(const pf_setup* s, const double** values, int64_t* nnz) {
+  return guard([&] {
+    if (!s) invalid("null setup");
+    if (s->prob.kind != PF_PROBLEM_HEAT) invalid("rhs operator exists for the heat problem only");
+    if (values) *values = s->rhs_op.data();
+    if (nnz) *nnz = static_cast<int64_t>(s->rhs_op.size());
+  });
+}
+
+pf_status pf_setup_load_at(const pf_setup* s, double t, double* out, int64_t n) {
+  return guard([&] {
+    if (!s || !out) invalid("null argument");
+    if (n != s->levels.back()->n) invalid("load length does not match the finest level");
+    finest_load(*s, t, out);
+  });
+}
+
+pf_status pf_setup_load_desc(const pf_setup* s, pf_load_desc* out) {
+  return guard([&] {
+    if (!s || !out) invalid("null argument");
+    const SetupLevel& L = *s->levels.back();
+    std::memset(out, 0, sizeof *out);
+    out->dim = s->d;
+    out->n_cells = static_cast<int32_t>(L.geo.N);
+    out->n_dofs = L.n;
+    out->lattice = s->ld_lattice.data();
+    out->cells = s->ld_cells.data();
+    out->factor = s->ld_factor.data();
+    out->extent = s->ld_extent.data();
+    out->phi = s->ld_phi.data();
+    out->qweight = s->d == 3 ? (0.5 * 0.5) * 0.5 : 0.5 * 0.5;
+    out->boundary = s->ld_boundary.data();
+    out->is_dirichlet = L.is_dir.data();
+  });
+}
+
+pf_status pf_setup_scales(const pf_setup* s, double t, double* source_scale, int32_t* has_dirichlet,
+                          double* dirichlet_scale) {
+  return guard([&] {
+    if (!s) invalid("null setup");
+    if (source_scale) *source_scale = s->prob.source_scale(t);
+    if (has_dirichlet) *has_dirichlet = s->prob.has_dirichlet() ? 1 : 0;
+    if (dirichlet_scale) *dirichlet_scale = s->prob.has_dirichlet() ? s->prob.dirichlet_scale(t) : 0.0;
   });
 }
 

@@ -74,16 +74,27 @@ def _arr(ptr, n, ctype, dtype):
 
 
 class StructuredSetup:
-    """The product's communication-free setup (include/pf_setup.h) for one rank."""
+    """The product's communication-free setup (include/pf_setup.h) for one rank.
+
+    problem = PF_PROBLEM_HEAT builds the Crank-Nicolson hierarchy of the reference's heat
+    run (every level's system M + dt/2 K) and keeps the native setup alive for the time
+    loop: `rhs_op`, `load_at(t)`, `load_desc()`, `scales(t)`."""
 
     def __init__(self, dim: int, n_coarse: int, n_levels: int, n_ranks: int = 1, rank: int = 0,
-                 problem: int = _lib.PF_PROBLEM_BASELINE):
+                 problem: int = _lib.PF_PROBLEM_BASELINE, dt: float | None = None):
         L = _lib.lib()
         self._h = C.c_void_p()
-        _lib.check(L.pf_setup_create(dim, n_coarse, n_levels, n_ranks, rank, problem,
-                                     C.byref(self._h)), setup=True)
+        if problem == _lib.PF_PROBLEM_HEAT:
+            _lib.check(L.pf_setup_create_heat(dim, n_coarse, n_levels, n_ranks, rank,
+                                              0.01 if dt is None else dt, C.byref(self._h)), setup=True)
+        else:
+            _lib.check(L.pf_setup_create(dim, n_coarse, n_levels, n_ranks, rank, problem,
+                                         C.byref(self._h)), setup=True)
         self.dim, self.n_coarse, self.n_levels = dim, n_coarse, n_levels
         self.n_ranks, self.rank, self.problem = n_ranks, rank, problem
+        self.dt = dt if problem == _lib.PF_PROBLEM_HEAT else None
+        if problem == _lib.PF_PROBLEM_HEAT and dt is None:
+            self.dt = 0.01
         self.levels = [self._level(l) for l in range(n_levels)]
         bp, xp, n = C.c_void_p(), C.c_void_p(), C.c_int64()
         _lib.check(L.pf_setup_rhs(self._h, C.byref(bp), C.byref(xp), C.byref(n)), setup=True)
@@ -95,8 +106,49 @@ class StructuredSetup:
         s = C.c_double()
         _lib.check(L.pf_setup_seconds(self._h, C.byref(s)), setup=True)
         self.seconds = s.value
-        L.pf_setup_destroy(self._h)
-        self._h = None
+        self.rhs_op = None
+        if problem == _lib.PF_PROBLEM_HEAT:
+            vp, nnz = C.c_void_p(), C.c_int64()
+            _lib.check(L.pf_setup_rhs_operator(self._h, C.byref(vp), C.byref(nnz)), setup=True)
+            self.rhs_op = _arr(vp, nnz.value, C.c_double, np.float64)
+        else:
+            self.close()
+
+    def close(self):
+        if self._h:
+            _lib.lib().pf_setup_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _live(self):
+        if not self._h:
+            raise _lib.PfError("native setup released (only heat setups keep it)")
+        return self._h
+
+    def load_at(self, t: float) -> np.ndarray:
+        """Finest-level load at time t (assemble_load, assembly.cpp:144-160), host order,
+        Dirichlet rows 0."""
+        out = np.zeros(self.levels[-1].n)
+        _lib.check(_lib.lib().pf_setup_load_at(self._live(), t, out.ctypes.data, out.size), setup=True)
+        return out
+
+    def load_desc(self) -> _lib.LoadDesc:
+        """The device load description (pointers valid while this setup lives)."""
+        d = _lib.LoadDesc()
+        _lib.check(_lib.lib().pf_setup_load_desc(self._live(), C.byref(d)), setup=True)
+        return d
+
+    def scales(self, t: float):
+        """(source_scale, has_dirichlet, dirichlet_scale) at time t, host libm."""
+        s, g, hd = C.c_double(), C.c_double(), C.c_int32()
+        _lib.check(_lib.lib().pf_setup_scales(self._live(), t, C.byref(s), C.byref(hd), C.byref(g)),
+                   setup=True)
+        return s.value, bool(hd.value), g.value
 
     def _level(self, l: int) -> LevelArrays:
         L = _lib.lib()

@@ -169,3 +169,26 @@ def test_golden_sweeps(name, sm):
     want = dict(zip(map(tuple, g["keys"]), g["values"]))
     scale = max(abs(v) for v in want.values())
     assert max(abs(got[k] - want[k]) for k in want) <= 1e-14 * scale
+
+
+@pytest.mark.parametrize("dim,nc,L,K", [(3, 2, 3, 2), (2, 3, 3, 3), (3, 2, 3, 1)])
+def test_oracle_heat_loop_matches_reference_run_heat(ref_lib, dim, nc, L, K):
+    """The restated Crank-Nicolson loop on the reference's own level data, rhs operator and
+    loads equals the reference's run_heat (app.cpp:146-230, :299-305) bit for bit: same
+    solution per carrier key, same last residual history.  Pins the oracle for the heat
+    parity tests on the GPU."""
+    from oracle.restated import Oracle, heat_loop
+    dt, steps = 0.02, 3
+    R = ref_lib.build(dim, nc, L, K, 3, dt=dt, n_loads=steps)
+    rep = ref_lib.heat(dim, nc, L, K, dt=dt, end_time=steps * dt, smoother=0, pre=2, post=2,
+                       outer_tol=1e-10)
+    O = Oracle([[lv.to_level_arrays() for lv in R.ranks[r]] for r in range(K)])
+    tops = [R.ranks[r][-1] for r in range(K)]
+    denom = nc * 2 ** (L - 1)
+    u, res = heat_loop(O, tops, R.rhs_op, R.x0, R.b, R.loads, dt, steps, cfg(), dim, denom)
+    got = {}
+    for r in range(K):
+        for i in np.flatnonzero(tops[r].owns_row):
+            got[tuple(int(k) for k in tops[r].keys[i])] = float(u[r][i])
+    assert got == rep["solution"]
+    assert np.array_equal(res, rep["residuals"])

@@ -1,8 +1,9 @@
 """CPU: the product's communication-free setup (include/pf_setup.h) reproduces the
 reference's setup pipeline (partition.cpp, fespace.cpp, femapper.cpp, assembly.cpp,
 multigrid.cpp:35-72) per carrier key: dof classes, owns_row, the ordered channel key
-lists, the matrix pattern and values, the prolongation map, the rhs and start vector —
-against the live compiled reference and against the committed golden structure tables.
+lists, the matrix pattern and values (bit for bit), the prolongation map, the rhs (bit for
+bit) and start vector — against the live compiled reference and against the committed
+golden structure tables.
 """
 import glob
 import os
@@ -16,7 +17,7 @@ from paper_1609_04809_b200.levels import StructuredSetup
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
-def compare(R, S):
+def compare(R, S, live_b_only=False):
     K, levels = R.K, R.n_levels
     for r in range(K):
         for l in range(levels):
@@ -39,8 +40,8 @@ def compare(R, S):
                         for i in range(x.n) for e in range(x.row_offsets[i], x.row_offsets[i + 1])}
             ma, mb = mat(a.to_level_arrays(), ka), mat(b, kb)
             assert ma.keys() == mb.keys()
-            scale = max(abs(v) for v in ma.values())
-            assert max(abs(ma[k] - mb[k]) for k in ma) <= 1e-14 * scale
+            # bit-exact: same element matrices per cell extent, same gcn summation order
+            assert ma == mb, (r, l)
             if l > 0:
                 kca = [tuple(k) for k in R.ranks[r][l - 1].keys]
                 kcb = [tuple(k) for k in S[r].levels[l - 1].keys]
@@ -52,7 +53,8 @@ def compare(R, S):
         ka = [tuple(k) for k in R.ranks[r][-1].keys]
         ib = {tuple(k): i for i, k in enumerate(S[r].levels[-1].keys)}
         bb = np.array([S[r].b[ib[k]] for k in ka])
-        assert np.abs(R.b[r] - bb).max() <= 1e-13 * max(np.abs(R.b[r]).max(), 1e-300)
+        live = (R.ranks[r][-1].class_of != 7) if live_b_only else slice(None)
+        assert np.array_equal(R.b[r][live], bb[live]), r
         assert np.array_equal(R.x0[r], np.array([S[r].x0[ib[k]] for k in ka]))
 
 
@@ -110,3 +112,64 @@ def test_setup_counts_at_c1():
     assert sorted(set(top.color.tolist())) == list(range(8))
     k = top.keys[:top.n_own, 1:]
     assert np.array_equal(top.color, (k[:, 0] & 1) * 4 + (k[:, 1] & 1) * 2 + (k[:, 2] & 1))
+
+
+@pytest.mark.parametrize("dim,nc,L,K", [(3, 2, 3, 1), (3, 2, 3, 4), (2, 3, 3, 5), (3, 3, 2, 3)])
+def test_heat_setup_matches_reference(ref_lib, dim, nc, L, K):
+    """The heat problem (model.cpp:19-31): every level's Crank-Nicolson system M + dt/2 K,
+    the finest rhs operator M - dt/2 K (app.cpp:185-189), u(0) and the loads at t = 0, dt,
+    2 dt (assembly.cpp:144-160) equal the reference's bit for bit, per carrier key."""
+    dt = 0.02
+    R = ref_lib.build(dim, nc, L, K, 3, dt=dt, n_loads=2)
+    S = [StructuredSetup(dim, nc, L, K, r, _lib.PF_PROBLEM_HEAT, dt=dt) for r in range(K)]
+    # systems, P, classes, channels, x0 = u(0), b = load(0) (Dirichlet rows of a load are
+    # never read: apply_dirichlet_rhs overwrites them, app.cpp:195)
+    compare(R, S, live_b_only=True)
+    for r in range(K):
+        a, b = R.ranks[r][-1], S[r].levels[-1]
+        ka, kb = [tuple(k) for k in a.keys], [tuple(k) for k in b.keys]
+        mb = {(kb[i], kb[b.cols[e]]): S[r].rhs_op[e]
+              for i in range(b.n) for e in range(b.row_offsets[i], b.row_offsets[i + 1])}
+        ma = {(ka[i], ka[a.cols[e]]): R.rhs_op[r][e]
+              for i in range(a.n) for e in range(a.row_offsets[i], a.row_offsets[i + 1])}
+        assert ma == mb, r
+        ib = {k: i for i, k in enumerate(kb)}
+        perm = np.array([ib[k] for k in ka])
+        live = a.class_of != 7  # Dirichlet rows of a load are overwritten (app.cpp:195)
+        for k in range(2):
+            got = S[r].load_at((k + 1) * dt)[perm]
+            assert np.array_equal(got[live], R.loads[r][k][live]), (r, k)
+        S[r].close()
+
+
+def test_heat_setup_arguments():
+    with pytest.raises(_lib.InvalidArgument, match="dt"):
+        StructuredSetup(3, 2, 2, problem=_lib.PF_PROBLEM_HEAT, dt=0.0)
+    with pytest.raises(_lib.InvalidArgument, match="heat"):
+        _lib.check(_lib.lib().pf_setup_create(3, 2, 2, 1, 0, _lib.PF_PROBLEM_HEAT, None), setup=True)
+
+
+@pytest.mark.parametrize("dim,nc,L,K,prob", [
+    (3, 2, 3, 1, 0), (3, 2, 4, 8, 0), (2, 3, 3, 5, 1), (3, 3, 2, 7, 2), (2, 4, 3, 6, 0), (3, 2, 3, 3, 3)])
+def test_setup_arrays_identical_to_reference(ref_lib, dim, nc, L, K, prob):
+    """Not just per key: the product numbers each rank's dofs exactly as the reference does
+    (first touch over the local cells in gcn order, then stable by class — fespace.cpp:47-85,
+    femapper.cpp:167-199) and orders every prolongation row by the home cell's parent
+    (multigrid.cpp:43-68), so the level data it hands to pf_hierarchy_set_level are the
+    reference's arrays byte for byte: CSR, keys, owns_row, channels, P, b, x0."""
+    R = ref_lib.build(dim, nc, L, K, prob)
+    S = [StructuredSetup(dim, nc, L, K, r, prob) for r in range(K)]
+    for r in range(K):
+        for l in range(L):
+            a, b = R.ranks[r][l].to_level_arrays(), S[r].levels[l]
+            for f in ("row_offsets", "cols", "vals", "keys", "owns_row", "is_dir", "class_of"):
+                assert np.array_equal(getattr(a, f), getattr(b, f)), (r, l, f)
+            if l > 0:
+                for f in ("p_offsets", "p_cols", "p_w"):
+                    assert np.array_equal(getattr(a, f), getattr(b, f)), (r, l, f)
+            ca = [(c.kind, c.peer, list(c.send), list(c.recv)) for c in a.channels]
+            cb = [(c.kind, c.peer, list(c.send), list(c.recv)) for c in b.channels if len(c.send) or len(c.recv)]
+            assert ca == cb, (r, l)
+        if prob != 3:
+            assert np.array_equal(R.b[r], S[r].b) and np.array_equal(R.x0[r], S[r].x0), r
+        S[r].close()
