@@ -74,6 +74,9 @@ def _bind(L):
         L.ref_heat_copy.argtypes = [P, P, P, P]
         L.ref_heat_free.argtypes = [P]
         L.ref_set_heat.argtypes = [C.c_double, C.c_int]
+        L.ref_heat_bench.argtypes = [C.c_int] * 4 + [C.c_double, C.c_int, C.c_double, C.c_int, C.c_int,
+                                                     C.c_double, C.c_int, C.c_int, P, P, i64p,
+                                                     C.POINTER(C.c_int)]
         L.ref_heat_data.argtypes = [P, C.c_int, P, P]
     return L
 
@@ -278,3 +281,20 @@ def heat(dim, n_coarse, levels, K, *, dt=0.01, end_time=0.05, smoother=0, dampin
     names = ("initialization", "assembling", "solving", "communication", "total")
     return dict(solution=sol, residuals=res[:nr.value], l2=float(l2[0]), linf=float(linf[0]),
                 phases=dict(zip(names, ph.tolist())))
+
+
+def heat_bench(dim, n_coarse, levels, K, *, dt=0.01, smoother=0, damping=0.8, pre=2, post=2,
+               outer_tol=1e-10, warmup=0, steps=1):
+    """Seconds per Crank-Nicolson step of the reference (heat_rank_body's loop body through
+    its public functions), max over K rank threads."""
+    L = lib()
+    per = np.zeros(steps)
+    setup = np.zeros(1)
+    ng = C.c_int64(0)
+    its = C.c_int(0)
+    rc = L.ref_heat_bench(dim, n_coarse, levels, K, dt, smoother, damping, pre, post, outer_tol,
+                          warmup, steps, _ptr(per), _ptr(setup), C.byref(ng), C.byref(its))
+    if rc:
+        raise RuntimeError(L.ref_last_error().decode())
+    return dict(step_seconds=per, setup_seconds=float(setup[0]), n_global=int(ng.value),
+                iterations=int(its.value))

@@ -491,6 +491,78 @@ int ref_bench(int dim, int n_coarse, int levels, int K, int problem, int smoothe
   return rc;
 }
 
+// Time per Crank-Nicolson step of heat_rank_body's loop (app.cpp:180-213: assemble_load,
+// spmv with M - dt/2 K, Dirichlet rows, solve_outer), max over K rank threads, driven
+// through the reference's own public functions; setup (build_hierarchy) excluded.
+int ref_heat_bench(int dim, int n_coarse, int levels, int K, double dt, int smoother_kind, double damping,
+                   int pre, int post, double outer_tol, int warmup, int steps, double* step_seconds,
+                   double* setup_seconds, std::int64_t* n_global, int* iterations) {
+  std::mutex mu;
+  std::vector<double> per(static_cast<std::size_t>(steps), 0.0);
+  double setup = 0;
+  std::int64_t ng = 0;
+  int its = 0;
+  g_heat_dt = dt;
+  const int rc = guarded([&] {
+    run_on_ranks(K, [&](Transport& tp) {
+      const double t0 = now_s();
+      MultigridHierarchy h = build(dim, n_coarse, levels, 3, tp);
+      const double t1 = now_s();
+      MultigridLevel& top = h.finest();
+      const ParFEMapper& mapper = *top.mapper;
+      const ScalarField f = HeatProblem{dim}.source();
+      const ScalarField g = HeatProblem{dim}.dirichlet();
+      CsrSparseMatrix rhs_op = top.stiffness;
+      for (std::size_t i = 0; i < rhs_op.values.size(); ++i)
+        rhs_op.values[i] = top.mass.values[i] - 0.5 * dt * top.stiffness.values[i];
+      MultigridConfig cfg;
+      cfg.smoother.kind = smoother_kind == 0 ? SmootherKind::Jacobi : SmootherKind::GaussSeidel;
+      cfg.smoother.damping = damping;
+      cfg.pre_smooth = pre;
+      cfg.post_smooth = post;
+      cfg.outer_tol = outer_tol;
+      const ScalarField uex = HeatProblem{dim}.exact();
+      DistributedVector u(static_cast<std::size_t>(mapper.n_dofs), 0.0);
+      for (int i = 0; i < mapper.n_dofs; ++i) u[static_cast<std::size_t>(i)] = uex(0.0, mapper.dofs[static_cast<std::size_t>(i)].coords);
+      DistributedVector load_now = top.load;
+      DistributedVector b(static_cast<std::size_t>(mapper.n_dofs), 0.0);
+      std::vector<double> mine(static_cast<std::size_t>(steps), 0.0);
+      int it = 0;
+      for (int step = 0; step < warmup + steps; ++step) {
+        const double t_next = static_cast<double>(step + 1) * dt;
+        barrier(tp);
+        const double a = now_s();
+        DistributedVector load_next = assemble_load(mapper, *top.comm, f, t_next);
+        spmv(rhs_op, u.values, b.values);
+        for (std::size_t i = 0; i < b.values.size(); ++i) b[i] += 0.5 * dt * (load_now[i] + load_next[i]);
+        apply_dirichlet_rhs(b, g, t_next, mapper);
+        for (int i = 0; i < mapper.n_dofs; ++i)
+          if (mapper.class_of[static_cast<std::size_t>(i)] == DofClass::Dirichlet)
+            u[static_cast<std::size_t>(i)] = b[static_cast<std::size_t>(i)];
+        const SolveStats st = outer(h, u, b, cfg);
+        load_now = std::move(load_next);
+        const double e = now_s();
+        it = st.iterations;
+        if (step >= warmup) mine[static_cast<std::size_t>(step - warmup)] = e - a;
+      }
+      done_with(h);
+      std::lock_guard<std::mutex> lock(mu);
+      for (int k = 0; k < steps; ++k)
+        per[static_cast<std::size_t>(k)] = std::max(per[static_cast<std::size_t>(k)], mine[static_cast<std::size_t>(k)]);
+      setup = std::max(setup, t1 - t0);
+      ng = mapper.n_global;
+      its = it;
+    });
+  });
+  if (rc == 0) {
+    std::copy(per.begin(), per.end(), step_seconds);
+    *setup_seconds = setup;
+    *n_global = ng;
+    *iterations = its;
+  }
+  return rc;
+}
+
 // The reference's own Crank-Nicolson heat run (run_heat, app.cpp:146-230,
 // :299-305), unmodified: returns a handle to its SolveReport (NULL on failure).
 void* ref_heat(int dim, int n_coarse, int levels, int K, double dt, double end_time, int smoother_kind,
