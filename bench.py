@@ -311,7 +311,8 @@ def run_b200(args):
         "vcycle_ms": vcycle_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(),
-                     "kernel": "k_jacobi (finest-level damped-Jacobi sweep, SELL-32 fp64)",
+                     "kernel": "k_jacobi (finest-level damped-Jacobi sweep; SELL-32x4, int32 columns, "
+                               "8-bit index into the table of distinct fp64 values)",
                      "kernel_us": sweep_ms * 1e3, "algorithmic_bytes_per_launch": sweep_bytes,
                      "peak_source": peak_src},
         "cpu_baseline": cpu,

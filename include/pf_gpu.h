@@ -102,6 +102,12 @@ typedef struct {
   const int64_t* p_offsets;
   const int32_t* p_cols;
   const double* p_weights;
+  /* optional placement hint, n_dofs entries or NULL: inside each colour the device lays
+   * own rows out in ascending row_order (ties: host order), e.g. a lexicographic lattice
+   * index so that a warp's 32 rows are neighbours and their column gathers coalesce.
+   * Placement never changes a result (rows of one colour are independent; every
+   * order-dependent sum is fixed by the host order). */
+  const int64_t* row_order;
 } pf_level_desc;
 
 /* parfem::SmootherConfig (solvers.hpp:9-14). `damping` is the Jacobi damping and

@@ -72,7 +72,8 @@ class LevelDesc(C.Structure):
                 ("row_offsets", C.c_void_p), ("col_indices", C.c_void_p), ("values", C.c_void_p),
                 ("owns_row", C.c_void_p), ("is_dirichlet", C.c_void_p), ("color", C.c_void_p),
                 ("n_channels", C.c_int32), ("channels", C.POINTER(ChannelDesc)),
-                ("p_offsets", C.c_void_p), ("p_cols", C.c_void_p), ("p_weights", C.c_void_p)]
+                ("p_offsets", C.c_void_p), ("p_cols", C.c_void_p), ("p_weights", C.c_void_p),
+                ("row_order", C.c_void_p)]
 
 
 class LoadDesc(C.Structure):

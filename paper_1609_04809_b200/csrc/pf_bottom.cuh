@@ -82,19 +82,19 @@ constexpr int kBotChunk = 28;  // a Q1 row has 27 entries
 
 __device__ __forceinline__ void bot_row_offdiag(const SellView& A, int32_t row, const double* x, double& acc,
                                                 double& diag) {
-  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
+  const int64_t base = sell_row_base(A.slice_ptr, row);
   const int len = A.row_len[row];
   if (len > kBotChunk) {  // long rows: the bandwidth kernel's loop
-    row_offdiag<false>(A, row, x, acc, diag);
+    row_offdiag<false, false, 0>(A, row, x, acc, diag);
     return;
   }
   int32_t c[kBotChunk];
   double v[kBotChunk], xv[kBotChunk];
 #pragma unroll
   for (int k = 0; k < kBotChunk; ++k) {
-    const int64_t e = base + static_cast<int64_t>(k < len ? k : 0) * kSlice;
+    const int64_t e = sell_entry(base, k < len ? k : 0);
     c[k] = A.cols[e];
-    v[k] = A.vals[e];
+    v[k] = A.vals[e];  // bottom levels are never index-encoded (fill_bottom)
   }
 #pragma unroll
   for (int k = 0; k < kBotChunk; ++k) xv[k] = x[c[k]];
@@ -111,7 +111,7 @@ __device__ __forceinline__ void bot_row_offdiag(const SellView& A, int32_t row, 
 // (measured: the 28-wide unrolled form that helps the sweeps makes the residual,
 // restriction and prolongation phases 2-3x slower; they keep the bandwidth loop)
 __device__ __forceinline__ double bot_row_dot(const SellView& A, int32_t row, const double* x, double acc) {
-  return row_dot<false, false>(A, row, x, acc);
+  return row_dot<false, false, 0>(A, row, x, acc);
 }
 
 // grid barrier + optional phase timestamp (block 0, thread 0)

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(kBlock) k_load(LoadView L, double s, double* _
 
 // b = Op u + half_dt (load_now + load_next) on every non-Dirichlet row (app.cpp:191-194:
 // spmv, then b_i += 0.5 dt (ln_i + lnx_i)); Dirichlet rows are written by k_dirichlet.
-__global__ void __launch_bounds__(kBlock) k_cn_rhs(SellView Op, const double* __restrict__ u,
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_cn_rhs(SellView Op, const double* __restrict__ u,
                                                    const double* __restrict__ ln,
                                                    const double* __restrict__ lnx, double half_dt,
                                                    const uint8_t* __restrict__ is_dir,
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kBlock) k_cn_rhs(SellView Op, const double* __
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n || is_dir[row]) return;
-  const double y = row_dot<false>(Op, row, u, 0.0);
+  const double y = row_dot<false, true, kVK>(Op, row, u, 0.0);
   b[row] = __dadd_rn(y, __dmul_rn(half_dt, __dadd_rn(ln[row], lnx[row])));
 }
 

@@ -35,34 +35,89 @@ namespace pf {
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
 
+// Value of stored entry e.  kVK = the view's value kind when known at compile time (the
+// bandwidth kernels are instantiated per kind), -1 = read it from the view.
+template <int kVK>
+__device__ __forceinline__ double sell_val(const SellView& A, int64_t e) {
+  if constexpr (kVK == 0) {
+    return ld_stream(A.vals + e);
+  } else if constexpr (kVK == 1) {
+    return __ldg(A.table + __ldcs(static_cast<const unsigned char*>(A.vidx) + e));
+  } else if constexpr (kVK == 2) {
+    return __ldg(A.table + __ldcs(static_cast<const unsigned short*>(A.vidx) + e));
+  } else {
+    if (A.vkind == 1) return __ldg(A.table + static_cast<const unsigned char*>(A.vidx)[e]);
+    if (A.vkind == 2) return __ldg(A.table + static_cast<const unsigned short*>(A.vidx)[e]);
+    return A.vals[e];
+  }
+}
+
+// One group of 4 stored entries (SELL-32x4) starting at e (e % 4 == 0): columns and values.
+template <int kVK>
+__device__ __forceinline__ void sell_group(const SellView& A, int64_t e, int32_t c[4], double v[4]) {
+  const int4 cc = __ldcs(reinterpret_cast<const int4*>(A.cols + e));
+  c[0] = cc.x;
+  c[1] = cc.y;
+  c[2] = cc.z;
+  c[3] = cc.w;
+  if constexpr (kVK == 1) {
+    const unsigned int w = __ldcs(reinterpret_cast<const unsigned int*>(static_cast<const unsigned char*>(A.vidx) + e));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldg(A.table + ((w >> (8 * k)) & 255u));
+  } else if constexpr (kVK == 2) {
+    const uint2 w = __ldcs(reinterpret_cast<const uint2*>(static_cast<const unsigned short*>(A.vidx) + e));
+    v[0] = __ldg(A.table + (w.x & 0xffffu));
+    v[1] = __ldg(A.table + (w.x >> 16));
+    v[2] = __ldg(A.table + (w.y & 0xffffu));
+    v[3] = __ldg(A.table + (w.y >> 16));
+  } else if constexpr (kVK == 0) {
+    const double2 a = __ldcs(reinterpret_cast<const double2*>(A.vals + e));
+    const double2 b = __ldcs(reinterpret_cast<const double2*>(A.vals + e + 2));
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = b.x;
+    v[3] = b.y;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = sell_val<-1>(A, e + k);
+  }
+}
+
 // acc := acc - sum_{c != row} a_rc x_c over the row's entries in stored order; diag := a_rr.
-// This is the inner loop of one_local_sweep (solvers.cpp:21-51).
-template <bool kReadOnlyX, bool kRes = false>
+// This is the inner loop of one_local_sweep (solvers.cpp:21-51).  Entries are consumed in
+// chunks of kChunkGroups x 4 (vector loads of columns and values first, then the x gathers,
+// then the arithmetic in stored order); entries past the row length are padding, never used.
+template <bool kReadOnlyX, bool kRes = false, int kVK = -1, int kGroups = kChunkGroups>
 __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, const double* x,
                                             double& acc, double& diag, double* res = nullptr,
                                             double x_row = 0.0) {
   // kRes: *res (starting at b_r) also subtracts every product in stored order, the
   // diagonal included — the reference's residual_norm row (linalg.cpp:66-70) bit for bit.
-  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
+  const int64_t base = sell_row_base(A.slice_ptr, row);
   const int len = A.row_len[row];
   double r = kRes ? *res : 0.0;
-  int j = 0;
-  // (measured: a branch-free variant that also gathers x for the diagonal needs 40
-  // registers and runs the C2 sweep 17 % slower — occupancy beats per-thread ILP here)
-  for (; j + kUnroll <= len; j += kUnroll) {
-    int32_t c[kUnroll];
-    double v[kUnroll], xv[kUnroll];
+  constexpr int kC = kGroups * kGroup;
+  for (int j = 0; j < len; j += kC) {
+    int32_t c[kC];
+    double v[kC], xv[kC];
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) {
-      const int64_t e = base + static_cast<int64_t>(j + k) * kSlice;
-      c[k] = ld_stream(A.cols + e);
-      v[k] = ld_stream(A.vals + e);
+    for (int g = 0; g < kGroups; ++g) {
+      if (j + g * kGroup < len) {
+        sell_group<kVK>(A, sell_entry(base, j + g * kGroup), c + g * kGroup, v + g * kGroup);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k) {
+          c[g * kGroup + k] = row;
+          v[g * kGroup + k] = 0.0;
+        }
+      }
     }
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k)
-      xv[k] = (c[k] == row) ? x_row : (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]);
+    for (int k = 0; k < kC; ++k)
+      xv[k] = (c[k] == row || j + k >= len) ? x_row : (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]);
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) {
+    for (int k = 0; k < kC; ++k) {
+      if (j + k >= len) break;
       const double p = __dmul_rn(v[k], xv[k]);
       if (kRes) r = __dsub_rn(r, p);
       if (c[k] == row)
@@ -71,49 +126,40 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
         acc = __dsub_rn(acc, p);
     }
   }
-  for (; j < len; ++j) {
-    const int64_t e = base + static_cast<int64_t>(j) * kSlice;
-    const int32_t c = ld_stream(A.cols + e);
-    const double v = ld_stream(A.vals + e);
-    const double p = __dmul_rn(v, c == row ? x_row : (kReadOnlyX ? __ldg(x + c) : x[c]));
-    if (kRes) r = __dsub_rn(r, p);
-    if (c == row)
-      diag = v;
-    else
-      acc = __dsub_rn(acc, p);
-  }
   if (kRes) *res = r;
 }
 
 // acc := acc op sum_c a_rc x_c over all entries in stored order.
 //   kSubtract: acc -= a x   (residual_norm, linalg.cpp:64-73: acc starts at b)
 //   else:      acc += a x   (spmv, linalg.cpp:49-56: acc starts at 0)
-template <bool kSubtract, bool kReadOnlyX = true>
+template <bool kSubtract, bool kReadOnlyX = true, int kVK = -1, int kGroups = kChunkGroups>
 __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const double* __restrict__ x,
                                           double acc) {
-  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
+  const int64_t base = sell_row_base(A.slice_ptr, row);
   const int len = A.row_len[row];
-  int j = 0;
-  for (; j + kUnroll <= len; j += kUnroll) {
-    int32_t c[kUnroll];
-    double v[kUnroll], xv[kUnroll];
+  constexpr int kC = kGroups * kGroup;
+  for (int j = 0; j < len; j += kC) {
+    int32_t c[kC];
+    double v[kC], xv[kC];
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) {
-      const int64_t e = base + static_cast<int64_t>(j + k) * kSlice;
-      c[k] = ld_stream(A.cols + e);
-      v[k] = ld_stream(A.vals + e);
+    for (int g = 0; g < kGroups; ++g) {
+      if (j + g * kGroup < len) {
+        sell_group<kVK>(A, sell_entry(base, j + g * kGroup), c + g * kGroup, v + g * kGroup);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k) {
+          c[g * kGroup + k] = 0;
+          v[g * kGroup + k] = 0.0;
+        }
+      }
     }
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) xv[k] = kReadOnlyX ? __ldg(x + c[k]) : x[c[k]];
+    for (int k = 0; k < kC; ++k) xv[k] = (j + k < len) ? (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]) : 0.0;
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k)
+    for (int k = 0; k < kC; ++k) {
+      if (j + k >= len) break;
       acc = kSubtract ? __dsub_rn(acc, __dmul_rn(v[k], xv[k])) : __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
-  }
-  for (; j < len; ++j) {
-    const int64_t e = base + static_cast<int64_t>(j) * kSlice;
-    const int32_t c = ld_stream(A.cols + e);
-    const double p = __dmul_rn(ld_stream(A.vals + e), kReadOnlyX ? __ldg(x + c) : x[c]);
-    acc = kSubtract ? __dsub_rn(acc, p) : __dadd_rn(acc, p);
+    }
   }
   return acc;
 }
@@ -122,7 +168,8 @@ __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const 
 // reference's full scratch copy: own rows [0, n_own) are relaxed from x_old into
 // x_new; every other row is carried over unchanged (the sweep never writes Slave,
 // Halo or Dirichlet entries, solvers.hpp:16-20).
-__global__ void __launch_bounds__(kBlock) k_jacobi(SellView A, const double* __restrict__ x_old,
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi(SellView A, const double* __restrict__ x_old,
                                                    double* __restrict__ x_new,
                                                    const double* __restrict__ b, int32_t n_own,
                                                    int32_t n, double omega) {
@@ -135,7 +182,7 @@ __global__ void __launch_bounds__(kBlock) k_jacobi(SellView A, const double* __r
     return;
   }
   double acc = b[row], diag = 0.0;
-  row_offdiag<true>(A, row, x_old, acc, diag);
+  row_offdiag<true, false, kVK>(A, row, x_old, acc, diag);
   x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
 }
 
@@ -185,8 +232,8 @@ __global__ void k_decide(const double* __restrict__ sumsq, int n_parts, double t
 // one colour never couple, so the result does not depend on the order in which the
 // threads of this launch run.  kSor=false: x = acc/diag (solvers.cpp:21-34);
 // kSor=true: x = (1-w) x + w acc/diag.
-template <bool kSor>
-__global__ void __launch_bounds__(kBlock) k_color_sweep(SellView A, double* x,
+template <bool kSor, int kVK>
+__global__ void __launch_bounds__(kBlock, PF_SOR_MINB) k_color_sweep(SellView A, double* x,
                                                         const double* __restrict__ b, int32_t row0,
                                                         int32_t row1, double omega) {
   PF_PDL_ENTRY();
@@ -195,7 +242,7 @@ __global__ void __launch_bounds__(kBlock) k_color_sweep(SellView A, double* x,
   double acc = b[row], diag = 0.0;
   // Other colours are read-only during this launch and this row's own entry is
   // skipped by row_offdiag, so the read-only path is safe for the gather.
-  row_offdiag<true>(A, row, x, acc, diag);
+  row_offdiag<true, false, kVK, kSorChunkGroups>(A, row, x, acc, diag);
   if (kSor)
     x[row] = __dadd_rn(__dmul_rn(1.0 - omega, x[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
   else
@@ -204,22 +251,24 @@ __global__ void __launch_bounds__(kBlock) k_color_sweep(SellView A, double* x,
 
 // Residual of the cycle (multigrid.cpp:166-167): y = A x (spmv order, acc from 0), r = b - y,
 // on rows [0, n).
-__global__ void __launch_bounds__(kBlock) k_residual(SellView A, const double* __restrict__ x,
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_residual(SellView A, const double* __restrict__ x,
                                                      const double* __restrict__ b,
                                                      double* __restrict__ r, int32_t n) {
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n) return;
-  r[row] = __dsub_rn(b[row], row_dot<false>(A, row, x, 0.0));
+  r[row] = __dsub_rn(b[row], row_dot<false, true, kVK>(A, row, x, 0.0));
 }
 
 // y = A x on every row (linalg.cpp:45-57).
-__global__ void __launch_bounds__(kBlock) k_spmv(SellView A, const double* __restrict__ x,
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_spmv(SellView A, const double* __restrict__ x,
                                                  double* __restrict__ y, int32_t n) {
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n) return;
-  y[row] = row_dot<false>(A, row, x, 0.0);
+  y[row] = row_dot<false, true, kVK>(A, row, x, 0.0);
 }
 
 // Deterministic block sum: fixed shuffle tree inside each warp, then warp 0 sums the
@@ -244,7 +293,8 @@ __device__ __forceinline__ double block_sum(double v, double* smem /* kBlock/32 
 // only) sums the partials in index order, stores the rank sum in *sumsq and, when
 // `norm_out` is set (single-subdomain case: the ascending-rank allreduce of one value
 // is 0.0 + s, transport.cpp:139-149), sqrt of it.  The ticket is reset for the next use.
-__global__ void __launch_bounds__(kBlock) k_resnorm(SellView A, const double* __restrict__ x,
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_resnorm(SellView A, const double* __restrict__ x,
                                                     const double* __restrict__ b, int32_t n_own,
                                                     double* __restrict__ partials,
                                                     unsigned int* ticket, double* sumsq,
@@ -255,7 +305,7 @@ __global__ void __launch_bounds__(kBlock) k_resnorm(SellView A, const double* __
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   double sq = 0.0;
   if (row < n_own) {
-    const double acc = row_dot<true>(A, row, x, b[row]);
+    const double acc = row_dot<true, true, kVK>(A, row, x, b[row]);
     sq = __dmul_rn(acc, acc);
   }
   const double s = block_sum(sq, smem);
@@ -284,7 +334,8 @@ __global__ void __launch_bounds__(kBlock) k_resnorm(SellView A, const double* __
 // test of the previous cycle (multigrid.cpp:230) costs no extra pass over the matrix.
 // Deterministic block sums + last-block finish exactly as k_resnorm; *sumsq gets this
 // subdomain's sum of squares.
-__global__ void __launch_bounds__(kBlock) k_jacobi_norm(SellView A, const double* __restrict__ x_old,
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_jacobi_norm(SellView A, const double* __restrict__ x_old,
                                                         double* __restrict__ x_new,
                                                         const double* __restrict__ b, int32_t n_own,
                                                         int32_t n, double omega,
@@ -301,7 +352,7 @@ __global__ void __launch_bounds__(kBlock) k_jacobi_norm(SellView A, const double
       x_new[row] = xo;
     } else {
       double acc = b[row], diag = 0.0, res = b[row];
-      row_offdiag<true, true>(A, row, x_old, acc, diag, &res, xo);
+      row_offdiag<true, true, kVK>(A, row, x_old, acc, diag, &res, xo);
       sq = __dmul_rn(res, res);
       x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
     }
@@ -337,12 +388,13 @@ __global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* o
 
 // x_f += P x_c over every local fine dof (multigrid.cpp:121-129 + :183-184): the
 // correction is accumulated from 0 in P's entry order, then added.
-__global__ void __launch_bounds__(kBlock) k_prolong_add(SellView P, const double* __restrict__ xc,
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_prolong_add(SellView P, const double* __restrict__ xc,
                                                         double* __restrict__ xf, int32_t n_f, int add) {
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_f) return;
-  const double acc = row_dot<false>(P, row, xc, 0.0);
+  const double acc = row_dot<false, true, kVK>(P, row, xc, 0.0);
   xf[row] = add ? __dadd_rn(xf[row], acc) : acc;
 }
 
@@ -352,7 +404,8 @@ __global__ void __launch_bounds__(kBlock) k_prolong_add(SellView P, const double
 // (multigrid.cpp:172-179): Dirichlet coarse entries of b become 0 and the coarse x is
 // zeroed.  (Zeroing before the master/slave accumulate is equivalent: Dirichlet
 // carriers are Dirichlet on every rank, so they only ever accumulate zeros.)
-__global__ void __launch_bounds__(kBlock) k_restrict(SellView R, const double* __restrict__ rf,
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_restrict(SellView R, const double* __restrict__ rf,
                                                      double* __restrict__ bc,
                                                      double* __restrict__ xc,
                                                      const uint8_t* __restrict__ is_dir_c,
@@ -360,7 +413,7 @@ __global__ void __launch_bounds__(kBlock) k_restrict(SellView R, const double* _
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_c) return;
-  const double acc = row_dot<false>(R, row, rf, 0.0);
+  const double acc = row_dot<false, true, kVK>(R, row, rf, 0.0);
   bc[row] = (zero_dirichlet && is_dir_c[row]) ? 0.0 : acc;
   if (xc) xc[row] = 0.0;
 }
@@ -387,11 +440,11 @@ __device__ void coarse_gs_body(const CoarseSub* __restrict__ subs, int n_sub, do
       double local = 0.0;
       for (int32_t i = 0; i < S.n_own; ++i) {
         const int32_t d = S.host_of_own[i];
-        const int64_t base = S.A.slice_ptr[d >> 5] + (d & 31);
+        const int64_t base = sell_row_base(S.A.slice_ptr, d);
         double acc = bs[d];
         for (int j = 0; j < S.A.row_len[d]; ++j) {
-          const int64_t e = base + static_cast<int64_t>(j) * kSlice;
-          acc = __dsub_rn(acc, __dmul_rn(S.A.vals[e], xs[S.A.cols[e]]));
+          const int64_t e = sell_entry(base, j);
+          acc = __dsub_rn(acc, __dmul_rn(sell_val<-1>(S.A, e), xs[S.A.cols[e]]));
         }
         local = __dadd_rn(local, __dmul_rn(acc, acc));
       }
@@ -414,15 +467,15 @@ __device__ void coarse_gs_body(const CoarseSub* __restrict__ subs, int n_sub, do
       const double* bs = b + S.offset;
       for (int32_t i = 0; i < S.n_own; ++i) {
         const int32_t d = S.host_of_own[i];
-        const int64_t base = S.A.slice_ptr[d >> 5] + (d & 31);
+        const int64_t base = sell_row_base(S.A.slice_ptr, d);
         double acc = bs[d], diag = 0.0;
         for (int j = 0; j < S.A.row_len[d]; ++j) {
-          const int64_t e = base + static_cast<int64_t>(j) * kSlice;
+          const int64_t e = sell_entry(base, j);
           const int32_t c = S.A.cols[e];
           if (c == d)
-            diag = S.A.vals[e];
+            diag = sell_val<-1>(S.A, e);
           else
-            acc = __dsub_rn(acc, __dmul_rn(S.A.vals[e], xs[c]));
+            acc = __dsub_rn(acc, __dmul_rn(sell_val<-1>(S.A, e), xs[c]));
         }
         xs[d] = __ddiv_rn(acc, diag);
       }

@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <type_traits>
+#include <unordered_map>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -89,7 +91,80 @@ thread_local int64_t* g_capture_counter = nullptr;
 
 Launcher launcher(pf_hierarchy* h) { return Launcher{h, g_capture_counter ? g_capture_counter : &h->launches}; }
 
-SellView view(const DevSell& s) { return SellView{s.vals.p, s.cols.p, s.slice_ptr.p, s.row_len.p}; }
+SellView view_of(const DevVals& v, const DevSell& s) {
+  const void* idx = v.vkind == 1 ? static_cast<const void*>(v.vi8.p)
+                  : v.vkind == 2 ? static_cast<const void*>(v.vi16.p) : nullptr;
+  return SellView{v.vals.p, s.cols.p, s.slice_ptr.p, s.row_len.p, idx, v.table.p, v.vkind};
+}
+SellView view(const DevSell& s) { return view_of(s.vals, s); }
+
+// Kernel instantiation for a view's value kind: f(std::integral_constant<int, kind>).
+template <typename F>
+void vk_dispatch(int vkind, F&& f) {
+  switch (vkind) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    default: f(std::integral_constant<int, 0>{}); break;
+  }
+}
+
+bool value_index_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_VALUE_INDEX");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+// Only bandwidth-bound operators are index-encoded: small ones (the bottom levels, whose
+// kernels are latency-bound) keep fp64 values and one dependent load fewer per entry.
+int64_t value_index_min_entries() {
+  static const int64_t m = [] {
+    const char* e = std::getenv("PF_VALUE_INDEX_MIN");
+    return e ? std::atoll(e) : int64_t(1) << 21;
+  }();
+  return m;
+}
+
+// Stored values (SELL order, padding included) -> device: an 8/16-bit index into the table
+// of distinct values (distinguished by bit pattern, so -0.0 and 0.0 stay apart) when there
+// are at most 65,536 of them, else fp64.
+void encode_values(const std::vector<double>& sv, DevVals& out) {
+  out = DevVals{};
+  if (value_index_enabled() && static_cast<int64_t>(sv.size()) >= value_index_min_entries()) {
+    std::unordered_map<uint64_t, uint32_t> ids;
+    std::vector<double> table;
+    std::vector<uint32_t> idx(sv.size());
+    bool fits = true;
+    for (size_t i = 0; i < sv.size(); ++i) {
+      uint64_t bits;
+      std::memcpy(&bits, &sv[i], sizeof bits);
+      auto it = ids.find(bits);
+      if (it == ids.end()) {
+        if (table.size() == 65536) {
+          fits = false;
+          break;
+        }
+        it = ids.emplace(bits, static_cast<uint32_t>(table.size())).first;
+        table.push_back(sv[i]);
+      }
+      idx[i] = it->second;
+    }
+    if (fits) {
+      out.table.upload(table);
+      if (table.size() <= 256) {
+        out.vkind = 1;
+        out.vi8.upload(std::vector<uint8_t>(idx.begin(), idx.end()));
+      } else {
+        out.vkind = 2;
+        out.vi16.upload(std::vector<uint16_t>(idx.begin(), idx.end()));
+      }
+      return;
+    }
+  }
+  out.vkind = 0;
+  out.vals.upload(sv);
+}
 
 void check_level(const pf_hierarchy* h, int level) {
   if (!h) invalid("null hierarchy");
@@ -117,6 +192,7 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
   for (int64_t s = 0; s < n_slices; ++s) {
     int32_t w = 0;
     for (int l = 0; l < kSlice; ++l) w = std::max(w, rlen[s * kSlice + l]);
+    w = (w + kGroup - 1) / kGroup * kGroup;  // SELL-32x4: whole groups of 4
     sptr[s + 1] = sptr[s] + static_cast<int64_t>(w) * kSlice;
   }
   std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
@@ -127,7 +203,7 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
       const int64_t d = s * kSlice + l;
       const int32_t len = d < n ? rlen[d] : 0;
       for (int64_t j = 0; j < w; ++j) {
-        const int64_t e = sptr[s] + j * kSlice + l;
+        const int64_t e = sell_entry(sptr[s] + static_cast<int64_t>(l) * kGroup, static_cast<int>(j));
         if (j < len) {
           sc[e] = col[off[d] + j];
           sv[e] = val[off[d] + j];
@@ -140,7 +216,7 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
   }
   out.slice_ptr.upload(sptr);
   out.row_len.upload(rlen);
-  out.vals.upload(sv);
+  encode_values(sv, out.vals);
   out.cols.upload(sc);
   out.nnz = n > 0 ? off[n] : 0;
   out.stored = sptr[n_slices];
@@ -208,7 +284,16 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
   std::vector<int32_t> inv(static_cast<size_t>(n), 0);
   {
     std::vector<int32_t> next(D.color_start.begin(), D.color_start.end() - 1);
-    for (int32_t i = 0; i < n_own; ++i) D.perm[i] = next[color[i]]++;
+    if (H.order.empty()) {
+      for (int32_t i = 0; i < n_own; ++i) D.perm[i] = next[color[i]]++;
+    } else {  // placement hint: inside a colour, ascending (order, host index)
+      std::vector<int32_t> own(static_cast<size_t>(n_own));
+      std::iota(own.begin(), own.end(), 0);
+      std::stable_sort(own.begin(), own.end(), [&](int32_t a, int32_t b) {
+        return color[a] != color[b] ? color[a] < color[b] : H.order[a] < H.order[b];
+      });
+      for (int32_t i : own) D.perm[i] = next[color[i]]++;
+    }
     for (int32_t i = n_own; i < n; ++i) D.perm[i] = i;
     for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
   }
@@ -500,6 +585,7 @@ HostLevel parse_desc(const pf_level_desc& dd, int me, int world, bool need_p) {
   if (d->is_dirichlet) H.is_dir.assign(d->is_dirichlet, d->is_dirichlet + d->n_dofs);
   else H.is_dir.assign(static_cast<size_t>(d->n_dofs), 0);
   if (d->color) H.color.assign(d->color, d->color + d->n_own_dofs);
+  if (d->row_order) H.order.assign(d->row_order, d->row_order + d->n_dofs);
   for (int i = 0; i < d->n_channels; ++i) {
     const pf_channel_desc& c = d->channels[i];
     if (c.kind < 0 || c.kind >= PF_NUM_CHANNEL_KINDS) invalid("bad channel kind");
@@ -627,6 +713,7 @@ bool fill_bottom(pf_hierarchy* h, pf_hierarchy::Bottom& bot, const std::vector<B
       B.max_colors = std::max(B.max_colors, D.n_colors);
       bot.color_bufs.emplace_back();
       bot.color_bufs.back().upload(D.color_start);
+      if (D.A.vals.vkind || D.P.vals.vkind || D.R.vals.vkind) return false;  // k_bottom reads fp64 values
       S.A = view(D.A);
       S.host_of_own = D.d_perm.p;
       S.color_start = bot.color_bufs.back().p;
@@ -774,8 +861,10 @@ void enq_resnorm(pf_hierarchy* h, int l, const double* x, const double* b) {
   const bool single = h->world == 1;
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = L.sub[s];
-    launch(static_cast<unsigned>(D.resnorm_blocks), kBlock, k_resnorm, view(D.A), x + D.offset,
+    vk_dispatch(D.A.vals.vkind, [&](auto V) {
+    launch(static_cast<unsigned>(D.resnorm_blocks), kBlock, k_resnorm<decltype(V)::value>, view(D.A), x + D.offset,
            b + D.offset, D.n_own, D.partials.p, D.ticket.p, L.sumsq.p + s, single ? L.norm.p : nullptr);
+    });
   }
   if (!single) enq_allreduce(h, L, true);
 }
@@ -784,14 +873,18 @@ void enq_residual(pf_hierarchy* h, int l, const double* x, const double* b, doub
   Level& L = h->levels[l];
   auto launch = launcher(h);
   for (DevLevel& D : L.sub)
-    launch(grid_for(D.n), kBlock, k_residual, view(D.A), x + D.offset, b + D.offset, r + D.offset, D.n);
+    vk_dispatch(D.A.vals.vkind, [&](auto V) {
+      launch(grid_for(D.n), kBlock, k_residual<decltype(V)::value>, view(D.A), x + D.offset, b + D.offset, r + D.offset, D.n);
+    });
 }
 
 void enq_spmv(pf_hierarchy* h, int l, const double* x, double* y) {
   Level& L = h->levels[l];
   auto launch = launcher(h);
   for (DevLevel& D : L.sub)
-    launch(grid_for(D.n), kBlock, k_spmv, view(D.A), x + D.offset, y + D.offset, D.n);
+    vk_dispatch(D.A.vals.vkind, [&](auto V) {
+      launch(grid_for(D.n), kBlock, k_spmv<decltype(V)::value>, view(D.A), x + D.offset, y + D.offset, D.n);
+    });
 }
 
 void enq_copy(pf_hierarchy* h, const double* src, double* dst, int64_t n) {
@@ -811,8 +904,11 @@ void enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
       if (sc.kind == PF_SMOOTHER_JACOBI) {
         if (!(first_done && sweep == 0 && local == 0))
           for (DevLevel& D : L.sub)
-            launch(grid_for(D.n), kBlock, k_jacobi, view(D.A), static_cast<const double*>(bufs[cur] + D.offset),
-                   bufs[cur ^ 1] + D.offset, b + D.offset, D.n_own, D.n, sc.damping);
+            vk_dispatch(D.A.vals.vkind, [&](auto V) {
+              launch(grid_for(D.n), kBlock, k_jacobi<decltype(V)::value>, view(D.A),
+                     static_cast<const double*>(bufs[cur] + D.offset), bufs[cur ^ 1] + D.offset, b + D.offset,
+                     D.n_own, D.n, sc.damping);
+            });
         cur ^= 1;
       } else {
         const bool sor = sc.kind == PF_SMOOTHER_MULTICOLOR_SOR;
@@ -822,12 +918,15 @@ void enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
           for (DevLevel& D : L.sub) {
             if (c >= D.n_colors) continue;
             const int32_t r0 = D.color_start[c], r1 = D.color_start[c + 1];
-            if (sor)
-              launch(grid_for(r1 - r0), kBlock, k_color_sweep<true>, view(D.A), bufs[cur] + D.offset,
-                     b + D.offset, r0, r1, sc.damping);
-            else
-              launch(grid_for(r1 - r0), kBlock, k_color_sweep<false>, view(D.A), bufs[cur] + D.offset,
-                     b + D.offset, r0, r1, 1.0);
+            vk_dispatch(D.A.vals.vkind, [&](auto V) {
+              constexpr int vk = decltype(V)::value;
+              if (sor)
+                launch(grid_for(r1 - r0), kBlock, k_color_sweep<true, vk>, view(D.A), bufs[cur] + D.offset,
+                       b + D.offset, r0, r1, sc.damping);
+              else
+                launch(grid_for(r1 - r0), kBlock, k_color_sweep<false, vk>, view(D.A), bufs[cur] + D.offset,
+                       b + D.offset, r0, r1, 1.0);
+            });
           }
       }
     }
@@ -843,7 +942,10 @@ void enq_prolong(pf_hierarchy* h, int fine, const double* xc, double* xf, int ad
   auto launch = launcher(h);
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = F.sub[s];
-    launch(grid_for(D.n), kBlock, k_prolong_add, view(D.P), xc + Cl.sub[s].offset, xf + D.offset, D.n, add);
+    vk_dispatch(D.P.vals.vkind, [&](auto V) {
+      launch(grid_for(D.n), kBlock, k_prolong_add<decltype(V)::value>, view(D.P), xc + Cl.sub[s].offset,
+             xf + D.offset, D.n, add);
+    });
   }
 }
 
@@ -855,8 +957,10 @@ void enq_restrict(pf_hierarchy* h, int fine, const double* rf, double* bc, doubl
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = F.sub[s];
     DevLevel& DC = Cl.sub[s];
-    launch(grid_for(DC.n), kBlock, k_restrict, view(D.R), rf + D.offset, bc + DC.offset, xc ? xc + DC.offset : nullptr,
-           static_cast<const uint8_t*>(DC.d_is_dir.p), DC.n, zero_dir);
+    vk_dispatch(D.R.vals.vkind, [&](auto V) {
+      launch(grid_for(DC.n), kBlock, k_restrict<decltype(V)::value>, view(D.R), rf + D.offset, bc + DC.offset,
+             xc ? xc + DC.offset : nullptr, static_cast<const uint8_t*>(DC.d_is_dir.p), DC.n, zero_dir);
+    });
   }
 }
 
@@ -1009,14 +1113,17 @@ void enq_norm_head(pf_hierarchy* h, pf_vector* x, const double* b, const pf_mult
   auto launch = launcher(h);
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = L.sub[s];
-    if (fused_head(cfg))
-      launch(grid_for(D.n), kBlock, k_jacobi_norm, view(D.A), static_cast<const double*>(x->cur() + D.offset),
-             x->alt() + D.offset, b + D.offset, D.n_own, D.n, cfg.smoother.damping, D.partials.p,
-             D.ticket.p, L.sumsq.p + s);
-    else
-      launch(static_cast<unsigned>(D.resnorm_blocks), kBlock, k_resnorm, view(D.A),
-             static_cast<const double*>(x->cur() + D.offset), b + D.offset, D.n_own, D.partials.p,
-             D.ticket.p, L.sumsq.p + s, static_cast<double*>(nullptr));
+    vk_dispatch(D.A.vals.vkind, [&](auto V) {
+      constexpr int vk = decltype(V)::value;
+      if (fused_head(cfg))
+        launch(grid_for(D.n), kBlock, k_jacobi_norm<vk>, view(D.A), static_cast<const double*>(x->cur() + D.offset),
+               x->alt() + D.offset, b + D.offset, D.n_own, D.n, cfg.smoother.damping, D.partials.p,
+               D.ticket.p, L.sumsq.p + s);
+      else
+        launch(static_cast<unsigned>(D.resnorm_blocks), kBlock, k_resnorm<vk>, view(D.A),
+               static_cast<const double*>(x->cur() + D.offset), b + D.offset, D.n_own, D.partials.p,
+               D.ticket.p, L.sumsq.p + s, static_cast<double*>(nullptr));
+    });
   }
 }
 
@@ -1303,7 +1410,7 @@ void set_error(const char* m) { g_last_error = m; }
 struct pf_operator {
   pf_hierarchy* h = nullptr;
   int level = 0;
-  std::vector<pf::DevBuf<double>> vals;  // per subdomain, SELL layout of DevLevel::A
+  std::vector<pf::DevVals> vals;  // per subdomain, SELL layout of DevLevel::A
   std::vector<bool> set;
 };
 
@@ -1869,11 +1976,16 @@ pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double*
     if (kind == PF_SMOOTHER_JACOBI) {
       const double* src = (i & 1) ? x->alt() : x->cur();
       double* dst = (i & 1) ? x->cur() : x->alt();
-      launch(grid_for(D.n), kBlock, k_jacobi, view(D.A), src, dst, b, D.n_own, D.n, 0.8);
+      vk_dispatch(D.A.vals.vkind, [&](auto V) {
+        launch(grid_for(D.n), kBlock, k_jacobi<decltype(V)::value>, view(D.A), src, dst, b, D.n_own, D.n, 0.8);
+      });
     } else {
       for (int c = 0; c < D.n_colors; ++c)
-        launch(grid_for(D.color_start[c + 1] - D.color_start[c]), kBlock, k_color_sweep<true>, view(D.A),
-               x->cur(), b, D.color_start[c], D.color_start[c + 1], kind == PF_SMOOTHER_MULTICOLOR_SOR ? 1.2 : 1.0);
+        vk_dispatch(D.A.vals.vkind, [&](auto V) {
+          launch(grid_for(D.color_start[c + 1] - D.color_start[c]), kBlock,
+                 k_color_sweep<true, decltype(V)::value>, view(D.A), x->cur(), b, D.color_start[c],
+                 D.color_start[c + 1], kind == PF_SMOOTHER_MULTICOLOR_SOR ? 1.2 : 1.0);
+        });
     }
   };
   for (int i = 0; i < 3; ++i) one(i);  // warm-up
@@ -1885,9 +1997,11 @@ pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double*
   PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   if (mean_ms) *mean_ms = ms / iters;
   // B = 12 z + 4 n + 8 m + 8 n (b) + 8 n (out), n = own rows,
-  // z = own nnz, m = distinct columns the own rows touch.
+  // z = own nnz, m = distinct columns the own rows touch — with the stored value width
+  // (8 B fp64, or a 1/2 B table index) in place of the 8 of the 12.
   if (bytes)
-    *bytes = 12.0 * D.A.own_nnz + 4.0 * D.n_own + 8.0 * D.own_cols_touched + 16.0 * D.n_own;
+    *bytes = (4.0 + D.A.vals.value_bytes()) * D.A.own_nnz + 4.0 * D.n_own + 8.0 * D.own_cols_touched +
+             16.0 * D.n_own;
   PF_API_END
 }
 
@@ -1950,8 +2064,7 @@ namespace pf {
 namespace {
 
 SellView op_view(const pf_operator* op, int s) {
-  const DevLevel& D = op->h->levels[op->level].sub[s];
-  return SellView{op->vals[s].p, D.A.cols.p, D.A.slice_ptr.p, D.A.row_len.p};
+  return view_of(op->vals[s], op->h->levels[op->level].sub[s].A);
 }
 
 void check_op(const pf_operator* op) {
@@ -1999,8 +2112,10 @@ void enq_cn_rhs(pf_operator* op, pf_load* ld, const double* u, const double* ln,
   auto launch = launcher(h);
   for (int s = 0; s < h->n_sub; ++s) {
     const DevLevel& D = L.sub[s];
-    launch(grid_for(D.n), kBlock, k_cn_rhs, op_view(op, s), u + D.offset, ln + D.offset, lnx + D.offset,
-           half_dt, static_cast<const uint8_t*>(D.d_is_dir.p), b + D.offset, D.n);
+    vk_dispatch(op->vals[s].vkind, [&](auto V) {
+      launch(grid_for(D.n), kBlock, k_cn_rhs<decltype(V)::value>, op_view(op, s), u + D.offset, ln + D.offset,
+             lnx + D.offset, half_dt, static_cast<const uint8_t*>(D.d_is_dir.p), b + D.offset, D.n);
+    });
   }
   enq_dirichlet(ld, has, gscale, b, u_out);
 }
@@ -2035,11 +2150,11 @@ pf_status pf_operator_set_values(pf_operator* op, int sub, const double* values,
   std::vector<double> sv(static_cast<size_t>(D.A.stored), 0.0);
   for (int32_t hr = 0; hr < D.n; ++hr) {
     const int32_t d = D.perm[hr];
-    const int64_t base = D.sell_ptr[d / kSlice] + (d % kSlice);
+    const int64_t base = sell_row_base(D.sell_ptr.data(), d);
     for (int64_t k = D.csr_rowptr[hr]; k < D.csr_rowptr[hr + 1]; ++k)
-      sv[static_cast<size_t>(base + (k - D.csr_rowptr[hr]) * kSlice)] = values[k];
+      sv[static_cast<size_t>(sell_entry(base, static_cast<int>(k - D.csr_rowptr[hr])))] = values[k];
   }
-  op->vals[sub].upload(sv);
+  encode_values(sv, op->vals[sub]);
   op->set[sub] = true;
   PF_API_END
 }
@@ -2055,7 +2170,9 @@ pf_status pf_operator_apply(pf_operator* op, const pf_vector* x, pf_vector* y) {
   auto launch = launcher(h);
   for (int s = 0; s < h->n_sub; ++s) {
     const DevLevel& D = L.sub[s];
-    launch(grid_for(D.n), kBlock, k_spmv, op_view(op, s), x->cur() + D.offset, y->cur() + D.offset, D.n);
+    vk_dispatch(op->vals[s].vkind, [&](auto V) {
+      launch(grid_for(D.n), kBlock, k_spmv<decltype(V)::value>, op_view(op, s), x->cur() + D.offset, y->cur() + D.offset, D.n);
+    });
   }
   sync(h);
   PF_API_END

@@ -69,15 +69,28 @@ struct HostLevel {
   std::vector<double> vals;
   std::vector<uint8_t> owns_row, is_dir;
   std::vector<int32_t> color;
+  std::vector<int64_t> order;  // optional device placement hint (pf_level_desc::row_order)
   std::vector<HostChannel> channels;
   std::vector<int64_t> p_off;
   std::vector<int32_t> p_col;
   std::vector<double> p_w;
 };
 
+// The stored values of a SELL-32 operator: fp64, or indices into a table of the distinct
+// values (SellView::vkind).
+struct DevVals {
+  int vkind = 0;
+  DevBuf<double> vals;
+  DevBuf<uint8_t> vi8;
+  DevBuf<uint16_t> vi16;
+  DevBuf<double> table;
+  int64_t bytes() const { return vals.bytes() + vi8.bytes() + vi16.bytes() + table.bytes(); }
+  int value_bytes() const { return vkind == 1 ? 1 : vkind == 2 ? 2 : 8; }
+};
+
 // SELL-32 operator on the device.
 struct DevSell {
-  DevBuf<double> vals;
+  DevVals vals;
   DevBuf<int32_t> cols;
   DevBuf<int64_t> slice_ptr;
   DevBuf<int32_t> row_len;

@@ -1094,6 +1094,7 @@ pf_status pf_setup_level(const pf_setup* s, int level, pf_level_desc* out) {
     out->owns_row = L.owns_row.data();
     out->is_dirichlet = L.is_dir.data();
     out->color = L.color.data();
+    out->row_order = L.vert.data();  // lexicographic lattice index: coalesced gathers
     out->n_channels = static_cast<int32_t>(L.descs.size());
     out->channels = L.descs.data();
     if (level > 0) {

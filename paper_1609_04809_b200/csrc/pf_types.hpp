@@ -17,14 +17,57 @@
 namespace pf {
 
 constexpr int kSlice = 32;     // SELL slice height == warp size
-constexpr int kBlock = 256;    // threads per block of the row kernels
+#ifndef PF_BLOCK
+#define PF_BLOCK 256
+#endif
+#ifndef PF_CHUNK_GROUPS
+#define PF_CHUNK_GROUPS 1
+#endif
+constexpr int kBlock = PF_BLOCK;  // threads per block of the row kernels
 constexpr int kUnroll = 9;     // 27 = 3 x 9 entries per Q1 row: 9 loads in flight per chunk
+constexpr int kGroup = 4;      // SELL-32x4: 4 consecutive entries of a row are contiguous per lane
+constexpr int kChunkGroups = PF_CHUNK_GROUPS;  // groups of 4 entries per chunk in the bandwidth kernels
+#ifndef PF_SOR_GROUPS
+#define PF_SOR_GROUPS 1
+#endif
+// colour sweeps are single-wave launches: a row's latency chain, not throughput, bounds them
+constexpr int kSorChunkGroups = PF_SOR_GROUPS;
+// Minimum resident blocks per SM of the row kernels (caps them at 32 registers): a full
+// SM of warps hides the gather latency better than extra registers per thread
+// (measured at C2: sweep 100 -> 92 us; each SOR colour fits one wave: 129 -> 112 us).
+#ifndef PF_SOR_MINB
+#define PF_SOR_MINB 8
+#endif
+#ifndef PF_JAC_MINB
+#define PF_JAC_MINB 8
+#endif
+#ifndef PF_ROW_MINB
+#define PF_ROW_MINB 8
+#endif
 
+// SELL-32x4 layout: slice s holds rows 32s..32s+31; entry j of lane l sits at
+//   slice_ptr[s] + (j / 4) * 128 + 4 l + j % 4,
+// so a lane reads 4 entries with one 16-byte column load (one 4-byte index / 32-byte value
+// load) and a warp's load of one group is one contiguous 512 B (128 B / 1 KB) run.
+PF_HD inline int64_t sell_row_base(const int64_t* slice_ptr, int32_t row) {
+  return slice_ptr[row >> 5] + (static_cast<int64_t>(row & 31) << 2);
+}
+PF_HD inline int64_t sell_entry(int64_t row_base, int j) {
+  return row_base + (static_cast<int64_t>(j >> 2) << 7) + (j & 3);
+}
+
+// SELL-32 operator view.  Values are stored either as fp64 (vkind 0) or, when the matrix
+// has few distinct values (a constant-coefficient stencil has 6-8), as 8-bit (vkind 1) or
+// 16-bit (vkind 2) indices into a table of the distinct values: lossless, the kernels read
+// the exact same doubles, and the finest sweep streams 5 instead of 12 bytes per entry.
 struct SellView {
   const double* __restrict__ vals;
   const int32_t* __restrict__ cols;
   const int64_t* __restrict__ slice_ptr;
   const int32_t* __restrict__ row_len;
+  const void* __restrict__ vidx;
+  const double* __restrict__ table;
+  int32_t vkind;
 };
 
 // One subdomain of the coarse level, for the sequential coarse solve.

@@ -40,6 +40,7 @@ class LevelArrays:
     p_w: np.ndarray | None = None
     keys: np.ndarray | None = None      # (n, 4) int64: entity kind, lattice key
     class_of: np.ndarray | None = None  # uint8 DofClass
+    order: np.ndarray | None = None     # int64 device placement hint (pf_level_desc.row_order)
 
     def normalized(self) -> "LevelArrays":
         def a(x, t):
@@ -51,7 +52,7 @@ class LevelArrays:
                            a(self.owns_row, np.uint8), a(self.is_dir, np.uint8),
                            a(self.color, np.int32), chans, a(self.p_offsets, np.int64),
                            a(self.p_cols, np.int32), a(self.p_w, np.float64),
-                           a(self.keys, np.int64), a(self.class_of, np.uint8))
+                           a(self.keys, np.int64), a(self.class_of, np.uint8), a(self.order, np.int64))
 
     def desc(self):
         """(LevelDesc, keepalive) pointing into this object's arrays."""
@@ -63,7 +64,7 @@ class LevelArrays:
         p = lambda x: None if x is None else x.ctypes.data  # noqa: E731
         d = _lib.LevelDesc(L.n, L.n_own, p(L.row_offsets), p(L.cols), p(L.vals), p(L.owns_row),
                            p(L.is_dir), p(L.color), len(L.channels), chans, p(L.p_offsets),
-                           p(L.p_cols), p(L.p_w))
+                           p(L.p_cols), p(L.p_w), p(L.order))
         return d, (L, chans)
 
 
@@ -170,7 +171,8 @@ class StructuredSetup:
                           _arr(d.is_dirichlet, n, C.c_uint8, np.uint8),
                           _arr(d.color, n_own, C.c_int32, np.int32), chans,
                           keys=_arr(kp, 4 * n, C.c_int64, np.int64).reshape(n, 4),
-                          class_of=_arr(cp, n, C.c_uint8, np.uint8))
+                          class_of=_arr(cp, n, C.c_uint8, np.uint8),
+                          order=_arr(d.row_order, n, C.c_int64, np.int64) if d.row_order else None)
         if l > 0:
             out.p_offsets = _arr(d.p_offsets, n + 1, C.c_int64, np.int64)
             pn = int(out.p_offsets[-1])
