@@ -72,6 +72,7 @@ struct BotCfg {
   int kind, pre, post, local_sweeps, coarse_max_iter;
   double omega, coarse_tol;
   int block_top;  // levels 0..block_top inside block 0 (-1: none); chosen per smoother
+  int calib;      // PF_BOTTOM_CALIB: empty grid-barrier phases first (profiling aid)
 };
 
 // Latency-oriented row routines for the bottom levels, where each phase is a chain of
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __restrict_
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     D.stamps[0] = t0;
   }
+  for (int i = 0; i < c.calib; ++i) G.sync(D, ph);
   if (accumulate_top) bot_accumulate_scatter(D, top, D.lev[top].b, G, ph);
   const int bt = c.block_top < D.block_top ? c.block_top : D.block_top;
   for (int l = top; l > bt && l >= 1; --l) bot_descend(D, l, c, G, ph);

@@ -84,9 +84,31 @@ __device__ __forceinline__ void sell_group(const SellView& A, int64_t e, int32_t
 }
 
 // acc := acc - sum_{c != row} a_rc x_c over the row's entries in stored order; diag := a_rr.
-// This is the inner loop of one_local_sweep (solvers.cpp:21-51).  Entries are consumed in
-// chunks of kChunkGroups x 4 (vector loads of columns and values first, then the x gathers,
-// then the arithmetic in stored order); entries past the row length are padding, never used.
+// This is the inner loop of one_local_sweep (solvers.cpp:21-51).  Entries are consumed a
+// group of 4 at a time (one 16-byte column load, one index / value load, four x gathers),
+// the next group's column and value loads issued before the current group's arithmetic;
+// the last, partial group is predicated (entries past the row length are padding).
+template <bool kReadOnlyX, bool kRes>
+__device__ __forceinline__ void offdiag_group(const int32_t c[4], const double v[4], int n, int32_t row,
+                                              const double* x, double x_row, double& acc, double& diag,
+                                              double& r) {
+  double xv[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    xv[k] = (k >= n || c[k] == row) ? x_row : (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < n) {
+      const double p = __dmul_rn(v[k], xv[k]);
+      if (kRes) r = __dsub_rn(r, p);
+      if (c[k] == row)
+        diag = v[k];
+      else
+        acc = __dsub_rn(acc, p);
+    }
+  }
+}
+
 template <bool kReadOnlyX, bool kRes = false, int kVK = -1, int kGroups = kChunkGroups>
 __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, const double* x,
                                             double& acc, double& diag, double* res = nullptr,
@@ -96,35 +118,23 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
   const int64_t base = sell_row_base(A.slice_ptr, row);
   const int len = A.row_len[row];
   double r = kRes ? *res : 0.0;
-  constexpr int kC = kGroups * kGroup;
-  for (int j = 0; j < len; j += kC) {
-    int32_t c[kC];
-    double v[kC], xv[kC];
+  if (len > 0) {
+    int32_t c[4];
+    double v[4];
+    sell_group<kVK>(A, base, c, v);
+    int j = 0;
+    for (; j + 4 < len; j += 4) {
+      int32_t cn[4];
+      double vn[4];
+      sell_group<kVK>(A, sell_entry(base, j + 4), cn, vn);
+      offdiag_group<kReadOnlyX, kRes>(c, v, 4, row, x, x_row, acc, diag, r);
 #pragma unroll
-    for (int g = 0; g < kGroups; ++g) {
-      if (j + g * kGroup < len) {
-        sell_group<kVK>(A, sell_entry(base, j + g * kGroup), c + g * kGroup, v + g * kGroup);
-      } else {
-#pragma unroll
-        for (int k = 0; k < kGroup; ++k) {
-          c[g * kGroup + k] = row;
-          v[g * kGroup + k] = 0.0;
-        }
+      for (int k = 0; k < 4; ++k) {
+        c[k] = cn[k];
+        v[k] = vn[k];
       }
     }
-#pragma unroll
-    for (int k = 0; k < kC; ++k)
-      xv[k] = (c[k] == row || j + k >= len) ? x_row : (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]);
-#pragma unroll
-    for (int k = 0; k < kC; ++k) {
-      if (j + k >= len) break;
-      const double p = __dmul_rn(v[k], xv[k]);
-      if (kRes) r = __dsub_rn(r, p);
-      if (c[k] == row)
-        diag = v[k];
-      else
-        acc = __dsub_rn(acc, p);
-    }
+    offdiag_group<kReadOnlyX, kRes>(c, v, len - j, row, x, x_row, acc, diag, r);
   }
   if (kRes) *res = r;
 }
@@ -132,34 +142,39 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
 // acc := acc op sum_c a_rc x_c over all entries in stored order.
 //   kSubtract: acc -= a x   (residual_norm, linalg.cpp:64-73: acc starts at b)
 //   else:      acc += a x   (spmv, linalg.cpp:49-56: acc starts at 0)
+template <bool kSubtract, bool kReadOnlyX>
+__device__ __forceinline__ void dot_group(const int32_t c[4], const double v[4], int n, const double* x,
+                                          double& acc) {
+  double xv[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) xv[k] = k < n ? (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]) : 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (k < n) acc = kSubtract ? __dsub_rn(acc, __dmul_rn(v[k], xv[k])) : __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
+}
+
 template <bool kSubtract, bool kReadOnlyX = true, int kVK = -1, int kGroups = kChunkGroups>
 __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const double* __restrict__ x,
                                           double acc) {
   const int64_t base = sell_row_base(A.slice_ptr, row);
   const int len = A.row_len[row];
-  constexpr int kC = kGroups * kGroup;
-  for (int j = 0; j < len; j += kC) {
-    int32_t c[kC];
-    double v[kC], xv[kC];
+  if (len > 0) {
+    int32_t c[4];
+    double v[4];
+    sell_group<kVK>(A, base, c, v);
+    int j = 0;
+    for (; j + 4 < len; j += 4) {
+      int32_t cn[4];
+      double vn[4];
+      sell_group<kVK>(A, sell_entry(base, j + 4), cn, vn);
+      dot_group<kSubtract, kReadOnlyX>(c, v, 4, x, acc);
 #pragma unroll
-    for (int g = 0; g < kGroups; ++g) {
-      if (j + g * kGroup < len) {
-        sell_group<kVK>(A, sell_entry(base, j + g * kGroup), c + g * kGroup, v + g * kGroup);
-      } else {
-#pragma unroll
-        for (int k = 0; k < kGroup; ++k) {
-          c[g * kGroup + k] = 0;
-          v[g * kGroup + k] = 0.0;
-        }
+      for (int k = 0; k < 4; ++k) {
+        c[k] = cn[k];
+        v[k] = vn[k];
       }
     }
-#pragma unroll
-    for (int k = 0; k < kC; ++k) xv[k] = (j + k < len) ? (kReadOnlyX ? __ldg(x + c[k]) : x[c[k]]) : 0.0;
-#pragma unroll
-    for (int k = 0; k < kC; ++k) {
-      if (j + k >= len) break;
-      acc = kSubtract ? __dsub_rn(acc, __dmul_rn(v[k], xv[k])) : __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
-    }
+    dot_group<kSubtract, kReadOnlyX>(c, v, len - j, x, acc);
   }
   return acc;
 }

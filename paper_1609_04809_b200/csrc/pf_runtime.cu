@@ -1045,8 +1045,9 @@ void enq_bottom(pf_hierarchy* h, const pf_hierarchy::Bottom& bot, const pf_multi
   // tiny levels inside one block (V-cycle 1.83 -> 1.75 ms); Jacobi (1 barrier per sweep)
   // loses parallelism there and keeps the whole grid
   const int block_top = cfg.smoother.kind == PF_SMOOTHER_JACOBI ? -1 : 1 << 20;
+  static const int calib = std::getenv("PF_BOTTOM_CALIB") ? std::atoi(std::getenv("PF_BOTTOM_CALIB")) : 0;
   const BotCfg c{cfg.smoother.kind, cfg.pre_smooth, cfg.post_smooth, cfg.smoother.local_sweeps,
-                 cfg.coarse_max_iter, cfg.smoother.damping, cfg.coarse_tol, block_top};
+                 cfg.coarse_max_iter, cfg.smoother.damping, cfg.coarse_tol, block_top, calib};
   PF_CUDA(cudaLaunchKernelEx(&lc, k_bottom, static_cast<const BotDesc*>(bot.desc), c, accumulate_top));
   ++*(g_capture_counter ? g_capture_counter : &h->launches);
 }

@@ -32,17 +32,17 @@ constexpr int kChunkGroups = PF_CHUNK_GROUPS;  // groups of 4 entries per chunk 
 #endif
 // colour sweeps are single-wave launches: a row's latency chain, not throughput, bounds them
 constexpr int kSorChunkGroups = PF_SOR_GROUPS;
-// Minimum resident blocks per SM of the row kernels (caps them at 32 registers): a full
-// SM of warps hides the gather latency better than extra registers per thread
-// (measured at C2: sweep 100 -> 92 us; each SOR colour fits one wave: 129 -> 112 us).
+// Minimum resident blocks per SM of the row kernels: 4 x 256 threads leaves 64 registers,
+// enough for the software-pipelined group loop without spills (measured at C2 against 8
+// blocks / 32 registers with spills: sweep 97 -> 87 us, SOR colour sweep 153 -> 109 us).
 #ifndef PF_SOR_MINB
-#define PF_SOR_MINB 8
+#define PF_SOR_MINB 4
 #endif
 #ifndef PF_JAC_MINB
-#define PF_JAC_MINB 8
+#define PF_JAC_MINB 4
 #endif
 #ifndef PF_ROW_MINB
-#define PF_ROW_MINB 8
+#define PF_ROW_MINB 4
 #endif
 
 // SELL-32x4 layout: slice s holds rows 32s..32s+31; entry j of lane l sits at
