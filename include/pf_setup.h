@@ -78,6 +78,15 @@ pf_status pf_setup_load_desc(const pf_setup* s, pf_load_desc* out);
  * !has_dirichlet), evaluated with this library's libm exactly as model.cpp does. */
 pf_status pf_setup_scales(const pf_setup* s, double t, double* source_scale, int32_t* has_dirichlet,
                           double* dirichlet_scale);
+/* MatrixMarket export of the finest level (export_system, app.cpp:379-396, through
+ * export_matrixmarket, matrix_market.cpp:47-112): setups[r] = rank r of one n_ranks
+ * decomposition, all in this process.  Global numbering as assign_global_numbers
+ * (femapper.cpp:353-472): own dofs rank by rank, then each rank's owned Dirichlet dofs.
+ * Writes the same bytes as the reference: "%lld %lld %.17g" coordinate entries of every
+ * owned row, and the rhs b as an array.  (The reference exports its PoissonProblem:
+ * build the setups with PF_PROBLEM_REFERENCE_POISSON for identical files.) */
+pf_status pf_setup_export_matrixmarket(const pf_setup* const* setups, int n_ranks, const char* matrix_path,
+                                       const char* rhs_path, int64_t* n_global, int64_t* nnz);
 /* Seconds spent in pf_setup_create. */
 pf_status pf_setup_seconds(const pf_setup* s, double* out);
 

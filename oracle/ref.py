@@ -74,6 +74,7 @@ def _bind(L):
         L.ref_heat_copy.argtypes = [P, P, P, P]
         L.ref_heat_free.argtypes = [P]
         L.ref_set_heat.argtypes = [C.c_double, C.c_int]
+        L.ref_export.argtypes = [C.c_int] * 4 + [C.c_char_p]
         L.ref_heat_bench.argtypes = [C.c_int] * 4 + [C.c_double, C.c_int, C.c_double, C.c_int, C.c_int,
                                                      C.c_double, C.c_int, C.c_int, P, P, i64p,
                                                      C.POINTER(C.c_int)]
@@ -298,3 +299,10 @@ def heat_bench(dim, n_coarse, levels, K, *, dt=0.01, smoother=0, damping=0.8, pr
         raise RuntimeError(L.ref_last_error().decode())
     return dict(step_seconds=per, setup_seconds=float(setup[0]), n_global=int(ng.value),
                 iterations=int(its.value))
+
+
+def export(dim, n_coarse, levels, K, prefix: str) -> None:
+    """The reference's export_system (app.cpp:379-396): writes prefix.mtx, prefix_rhs.mtx."""
+    L = lib()
+    if L.ref_export(dim, n_coarse, levels, K, prefix.encode()):
+        raise RuntimeError(L.ref_last_error().decode())

@@ -563,6 +563,19 @@ int ref_heat_bench(int dim, int n_coarse, int levels, int K, double dt, int smoo
   return rc;
 }
 
+// The reference's own MatrixMarket export (export_system, app.cpp:379-396): <prefix>.mtx and
+// <prefix>_rhs.mtx of its PoissonProblem on K rank threads.
+int ref_export(int dim, int n_coarse, int levels, int K, const char* prefix) {
+  return guarded([&] {
+    AppConfig cfg;
+    cfg.dimension = dim;
+    cfg.n_coarse = n_coarse;
+    cfg.ranks = K;
+    cfg.levels = levels;
+    export_system(cfg, prefix);
+  });
+}
+
 // The reference's own Crank-Nicolson heat run (run_heat, app.cpp:146-230,
 // :299-305), unmodified: returns a handle to its SolveReport (NULL on failure).
 void* ref_heat(int dim, int n_coarse, int levels, int K, double dt, double end_time, int smoother_kind,

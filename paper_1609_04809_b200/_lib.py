@@ -119,7 +119,7 @@ EXPORTS = [
     "pf_cn_rhs", "pf_heat_run",
     "pf_setup_create", "pf_setup_create_heat", "pf_setup_destroy", "pf_setup_level", "pf_setup_level_keys",
     "pf_setup_rhs", "pf_setup_counts", "pf_setup_seconds", "pf_setup_rhs_operator", "pf_setup_load_at",
-    "pf_setup_load_desc", "pf_setup_scales",
+    "pf_setup_load_desc", "pf_setup_scales", "pf_setup_export_matrixmarket",
 ]
 
 _lib = None
@@ -203,6 +203,7 @@ def lib():
         "pf_setup_load_at": [P, C.c_double, P, C.c_int64],
         "pf_setup_load_desc": [P, C.POINTER(LoadDesc)],
         "pf_setup_scales": [P, C.c_double, dp, C.POINTER(C.c_int32), dp],
+        "pf_setup_export_matrixmarket": [P, C.c_int, C.c_char_p, C.c_char_p, i64p, i64p],
         "pf_setup_destroy": [P],
         "pf_setup_level": [P, C.c_int, C.POINTER(LevelDesc)],
         "pf_setup_level_keys": [P, C.c_int, PP, PP],

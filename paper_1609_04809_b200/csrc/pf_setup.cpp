@@ -20,6 +20,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -1181,6 +1182,98 @@ pf_status pf_setup_scales(const pf_setup* s, double t, double* source_scale, int
     if (source_scale) *source_scale = s->prob.source_scale(t);
     if (has_dirichlet) *has_dirichlet = s->prob.has_dirichlet() ? 1 : 0;
     if (dirichlet_scale) *dirichlet_scale = s->prob.has_dirichlet() ? s->prob.dirichlet_scale(t) : 0.0;
+  });
+}
+
+pf_status pf_setup_export_matrixmarket(const pf_setup* const* setups, int n_ranks, const char* matrix_path,
+                                       const char* rhs_path, int64_t* n_global, int64_t* nnz) {
+  return guard([&] {
+    if (!setups || n_ranks < 1 || !matrix_path || !rhs_path) invalid("null argument");
+    for (int r = 0; r < n_ranks; ++r) {
+      if (!setups[r]) invalid("null setup");
+      if (setups[r]->rank != r || setups[r]->n_ranks != n_ranks)
+        invalid("setups[r] must be rank r of one n_ranks decomposition");
+      if (setups[r]->d != setups[0]->d || setups[r]->n_coarse != setups[0]->n_coarse ||
+          setups[r]->n_levels != setups[0]->n_levels || setups[r]->prob.kind != setups[0]->prob.kind)
+        invalid("setups of different problems");
+    }
+    // assign_global_numbers (femapper.cpp:353-472): own dofs rank by rank in local order,
+    // then the Dirichlet dofs each rank is the authority of (owns_row), rank by rank; every
+    // other local dof takes its carrier's number from the rank that numbered it.
+    const Geo& g0 = setups[0]->levels.back()->geo;
+    const int64_t nv = (g0.N + 1) * (g0.N + 1) * g0.nzv();
+    std::vector<int64_t> gid_of_key(static_cast<size_t>(nv), -1);
+    int64_t next = 0;
+    for (int r = 0; r < n_ranks; ++r) {
+      const SetupLevel& L = *setups[r]->levels.back();
+      for (int32_t i = 0; i < L.n_own; ++i) gid_of_key[static_cast<size_t>(L.vert[i])] = next++;
+    }
+    const int64_t total_own = next;
+    for (int r = 0; r < n_ranks; ++r) {
+      const SetupLevel& L = *setups[r]->levels.back();
+      for (int32_t i = 0; i < L.n; ++i)
+        if (L.owns_row[i] && L.class_of[i] == kDirichlet) gid_of_key[static_cast<size_t>(L.vert[i])] = next++;
+    }
+    const int64_t n = next;
+    (void)total_own;
+    // export_matrixmarket (matrix_market.cpp:47-112): "%lld %lld %.17g" per entry of every
+    // owned row, rank by rank in local order; the rhs as an array, own rows of all ranks
+    // first, then the owned Dirichlet rows.
+    int64_t total_nnz = 0;
+    for (int r = 0; r < n_ranks; ++r) {
+      const SetupLevel& L = *setups[r]->levels.back();
+      for (int32_t i = 0; i < L.n; ++i)
+        if (L.owns_row[i]) total_nnz += L.rowptr[i + 1] - L.rowptr[i];
+    }
+    std::FILE* fm = std::fopen(matrix_path, "wb");
+    if (!fm) throw SetupError(PF_ERR_STATE, std::string("cannot open '") + matrix_path + "' for writing");
+    std::fprintf(fm, "%%%%MatrixMarket matrix coordinate real general\n%lld %lld %lld\n", static_cast<long long>(n),
+                 static_cast<long long>(n), static_cast<long long>(total_nnz));
+    for (int r = 0; r < n_ranks; ++r) {
+      const SetupLevel& L = *setups[r]->levels.back();
+      // rows formatted in parallel blocks, written in order
+      constexpr int32_t kRows = 1 << 14;
+      for (int32_t r0 = 0; r0 < L.n; r0 += kRows * 16) {
+        const int32_t r1 = std::min<int32_t>(L.n, r0 + kRows * 16);
+        const int nb = (r1 - r0 + kRows - 1) / kRows;
+        std::vector<std::string> out(static_cast<size_t>(nb));
+#pragma omp parallel for schedule(dynamic)
+        for (int b = 0; b < nb; ++b) {
+          std::string& o = out[static_cast<size_t>(b)];
+          char buf[128];
+          for (int32_t i = r0 + b * kRows; i < std::min<int32_t>(r1, r0 + (b + 1) * kRows); ++i) {
+            if (!L.owns_row[i]) continue;
+            const long long grow = gid_of_key[static_cast<size_t>(L.vert[i])] + 1;
+            for (int64_t k = L.rowptr[i]; k < L.rowptr[i + 1]; ++k) {
+              const long long gcol = gid_of_key[static_cast<size_t>(L.vert[static_cast<size_t>(L.cols[k])])] + 1;
+              const int len = std::snprintf(buf, sizeof buf, "%lld %lld %.17g\n", grow, gcol, L.vals[static_cast<size_t>(k)]);
+              o.append(buf, static_cast<size_t>(len));
+            }
+          }
+        }
+        for (const std::string& o : out) std::fwrite(o.data(), 1, o.size(), fm);
+      }
+    }
+    const bool ok_m = std::fflush(fm) == 0 && !std::ferror(fm);
+    std::fclose(fm);
+    if (!ok_m) throw SetupError(PF_ERR_STATE, std::string("write failed for '") + matrix_path + "'");
+    std::FILE* fr = std::fopen(rhs_path, "wb");
+    if (!fr) throw SetupError(PF_ERR_STATE, std::string("cannot open '") + rhs_path + "' for writing");
+    std::fprintf(fr, "%%%%MatrixMarket matrix array real general\n%lld 1\n", static_cast<long long>(n));
+    for (int pass = 0; pass < 2; ++pass)
+      for (int r = 0; r < n_ranks; ++r) {
+        const SetupLevel& L = *setups[r]->levels.back();
+        const std::vector<double>& b = setups[r]->b;
+        for (int32_t i = pass == 0 ? 0 : L.n_own; i < (pass == 0 ? L.n_own : L.n); ++i) {
+          if (pass == 1 && !L.owns_row[i]) continue;
+          std::fprintf(fr, "%.17g\n", b[static_cast<size_t>(i)]);
+        }
+      }
+    const bool ok_r = std::fflush(fr) == 0 && !std::ferror(fr);
+    std::fclose(fr);
+    if (!ok_r) throw SetupError(PF_ERR_STATE, std::string("write failed for '") + rhs_path + "'");
+    if (n_global) *n_global = n;
+    if (nnz) *nnz = total_nnz;
   });
 }
 

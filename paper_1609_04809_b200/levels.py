@@ -82,7 +82,7 @@ class StructuredSetup:
     loop: `rhs_op`, `load_at(t)`, `load_desc()`, `scales(t)`."""
 
     def __init__(self, dim: int, n_coarse: int, n_levels: int, n_ranks: int = 1, rank: int = 0,
-                 problem: int = _lib.PF_PROBLEM_BASELINE, dt: float | None = None):
+                 problem: int = _lib.PF_PROBLEM_BASELINE, dt: float | None = None, keep: bool = False):
         L = _lib.lib()
         self._h = C.c_void_p()
         if problem == _lib.PF_PROBLEM_HEAT:
@@ -112,7 +112,7 @@ class StructuredSetup:
             vp, nnz = C.c_void_p(), C.c_int64()
             _lib.check(L.pf_setup_rhs_operator(self._h, C.byref(vp), C.byref(nnz)), setup=True)
             self.rhs_op = _arr(vp, nnz.value, C.c_double, np.float64)
-        else:
+        elif not keep:
             self.close()
 
     def close(self):
@@ -128,7 +128,7 @@ class StructuredSetup:
 
     def _live(self):
         if not self._h:
-            raise _lib.PfError("native setup released (only heat setups keep it)")
+            raise _lib.PfError("native setup released (heat setups, or keep=True, keep it)")
         return self._h
 
     def load_at(self, t: float) -> np.ndarray:
@@ -179,3 +179,14 @@ class StructuredSetup:
             out.p_cols = _arr(d.p_cols, pn, C.c_int32, np.int32)
             out.p_w = _arr(d.p_weights, pn, C.c_double, np.float64)
         return out
+
+
+def export_matrixmarket(setups, matrix_path: str, rhs_path: str):
+    """export_system (app.cpp:379-396): the finest level of all ranks as MatrixMarket files,
+    byte-identical to the reference's.  setups[r] = rank r, built with keep=True.
+    Returns (n_global, nnz)."""
+    arr = (C.c_void_p * len(setups))(*[s._live() for s in setups])
+    ng, nz = C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib().pf_setup_export_matrixmarket(arr, len(setups), matrix_path.encode(),
+                                                       rhs_path.encode(), C.byref(ng), C.byref(nz)), setup=True)
+    return ng.value, nz.value
