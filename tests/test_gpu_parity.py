@@ -247,13 +247,16 @@ def test_multiprocess_path_loopback(cuda, K, L, kind, rep):
         assert rn == pytest.approx(res[0][2], rel=0, abs=0)
 
 
-@pytest.mark.parametrize("bottom_rows", ["0", "65536", "1000000"], ids=["multilaunch", "bottom", "bottom-all"])
+@pytest.mark.parametrize("bottom_rows", ["0", "1024", "65536", "1000000"],
+                         ids=["multilaunch", "bottom", "bottom-64k", "bottom-all"])
 @pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
 def test_bottom_kernel_equals_multilaunch(cuda, monkeypatch, bottom_rows, kind):
     """The cooperative bottom-of-cycle kernel is a launch-structure change only: with it
     disabled, covering the default levels, or covering every level below the finest, the
-    solve must equal the oracle bit for bit (1 and 4 subdomains)."""
+    solve must equal the oracle bit for bit (1 and 4 subdomains).  Jacobi is forced onto
+    it too (by default it runs per-level kernels)."""
     monkeypatch.setenv("PF_BOTTOM_ROWS", bottom_rows)
+    monkeypatch.setenv("PF_BOTTOM_JACOBI", "1")
     c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
     for K in (1, 4):
         setups, levels = structured(3, 2, 5, K)
