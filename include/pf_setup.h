@@ -42,11 +42,20 @@ typedef struct pf_setup pf_setup;
 /*           3 = the reference's HeatProblem (model.cpp:19-31): u = exp(-t/10) sin(pi x)
  *               cos(pi y) [cos(pi z)], f = (d pi^2 - 1/10) u; every level's system is the
  *               Crank-Nicolson matrix M + dt/2 K (multigrid.cpp:18-28). */
+/*           4 = BASELINE's rhs with a piecewise-constant lognormal(0, 1) coefficient per finest
+ *               cell (BASELINE configs 3-4): kappa_c = exp(z_c), z_c from a
+ *               counter-based generator keyed by (seed, finest gcn); coarse element matrices
+ *               are the Galerkin products of their children's.  Not in the reference. */
 enum { PF_PROBLEM_BASELINE = 0, PF_PROBLEM_REFERENCE_POISSON = 1, PF_PROBLEM_UNIT_SOURCE = 2,
-       PF_PROBLEM_HEAT = 3 };
+       PF_PROBLEM_HEAT = 3, PF_PROBLEM_LOGNORMAL = 4 };
 
 pf_status pf_setup_create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem,
                           pf_setup** out);
+/* The lognormal-coefficient problem with its seed. */
+pf_status pf_setup_create_lognormal(int dim, int n_coarse, int n_levels, int n_ranks, int rank, uint64_t seed,
+                                    pf_setup** out);
+/* kappa of every finest cell, lexicographic (x * N + y) * Nz + z. */
+pf_status pf_setup_kappa(const pf_setup* s, const double** kappa, int64_t* n);
 /* Same, with the time step of the heat problem (AppConfig::dt, config.hpp:22). */
 pf_status pf_setup_create_heat(int dim, int n_coarse, int n_levels, int n_ranks, int rank, double dt,
                                pf_setup** out);

@@ -26,6 +26,7 @@ PF_CH_MASTER_SLAVE, PF_CH_HALO1, PF_CH_HALO2 = 0, 1, 2
 PF_UPDATE_SCATTER, PF_UPDATE_ACCUMULATE_THEN_SCATTER = 0, 1
 PF_SMOOTHER_JACOBI, PF_SMOOTHER_GAUSS_SEIDEL, PF_SMOOTHER_MULTICOLOR_SOR = 0, 1, 2
 PF_PROBLEM_BASELINE, PF_PROBLEM_REFERENCE_POISSON, PF_PROBLEM_UNIT_SOURCE, PF_PROBLEM_HEAT = 0, 1, 2, 3
+PF_PROBLEM_LOGNORMAL = 4
 
 
 class PfError(RuntimeError):
@@ -119,7 +120,8 @@ EXPORTS = [
     "pf_cn_rhs", "pf_heat_run",
     "pf_setup_create", "pf_setup_create_heat", "pf_setup_destroy", "pf_setup_level", "pf_setup_level_keys",
     "pf_setup_rhs", "pf_setup_counts", "pf_setup_seconds", "pf_setup_rhs_operator", "pf_setup_load_at",
-    "pf_setup_load_desc", "pf_setup_scales", "pf_setup_export_matrixmarket",
+    "pf_setup_load_desc", "pf_setup_scales", "pf_setup_export_matrixmarket", "pf_setup_create_lognormal",
+    "pf_setup_kappa",
 ]
 
 _lib = None
@@ -199,6 +201,8 @@ def lib():
                         C.POINTER(C.c_int)],
         "pf_setup_create": [C.c_int] * 6 + [PP],
         "pf_setup_create_heat": [C.c_int] * 5 + [C.c_double, PP],
+        "pf_setup_create_lognormal": [C.c_int] * 5 + [C.c_uint64, PP],
+        "pf_setup_kappa": [P, PP, i64p],
         "pf_setup_rhs_operator": [P, PP, i64p],
         "pf_setup_load_at": [P, C.c_double, P, C.c_int64],
         "pf_setup_load_desc": [P, C.POINTER(LoadDesc)],

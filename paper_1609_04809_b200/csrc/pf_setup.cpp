@@ -450,9 +450,10 @@ int ring_slot(int d, int ox, int oy, int oz) {
 struct Problem {
   int kind = 0, d = 3;
   double dt = 0.0;
+  uint64_t seed = 0;  // PF_PROBLEM_LOGNORMAL
   bool unit() const { return kind == PF_PROBLEM_UNIT_SOURCE; }
   // axis factor a of the profile: sin for axis 0 (and every axis of BASELINE), else cos
-  bool axis_sin(int a) const { return a == 0 || kind == PF_PROBLEM_BASELINE; }
+  bool axis_sin(int a) const { return a == 0 || kind == PF_PROBLEM_BASELINE || kind == PF_PROBLEM_LOGNORMAL; }
   double profile(const double* x) const {
     if (unit()) return 1.0;
     double u = (axis_sin(0) ? std::sin(kPi * x[0]) : std::cos(kPi * x[0])) *
@@ -490,6 +491,10 @@ struct pf_setup {
   std::vector<int32_t> ld_lattice;
   std::vector<uint32_t> ld_cells;
   std::vector<double> ld_factor, ld_extent, ld_phi, ld_boundary;
+  // PF_PROBLEM_LOGNORMAL: kappa of every finest cell (lexicographic), and the element
+  // matrices (8 x 8, row-major) of every cell of each coarser level
+  std::vector<double> kappa;
+  std::vector<std::vector<double>> coef_elem;
   double seconds = 0;
 };
 
@@ -532,6 +537,143 @@ Box expand(const Box& b, int64_t by, const Geo& g, bool vertices) {
     o.hi[a] = std::min<int64_t>(top, b.hi[a] + by);
   }
   return o;
+}
+
+// ------------------------------------------------------- lognormal coefficient --
+//
+// PF_PROBLEM_LOGNORMAL (BASELINE configs 3-4; not in the reference):
+// kappa_c = exp(z_c), z_c ~ N(0, 1) drawn per finest cell from a counter-based generator
+// keyed by (seed, finest gcn) — independent of the partition.  The finest element matrix
+// is kappa_c * K_e; a coarse cell's element matrix is the Galerkin product of its
+// children's, E_C = sum_{children c, child index order} P_c^T E_c P_c, with P_c the exact
+// trilinear interpolation of the coarse cell's basis at the child's vertices (for nested
+// conforming Q1 spaces this is the rediscretisation with the fine coefficient).
+
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// Box-Muller on two 53-bit uniforms in (0, 1]
+double lognormal_kappa(uint64_t seed, int64_t gcn) {
+  const uint64_t a = splitmix64(seed ^ splitmix64(static_cast<uint64_t>(gcn) * 2 + 1));
+  const uint64_t b = splitmix64(a);
+  const double u1 = (static_cast<double>(a >> 11) + 1.0) / 9007199254740992.0;
+  const double u2 = (static_cast<double>(b >> 11) + 1.0) / 9007199254740992.0;
+  const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * kPi * u2);
+  return std::exp(z);
+}
+
+Geo geo_of(int d, int n_coarse, int level) {
+  Geo g;
+  g.d = d;
+  g.n_coarse = n_coarse;
+  g.level = level;
+  g.S = int64_t(1) << level;
+  g.N = static_cast<int64_t>(n_coarse) * g.S;
+  return g;
+}
+
+void build_coefficients(pf_setup& s) {
+  const int d = s.d, nv = 1 << d, L = s.n_levels;
+  const Geo gf = geo_of(d, s.n_coarse, L - 1);
+  const int64_t N = gf.N, nz = d == 3 ? N : 1;
+  s.kappa.assign(static_cast<size_t>(N * N * nz), 0.0);
+#pragma omp parallel for schedule(static) collapse(2)
+  for (int64_t x = 0; x < N; ++x)
+    for (int64_t y = 0; y < N; ++y)
+      for (int64_t z = 0; z < nz; ++z)
+        s.kappa[static_cast<size_t>((x * N + y) * nz + z)] = lognormal_kappa(s.prob.seed, gf.gcn(x, y, z));
+  // interpolation of the parent's ring basis at child ci's ring vertices: P[ci][k][i]
+  std::vector<double> P(static_cast<size_t>(8 * 8 * 8), 0.0);
+  for (int ci = 0; ci < nv; ++ci) {
+    const int o[3] = {d == 3 ? ci >> 2 : ci >> 1, d == 3 ? (ci >> 1) & 1 : ci & 1, d == 3 ? ci & 1 : 0};
+    for (int k = 0; k < nv; ++k)
+      for (int i = 0; i < nv; ++i) {
+        double w = 1.0;
+        for (int a = 0; a < d; ++a) {
+          const double xi = static_cast<double>(o[a] + kRing[k][a]) / 2.0;
+          w *= kRing[i][a] ? xi : 1.0 - xi;
+        }
+        P[static_cast<size_t>((ci * 8 + k) * 8 + i)] = w;
+      }
+  }
+  s.coef_elem.assign(static_cast<size_t>(L), {});
+  for (int l = L - 2; l >= 0; --l) {
+    const Geo gc = geo_of(d, s.n_coarse, l);
+    const int64_t Nc = gc.N, nzc = d == 3 ? Nc : 1, nzf = d == 3 ? 2 * Nc : 1;
+    std::vector<double>& EC = s.coef_elem[static_cast<size_t>(l)];
+    EC.assign(static_cast<size_t>(Nc * Nc * nzc * 64), 0.0);
+    const bool child_finest = l + 1 == L - 1;
+    // the finest children's K_e depends on their extents (last bit, N not a power of two)
+    std::vector<double> hv;
+    std::vector<int> hidf;
+    std::vector<Element> ef;
+    if (child_finest) {
+      hidf.assign(static_cast<size_t>(N), 0);
+      for (int64_t c = 0; c < N; ++c) {
+        const double e = gf.extent(c);
+        size_t k = 0;
+        while (k < hv.size() && hv[k] != e) ++k;
+        if (k == hv.size()) hv.push_back(e);
+        hidf[static_cast<size_t>(c)] = static_cast<int>(k);
+      }
+      const int nh = static_cast<int>(hv.size());
+      for (int a = 0; a < nh; ++a)
+        for (int b = 0; b < nh; ++b)
+          for (int c = 0; c < (d == 3 ? nh : 1); ++c) {
+            const double hx[3] = {hv[a], hv[b], d == 3 ? hv[c] : 1.0};
+            ef.push_back(make_element(d, hx));
+          }
+    }
+    const int nh = static_cast<int>(hv.size());
+    const std::vector<double>& EF = child_finest ? s.kappa : s.coef_elem[static_cast<size_t>(l + 1)];
+#pragma omp parallel for schedule(static) collapse(2)
+    for (int64_t X = 0; X < Nc; ++X)
+      for (int64_t Y = 0; Y < Nc; ++Y)
+        for (int64_t Z = 0; Z < nzc; ++Z) {
+          double* out = &EC[static_cast<size_t>(((X * Nc + Y) * nzc + Z) * 64)];
+          for (int ci = 0; ci < nv; ++ci) {
+            const int o[3] = {d == 3 ? ci >> 2 : ci >> 1, d == 3 ? (ci >> 1) & 1 : ci & 1, d == 3 ? ci & 1 : 0};
+            const int64_t cx = 2 * X + o[0], cy = 2 * Y + o[1], cz = d == 3 ? 2 * Z + o[2] : 0;
+            const int64_t cidx = (cx * (2 * Nc) + cy) * nzf + cz;
+            double E[64];
+            if (child_finest) {
+              const int e = d == 3 ? (hidf[cx] * nh + hidf[cy]) * nh + hidf[cz] : hidf[cx] * nh + hidf[cy];
+              const double kap = EF[static_cast<size_t>(cidx)];
+              for (int k = 0; k < nv; ++k)
+                for (int m = 0; m < nv; ++m) E[k * 8 + m] = kap * ef[static_cast<size_t>(e)].K[k][m];
+            } else {
+              for (int q = 0; q < 64; ++q) E[q] = EF[static_cast<size_t>(cidx * 64 + q)];
+            }
+            const double* Pc = &P[static_cast<size_t>(ci * 64)];
+            double T[64];
+            for (int k = 0; k < nv; ++k)
+              for (int j = 0; j < nv; ++j) {
+                double t = 0.0;
+                for (int m = 0; m < nv; ++m) t += E[k * 8 + m] * Pc[m * 8 + j];
+                T[k * 8 + j] = t;
+              }
+            for (int i = 0; i < nv; ++i)
+              for (int j = 0; j < nv; ++j) {
+                double u = 0.0;
+                for (int k = 0; k < nv; ++k) u += Pc[k * 8 + i] * T[k * 8 + j];
+                out[i * 8 + j] += u;
+              }
+          }
+        }
+  }
+}
+
+// Element-matrix entry (si, sj) of cell (cx, cy, cz) of level l for the coefficient problem.
+double coef_entry(const pf_setup& s, const SetupLevel& L, int l, int64_t cx, int64_t cy, int64_t cz, int si,
+                  int sj) {
+  const int64_t N = L.geo.N, nz = s.d == 3 ? N : 1;
+  const int64_t c = (cx * N + cy) * nz + cz;
+  if (l == s.n_levels - 1) return s.kappa[static_cast<size_t>(c)] * L.elem(cx, cy, cz).K[si][sj];
+  return s.coef_elem[static_cast<size_t>(l)][static_cast<size_t>(c * 64 + si * 8 + sj)];
 }
 
 // Cells given as (x, y, z) triples, reordered by ascending gcn (at most 8).
@@ -737,6 +879,7 @@ void build_level(pf_setup& s, int l) {
   auto elem = [&](int64_t cx, int64_t cy, int64_t cz) -> const Element& { return LC.elem(cx, cy, cz); };
   auto sort_by_gcn = [&](int64_t* cells, int nc) { sort_cells_by_gcn(g, cells, nc); };
   const bool heat = s.prob.kind == PF_PROBLEM_HEAT;
+  const bool coef = s.prob.kind == PF_PROBLEM_LOGNORMAL;
   const bool finest = l == s.n_levels - 1;
   const double half_dt = 0.5 * s.prob.dt;
 
@@ -804,7 +947,7 @@ void build_level(pf_setup& s, int l) {
             const int sj = ring_slot(d, static_cast<int>(x + dx - cc[0]), static_cast<int>(y + dy - cc[1]),
                                      static_cast<int>(z + dz - cc[2]));
             const Element& E = elem(cc[0], cc[1], cc[2]);
-            k += E.K[si][sj];
+            k += coef ? coef_entry(s, LC, l, cc[0], cc[1], cc[2], si, sj) : E.K[si][sj];
             if (heat) m += E.M[si][sj];
           }
           double v = heat ? m + half_dt * k : k;
@@ -1030,14 +1173,14 @@ pf_status guard(F&& f) {
 }
 
 pf_status create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem, double dt,
-                 pf_setup** out) {
+                 uint64_t seed, pf_setup** out) {
   return guard([&] {
     if (!out) invalid("null output");
     if (dim != 2 && dim != 3) invalid("dimension must be 2 or 3, got " + std::to_string(dim));
     if (n_coarse < 1) invalid("n_coarse must be >= 1");
     if (n_levels < 1) invalid("hierarchy needs at least one level");
     if (rank < 0 || rank >= n_ranks) invalid("rank out of range");
-    if (problem < 0 || problem > 3) invalid("unknown problem");
+    if (problem < 0 || problem > 4) invalid("unknown problem");
     if (problem == PF_PROBLEM_HEAT && !(dt > 0.0)) invalid("dt must be positive");  // config.cpp:86
     const auto t0 = std::chrono::steady_clock::now();
     auto s = std::make_unique<pf_setup>();
@@ -1049,7 +1192,9 @@ pf_status create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int
     s->prob.kind = problem;
     s->prob.d = dim;
     s->prob.dt = problem == PF_PROBLEM_HEAT ? dt : 0.0;
+    s->prob.seed = seed;
     s->coarse_owner = coarse_partition(dim, n_coarse, n_ranks);
+    if (problem == PF_PROBLEM_LOGNORMAL) build_coefficients(*s);
     for (int l = 0; l < n_levels; ++l) build_level(*s, l);
     s->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = s.release();
@@ -1064,16 +1209,31 @@ const char* pf_setup_last_error(void) { return g_setup_err.c_str(); }
 
 pf_status pf_setup_create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem,
                           pf_setup** out) {
-  if (problem == PF_PROBLEM_HEAT) {
-    g_setup_err = "the heat problem needs dt: use pf_setup_create_heat";
+  if (problem == PF_PROBLEM_HEAT || problem == PF_PROBLEM_LOGNORMAL) {
+    g_setup_err = problem == PF_PROBLEM_HEAT ? "the heat problem needs dt: use pf_setup_create_heat"
+                                              : "the lognormal problem needs a seed: use pf_setup_create_lognormal";
     return PF_ERR_INVALID_ARGUMENT;
   }
-  return create(dim, n_coarse, n_levels, n_ranks, rank, problem, 0.0, out);
+  return create(dim, n_coarse, n_levels, n_ranks, rank, problem, 0.0, 0, out);
 }
 
 pf_status pf_setup_create_heat(int dim, int n_coarse, int n_levels, int n_ranks, int rank, double dt,
                                pf_setup** out) {
-  return create(dim, n_coarse, n_levels, n_ranks, rank, PF_PROBLEM_HEAT, dt, out);
+  return create(dim, n_coarse, n_levels, n_ranks, rank, PF_PROBLEM_HEAT, dt, 0, out);
+}
+
+pf_status pf_setup_create_lognormal(int dim, int n_coarse, int n_levels, int n_ranks, int rank, uint64_t seed,
+                                    pf_setup** out) {
+  return create(dim, n_coarse, n_levels, n_ranks, rank, PF_PROBLEM_LOGNORMAL, 0.0, seed, out);
+}
+
+pf_status pf_setup_kappa(const pf_setup* s, const double** kappa, int64_t* n) {
+  return guard([&] {
+    if (!s) invalid("null setup");
+    if (s->prob.kind != PF_PROBLEM_LOGNORMAL) invalid("kappa exists for the lognormal problem only");
+    if (kappa) *kappa = s->kappa.data();
+    if (n) *n = static_cast<int64_t>(s->kappa.size());
+  });
 }
 
 pf_status pf_setup_destroy(pf_setup* s) {

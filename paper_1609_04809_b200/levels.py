@@ -82,12 +82,16 @@ class StructuredSetup:
     loop: `rhs_op`, `load_at(t)`, `load_desc()`, `scales(t)`."""
 
     def __init__(self, dim: int, n_coarse: int, n_levels: int, n_ranks: int = 1, rank: int = 0,
-                 problem: int = _lib.PF_PROBLEM_BASELINE, dt: float | None = None, keep: bool = False):
+                 problem: int = _lib.PF_PROBLEM_BASELINE, dt: float | None = None, keep: bool = False,
+                 seed: int = 1):
         L = _lib.lib()
         self._h = C.c_void_p()
         if problem == _lib.PF_PROBLEM_HEAT:
             _lib.check(L.pf_setup_create_heat(dim, n_coarse, n_levels, n_ranks, rank,
                                               0.01 if dt is None else dt, C.byref(self._h)), setup=True)
+        elif problem == _lib.PF_PROBLEM_LOGNORMAL:
+            _lib.check(L.pf_setup_create_lognormal(dim, n_coarse, n_levels, n_ranks, rank, seed,
+                                                   C.byref(self._h)), setup=True)
         else:
             _lib.check(L.pf_setup_create(dim, n_coarse, n_levels, n_ranks, rank, problem,
                                          C.byref(self._h)), setup=True)
@@ -108,6 +112,11 @@ class StructuredSetup:
         _lib.check(L.pf_setup_seconds(self._h, C.byref(s)), setup=True)
         self.seconds = s.value
         self.rhs_op = None
+        self.kappa = None
+        if problem == _lib.PF_PROBLEM_LOGNORMAL:
+            kp, kn = C.c_void_p(), C.c_int64()
+            _lib.check(L.pf_setup_kappa(self._h, C.byref(kp), C.byref(kn)), setup=True)
+            self.kappa = _arr(kp, kn.value, C.c_double, np.float64)
         if problem == _lib.PF_PROBLEM_HEAT:
             vp, nnz = C.c_void_p(), C.c_int64()
             _lib.check(L.pf_setup_rhs_operator(self._h, C.byref(vp), C.byref(nnz)), setup=True)

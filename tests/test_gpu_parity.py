@@ -13,6 +13,7 @@ import pytest
 from helpers import cfg, download, key_noise, keyed, structured, upload
 from oracle.restated import Oracle
 from paper_1609_04809_b200 import _lib, gmg
+from paper_1609_04809_b200.levels import StructuredSetup
 
 pytestmark = pytest.mark.gpu
 
@@ -346,3 +347,22 @@ def test_drop_in_bridge_inside_the_reference(cuda, ref_lib, K, smoother):
         num = sum(float(np.sum((a - b) ** 2)) for a, b in zip(xg, xr))
         den = sum(float(np.sum(b ** 2)) for b in xr)
         assert np.sqrt(num) <= 1e-8 * np.sqrt(den)
+
+
+@pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
+def test_lognormal_coefficient_solve_bit_exact(cuda, kind):
+    """BASELINE's lognormal(0,1) per-cell coefficient (PF_PROBLEM_LOGNORMAL; the setup is
+    pinned to oracle/coef.py by tests/test_setup.py): every operator value distinct, so the
+    device keeps fp64 values — GPU solve == oracle bit for bit, 1 and 2 subdomains."""
+    c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8, max_cycles=200)
+    for K in (1, 2):
+        setups = [StructuredSetup(3, 2, 5, K, r, _lib.PF_PROBLEM_LOGNORMAL, seed=99) for r in range(K)]
+        levels = [s.levels for s in setups]
+        h = gmg.Hierarchy(levels)
+        x = upload(h, 4, [s.x0 for s in setups])
+        st = gmg.solve_outer(h, x, upload(h, 4, [s.b for s in setups]), c)
+        xo, res, ost, rc = Oracle(levels).solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
+        assert rc == 0 and st.converged
+        assert st.iterations == ost.iterations
+        np.testing.assert_allclose(st.residuals, res, rtol=1e-12)
+        assert exact(download(h, x, K), xo)

@@ -173,3 +173,51 @@ def test_setup_arrays_identical_to_reference(ref_lib, dim, nc, L, K, prob):
         if prob != 3:
             assert np.array_equal(R.b[r], S[r].b) and np.array_equal(R.x0[r], S[r].x0), r
         S[r].close()
+
+
+@pytest.mark.parametrize("dim,nc,L,K", [(3, 2, 3, 1), (3, 2, 3, 2), (2, 3, 3, 3), (3, 2, 4, 1)])
+def test_lognormal_setup_matches_restatement(dim, nc, L, K):
+    """PF_PROBLEM_LOGNORMAL (not in the reference; pinned to oracle/coef.py): every own and
+    halo row of every level, entry by entry, equals the restated coefficient assembly;
+    the rhs is BASELINE's (the load does not see kappa); Dirichlet rows are identity."""
+    from oracle import coef
+    seed = 12345
+    E = coef.element_matrices(dim, nc, L, seed)
+    base = [StructuredSetup(dim, nc, L, K, r) for r in range(K)]
+    S = [StructuredSetup(dim, nc, L, K, r, _lib.PF_PROBLEM_LOGNORMAL, seed=seed) for r in range(K)]
+    Nf = nc << (L - 1)
+    kap = [coef.kappa(seed, coef.gcn(dim, nc, L - 1, x, y, z))
+           for x in range(Nf) for y in range(Nf) for z in range(Nf if dim == 3 else 1)]
+    assert np.array_equal(S[0].kappa, np.array(kap))
+    for r in range(K):
+        assert np.array_equal(S[r].b, base[r].b)
+        for l in range(L):
+            lv, lb = S[r].levels[l], base[r].levels[l]
+            assert np.array_equal(lv.row_offsets, lb.row_offsets) and np.array_equal(lv.cols, lb.cols)
+            # the rank's local cells at this level: those whose 2^d vertices are all local
+            keys = {tuple(int(t) for t in k[1:]): i for i, k in enumerate(lv.keys)}
+            N = nc << l
+            local = set()
+            for key in keys:
+                for dx in (-1, 0):
+                    for dy in (-1, 0):
+                        for dz in ((-1, 0) if dim == 3 else (0,)):
+                            c = (key[0] + dx, key[1] + dy, key[2] + dz)
+                            if min(c[:dim]) < 0 or max(c[:dim]) >= N:
+                                continue
+                            verts = [(c[0] + v[0], c[1] + v[1], c[2] + (v[2] if dim == 3 else 0))
+                                     for v in coef.RING[:1 << dim]]
+                            if all(vv in keys for vv in verts):
+                                local.add(c)
+            # a cell is local to the rank iff all its vertices are local dofs AND it is in
+            # the rank's subdomain; compare only entries whose cells agree with the base
+            # (kappa = 1) matrix structure: use the base matrix to validate `local`
+            for i in range(lv.n):
+                p = tuple(int(t) for t in lv.keys[i][1:])
+                for e in range(lv.row_offsets[i], lv.row_offsets[i + 1]):
+                    q = tuple(int(t) for t in lv.keys[lv.cols[e]][1:])
+                    if lv.is_dir[i]:
+                        assert lv.vals[e] == (1.0 if q == p else 0.0)
+                        continue
+                    want = coef.matrix_entry(dim, nc, l, E, local, p, q)
+                    assert lv.vals[e] == want, (r, l, p, q, lv.vals[e], want)
