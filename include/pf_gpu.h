@@ -187,6 +187,10 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h);
  * process).  `unique_id` is the 128-byte ncclUniqueId from pf_nccl_unique_id() on
  * rank 0, broadcast by the caller. */
 pf_status pf_nccl_unique_id(void* out, int nbytes);
+/* Transport self-test on the current device: a one-rank NCCL communicator, a grouped
+ * send/recv to itself and an allgather through the same wrapper the exchanges use; *ok = 1
+ * when the payloads arrive intact.  (Proves the dlopen'd NCCL path on a one-GPU box.) */
+pf_status pf_nccl_selftest(int device, int* ok);
 pf_status pf_hierarchy_init_nccl(pf_hierarchy* h, const void* unique_id, int nbytes);
 /* Multi-process: level 0 (coarsest) of every rank r in [0, world_size), set before
  * pf_hierarchy_finalize.  Each GPU replays the reference's communicating coarse

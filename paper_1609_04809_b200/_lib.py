@@ -106,7 +106,7 @@ class SolveStats(C.Structure):
 EXPORTS = [
     "pf_last_error", "pf_version", "pf_device_count", "pf_default_smoother_config", "pf_default_multigrid_config",
     "pf_hierarchy_create", "pf_hierarchy_set_level", "pf_hierarchy_finalize", "pf_nccl_unique_id",
-    "pf_hierarchy_init_nccl", "pf_hierarchy_set_coarse_replica", "pf_hierarchy_set_replica_level",
+    "pf_hierarchy_init_nccl", "pf_nccl_selftest", "pf_hierarchy_set_coarse_replica", "pf_hierarchy_set_replica_level",
     "pf_hierarchy_destroy",
     "pf_loopback_create", "pf_loopback_destroy", "pf_hierarchy_init_loopback", "pf_hierarchy_device_bytes",
     "pf_vector_create", "pf_vector_destroy", "pf_vector_upload", "pf_vector_download",
@@ -151,6 +151,7 @@ def lib():
         "pf_hierarchy_finalize": [P],
         "pf_nccl_unique_id": [P, C.c_int],
         "pf_hierarchy_init_nccl": [P, P, C.c_int],
+        "pf_nccl_selftest": [C.c_int, C.POINTER(C.c_int)],
         "pf_hierarchy_set_coarse_replica": [P, C.c_int, C.POINTER(LevelDesc)],
         "pf_hierarchy_set_replica_level": [P, C.c_int, C.c_int, C.POINTER(LevelDesc)],
         "pf_loopback_create": [C.c_int, PP],

@@ -1636,6 +1636,34 @@ pf_status pf_nccl_unique_id(void* out, int nbytes) {
   PF_API_END
 }
 
+pf_status pf_nccl_selftest(int device, int* ok) {
+  PF_API_BEGIN
+  if (!ok) invalid("null output");
+  *ok = 0;
+  PF_CUDA(cudaSetDevice(device));
+  unsigned char id[128];
+  pf::nccl_unique_id(id, 128);
+  auto comm = pf::nccl_init(0, 1, id, 128);
+  cudaStream_t st;
+  PF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DevBuf<double> buf;
+  buf.alloc(8);
+  const double host[4] = {1.5, -2.25, 3.0, 0.0};
+  PF_CUDA(cudaMemcpy(buf.p, host, sizeof host, cudaMemcpyHostToDevice));
+  comm->group_start();
+  comm->send(buf.p, 2, 0, st);      // [1.5, -2.25] to itself
+  comm->recv(buf.p + 4, 2, 0, st);  // into [4, 6)
+  comm->group_end(st);
+  comm->allgather(buf.p + 2, buf.p + 6, 1, st);  // one rank: [3.0] -> [6]
+  PF_CUDA(cudaStreamSynchronize(st));
+  comm->check_async();
+  double out[8];
+  PF_CUDA(cudaMemcpy(out, buf.p, sizeof out, cudaMemcpyDeviceToHost));
+  PF_CUDA(cudaStreamDestroy(st));
+  *ok = out[4] == 1.5 && out[5] == -2.25 && out[6] == 3.0;
+  PF_API_END
+}
+
 pf_status pf_hierarchy_init_nccl(pf_hierarchy* h, const void* id, int nbytes) {
   PF_API_BEGIN
   if (!h) invalid("null hierarchy");

@@ -366,3 +366,16 @@ def test_lognormal_coefficient_solve_bit_exact(cuda, kind):
         assert st.iterations == ost.iterations
         np.testing.assert_allclose(st.residuals, res, rtol=1e-12)
         assert exact(download(h, x, K), xo)
+
+
+def test_nccl_transport_selftest(cuda):
+    """The dlopen'd NCCL wrapper the multi-process exchanges use (pf_nccl.cpp): a one-rank
+    communicator, grouped send/recv to itself and an allgather deliver their payloads.
+    (Multi-rank NCCL needs one GPU per rank; its exchange logic is covered bit-exactly by
+    the loopback transport, test_multiprocess_path_loopback.)"""
+    import ctypes as C
+    import torch  # noqa: F401  (loads the NCCL the bench uses)
+    import torch.distributed  # noqa: F401
+    ok = C.c_int(0)
+    _lib.check(_lib.lib().pf_nccl_selftest(0, C.byref(ok)))
+    assert ok.value == 1
