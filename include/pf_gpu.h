@@ -288,6 +288,38 @@ pf_status pf_solve_outer_host(pf_hierarchy* h, double* const* x_host, const doub
                               const pf_multigrid_config* cfg, pf_solve_stats* stats,
                               double* residuals, int max_residuals);
 
+/* ----------------------------------------------------------- device assembly -- */
+/* The finest level's Q1 stiffness system assembled on the device (assemble_system +
+ * apply_dirichlet_rows, assembly.cpp:103-142, :162-170): each
+ * stored entry (p, q) sums, over the rank's local cells containing both vertices in
+ * ascending global cell number, kappa_c * K_e(c)[slot p][slot q]; Dirichlet rows become
+ * identity.  Same products and order as the host assembly, so the values are identical. */
+typedef struct {
+  int32_t dim;
+  int32_t n_cells;             /* N: cells per axis */
+  int32_t n_dofs;
+  int32_t n_coarse;            /* for the global cell number (gcn) */
+  int32_t level;               /* refinement level of this grid (N = n_coarse 2^level) */
+  const int32_t* lattice;      /* [3 * n_dofs] */
+  const uint8_t* cell_mask;    /* [n_dofs] bit k: cell with low corner = vertex along axis a
+                                * iff bit a of k, is local to the rank */
+  const uint8_t* is_dirichlet; /* [n_dofs] */
+  const double* kappa;         /* [N^d] per cell, lexicographic, or NULL (kappa = 1) */
+  const double* elem;          /* [n_classes^d][8][8] element stiffness per extent class */
+  const int32_t* elem_class;   /* [3][N] extent class of each cell index along each axis */
+  int32_t n_classes;
+} pf_assembly_desc;
+
+typedef struct pf_operator pf_operator;
+typedef struct pf_assembly pf_assembly;
+pf_status pf_assembly_create(pf_hierarchy* h, int level, pf_assembly** out);
+pf_status pf_assembly_set(pf_assembly* a, int subdomain, const pf_assembly_desc* desc);
+/* Assemble into `op` (a value set on the level's pattern, pf_operator_create). */
+pf_status pf_assemble_operator(pf_assembly* a, pf_operator* op);
+pf_status pf_assembly_destroy(pf_assembly* a);
+/* An operator's values of one subdomain, in the CSR entry order of its level desc. */
+pf_status pf_operator_get_values(const pf_operator* op, int subdomain, double* values, int64_t nnz);
+
 /* ----------------------------------------------------- heat (Crank-Nicolson) -- */
 /* The reference's heat run (heat_rank_body, app.cpp:146-230) on the
  * device.  Per time step t_{k+1}:

@@ -83,6 +83,8 @@ pf_status pf_setup_load_at(const pf_setup* s, double t, double* out, int64_t n);
 /* The device description of the same load (pf_load_set).  Pointers stay valid until
  * pf_setup_destroy. */
 pf_status pf_setup_load_desc(const pf_setup* s, pf_load_desc* out);
+/* The device assembly description of the finest level (pf_assembly_set). */
+pf_status pf_setup_assembly_desc(pf_setup* s, pf_assembly_desc* out);
 /* f(t) = source_scale * profile, g(t) = dirichlet_scale * profile (or 0 when
  * !has_dirichlet), evaluated with this library's libm exactly as model.cpp does. */
 pf_status pf_setup_scales(const pf_setup* s, double t, double* source_scale, int32_t* has_dirichlet,

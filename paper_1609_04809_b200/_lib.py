@@ -84,6 +84,13 @@ class LoadDesc(C.Structure):
                 ("boundary", C.c_void_p), ("is_dirichlet", C.c_void_p)]
 
 
+class AssemblyDesc(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("n_cells", C.c_int32), ("n_dofs", C.c_int32), ("n_coarse", C.c_int32),
+                ("level", C.c_int32), ("lattice", C.c_void_p), ("cell_mask", C.c_void_p),
+                ("is_dirichlet", C.c_void_p), ("kappa", C.c_void_p), ("elem", C.c_void_p),
+                ("elem_class", C.c_void_p), ("n_classes", C.c_int32)]
+
+
 class SmootherConfig(C.Structure):
     _fields_ = [("kind", C.c_int32), ("sweeps", C.c_int32), ("local_sweeps", C.c_int32),
                 ("damping", C.c_double)]
@@ -117,11 +124,12 @@ EXPORTS = [
     "pf_time_vcycle", "pf_hierarchy_stream", "pf_level_info",
     "pf_operator_create", "pf_operator_set_values", "pf_operator_apply", "pf_operator_destroy",
     "pf_load_create", "pf_load_set", "pf_load_assemble", "pf_load_apply_dirichlet", "pf_load_destroy",
-    "pf_cn_rhs", "pf_heat_run",
+    "pf_cn_rhs", "pf_heat_run", "pf_assembly_create", "pf_assembly_set", "pf_assemble_operator",
+    "pf_assembly_destroy", "pf_operator_get_values",
     "pf_setup_create", "pf_setup_create_heat", "pf_setup_destroy", "pf_setup_level", "pf_setup_level_keys",
     "pf_setup_rhs", "pf_setup_counts", "pf_setup_seconds", "pf_setup_rhs_operator", "pf_setup_load_at",
     "pf_setup_load_desc", "pf_setup_scales", "pf_setup_export_matrixmarket", "pf_setup_create_lognormal",
-    "pf_setup_kappa",
+    "pf_setup_kappa", "pf_setup_assembly_desc",
 ]
 
 _lib = None
@@ -197,6 +205,12 @@ def lib():
         "pf_load_apply_dirichlet": [P, C.c_int, C.c_double, P, P],
         "pf_load_destroy": [P],
         "pf_cn_rhs": [P, P, P, P, P, C.c_double, C.c_int, C.c_double, P, P],
+        "pf_assembly_create": [P, C.c_int, PP],
+        "pf_assembly_set": [P, C.c_int, C.POINTER(AssemblyDesc)],
+        "pf_assemble_operator": [P, P],
+        "pf_assembly_destroy": [P],
+        "pf_operator_get_values": [P, C.c_int, P, C.c_int64],
+        "pf_setup_assembly_desc": [P, C.POINTER(AssemblyDesc)],
         "pf_heat_run": [P, P, P, P, P, C.c_int, C.c_int, C.c_double, dp, C.c_int, dp,
                         C.POINTER(MultigridConfig), C.POINTER(SolveStats), dp, C.c_int,
                         C.POINTER(C.c_int)],

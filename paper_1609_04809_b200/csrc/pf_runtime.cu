@@ -24,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "pf_assembly.cuh"
 #include "pf_bottom.cuh"
 #include "pf_heat.cuh"
 #include "pf_kernels.cuh"
@@ -1431,6 +1432,21 @@ struct pf_operator {
   std::vector<bool> set;
 };
 
+// Device assembly description per subdomain (pf_assembly_create / pf_assembly_set).
+struct pf_assembly {
+  pf_hierarchy* h = nullptr;
+  int level = 0;
+  struct Sub {
+    bool set = false;
+    int dim = 3;
+    int32_t N = 0, nh = 0, n_coarse = 0, grid_level = 0;
+    pf::DevBuf<int32_t> lattice, cls;
+    pf::DevBuf<uint8_t> cell_mask;
+    pf::DevBuf<double> kappa, elem;
+  };
+  std::vector<Sub> sub;
+};
+
 // The finest-level load description on the device (pf_load_create / pf_load_set).
 struct pf_load {
   pf_hierarchy* h = nullptr;
@@ -2220,6 +2236,130 @@ pf_status pf_operator_apply(pf_operator* op, const pf_vector* x, pf_vector* y) {
     });
   }
   sync(h);
+  PF_API_END
+}
+
+pf_status pf_operator_get_values(const pf_operator* op, int sub, double* values, int64_t nnz) {
+  PF_API_BEGIN
+  if (!op || !values) invalid("null argument");
+  pf_hierarchy* h = op->h;
+  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
+  if (!op->set[static_cast<size_t>(sub)]) state("operator values not set");
+  const DevLevel& D = h->levels[op->level].sub[sub];
+  if (nnz != D.A.nnz) invalid("nnz does not match the level");
+  PF_CUDA(cudaSetDevice(h->device));
+  const DevVals& V = op->vals[static_cast<size_t>(sub)];
+  std::vector<double> sv(static_cast<size_t>(D.A.stored));
+  if (V.vkind == 0) {
+    PF_CUDA(cudaMemcpy(sv.data(), V.vals.p, sizeof(double) * sv.size(), cudaMemcpyDeviceToHost));
+  } else {
+    std::vector<double> table(static_cast<size_t>(V.table.n));
+    PF_CUDA(cudaMemcpy(table.data(), V.table.p, sizeof(double) * table.size(), cudaMemcpyDeviceToHost));
+    if (V.vkind == 1) {
+      std::vector<uint8_t> ix(sv.size());
+      PF_CUDA(cudaMemcpy(ix.data(), V.vi8.p, ix.size(), cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < sv.size(); ++i) sv[i] = table[ix[i]];
+    } else {
+      std::vector<uint16_t> ix(sv.size());
+      PF_CUDA(cudaMemcpy(ix.data(), V.vi16.p, 2 * ix.size(), cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < sv.size(); ++i) sv[i] = table[ix[i]];
+    }
+  }
+  for (int32_t hr = 0; hr < D.n; ++hr) {
+    const int64_t base = sell_row_base(D.sell_ptr.data(), D.perm[hr]);
+    for (int64_t k = D.csr_rowptr[hr]; k < D.csr_rowptr[hr + 1]; ++k)
+      values[k] = sv[static_cast<size_t>(sell_entry(base, static_cast<int>(k - D.csr_rowptr[hr])))];
+  }
+  PF_API_END
+}
+
+pf_status pf_assembly_create(pf_hierarchy* h, int level, pf_assembly** out) {
+  PF_API_BEGIN
+  check_level(h, level);
+  if (!out) invalid("null output");
+  auto a = std::make_unique<pf_assembly>();
+  a->h = h;
+  a->level = level;
+  a->sub.resize(static_cast<size_t>(h->n_sub));
+  *out = a.release();
+  PF_API_END
+}
+
+pf_status pf_assembly_set(pf_assembly* a, int sub, const pf_assembly_desc* d) {
+  PF_API_BEGIN
+  if (!a || !d) invalid("null argument");
+  pf_hierarchy* h = a->h;
+  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
+  const DevLevel& D = h->levels[a->level].sub[sub];
+  if (d->n_dofs != D.n) invalid("assembly description does not match the level's dof count");
+  if (d->dim != 2 && d->dim != 3) invalid("dimension must be 2 or 3");
+  if (!d->lattice || !d->cell_mask || !d->elem || !d->elem_class || d->n_classes < 1 || d->n_cells < 1)
+    invalid("null assembly array");
+  if (d->n_coarse < 1 || d->level < 0 || (static_cast<int64_t>(d->n_coarse) << d->level) != d->n_cells)
+    invalid("n_cells must be n_coarse * 2^level");
+  PF_CUDA(cudaSetDevice(h->device));
+  const int32_t n = D.n;
+  std::vector<int32_t> lat(static_cast<size_t>(3 * n));
+  std::vector<uint8_t> mask(static_cast<size_t>(n));
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t r = D.perm[i];
+    for (int k = 0; k < 3; ++k) lat[3 * static_cast<size_t>(r) + k] = d->lattice[3 * static_cast<int64_t>(i) + k];
+    mask[static_cast<size_t>(r)] = d->cell_mask[i];
+  }
+  const int64_t N = d->n_cells, ncells = d->dim == 3 ? N * N * N : N * N;
+  const int64_t nel = d->dim == 3 ? int64_t(d->n_classes) * d->n_classes * d->n_classes
+                                  : int64_t(d->n_classes) * d->n_classes;
+  pf_assembly::Sub& S = a->sub[static_cast<size_t>(sub)];
+  S.dim = d->dim;
+  S.N = d->n_cells;
+  S.nh = d->n_classes;
+  S.n_coarse = d->n_coarse;
+  S.grid_level = d->level;
+  S.lattice.upload(lat);
+  S.cell_mask.upload(mask);
+  S.cls.upload(std::vector<int32_t>(d->elem_class, d->elem_class + 3 * N));
+  S.elem.upload(std::vector<double>(d->elem, d->elem + 64 * nel));
+  if (d->kappa) S.kappa.upload(std::vector<double>(d->kappa, d->kappa + ncells));
+  else S.kappa.reset();
+  S.set = true;
+  PF_API_END
+}
+
+pf_status pf_assemble_operator(pf_assembly* a, pf_operator* op) {
+  PF_API_BEGIN
+  if (!a || !op) invalid("null argument");
+  pf_hierarchy* h = a->h;
+  if (op->h != h || op->level != a->level) invalid("operator of another level");
+  for (const auto& S : a->sub)
+    if (!S.set) state("assembly description not set for every subdomain");
+  PF_CUDA(cudaSetDevice(h->device));
+  auto launch = launcher(h);
+  for (int s = 0; s < h->n_sub; ++s) {
+    const DevLevel& D = h->levels[a->level].sub[s];
+    const pf_assembly::Sub& S = a->sub[static_cast<size_t>(s)];
+    DevVals& out = op->vals[static_cast<size_t>(s)];
+    if (out.vkind != 0 || out.vals.n != D.A.stored) {  // fp64 values, allocated once
+      out = DevVals{};
+      out.vkind = 0;
+      out.vals.alloc(D.A.stored);
+      PF_CUDA(cudaMemsetAsync(out.vals.p, 0, sizeof(double) * static_cast<size_t>(D.A.stored), h->stream));
+    }
+    const AsmView v{S.lattice.p, S.cell_mask.p, D.d_is_dir.p, S.kappa.p, S.elem.p, S.cls.p, S.N, S.nh, S.n_coarse,
+                    S.grid_level};
+    if (S.dim == 3)
+      launch(grid_for(D.n), kBlock, k_assemble<3>, v, view(D.A), out.vals.p, D.n);
+    else
+      launch(grid_for(D.n), kBlock, k_assemble<2>, v, view(D.A), out.vals.p, D.n);
+    op->set[static_cast<size_t>(s)] = true;
+  }
+  sync(h);
+  PF_API_END
+}
+
+pf_status pf_assembly_destroy(pf_assembly* a) {
+  PF_API_BEGIN
+  if (a) cudaSetDevice(a->h->device);
+  delete a;
   PF_API_END
 }
 

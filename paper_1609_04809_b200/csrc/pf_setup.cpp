@@ -423,6 +423,9 @@ struct SetupLevel {
   std::vector<int64_t> p_off;
   std::vector<int32_t> p_col;
   std::vector<double> p_w;
+  // per local dof: which of the 2^d cells around the vertex are local (finest level; bit k
+  // <-> cell with low corner = vertex along axis a iff bit a of k), for device assembly
+  std::vector<uint8_t> cell_mask;
   // element matrices per distinct cell shape (extents differ in the last bit across cells
   // unless N is a power of two)
   std::vector<Element> elems;
@@ -495,6 +498,9 @@ struct pf_setup {
   // matrices (8 x 8, row-major) of every cell of each coarser level
   std::vector<double> kappa;
   std::vector<std::vector<double>> coef_elem;
+  // device assembly description of the finest level (pf_assembly_desc)
+  std::vector<double> asm_elem;
+  std::vector<int32_t> asm_hid;
   double seconds = 0;
 };
 
@@ -917,6 +923,20 @@ void build_level(pf_setup& s, int l) {
   }
   L->rowptr.assign(static_cast<size_t>(n) + 1, 0);
   for (int32_t i = 0; i < n; ++i) L->rowptr[i + 1] = L->rowptr[i] + rowlen[i + 1];
+  if (finest) {
+    L->cell_mask.assign(static_cast<size_t>(n), 0);
+#pragma omp parallel for schedule(static)
+    for (int32_t i = 0; i < n; ++i) {
+      int64_t x, y, z;
+      unpack(L->vert[i], x, y, z);
+      uint8_t m = 0;
+      for (int k = 0; k < (1 << d); ++k) {
+        const int64_t cx = x - 1 + (k & 1), cy = y - 1 + ((k >> 1) & 1), cz = d == 3 ? z - 1 + ((k >> 2) & 1) : 0;
+        if (V.cell_local(cx, cy, cz)) m |= static_cast<uint8_t>(1u << k);
+      }
+      L->cell_mask[static_cast<size_t>(i)] = m;
+    }
+  }
   const int64_t nnz = L->rowptr[n];
   L->cols.resize(static_cast<size_t>(nnz));
   L->vals.resize(static_cast<size_t>(nnz));
@@ -1332,6 +1352,37 @@ pf_status pf_setup_load_desc(const pf_setup* s, pf_load_desc* out) {
     out->qweight = s->d == 3 ? (0.5 * 0.5) * 0.5 : 0.5 * 0.5;
     out->boundary = s->ld_boundary.data();
     out->is_dirichlet = L.is_dir.data();
+  });
+}
+
+pf_status pf_setup_assembly_desc(pf_setup* s, pf_assembly_desc* out) {
+  return guard([&] {
+    if (!s || !out) invalid("null argument");
+    if (s->prob.kind == PF_PROBLEM_HEAT) invalid("device assembly covers the stiffness systems (not the CN system)");
+    const SetupLevel& L = *s->levels.back();
+    const int d = s->d;
+    const int64_t N = L.geo.N;
+    if (s->asm_elem.empty()) {
+      for (const Element& E : L.elems)
+        for (int i = 0; i < 8; ++i)
+          for (int j = 0; j < 8; ++j) s->asm_elem.push_back(E.K[i][j]);
+      s->asm_hid.assign(static_cast<size_t>(3 * N), 0);
+      for (int a = 0; a < d; ++a)
+        for (int64_t c = 0; c < N; ++c) s->asm_hid[static_cast<size_t>(a * N + c)] = L.hid[static_cast<size_t>(c)];
+    }
+    std::memset(out, 0, sizeof *out);
+    out->dim = d;
+    out->n_cells = static_cast<int32_t>(N);
+    out->n_dofs = L.n;
+    out->n_coarse = s->n_coarse;
+    out->level = s->n_levels - 1;
+    out->lattice = s->ld_lattice.data();
+    out->cell_mask = L.cell_mask.data();
+    out->is_dirichlet = L.is_dir.data();
+    out->kappa = s->prob.kind == PF_PROBLEM_LOGNORMAL ? s->kappa.data() : nullptr;
+    out->elem = s->asm_elem.data();
+    out->elem_class = s->asm_hid.data();
+    out->n_classes = L.nh;
   });
 }
 

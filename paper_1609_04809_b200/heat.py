@@ -39,7 +39,7 @@ def time_steps(end_time: float, dt: float) -> int:
 class Operator:
     """A second matrix on a level's sparsity pattern (pf_operator_create)."""
 
-    def __init__(self, h: Hierarchy, level: int, values):
+    def __init__(self, h: Hierarchy, level: int, values=()):
         self.h, self.level = h, level
         self._p = C.c_void_p()
         _lib.check(_lib.lib().pf_operator_create(h._h, level, C.byref(self._p)))
@@ -51,6 +51,12 @@ class Operator:
     def apply(self, x: DeviceVector, y: DeviceVector) -> None:
         """spmv (linalg.cpp:45-57) with this operator."""
         _lib.check(_lib.lib().pf_operator_apply(self._p, x._p, y._p))
+
+    def values(self, sub: int, nnz: int) -> np.ndarray:
+        """The values of one subdomain in its level desc's CSR entry order."""
+        out = np.empty(nnz)
+        _lib.check(_lib.lib().pf_operator_get_values(self._p, sub, out.ctypes.data, nnz))
+        return out
 
     def close(self):
         if self._p:
@@ -188,3 +194,31 @@ class HeatRun:
         self.h.close()
         for s in self.setups:
             s.close()
+
+
+class Assembly:
+    """Device assembly of a level's Q1 stiffness system (pf_assembly_*; assemble_system +
+    apply_dirichlet_rows, assembly.cpp:103-170), optionally with a per-cell coefficient."""
+
+    def __init__(self, h: Hierarchy, level: int, descs):
+        self.h, self.level = h, level
+        self._p = C.c_void_p()
+        _lib.check(_lib.lib().pf_assembly_create(h._h, level, C.byref(self._p)))
+        h._vectors.add(self)
+        for s, d in enumerate(descs):
+            _lib.check(_lib.lib().pf_assembly_set(self._p, s, C.byref(d)))
+
+    def assemble(self, op: Operator) -> Operator:
+        _lib.check(_lib.lib().pf_assemble_operator(self._p, op._p))
+        return op
+
+    def close(self):
+        if self._p:
+            _lib.lib().pf_assembly_destroy(self._p)
+            self._p = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

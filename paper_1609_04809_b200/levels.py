@@ -153,6 +153,13 @@ class StructuredSetup:
         _lib.check(_lib.lib().pf_setup_load_desc(self._live(), C.byref(d)), setup=True)
         return d
 
+    def assembly_desc(self) -> _lib.AssemblyDesc:
+        """The device assembly description of the finest level (pointers valid while this
+        setup lives; needs keep=True for non-heat problems)."""
+        d = _lib.AssemblyDesc()
+        _lib.check(_lib.lib().pf_setup_assembly_desc(self._live(), C.byref(d)), setup=True)
+        return d
+
     def scales(self, t: float):
         """(source_scale, has_dirichlet, dirichlet_scale) at time t, host libm."""
         s, g, hd = C.c_double(), C.c_double(), C.c_int32()
