@@ -197,12 +197,16 @@ def run_b200(args):
 
     W = WORKLOAD
     t0 = time.time()
-    setup = StructuredSetup(W["dim"], W["n_coarse"], W["levels"], world, rank)
-    # multi-process: every rank's bottom levels, replicated on each GPU (one allgather per
-    # cycle feeds a redundant bottom V-cycle instead of per-sweep exchanges on tiny levels)
-    replicas = (gmg.replica_levels(W["dim"], W["n_coarse"], W["levels"], world) if world > 1 else None)
+    # multi-process: direct halo lists + fused exchanges (one message group per sweep for
+    # master/slave + halo1, + halo2 after each smoothing phase; results unchanged), and
+    # every rank's bottom levels replicated on each GPU (one allgather per cycle feeds a
+    # redundant bottom V-cycle instead of per-sweep exchanges on the tiny levels)
+    multi = world > 1
+    setup = StructuredSetup(W["dim"], W["n_coarse"], W["levels"], world, rank, direct_halos=multi)
+    replicas = (gmg.replica_levels(W["dim"], W["n_coarse"], W["levels"], world, direct_halos=True)
+                if multi else None)
     h = gmg.Hierarchy([setup.levels], device=local, rank_base=rank, world_size=world,
-                      coarse_replicas=replicas)
+                      coarse_replicas=replicas, fused_exchanges=multi)
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:

@@ -204,6 +204,12 @@ pf_status pf_hierarchy_set_coarse_replica(pf_hierarchy* h, int rank, const pf_le
  * after ONE allgather of the restricted residual, instead of the per-sweep halo
  * exchanges the reference performs on those latency-bound levels; bit-identical. */
 pf_status pf_hierarchy_set_replica_level(pf_hierarchy* h, int level, int rank, const pf_level_desc* desc);
+/* Before finalize: run each smoothing sweep's master/slave and halo1 scatters (and the
+ * halo2 scatter that follows a smoothing phase) as ONE message group instead of two or
+ * three dependent ones.  Needs halo channel lists that never forward a Slave-held value
+ * (pf_setup_options.direct_halos; checked at finalize, PF_ERR_INVALID_ARGUMENT otherwise).
+ * Must be set identically on every rank.  Results are unchanged bit for bit. */
+pf_status pf_hierarchy_set_fused_exchanges(pf_hierarchy* h, int on);
 pf_status pf_hierarchy_destroy(pf_hierarchy* h);
 
 /* Single-GPU test bench of the multi-process path: `world_size` single-subdomain

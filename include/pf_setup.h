@@ -51,6 +51,19 @@ enum { PF_PROBLEM_BASELINE = 0, PF_PROBLEM_REFERENCE_POISSON = 1, PF_PROBLEM_UNI
 
 pf_status pf_setup_create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem,
                           pf_setup** out);
+/* All options at once.  direct_halos = 1: a Halo1/Halo2 request for a carrier that its
+ * owner holds as Slave goes to the carrier's Master instead (which holds the same value
+ * after the master/slave scatter), so the halo exchanges no longer depend on the
+ * master/slave one; with pf_hierarchy_set_fused_exchanges() a smoothing sweep then needs
+ * one message group instead of two (results unchanged bit for bit).  The channel lists
+ * then differ from the reference's (which routes through the Slave). */
+typedef struct {
+  int32_t dim, n_coarse, n_levels, n_ranks, rank, problem;
+  double dt;               /* PF_PROBLEM_HEAT */
+  uint64_t seed;           /* PF_PROBLEM_LOGNORMAL */
+  int32_t direct_halos;
+} pf_setup_options;
+pf_status pf_setup_create_opts(const pf_setup_options* opts, pf_setup** out);
 /* The lognormal-coefficient problem with its seed. */
 pf_status pf_setup_create_lognormal(int dim, int n_coarse, int n_levels, int n_ranks, int rank, uint64_t seed,
                                     pf_setup** out);

@@ -91,6 +91,12 @@ class AssemblyDesc(C.Structure):
                 ("elem_class", C.c_void_p), ("n_classes", C.c_int32)]
 
 
+class SetupOptions(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("n_coarse", C.c_int32), ("n_levels", C.c_int32), ("n_ranks", C.c_int32),
+                ("rank", C.c_int32), ("problem", C.c_int32), ("dt", C.c_double), ("seed", C.c_uint64),
+                ("direct_halos", C.c_int32)]
+
+
 class SmootherConfig(C.Structure):
     _fields_ = [("kind", C.c_int32), ("sweeps", C.c_int32), ("local_sweeps", C.c_int32),
                 ("damping", C.c_double)]
@@ -113,7 +119,7 @@ class SolveStats(C.Structure):
 EXPORTS = [
     "pf_last_error", "pf_version", "pf_device_count", "pf_default_smoother_config", "pf_default_multigrid_config",
     "pf_hierarchy_create", "pf_hierarchy_set_level", "pf_hierarchy_finalize", "pf_nccl_unique_id",
-    "pf_hierarchy_init_nccl", "pf_nccl_selftest", "pf_hierarchy_set_coarse_replica", "pf_hierarchy_set_replica_level",
+    "pf_hierarchy_init_nccl", "pf_nccl_selftest", "pf_hierarchy_set_fused_exchanges", "pf_hierarchy_set_coarse_replica", "pf_hierarchy_set_replica_level",
     "pf_hierarchy_destroy",
     "pf_loopback_create", "pf_loopback_destroy", "pf_hierarchy_init_loopback", "pf_hierarchy_device_bytes",
     "pf_vector_create", "pf_vector_destroy", "pf_vector_upload", "pf_vector_download",
@@ -129,7 +135,7 @@ EXPORTS = [
     "pf_setup_create", "pf_setup_create_heat", "pf_setup_destroy", "pf_setup_level", "pf_setup_level_keys",
     "pf_setup_rhs", "pf_setup_counts", "pf_setup_seconds", "pf_setup_rhs_operator", "pf_setup_load_at",
     "pf_setup_load_desc", "pf_setup_scales", "pf_setup_export_matrixmarket", "pf_setup_create_lognormal",
-    "pf_setup_kappa", "pf_setup_assembly_desc",
+    "pf_setup_kappa", "pf_setup_assembly_desc", "pf_setup_create_opts",
 ]
 
 _lib = None
@@ -160,6 +166,8 @@ def lib():
         "pf_nccl_unique_id": [P, C.c_int],
         "pf_hierarchy_init_nccl": [P, P, C.c_int],
         "pf_nccl_selftest": [C.c_int, C.POINTER(C.c_int)],
+        "pf_hierarchy_set_fused_exchanges": [P, C.c_int],
+        "pf_setup_create_opts": [C.POINTER(SetupOptions), PP],
         "pf_hierarchy_set_coarse_replica": [P, C.c_int, C.POINTER(LevelDesc)],
         "pf_hierarchy_set_replica_level": [P, C.c_int, C.c_int, C.POINTER(LevelDesc)],
         "pf_loopback_create": [C.c_int, PP],

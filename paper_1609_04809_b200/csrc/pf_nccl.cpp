@@ -173,11 +173,18 @@ void Loopback::group_end(cudaStream_t s) {
   auto& mine = hub->posts[static_cast<size_t>(rank)];
   cuda_check(cudaEventRecord(mine.ready, s), "cudaEventRecord");
   hub->barrier();
+  // NCCL semantics: the k-th receive from a peer in a group matches that peer's k-th
+  // send to this rank in the same group
+  std::vector<int> nth(static_cast<size_t>(hub->world), 0);
   for (const auto& r : mine.recvs) {
     const auto& src = hub->posts[static_cast<size_t>(r.peer)];
     const LoopbackHub::Msg* m = nullptr;
+    int k = nth[static_cast<size_t>(r.peer)]++;
     for (const auto& snd : src.sends)
-      if (snd.peer == rank) m = &snd;
+      if (snd.peer == rank && k-- == 0) {
+        m = &snd;
+        break;
+      }
     if (!m || m->n != r.n) {
       hub->abort();
       throw Error(PF_ERR_TRANSPORT, "loopback: unmatched receive from rank " + std::to_string(r.peer));

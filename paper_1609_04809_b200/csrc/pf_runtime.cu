@@ -410,17 +410,20 @@ const HostChannel* find_channel(const HostLevel& H, int kind, int peer) {
 // Exchange plans of one level from the per-subdomain channel lists.  local: every peer
 // is one of the subdomains in H (ranks rank_base + s); else one subdomain whose peers
 // live in other processes (NCCL segments).
-void build_exchange(const std::vector<HostLevel>& H, const std::vector<DevLevel>& D, int rank_base,
-                    bool local, std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS>& scatter, ExchangePlan& A) {
+// One scatter plan over a set of channel kinds (several kinds: one message group; their
+// send and receive sets must be independent — see build_fused_plans).
+void build_scatter_plan(const std::vector<HostLevel>& H, const std::vector<DevLevel>& D, int rank_base, bool local,
+                        const std::vector<int>& kinds, ExchangePlan& P) {
   const int n_sub = static_cast<int>(H.size());
-  for (int kind = 0; kind < PF_NUM_CHANNEL_KINDS; ++kind) {
-    ExchangePlan& P = scatter[kind];
+  {
+    auto in = [&](int k) { return std::find(kinds.begin(), kinds.end(), k) != kinds.end(); };
     if (local) {
       std::vector<int32_t> dst, src;
       for (int s = 0; s < n_sub; ++s) {
         const int R = rank_base + s;
         for (const HostChannel& c : H[s].channels) {
-          if (c.kind != kind || c.recv.empty()) continue;
+          if (!in(c.kind) || c.recv.empty()) continue;
+          const int kind = c.kind;
           const int p = c.peer - rank_base;
           if (p < 0 || p >= n_sub || p == s) invalid("channel peer " + std::to_string(c.peer) + " out of range");
           const HostChannel* pc = find_channel(H[p], kind, R);
@@ -441,7 +444,7 @@ void build_exchange(const std::vector<HostLevel>& H, const std::vector<DevLevel>
       const DevLevel& D0 = D[0];
       std::vector<int32_t> pk, up;
       for (const HostChannel& c : H[0].channels) {
-        if (c.kind != kind) continue;
+        if (!in(c.kind)) continue;
         if (!c.send.empty()) {
           P.send_segs.push_back({c.peer, static_cast<int64_t>(pk.size()), static_cast<int64_t>(c.send.size())});
           for (int32_t d : c.send) pk.push_back(D0.perm[d]);
@@ -458,6 +461,12 @@ void build_exchange(const std::vector<HostLevel>& H, const std::vector<DevLevel>
       P.recvbuf.alloc(static_cast<int64_t>(up.size()));
     }
   }
+}
+
+void build_exchange(const std::vector<HostLevel>& H, const std::vector<DevLevel>& D, int rank_base,
+                    bool local, std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS>& scatter, ExchangePlan& A) {
+  const int n_sub = static_cast<int>(H.size());
+  for (int kind = 0; kind < PF_NUM_CHANNEL_KINDS; ++kind) build_scatter_plan(H, D, rank_base, local, {kind}, scatter[kind]);
   // master/slave accumulate: slaves push v[recv_dofs], masters add in ascending peer order
   std::map<int32_t, std::vector<int32_t>> contrib;  // master dst -> sources, peer-ascending
   if (local) {
@@ -514,9 +523,34 @@ void build_exchange(const std::vector<HostLevel>& H, const std::vector<DevLevel>
   A.acc_dst.upload(dsts);
 }
 
+// Fused exchanges (pf_hierarchy_set_fused_exchanges): master/slave + halo1 as one message
+// group per sweep, + halo2 after a smoothing phase.  Valid when no halo send entry is a
+// master/slave receive entry of the same subdomain (the halo value would otherwise be the
+// one the master/slave scatter is still delivering) — pf_setup's direct_halos lists.
+void build_fused_plans(pf_hierarchy* h, int l) {
+  Level& L = h->levels[l];
+  for (const HostLevel& H : L.host) {
+    std::vector<uint8_t> slave(static_cast<size_t>(H.n), 0);
+    for (const HostChannel& c : H.channels)
+      if (c.kind == PF_CH_MASTER_SLAVE)
+        for (int32_t d : c.recv) slave[static_cast<size_t>(d)] = 1;
+    for (const HostChannel& c : H.channels)
+      if (c.kind != PF_CH_MASTER_SLAVE)
+        for (int32_t d : c.send)
+          if (slave[static_cast<size_t>(d)])
+            invalid("fused exchanges need halo lists that never forward a Slave-held value "
+                    "(level " + std::to_string(l) + "): build them with direct_halos");
+  }
+  const bool local = h->world == h->n_sub;
+  build_scatter_plan(L.host, L.sub, h->rank_base, local, {PF_CH_MASTER_SLAVE, PF_CH_HALO1}, L.fused_ms_h1);
+  build_scatter_plan(L.host, L.sub, h->rank_base, local, {PF_CH_MASTER_SLAVE, PF_CH_HALO1, PF_CH_HALO2},
+                     L.fused_all);
+}
+
 void build_plans(pf_hierarchy* h, int l) {
   Level& L = h->levels[l];
   build_exchange(L.host, L.sub, h->rank_base, h->world == h->n_sub, L.scatter, L.accumulate);
+  if (h->fused) build_fused_plans(h, l);
 }
 
 // Pack a coarse level (all subdomains of H/D, level-global indices) for the shared-memory
@@ -808,8 +842,11 @@ void build_rep_bottom(pf_hierarchy* h) {
 
 // ------------------------------------------------------------------ enqueue --
 
-void enq_scatter(pf_hierarchy* h, int l, int kind, double* v) {
-  ExchangePlan& P = h->levels[l].scatter[kind];
+void enq_plan(pf_hierarchy* h, ExchangePlan& P, double* v);
+
+void enq_scatter(pf_hierarchy* h, int l, int kind, double* v) { enq_plan(h, h->levels[l].scatter[kind], v); }
+
+void enq_plan(pf_hierarchy* h, ExchangePlan& P, double* v) {
   auto launch = launcher(h);
   if (h->world == h->n_sub) {
     if (P.n == 0) return;
@@ -910,8 +947,10 @@ void enq_copy(pf_hierarchy* h, const double* src, double* dst, int64_t n) {
 
 // smooth (solvers.cpp:56-68) on x (primary buffer) with b.
 // first_done: the first Jacobi sweep already ran (k_jacobi_norm in the solve graph).
-void enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_smoother_config& sc,
-                bool first_done = false) {
+// Returns true when the halo2 scatter that follows a smoothing phase in the cycle was
+// already done (fused into the last sweep's exchange).
+bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_smoother_config& sc,
+                bool first_done = false, bool then_h2 = false) {
   Level& L = h->levels[l];
   auto launch = launcher(h);
   double* bufs[2] = {xv->cur(), xv->alt()};
@@ -947,10 +986,16 @@ void enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
           }
       }
     }
-    enq_update_ms(h, l, bufs[cur], PF_UPDATE_SCATTER);
-    enq_scatter(h, l, PF_CH_HALO1, bufs[cur]);
+    if (h->fused) {
+      const bool last = sweep + 1 == sc.sweeps;
+      enq_plan(h, last && then_h2 ? L.fused_all : L.fused_ms_h1, bufs[cur]);
+    } else {
+      enq_update_ms(h, l, bufs[cur], PF_UPDATE_SCATTER);
+      enq_scatter(h, l, PF_CH_HALO1, bufs[cur]);
+    }
   }
   if (cur) enq_copy(h, bufs[1], bufs[0], L.total);
+  return h->fused && then_h2 && sc.sweeps > 0;
 }
 
 void enq_prolong(pf_hierarchy* h, int fine, const double* xc, double* xf, int add) {
@@ -1081,8 +1126,7 @@ void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_
   }
   pf_smoother_config pre = cfg.smoother;
   pre.sweeps = cfg.pre_smooth;
-  enq_smooth(h, l, xv, b, pre, first_done && cfg.pre_smooth > 0);
-  enq_scatter(h, l, PF_CH_HALO2, x);
+  if (!enq_smooth(h, l, xv, b, pre, first_done && cfg.pre_smooth > 0, true)) enq_scatter(h, l, PF_CH_HALO2, x);
   enq_residual(h, l, x, b, L.r.p);
   Level& Cl = h->levels[l - 1];
   enq_restrict(h, l, L.r.p, Cl.b->cur(), Cl.x->cur(), 1);
@@ -1107,8 +1151,7 @@ void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_
   enq_prolong(h, l, Cl.x->cur(), x, 1);
   pf_smoother_config post = cfg.smoother;
   post.sweeps = cfg.post_smooth;
-  enq_smooth(h, l, xv, b, post);
-  enq_scatter(h, l, PF_CH_HALO2, x);
+  if (!enq_smooth(h, l, xv, b, post, false, true)) enq_scatter(h, l, PF_CH_HALO2, x);
 }
 
 // v_cycle (multigrid.cpp:194-208)
@@ -1677,6 +1720,14 @@ pf_status pf_nccl_selftest(int device, int* ok) {
   PF_CUDA(cudaMemcpy(out, buf.p, sizeof out, cudaMemcpyDeviceToHost));
   PF_CUDA(cudaStreamDestroy(st));
   *ok = out[4] == 1.5 && out[5] == -2.25 && out[6] == 3.0;
+  PF_API_END
+}
+
+pf_status pf_hierarchy_set_fused_exchanges(pf_hierarchy* h, int on) {
+  PF_API_BEGIN
+  if (!h) invalid("null hierarchy");
+  if (h->finalized) state("set fused exchanges before pf_hierarchy_finalize");
+  h->fused = on != 0;
   PF_API_END
 }
 

@@ -149,6 +149,7 @@ struct Level {
   int64_t total = 0;            // sum of subdomain sizes
   std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS> scatter;
   ExchangePlan accumulate;
+  ExchangePlan fused_ms_h1, fused_all;  // pf_hierarchy_set_fused_exchanges
   DevBuf<double> r;             // residual scratch
   DevBuf<double> sumsq;         // per-subdomain sums of squares
   DevBuf<double> norm;          // allreduced norm
@@ -180,6 +181,7 @@ struct pf_hierarchy {
   int device = 0;
   int n_levels = 0, n_sub = 1, rank_base = 0, world = 1;
   bool finalized = false;
+  bool fused = false;  // master/slave + halo scatters as one message group (direct halo lists)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<pf::Level> levels;

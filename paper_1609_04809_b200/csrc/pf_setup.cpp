@@ -290,7 +290,10 @@ struct VInfo {
 };
 
 // femapper.cpp:123-165 (classes) and :237-264 (requests) for one vertex of rank q.
-VInfo classify(const RankView& V, int64_t x, int64_t y, int64_t z) {
+// direct: halo requests for a carrier the owner holds as Slave go to its Master instead
+// (the value the Slave would forward after the master/slave scatter), so the Halo1/Halo2
+// exchanges no longer depend on the master/slave one and can share its message group.
+VInfo classify(const RankView& V, int64_t x, int64_t y, int64_t z, bool direct = false) {
   const Geo& g = *V.g;
   VInfo info;
   int owners[8];
@@ -334,6 +337,7 @@ VInfo classify(const RankView& V, int64_t x, int64_t y, int64_t z) {
   } else if (info.cls == kHalo1 || info.cls == kHalo2) {
     info.kind = info.cls == kHalo1 ? PF_CH_HALO1 : PF_CH_HALO2;
     info.target = owners[0];
+    if (direct && master >= 0 && master != owners[0]) info.target = master;
   }
   return info;
 }
@@ -485,6 +489,7 @@ struct Problem {
 
 struct pf_setup {
   int d = 3, n_coarse = 2, n_levels = 1, n_ranks = 1, rank = 0;
+  bool direct_halos = false;  // pf_setup_options::direct_halos
   Problem prob;
   std::vector<int> coarse_owner;
   std::vector<std::unique_ptr<SetupLevel>> levels;
@@ -781,7 +786,7 @@ void build_level(pf_setup& s, int l) {
 #pragma omp parallel for schedule(static) collapse(2)
   for (int64_t x = vb.lo[0]; x < vb.hi[0]; ++x)
     for (int64_t y = vb.lo[1]; y < vb.hi[1]; ++y)
-      for (int64_t z = vb.lo[2]; z < vb.hi[2]; ++z) info[vb.idx(x, y, z)] = classify(V, x, y, z);
+      for (int64_t z = vb.lo[2]; z < vb.hi[2]; ++z) info[vb.idx(x, y, z)] = classify(V, x, y, z, s.direct_halos);
 
   // --- numbering: the reference's own.  build_fespace numbers vertices at first touch
   // over the local cells in gcn order, ring-slot order inside a cell (fespace.cpp:47-85);
@@ -1006,7 +1011,7 @@ void build_level(pf_setup& s, int l) {
     for (int64_t x = vb.lo[0]; x < vb.hi[0]; ++x)
       for (int64_t y = vb.lo[1]; y < vb.hi[1]; ++y)
         for (int64_t z = vb.lo[2]; z < vb.hi[2]; ++z) {
-          const VInfo v = classify(W, x, y, z);
+          const VInfo v = classify(W, x, y, z, s.direct_halos);
           if (!v.local || v.target != me) continue;
           const int32_t li = L->lookup(x, y, z);
           if (li < 0) throw SetupError(PF_ERR_STATE, "request from a neighbour resolves to no local dof");
@@ -1193,7 +1198,7 @@ pf_status guard(F&& f) {
 }
 
 pf_status create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int problem, double dt,
-                 uint64_t seed, pf_setup** out) {
+                 uint64_t seed, pf_setup** out, bool direct_halos = false) {
   return guard([&] {
     if (!out) invalid("null output");
     if (dim != 2 && dim != 3) invalid("dimension must be 2 or 3, got " + std::to_string(dim));
@@ -1213,6 +1218,7 @@ pf_status create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int
     s->prob.d = dim;
     s->prob.dt = problem == PF_PROBLEM_HEAT ? dt : 0.0;
     s->prob.seed = seed;
+    s->direct_halos = direct_halos;
     s->coarse_owner = coarse_partition(dim, n_coarse, n_ranks);
     if (problem == PF_PROBLEM_LOGNORMAL) build_coefficients(*s);
     for (int l = 0; l < n_levels; ++l) build_level(*s, l);
@@ -1240,6 +1246,15 @@ pf_status pf_setup_create(int dim, int n_coarse, int n_levels, int n_ranks, int 
 pf_status pf_setup_create_heat(int dim, int n_coarse, int n_levels, int n_ranks, int rank, double dt,
                                pf_setup** out) {
   return create(dim, n_coarse, n_levels, n_ranks, rank, PF_PROBLEM_HEAT, dt, 0, out);
+}
+
+pf_status pf_setup_create_opts(const pf_setup_options* o, pf_setup** out) {
+  if (!o) {
+    g_setup_err = "null options";
+    return PF_ERR_INVALID_ARGUMENT;
+  }
+  return create(o->dim, o->n_coarse, o->n_levels, o->n_ranks, o->rank, o->problem, o->dt, o->seed, out,
+                o->direct_halos != 0);
 }
 
 pf_status pf_setup_create_lognormal(int dim, int n_coarse, int n_levels, int n_ranks, int rank, uint64_t seed,

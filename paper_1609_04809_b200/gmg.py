@@ -149,7 +149,7 @@ class Hierarchy:
     """
 
     def __init__(self, levels, device: int = 0, rank_base: int = 0, world_size: int | None = None,
-                 finalize: bool = True, coarse_replicas=None):
+                 finalize: bool = True, coarse_replicas=None, fused_exchanges: bool = False):
         n_sub = len(levels)
         n_levels = len(levels[0])
         world = n_sub if world_size is None else world_size
@@ -172,6 +172,8 @@ class Hierarchy:
                     d, keep = lv.desc()
                     _lib.check(L.pf_hierarchy_set_replica_level(self._h, l, r, C.byref(d)))
                     del keep
+        if fused_exchanges:
+            _lib.check(L.pf_hierarchy_set_fused_exchanges(self._h, 1))
         if finalize:
             self.finalize()
 
@@ -357,11 +359,12 @@ def solve_outer_host(h: Hierarchy, x_host: list, b_host: list, cfg: MultigridCon
 
 
 def replica_levels(dim: int, n_coarse: int, n_levels: int, world: int, problem: int = 0,
-                   max_rows: int = 65536):
+                   max_rows: int = 65536, direct_halos: bool = False):
     """Every rank's bottom levels 0..top for a multi-process hierarchy (coarse_replicas):
     top is the highest level below the finest whose rows over all ranks stay <= max_rows
     (those levels then run redundantly on every GPU after one allgather)."""
-    per_rank = [StructuredSetup(dim, n_coarse, max(1, n_levels - 1), world, q, problem).levels
+    per_rank = [StructuredSetup(dim, n_coarse, max(1, n_levels - 1), world, q, problem,
+                                direct_halos=direct_halos).levels
                 for q in range(world)]
     top = 0
     for l in range(len(per_rank[0])):

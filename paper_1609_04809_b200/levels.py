@@ -83,10 +83,14 @@ class StructuredSetup:
 
     def __init__(self, dim: int, n_coarse: int, n_levels: int, n_ranks: int = 1, rank: int = 0,
                  problem: int = _lib.PF_PROBLEM_BASELINE, dt: float | None = None, keep: bool = False,
-                 seed: int = 1):
+                 seed: int = 1, direct_halos: bool = False):
         L = _lib.lib()
         self._h = C.c_void_p()
-        if problem == _lib.PF_PROBLEM_HEAT:
+        if direct_halos:
+            o = _lib.SetupOptions(dim, n_coarse, n_levels, n_ranks, rank, problem,
+                                  0.01 if dt is None else dt, seed, 1)
+            _lib.check(L.pf_setup_create_opts(C.byref(o), C.byref(self._h)), setup=True)
+        elif problem == _lib.PF_PROBLEM_HEAT:
             _lib.check(L.pf_setup_create_heat(dim, n_coarse, n_levels, n_ranks, rank,
                                               0.01 if dt is None else dt, C.byref(self._h)), setup=True)
         elif problem == _lib.PF_PROBLEM_LOGNORMAL:

@@ -7,8 +7,8 @@ from paper_1609_04809_b200 import gmg
 from paper_1609_04809_b200.levels import StructuredSetup
 
 
-def structured(dim, n_coarse, levels, K, problem=0):
-    setups = [StructuredSetup(dim, n_coarse, levels, K, r, problem) for r in range(K)]
+def structured(dim, n_coarse, levels, K, problem=0, direct_halos=False):
+    setups = [StructuredSetup(dim, n_coarse, levels, K, r, problem, direct_halos=direct_halos) for r in range(K)]
     return setups, [s.levels for s in setups]
 
 

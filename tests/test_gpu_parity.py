@@ -379,3 +379,44 @@ def test_nccl_transport_selftest(cuda):
     ok = C.c_int(0)
     _lib.check(_lib.lib().pf_nccl_selftest(0, C.byref(ok)))
     assert ok.value == 1
+
+
+@pytest.mark.parametrize("K,L", [(4, 4), (8, 4), (3, 3)])
+@pytest.mark.parametrize("kind", [gmg.PF_SMOOTHER_JACOBI, gmg.PF_SMOOTHER_MULTICOLOR_SOR], ids=["jacobi", "sor"])
+def test_fused_exchanges_bit_exact(cuda, K, L, kind):
+    """Direct halo lists (pf_setup_options.direct_halos) + fused exchanges (one message group
+    per sweep for master/slave + halo1, + halo2 after a smoothing phase): the solve equals
+    the oracle's — and the standard-lists solve — bit for bit, with K subdomains on one
+    device and through the loopback transport (the multi-process code path)."""
+    c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
+    setups, levels = structured(3, 2, L, K, direct_halos=True)
+    xs, resid, ost, rc = Oracle(levels).solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
+    std_setups, std_levels = structured(3, 2, L, K)
+    xstd, _, _, _ = Oracle(std_levels).solve_outer([s.x0 for s in std_setups], [s.b for s in std_setups], c)
+    assert exact(xs, xstd)
+    h = gmg.Hierarchy(levels, fused_exchanges=True)
+    x = upload(h, L - 1, [s.x0 for s in setups])
+    st = gmg.solve_outer(h, x, upload(h, L - 1, [s.b for s in setups]), c)
+    assert st.iterations == ost.iterations
+    assert exact(download(h, x, K), xs)
+    replicas = [s[0] for s in levels]
+    hub = gmg.LoopbackHub(K)
+
+    def body(r):
+        hr = gmg.Hierarchy([levels[r]], rank_base=r, world_size=K, coarse_replicas=replicas, fused_exchanges=True)
+        hr.init_loopback(hub)
+        xr = hr.vector(L - 1, setups[r].x0)
+        str_ = gmg.solve_outer(hr, xr, hr.vector(L - 1, setups[r].b), c)
+        return str_.iterations, xr.download()
+
+    res = _run_ranks(K, body)
+    hub.close()
+    for r in range(K):
+        assert res[r][0] == ost.iterations
+        assert np.array_equal(res[r][1], xs[r]), r
+
+
+def test_fused_exchanges_need_direct_lists(cuda):
+    setups, levels = structured(3, 2, 4, 4)  # standard lists forward Slave-held values
+    with pytest.raises(_lib.InvalidArgument, match="direct_halos"):
+        gmg.Hierarchy(levels, fused_exchanges=True)

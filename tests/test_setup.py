@@ -221,3 +221,36 @@ def test_lognormal_setup_matches_restatement(dim, nc, L, K):
                         continue
                     want = coef.matrix_entry(dim, nc, l, E, local, p, q)
                     assert lv.vals[e] == want, (r, l, p, q, lv.vals[e], want)
+
+
+@pytest.mark.parametrize("dim,nc,L,K", [(3, 2, 4, 4), (3, 2, 4, 8), (2, 4, 3, 6), (3, 3, 3, 5)])
+def test_direct_halo_lists(dim, nc, L, K):
+    """direct_halos: halo requests for a carrier the owner holds as Slave go to its Master.
+    The lists still pair up rank to rank, no halo send entry is a master/slave receive
+    entry (so halo and master/slave scatters can share one message group), every halo copy
+    still has exactly one source, and the master/slave lists are unchanged."""
+    S = [StructuredSetup(dim, nc, L, K, r) for r in range(K)]
+    D = [StructuredSetup(dim, nc, L, K, r, direct_halos=True) for r in range(K)]
+    for l in range(L):
+        for r in range(K):
+            ms_std = [(c.peer, list(c.send), list(c.recv)) for c in S[r].levels[l].channels if c.kind == 0]
+            ms_dir = [(c.peer, list(c.send), list(c.recv)) for c in D[r].levels[l].channels if c.kind == 0]
+            assert ms_std == ms_dir
+            lv = D[r].levels[l]
+            slave = set()
+            for c in lv.channels:
+                if c.kind == 0:
+                    slave.update(int(d) for d in c.recv)
+            for c in lv.channels:
+                if c.kind != 0:
+                    assert not slave.intersection(int(d) for d in c.send), (l, r, c.kind, c.peer)
+                    peer = next(pc for pc in D[c.peer].levels[l].channels if pc.kind == c.kind and pc.peer == r)
+                    assert len(peer.recv) == len(c.send)
+                    keys_send = [tuple(lv.keys[d]) for d in c.send]
+                    keys_recv = [tuple(D[c.peer].levels[l].keys[d]) for d in peer.recv]
+                    assert keys_send == keys_recv
+            # the same halo dofs are received, now possibly from a different peer
+            for kind in (1, 2):
+                a = sorted(int(d) for c in S[r].levels[l].channels if c.kind == kind for d in c.recv)
+                b = sorted(int(d) for c in lv.channels if c.kind == kind for d in c.recv)
+                assert a == b
