@@ -383,7 +383,8 @@ def test_nccl_transport_selftest(cuda):
 
 @pytest.mark.parametrize("K,L", [(4, 4), (8, 4), (3, 3)])
 @pytest.mark.parametrize("kind", [gmg.PF_SMOOTHER_JACOBI, gmg.PF_SMOOTHER_MULTICOLOR_SOR], ids=["jacobi", "sor"])
-def test_fused_exchanges_bit_exact(cuda, K, L, kind):
+@pytest.mark.parametrize("rep", ["coarse", "bottom"])
+def test_fused_exchanges_bit_exact(cuda, K, L, kind, rep):
     """Direct halo lists (pf_setup_options.direct_halos) + fused exchanges (one message group
     per sweep for master/slave + halo1, + halo2 after a smoothing phase): the solve equals
     the oracle's — and the standard-lists solve — bit for bit, with K subdomains on one
@@ -399,7 +400,7 @@ def test_fused_exchanges_bit_exact(cuda, K, L, kind):
     st = gmg.solve_outer(h, x, upload(h, L - 1, [s.b for s in setups]), c)
     assert st.iterations == ost.iterations
     assert exact(download(h, x, K), xs)
-    replicas = [s[0] for s in levels]
+    replicas = [s[0] for s in levels] if rep == "coarse" else [s[:L - 2] for s in levels]
     hub = gmg.LoopbackHub(K)
 
     def body(r):
