@@ -201,6 +201,44 @@ __global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi(SellView A, cons
   x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
 }
 
+// The two halves of a multi-process damped-Jacobi sweep whose exchange overlaps the
+// interior rows (same per-row arithmetic as k_jacobi): the boundary rows from a list plus
+// the carry-over of the non-own rows, then the interior own rows.
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi_boundary(SellView A, const int32_t* __restrict__ list,
+                                                                    int32_t n_list, const double* __restrict__ x_old,
+                                                                    double* __restrict__ x_new,
+                                                                    const double* __restrict__ b, int32_t n_own,
+                                                                    int32_t n, double omega) {
+  PF_PDL_ENTRY();
+  const int32_t nb_blocks = max(1, (n_list + kBlock - 1) / kBlock);
+  if (static_cast<int32_t>(blockIdx.x) >= nb_blocks) {  // non-own rows: carried over
+    const int32_t row = n_own + (static_cast<int32_t>(blockIdx.x) - nb_blocks) * kBlock + threadIdx.x;
+    if (row < n) x_new[row] = x_old[row];
+    return;
+  }
+  const int32_t i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= n_list) return;
+  const int32_t row = list[i];
+  double acc = b[row], diag = 0.0;
+  row_offdiag<true, false, kVK>(A, row, x_old, acc, diag);
+  x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, x_old[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
+}
+
+template <int kVK>
+__global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi_interior(SellView A, const uint8_t* __restrict__ is_b,
+                                                                    const double* __restrict__ x_old,
+                                                                    double* __restrict__ x_new,
+                                                                    const double* __restrict__ b, int32_t n_own,
+                                                                    double omega) {
+  PF_PDL_ENTRY();
+  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  if (row >= n_own || is_b[row]) return;
+  double acc = b[row], diag = 0.0;
+  row_offdiag<true, false, kVK>(A, row, x_old, acc, diag);
+  x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, x_old[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
+}
+
 // State of a device-driven solve_outer (multigrid.cpp:210-246).
 struct SolveState {
   double r0;

@@ -70,13 +70,14 @@ bool pdl_enabled() {
 struct Launcher {
   pf_hierarchy* h;
   int64_t* counter;
+  cudaStream_t stream = nullptr;  // default: the hierarchy's stream
   template <typename... KArgs, typename... Args>
   void operator()(unsigned grid, unsigned block, void (*kern)(KArgs...), Args... args) {
     if (grid == 0) return;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(grid);
     lc.blockDim = dim3(block);
-    lc.stream = h->stream;
+    lc.stream = stream ? stream : h->stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -90,7 +91,9 @@ struct Launcher {
 // While a graph is being captured, kernel launches are counted into the graph entry.
 thread_local int64_t* g_capture_counter = nullptr;
 
-Launcher launcher(pf_hierarchy* h) { return Launcher{h, g_capture_counter ? g_capture_counter : &h->launches}; }
+Launcher launcher(pf_hierarchy* h, cudaStream_t stream = nullptr) {
+  return Launcher{h, g_capture_counter ? g_capture_counter : &h->launches, stream};
+}
 
 SellView view_of(const DevVals& v, const DevSell& s) {
   const void* idx = v.vkind == 1 ? static_cast<const void*>(v.vi8.p)
@@ -542,6 +545,23 @@ void build_fused_plans(pf_hierarchy* h, int l) {
                     "(level " + std::to_string(l) + "): build them with direct_halos");
   }
   const bool local = h->world == h->n_sub;
+  if (!local) {
+    // multi-process: the own rows whose values leave this rank (master/slave and halo
+    // sends) form the boundary set; a Jacobi sweep computes them first, starts the
+    // exchange on the side stream, and sweeps the interior rows meanwhile
+    const HostLevel& H = L.host[0];
+    DevLevel& D = L.sub[0];
+    std::vector<uint8_t> isb(static_cast<size_t>(D.n), 0);
+    for (const HostChannel& c : H.channels)
+      for (int32_t d : c.send)
+        if (d < H.n_own) isb[static_cast<size_t>(D.perm[d])] = 1;
+    std::vector<int32_t> list;
+    for (int32_t r = 0; r < D.n_own; ++r)
+      if (isb[static_cast<size_t>(r)]) list.push_back(r);
+    D.n_brows = static_cast<int32_t>(list.size());
+    D.brows.upload(list);
+    D.is_brow.upload(isb);
+  }
   build_scatter_plan(L.host, L.sub, h->rank_base, local, {PF_CH_MASTER_SLAVE, PF_CH_HALO1}, L.fused_ms_h1);
   build_scatter_plan(L.host, L.sub, h->rank_base, local, {PF_CH_MASTER_SLAVE, PF_CH_HALO1, PF_CH_HALO2},
                      L.fused_all);
@@ -842,12 +862,14 @@ void build_rep_bottom(pf_hierarchy* h) {
 
 // ------------------------------------------------------------------ enqueue --
 
-void enq_plan(pf_hierarchy* h, ExchangePlan& P, double* v);
+void enq_plan(pf_hierarchy* h, ExchangePlan& P, double* v, cudaStream_t st = nullptr);
 
 void enq_scatter(pf_hierarchy* h, int l, int kind, double* v) { enq_plan(h, h->levels[l].scatter[kind], v); }
 
-void enq_plan(pf_hierarchy* h, ExchangePlan& P, double* v) {
-  auto launch = launcher(h);
+// Execute one exchange plan on stream st (default: the hierarchy's stream).
+void enq_plan(pf_hierarchy* h, ExchangePlan& P, double* v, cudaStream_t st) {
+  auto launch = launcher(h, st);
+  if (!st) st = h->stream;
   if (h->world == h->n_sub) {
     if (P.n == 0) return;
     // pack, transport and unpack in one device copy: sends and receives of one
@@ -861,9 +883,9 @@ void enq_plan(pf_hierarchy* h, ExchangePlan& P, double* v) {
   launch(grid_for(P.pack_idx.n), kBlock, k_pack, static_cast<const double*>(v),
          static_cast<const int32_t*>(P.pack_idx.p), P.sendbuf.p, static_cast<int32_t>(P.pack_idx.n));
   h->xport->group_start();
-  for (const PeerSeg& s : P.send_segs) h->xport->send(P.sendbuf.p + s.off, s.len, s.peer, h->stream);
-  for (const PeerSeg& s : P.recv_segs) h->xport->recv(P.recvbuf.p + s.off, s.len, s.peer, h->stream);
-  h->xport->group_end(h->stream);
+  for (const PeerSeg& s : P.send_segs) h->xport->send(P.sendbuf.p + s.off, s.len, s.peer, st);
+  for (const PeerSeg& s : P.recv_segs) h->xport->recv(P.recvbuf.p + s.off, s.len, s.peer, st);
+  h->xport->group_end(st);
   launch(grid_for(P.unpack_idx.n), kBlock, k_unpack, static_cast<const double*>(P.recvbuf.p),
          static_cast<const int32_t*>(P.unpack_idx.p), v, static_cast<int32_t>(P.unpack_idx.n));
 }
@@ -955,8 +977,38 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
   auto launch = launcher(h);
   double* bufs[2] = {xv->cur(), xv->alt()};
   int cur = 0;
+  bool exchanged = false;
   for (int sweep = 0; sweep < sc.sweeps; ++sweep) {
     for (int local = 0; local < sc.local_sweeps; ++local) {
+      const bool overlap = h->fused && h->world > h->n_sub && sc.kind == PF_SMOOTHER_JACOBI &&
+                           local + 1 == sc.local_sweeps && !(first_done && sweep == 0 && local == 0);
+      if (overlap) {
+        // boundary rows (+ the non-own carry-over) first, then the exchange on the side
+        // stream overlapped with the interior rows
+        const DevLevel& D = L.sub[0];
+        const bool last = sweep + 1 == sc.sweeps;
+        vk_dispatch(D.A.vals.vkind, [&](auto V) {
+          constexpr int vk = decltype(V)::value;
+          launch(std::max<unsigned>(grid_for(D.n_brows), 1u) + grid_for(D.n - D.n_own), kBlock, k_jacobi_boundary<vk>,
+                 view(D.A), static_cast<const int32_t*>(D.brows.p), D.n_brows,
+                 static_cast<const double*>(bufs[cur] + D.offset), bufs[cur ^ 1] + D.offset, b + D.offset,
+                 D.n_own, D.n, sc.damping);
+        });
+        PF_CUDA(cudaEventRecord(h->ev_fork, h->stream));
+        PF_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_fork, 0));
+        enq_plan(h, last && then_h2 ? L.fused_all : L.fused_ms_h1, bufs[cur ^ 1], h->comm_stream);
+        vk_dispatch(D.A.vals.vkind, [&](auto V) {
+          constexpr int vk = decltype(V)::value;
+          launch(grid_for(D.n_own), kBlock, k_jacobi_interior<vk>, view(D.A),
+                 static_cast<const uint8_t*>(D.is_brow.p), static_cast<const double*>(bufs[cur] + D.offset),
+                 bufs[cur ^ 1] + D.offset, b + D.offset, D.n_own, sc.damping);
+        });
+        PF_CUDA(cudaEventRecord(h->ev_join, h->comm_stream));
+        PF_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+        cur ^= 1;
+        exchanged = true;
+        continue;
+      }
       if (sc.kind == PF_SMOOTHER_JACOBI) {
         if (!(first_done && sweep == 0 && local == 0))
           for (DevLevel& D : L.sub)
@@ -986,7 +1038,9 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
           }
       }
     }
-    if (h->fused) {
+    if (exchanged) {
+      exchanged = false;  // done by the overlapped sweep
+    } else if (h->fused) {
       const bool last = sweep + 1 == sc.sweeps;
       enq_plan(h, last && then_h2 ? L.fused_all : L.fused_ms_h1, bufs[cur]);
     } else {
@@ -1523,6 +1577,9 @@ pf_hierarchy::~pf_hierarchy() {
   xport.reset();
   if (pinned) cudaFreeHost(pinned);
   if (ev0) cudaEventDestroy(ev0);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (comm_stream) cudaStreamDestroy(comm_stream);
   if (ev1) cudaEventDestroy(ev1);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -1601,6 +1658,9 @@ pf_status pf_hierarchy_create(int device, int n_levels, int n_subdomains, int ra
   h->levels.resize(static_cast<size_t>(n_levels));
   for (auto& L : h->levels) L.host.resize(static_cast<size_t>(n_subdomains));
   PF_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  PF_CUDA(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+  PF_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  PF_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   PF_CUDA(cudaEventCreate(&h->ev0));
   PF_CUDA(cudaEventCreate(&h->ev1));
   PF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->pinned), 64 * sizeof(double)));

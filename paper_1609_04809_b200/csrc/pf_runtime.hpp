@@ -117,6 +117,11 @@ struct DevLevel {
   // restriction to the parent level (rows: parent device rows; columns: this level's
   // device rows), entries in ascending fine host index
   DevSell R;
+  // multi-process fused exchanges: own rows whose values are sent (boundary), as a list and
+  // as a per-row mask (the interior sweep skips them)
+  DevBuf<int32_t> brows;
+  DevBuf<uint8_t> is_brow;
+  int32_t n_brows = 0;
   // residual-norm scratch
   int resnorm_blocks = 0;
   DevBuf<double> partials;
@@ -184,6 +189,8 @@ struct pf_hierarchy {
   bool fused = false;  // master/slave + halo scatters as one message group (direct halo lists)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t comm_stream = nullptr;  // exchanges overlapped with interior sweeps
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<pf::Level> levels;
   pf::DevBuf<double> staging;  // host-order staging for uploads/downloads
   double* pinned = nullptr;    // pinned host slots for scalars read back each cycle
