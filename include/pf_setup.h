@@ -111,6 +111,15 @@ pf_status pf_setup_scales(const pf_setup* s, double t, double* source_scale, int
  * build the setups with PF_PROBLEM_REFERENCE_POISSON for identical files.) */
 pf_status pf_setup_export_matrixmarket(const pf_setup* const* setups, int n_ranks, const char* matrix_path,
                                        const char* rhs_path, int64_t* n_global, int64_t* nnz);
+/* Hands level `level` of a setup to a hierarchy (instead of pf_setup_level +
+ * pf_hierarchy_set_level) by moving its arrays: no second host copy of the matrices, which
+ * is what makes a 512^3 grid fit in host memory.  The setup's level descriptions are
+ * unavailable afterwards (its rhs, keys and device descriptions stay). */
+pf_status pf_hierarchy_set_level_from_setup(pf_hierarchy* h, int level, int subdomain, pf_setup* s);
+/* Frees every level's matrices (CSR, prolongation, rhs operator) once a hierarchy holds
+ * its own copy (after pf_hierarchy_set_level of every level): large grids keep only one
+ * host copy alive.  pf_setup_level fails afterwards; rhs, keys and descriptions stay. */
+pf_status pf_setup_release_matrices(pf_setup* s);
 /* Seconds spent in pf_setup_create. */
 pf_status pf_setup_seconds(const pf_setup* s, double* out);
 

@@ -135,7 +135,8 @@ EXPORTS = [
     "pf_setup_create", "pf_setup_create_heat", "pf_setup_destroy", "pf_setup_level", "pf_setup_level_keys",
     "pf_setup_rhs", "pf_setup_counts", "pf_setup_seconds", "pf_setup_rhs_operator", "pf_setup_load_at",
     "pf_setup_load_desc", "pf_setup_scales", "pf_setup_export_matrixmarket", "pf_setup_create_lognormal",
-    "pf_setup_kappa", "pf_setup_assembly_desc", "pf_setup_create_opts",
+    "pf_setup_kappa", "pf_setup_assembly_desc", "pf_setup_create_opts", "pf_setup_release_matrices",
+    "pf_hierarchy_set_level_from_setup",
 ]
 
 _lib = None
@@ -168,6 +169,8 @@ def lib():
         "pf_nccl_selftest": [C.c_int, C.POINTER(C.c_int)],
         "pf_hierarchy_set_fused_exchanges": [P, C.c_int],
         "pf_setup_create_opts": [C.POINTER(SetupOptions), PP],
+        "pf_setup_release_matrices": [P],
+        "pf_hierarchy_set_level_from_setup": [P, C.c_int, C.c_int, P],
         "pf_hierarchy_set_coarse_replica": [P, C.c_int, C.POINTER(LevelDesc)],
         "pf_hierarchy_set_replica_level": [P, C.c_int, C.c_int, C.POINTER(LevelDesc)],
         "pf_loopback_create": [C.c_int, PP],

@@ -136,23 +136,29 @@ int64_t value_index_min_entries() {
 void encode_values(const std::vector<double>& sv, DevVals& out) {
   out = DevVals{};
   if (value_index_enabled() && static_cast<int64_t>(sv.size()) >= value_index_min_entries()) {
+    // pass 1: the distinct values (first-seen order), giving up past 65,536
     std::unordered_map<uint64_t, uint32_t> ids;
     std::vector<double> table;
-    std::vector<uint32_t> idx(sv.size());
     bool fits = true;
     for (size_t i = 0; i < sv.size(); ++i) {
       uint64_t bits;
       std::memcpy(&bits, &sv[i], sizeof bits);
-      auto it = ids.find(bits);
-      if (it == ids.end()) {
-        if (table.size() == 65536) {
-          fits = false;
-          break;
-        }
-        it = ids.emplace(bits, static_cast<uint32_t>(table.size())).first;
-        table.push_back(sv[i]);
+      if (ids.find(bits) != ids.end()) continue;
+      if (table.size() == 65536) {
+        fits = false;
+        break;
       }
-      idx[i] = it->second;
+      ids.emplace(bits, static_cast<uint32_t>(table.size()));
+      table.push_back(sv[i]);
+    }
+    std::vector<uint32_t> idx;
+    if (fits) {  // pass 2: the indices
+      idx.resize(sv.size());
+      for (size_t i = 0; i < sv.size(); ++i) {
+        uint64_t bits;
+        std::memcpy(&bits, &sv[i], sizeof bits);
+        idx[i] = ids.find(bits)->second;
+      }
     }
     if (fits) {
       out.table.upload(table);
@@ -223,6 +229,44 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
   encode_values(sv, out.vals);
   out.cols.upload(sc);
   out.nnz = n > 0 ? off[n] : 0;
+  out.stored = sptr[n_slices];
+}
+
+// SELL-32x4 of a host CSR whose device row d is host row inv[d] and whose columns map
+// through perm; entry order inside a row preserved.
+void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector<int32_t>& perm,
+                   const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
+                   const std::vector<double>& vals, DevSell& out) {
+  const int64_t n_slices = (n + kSlice - 1) / kSlice;
+  std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
+  std::vector<int32_t> rlen(static_cast<size_t>(std::max<int64_t>(n_slices, 1) * kSlice), 0);
+  for (int32_t d = 0; d < n; ++d) rlen[d] = static_cast<int32_t>(rowptr[inv[d] + 1] - rowptr[inv[d]]);
+  for (int64_t s = 0; s < n_slices; ++s) {
+    int32_t w = 0;
+    for (int l = 0; l < kSlice; ++l) w = std::max(w, rlen[s * kSlice + l]);
+    w = (w + kGroup - 1) / kGroup * kGroup;
+    sptr[s + 1] = sptr[s] + static_cast<int64_t>(w) * kSlice;
+  }
+  // columns, then values, one host array at a time (peak host memory on large grids)
+  {
+    std::vector<int32_t> sc(static_cast<size_t>(sptr[n_slices]), 0);
+    for (int32_t d = 0; d < n; ++d) {
+      const int64_t base = sell_row_base(sptr.data(), d), k0 = rowptr[inv[d]];
+      for (int j = 0; j < rlen[d]; ++j) sc[static_cast<size_t>(sell_entry(base, j))] = perm[cols[static_cast<size_t>(k0 + j)]];
+    }
+    out.cols.upload(sc);
+  }
+  {
+    std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
+    for (int32_t d = 0; d < n; ++d) {
+      const int64_t base = sell_row_base(sptr.data(), d), k0 = rowptr[inv[d]];
+      for (int j = 0; j < rlen[d]; ++j) sv[static_cast<size_t>(sell_entry(base, j))] = vals[static_cast<size_t>(k0 + j)];
+    }
+    encode_values(sv, out.vals);
+  }
+  out.slice_ptr.upload(sptr);
+  out.row_len.upload(rlen);
+  out.nnz = n > 0 ? rowptr[n] : 0;
   out.stored = sptr[n_slices];
 }
 
@@ -302,23 +346,10 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
     for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
   }
   D.d_perm.upload(D.perm);
-  // --- SELL-32 operator: rows in device order, columns mapped, entries in CSR order
-  {
-    std::vector<int64_t> off(static_cast<size_t>(n) + 1, 0);
-    std::vector<int32_t> col;
-    std::vector<double> val;
-    col.reserve(H.cols.size());
-    val.reserve(H.vals.size());
-    for (int32_t d = 0; d < n; ++d) {
-      const int32_t hr = inv[d];
-      for (int64_t k = H.rowptr[hr]; k < H.rowptr[hr + 1]; ++k) {
-        col.push_back(D.perm[H.cols[k]]);
-        val.push_back(H.vals[k]);
-      }
-      off[d + 1] = static_cast<int64_t>(col.size());
-    }
-    sell_from_rows(n, off, col, val, D.A);
-  }
+  // --- SELL-32x4 operator: rows in device order, columns mapped, entries in CSR order,
+  // written straight from the host CSR (no intermediate re-layout: at 512^3 the finest
+  // level alone is 44 GB of host CSR)
+  sell_from_csr(n, inv, D.perm, H.rowptr, H.cols, H.vals, D.A);
   D.A.own_nnz = H.rowptr[n_own];
   D.csr_rowptr = H.rowptr;
   D.sell_ptr.resize(static_cast<size_t>(D.A.slice_ptr.n));
@@ -1678,6 +1709,16 @@ pf_status pf_hierarchy_set_level(pf_hierarchy* h, int level, int sub, const pf_l
   PF_API_END
 }
 
+pf_status pf_hierarchy_set_level_from_setup(pf_hierarchy* h, int level, int sub, pf_setup* s) {
+  PF_API_BEGIN
+  if (!h) invalid("null hierarchy");
+  if (h->finalized) state("hierarchy already finalized");
+  if (level < 0 || level >= h->n_levels) invalid("level out of range");
+  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
+  pf::adopt_setup_level(s, level, h->levels[level].host[sub]);
+  PF_API_END
+}
+
 pf_status pf_hierarchy_set_replica_level(pf_hierarchy* h, int level, int rank, const pf_level_desc* d) {
   PF_API_BEGIN
   if (!h || !d) invalid("null argument");
@@ -1710,6 +1751,10 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
       if (!L.host[s].set)
         state("level " + std::to_string(l) + " subdomain " + std::to_string(s) + " not set");
       build_dev_level(L.host[s], L.sub[s], l);
+      if (l > 0) {  // the operator is on the device; level 0 keeps its CSR for the coarse pack
+        std::vector<int32_t>().swap(L.host[s].cols);
+        std::vector<double>().swap(L.host[s].vals);
+      }
       L.sub[s].offset = off;
       off += L.sub[s].n;
       max_total = std::max<int64_t>(max_total, L.sub[s].n);
@@ -1720,6 +1765,11 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
       for (int s = 0; s < h->n_sub; ++s)
         build_transfer(L.host[s], L.sub[s], h->levels[l - 1].host[s], h->levels[l - 1].sub[s]);
     build_plans(h, l);
+    if (l > 0)  // the prolongation is on the device too
+      for (HostLevel& H : L.host) {
+        std::vector<int32_t>().swap(H.p_col);
+        std::vector<double>().swap(H.p_w);
+      }
     L.r.alloc(std::max<int64_t>(off, 1));
     L.sumsq.alloc(1 + std::max(h->world, h->n_sub));
     L.norm.alloc(1);

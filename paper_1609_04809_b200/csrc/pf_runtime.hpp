@@ -172,6 +172,11 @@ struct Transport;  // pf_nccl.hpp
 
 }  // namespace pf
 
+struct pf_setup;
+namespace pf {
+void adopt_setup_level(pf_setup* s, int level, HostLevel& H);  // pf_setup.cpp
+}  // namespace pf
+
 struct pf_vector {
   pf_hierarchy* h = nullptr;
   int device = 0;  // kept here so destruction never reads the hierarchy

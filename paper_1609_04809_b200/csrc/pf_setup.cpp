@@ -16,6 +16,8 @@
 
 #include <omp.h>
 
+#include "pf_runtime.hpp"
+
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -36,6 +38,7 @@ struct SetupError : std::runtime_error {
   SetupError(pf_status c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 [[noreturn]] void invalid(const std::string& m) { throw SetupError(PF_ERR_INVALID_ARGUMENT, m); }
+[[noreturn]] void state_error(const std::string& m) { throw SetupError(PF_ERR_STATE, m); }
 
 thread_local std::string g_setup_err;
 
@@ -506,6 +509,7 @@ struct pf_setup {
   // device assembly description of the finest level (pf_assembly_desc)
   std::vector<double> asm_elem;
   std::vector<int32_t> asm_hid;
+  bool matrices_released = false;  // pf_setup_release_matrices
   double seconds = 0;
 };
 
@@ -1280,6 +1284,7 @@ pf_status pf_setup_level(const pf_setup* s, int level, pf_level_desc* out) {
   return guard([&] {
     if (!s || !out) invalid("null argument");
     if (level < 0 || level >= s->n_levels) invalid("level out of range");
+    if (s->matrices_released) state_error("level matrices released (pf_setup_release_matrices)");
     const SetupLevel& L = *s->levels[static_cast<size_t>(level)];
     std::memset(out, 0, sizeof *out);
     out->n_dofs = L.n;
@@ -1502,6 +1507,68 @@ pf_status pf_setup_export_matrixmarket(const pf_setup* const* setups, int n_rank
     if (nnz) *nnz = total_nnz;
   });
 }
+
+pf_status pf_setup_release_matrices(pf_setup* s) {
+  return guard([&] {
+    if (!s) invalid("null setup");
+    for (auto& L : s->levels) {
+      std::vector<int64_t>().swap(L->rowptr);
+      std::vector<int32_t>().swap(L->cols);
+      std::vector<double>().swap(L->vals);
+      std::vector<int64_t>().swap(L->p_off);
+      std::vector<int32_t>().swap(L->p_col);
+      std::vector<double>().swap(L->p_w);
+    }
+    std::vector<double>().swap(s->rhs_op);
+    s->matrices_released = true;
+  });
+}
+
+}  // extern "C"
+
+namespace pf {
+
+// Hand one level of a setup to a hierarchy by moving its arrays (no second host copy of
+// the matrices; pf_hierarchy_set_level_from_setup).  The setup's matrices of that level
+// are gone afterwards.
+void adopt_setup_level(pf_setup* s, int level, HostLevel& H) {
+  if (!s) throw Error(PF_ERR_INVALID_ARGUMENT, "null setup");
+  if (level < 0 || level >= s->n_levels) throw Error(PF_ERR_INVALID_ARGUMENT, "level out of range");
+  SetupLevel& L = *s->levels[static_cast<size_t>(level)];
+  if (L.rowptr.empty()) throw Error(PF_ERR_STATE, "level matrices already released or adopted");
+  H = HostLevel{};
+  H.set = true;
+  H.n = L.n;
+  H.n_own = L.n_own;
+  H.rowptr = std::move(L.rowptr);
+  H.cols = std::move(L.cols);
+  H.vals = std::move(L.vals);
+  H.owns_row = L.owns_row;
+  H.is_dir = L.is_dir;
+  H.color = L.color;
+  H.order = L.vert;  // lexicographic lattice index: the device placement hint
+  for (const OwnedChannel& c : L.channels) {
+    HostChannel hc;
+    hc.kind = c.kind;
+    hc.peer = c.peer;
+    hc.send = c.send;
+    hc.recv = c.recv;
+    H.channels.push_back(std::move(hc));
+  }
+  std::sort(H.channels.begin(), H.channels.end(), [](const HostChannel& a, const HostChannel& b) {
+    return a.kind != b.kind ? a.kind < b.kind : a.peer < b.peer;
+  });
+  if (level > 0) {
+    H.p_off = std::move(L.p_off);
+    H.p_col = std::move(L.p_col);
+    H.p_w = std::move(L.p_w);
+  }
+  s->matrices_released = true;  // pf_setup_level no longer describes this setup
+}
+
+}  // namespace pf
+
+extern "C" {
 
 pf_status pf_setup_seconds(const pf_setup* s, double* out) {
   return guard([&] {

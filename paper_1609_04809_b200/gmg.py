@@ -177,6 +177,35 @@ class Hierarchy:
         if finalize:
             self.finalize()
 
+    @classmethod
+    def from_setups(cls, setups, device: int = 0, rank_base: int = 0, world_size: int | None = None,
+                    coarse_replicas=None, fused_exchanges: bool = False) -> "Hierarchy":
+        """A hierarchy straight from native StructuredSetups (materialize=False): the level
+        arrays move from each setup into the hierarchy and on to the device, without numpy
+        copies or a second host copy (large grids: 512^3 fits in host memory)."""
+        self = cls.__new__(cls)
+        L = _lib.lib()
+        n_sub, n_levels = len(setups), setups[0].n_levels
+        world = n_sub if world_size is None else world_size
+        self._h = C.c_void_p()
+        self._vectors = weakref.WeakSet()
+        _lib.check(L.pf_hierarchy_create(device, n_levels, n_sub, rank_base, world, C.byref(self._h)))
+        self.n_levels, self.n_sub, self.rank_base, self.world = n_levels, n_sub, rank_base, world
+        self._sizes = [list(s.sizes) for s in setups]
+        for si, s in enumerate(setups):
+            for l in range(n_levels):  # the arrays move from the setup: one host copy
+                _lib.check(L.pf_hierarchy_set_level_from_setup(self._h, l, si, s._live()))
+        if coarse_replicas is not None:
+            for r, lvs in enumerate(coarse_replicas):
+                for l, lv in enumerate(lvs if isinstance(lvs, (list, tuple)) else [lvs]):
+                    d, keep = lv.desc()
+                    _lib.check(L.pf_hierarchy_set_replica_level(self._h, l, r, C.byref(d)))
+                    del keep
+        if fused_exchanges:
+            _lib.check(L.pf_hierarchy_set_fused_exchanges(self._h, 1))
+        self.finalize()
+        return self
+
     def finalize(self):
         _lib.check(_lib.lib().pf_hierarchy_finalize(self._h))
 

@@ -83,7 +83,7 @@ class StructuredSetup:
 
     def __init__(self, dim: int, n_coarse: int, n_levels: int, n_ranks: int = 1, rank: int = 0,
                  problem: int = _lib.PF_PROBLEM_BASELINE, dt: float | None = None, keep: bool = False,
-                 seed: int = 1, direct_halos: bool = False):
+                 seed: int = 1, direct_halos: bool = False, materialize: bool = True):
         L = _lib.lib()
         self._h = C.c_void_p()
         if direct_halos:
@@ -104,7 +104,14 @@ class StructuredSetup:
         self.dt = dt if problem == _lib.PF_PROBLEM_HEAT else None
         if problem == _lib.PF_PROBLEM_HEAT and dt is None:
             self.dt = 0.01
-        self.levels = [self._level(l) for l in range(n_levels)]
+        # materialize=False: no numpy copies of the level data (large grids); the native
+        # setup stays alive and gmg.Hierarchy.from_setups reads it directly
+        self.levels = [self._level(l) for l in range(n_levels)] if materialize else None
+        self.sizes = []
+        for l in range(n_levels):
+            nd = C.c_int64()
+            _lib.check(L.pf_setup_counts(self._h, l, None, C.byref(nd), None, None), setup=True)
+            self.sizes.append(nd.value)
         bp, xp, n = C.c_void_p(), C.c_void_p(), C.c_int64()
         _lib.check(L.pf_setup_rhs(self._h, C.byref(bp), C.byref(xp), C.byref(n)), setup=True)
         self.b = _arr(bp, n.value, C.c_double, np.float64)
@@ -125,7 +132,7 @@ class StructuredSetup:
             vp, nnz = C.c_void_p(), C.c_int64()
             _lib.check(L.pf_setup_rhs_operator(self._h, C.byref(vp), C.byref(nnz)), setup=True)
             self.rhs_op = _arr(vp, nnz.value, C.c_double, np.float64)
-        elif not keep:
+        elif not keep and materialize:
             self.close()
 
     def close(self):
@@ -144,10 +151,20 @@ class StructuredSetup:
             raise _lib.PfError("native setup released (heat setups, or keep=True, keep it)")
         return self._h
 
+    def level_desc(self, l: int) -> _lib.LevelDesc:
+        """Level l as the native setup holds it (pointers valid while this setup lives and
+        until release_matrices)."""
+        d = _lib.LevelDesc()
+        _lib.check(_lib.lib().pf_setup_level(self._live(), l, C.byref(d)), setup=True)
+        return d
+
+    def release_matrices(self):
+        _lib.check(_lib.lib().pf_setup_release_matrices(self._live()), setup=True)
+
     def load_at(self, t: float) -> np.ndarray:
         """Finest-level load at time t (assemble_load, assembly.cpp:144-160), host order,
         Dirichlet rows 0."""
-        out = np.zeros(self.levels[-1].n)
+        out = np.zeros(self.sizes[-1])
         _lib.check(_lib.lib().pf_setup_load_at(self._live(), t, out.ctypes.data, out.size), setup=True)
         return out
 

@@ -421,3 +421,21 @@ def test_fused_exchanges_need_direct_lists(cuda):
     setups, levels = structured(3, 2, 4, 4)  # standard lists forward Slave-held values
     with pytest.raises(_lib.InvalidArgument, match="direct_halos"):
         gmg.Hierarchy(levels, fused_exchanges=True)
+
+
+def test_hierarchy_from_native_setups(cuda):
+    """Hierarchy.from_setups (no numpy copies; the setups' matrices released after the
+    upload — the large-grid path) solves exactly like the materialized path."""
+    K, L = 2, 4
+    setups, levels = structured(3, 2, L, K)
+    h = gmg.Hierarchy(levels)
+    x = upload(h, L - 1, [s.x0 for s in setups])
+    st = gmg.solve_outer(h, x, upload(h, L - 1, [s.b for s in setups]), cfg())
+    native = [StructuredSetup(3, 2, L, K, r, materialize=False) for r in range(K)]
+    hn = gmg.Hierarchy.from_setups(native)
+    xn = upload(hn, L - 1, [s.x0 for s in native])
+    stn = gmg.solve_outer(hn, xn, upload(hn, L - 1, [s.b for s in native]), cfg())
+    assert stn.iterations == st.iterations and list(stn.residuals) == list(st.residuals)
+    assert exact(download(hn, xn, K), download(h, x, K))
+    with pytest.raises(_lib.PfError):
+        native[0].level_desc(0)  # released
