@@ -27,6 +27,8 @@ PF_UPDATE_SCATTER, PF_UPDATE_ACCUMULATE_THEN_SCATTER = 0, 1
 PF_SMOOTHER_JACOBI, PF_SMOOTHER_GAUSS_SEIDEL, PF_SMOOTHER_MULTICOLOR_SOR = 0, 1, 2
 PF_PROBLEM_BASELINE, PF_PROBLEM_REFERENCE_POISSON, PF_PROBLEM_UNIT_SOURCE, PF_PROBLEM_HEAT = 0, 1, 2, 3
 PF_PROBLEM_LOGNORMAL = 4
+PF_FE_Q2, PF_FE_ROTATED_Q1 = 2, 3
+PF_COEF_CONSTANT, PF_COEF_LOGNORMAL = 0, 1
 
 
 class PfError(RuntimeError):
@@ -137,6 +139,8 @@ EXPORTS = [
     "pf_setup_load_desc", "pf_setup_scales", "pf_setup_export_matrixmarket", "pf_setup_create_lognormal",
     "pf_setup_kappa", "pf_setup_assembly_desc", "pf_setup_create_opts", "pf_setup_release_matrices",
     "pf_hierarchy_set_level_from_setup",
+    "pf_fe_setup_create", "pf_fe_setup_destroy", "pf_fe_setup_level", "pf_fe_setup_level_keys",
+    "pf_fe_setup_rhs", "pf_fe_setup_kappa", "pf_fe_setup_seconds",
 ]
 
 _lib = None
@@ -157,6 +161,7 @@ def lib():
     L.pf_last_error.restype = C.c_char_p
     L.pf_version.restype = C.c_char_p
     L.pf_setup_last_error.restype = C.c_char_p
+    L.pf_fe_last_error.restype = C.c_char_p
     L.pf_default_smoother_config.argtypes = [C.POINTER(SmootherConfig)]
     L.pf_default_multigrid_config.argtypes = [C.POINTER(MultigridConfig)]
     sigs = {
@@ -240,6 +245,13 @@ def lib():
         "pf_setup_rhs": [P, PP, PP, i64p],
         "pf_setup_counts": [P, C.c_int, i64p, i64p, i64p, i64p],
         "pf_setup_seconds": [P, dp],
+        "pf_fe_setup_create": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, PP],
+        "pf_fe_setup_destroy": [P],
+        "pf_fe_setup_level": [P, C.c_int, C.POINTER(LevelDesc)],
+        "pf_fe_setup_level_keys": [P, C.c_int, PP, PP],
+        "pf_fe_setup_rhs": [P, PP, PP, PP, i64p],
+        "pf_fe_setup_kappa": [P, PP, i64p],
+        "pf_fe_setup_seconds": [P, dp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -249,9 +261,10 @@ def lib():
     return L
 
 
-def check(rc: int, setup: bool = False) -> None:
+def check(rc: int, setup: bool | str = False) -> None:
     if rc == PF_OK:
         return
     L = lib()
-    msg = (L.pf_setup_last_error() if setup else L.pf_last_error()).decode()
+    msg = (L.pf_fe_last_error() if setup == "fe" else L.pf_setup_last_error() if setup
+           else L.pf_last_error()).decode()
     raise _ERRORS.get(rc, PfError)(msg)

@@ -1,0 +1,808 @@
+// pf_fe_setup.cpp — Q2 and rotated-Q1 (Rannacher-Turek) hierarchies for the V-cycle
+// (include/pf_fe.h; BASELINE configs[2] and configs[3]).
+//
+// Both families follow the reference's Q1 pipeline step for step:
+//   element matrices by tensor Gauss quadrature         assembly.cpp:48-88
+//   global sums over the cells of an entry in ascending cell order  assembly.cpp:90-142
+//   Dirichlet rows kept with identity values            assembly.cpp:162-170
+//   the load by the same quadrature, own cells only     assembly.cpp:144-160
+//   prolongation as (coarse dof, weight) lists per fine dof         multigrid.cpp:35-72
+// and every floating-point expression is written out so that the numpy restatement
+// (oracle/fe_restated.py) reproduces it bit for bit.  One subdomain; rows are built in
+// parallel (each row's sums are serial, so the result does not depend on the threads).
+#include "pf_fe.h"
+
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "pf_coef.hpp"
+
+namespace {
+
+struct FeError : std::runtime_error {
+  pf_status code;
+  FeError(pf_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void invalid(const std::string& m) { throw FeError(PF_ERR_INVALID_ARGUMENT, m); }
+
+thread_local std::string g_fe_err;
+
+const double kPi = std::acos(-1.0);
+constexpr uint8_t kIndep = 1, kDirichlet = 7;  // DofClass (femapper.hpp:16-25)
+
+// Gauss-Legendre rules on [0, 1]
+struct Rule {
+  int n;
+  double t[3], w[3];
+};
+Rule gauss2() {
+  const double r = 0.5 / std::sqrt(3.0);
+  return {2, {0.5 - r, 0.5 + r, 0.0}, {0.5, 0.5, 0.0}};
+}
+Rule gauss3() {
+  const double r = 0.5 * std::sqrt(0.6);
+  return {3, {0.5 - r, 0.5, 0.5 + r}, {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0}};
+}
+
+}  // namespace
+
+struct FeLevel {
+  int64_t N = 0;  // cells per axis
+  int32_t n = 0, n_own = 0;
+  std::vector<int64_t> rowptr;
+  std::vector<int32_t> cols;
+  std::vector<double> vals;
+  std::vector<uint8_t> owns_row, is_dir, class_of;
+  std::vector<int32_t> color;
+  std::vector<int64_t> order, keys;  // keys: 4 per dof
+  std::vector<int64_t> p_off;
+  std::vector<int32_t> p_col;
+  std::vector<double> p_w;
+  // lexicographic entity index <-> host index
+  std::vector<int32_t> host_of;
+  std::vector<int64_t> lex_of;
+};
+
+struct pf_fe_setup {
+  int family = 0, n_coarse = 2, n_levels = 1, coefficient = 0;
+  uint64_t seed = 0;
+  std::vector<std::unique_ptr<FeLevel>> levels;
+  std::vector<double> b, x0, exact, kappa;
+  double seconds = 0;
+};
+
+namespace {
+
+// Host order: own entities (interior) first, then Dirichlet ones, each lexicographic.
+void number(FeLevel& L, int64_t n_lex, const std::vector<uint8_t>& boundary) {
+  L.host_of.assign(static_cast<size_t>(n_lex), 0);
+  L.lex_of.assign(static_cast<size_t>(n_lex), 0);
+  int64_t own = 0;
+  for (int64_t e = 0; e < n_lex; ++e) own += boundary[static_cast<size_t>(e)] ? 0 : 1;
+  int64_t a = 0, d = own;
+  for (int64_t e = 0; e < n_lex; ++e) {
+    const int64_t h = boundary[static_cast<size_t>(e)] ? d++ : a++;
+    L.host_of[static_cast<size_t>(e)] = static_cast<int32_t>(h);
+    L.lex_of[static_cast<size_t>(h)] = e;
+  }
+  if (n_lex > INT32_MAX) invalid("level too large for int32 dof indices");
+  L.n = static_cast<int32_t>(n_lex);
+  L.n_own = static_cast<int32_t>(own);
+  L.owns_row.assign(static_cast<size_t>(n_lex), 1);  // one subdomain: every row is authoritative
+  L.is_dir.assign(static_cast<size_t>(n_lex), 0);
+  L.class_of.assign(static_cast<size_t>(n_lex), kIndep);
+  for (int64_t h = own; h < n_lex; ++h) {
+    L.is_dir[static_cast<size_t>(h)] = 1;
+    L.class_of[static_cast<size_t>(h)] = kDirichlet;
+  }
+  L.order.assign(L.lex_of.begin(), L.lex_of.end());
+}
+
+// Rows as (column, value) lists sorted by host column; row_fn(h, out) appends a row.
+template <typename RowFn>
+void build_csr(FeLevel& L, RowFn row_fn) {
+  const int64_t n = L.n;
+  std::vector<int32_t> len(static_cast<size_t>(n), 0);
+#pragma omp parallel
+  {
+    std::vector<std::pair<int32_t, double>> row;
+#pragma omp for schedule(static)
+    for (int64_t h = 0; h < n; ++h) {
+      row.clear();
+      row_fn(h, row, /*values=*/false);
+      len[static_cast<size_t>(h)] = static_cast<int32_t>(row.size());
+    }
+  }
+  L.rowptr.assign(static_cast<size_t>(n) + 1, 0);
+  for (int64_t h = 0; h < n; ++h) L.rowptr[static_cast<size_t>(h) + 1] = L.rowptr[static_cast<size_t>(h)] + len[static_cast<size_t>(h)];
+  L.cols.resize(static_cast<size_t>(L.rowptr.back()));
+  L.vals.resize(static_cast<size_t>(L.rowptr.back()));
+#pragma omp parallel
+  {
+    std::vector<std::pair<int32_t, double>> row;
+#pragma omp for schedule(static)
+    for (int64_t h = 0; h < n; ++h) {
+      row.clear();
+      row_fn(h, row, /*values=*/true);
+      std::sort(row.begin(), row.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+      int64_t k = L.rowptr[static_cast<size_t>(h)];
+      for (const auto& [c, v] : row) {
+        L.cols[static_cast<size_t>(k)] = c;
+        L.vals[static_cast<size_t>(k)] = v;
+        ++k;
+      }
+    }
+  }
+}
+
+template <typename RowFn>
+void build_p(FeLevel& L, RowFn row_fn) {
+  const int64_t n = L.n;
+  std::vector<int32_t> len(static_cast<size_t>(n), 0);
+  std::vector<std::vector<std::pair<int32_t, double>>> rows(static_cast<size_t>(omp_get_max_threads()));
+#pragma omp parallel for schedule(static)
+  for (int64_t h = 0; h < n; ++h) {
+    auto& row = rows[static_cast<size_t>(omp_get_thread_num())];
+    row.clear();
+    row_fn(h, row);
+    len[static_cast<size_t>(h)] = static_cast<int32_t>(row.size());
+  }
+  L.p_off.assign(static_cast<size_t>(n) + 1, 0);
+  for (int64_t h = 0; h < n; ++h) L.p_off[static_cast<size_t>(h) + 1] = L.p_off[static_cast<size_t>(h)] + len[static_cast<size_t>(h)];
+  L.p_col.resize(static_cast<size_t>(L.p_off.back()));
+  L.p_w.resize(static_cast<size_t>(L.p_off.back()));
+#pragma omp parallel for schedule(static)
+  for (int64_t h = 0; h < n; ++h) {
+    auto& row = rows[static_cast<size_t>(omp_get_thread_num())];
+    row.clear();
+    row_fn(h, row);
+    std::sort(row.begin(), row.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    int64_t k = L.p_off[static_cast<size_t>(h)];
+    for (const auto& [c, w] : row) {
+      L.p_col[static_cast<size_t>(k)] = c;
+      L.p_w[static_cast<size_t>(k)] = w;
+      ++k;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ Q2 --
+
+// 1D Q2 basis on [0, 1] (nodes 0, 1/2, 1) and its derivative
+double q2_phi(int i, double t) {
+  return i == 0 ? (1.0 - t) * (1.0 - 2.0 * t) : i == 1 ? (4.0 * t) * (1.0 - t) : t * (2.0 * t - 1.0);
+}
+double q2_dphi(int i, double t) { return i == 0 ? 4.0 * t - 3.0 : i == 1 ? 4.0 - 8.0 * t : 4.0 * t - 1.0; }
+
+// Stiffness of the unit cube, 27 x 27, local node a = (ax * 3 + ay) * 3 + az.
+std::vector<double> q2_kref() {
+  const Rule g = gauss3();
+  double V[3][3], D[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int q = 0; q < 3; ++q) {
+      V[i][q] = q2_phi(i, g.t[q]);
+      D[i][q] = q2_dphi(i, g.t[q]);
+    }
+  std::vector<double> K(27 * 27, 0.0);
+  for (int a = 0; a < 27; ++a)
+    for (int b = 0; b < 27; ++b) {
+      const int ax = a / 9, ay = (a / 3) % 3, az = a % 3, bx = b / 9, by = (b / 3) % 3, bz = b % 3;
+      double s = 0.0;
+      for (int qx = 0; qx < 3; ++qx)
+        for (int qy = 0; qy < 3; ++qy)
+          for (int qz = 0; qz < 3; ++qz) {
+            const double w = (g.w[qx] * g.w[qy]) * g.w[qz];
+            const double ga0 = (D[ax][qx] * V[ay][qy]) * V[az][qz], gb0 = (D[bx][qx] * V[by][qy]) * V[bz][qz];
+            const double ga1 = (V[ax][qx] * D[ay][qy]) * V[az][qz], gb1 = (V[bx][qx] * D[by][qy]) * V[bz][qz];
+            const double ga2 = (V[ax][qx] * V[ay][qy]) * D[az][qz], gb2 = (V[bx][qx] * V[by][qy]) * D[bz][qz];
+            s += w * ((ga0 * gb0 + ga1 * gb1) + ga2 * gb2);
+          }
+      K[static_cast<size_t>(a * 27 + b)] = s;
+    }
+  return K;
+}
+
+// cells along one axis containing node i (at most 2, ascending)
+int q2_cells(int64_t i, int64_t N, int64_t* out) {
+  if (i & 1) {
+    out[0] = (i - 1) / 2;
+    return 1;
+  }
+  int n = 0;
+  if (i / 2 - 1 >= 0) out[n++] = i / 2 - 1;
+  if (i / 2 < N) out[n++] = i / 2;
+  return n;
+}
+
+// nodes along one axis sharing a cell with node i
+int q2_nbrs(int64_t i, int64_t M, int64_t* out) {
+  int n = 0;
+  const int64_t r = (i & 1) ? 1 : 2;
+  for (int64_t j = i - r; j <= i + r; ++j)
+    if (j >= 0 && j < M) out[n++] = j;
+  return n;
+}
+
+void q2_level(FeLevel& L, int64_t N, const std::vector<double>& Ke) {
+  const int64_t M = 2 * N + 1;
+  L.N = N;
+  std::vector<uint8_t> bnd(static_cast<size_t>(M * M * M));
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t j = 0; j < M; ++j)
+      for (int64_t k = 0; k < M; ++k)
+        bnd[static_cast<size_t>((i * M + j) * M + k)] =
+            (i == 0 || j == 0 || k == 0 || i == M - 1 || j == M - 1 || k == M - 1) ? 1 : 0;
+  number(L, M * M * M, bnd);
+  L.keys.resize(static_cast<size_t>(L.n) * 4);
+  L.color.resize(static_cast<size_t>(L.n_own));
+  auto cls = [](int64_t i) { return (i & 1) ? 2 : ((i & 3) == 0 ? 0 : 1); };
+  for (int64_t h = 0; h < L.n; ++h) {
+    const int64_t e = L.lex_of[static_cast<size_t>(h)];
+    const int64_t i = e / (M * M), j = (e / M) % M, k = e % M;
+    int64_t* key = &L.keys[static_cast<size_t>(h) * 4];
+    key[0] = 0;
+    key[1] = i;
+    key[2] = j;
+    key[3] = k;
+    if (h < L.n_own) L.color[static_cast<size_t>(h)] = (cls(i) * 3 + cls(j)) * 3 + cls(k);
+  }
+  build_csr(L, [&](int64_t h, std::vector<std::pair<int32_t, double>>& row, bool values) {
+    const int64_t e = L.lex_of[static_cast<size_t>(h)];
+    const int64_t p[3] = {e / (M * M), (e / M) % M, e % M};
+    int64_t nb[3][5];
+    int nn[3];
+    for (int a = 0; a < 3; ++a) nn[a] = q2_nbrs(p[a], M, nb[a]);
+    const bool dir = h >= L.n_own;
+    int64_t pc[3][2];
+    int npc[3];
+    for (int a = 0; a < 3; ++a) npc[a] = q2_cells(p[a], N, pc[a]);
+    for (int x = 0; x < nn[0]; ++x)
+      for (int y = 0; y < nn[1]; ++y)
+        for (int z = 0; z < nn[2]; ++z) {
+          const int64_t c[3] = {nb[0][x], nb[1][y], nb[2][z]};
+          const int32_t col = L.host_of[static_cast<size_t>((c[0] * M + c[1]) * M + c[2])];
+          double v = 0.0;
+          if (values) {
+            if (dir) {
+              v = col == h ? 1.0 : 0.0;
+            } else {
+              // cells containing both nodes, per axis, ascending -> ascending cell order
+              int64_t sc[3][2];
+              int ns[3];
+              for (int a = 0; a < 3; ++a) {
+                int64_t qc[2];
+                const int nq = q2_cells(c[a], N, qc);
+                ns[a] = 0;
+                for (int u = 0; u < npc[a]; ++u)
+                  for (int w = 0; w < nq; ++w)
+                    if (pc[a][u] == qc[w]) sc[a][ns[a]++] = pc[a][u];
+              }
+              for (int u = 0; u < ns[0]; ++u)
+                for (int w = 0; w < ns[1]; ++w)
+                  for (int t = 0; t < ns[2]; ++t) {
+                    const int64_t cc[3] = {sc[0][u], sc[1][w], sc[2][t]};
+                    const int la = static_cast<int>(((p[0] - 2 * cc[0]) * 3 + (p[1] - 2 * cc[1])) * 3 + (p[2] - 2 * cc[2]));
+                    const int lb = static_cast<int>(((c[0] - 2 * cc[0]) * 3 + (c[1] - 2 * cc[1])) * 3 + (c[2] - 2 * cc[2]));
+                    v += Ke[static_cast<size_t>(la * 27 + lb)];
+                  }
+            }
+          }
+          row.emplace_back(col, v);
+        }
+  });
+}
+
+// (coarse index, weight) of fine node i along one axis
+int q2_pw(int64_t i, int64_t* c, double* w) {
+  if ((i & 1) == 0) {
+    c[0] = i / 2;
+    w[0] = 1.0;
+    return 1;
+  }
+  const int64_t cell = i / 4;
+  const bool first = (i & 3) == 1;
+  c[0] = 2 * cell;
+  c[1] = 2 * cell + 1;
+  c[2] = 2 * cell + 2;
+  w[0] = first ? 0.375 : -0.125;
+  w[1] = 0.75;
+  w[2] = first ? -0.125 : 0.375;
+  return 3;
+}
+
+void q2_prolongation(FeLevel& F, const FeLevel& Cl) {
+  const int64_t Mf = 2 * F.N + 1, Mc = 2 * Cl.N + 1;
+  build_p(F, [&](int64_t h, std::vector<std::pair<int32_t, double>>& row) {
+    const int64_t e = F.lex_of[static_cast<size_t>(h)];
+    const int64_t p[3] = {e / (Mf * Mf), (e / Mf) % Mf, e % Mf};
+    int64_t c[3][3];
+    double w[3][3];
+    int n[3];
+    for (int a = 0; a < 3; ++a) n[a] = q2_pw(p[a], c[a], w[a]);
+    for (int x = 0; x < n[0]; ++x)
+      for (int y = 0; y < n[1]; ++y)
+        for (int z = 0; z < n[2]; ++z)
+          row.emplace_back(Cl.host_of[static_cast<size_t>((c[0][x] * Mc + c[1][y]) * Mc + c[2][z])],
+                           (w[0][x] * w[1][y]) * w[2][z]);
+  });
+}
+
+void q2_rhs(pf_fe_setup& s) {
+  const FeLevel& L = *s.levels.back();
+  const int64_t N = L.N, M = 2 * N + 1;
+  const Rule g = gauss3();
+  const double h = 1.0 / static_cast<double>(N);
+  const double vol = (h * h) * h, K3 = (3.0 * kPi) * kPi;
+  // sin(pi x) at the Gauss points of every cell interval
+  std::vector<double> S(static_cast<size_t>(N * 3));
+  for (int64_t c = 0; c < N; ++c)
+    for (int q = 0; q < 3; ++q) S[static_cast<size_t>(c * 3 + q)] = std::sin(kPi * ((static_cast<double>(c) + g.t[q]) * h));
+  double V[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int q = 0; q < 3; ++q) V[i][q] = q2_phi(i, g.t[q]);
+  std::vector<double> le(static_cast<size_t>(N * N * N * 27));
+#pragma omp parallel for schedule(static)
+  for (int64_t cell = 0; cell < N * N * N; ++cell) {
+    const int64_t cx = cell / (N * N), cy = (cell / N) % N, cz = cell % N;
+    double* out = &le[static_cast<size_t>(cell * 27)];
+    for (int a = 0; a < 27; ++a) out[a] = 0.0;
+    for (int qx = 0; qx < 3; ++qx)
+      for (int qy = 0; qy < 3; ++qy)
+        for (int qz = 0; qz < 3; ++qz) {
+          const double w = (g.w[qx] * g.w[qy]) * g.w[qz];
+          const double f = ((K3 * S[static_cast<size_t>(cx * 3 + qx)]) * S[static_cast<size_t>(cy * 3 + qy)]) *
+                           S[static_cast<size_t>(cz * 3 + qz)];
+          const double wf = (w * vol) * f;
+          for (int a = 0; a < 27; ++a) out[a] += wf * ((V[a / 9][qx] * V[(a / 3) % 3][qy]) * V[a % 3][qz]);
+        }
+  }
+  s.b.assign(static_cast<size_t>(L.n), 0.0);
+  s.x0.assign(static_cast<size_t>(L.n), 0.0);
+  s.exact.assign(static_cast<size_t>(L.n), 0.0);
+#pragma omp parallel for schedule(static)
+  for (int64_t hh = 0; hh < L.n; ++hh) {
+    const int64_t e = L.lex_of[static_cast<size_t>(hh)];
+    const int64_t p[3] = {e / (M * M), (e / M) % M, e % M};
+    double u = 1.0;
+    for (int a = 0; a < 3; ++a) u *= std::sin(kPi * (static_cast<double>(p[a]) / static_cast<double>(2 * N)));
+    s.exact[static_cast<size_t>(hh)] = u;
+    if (hh >= L.n_own) continue;
+    int64_t pc[3][2];
+    int np[3];
+    for (int a = 0; a < 3; ++a) np[a] = q2_cells(p[a], N, pc[a]);
+    double acc = 0.0;
+    for (int x = 0; x < np[0]; ++x)
+      for (int y = 0; y < np[1]; ++y)
+        for (int z = 0; z < np[2]; ++z) {
+          const int64_t cell = (pc[0][x] * N + pc[1][y]) * N + pc[2][z];
+          const int la = static_cast<int>(((p[0] - 2 * pc[0][x]) * 3 + (p[1] - 2 * pc[1][y])) * 3 + (p[2] - 2 * pc[2][z]));
+          acc += le[static_cast<size_t>(cell * 27 + la)];
+        }
+    s.b[static_cast<size_t>(hh)] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- rotated Q1 --
+
+// Face entity (o, a0, a1, a2): a_o in [0, N], the others in [0, N).
+struct Faces {
+  int64_t N, per;  // per orientation: N^2 (N + 1)
+  int64_t lex(int o, const int64_t* a) const {
+    const int64_t e1 = N + (o == 1), e2 = N + (o == 2);
+    return o * per + (a[0] * e1 + a[1]) * e2 + a[2];
+  }
+  void unlex(int64_t e, int* o, int64_t* a) const {
+    *o = static_cast<int>(e / per);
+    const int64_t r = e % per, e1 = N + (*o == 1), e2 = N + (*o == 2);
+    a[0] = r / (e1 * e2);
+    a[1] = (r / e2) % e1;
+    a[2] = r % e2;
+  }
+};
+
+// basis of the face (o, sigma) on the unit cube in X = 2 t - 1 coordinates:
+//   phi = 1/6 + sigma X_o / 2 + (2 X_o^2 - X_p^2 - X_q^2) / 4     (p < q the other axes)
+double rt_phi(int o, double sigma, const double* X) {
+  const int p = o == 0 ? 1 : 0, q = o == 2 ? 1 : 2;
+  return (1.0 / 6.0 + (0.5 * sigma) * X[o]) + 0.25 * ((2.0 * X[o] * X[o] - X[p] * X[p]) - X[q] * X[q]);
+}
+// its gradient in t: d/dt_o = sigma + 2 X_o, d/dt_p = -X_p
+void rt_grad(int o, double sigma, const double* X, double* g) {
+  for (int a = 0; a < 3; ++a) g[a] = a == o ? sigma + 2.0 * X[a] : -X[a];
+}
+
+// Stiffness of the unit cube, 6 x 6, local face s = 2 o + (sigma > 0).
+std::vector<double> rt_kref() {
+  const Rule g = gauss2();
+  std::vector<double> K(36, 0.0);
+  for (int a = 0; a < 6; ++a)
+    for (int b = 0; b < 6; ++b) {
+      double s = 0.0;
+      for (int qx = 0; qx < 2; ++qx)
+        for (int qy = 0; qy < 2; ++qy)
+          for (int qz = 0; qz < 2; ++qz) {
+            const double X[3] = {2.0 * g.t[qx] - 1.0, 2.0 * g.t[qy] - 1.0, 2.0 * g.t[qz] - 1.0};
+            const double w = (g.w[qx] * g.w[qy]) * g.w[qz];
+            double ga[3], gb[3];
+            rt_grad(a / 2, (a & 1) ? 1.0 : -1.0, X, ga);
+            rt_grad(b / 2, (b & 1) ? 1.0 : -1.0, X, gb);
+            s += w * ((ga[0] * gb[0] + ga[1] * gb[1]) + ga[2] * gb[2]);
+          }
+      K[static_cast<size_t>(a * 6 + b)] = s;
+    }
+  return K;
+}
+
+// the cells of a face (ascending) and the face's local slot in each
+int rt_cells(const Faces& Fc, int o, const int64_t* a, int64_t* cell, int* slot) {
+  const int64_t N = Fc.N;
+  int n = 0;
+  for (int side = 0; side < 2; ++side) {
+    const int64_t co = a[o] - 1 + side;
+    if (co < 0 || co >= N) continue;
+    int64_t c[3] = {a[0], a[1], a[2]};
+    c[o] = co;
+    cell[n] = (c[0] * N + c[1]) * N + c[2];
+    slot[n] = 2 * o + (side == 0 ? 1 : 0);  // the + face of the lower cell, the - face of the upper
+    ++n;
+  }
+  return n;
+}
+// face lex of local slot s of cell (cx, cy, cz)
+int64_t rt_face_of(const Faces& Fc, int64_t cell, int s) {
+  const int64_t N = Fc.N;
+  int64_t a[3] = {cell / (N * N), (cell / N) % N, cell % N};
+  const int o = s / 2;
+  a[o] += s & 1;
+  return Fc.lex(o, a);
+}
+
+void rt_level(FeLevel& L, int64_t N, const std::vector<double>& Kref, const std::vector<double>& kappa) {
+  L.N = N;
+  const Faces Fc{N, N * N * (N + 1)};
+  const int64_t n_lex = 3 * Fc.per;
+  std::vector<uint8_t> bnd(static_cast<size_t>(n_lex));
+  for (int64_t e = 0; e < n_lex; ++e) {
+    int o;
+    int64_t a[3];
+    Fc.unlex(e, &o, a);
+    bnd[static_cast<size_t>(e)] = (a[o] == 0 || a[o] == N) ? 1 : 0;
+  }
+  number(L, n_lex, bnd);
+  L.keys.resize(static_cast<size_t>(L.n) * 4);
+  L.color.resize(static_cast<size_t>(L.n_own));
+  for (int64_t h = 0; h < L.n; ++h) {
+    int o;
+    int64_t a[3];
+    Fc.unlex(L.lex_of[static_cast<size_t>(h)], &o, a);
+    int64_t* key = &L.keys[static_cast<size_t>(h) * 4];
+    key[0] = o;
+    key[1] = a[0];
+    key[2] = a[1];
+    key[3] = a[2];
+    if (h < L.n_own) L.color[static_cast<size_t>(h)] = 2 * o + static_cast<int32_t>(a[o] & 1);
+  }
+  const double hx = 1.0 / static_cast<double>(N);
+  std::vector<double> Ke(36);
+  for (int i = 0; i < 36; ++i) Ke[static_cast<size_t>(i)] = hx * Kref[static_cast<size_t>(i)];
+  build_csr(L, [&](int64_t h, std::vector<std::pair<int32_t, double>>& row, bool values) {
+    int o;
+    int64_t a[3];
+    Fc.unlex(L.lex_of[static_cast<size_t>(h)], &o, a);
+    int64_t cell[2];
+    int slot[2];
+    const int nc = rt_cells(Fc, o, a, cell, slot);
+    const bool dir = h >= L.n_own;
+    // the faces of the face's cells, each once: cell 0's six, then cell 1's other five
+    for (int k = 0; k < nc; ++k)
+      for (int s2 = 0; s2 < 6; ++s2) {
+        if (k == 1 && s2 == slot[1]) continue;  // the face itself, already listed by cell 0
+        const int32_t col = L.host_of[static_cast<size_t>(rt_face_of(Fc, cell[k], s2))];
+        double v = 0.0;
+        if (values) {
+          if (dir) {
+            v = col == h ? 1.0 : 0.0;
+          } else if (col == h) {
+            for (int u = 0; u < nc; ++u)
+              v += kappa[static_cast<size_t>(cell[u])] * Ke[static_cast<size_t>(slot[u] * 6 + slot[u])];
+          } else {
+            v += kappa[static_cast<size_t>(cell[k])] * Ke[static_cast<size_t>(slot[k] * 6 + s2)];
+          }
+        }
+        row.emplace_back(col, v);
+      }
+  });
+}
+
+// Fine face means of the coarse function, averaged over the two sides of a coarse face;
+// no entries for Dirichlet fine faces (the correction keeps their values).
+void rt_prolongation(FeLevel& F, const FeLevel& Cl) {
+  const Faces Ff{F.N, F.N * F.N * (F.N + 1)}, Fcn{Cl.N, Cl.N * Cl.N * (Cl.N + 1)};
+  const int64_t Nc = Cl.N;
+  build_p(F, [&](int64_t h, std::vector<std::pair<int32_t, double>>& row) {
+    if (h >= F.n_own) return;
+    int o;
+    int64_t a[3];
+    Ff.unlex(F.lex_of[static_cast<size_t>(h)], &o, a);
+    // coarse cells containing the fine face and the face's normal coordinate X_o in each
+    int64_t cells[2];
+    double Xo[2];
+    int nc = 0;
+    if (a[o] & 1) {
+      cells[0] = (a[o] - 1) / 2;
+      Xo[0] = 0.0;
+      nc = 1;
+    } else {
+      const int64_t pl = a[o] / 2;
+      if (pl - 1 >= 0) {
+        cells[nc] = pl - 1;
+        Xo[nc++] = 1.0;
+      }
+      if (pl < Nc) {
+        cells[nc] = pl;
+        Xo[nc++] = -1.0;
+      }
+    }
+    const double scale = nc == 2 ? 0.5 : 1.0;
+    for (int k = 0; k < nc; ++k) {
+      int64_t c[3];
+      double m[3];  // mean of X_t over the fine face along each tangential axis
+      for (int t = 0; t < 3; ++t) {
+        if (t == o) {
+          c[t] = cells[k];
+          m[t] = 0.0;
+        } else {
+          c[t] = a[t] / 2;
+          m[t] = (a[t] & 1) ? 0.5 : -0.5;
+        }
+      }
+      const int64_t cell = (c[0] * Nc + c[1]) * Nc + c[2];
+      for (int s2 = 0; s2 < 6; ++s2) {
+        const int o2 = s2 / 2;
+        const double sg = (s2 & 1) ? 1.0 : -1.0;
+        double w;
+        if (o2 == o)
+          w = Xo[k] == 0.0 ? 0.0 : (sg == Xo[k] ? 1.0 : 0.0);
+        else
+          w = (Xo[k] == 0.0 ? 0.25 : 0.0) + 0.5 * (sg * m[o2]);
+        if (w == 0.0) continue;
+        const int32_t col = Cl.host_of[static_cast<size_t>(rt_face_of(Fcn, cell, s2))];
+        const double ws = scale * w;
+        bool merged = false;
+        for (auto& [cc, ww] : row)
+          if (cc == col) {
+            ww += ws;
+            merged = true;
+          }
+        if (!merged) row.emplace_back(col, ws);
+      }
+    }
+  });
+}
+
+void rt_rhs(pf_fe_setup& s) {
+  const FeLevel& L = *s.levels.back();
+  const int64_t N = L.N;
+  const Faces Fc{N, N * N * (N + 1)};
+  const Rule g = gauss3();
+  const double h = 1.0 / static_cast<double>(N);
+  const double vol = (h * h) * h, K3 = (3.0 * kPi) * kPi;
+  std::vector<double> S(static_cast<size_t>(N * 3));
+  for (int64_t c = 0; c < N; ++c)
+    for (int q = 0; q < 3; ++q) S[static_cast<size_t>(c * 3 + q)] = std::sin(kPi * ((static_cast<double>(c) + g.t[q]) * h));
+  double phi[27][6];
+  for (int q = 0; q < 27; ++q) {
+    const double X[3] = {2.0 * g.t[q / 9] - 1.0, 2.0 * g.t[(q / 3) % 3] - 1.0, 2.0 * g.t[q % 3] - 1.0};
+    for (int a = 0; a < 6; ++a) phi[q][a] = rt_phi(a / 2, (a & 1) ? 1.0 : -1.0, X);
+  }
+  std::vector<double> le(static_cast<size_t>(N * N * N * 6));
+#pragma omp parallel for schedule(static)
+  for (int64_t cell = 0; cell < N * N * N; ++cell) {
+    const int64_t cx = cell / (N * N), cy = (cell / N) % N, cz = cell % N;
+    double* out = &le[static_cast<size_t>(cell * 6)];
+    for (int a = 0; a < 6; ++a) out[a] = 0.0;
+    for (int q = 0; q < 27; ++q) {
+      const int qx = q / 9, qy = (q / 3) % 3, qz = q % 3;
+      const double w = (g.w[qx] * g.w[qy]) * g.w[qz];
+      const double f = ((K3 * S[static_cast<size_t>(cx * 3 + qx)]) * S[static_cast<size_t>(cy * 3 + qy)]) *
+                       S[static_cast<size_t>(cz * 3 + qz)];
+      const double wf = (w * vol) * f;
+      for (int a = 0; a < 6; ++a) out[a] += wf * phi[q][a];
+    }
+  }
+  s.b.assign(static_cast<size_t>(L.n), 0.0);
+  s.x0.assign(static_cast<size_t>(L.n), 0.0);
+  s.exact.assign(static_cast<size_t>(L.n), 0.0);
+  const double ph = kPi * h;
+#pragma omp parallel for schedule(static)
+  for (int64_t hh = 0; hh < L.n; ++hh) {
+    int o;
+    int64_t a[3];
+    Fc.unlex(L.lex_of[static_cast<size_t>(hh)], &o, a);
+    double u = 1.0;
+    for (int t = 0; t < 3; ++t) {
+      const double x0 = static_cast<double>(a[t]) * h;
+      u *= t == o ? std::sin(kPi * x0) : (std::cos(kPi * x0) - std::cos(kPi * (static_cast<double>(a[t] + 1) * h))) / ph;
+    }
+    s.exact[static_cast<size_t>(hh)] = u;
+    if (hh >= L.n_own) continue;
+    int64_t cell[2];
+    int slot[2];
+    const int nc = rt_cells(Fc, o, a, cell, slot);
+    double acc = 0.0;
+    for (int k = 0; k < nc; ++k) acc += le[static_cast<size_t>(cell[k] * 6 + slot[k])];
+    s.b[static_cast<size_t>(hh)] = acc;
+  }
+}
+
+// ------------------------------------------------------------------- create --
+
+void create(pf_fe_setup& s) {
+  const int nl = s.n_levels;
+  s.levels.clear();
+  for (int l = 0; l < nl; ++l) s.levels.push_back(std::make_unique<FeLevel>());
+  const int64_t Nf = static_cast<int64_t>(s.n_coarse) << (nl - 1);
+  if (s.family == PF_FE_Q2) {
+    const std::vector<double> Kref = q2_kref();
+    s.kappa.assign(static_cast<size_t>(Nf * Nf * Nf), 1.0);
+    for (int l = 0; l < nl; ++l) {
+      const int64_t N = static_cast<int64_t>(s.n_coarse) << l;
+      const double h = 1.0 / static_cast<double>(N);
+      std::vector<double> Ke(Kref.size());
+      for (size_t i = 0; i < Kref.size(); ++i) Ke[i] = h * Kref[i];
+      q2_level(*s.levels[static_cast<size_t>(l)], N, Ke);
+      if (l > 0) q2_prolongation(*s.levels[static_cast<size_t>(l)], *s.levels[static_cast<size_t>(l) - 1]);
+    }
+    q2_rhs(s);
+  } else {
+    const std::vector<double> Kref = rt_kref();
+    // coefficients: finest by the generator, each coarser cell the mean of its 8 children
+    std::vector<std::vector<double>> kap(static_cast<size_t>(nl));
+    kap.back().resize(static_cast<size_t>(Nf * Nf * Nf));
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < Nf * Nf * Nf; ++c)
+      kap.back()[static_cast<size_t>(c)] = s.coefficient == PF_COEF_LOGNORMAL ? pf::lognormal_kappa(s.seed, c) : 1.0;
+    for (int l = nl - 2; l >= 0; --l) {
+      const int64_t N = static_cast<int64_t>(s.n_coarse) << l, N2 = 2 * N;
+      auto& kc = kap[static_cast<size_t>(l)];
+      const auto& kf = kap[static_cast<size_t>(l) + 1];
+      kc.resize(static_cast<size_t>(N * N * N));
+#pragma omp parallel for schedule(static)
+      for (int64_t c = 0; c < N * N * N; ++c) {
+        const int64_t cx = c / (N * N), cy = (c / N) % N, cz = c % N;
+        double sum = 0.0;
+        for (int d = 0; d < 8; ++d)
+          sum += kf[static_cast<size_t>(((2 * cx + (d >> 2)) * N2 + 2 * cy + ((d >> 1) & 1)) * N2 + 2 * cz + (d & 1))];
+        kc[static_cast<size_t>(c)] = 0.125 * sum;
+      }
+    }
+    for (int l = 0; l < nl; ++l) {
+      rt_level(*s.levels[static_cast<size_t>(l)], static_cast<int64_t>(s.n_coarse) << l, Kref, kap[static_cast<size_t>(l)]);
+      if (l > 0) rt_prolongation(*s.levels[static_cast<size_t>(l)], *s.levels[static_cast<size_t>(l) - 1]);
+    }
+    s.kappa = std::move(kap.back());
+    rt_rhs(s);
+  }
+  for (auto& L : s.levels) {
+    L->host_of.clear();
+    L->host_of.shrink_to_fit();
+    L->lex_of.clear();
+    L->lex_of.shrink_to_fit();
+  }
+}
+
+template <typename F>
+pf_status guard(F&& f) {
+  try {
+    f();
+    return PF_OK;
+  } catch (const FeError& e) {
+    g_fe_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_fe_err = e.what();
+    return PF_ERR_STATE;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pf_fe_last_error(void) { return g_fe_err.c_str(); }
+
+pf_status pf_fe_setup_create(int family, int n_coarse, int n_levels, int coefficient, uint64_t seed,
+                             pf_fe_setup** out) {
+  return guard([&] {
+    if (!out) invalid("null argument");
+    *out = nullptr;
+    if (family != PF_FE_Q2 && family != PF_FE_ROTATED_Q1) invalid("unknown element family");
+    if (coefficient != PF_COEF_CONSTANT && coefficient != PF_COEF_LOGNORMAL) invalid("unknown coefficient");
+    if (family == PF_FE_Q2 && coefficient != PF_COEF_CONSTANT) invalid("Q2 takes the constant coefficient only");
+    if (n_coarse < 2 || n_levels < 1 || n_levels > 12) invalid("need n_coarse >= 2 and 1 <= n_levels <= 12");
+    auto s = std::make_unique<pf_fe_setup>();
+    s->family = family;
+    s->n_coarse = n_coarse;
+    s->n_levels = n_levels;
+    s->coefficient = coefficient;
+    s->seed = seed;
+    const auto t0 = std::chrono::steady_clock::now();
+    create(*s);
+    s->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = s.release();
+  });
+}
+
+pf_status pf_fe_setup_destroy(pf_fe_setup* s) {
+  delete s;
+  return PF_OK;
+}
+
+pf_status pf_fe_setup_level(const pf_fe_setup* s, int level, pf_level_desc* out) {
+  return guard([&] {
+    if (!s || !out) invalid("null argument");
+    if (level < 0 || level >= s->n_levels) invalid("level out of range");
+    const FeLevel& L = *s->levels[static_cast<size_t>(level)];
+    std::memset(out, 0, sizeof *out);
+    out->n_dofs = L.n;
+    out->n_own_dofs = L.n_own;
+    out->row_offsets = L.rowptr.data();
+    out->col_indices = L.cols.data();
+    out->values = L.vals.data();
+    out->owns_row = L.owns_row.data();
+    out->is_dirichlet = L.is_dir.data();
+    out->color = L.color.data();
+    out->row_order = L.order.data();
+    if (level > 0) {
+      out->p_offsets = L.p_off.data();
+      out->p_cols = L.p_col.data();
+      out->p_weights = L.p_w.data();
+    }
+  });
+}
+
+pf_status pf_fe_setup_level_keys(const pf_fe_setup* s, int level, const int64_t** keys4, const uint8_t** class_of) {
+  return guard([&] {
+    if (!s || !keys4 || !class_of) invalid("null argument");
+    if (level < 0 || level >= s->n_levels) invalid("level out of range");
+    *keys4 = s->levels[static_cast<size_t>(level)]->keys.data();
+    *class_of = s->levels[static_cast<size_t>(level)]->class_of.data();
+  });
+}
+
+pf_status pf_fe_setup_rhs(const pf_fe_setup* s, const double** b, const double** x0, const double** exact,
+                          int64_t* n) {
+  return guard([&] {
+    if (!s || !b || !x0 || !exact || !n) invalid("null argument");
+    *b = s->b.data();
+    *x0 = s->x0.data();
+    *exact = s->exact.data();
+    *n = static_cast<int64_t>(s->b.size());
+  });
+}
+
+pf_status pf_fe_setup_kappa(const pf_fe_setup* s, const double** kappa, int64_t* n) {
+  return guard([&] {
+    if (!s || !kappa || !n) invalid("null argument");
+    *kappa = s->kappa.data();
+    *n = static_cast<int64_t>(s->kappa.size());
+  });
+}
+
+pf_status pf_fe_setup_seconds(const pf_fe_setup* s, double* out) {
+  return guard([&] {
+    if (!s || !out) invalid("null argument");
+    *out = s->seconds;
+  });
+}
+
+}  // extern "C"

@@ -545,14 +545,19 @@ __device__ void coarse_gs_body(const CoarseSub* __restrict__ subs, int n_sub, do
 }
 
 // coarse_gs_body on a block: all threads stage the packed level in shared memory (one
-// round of parallel loads), thread 0 runs the sequential algorithm there, all threads
-// write x back.  Same operations in the same order as coarse_gs_body.
+// round of parallel loads); the residual norm takes one row per thread (squares summed
+// by thread 0 in row order); the Gauss-Seidel sweep visits the rows in order with warp 0:
+// its lanes form the row's products a_e x_c from the current x, lane 0 subtracts them in
+// stored order.  Same operations in the same order as coarse_gs_body.
 __device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __restrict__ b, double tol,
                                int32_t max_iter, double* stats, unsigned char* smem) {
   double* sx = reinterpret_cast<double*>(smem);
   double* sb = sx + P.n_total;
   double* sv = sb + P.n_rows;
-  int32_t* srp = reinterpret_cast<int32_t*>(sv + P.nnz);
+  double* ssq = sv + P.nnz;
+  double* sp = ssq + P.n_rows;
+  double* stot = sp + P.max_row;
+  int32_t* srp = reinterpret_cast<int32_t*>(stot + 1);
   int32_t* srd = srp + P.n_rows + 1;
   int32_t* sc = srd + P.n_rows;
   int32_t* ssr = sc + P.nnz;
@@ -560,6 +565,7 @@ __device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __r
   int32_t* sms = smd + P.ms_n;
   int32_t* shd = sms + P.ms_n;
   int32_t* shs = shd + P.h1_n;
+  int32_t* sdg = shs + P.h1_n;
   for (int i = threadIdx.x; i < P.n_total; i += blockDim.x) sx[i] = x[i];
   for (int i = threadIdx.x; i < P.n_rows; i += blockDim.x) {
     srd[i] = P.rowdev[i];
@@ -580,55 +586,81 @@ __device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __r
     shs[i] = P.h1_src[i];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    auto norm = [&]() {
+  // position of each row's diagonal entry (the last one, as the sequential scan keeps)
+  for (int i = threadIdx.x; i < P.n_rows; i += blockDim.x) {
+    int32_t dpos = -1;
+    for (int32_t e = srp[i]; e < srp[i + 1]; ++e)
+      if (sc[e] == srd[i]) dpos = e;
+    sdg[i] = dpos;
+  }
+  auto norm = [&]() {
+    __syncthreads();
+    for (int i = threadIdx.x; i < P.n_rows; i += blockDim.x) {
+      double acc = sb[i];
+      for (int32_t e = srp[i]; e < srp[i + 1]; ++e) acc = __dsub_rn(acc, __dmul_rn(sv[e], sx[sc[e]]));
+      ssq[i] = __dmul_rn(acc, acc);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
       double total = 0.0;
       for (int s = 0; s < P.n_sub; ++s) {
         double local = 0.0;
-        for (int32_t i = ssr[s]; i < ssr[s + 1]; ++i) {
-          double acc = sb[i];
-          for (int32_t e = srp[i]; e < srp[i + 1]; ++e) acc = __dsub_rn(acc, __dmul_rn(sv[e], sx[sc[e]]));
-          local = __dadd_rn(local, __dmul_rn(acc, acc));
-        }
+        for (int32_t i = ssr[s]; i < ssr[s + 1]; ++i) local = __dadd_rn(local, ssq[i]);
         total = __dadd_rn(total, local);
       }
-      return sqrt(total);
-    };
-    const double r0 = norm();
+      stot[0] = sqrt(total);
+    }
+    __syncthreads();
+    return stot[0];
+  };
+  const double r0 = norm();
+  if (threadIdx.x == 0) {
     stats[0] = 0;
     stats[1] = 1;
     stats[2] = r0;
     stats[3] = r0;
-    if (r0 != 0.0) {
-      const double target = __dmul_rn(tol, r0);
-      int it = 0;
-      bool conv = false;
-      while (it < max_iter) {
+  }
+  if (r0 != 0.0) {
+    const double target = __dmul_rn(tol, r0);
+    const int lane = threadIdx.x & 31;
+    int it = 0;
+    bool conv = false;
+    while (it < max_iter) {
+      if (threadIdx.x < 32) {
         for (int32_t i = 0; i < P.n_rows; ++i) {
-          const int32_t d = srd[i];
-          double acc = sb[i], diag = 0.0;
-          for (int32_t e = srp[i]; e < srp[i + 1]; ++e) {
-            const int32_t c = sc[e];
-            if (c == d)
-              diag = sv[e];
-            else
-              acc = __dsub_rn(acc, __dmul_rn(sv[e], sx[c]));
+          const int32_t r0e = srp[i], r1e = srp[i + 1];
+          for (int32_t e = r0e + lane; e < r1e; e += 32) sp[e - r0e] = __dmul_rn(sv[e], sx[sc[e]]);
+          __syncwarp();
+          if (lane == 0) {
+            const int32_t de = sdg[i];
+            double acc = sb[i], diag = 0.0;
+            for (int32_t e = r0e; e < r1e; ++e) {
+              if (e == de)
+                diag = sv[e];
+              else
+                acc = __dsub_rn(acc, sp[e - r0e]);
+            }
+            sx[srd[i]] = __ddiv_rn(acc, diag);
           }
-          sx[d] = __ddiv_rn(acc, diag);
+          __syncwarp();
         }
-        for (int32_t i = 0; i < P.ms_n; ++i) sx[smd[i]] = sx[sms[i]];
-        for (int32_t i = 0; i < P.h1_n; ++i) sx[shd[i]] = sx[shs[i]];
-        ++it;
-        const double fr = norm();
-        stats[0] = it;
-        stats[3] = fr;
-        if (fr <= target) {
-          conv = true;
-          break;
+        if (lane == 0) {
+          for (int32_t i = 0; i < P.ms_n; ++i) sx[smd[i]] = sx[sms[i]];
+          for (int32_t i = 0; i < P.h1_n; ++i) sx[shd[i]] = sx[shs[i]];
         }
       }
-      if (!conv) stats[1] = 0;
+      ++it;
+      const double fr = norm();
+      if (threadIdx.x == 0) {
+        stats[0] = it;
+        stats[3] = fr;
+      }
+      if (fr <= target) {
+        conv = true;
+        break;
+      }
     }
+    if (!conv && threadIdx.x == 0) stats[1] = 0;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < P.n_total; i += blockDim.x) x[i] = sx[i];

@@ -648,6 +648,8 @@ CoarsePack make_coarse_pack(const std::vector<HostLevel>& H, const std::vector<D
   P.h1_dst = plans[PF_CH_HALO1].dst.p;
   P.h1_src = plans[PF_CH_HALO1].src.p;
   P.h1_n = static_cast<int32_t>(plans[PF_CH_HALO1].n);
+  P.max_row = 0;
+  for (size_t i = 0; i + 1 < rp.size(); ++i) P.max_row = std::max(P.max_row, rp[i + 1] - rp[i]);
   return P;
 }
 

@@ -31,6 +31,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include "pf_coef.hpp"
+
 namespace {
 
 struct SetupError : std::runtime_error {
@@ -564,22 +566,7 @@ Box expand(const Box& b, int64_t by, const Geo& g, bool vertices) {
 // trilinear interpolation of the coarse cell's basis at the child's vertices (for nested
 // conforming Q1 spaces this is the rediscretisation with the fine coefficient).
 
-uint64_t splitmix64(uint64_t x) {
-  x += 0x9e3779b97f4a7c15ULL;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-  return x ^ (x >> 31);
-}
-
-// Box-Muller on two 53-bit uniforms in (0, 1]
-double lognormal_kappa(uint64_t seed, int64_t gcn) {
-  const uint64_t a = splitmix64(seed ^ splitmix64(static_cast<uint64_t>(gcn) * 2 + 1));
-  const uint64_t b = splitmix64(a);
-  const double u1 = (static_cast<double>(a >> 11) + 1.0) / 9007199254740992.0;
-  const double u2 = (static_cast<double>(b >> 11) + 1.0) / 9007199254740992.0;
-  const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * kPi * u2);
-  return std::exp(z);
-}
+using pf::lognormal_kappa;
 
 Geo geo_of(int d, int n_coarse, int level) {
   Geo g;

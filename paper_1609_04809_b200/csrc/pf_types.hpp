@@ -93,11 +93,12 @@ struct CoarsePack {
   const double* vals;
   const int32_t *ms_dst, *ms_src, *h1_dst, *h1_src;
   int32_t ms_n, h1_n;
+  int32_t max_row;  // longest row (products scratch of the sweep)
 };
 
 PF_HD inline size_t coarse_pack_smem(const CoarsePack& P) {
-  return sizeof(double) * (static_cast<size_t>(P.n_total) + P.n_rows + P.nnz) +
-         sizeof(int32_t) * (static_cast<size_t>(P.n_rows) * 2 + 1 + P.nnz + P.n_sub + 1 +
+  return sizeof(double) * (static_cast<size_t>(P.n_total) + 2 * static_cast<size_t>(P.n_rows) + P.nnz + P.max_row + 1) +
+         sizeof(int32_t) * (static_cast<size_t>(P.n_rows) * 3 + 1 + P.nnz + P.n_sub + 1 +
                             2 * static_cast<size_t>(P.ms_n) + 2 * static_cast<size_t>(P.h1_n));
 }
 

@@ -17,18 +17,19 @@ def declared(header):
     return sorted(set(re.findall(r"\b(pf_[a-z0-9_]+)\s*\(", text)))
 
 
-@pytest.mark.parametrize("header", ["pf_gpu.h", "pf_setup.h"])
+@pytest.mark.parametrize("header", ["pf_gpu.h", "pf_setup.h", "pf_fe.h"])
 def test_every_declared_symbol_is_exported(header):
     lib = _lib.lib()
     names = declared(header)
     assert names, header
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
-    assert set(names) <= set(_lib.EXPORTS) | {"pf_setup_last_error"}
+    assert set(names) <= set(_lib.EXPORTS) | {"pf_setup_last_error", "pf_fe_last_error"}
 
 
 def test_python_export_list_matches_headers():
-    assert sorted(_lib.EXPORTS) == sorted(set(declared("pf_gpu.h")) | set(declared("pf_setup.h")))
+    assert sorted(_lib.EXPORTS) == sorted(set(declared("pf_gpu.h")) | set(declared("pf_setup.h"))
+                                         | (set(declared("pf_fe.h")) - {"pf_fe_last_error"}))
 
 
 def test_version_names_the_target():

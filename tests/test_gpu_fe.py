@@ -1,0 +1,86 @@
+"""GPU parity of the V-cycle on the Q2 and rotated-Q1 hierarchies (include/pf_fe.h;
+BASELINE configs[2] and configs[3]).  The device runs the same kernels as for Q1 (SELL
+rows of up to 125 entries for Q2, 27 colours; 11 entries and 6 colours for rotated Q1,
+fp64 values under the lognormal coefficient); the oracle (oracle/gmg_oracle.c, the
+reference's V-cycle restated) runs on the same level arrays, which
+tests/test_fe_setup.py pins to oracle/fe_restated.py."""
+import numpy as np
+import pytest
+
+from helpers import cfg, download, upload
+from oracle.restated import Oracle
+from paper_1609_04809_b200 import gmg
+from paper_1609_04809_b200.fe import CONSTANT, LOGNORMAL, Q2, ROTATED_Q1, FESetup
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [gmg.PF_SMOOTHER_JACOBI, gmg.PF_SMOOTHER_GAUSS_SEIDEL, gmg.PF_SMOOTHER_MULTICOLOR_SOR]
+SYSTEMS = [(Q2, CONSTANT, 3), (Q2, CONSTANT, 4), (ROTATED_Q1, CONSTANT, 4), (ROTATED_Q1, LOGNORMAL, 4)]
+IDS = ["q2_L3", "q2_L4", "rt_L4", "rt_lognormal_L4"]
+
+
+def _cfg(kind, family, max_cycles=400):
+    pp = 3 if family == Q2 else 2  # V(3,3) for Q2 (BASELINE configs[2]), V(2,2) otherwise
+    return cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8, pre=pp, post=pp,
+               max_cycles=max_cycles)
+
+
+@pytest.fixture(scope="module", params=SYSTEMS, ids=IDS)
+def fe_system(request, cuda):
+    family, coef, L = request.param
+    s = FESetup(family, 2, L, coef, seed=31)
+    return dict(s=s, h=gmg.Hierarchy([s.levels]), o=Oracle([s.levels]), family=family, L=L)
+
+
+@pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
+def test_fe_smooth_and_transfers_bit_exact(fe_system, kind):
+    """One to three sweeps on every level, the residual, restriction and prolongation:
+    device == oracle bit for bit."""
+    s, h, o = fe_system["s"], fe_system["h"], fe_system["o"]
+    rng = np.random.default_rng(5)
+    omega = 1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8
+    for l, lv in enumerate(s.levels):
+        x0 = rng.standard_normal(lv.n)
+        x0[lv.is_dir == 1] = 0.0
+        b = rng.standard_normal(lv.n)
+        for sweeps in (1, 3):
+            x = upload(h, l, [x0])
+            gmg.smooth(h, l, x, upload(h, l, [b]), gmg.SmootherConfig(kind=kind, sweeps=sweeps, damping=omega))
+            assert np.array_equal(download(h, x, 1)[0], o.smooth(l, [x0], [b], kind, sweeps=sweeps,
+                                                                  damping=omega)[0]), (l, sweeps)
+        if l:
+            r = h.vector(l - 1)
+            gmg.restrict_residual(h, l, upload(h, l, [b]), r)
+            assert np.array_equal(download(h, r, 1)[0], o.restrict_residual(l, [b])[0]), l
+            xc = rng.standard_normal(s.levels[l - 1].n)
+            px = h.vector(l)
+            gmg.prolongate(h, l, upload(h, l - 1, [xc]), px)
+            assert np.array_equal(download(h, px, 1)[0], o.prolongate(l, [xc])[0]), l
+
+
+@pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
+def test_fe_solve_bit_exact(fe_system, kind):
+    """solve_outer to 1e-10: the oracle's cycle count, residual history (norm summation
+    order: 1e-12) and iterate bit for bit."""
+    s, h, o, family, L = fe_system["s"], fe_system["h"], fe_system["o"], fe_system["family"], fe_system["L"]
+    c = _cfg(kind, family)
+    x = upload(h, L - 1, [s.x0])
+    st = gmg.solve_outer(h, x, upload(h, L - 1, [s.b]), c)
+    xo, res, ost, rc = o.solve_outer([s.x0], [s.b], c)
+    assert rc == 0 and st.converged
+    assert st.iterations == ost.iterations
+    np.testing.assert_allclose(st.residuals, res, rtol=1e-12)
+    assert np.array_equal(download(h, x, 1)[0], xo[0])
+
+
+@pytest.mark.parametrize("family", [Q2, ROTATED_Q1], ids=["q2", "rt"])
+def test_fe_solution_matches_exact_solution(cuda, family):
+    """The converged multigrid solution has the discretisation error of the direct solve:
+    Q2 nodal error ~h^4, rotated-Q1 face means ~h^2 (32^3 cells)."""
+    s = FESetup(family, 2, 5)
+    h = gmg.Hierarchy([s.levels])
+    x = upload(h, 4, [s.x0])
+    st = gmg.solve_outer(h, x, upload(h, 4, [s.b]), _cfg(gmg.PF_SMOOTHER_MULTICOLOR_SOR, family))
+    assert st.converged and st.iterations <= 15
+    err = np.abs(download(h, x, 1)[0] - s.exact).max()
+    assert err < (3e-7 if family == Q2 else 2e-3), err
