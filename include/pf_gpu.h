@@ -183,6 +183,14 @@ pf_status pf_hierarchy_set_level(pf_hierarchy* h, int level, int subdomain,
  * Raises PF_ERR_SINGULAR_DIAGONAL for a zero or missing own-row diagonal — the check
  * smooth() repeats on every call in the reference (solvers.cpp:10-15, :57). */
 pf_status pf_hierarchy_finalize(pf_hierarchy* h);
+/* Direct coarse solve (BASELINE configs[0] names a "coarse direct solve"): coarse_solve on
+ * level 0 becomes x_own = inv(A_oo) (b_own - A_o,rest x_rest) — the inverse of the own-own
+ * block formed once on the host by Gauss-Jordan elimination with partial pivoting
+ * (restated in oracle/gmg_oracle.c) — instead of the reference's Gauss-Seidel iteration to
+ * coarse_tol (solvers.cpp:70-92); stats report 1 iteration.  The V-cycle iterates then
+ * differ from the reference's at the coarse-tolerance level.  One subdomain in one
+ * process; call after pf_hierarchy_finalize (captured solve graphs are rebuilt). */
+pf_status pf_hierarchy_set_coarse_direct(pf_hierarchy* h, int on);
 /* Multi-process: join the NCCL communicator of `world_size` ranks (one hierarchy per
  * process).  `unique_id` is the 128-byte ncclUniqueId from pf_nccl_unique_id() on
  * rank 0, broadcast by the caller. */

@@ -47,7 +47,8 @@ typedef struct {
 
 struct orc_hier {
   int nl, ns;
-  OLev* lev; /* [level * ns + sub] */
+  OLev* lev;   /* [level * ns + sub] */
+  double* cinv; /* orc_set_coarse_direct: inverse of level 0's own block, or NULL */
 };
 
 static OLev* L_(orc_hier* h, int l, int s) { return &h->lev[l * h->ns + s]; }
@@ -71,6 +72,7 @@ int orc_create(int n_levels, int n_sub, orc_hier** out) {
 
 void orc_destroy(orc_hier* h) {
   if (!h) return;
+  free(h->cinv);
   for (int i = 0; i < h->nl * h->ns; ++i) {
     OLev* L = &h->lev[i];
     free(L->rp); free(L->ci); free(L->v); free(L->owns); free(L->isdir); free(L->color);
@@ -336,7 +338,53 @@ int orc_smooth(orc_hier* h, int level, double* const* x, double* const* b, const
   return rc;
 }
 
-/* coarse_solve (solvers.cpp:70-92) with the reference's lexicographic Gauss-Seidel */
+/* Direct coarse solve of the B200 build (pf_hierarchy_set_coarse_direct): the inverse of
+ * the own-own block by Gauss-Jordan elimination with partial pivoting (first row of
+ * maximal |pivot|), pivot rows scaled by division. */
+int orc_set_coarse_direct(orc_hier* h, int on) {
+  free(h->cinv);
+  h->cinv = NULL;
+  if (!on) return 0;
+  if (h->ns != 1) return fail(1, "direct coarse solve needs one subdomain");
+  OLev* L = L_(h, 0, 0);
+  const int n = L->n_own;
+  double* M = calloc((size_t)n * n + 1, sizeof(double));
+  double* I = calloc((size_t)n * n + 1, sizeof(double));
+  for (int i = 0; i < n; ++i) {
+    I[(size_t)i * n + i] = 1.0;
+    for (int64_t e = L->rp[i]; e < L->rp[i + 1]; ++e)
+      if (L->ci[e] < n) M[(size_t)i * n + L->ci[e]] = L->v[e];
+  }
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    double best = fabs(M[(size_t)k * n + k]);
+    for (int i = k + 1; i < n; ++i)
+      if (fabs(M[(size_t)i * n + k]) > best) { best = fabs(M[(size_t)i * n + k]); p = i; }
+    if (best == 0.0) { free(M); free(I); return fail(2, "singular coarse matrix"); }
+    if (p != k)
+      for (int j = 0; j < n; ++j) {
+        double t = M[(size_t)p * n + j]; M[(size_t)p * n + j] = M[(size_t)k * n + j]; M[(size_t)k * n + j] = t;
+        t = I[(size_t)p * n + j]; I[(size_t)p * n + j] = I[(size_t)k * n + j]; I[(size_t)k * n + j] = t;
+      }
+    const double piv = M[(size_t)k * n + k];
+    for (int j = 0; j < n; ++j) { M[(size_t)k * n + j] /= piv; I[(size_t)k * n + j] /= piv; }
+    for (int i = 0; i < n; ++i) {
+      if (i == k) continue;
+      const double f = M[(size_t)i * n + k];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        M[(size_t)i * n + j] = M[(size_t)i * n + j] - f * M[(size_t)k * n + j];
+        I[(size_t)i * n + j] = I[(size_t)i * n + j] - f * I[(size_t)k * n + j];
+      }
+    }
+  }
+  free(M);
+  h->cinv = I;
+  return 0;
+}
+
+/* coarse_solve (solvers.cpp:70-92) with the reference's lexicographic Gauss-Seidel, or
+ * the direct solve x_own = inv (b_own - A_o,rest x_rest) when set */
 int orc_coarse_solve(orc_hier* h, int level, double* const* x, double* const* b, double tol, int max_iter,
                      pf_solve_stats* st) {
   pf_solve_stats s;
@@ -344,7 +392,26 @@ int orc_coarse_solve(orc_hier* h, int level, double* const* x, double* const* b,
   s.converged = 1;
   orc_residual_norm(h, level, x, b, &s.initial_residual);
   s.final_residual = s.initial_residual;
-  if (s.initial_residual != 0.0) {
+  if (h->cinv && level == 0 && s.initial_residual != 0.0) {
+    OLev* L = L_(h, 0, 0);
+    const int n = L->n_own;
+    double* r = malloc(sizeof(double) * (size_t)(n + 1));
+    for (int i = 0; i < n; ++i) {
+      double acc = b[0][i];
+      for (int64_t e = L->rp[i]; e < L->rp[i + 1]; ++e)
+        if (L->ci[e] >= n) acc -= L->v[e] * x[0][L->ci[e]];
+      r[i] = acc;
+    }
+    for (int i = 0; i < n; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < n; ++j) acc += h->cinv[(size_t)i * n + j] * r[j];
+      x[0][i] = acc;
+    }
+    free(r);
+    s.iterations = 1;
+    orc_residual_norm(h, level, x, b, &s.final_residual);
+    s.converged = s.final_residual <= tol * s.initial_residual;
+  } else if (s.initial_residual != 0.0) {
     pf_smoother_config gs = {ORC_SMOOTHER_LEX_GS, 1, 1, 0.8};
     const double target = tol * s.initial_residual;
     s.converged = 0;

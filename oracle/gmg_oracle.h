@@ -29,6 +29,7 @@ const char* orc_last_error(void);
 int orc_create(int n_levels, int n_sub, orc_hier** out);
 int orc_set_level(orc_hier* h, int level, int sub, const pf_level_desc* d);
 int orc_finalize(orc_hier* h);
+int orc_set_coarse_direct(orc_hier* h, int on);
 void orc_destroy(orc_hier* h);
 int orc_n_dofs(const orc_hier* h, int level, int sub);
 

@@ -30,6 +30,7 @@ def lib():
         L.orc_create.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.orc_set_level.argtypes = [P, C.c_int, C.c_int, C.POINTER(_lib.LevelDesc)]
         L.orc_finalize.argtypes = [P]
+        L.orc_set_coarse_direct.argtypes = [P, C.c_int]
         L.orc_destroy.argtypes = [P]
         L.orc_destroy.restype = None
         vec = P  # double* const*
@@ -58,7 +59,7 @@ def _vec(arrs):
 class Oracle:
     """K subdomains (ranks 0..K-1) of one hierarchy, host order, reference semantics."""
 
-    def __init__(self, levels):
+    def __init__(self, levels, coarse_direct=False):
         L = lib()
         self.K, self.n_levels = len(levels), len(levels[0])
         self.sizes = [[lv.n for lv in sub] for sub in levels]
@@ -70,6 +71,8 @@ class Oracle:
                 self._check(L.orc_set_level(self._h, l, s, C.byref(d)))
                 del keep
         self._check(L.orc_finalize(self._h))
+        if coarse_direct:
+            self._check(L.orc_set_coarse_direct(self._h, 1))
 
     @staticmethod
     def _check(rc):

@@ -556,7 +556,7 @@ __device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __r
   double* sv = sb + P.n_rows;
   double* ssq = sv + P.nnz;
   double* sp = ssq + P.n_rows;
-  double* stot = sp + P.max_row;
+  double* stot = sp + (P.max_row > P.n_rows ? P.max_row : P.n_rows);
   int32_t* srp = reinterpret_cast<int32_t*>(stot + 1);
   int32_t* srd = srp + P.n_rows + 1;
   int32_t* sc = srd + P.n_rows;
@@ -620,7 +620,28 @@ __device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __r
     stats[2] = r0;
     stats[3] = r0;
   }
-  if (r0 != 0.0) {
+  if (P.inv && r0 != 0.0) {
+    // direct: r = b - A_o,rest x_rest (stored order), x_own = inv r (ascending columns)
+    for (int i = threadIdx.x; i < P.n_rows; i += blockDim.x) {
+      double acc = sb[i];
+      for (int32_t e = srp[i]; e < srp[i + 1]; ++e)
+        if (sc[e] >= P.n_own_dev) acc = __dsub_rn(acc, __dmul_rn(sv[e], sx[sc[e]]));
+      sp[i] = acc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P.n_rows; i += blockDim.x) {
+      double acc = 0.0;
+      const double* row = P.inv + static_cast<int64_t>(i) * P.n_rows;
+      for (int32_t j = 0; j < P.n_rows; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(row + j), sp[j]));
+      sx[srd[i]] = acc;
+    }
+    const double fr = norm();
+    if (threadIdx.x == 0) {
+      stats[0] = 1;
+      stats[1] = fr <= __dmul_rn(tol, r0) ? 1 : 0;
+      stats[3] = fr;
+    }
+  } else if (r0 != 0.0) {
     const double target = __dmul_rn(tol, r0);
     const int lane = threadIdx.x & 31;
     int it = 0;

@@ -1113,6 +1113,53 @@ void enq_restrict(pf_hierarchy* h, int fine, const double* rf, double* bc, doubl
   }
 }
 
+// Inverse by Gauss-Jordan elimination with partial pivoting (the first row of maximal
+// |pivot|), pivot rows scaled by division; oracle/gmg_oracle.c restates it.
+void gauss_jordan_inverse(int n, std::vector<double> M, std::vector<double>& inv) {
+  inv.assign(static_cast<size_t>(n) * n, 0.0);
+  for (int i = 0; i < n; ++i) inv[static_cast<size_t>(i) * n + i] = 1.0;
+  auto at = [n](std::vector<double>& v, int i, int j) -> double& { return v[static_cast<size_t>(i) * n + j]; };
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    double best = std::fabs(at(M, k, k));
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(at(M, i, k)) > best) {
+        best = std::fabs(at(M, i, k));
+        p = i;
+      }
+    if (best == 0.0) throw Error(PF_ERR_SINGULAR_DIAGONAL, "singular coarse matrix");
+    if (p != k)
+      for (int j = 0; j < n; ++j) {
+        std::swap(at(M, p, j), at(M, k, j));
+        std::swap(at(inv, p, j), at(inv, k, j));
+      }
+    const double piv = at(M, k, k);
+    for (int j = 0; j < n; ++j) {
+      at(M, k, j) = at(M, k, j) / piv;
+      at(inv, k, j) = at(inv, k, j) / piv;
+    }
+    for (int i = 0; i < n; ++i) {
+      if (i == k) continue;
+      const double f = at(M, i, k);
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        at(M, i, j) = at(M, i, j) - f * at(M, k, j);
+        at(inv, i, j) = at(inv, i, j) - f * at(inv, k, j);
+      }
+    }
+  }
+}
+
+void drop_graphs(pf_hierarchy* h) {
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  for (auto& [k, e] : h->graphs) {
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (e.state) cudaFree(e.state);
+    if (e.host_state) cudaFreeHost(e.host_state);
+  }
+  h->graphs.clear();
+}
+
 void enq_coarse_smem(pf_hierarchy* h, const CoarsePack& P, double* x, const double* b, double tol,
                      int max_iter, double* stats) {
   const size_t bytes = coarse_pack_smem(P);
@@ -1794,7 +1841,9 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
   }
   build_bottom(h);
   if (h->world != h->n_sub) build_rep_bottom(h);
-  for (Level& L : h->levels) L.host.clear();
+  // the host copies go; one subdomain keeps level 0 (pf_hierarchy_set_coarse_direct)
+  for (int l = 0; l < h->n_levels; ++l)
+    if (l > 0 || h->world != 1 || h->n_sub != 1) h->levels[l].host.clear();
   for (auto& RL : h->rep.lv) RL.host.clear();
   PF_CUDA(cudaStreamSynchronize(h->stream));
   h->finalized = true;
@@ -1840,6 +1889,36 @@ pf_status pf_hierarchy_set_fused_exchanges(pf_hierarchy* h, int on) {
   if (!h) invalid("null hierarchy");
   if (h->finalized) state("set fused exchanges before pf_hierarchy_finalize");
   h->fused = on != 0;
+  PF_API_END
+}
+
+pf_status pf_hierarchy_set_coarse_direct(pf_hierarchy* h, int on) {
+  PF_API_BEGIN
+  if (!h) invalid("null hierarchy");
+  if (!h->finalized) state("set the direct coarse solve after pf_hierarchy_finalize");
+  if (h->world != 1 || h->n_sub != 1) invalid("the direct coarse solve needs one subdomain in one process");
+  PF_CUDA(cudaSetDevice(h->device));
+  Level& L = h->levels[0];
+  if (on) {
+    if (coarse_pack_smem(L.cpack) > kCoarseSmemMax) invalid("coarse level too large for the direct solve");
+    if (L.host.empty() || L.host[0].rowptr.empty()) state("level 0 host data not kept");
+    const HostLevel& H = L.host[0];
+    const int n = H.n_own;
+    std::vector<double> A(static_cast<size_t>(n) * n, 0.0), inv(static_cast<size_t>(n) * n, 0.0);
+    for (int i = 0; i < n; ++i)
+      for (int64_t k = H.rowptr[i]; k < H.rowptr[i + 1]; ++k)
+        if (H.cols[k] < n) A[static_cast<size_t>(i) * n + H.cols[k]] = H.vals[k];
+    gauss_jordan_inverse(n, A, inv);
+    h->coarse_inv.upload(inv);
+    L.cpack.inv = h->coarse_inv.p;
+    L.cpack.n_own_dev = n;
+  } else {
+    L.cpack.inv = nullptr;
+  }
+  if (h->bot.active)
+    PF_CUDA(cudaMemcpy(static_cast<char*>(h->bot.desc) + offsetof(BotDesc, coarse), &L.cpack, sizeof(CoarsePack),
+                       cudaMemcpyHostToDevice));
+  drop_graphs(h);  // captured launches carry the old pack
   PF_API_END
 }
 

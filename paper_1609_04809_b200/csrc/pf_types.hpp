@@ -94,10 +94,16 @@ struct CoarsePack {
   const int32_t *ms_dst, *ms_src, *h1_dst, *h1_src;
   int32_t ms_n, h1_n;
   int32_t max_row;  // longest row (products scratch of the sweep)
+  // direct coarse solve (pf_hierarchy_set_coarse_direct), one subdomain: the inverse of the
+  // own-own block (n_rows x n_rows, host order) or nullptr for Gauss-Seidel; columns >=
+  // n_own_dev are the non-own (Dirichlet) ones
+  const double* inv;
+  int32_t n_own_dev;
 };
 
 PF_HD inline size_t coarse_pack_smem(const CoarsePack& P) {
-  return sizeof(double) * (static_cast<size_t>(P.n_total) + 2 * static_cast<size_t>(P.n_rows) + P.nnz + P.max_row + 1) +
+  const size_t scratch = static_cast<size_t>(P.max_row > P.n_rows ? P.max_row : P.n_rows);
+  return sizeof(double) * (static_cast<size_t>(P.n_total) + 2 * static_cast<size_t>(P.n_rows) + P.nnz + scratch + 1) +
          sizeof(int32_t) * (static_cast<size_t>(P.n_rows) * 3 + 1 + P.nnz + P.n_sub + 1 +
                             2 * static_cast<size_t>(P.ms_n) + 2 * static_cast<size_t>(P.h1_n));
 }

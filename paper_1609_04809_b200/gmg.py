@@ -239,6 +239,11 @@ class Hierarchy:
                 v.upload(values, 0)
         return v
 
+    def set_coarse_direct(self, on: bool = True) -> "Hierarchy":
+        """Direct coarse solve on level 0 (pf_hierarchy_set_coarse_direct): one subdomain."""
+        _lib.check(_lib.lib().pf_hierarchy_set_coarse_direct(self._h, 1 if on else 0))
+        return self
+
     def device_bytes(self) -> int:
         out = C.c_int64()
         _lib.check(_lib.lib().pf_hierarchy_device_bytes(self._h, C.byref(out)))

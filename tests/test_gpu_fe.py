@@ -84,3 +84,35 @@ def test_fe_solution_matches_exact_solution(cuda, family):
     assert st.converged and st.iterations <= 15
     err = np.abs(download(h, x, 1)[0] - s.exact).max()
     assert err < (3e-7 if family == Q2 else 2e-3), err
+
+
+@pytest.mark.parametrize("family,coef,L", [(Q2, CONSTANT, 4), (ROTATED_Q1, LOGNORMAL, 4), (None, None, 5)],
+                         ids=["q2", "rt_lognormal", "q1_nc4"])
+@pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
+def test_direct_coarse_solve_bit_exact(cuda, family, coef, L, kind):
+    """pf_hierarchy_set_coarse_direct: the coarse solve as inv(A_oo) r (Gauss-Jordan on the
+    host, restated in the oracle): coarse_solve and the whole solve equal the oracle's bit
+    for bit, on the per-level path and inside the bottom kernel (coloured smoothers)."""
+    from paper_1609_04809_b200.levels import StructuredSetup
+    if family is None:  # Q1 with 4^3 coarse cells: 27 coarse unknowns
+        s = StructuredSetup(3, 4, L - 2, 1)
+        levels, b0, x0, fam = s.levels, s.b, s.x0, ROTATED_Q1
+    else:
+        s = FESetup(family, 2, L, coef, seed=3)
+        levels, b0, x0, fam = s.levels, s.b, s.x0, family
+    nl = len(levels)
+    h = gmg.Hierarchy([levels]).set_coarse_direct()
+    o = Oracle([levels], coarse_direct=True)
+    rng = np.random.default_rng(2)
+    b = rng.standard_normal(levels[0].n)
+    xd = upload(h, 0, [np.zeros(levels[0].n)])
+    st = gmg.coarse_solve(h, 0, xd, upload(h, 0, [b]), 1e-12, 20000)
+    xo, ost = o.coarse_solve(0, [np.zeros(levels[0].n)], [b])
+    assert st.iterations == ost.iterations == 1 and st.converged
+    assert np.array_equal(download(h, xd, 1)[0], xo[0])
+    c = _cfg(kind, fam)
+    x = upload(h, nl - 1, [x0])
+    st = gmg.solve_outer(h, x, upload(h, nl - 1, [b0]), c)
+    xo, res, ost, rc = o.solve_outer([x0], [b0], c)
+    assert rc == 0 and st.converged and st.iterations == ost.iterations
+    assert np.array_equal(download(h, x, 1)[0], xo[0])

@@ -1,7 +1,7 @@
 """Q2 (BASELINE configs[2]: 64^3 cells, 129^3 dofs, 6 levels, V(3,3)) and rotated Q1
 (configs[3]: 128^3 cells, 6.3M face dofs, lognormal(0,1) coefficient, 7 levels, V(2,2))
 on one B200: setup time, device bytes, finest sweep GB/s, V-cycle ms, solve ms and
-cycles per smoother.  Usage: python tools/fe_run.py [q2|rt|rt1] [levels]"""
+cycles per smoother.  Usage: python tools/fe_run.py [q2|rt|rt1] [levels] [--direct]"""
 import json
 import os
 import sys
@@ -18,13 +18,17 @@ def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "q2"
     family, coef, pp = {"q2": (Q2, CONSTANT, 3), "rt": (ROTATED_Q1, LOGNORMAL, 2),
                         "rt1": (ROTATED_Q1, CONSTANT, 2)}[which]
-    L = int(sys.argv[2]) if len(sys.argv) > 2 else (6 if family == Q2 else 7)
+    args = [a for a in sys.argv[2:] if not a.startswith("--")]
+    direct = "--direct" in sys.argv
+    L = int(args[0]) if args else (6 if family == Q2 else 7)
     t = time.time()
     s = FESetup(family, 2, L, coef, seed=2024)
     t_setup = time.time() - t
     fin = s.levels[-1]
     h = gmg.Hierarchy([s.levels])
-    out = dict(family=which, levels=L, n_global=s.n_global, nnz=int(fin.row_offsets[-1]),
+    if direct:
+        h.set_coarse_direct()
+    out = dict(family=which, levels=L, coarse="direct" if direct else "gauss-seidel", n_global=s.n_global, nnz=int(fin.row_offsets[-1]),
                setup_s=round(t_setup, 2), device_gb=round(h.device_bytes() / 1e9, 2))
     n_own = fin.n_own
     nnz_own = int(fin.row_offsets[n_own])
