@@ -302,6 +302,64 @@ __global__ void __launch_bounds__(kBlock, PF_SOR_MINB) k_color_sweep(SellView A,
     x[row] = __ddiv_rn(acc, diag);
 }
 
+// k_color_sweep for long rows: one block per SELL slice (32 rows), kSplitBlock / 32 warps.
+// Warp w loads groups w, w + 8, ... of all 32 rows (coalesced, as the row kernel's single
+// warp would), gathers x and forms the products a_e x_c into shared memory (entry-major,
+// conflict-free); then warp 0 — lane = row — subtracts them in stored order, skipping the
+// diagonal, and applies the update.  Same operations in the same order as k_color_sweep.
+constexpr int kSplitBlock = 256;
+template <bool kSor, int kVK>
+__global__ void __launch_bounds__(kSplitBlock) k_color_sweep_split(SellView A, double* x, const double* __restrict__ b,
+                                                                  int32_t row0, int32_t row1, double omega,
+                                                                  int32_t width) {
+  extern __shared__ double prod[];  // [width][32]
+  __shared__ double sdiag[32];
+  __shared__ int32_t sdpos[32];
+  PF_PDL_ENTRY();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t slice = (row0 >> 5) + static_cast<int32_t>(blockIdx.x);
+  const int32_t row = slice * 32 + lane;
+  const bool active = row >= row0 && row < row1;
+  const int len = active ? A.row_len[row] : 0;
+  if (w == 0) {
+    sdpos[lane] = -1;
+    sdiag[lane] = 0.0;
+  }
+  __syncthreads();
+  const int64_t base = A.slice_ptr[slice] + 4 * lane;
+  for (int g = w; 4 * g < len; g += kSplitBlock / 32) {
+    int32_t c[4];
+    double v[4];
+    sell_group<kVK>(A, base + 128 * static_cast<int64_t>(g), c, v);
+    double xv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) xv[k] = (4 * g + k < len && c[k] != row) ? __ldg(x + c[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = 4 * g + k;
+      if (j < len) {
+        if (c[k] == row) {
+          sdpos[lane] = j;
+          sdiag[lane] = v[k];
+        } else {
+          prod[j * 32 + lane] = __dmul_rn(v[k], xv[k]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (w != 0 || !active) return;
+  const int dp = sdpos[lane];
+  double acc = b[row];
+  for (int j = 0; j < len; ++j)
+    if (j != dp) acc = __dsub_rn(acc, prod[j * 32 + lane]);
+  const double diag = sdiag[lane];
+  if (kSor)
+    x[row] = __dadd_rn(__dmul_rn(1.0 - omega, x[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
+  else
+    x[row] = __ddiv_rn(acc, diag);
+}
+
 // Residual of the cycle (multigrid.cpp:166-167): y = A x (spmv order, acc from 0), r = b - y,
 // on rows [0, n).
 template <int kVK>

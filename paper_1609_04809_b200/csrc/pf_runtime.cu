@@ -71,12 +71,19 @@ struct Launcher {
   pf_hierarchy* h;
   int64_t* counter;
   cudaStream_t stream = nullptr;  // default: the hierarchy's stream
+  size_t smem = 0;                // dynamic shared memory of the next launch (with_smem)
+  Launcher& with_smem(size_t bytes) {
+    smem = bytes;
+    return *this;
+  }
   template <typename... KArgs, typename... Args>
   void operator()(unsigned grid, unsigned block, void (*kern)(KArgs...), Args... args) {
     if (grid == 0) return;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(grid);
     lc.blockDim = dim3(block);
+    lc.dynamicSmemBytes = smem;
+    smem = 0;
     lc.stream = stream ? stream : h->stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -226,6 +233,7 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
   }
   out.slice_ptr.upload(sptr);
   out.row_len.upload(rlen);
+  out.max_len = rlen.empty() ? 0 : *std::max_element(rlen.begin(), rlen.end());
   encode_values(sv, out.vals);
   out.cols.upload(sc);
   out.nnz = n > 0 ? off[n] : 0;
@@ -266,6 +274,7 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
   }
   out.slice_ptr.upload(sptr);
   out.row_len.upload(rlen);
+  out.max_len = rlen.empty() ? 0 : *std::max_element(rlen.begin(), rlen.end());
   out.nnz = n > 0 ? rowptr[n] : 0;
   out.stored = sptr[n_slices];
 }
@@ -1000,6 +1009,53 @@ void enq_copy(pf_hierarchy* h, const double* src, double* dst, int64_t n) {
   launcher(h)(grid_for(n), kBlock, k_copy, src, dst, n);
 }
 
+// One colour of a coloured sweep.  Levels with long rows (Q2: up to 125 entries) take
+// the slice-split kernel: a colour has few rows there (1/27 of the level), so one thread
+// per row leaves most SMs idle while each thread walks its 32 groups.
+int split_row_len() {
+  static const int v = [] {
+    const char* e = std::getenv("PF_SPLIT_ROW_LEN");
+    return e ? std::atoi(e) : 48;
+  }();
+  return v;
+}
+
+// ... on levels up to PF_SPLIT_MAX_ROWS own rows (default 1M): on larger ones the colours
+// are big enough for the row kernel (Q2 at 64^3: 482 vs 431 us per sweep).
+int64_t split_max_rows() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("PF_SPLIT_MAX_ROWS");
+    return e ? std::atoll(e) : int64_t(1) << 20;
+  }();
+  return v;
+}
+
+void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega, double* x, const double* b) {
+  const int32_t r0 = D.color_start[c], r1 = D.color_start[c + 1];
+  if (r1 <= r0) return;
+  auto launch = launcher(h);
+  const int split = split_row_len();
+  vk_dispatch(D.A.vals.vkind, [&](auto V) {
+    constexpr int vk = decltype(V)::value;
+    if (split > 0 && D.A.max_len > split && D.n_own <= split_max_rows()) {
+      const int32_t width = (D.A.max_len + 3) / 4 * 4;
+      const size_t smem = sizeof(double) * kSlice * static_cast<size_t>(width);
+      auto kern = sor ? k_color_sweep_split<true, vk> : k_color_sweep_split<false, vk>;
+      static thread_local const void* attr_set[2][4] = {};
+      if (smem > 48 * 1024 && attr_set[sor][vk + 1] != reinterpret_cast<const void*>(smem)) {
+        PF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr_set[sor][vk + 1] = reinterpret_cast<const void*>(smem);
+      }
+      const unsigned grid = static_cast<unsigned>(((r1 - 1) >> 5) - (r0 >> 5) + 1);
+      launch.with_smem(smem)(grid, kSplitBlock, kern, view(D.A), x, b, r0, r1, omega, width);
+    } else if (sor) {
+      launch(grid_for(r1 - r0), kBlock, k_color_sweep<true, vk>, view(D.A), x, b, r0, r1, omega);
+    } else {
+      launch(grid_for(r1 - r0), kBlock, k_color_sweep<false, vk>, view(D.A), x, b, r0, r1, 1.0);
+    }
+  });
+}
+
 // smooth (solvers.cpp:56-68) on x (primary buffer) with b.
 // first_done: the first Jacobi sweep already ran (k_jacobi_norm in the solve graph).
 // Returns true when the halo2 scatter that follows a smoothing phase in the cycle was
@@ -1058,16 +1114,7 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
         for (int c = 0; c < max_colors; ++c)
           for (DevLevel& D : L.sub) {
             if (c >= D.n_colors) continue;
-            const int32_t r0 = D.color_start[c], r1 = D.color_start[c + 1];
-            vk_dispatch(D.A.vals.vkind, [&](auto V) {
-              constexpr int vk = decltype(V)::value;
-              if (sor)
-                launch(grid_for(r1 - r0), kBlock, k_color_sweep<true, vk>, view(D.A), bufs[cur] + D.offset,
-                       b + D.offset, r0, r1, sc.damping);
-              else
-                launch(grid_for(r1 - r0), kBlock, k_color_sweep<false, vk>, view(D.A), bufs[cur] + D.offset,
-                       b + D.offset, r0, r1, 1.0);
-            });
+            enq_color_sweep(h, D, c, sor, sor ? sc.damping : 1.0, bufs[cur] + D.offset, b + D.offset);
           }
       }
     }
@@ -2284,11 +2331,7 @@ pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double*
       });
     } else {
       for (int c = 0; c < D.n_colors; ++c)
-        vk_dispatch(D.A.vals.vkind, [&](auto V) {
-          launch(grid_for(D.color_start[c + 1] - D.color_start[c]), kBlock,
-                 k_color_sweep<true, decltype(V)::value>, view(D.A), x->cur(), b, D.color_start[c],
-                 D.color_start[c + 1], kind == PF_SMOOTHER_MULTICOLOR_SOR ? 1.2 : 1.0);
-        });
+        enq_color_sweep(h, D, c, true, kind == PF_SMOOTHER_MULTICOLOR_SOR ? 1.2 : 1.0, x->cur(), b);
     }
   };
   for (int i = 0; i < 3; ++i) one(i);  // warm-up

@@ -95,6 +95,7 @@ struct DevSell {
   DevBuf<int64_t> slice_ptr;
   DevBuf<int32_t> row_len;
   int64_t nnz = 0, own_nnz = 0, stored = 0;
+  int32_t max_len = 0;  // longest row
 };
 
 // One subdomain of one level on the device.
