@@ -330,6 +330,48 @@ def run_b200(args):
                 "note": "fp64 SELL-32x4 values (12 B per entry): the finest sweep at the HBM roofline"}
         lh.close()
 
+    # BASELINE configs[2] (Q2, 64^3 cells, 129^3 dofs, 6 levels, V(3,3)) and configs[3]
+    # (rotated Q1, 128^3 cells, 6.3M face dofs, lognormal(0,1) coefficient, 7 levels):
+    # include/pf_fe.h, direct coarse solve (BASELINE configs[0]'s "coarse direct solve")
+    fe = {}
+    if world == 1 and not args.no_fe:
+        from paper_1609_04809_b200.fe import LOGNORMAL, Q2, ROTATED_Q1, CONSTANT, FESetup
+
+        def fe_variant(family, coef, levels, pp, kind, omega):
+            fs = FESetup(family, 2, levels, coef, seed=2024)
+            fh = gmg.Hierarchy([fs.levels], device=local).set_coarse_direct()
+            fc = gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=kind, damping=omega), pre_smooth=pp,
+                                     post_smooth=pp, outer_tol=W["tol"], outer_max_cycles=400)
+            ftop = levels - 1
+            fx, fb = fh.vector(ftop, fs.x0), fh.vector(ftop, fs.b)
+            fstream = torch.cuda.ExternalStream(fh.stream_handle(), device=torch.device("cuda", local))
+            fst = gmg.solve_outer(fh, fx, fb, fc)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            w0 = time.time()
+            e0.record(fstream)
+            for _ in range(3):
+                fx.upload(fs.x0)
+                fst = gmg.solve_outer(fh, fx, fb, fc)
+            e1.record(fstream)
+            torch.cuda.synchronize()
+            clk.window(w0, time.time())
+            f_ms = e0.elapsed_time(e1) / 3
+            err = float(np.abs(fx.download(0) - fs.exact).max())
+            sw_ms, sw_bytes = fh.time_sweep(ftop, gmg.PF_SMOOTHER_JACOBI, 20)
+            out = {"value": fs.n_global / (f_ms / 1e3), "unit": "DOF/s", "n_global": fs.n_global,
+                   "nnz": int(fs.levels[-1].row_offsets[-1]), "cycles": fst.iterations,
+                   "converged": bool(fst.converged), "ms_per_step": f_ms,
+                   "vcycle_ms": fh.time_vcycle(fx, fb, fc, 10), "max_error_vs_exact": err,
+                   "jacobi_sweep_us": sw_ms * 1e3, "jacobi_sweep_gbs": sw_bytes / (sw_ms / 1e3) / 1e9,
+                   "jacobi_sweep_frac": sw_bytes / (sw_ms / 1e3) / 1e9 / peak, "coarse": "direct"}
+            fh.close()
+            return out
+
+        fe["q2_c3_jacobi_v33"] = fe_variant(Q2, CONSTANT, 6, 3, gmg.PF_SMOOTHER_JACOBI, W["omega"])
+        fe["rotated_q1_c4_lognormal_sor_1.2"] = fe_variant(ROTATED_Q1, LOGNORMAL, 7, 2,
+                                                          gmg.PF_SMOOTHER_MULTICOLOR_SOR, 1.2)
+
     clk.stop()
     clocks = clk.summary()
     if rank != 0:
@@ -367,7 +409,7 @@ def run_b200(args):
             "cycles": st_sor.iterations, "ms_per_step": sor_ms_total / sor_steps,
             "sweep_us": sor_ms * 1e3,
             "sweep_frac": sweep_bytes / (sor_ms / 1e3) / 1e9 / peak},
-            "lognormal_jacobi": logn},
+            "lognormal_jacobi": logn, **fe},
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -535,6 +577,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fe", action="store_true", help="skip the Q2 / rotated-Q1 variants")
     ap.add_argument("--workload", choices=["poisson", "heat"], default="poisson",
                     help="poisson: BASELINE configs[1] (default); heat: the reference's CN run at C2")
     args = ap.parse_args()
