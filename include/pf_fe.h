@@ -61,6 +61,23 @@ pf_status pf_fe_setup_rhs(const pf_fe_setup* s, const double** b, const double**
 pf_status pf_fe_setup_kappa(const pf_fe_setup* s, const double** kappa, int64_t* n);
 pf_status pf_fe_setup_seconds(const pf_fe_setup* s, double* out);
 
+/* Device assembly of a level's system: what the device needs to
+ * recompute every stored entry of the level from the entity lattice, the level's element
+ * matrix and the cell coefficient.  Hand it to pf_fe_assembly_set (pf_gpu.h's pf_assembly,
+ * created on the hierarchy holding this level), then pf_assemble_operator fills a
+ * pf_operator with values equal to the setup's, bit for bit. */
+typedef struct {
+  int32_t family;              /* PF_FE_Q2 or PF_FE_ROTATED_Q1 */
+  int32_t n_cells;             /* N: cells per axis */
+  int32_t n_dofs;
+  const int64_t* keys4;        /* [4 * n_dofs] host order: (0 | orientation, a0, a1, a2) */
+  const uint8_t* is_dirichlet; /* [n_dofs] */
+  const double* elem;          /* the level's element matrix, 27 x 27 or 6 x 6, row-major */
+  const double* kappa;         /* [N^3] cell coefficient (rotated Q1), or NULL (Q2: 1) */
+} pf_fe_assembly_desc;
+pf_status pf_fe_setup_assembly_desc(const pf_fe_setup* s, int level, pf_fe_assembly_desc* out);
+pf_status pf_fe_assembly_set(pf_assembly* a, int subdomain, const pf_fe_assembly_desc* desc);
+
 #ifdef __cplusplus
 }
 #endif

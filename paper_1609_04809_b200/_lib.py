@@ -93,6 +93,11 @@ class AssemblyDesc(C.Structure):
                 ("elem_class", C.c_void_p), ("n_classes", C.c_int32)]
 
 
+class FeAssemblyDesc(C.Structure):
+    _fields_ = [("family", C.c_int32), ("n_cells", C.c_int32), ("n_dofs", C.c_int32), ("keys4", C.c_void_p),
+                ("is_dirichlet", C.c_void_p), ("elem", C.c_void_p), ("kappa", C.c_void_p)]
+
+
 class SetupOptions(C.Structure):
     _fields_ = [("dim", C.c_int32), ("n_coarse", C.c_int32), ("n_levels", C.c_int32), ("n_ranks", C.c_int32),
                 ("rank", C.c_int32), ("problem", C.c_int32), ("dt", C.c_double), ("seed", C.c_uint64),
@@ -140,7 +145,8 @@ EXPORTS = [
     "pf_setup_kappa", "pf_setup_assembly_desc", "pf_setup_create_opts", "pf_setup_release_matrices",
     "pf_hierarchy_set_level_from_setup",
     "pf_fe_setup_create", "pf_fe_setup_destroy", "pf_fe_setup_level", "pf_fe_setup_level_keys",
-    "pf_fe_setup_rhs", "pf_fe_setup_kappa", "pf_fe_setup_seconds",
+    "pf_fe_setup_rhs", "pf_fe_setup_kappa", "pf_fe_setup_seconds", "pf_fe_setup_assembly_desc",
+    "pf_fe_assembly_set",
 ]
 
 _lib = None
@@ -253,6 +259,8 @@ def lib():
         "pf_fe_setup_rhs": [P, PP, PP, PP, i64p],
         "pf_fe_setup_kappa": [P, PP, i64p],
         "pf_fe_setup_seconds": [P, dp],
+        "pf_fe_setup_assembly_desc": [P, C.c_int, C.POINTER(FeAssemblyDesc)],
+        "pf_fe_assembly_set": [P, C.c_int, C.POINTER(FeAssemblyDesc)],
     }
     for name, args in sigs.items():
         f = getattr(L, name)

@@ -67,6 +67,7 @@ struct FeLevel {
   std::vector<int64_t> p_off;
   std::vector<int32_t> p_col;
   std::vector<double> p_w;
+  std::vector<double> elem, kappa;  // element matrix (h included) and cell coefficients
   // lexicographic entity index <-> host index
   std::vector<int32_t> host_of;
   std::vector<int64_t> lex_of;
@@ -660,6 +661,7 @@ void create(pf_fe_setup& s) {
       std::vector<double> Ke(Kref.size());
       for (size_t i = 0; i < Kref.size(); ++i) Ke[i] = h * Kref[i];
       q2_level(*s.levels[static_cast<size_t>(l)], N, Ke);
+      s.levels[static_cast<size_t>(l)]->elem = Ke;
       if (l > 0) q2_prolongation(*s.levels[static_cast<size_t>(l)], *s.levels[static_cast<size_t>(l) - 1]);
     }
     q2_rhs(s);
@@ -686,7 +688,12 @@ void create(pf_fe_setup& s) {
       }
     }
     for (int l = 0; l < nl; ++l) {
-      rt_level(*s.levels[static_cast<size_t>(l)], static_cast<int64_t>(s.n_coarse) << l, Kref, kap[static_cast<size_t>(l)]);
+      FeLevel& L = *s.levels[static_cast<size_t>(l)];
+      rt_level(L, static_cast<int64_t>(s.n_coarse) << l, Kref, kap[static_cast<size_t>(l)]);
+      const double hx = 1.0 / static_cast<double>(static_cast<int64_t>(s.n_coarse) << l);
+      L.elem.resize(36);
+      for (int i = 0; i < 36; ++i) L.elem[static_cast<size_t>(i)] = hx * Kref[static_cast<size_t>(i)];
+      if (l + 1 < nl) L.kappa = kap[static_cast<size_t>(l)];
       if (l > 0) rt_prolongation(*s.levels[static_cast<size_t>(l)], *s.levels[static_cast<size_t>(l) - 1]);
     }
     s.kappa = std::move(kap.back());
@@ -795,6 +802,23 @@ pf_status pf_fe_setup_kappa(const pf_fe_setup* s, const double** kappa, int64_t*
     if (!s || !kappa || !n) invalid("null argument");
     *kappa = s->kappa.data();
     *n = static_cast<int64_t>(s->kappa.size());
+  });
+}
+
+pf_status pf_fe_setup_assembly_desc(const pf_fe_setup* s, int level, pf_fe_assembly_desc* out) {
+  return guard([&] {
+    if (!s || !out) invalid("null argument");
+    if (level < 0 || level >= s->n_levels) invalid("level out of range");
+    const FeLevel& L = *s->levels[static_cast<size_t>(level)];
+    std::memset(out, 0, sizeof *out);
+    out->family = s->family;
+    out->n_cells = static_cast<int32_t>(L.N);
+    out->n_dofs = L.n;
+    out->keys4 = L.keys.data();
+    out->is_dirichlet = L.is_dir.data();
+    out->elem = L.elem.data();
+    if (s->family == PF_FE_ROTATED_Q1)
+      out->kappa = level + 1 == s->n_levels ? s->kappa.data() : L.kappa.data();
   });
 }
 

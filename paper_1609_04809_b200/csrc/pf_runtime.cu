@@ -1667,6 +1667,8 @@ struct pf_assembly {
     pf::DevBuf<int32_t> lattice, cls;
     pf::DevBuf<uint8_t> cell_mask;
     pf::DevBuf<double> kappa, elem;
+    int family = 0;  // 0: Q1 (pf_assembly_desc); PF_FE_Q2 / PF_FE_ROTATED_Q1 (pf_fe_assembly_desc)
+    pf::DevBuf<uint8_t> orient;
   };
   std::vector<Sub> sub;
 };
@@ -2595,6 +2597,7 @@ pf_status pf_assembly_set(pf_assembly* a, int sub, const pf_assembly_desc* d) {
   const int64_t nel = d->dim == 3 ? int64_t(d->n_classes) * d->n_classes * d->n_classes
                                   : int64_t(d->n_classes) * d->n_classes;
   pf_assembly::Sub& S = a->sub[static_cast<size_t>(sub)];
+  S.family = 0;
   S.dim = d->dim;
   S.N = d->n_cells;
   S.nh = d->n_classes;
@@ -2605,6 +2608,39 @@ pf_status pf_assembly_set(pf_assembly* a, int sub, const pf_assembly_desc* d) {
   S.cls.upload(std::vector<int32_t>(d->elem_class, d->elem_class + 3 * N));
   S.elem.upload(std::vector<double>(d->elem, d->elem + 64 * nel));
   if (d->kappa) S.kappa.upload(std::vector<double>(d->kappa, d->kappa + ncells));
+  else S.kappa.reset();
+  S.set = true;
+  PF_API_END
+}
+
+pf_status pf_fe_assembly_set(pf_assembly* a, int sub, const pf_fe_assembly_desc* d) {
+  PF_API_BEGIN
+  if (!a || !d) invalid("null argument");
+  pf_hierarchy* h = a->h;
+  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
+  const DevLevel& D = h->levels[a->level].sub[sub];
+  if (d->n_dofs != D.n) invalid("assembly description does not match the level's dof count");
+  if (d->family != PF_FE_Q2 && d->family != PF_FE_ROTATED_Q1) invalid("unknown element family");
+  if (!d->keys4 || !d->elem || d->n_cells < 1 || (d->family == PF_FE_ROTATED_Q1 && !d->kappa))
+    invalid("null assembly array");
+  PF_CUDA(cudaSetDevice(h->device));
+  const int32_t n = D.n;
+  std::vector<int32_t> lat(static_cast<size_t>(3 * n));
+  std::vector<uint8_t> ori(static_cast<size_t>(n));
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t r = D.perm[i];
+    for (int k = 0; k < 3; ++k) lat[3 * static_cast<size_t>(r) + k] = static_cast<int32_t>(d->keys4[4 * static_cast<int64_t>(i) + 1 + k]);
+    ori[static_cast<size_t>(r)] = static_cast<uint8_t>(d->keys4[4 * static_cast<int64_t>(i)]);
+  }
+  const int64_t N = d->n_cells;
+  pf_assembly::Sub& S = a->sub[static_cast<size_t>(sub)];
+  S.family = d->family;
+  S.dim = 3;
+  S.N = d->n_cells;
+  S.lattice.upload(lat);
+  S.orient.upload(ori);
+  S.elem.upload(std::vector<double>(d->elem, d->elem + (d->family == PF_FE_Q2 ? 27 * 27 : 36)));
+  if (d->kappa) S.kappa.upload(std::vector<double>(d->kappa, d->kappa + N * N * N));
   else S.kappa.reset();
   S.set = true;
   PF_API_END
@@ -2628,6 +2664,15 @@ pf_status pf_assemble_operator(pf_assembly* a, pf_operator* op) {
       out.vkind = 0;
       out.vals.alloc(D.A.stored);
       PF_CUDA(cudaMemsetAsync(out.vals.p, 0, sizeof(double) * static_cast<size_t>(D.A.stored), h->stream));
+    }
+    if (S.family != 0) {
+      const FeAsmView fv{S.lattice.p, S.orient.p, D.d_is_dir.p, S.elem.p, S.kappa.p, S.N};
+      if (S.family == PF_FE_Q2)
+        launch(grid_for(D.n), kBlock, k_fe_assemble<PF_FE_Q2>, fv, view(D.A), out.vals.p, D.n);
+      else
+        launch(grid_for(D.n), kBlock, k_fe_assemble<PF_FE_ROTATED_Q1>, fv, view(D.A), out.vals.p, D.n);
+      op->set[static_cast<size_t>(s)] = true;
+      continue;
     }
     const AsmView v{S.lattice.p, S.cell_mask.p, D.d_is_dir.p, S.kappa.p, S.elem.p, S.cls.p, S.N, S.nh, S.n_coarse,
                     S.grid_level};

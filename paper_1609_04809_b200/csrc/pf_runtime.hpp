@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "pf_gpu.h"
+#include "pf_fe.h"
 #include "pf_types.hpp"
 
 namespace pf {

@@ -20,7 +20,7 @@ class FESetup:
     constant-coefficient solution sin(pi x) sin(pi y) sin(pi z)."""
 
     def __init__(self, family: int, n_coarse: int, n_levels: int, coefficient: int = CONSTANT,
-                 seed: int = 2024):
+                 seed: int = 2024, keep: bool = False):
         L = _lib.lib()
         self._h = C.c_void_p()
         _lib.check(L.pf_fe_setup_create(family, n_coarse, n_levels, coefficient, seed, C.byref(self._h)),
@@ -41,10 +41,32 @@ class FESetup:
             s = C.c_double()
             _lib.check(L.pf_fe_setup_seconds(self._h, C.byref(s)), setup="fe")
             self.seconds = s.value
-        finally:
-            L.pf_fe_setup_destroy(self._h)
-            self._h = None
+        except BaseException:
+            self.close()
+            raise
+        if not keep:
+            self.close()
         self.n_global = self.levels[-1].n
+
+    def close(self):
+        if self._h:
+            _lib.lib().pf_fe_setup_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def assembly_desc(self, level: int) -> _lib.FeAssemblyDesc:
+        """The device assembly description of a level (needs keep=True; pointers valid while
+        this setup lives)."""
+        if not self._h:
+            raise _lib.PfError("native setup released: build it with keep=True")
+        d = _lib.FeAssemblyDesc()
+        _lib.check(_lib.lib().pf_fe_setup_assembly_desc(self._h, level, C.byref(d)), setup="fe")
+        return d
 
     def _level(self, l: int) -> LevelArrays:
         L = _lib.lib()

@@ -197,8 +197,9 @@ class HeatRun:
 
 
 class Assembly:
-    """Device assembly of a level's Q1 stiffness system (pf_assembly_*; assemble_system +
-    apply_dirichlet_rows, assembly.cpp:103-170), optionally with a per-cell coefficient."""
+    """Device assembly of a level's stiffness system (pf_assembly_*; assemble_system +
+    apply_dirichlet_rows, assembly.cpp:103-170): Q1 with an optional per-cell coefficient
+    (pf_assembly_desc), or Q2 / rotated Q1 (pf_fe_assembly_desc, FESetup.assembly_desc)."""
 
     def __init__(self, h: Hierarchy, level: int, descs):
         self.h, self.level = h, level
@@ -206,7 +207,10 @@ class Assembly:
         _lib.check(_lib.lib().pf_assembly_create(h._h, level, C.byref(self._p)))
         h._vectors.add(self)
         for s, d in enumerate(descs):
-            _lib.check(_lib.lib().pf_assembly_set(self._p, s, C.byref(d)))
+            if isinstance(d, _lib.FeAssemblyDesc):  # Q2 / rotated Q1 (pf_fe.h)
+                _lib.check(_lib.lib().pf_fe_assembly_set(self._p, s, C.byref(d)))
+            else:
+                _lib.check(_lib.lib().pf_assembly_set(self._p, s, C.byref(d)))
 
     def assemble(self, op: Operator) -> Operator:
         _lib.check(_lib.lib().pf_assemble_operator(self._p, op._p))

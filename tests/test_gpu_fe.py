@@ -116,3 +116,18 @@ def test_direct_coarse_solve_bit_exact(cuda, family, coef, L, kind):
     xo, res, ost, rc = o.solve_outer([x0], [b0], c)
     assert rc == 0 and st.converged and st.iterations == ost.iterations
     assert np.array_equal(download(h, x, 1)[0], xo[0])
+
+
+@pytest.mark.parametrize("family,coef", [(Q2, CONSTANT), (ROTATED_Q1, LOGNORMAL), (ROTATED_Q1, CONSTANT)],
+                         ids=["q2", "rt_lognormal", "rt"])
+def test_device_assembly_equals_setup(cuda, family, coef):
+    """pf_fe_assembly_set + pf_assemble_operator: every level's system recomputed on the
+    device (entity lattice, element matrix, cell coefficient) equals the setup's values bit
+    for bit, Dirichlet rows included."""
+    from paper_1609_04809_b200.heat import Assembly, Operator
+    s = FESetup(family, 2, 4, coef, seed=8, keep=True)
+    h = gmg.Hierarchy([s.levels])
+    for l, lv in enumerate(s.levels):
+        op = Assembly(h, l, [s.assembly_desc(l)]).assemble(Operator(h, l))
+        assert np.array_equal(op.values(0, len(lv.vals)), lv.vals), l
+    s.close()

@@ -22,7 +22,7 @@ def main():
     direct = "--direct" in sys.argv
     L = int(args[0]) if args else (6 if family == Q2 else 7)
     t = time.time()
-    s = FESetup(family, 2, L, coef, seed=2024)
+    s = FESetup(family, 2, L, coef, seed=2024, keep=True)
     t_setup = time.time() - t
     fin = s.levels[-1]
     h = gmg.Hierarchy([s.levels])
@@ -30,6 +30,20 @@ def main():
         h.set_coarse_direct()
     out = dict(family=which, levels=L, coarse="direct" if direct else "gauss-seidel", n_global=s.n_global, nnz=int(fin.row_offsets[-1]),
                setup_s=round(t_setup, 2), device_gb=round(h.device_bytes() / 1e9, 2))
+    # device assembly of the finest system (pf_fe_assembly_set + pf_assemble_operator)
+    from paper_1609_04809_b200.heat import Assembly, Operator
+    asm, op = Assembly(h, L - 1, [s.assembly_desc(L - 1)]), Operator(h, L - 1)
+    ta = []
+    for _ in range(4):
+        t0 = time.time()
+        asm.assemble(op)
+        ta.append(time.time() - t0)
+    out["device_assembly_ms"] = round(min(ta[1:]) * 1e3, 3)
+    out["device_assembly_equal"] = bool(np.array_equal(op.values(0, len(fin.vals)), fin.vals))
+    out["host_setup_all_levels_s"] = round(s.seconds, 2)
+    asm.close()
+    op.close()
+    s.close()
     n_own = fin.n_own
     nnz_own = int(fin.row_offsets[n_own])
     for kind, omega, name in [(gmg.PF_SMOOTHER_JACOBI, 0.8, "jacobi"), (gmg.PF_SMOOTHER_MULTICOLOR_SOR, 1.2, "sor")]:
