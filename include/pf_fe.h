@@ -48,6 +48,14 @@ const char* pf_fe_last_error(void);
  * sin(pi z), g = 0, x0 = 0.  Q2 takes PF_COEF_CONSTANT only. */
 pf_status pf_fe_setup_create(int family, int n_coarse, int n_levels, int coefficient, uint64_t seed,
                              pf_fe_setup** out);
+/* One rank of a box partition: the coarse cells split by coordinate bisection (as
+ * pf_setup.h), each rank's subdomain its own cells plus one cell layer.  Own entities are
+ * those whose lowest-ranked owning cell is this rank's; every other local non-Dirichlet
+ * entity is a Slave of its owner on the master/slave channel (no halo channels: the
+ * scatter after each sweep refreshes every copy, and AccumulateThenScatter gathers the
+ * restricted partial sums of every copy).  n_ranks = 1 is pf_fe_setup_create. */
+pf_status pf_fe_setup_create_part(int family, int n_coarse, int n_levels, int coefficient, uint64_t seed,
+                                  int n_ranks, int rank, pf_fe_setup** out);
 pf_status pf_fe_setup_destroy(pf_fe_setup* s);
 /* Level data (level 0 = coarsest); pointers valid until pf_fe_setup_destroy. */
 pf_status pf_fe_setup_level(const pf_fe_setup* s, int level, pf_level_desc* out);

@@ -144,7 +144,7 @@ EXPORTS = [
     "pf_setup_load_desc", "pf_setup_scales", "pf_setup_export_matrixmarket", "pf_setup_create_lognormal",
     "pf_setup_kappa", "pf_setup_assembly_desc", "pf_setup_create_opts", "pf_setup_release_matrices",
     "pf_hierarchy_set_level_from_setup",
-    "pf_fe_setup_create", "pf_fe_setup_destroy", "pf_fe_setup_level", "pf_fe_setup_level_keys",
+    "pf_fe_setup_create", "pf_fe_setup_create_part", "pf_fe_setup_destroy", "pf_fe_setup_level", "pf_fe_setup_level_keys",
     "pf_fe_setup_rhs", "pf_fe_setup_kappa", "pf_fe_setup_seconds", "pf_fe_setup_assembly_desc",
     "pf_fe_assembly_set",
 ]
@@ -253,6 +253,7 @@ def lib():
         "pf_setup_counts": [P, C.c_int, i64p, i64p, i64p, i64p],
         "pf_setup_seconds": [P, dp],
         "pf_fe_setup_create": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, PP],
+        "pf_fe_setup_create_part": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, PP],
         "pf_fe_setup_destroy": [P],
         "pf_fe_setup_level": [P, C.c_int, C.POINTER(LevelDesc)],
         "pf_fe_setup_level_keys": [P, C.c_int, PP, PP],

@@ -26,6 +26,8 @@
 
 #include "pf_coef.hpp"
 
+std::vector<int> pf_coarse_partition(int d, int n, int k);  // pf_setup.cpp
+
 namespace {
 
 struct FeError : std::runtime_error {
@@ -37,7 +39,7 @@ struct FeError : std::runtime_error {
 thread_local std::string g_fe_err;
 
 const double kPi = std::acos(-1.0);
-constexpr uint8_t kIndep = 1, kDirichlet = 7;  // DofClass (femapper.hpp:16-25)
+constexpr uint8_t kIndep = 1, kSlaveCls = 4, kDirichlet = 7;  // DofClass (femapper.hpp:16-25)
 
 // Gauss-Legendre rules on [0, 1]
 struct Rule {
@@ -68,13 +70,20 @@ struct FeLevel {
   std::vector<int32_t> p_col;
   std::vector<double> p_w;
   std::vector<double> elem, kappa;  // element matrix (h included) and cell coefficients
+  struct Chan {
+    int32_t peer;
+    std::vector<int32_t> send, recv;
+  };
+  std::vector<Chan> chans;               // master/slave channels, peers ascending
+  std::vector<pf_channel_desc> descs;
   // lexicographic entity index <-> host index
   std::vector<int32_t> host_of;
   std::vector<int64_t> lex_of;
 };
 
 struct pf_fe_setup {
-  int family = 0, n_coarse = 2, n_levels = 1, coefficient = 0;
+  int family = 0, n_coarse = 2, n_levels = 1, coefficient = 0, n_ranks = 1, rank = 0;
+  std::vector<int> coarse_owner;
   uint64_t seed = 0;
   std::vector<std::unique_ptr<FeLevel>> levels;
   std::vector<double> b, x0, exact, kappa;
@@ -83,29 +92,133 @@ struct pf_fe_setup {
 
 namespace {
 
-// Host order: own entities (interior) first, then Dirichlet ones, each lexicographic.
-void number(FeLevel& L, int64_t n_lex, const std::vector<uint8_t>& boundary) {
-  L.host_of.assign(static_cast<size_t>(n_lex), 0);
-  L.lex_of.assign(static_cast<size_t>(n_lex), 0);
-  int64_t own = 0;
-  for (int64_t e = 0; e < n_lex; ++e) own += boundary[static_cast<size_t>(e)] ? 0 : 1;
-  int64_t a = 0, d = own;
+// One rank's view of a level: the owner of every cell (coordinate bisection of the coarse
+// cells, inherited by their descendants) and, per rank, its local cells = own cells plus
+// the one-cell layer around them (the reference's subdomain: partition.cpp:156-365).
+struct Region {
+  int64_t N = 0;
+  int rank = 0, n_ranks = 1;
+  std::vector<int8_t> owner;                // [N^3]
+  std::vector<std::vector<uint8_t>> local;  // [rank][N^3]
+  bool is_local(int64_t cell) const { return local[static_cast<size_t>(rank)][static_cast<size_t>(cell)] != 0; }
+};
+
+Region make_region(const pf_fe_setup& s, int level) {
+  Region R;
+  const int64_t N = static_cast<int64_t>(s.n_coarse) << level, nc = s.n_coarse;
+  R.N = N;
+  R.rank = s.rank;
+  R.n_ranks = s.n_ranks;
+  R.owner.resize(static_cast<size_t>(N * N * N));
+#pragma omp parallel for schedule(static)
+  for (int64_t c = 0; c < N * N * N; ++c) {
+    const int64_t x = c / (N * N) >> level, y = (c / N) % N >> level, z = c % N >> level;
+    R.owner[static_cast<size_t>(c)] = static_cast<int8_t>(s.coarse_owner[static_cast<size_t>((x * nc + y) * nc + z)]);
+  }
+  R.local.assign(static_cast<size_t>(s.n_ranks), std::vector<uint8_t>(static_cast<size_t>(N * N * N), 0));
+  for (int r = 0; r < s.n_ranks; ++r) {
+    auto& L = R.local[static_cast<size_t>(r)];
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < N * N * N; ++c) {
+      const int64_t x = c / (N * N), y = (c / N) % N, z = c % N;
+      uint8_t any = 0;
+      for (int64_t dx = -1; dx <= 1 && !any; ++dx)
+        for (int64_t dy = -1; dy <= 1 && !any; ++dy)
+          for (int64_t dz = -1; dz <= 1 && !any; ++dz) {
+            const int64_t u = x + dx, v = y + dy, w = z + dz;
+            if (u < 0 || v < 0 || w < 0 || u >= N || v >= N || w >= N) continue;
+            if (R.owner[static_cast<size_t>((u * N + v) * N + w)] == r) any = 1;
+          }
+      L[static_cast<size_t>(c)] = any;
+    }
+  }
+  return R;
+}
+
+enum : int8_t { kNotLocal = -1, kOwn = 0, kSlave = 1, kDir = 2 };
+
+// Host order: own entities first, then slaves (owned by another rank), then Dirichlet
+// ones, each lexicographic.  cls[e]: kNotLocal / kOwn / kSlave / kDir; owner[e]: the
+// lowest rank whose own cells contain e.
+void number(FeLevel& L, int64_t n_lex, const std::vector<int8_t>& cls, const std::vector<int8_t>& owner, int rank) {
+  L.host_of.assign(static_cast<size_t>(n_lex), -1);
+  int64_t cnt[3] = {0, 0, 0};
+  for (int64_t e = 0; e < n_lex; ++e)
+    if (cls[static_cast<size_t>(e)] >= 0) ++cnt[cls[static_cast<size_t>(e)]];
+  const int64_t n = cnt[0] + cnt[1] + cnt[2];
+  if (n > INT32_MAX) invalid("level too large for int32 dof indices");
+  int64_t next[3] = {0, cnt[0], cnt[0] + cnt[1]};
+  L.lex_of.assign(static_cast<size_t>(n), 0);
+  L.n = static_cast<int32_t>(n);
+  L.n_own = static_cast<int32_t>(cnt[0]);
+  L.owns_row.assign(static_cast<size_t>(n), 0);
+  L.is_dir.assign(static_cast<size_t>(n), 0);
+  L.class_of.assign(static_cast<size_t>(n), kIndep);
   for (int64_t e = 0; e < n_lex; ++e) {
-    const int64_t h = boundary[static_cast<size_t>(e)] ? d++ : a++;
+    const int8_t c = cls[static_cast<size_t>(e)];
+    if (c < 0) continue;
+    const int64_t h = next[c]++;
     L.host_of[static_cast<size_t>(e)] = static_cast<int32_t>(h);
     L.lex_of[static_cast<size_t>(h)] = e;
-  }
-  if (n_lex > INT32_MAX) invalid("level too large for int32 dof indices");
-  L.n = static_cast<int32_t>(n_lex);
-  L.n_own = static_cast<int32_t>(own);
-  L.owns_row.assign(static_cast<size_t>(n_lex), 1);  // one subdomain: every row is authoritative
-  L.is_dir.assign(static_cast<size_t>(n_lex), 0);
-  L.class_of.assign(static_cast<size_t>(n_lex), kIndep);
-  for (int64_t h = own; h < n_lex; ++h) {
-    L.is_dir[static_cast<size_t>(h)] = 1;
-    L.class_of[static_cast<size_t>(h)] = kDirichlet;
+    // authoritative rows (femapper.cpp:214-217): own ones and the Dirichlet ones this rank owns
+    L.owns_row[static_cast<size_t>(h)] = (c == kOwn || (c == kDir && owner[static_cast<size_t>(e)] == rank)) ? 1 : 0;
+    L.is_dir[static_cast<size_t>(h)] = c == kDir ? 1 : 0;
+    L.class_of[static_cast<size_t>(h)] = c == kOwn ? kIndep : c == kSlave ? kSlaveCls : kDirichlet;
   }
   L.order.assign(L.lex_of.begin(), L.lex_of.end());
+}
+
+// Classify every entity of a level and build the master/slave channels: an entity is
+// local when one of its cells is; its owner is the lowest rank whose own cells contain
+// it; every local non-own, non-Dirichlet copy is a Slave of its owner, refreshed by the
+// master/slave scatter after each sweep (so no halo channels are needed) and accumulated
+// into the owner by AccumulateThenScatter after the restriction.
+template <typename CellsOf>
+void classify(FeLevel& L, const Region& R, int64_t n_lex, CellsOf cells_of, const std::vector<uint8_t>& boundary) {
+  std::vector<int8_t> cls(static_cast<size_t>(n_lex), kNotLocal), owner(static_cast<size_t>(n_lex), 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < n_lex; ++e) {
+    int64_t cells[8];
+    const int nc = cells_of(e, cells);
+    bool local = false;
+    int own = 127;
+    for (int k = 0; k < nc; ++k) {
+      local = local || R.is_local(cells[k]);
+      own = std::min<int>(own, R.owner[static_cast<size_t>(cells[k])]);
+    }
+    owner[static_cast<size_t>(e)] = static_cast<int8_t>(own);
+    if (!local) continue;
+    cls[static_cast<size_t>(e)] = boundary[static_cast<size_t>(e)] ? kDir : own == R.rank ? kOwn : kSlave;
+  }
+  number(L, n_lex, cls, owner, R.rank);
+  // channels: to peer p, my own entities that p holds (one of their cells is local to p);
+  // from p, my slaves owned by p; both in lexicographic order, so the i-th entries match
+  L.chans.clear();
+  for (int p = 0; p < R.n_ranks; ++p) {
+    if (p == R.rank) continue;
+    FeLevel::Chan ch;
+    ch.peer = p;
+    const auto& lp = R.local[static_cast<size_t>(p)];
+    for (int64_t h = 0; h < L.n; ++h) {
+      const int64_t e = L.lex_of[static_cast<size_t>(h)];
+      if (h < L.n_own) {
+        int64_t cells[8];
+        const int nc = cells_of(e, cells);
+        for (int k = 0; k < nc; ++k)
+          if (lp[static_cast<size_t>(cells[k])]) {
+            ch.send.push_back(static_cast<int32_t>(h));
+            break;
+          }
+      } else if (!L.is_dir[static_cast<size_t>(h)] && owner[static_cast<size_t>(e)] == p) {
+        ch.recv.push_back(static_cast<int32_t>(h));
+      }
+    }
+    if (!ch.send.empty() || !ch.recv.empty()) L.chans.push_back(std::move(ch));
+  }
+  L.descs.clear();
+  for (const auto& c : L.chans)
+    L.descs.push_back(pf_channel_desc{PF_CH_MASTER_SLAVE, c.peer, static_cast<int32_t>(c.send.size()),
+                                      static_cast<int32_t>(c.recv.size()), c.send.data(), c.recv.data()});
 }
 
 // Rows as (column, value) lists sorted by host column; row_fn(h, out) appends a row.
@@ -224,25 +337,31 @@ int q2_cells(int64_t i, int64_t N, int64_t* out) {
   return n;
 }
 
-// nodes along one axis sharing a cell with node i
-int q2_nbrs(int64_t i, int64_t M, int64_t* out) {
-  int n = 0;
-  const int64_t r = (i & 1) ? 1 : 2;
-  for (int64_t j = i - r; j <= i + r; ++j)
-    if (j >= 0 && j < M) out[n++] = j;
-  return n;
-}
 
-void q2_level(FeLevel& L, int64_t N, const std::vector<double>& Ke) {
-  const int64_t M = 2 * N + 1;
+// The row of entity e: the entities of its local cells, each entry summed over the local
+// cells containing both entities in ascending cell order (own rows: all their cells are
+// local, so the sum is the global one); Dirichlet rows keep the pattern with identity values.
+void q2_level(FeLevel& L, const Region& R, const std::vector<double>& Ke) {
+  const int64_t N = R.N, M = 2 * N + 1;
   L.N = N;
+  auto cells_of = [N, M](int64_t e, int64_t* cells) {
+    const int64_t p[3] = {e / (M * M), (e / M) % M, e % M};
+    int64_t pc[3][2];
+    int np[3];
+    for (int t = 0; t < 3; ++t) np[t] = q2_cells(p[t], N, pc[t]);
+    int n = 0;
+    for (int x = 0; x < np[0]; ++x)
+      for (int y = 0; y < np[1]; ++y)
+        for (int z = 0; z < np[2]; ++z) cells[n++] = (pc[0][x] * N + pc[1][y]) * N + pc[2][z];
+    return n;
+  };
   std::vector<uint8_t> bnd(static_cast<size_t>(M * M * M));
   for (int64_t i = 0; i < M; ++i)
     for (int64_t j = 0; j < M; ++j)
       for (int64_t k = 0; k < M; ++k)
         bnd[static_cast<size_t>((i * M + j) * M + k)] =
             (i == 0 || j == 0 || k == 0 || i == M - 1 || j == M - 1 || k == M - 1) ? 1 : 0;
-  number(L, M * M * M, bnd);
+  classify(L, R, M * M * M, cells_of, bnd);
   L.keys.resize(static_cast<size_t>(L.n) * 4);
   L.color.resize(static_cast<size_t>(L.n_own));
   auto cls = [](int64_t i) { return (i & 1) ? 2 : ((i & 3) == 0 ? 0 : 1); };
@@ -259,46 +378,45 @@ void q2_level(FeLevel& L, int64_t N, const std::vector<double>& Ke) {
   build_csr(L, [&](int64_t h, std::vector<std::pair<int32_t, double>>& row, bool values) {
     const int64_t e = L.lex_of[static_cast<size_t>(h)];
     const int64_t p[3] = {e / (M * M), (e / M) % M, e % M};
-    int64_t nb[3][5];
-    int nn[3];
-    for (int a = 0; a < 3; ++a) nn[a] = q2_nbrs(p[a], M, nb[a]);
-    const bool dir = h >= L.n_own;
-    int64_t pc[3][2];
-    int npc[3];
-    for (int a = 0; a < 3; ++a) npc[a] = q2_cells(p[a], N, pc[a]);
-    for (int x = 0; x < nn[0]; ++x)
-      for (int y = 0; y < nn[1]; ++y)
-        for (int z = 0; z < nn[2]; ++z) {
-          const int64_t c[3] = {nb[0][x], nb[1][y], nb[2][z]};
-          const int32_t col = L.host_of[static_cast<size_t>((c[0] * M + c[1]) * M + c[2])];
-          double v = 0.0;
-          if (values) {
-            if (dir) {
-              v = col == h ? 1.0 : 0.0;
-            } else {
-              // cells containing both nodes, per axis, ascending -> ascending cell order
-              int64_t sc[3][2];
-              int ns[3];
-              for (int a = 0; a < 3; ++a) {
-                int64_t qc[2];
-                const int nq = q2_cells(c[a], N, qc);
-                ns[a] = 0;
-                for (int u = 0; u < npc[a]; ++u)
-                  for (int w = 0; w < nq; ++w)
-                    if (pc[a][u] == qc[w]) sc[a][ns[a]++] = pc[a][u];
-              }
-              for (int u = 0; u < ns[0]; ++u)
-                for (int w = 0; w < ns[1]; ++w)
-                  for (int t = 0; t < ns[2]; ++t) {
-                    const int64_t cc[3] = {sc[0][u], sc[1][w], sc[2][t]};
-                    const int la = static_cast<int>(((p[0] - 2 * cc[0]) * 3 + (p[1] - 2 * cc[1])) * 3 + (p[2] - 2 * cc[2]));
-                    const int lb = static_cast<int>(((c[0] - 2 * cc[0]) * 3 + (c[1] - 2 * cc[1])) * 3 + (c[2] - 2 * cc[2]));
-                    v += Ke[static_cast<size_t>(la * 27 + lb)];
-                  }
-            }
+    int64_t cells[8];
+    const int nall = cells_of(e, cells);
+    int nc = 0;
+    for (int k = 0; k < nall; ++k)
+      if (R.is_local(cells[k])) cells[nc++] = cells[k];
+    if (h < L.n_own && nc != nall) invalid("own row with a non-local cell");
+    const bool dir = L.is_dir[static_cast<size_t>(h)] != 0;
+    // the nodes of the local cells, each once, lexicographic
+    int64_t cand[216];
+    int nn = 0;
+    for (int k = 0; k < nc; ++k) {
+      const int64_t cx = cells[k] / (N * N), cy = (cells[k] / N) % N, cz = cells[k] % N;
+      for (int q = 0; q < 27; ++q)
+        cand[nn++] = ((2 * cx + q / 9) * M + 2 * cy + (q / 3) % 3) * M + 2 * cz + q % 3;
+    }
+    std::sort(cand, cand + nn);
+    nn = static_cast<int>(std::unique(cand, cand + nn) - cand);
+    for (int u = 0; u < nn; ++u) {
+      const int64_t f = cand[u];
+      const int32_t col = L.host_of[static_cast<size_t>(f)];
+      double v = 0.0;
+      if (values) {
+        if (dir) {
+          v = col == h ? 1.0 : 0.0;
+        } else {
+          const int64_t q[3] = {f / (M * M), (f / M) % M, f % M};
+          for (int k = 0; k < nc; ++k) {
+            const int64_t cc[3] = {cells[k] / (N * N), (cells[k] / N) % N, cells[k] % N};
+            bool in = true;
+            for (int t = 0; t < 3; ++t) in = in && q[t] >= 2 * cc[t] && q[t] <= 2 * cc[t] + 2;
+            if (!in) continue;
+            const int la = static_cast<int>(((p[0] - 2 * cc[0]) * 3 + (p[1] - 2 * cc[1])) * 3 + (p[2] - 2 * cc[2]));
+            const int lb = static_cast<int>(((q[0] - 2 * cc[0]) * 3 + (q[1] - 2 * cc[1])) * 3 + (q[2] - 2 * cc[2]));
+            v += Ke[static_cast<size_t>(la * 27 + lb)];
           }
-          row.emplace_back(col, v);
         }
+      }
+      row.emplace_back(col, v);
+    }
   });
 }
 
@@ -331,9 +449,11 @@ void q2_prolongation(FeLevel& F, const FeLevel& Cl) {
     for (int a = 0; a < 3; ++a) n[a] = q2_pw(p[a], c[a], w[a]);
     for (int x = 0; x < n[0]; ++x)
       for (int y = 0; y < n[1]; ++y)
-        for (int z = 0; z < n[2]; ++z)
-          row.emplace_back(Cl.host_of[static_cast<size_t>((c[0][x] * Mc + c[1][y]) * Mc + c[2][z])],
-                           (w[0][x] * w[1][y]) * w[2][z]);
+        for (int z = 0; z < n[2]; ++z) {
+          const int32_t col = Cl.host_of[static_cast<size_t>((c[0][x] * Mc + c[1][y]) * Mc + c[2][z])];
+          if (col < 0) invalid("prolongation reaches a non-local coarse node");
+          row.emplace_back(col, (w[0][x] * w[1][y]) * w[2][z]);
+        }
   });
 }
 
@@ -467,10 +587,18 @@ int64_t rt_face_of(const Faces& Fc, int64_t cell, int s) {
   return Fc.lex(o, a);
 }
 
-void rt_level(FeLevel& L, int64_t N, const std::vector<double>& Kref, const std::vector<double>& kappa) {
+void rt_level(FeLevel& L, const Region& R, const std::vector<double>& Kref, const std::vector<double>& kappa) {
+  const int64_t N = R.N;
   L.N = N;
   const Faces Fc{N, N * N * (N + 1)};
   const int64_t n_lex = 3 * Fc.per;
+  auto cells_of = [&Fc](int64_t e, int64_t* cells) {
+    int o;
+    int64_t a[3];
+    Fc.unlex(e, &o, a);
+    int slot[2];
+    return rt_cells(Fc, o, a, cells, slot);
+  };
   std::vector<uint8_t> bnd(static_cast<size_t>(n_lex));
   for (int64_t e = 0; e < n_lex; ++e) {
     int o;
@@ -478,7 +606,7 @@ void rt_level(FeLevel& L, int64_t N, const std::vector<double>& Kref, const std:
     Fc.unlex(e, &o, a);
     bnd[static_cast<size_t>(e)] = (a[o] == 0 || a[o] == N) ? 1 : 0;
   }
-  number(L, n_lex, bnd);
+  classify(L, R, n_lex, cells_of, bnd);
   L.keys.resize(static_cast<size_t>(L.n) * 4);
   L.color.resize(static_cast<size_t>(L.n_own));
   for (int64_t h = 0; h < L.n; ++h) {
@@ -501,9 +629,17 @@ void rt_level(FeLevel& L, int64_t N, const std::vector<double>& Kref, const std:
     Fc.unlex(L.lex_of[static_cast<size_t>(h)], &o, a);
     int64_t cell[2];
     int slot[2];
-    const int nc = rt_cells(Fc, o, a, cell, slot);
-    const bool dir = h >= L.n_own;
-    // the faces of the face's cells, each once: cell 0's six, then cell 1's other five
+    const int nall = rt_cells(Fc, o, a, cell, slot);
+    int nc = 0;
+    for (int k = 0; k < nall; ++k)
+      if (R.is_local(cell[k])) {
+        cell[nc] = cell[k];
+        slot[nc] = slot[k];
+        ++nc;
+      }
+    if (h < L.n_own && nc != nall) invalid("own row with a non-local cell");
+    const bool dir = L.is_dir[static_cast<size_t>(h)] != 0;
+    // the faces of the face's local cells, each once: cell 0's six, then cell 1's other five
     for (int k = 0; k < nc; ++k)
       for (int s2 = 0; s2 < 6; ++s2) {
         if (k == 1 && s2 == slot[1]) continue;  // the face itself, already listed by cell 0
@@ -530,7 +666,7 @@ void rt_prolongation(FeLevel& F, const FeLevel& Cl) {
   const Faces Ff{F.N, F.N * F.N * (F.N + 1)}, Fcn{Cl.N, Cl.N * Cl.N * (Cl.N + 1)};
   const int64_t Nc = Cl.N;
   build_p(F, [&](int64_t h, std::vector<std::pair<int32_t, double>>& row) {
-    if (h >= F.n_own) return;
+    if (F.is_dir[static_cast<size_t>(h)]) return;
     int o;
     int64_t a[3];
     Ff.unlex(F.lex_of[static_cast<size_t>(h)], &o, a);
@@ -577,6 +713,7 @@ void rt_prolongation(FeLevel& F, const FeLevel& Cl) {
           w = (Xo[k] == 0.0 ? 0.25 : 0.0) + 0.5 * (sg * m[o2]);
         if (w == 0.0) continue;
         const int32_t col = Cl.host_of[static_cast<size_t>(rt_face_of(Fcn, cell, s2))];
+        if (col < 0) invalid("prolongation reaches a non-local coarse face");
         const double ws = scale * w;
         bool merged = false;
         for (auto& [cc, ww] : row)
@@ -649,6 +786,7 @@ void rt_rhs(pf_fe_setup& s) {
 
 void create(pf_fe_setup& s) {
   const int nl = s.n_levels;
+  s.coarse_owner = pf_coarse_partition(3, s.n_coarse, s.n_ranks);
   s.levels.clear();
   for (int l = 0; l < nl; ++l) s.levels.push_back(std::make_unique<FeLevel>());
   const int64_t Nf = static_cast<int64_t>(s.n_coarse) << (nl - 1);
@@ -660,7 +798,7 @@ void create(pf_fe_setup& s) {
       const double h = 1.0 / static_cast<double>(N);
       std::vector<double> Ke(Kref.size());
       for (size_t i = 0; i < Kref.size(); ++i) Ke[i] = h * Kref[i];
-      q2_level(*s.levels[static_cast<size_t>(l)], N, Ke);
+      q2_level(*s.levels[static_cast<size_t>(l)], make_region(s, l), Ke);
       s.levels[static_cast<size_t>(l)]->elem = Ke;
       if (l > 0) q2_prolongation(*s.levels[static_cast<size_t>(l)], *s.levels[static_cast<size_t>(l) - 1]);
     }
@@ -689,7 +827,7 @@ void create(pf_fe_setup& s) {
     }
     for (int l = 0; l < nl; ++l) {
       FeLevel& L = *s.levels[static_cast<size_t>(l)];
-      rt_level(L, static_cast<int64_t>(s.n_coarse) << l, Kref, kap[static_cast<size_t>(l)]);
+      rt_level(L, make_region(s, l), Kref, kap[static_cast<size_t>(l)]);
       const double hx = 1.0 / static_cast<double>(static_cast<int64_t>(s.n_coarse) << l);
       L.elem.resize(36);
       for (int i = 0; i < 36; ++i) L.elem[static_cast<size_t>(i)] = hx * Kref[static_cast<size_t>(i)];
@@ -727,8 +865,8 @@ extern "C" {
 
 const char* pf_fe_last_error(void) { return g_fe_err.c_str(); }
 
-pf_status pf_fe_setup_create(int family, int n_coarse, int n_levels, int coefficient, uint64_t seed,
-                             pf_fe_setup** out) {
+pf_status pf_fe_setup_create_part(int family, int n_coarse, int n_levels, int coefficient, uint64_t seed,
+                                  int n_ranks, int rank, pf_fe_setup** out) {
   return guard([&] {
     if (!out) invalid("null argument");
     *out = nullptr;
@@ -736,17 +874,26 @@ pf_status pf_fe_setup_create(int family, int n_coarse, int n_levels, int coeffic
     if (coefficient != PF_COEF_CONSTANT && coefficient != PF_COEF_LOGNORMAL) invalid("unknown coefficient");
     if (family == PF_FE_Q2 && coefficient != PF_COEF_CONSTANT) invalid("Q2 takes the constant coefficient only");
     if (n_coarse < 2 || n_levels < 1 || n_levels > 12) invalid("need n_coarse >= 2 and 1 <= n_levels <= 12");
+    if (n_ranks < 1 || n_ranks > n_coarse * n_coarse * n_coarse || n_ranks > 127 || rank < 0 || rank >= n_ranks)
+      invalid("need 1 <= n_ranks <= coarse cells and 0 <= rank < n_ranks");
     auto s = std::make_unique<pf_fe_setup>();
     s->family = family;
     s->n_coarse = n_coarse;
     s->n_levels = n_levels;
     s->coefficient = coefficient;
     s->seed = seed;
+    s->n_ranks = n_ranks;
+    s->rank = rank;
     const auto t0 = std::chrono::steady_clock::now();
     create(*s);
     s->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = s.release();
   });
+}
+
+pf_status pf_fe_setup_create(int family, int n_coarse, int n_levels, int coefficient, uint64_t seed,
+                             pf_fe_setup** out) {
+  return pf_fe_setup_create_part(family, n_coarse, n_levels, coefficient, seed, 1, 0, out);
 }
 
 pf_status pf_fe_setup_destroy(pf_fe_setup* s) {
@@ -769,6 +916,8 @@ pf_status pf_fe_setup_level(const pf_fe_setup* s, int level, pf_level_desc* out)
     out->is_dirichlet = L.is_dir.data();
     out->color = L.color.data();
     out->row_order = L.order.data();
+    out->n_channels = static_cast<int32_t>(L.descs.size());
+    out->channels = L.descs.data();
     if (level > 0) {
       out->p_offsets = L.p_off.data();
       out->p_cols = L.p_col.data();

@@ -1565,3 +1565,6 @@ pf_status pf_setup_seconds(const pf_setup* s, double* out) {
 }
 
 }  // extern "C"
+
+// Coordinate bisection of the coarse cells, for the element families (pf_fe_setup.cpp).
+std::vector<int> pf_coarse_partition(int d, int n, int k) { return coarse_partition(d, n, k); }

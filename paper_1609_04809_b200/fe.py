@@ -8,7 +8,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .levels import LevelArrays, _arr
+from .levels import Channel, LevelArrays, _arr
 
 Q2, ROTATED_Q1 = _lib.PF_FE_Q2, _lib.PF_FE_ROTATED_Q1
 CONSTANT, LOGNORMAL = _lib.PF_COEF_CONSTANT, _lib.PF_COEF_LOGNORMAL
@@ -20,11 +20,12 @@ class FESetup:
     constant-coefficient solution sin(pi x) sin(pi y) sin(pi z)."""
 
     def __init__(self, family: int, n_coarse: int, n_levels: int, coefficient: int = CONSTANT,
-                 seed: int = 2024, keep: bool = False):
+                 seed: int = 2024, keep: bool = False, n_ranks: int = 1, rank: int = 0):
         L = _lib.lib()
         self._h = C.c_void_p()
-        _lib.check(L.pf_fe_setup_create(family, n_coarse, n_levels, coefficient, seed, C.byref(self._h)),
-                   setup="fe")
+        _lib.check(L.pf_fe_setup_create_part(family, n_coarse, n_levels, coefficient, seed, n_ranks, rank,
+                                             C.byref(self._h)), setup="fe")
+        self.n_ranks, self.rank = n_ranks, rank
         self.family, self.n_coarse, self.n_levels = family, n_coarse, n_levels
         self.coefficient, self.seed = coefficient, seed
         try:
@@ -77,11 +78,16 @@ class FESetup:
         nnz = int(rp[-1])
         kp, cp = C.c_void_p(), C.c_void_p()
         _lib.check(L.pf_fe_setup_level_keys(self._h, l, C.byref(kp), C.byref(cp)), setup="fe")
+        chans = []
+        for i in range(d.n_channels):
+            c = d.channels[i]
+            chans.append(Channel(c.kind, c.peer, _arr(c.send_dofs, c.n_send, C.c_int32, np.int32),
+                                 _arr(c.recv_dofs, c.n_recv, C.c_int32, np.int32)))
         out = LevelArrays(n, n_own, rp, _arr(d.col_indices, nnz, C.c_int32, np.int32),
                           _arr(d.values, nnz, C.c_double, np.float64),
                           _arr(d.owns_row, n, C.c_uint8, np.uint8),
                           _arr(d.is_dirichlet, n, C.c_uint8, np.uint8),
-                          _arr(d.color, n_own, C.c_int32, np.int32), [],
+                          _arr(d.color, n_own, C.c_int32, np.int32), chans,
                           keys=_arr(kp, 4 * n, C.c_int64, np.int64).reshape(n, 4),
                           class_of=_arr(cp, n, C.c_uint8, np.uint8),
                           order=_arr(d.row_order, n, C.c_int64, np.int64))

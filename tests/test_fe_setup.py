@@ -105,3 +105,42 @@ def test_bad_arguments_raise():
         FESetup(7, 2, 2)
     with pytest.raises(_lib.InvalidArgument):
         FESetup(ROTATED_Q1, 1, 2)
+
+
+@pytest.mark.parametrize("family,coef", [(Q2, CONSTANT), (ROTATED_Q1, LOGNORMAL)], ids=["q2", "rt_lognormal"])
+def test_partitioned_setup(family, coef):
+    """Box partitions (1, 2, 3, 4, 8 ranks): the master/slave channels pair up (the i-th
+    entries of r -> p and p <- r name the same entity), every entity has exactly one
+    authoritative copy, and the partitioned solve (oracle, K subdomains) takes the same
+    cycles as one subdomain, its solution equal by key to roundoff (the restricted partial
+    sums are accumulated in another order)."""
+    from helpers import cfg, keyed
+    from oracle.restated import Oracle
+    from paper_1609_04809_b200 import gmg
+    ref = None
+    pp = 3 if family == Q2 else 2
+    for K in (1, 2, 3, 4, 8):
+        S = [FESetup(family, 2, 3, coef, seed=5, n_ranks=K, rank=r) for r in range(K)]
+        for l in range(3):
+            lv = [s.levels[l] for s in S]
+            auth = {}
+            for r, a in enumerate(lv):
+                for i in np.flatnonzero(a.owns_row):
+                    k = tuple(a.keys[i])
+                    assert k not in auth
+                    auth[k] = r
+            assert len(auth) == len({tuple(k) for a in lv for k in a.keys})
+            for r, a in enumerate(lv):
+                for c in a.channels:
+                    back = [d for d in lv[c.peer].channels if d.peer == r][0]
+                    assert np.array_equal(a.keys[c.send], lv[c.peer].keys[back.recv])
+        o = Oracle([s.levels for s in S])
+        x, res, st, rc = o.solve_outer([s.x0 for s in S], [s.b for s in S],
+                                       cfg(gmg.PF_SMOOTHER_JACOBI, pre=pp, post=pp, max_cycles=300))
+        assert rc == 0
+        got = keyed([s.levels[-1] for s in S], x)
+        if ref is None:
+            ref, cycles = got, st.iterations
+        assert st.iterations == cycles and got.keys() == ref.keys()
+        scale = max(abs(v) for v in ref.values())
+        assert max(abs(got[k] - ref[k]) for k in ref) <= 1e-13 * scale
