@@ -1,4 +1,5 @@
-"""CPU, world_size 2 (gloo): the N>1 host path across real processes.
+"""CPU, world_size 2 (gloo): the N>1 host path across real processes (Q1, and the Q2 /
+rotated-Q1 box partitions of pf_fe.h).
 
 Each process plays one rank exactly as a GPU rank of `bench.py --gpus 2` does: it builds
 only its own subdomain with the product's communication-free setup, then
@@ -61,11 +62,22 @@ def _exchange(lv, v, kind, rank):
         q.wait()
 
 
-def _worker(rank, world, port, out_dir):
+def _setup(family, world, rank):
+    """q1: the reference's Q1 hierarchy (pf_setup.h); q2 / rt: the element families of
+    pf_fe.h, box-partitioned the same way."""
+    if family == "q1":
+        from paper_1609_04809_b200.levels import StructuredSetup
+        return StructuredSetup(3, 2, 4, world, rank)
+    from paper_1609_04809_b200.fe import LOGNORMAL, Q2, ROTATED_Q1, CONSTANT, FESetup
+    if family == "q2":
+        return FESetup(Q2, 2, 2, CONSTANT, n_ranks=world, rank=rank)
+    return FESetup(ROTATED_Q1, 2, 3, LOGNORMAL, seed=4, n_ranks=world, rank=rank)
+
+
+def _worker(rank, world, port, out_dir, family):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1609_04809_b200.levels import StructuredSetup
-    s = StructuredSetup(3, 2, 4, world, rank)
+    s = _setup(family, world, rank)
     top = s.levels[-1]
     # 1. channel symmetry by carrier key
     mine = {(c.kind, c.peer): ([tuple(top.keys[i]) for i in c.send],
@@ -97,18 +109,19 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_two_process_sweep_matches_oracle(tmp_path):
+@pytest.mark.parametrize("family", ["q1", "q2", "rt"])
+def test_two_process_sweep_matches_oracle(tmp_path, family):
     world = 2
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), family), nprocs=world,
                        join=True, start_method="spawn")
     from oracle.restated import Oracle
     from paper_1609_04809_b200 import gmg
-    from paper_1609_04809_b200.levels import StructuredSetup
-    setups = [StructuredSetup(3, 2, 4, world, r) for r in range(world)]
+    setups = [_setup(family, world, r) for r in range(world)]
+    top = len(setups[0].levels) - 1
     o = Oracle([s.levels for s in setups])
-    want = o.smooth(3, [s.x0 for s in setups], [s.b for s in setups], gmg.PF_SMOOTHER_JACOBI,
+    want = o.smooth(top, [s.x0 for s in setups], [s.b for s in setups], gmg.PF_SMOOTHER_JACOBI,
                     sweeps=1, damping=0.8)
-    norm = o.residual_norm(3, want, [s.b for s in setups])
+    norm = o.residual_norm(top, want, [s.b for s in setups])
     for r in range(world):
         got = np.load(tmp_path / f"x{r}.npy")
         assert np.array_equal(got, want[r]), f"rank {r}"
