@@ -377,8 +377,9 @@ def run_b200(args):
             return out
 
         fe["q2_c3_jacobi_v33"] = fe_variant(Q2, CONSTANT, 6, 3, gmg.PF_SMOOTHER_JACOBI, W["omega"])
-        fe["rotated_q1_c4_lognormal_sor_1.2"] = fe_variant(ROTATED_Q1, LOGNORMAL, 7, 2,
-                                                          gmg.PF_SMOOTHER_MULTICOLOR_SOR, 1.2)
+        # omega 1.6: 68 cycles at 128^3 (1.2: 101, 1.4: 81, 1.8: 156; tools/fe_run.py)
+        fe["rotated_q1_c4_lognormal_sor_1.6"] = fe_variant(ROTATED_Q1, LOGNORMAL, 7, 2,
+                                                          gmg.PF_SMOOTHER_MULTICOLOR_SOR, 1.6)
 
     clk.stop()
     clocks = clk.summary()

@@ -46,7 +46,9 @@ def main():
     s.close()
     n_own = fin.n_own
     nnz_own = int(fin.row_offsets[n_own])
-    for kind, omega, name in [(gmg.PF_SMOOTHER_JACOBI, 0.8, "jacobi"), (gmg.PF_SMOOTHER_MULTICOLOR_SOR, 1.2, "sor")]:
+    sor_omega = float(os.environ.get("FE_SOR_OMEGA", "1.2"))
+    for kind, omega, name in [(gmg.PF_SMOOTHER_JACOBI, 0.8, "jacobi"),
+                              (gmg.PF_SMOOTHER_MULTICOLOR_SOR, sor_omega, "sor_%g" % sor_omega)]:
         c = gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=kind, damping=omega), pre_smooth=pp,
                                 post_smooth=pp, outer_tol=1e-10, outer_max_cycles=500)
         x, b = h.vector(L - 1), h.vector(L - 1)
