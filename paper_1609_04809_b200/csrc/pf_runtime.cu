@@ -12,6 +12,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <parallel/algorithm>
+#include <unordered_set>
+#include <omp.h>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -140,41 +143,82 @@ int64_t value_index_min_entries() {
 // Stored values (SELL order, padding included) -> device: an 8/16-bit index into the table
 // of distinct values (distinguished by bit pattern, so -0.0 and 0.0 stay apart) when there
 // are at most 65,536 of them, else fp64.
+// PF_TIMING=1: host-side phase times of pf_hierarchy_finalize on stderr (large grids)
+struct PhaseTimer {
+  bool on = std::getenv("PF_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void operator()(const char* what, int level) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pf_timing] level %d %-22s %8.3f s\n", level, what,
+                 std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
+
 void encode_values(const std::vector<double>& sv, DevVals& out) {
   out = DevVals{};
   if (value_index_enabled() && static_cast<int64_t>(sv.size()) >= value_index_min_entries()) {
-    // pass 1: the distinct values (first-seen order), giving up past 65,536
+    // pass 1: the distinct values in first-seen order, giving up past 65,536.  Each chunk
+    // collects its own first-seen list; merging the lists in chunk order gives the
+    // sequential first-seen order.
+    const int64_t n = static_cast<int64_t>(sv.size());
+    const int nchunk = std::max(1, std::min<int>(omp_get_max_threads(), static_cast<int>(n / (1 << 20)) + 1));
+    std::vector<std::vector<uint64_t>> firsts(static_cast<size_t>(nchunk));
+    std::vector<int> overflow(static_cast<size_t>(nchunk), 0);
+#pragma omp parallel for schedule(static, 1)
+    for (int c = 0; c < nchunk; ++c) {
+      std::unordered_set<uint64_t> seen;
+      const int64_t lo = n * c / nchunk, hi = n * (c + 1) / nchunk;
+      for (int64_t i = lo; i < hi; ++i) {
+        uint64_t bits;
+        std::memcpy(&bits, &sv[static_cast<size_t>(i)], sizeof bits);
+        if (seen.insert(bits).second) {
+          firsts[static_cast<size_t>(c)].push_back(bits);
+          if (seen.size() > 65536) {
+            overflow[static_cast<size_t>(c)] = 1;
+            break;
+          }
+        }
+      }
+    }
     std::unordered_map<uint64_t, uint32_t> ids;
     std::vector<double> table;
-    bool fits = true;
-    for (size_t i = 0; i < sv.size(); ++i) {
-      uint64_t bits;
-      std::memcpy(&bits, &sv[i], sizeof bits);
-      if (ids.find(bits) != ids.end()) continue;
-      if (table.size() == 65536) {
-        fits = false;
-        break;
+    bool fits = std::find(overflow.begin(), overflow.end(), 1) == overflow.end();
+    for (int c = 0; c < nchunk && fits; ++c)
+      for (uint64_t bits : firsts[static_cast<size_t>(c)]) {
+        if (ids.find(bits) != ids.end()) continue;
+        if (table.size() == 65536) {
+          fits = false;
+          break;
+        }
+        ids.emplace(bits, static_cast<uint32_t>(table.size()));
+        double v;
+        std::memcpy(&v, &bits, sizeof v);
+        table.push_back(v);
       }
-      ids.emplace(bits, static_cast<uint32_t>(table.size()));
-      table.push_back(sv[i]);
-    }
-    std::vector<uint32_t> idx;
     if (fits) {  // pass 2: the indices
-      idx.resize(sv.size());
-      for (size_t i = 0; i < sv.size(); ++i) {
-        uint64_t bits;
-        std::memcpy(&bits, &sv[i], sizeof bits);
-        idx[i] = ids.find(bits)->second;
-      }
-    }
-    if (fits) {
       out.table.upload(table);
       if (table.size() <= 256) {
         out.vkind = 1;
-        out.vi8.upload(std::vector<uint8_t>(idx.begin(), idx.end()));
+        std::vector<uint8_t> idx(sv.size());
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i) {
+          uint64_t bits;
+          std::memcpy(&bits, &sv[static_cast<size_t>(i)], sizeof bits);
+          idx[static_cast<size_t>(i)] = static_cast<uint8_t>(ids.find(bits)->second);
+        }
+        out.vi8.upload(idx);
       } else {
         out.vkind = 2;
-        out.vi16.upload(std::vector<uint16_t>(idx.begin(), idx.end()));
+        std::vector<uint16_t> idx(sv.size());
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i) {
+          uint64_t bits;
+          std::memcpy(&bits, &sv[static_cast<size_t>(i)], sizeof bits);
+          idx[static_cast<size_t>(i)] = static_cast<uint16_t>(ids.find(bits)->second);
+        }
+        out.vi16.upload(idx);
       }
       return;
     }
@@ -214,6 +258,7 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
   }
   std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
   std::vector<int32_t> sc(static_cast<size_t>(sptr[n_slices]), 0);
+#pragma omp parallel for schedule(static)
   for (int64_t s = 0; s < n_slices; ++s) {
     const int64_t w = (sptr[s + 1] - sptr[s]) / kSlice;
     for (int l = 0; l < kSlice; ++l) {
@@ -248,6 +293,7 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
   const int64_t n_slices = (n + kSlice - 1) / kSlice;
   std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
   std::vector<int32_t> rlen(static_cast<size_t>(std::max<int64_t>(n_slices, 1) * kSlice), 0);
+#pragma omp parallel for schedule(static)
   for (int32_t d = 0; d < n; ++d) rlen[d] = static_cast<int32_t>(rowptr[inv[d] + 1] - rowptr[inv[d]]);
   for (int64_t s = 0; s < n_slices; ++s) {
     int32_t w = 0;
@@ -258,6 +304,7 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
   // columns, then values, one host array at a time (peak host memory on large grids)
   {
     std::vector<int32_t> sc(static_cast<size_t>(sptr[n_slices]), 0);
+#pragma omp parallel for schedule(static)
     for (int32_t d = 0; d < n; ++d) {
       const int64_t base = sell_row_base(sptr.data(), d), k0 = rowptr[inv[d]];
       for (int j = 0; j < rlen[d]; ++j) sc[static_cast<size_t>(sell_entry(base, j))] = perm[cols[static_cast<size_t>(k0 + j)]];
@@ -266,6 +313,7 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
   }
   {
     std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
+#pragma omp parallel for schedule(static)
     for (int32_t d = 0; d < n; ++d) {
       const int64_t base = sell_row_base(sptr.data(), d), k0 = rowptr[inv[d]];
       for (int j = 0; j < rlen[d]; ++j) sv[static_cast<size_t>(sell_entry(base, j))] = vals[static_cast<size_t>(k0 + j)];
@@ -282,6 +330,7 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
 // Device layout of one subdomain level: own rows colour-major (stable in host order),
 // then every other row in host order; SELL-32 operator; P (rows of this level).
 void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
+  PhaseTimer tm;
   const int32_t n = H.n, n_own = H.n_own;
   D.n = n;
   D.n_own = n_own;
@@ -289,16 +338,25 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
   for (int32_t r = 0; r < n; ++r) {
     if (H.rowptr[r + 1] < H.rowptr[r]) invalid("row offsets must be non-decreasing");
   }
-  for (int64_t k = 0; k < H.rowptr[n]; ++k)
-    if (H.cols[k] < 0 || H.cols[k] >= n) invalid("column index out of range");
-  for (int32_t r = 0; r < n_own; ++r) {
-    double diag = 0.0;
-    for (int64_t k = H.rowptr[r]; k < H.rowptr[r + 1]; ++k)
-      if (H.cols[k] == r) diag = H.vals[k];
-    if (diag == 0.0)
-      throw Error(PF_ERR_SINGULAR_DIAGONAL, "zero diagonal at own dof " + std::to_string(r) +
+  {
+    const int64_t nnz = H.rowptr[n];
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (int64_t k = 0; k < nnz; ++k) bad |= (H.cols[k] < 0 || H.cols[k] >= n) ? 1 : 0;
+    if (bad) invalid("column index out of range");
+    int32_t first_zero = INT32_MAX;
+#pragma omp parallel for schedule(static) reduction(min : first_zero)
+    for (int32_t r = 0; r < n_own; ++r) {
+      double diag = 0.0;
+      for (int64_t k = H.rowptr[r]; k < H.rowptr[r + 1]; ++k)
+        if (H.cols[k] == r) diag = H.vals[k];
+      if (diag == 0.0) first_zero = std::min(first_zero, r);
+    }
+    if (first_zero != INT32_MAX)
+      throw Error(PF_ERR_SINGULAR_DIAGONAL, "zero diagonal at own dof " + std::to_string(first_zero) +
                                                 " (level " + std::to_string(level) + ")");
   }
+  tm("checks", level);
   // --- colours of own rows
   std::vector<int32_t> color(static_cast<size_t>(n_own), 0);
   if (!H.color.empty()) {
@@ -307,12 +365,17 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
       color[i] = H.color[i];
     }
     // a colour class must be an independent set of the own-row graph
+    int64_t first_bad = INT64_MAX;
+#pragma omp parallel for schedule(static) reduction(min : first_bad)
     for (int32_t i = 0; i < n_own; ++i)
       for (int64_t k = H.rowptr[i]; k < H.rowptr[i + 1]; ++k) {
         const int32_t c = H.cols[k];
-        if (c != i && c < n_own && color[c] == color[i] && H.vals[k] != 0.0)
-          invalid("colouring couples rows " + std::to_string(i) + " and " + std::to_string(c));
+        if (c != i && c < n_own && color[c] == color[i] && H.vals[k] != 0.0) first_bad = std::min(first_bad, k);
       }
+    if (first_bad != INT64_MAX) {
+      const int32_t i = static_cast<int32_t>(std::upper_bound(H.rowptr.begin(), H.rowptr.end(), first_bad) - H.rowptr.begin() - 1);
+      invalid("colouring couples rows " + std::to_string(i) + " and " + std::to_string(H.cols[first_bad]));
+    }
   } else {
     std::vector<int32_t> seen;
     for (int32_t i = 0; i < n_own; ++i) {
@@ -346,20 +409,26 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
     } else {  // placement hint: inside a colour, ascending (order, host index)
       std::vector<int32_t> own(static_cast<size_t>(n_own));
       std::iota(own.begin(), own.end(), 0);
-      std::stable_sort(own.begin(), own.end(), [&](int32_t a, int32_t b) {
-        return color[a] != color[b] ? color[a] < color[b] : H.order[a] < H.order[b];
+      // (colour, order, index) is a strict total order, so any sort gives the stable result
+      __gnu_parallel::sort(own.begin(), own.end(), [&](int32_t a, int32_t b) {
+        if (color[a] != color[b]) return color[a] < color[b];
+        if (H.order[a] != H.order[b]) return H.order[a] < H.order[b];
+        return a < b;
       });
       for (int32_t i : own) D.perm[i] = next[color[i]]++;
     }
     for (int32_t i = n_own; i < n; ++i) D.perm[i] = i;
+#pragma omp parallel for schedule(static)
     for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
   }
   D.d_perm.upload(D.perm);
+  tm("colours + perm", level);
   // --- SELL-32x4 operator: rows in device order, columns mapped, entries in CSR order,
   // written straight from the host CSR (no intermediate re-layout: at 512^3 the finest
   // level alone is 44 GB of host CSR)
   sell_from_csr(n, inv, D.perm, H.rowptr, H.cols, H.vals, D.A);
   D.A.own_nnz = H.rowptr[n_own];
+  tm("sell", level);
   D.csr_rowptr = H.rowptr;
   D.sell_ptr.resize(static_cast<size_t>(D.A.slice_ptr.n));
   if (D.A.slice_ptr.n > 0)
@@ -367,7 +436,9 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
                        cudaMemcpyDeviceToHost));
   {
     std::vector<uint8_t> touched(static_cast<size_t>(n), 0);
-    for (int64_t k = 0; k < H.rowptr[n_own]; ++k) touched[H.cols[k]] = 1;
+    const int64_t z = H.rowptr[n_own];
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < z; ++k) __atomic_store_n(&touched[static_cast<size_t>(H.cols[k])], 1, __ATOMIC_RELAXED);
     D.own_cols_touched = std::count(touched.begin(), touched.end(), 1);
   }
   // --- Dirichlet mask in device order
@@ -380,6 +451,7 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
   D.partials.alloc(std::max<int64_t>(D.resnorm_blocks, grid_for(n)));
   D.ticket.alloc(1);
   PF_CUDA(cudaMemset(D.ticket.p, 0, sizeof(unsigned int)));
+  tm("touched + masks", level);
 }
 
 // P rows of the fine level in device order; R = P^T over owns_row fine rows as a
@@ -390,57 +462,67 @@ void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const
   for (int64_t e = 0; e < F.p_off[nf]; ++e)
     if (F.p_col[e] < 0 || F.p_col[e] >= nc) invalid("prolongation column out of the parent level");
   std::vector<int32_t> inv_f(static_cast<size_t>(nf));
+#pragma omp parallel for schedule(static)
   for (int32_t i = 0; i < nf; ++i) inv_f[DF.perm[i]] = i;
   std::vector<int64_t> poff(static_cast<size_t>(nf) + 1, 0);
-  std::vector<int32_t> pcol;
-  std::vector<double> pw;
-  pcol.reserve(static_cast<size_t>(F.p_off[nf]));
-  pw.reserve(static_cast<size_t>(F.p_off[nf]));
+  for (int32_t d = 0; d < nf; ++d) poff[d + 1] = poff[d] + (F.p_off[inv_f[d] + 1] - F.p_off[inv_f[d]]);
+  std::vector<int32_t> pcol(static_cast<size_t>(poff[nf]));
+  std::vector<double> pw(static_cast<size_t>(poff[nf]));
+#pragma omp parallel for schedule(static)
   for (int32_t d = 0; d < nf; ++d) {
     const int32_t hr = inv_f[d];
-    for (int64_t e = F.p_off[hr]; e < F.p_off[hr + 1]; ++e) {
-      pcol.push_back(DC.perm[F.p_col[e]]);
-      pw.push_back(F.p_w[e]);
+    int64_t q = poff[d];
+    for (int64_t e = F.p_off[hr]; e < F.p_off[hr + 1]; ++e, ++q) {
+      pcol[static_cast<size_t>(q)] = DC.perm[F.p_col[e]];
+      pw[static_cast<size_t>(q)] = F.p_w[e];
     }
-    poff[d + 1] = static_cast<int64_t>(pcol.size());
   }
   sell_from_rows(nf, poff, pcol, pw, DF.P);
-  // R by counting sort over parent host rows; iterating fine host rows ascending keeps
-  // each parent row's contributions in the reference's scatter-add order.
-  std::vector<int64_t> cnt(static_cast<size_t>(nc) + 1, 0);
-  for (int32_t f = 0; f < nf; ++f)
-    if (F.owns_row[f])
-      for (int64_t e = F.p_off[f]; e < F.p_off[f + 1]; ++e) ++cnt[F.p_col[e] + 1];
-  std::vector<int64_t> start(static_cast<size_t>(nc) + 1, 0);
-  for (int32_t c = 0; c < nc; ++c) start[c + 1] = start[c] + cnt[c + 1];
-  std::vector<int32_t> rf(static_cast<size_t>(start[nc]));
-  std::vector<double> rw(static_cast<size_t>(start[nc]));
+  // R rows: each parent row's contributions in ascending fine host index (the reference's
+  // scatter-add order).  The owned P entries in fine host order, sorted by (parent device
+  // row, position) — a strict order, so the parallel sort reproduces the counting sort.
+  std::vector<int64_t> src;      // positions e of owned entries, ascending (= fine host order)
+  std::vector<int32_t> fine_of;  // their fine host rows
   {
-    std::vector<int64_t> pos(start.begin(), start.end() - 1);
+    std::vector<int64_t> cnt(static_cast<size_t>(nf) + 1, 0);
+#pragma omp parallel for schedule(static)
+    for (int32_t f = 0; f < nf; ++f) cnt[f + 1] = F.owns_row[f] ? F.p_off[f + 1] - F.p_off[f] : 0;
+    for (int32_t f = 0; f < nf; ++f) cnt[f + 1] += cnt[f];
+    src.resize(static_cast<size_t>(cnt[nf]));
+    fine_of.resize(static_cast<size_t>(cnt[nf]));
+#pragma omp parallel for schedule(static)
     for (int32_t f = 0; f < nf; ++f)
       if (F.owns_row[f])
-        for (int64_t e = F.p_off[f]; e < F.p_off[f + 1]; ++e) {
-          const int64_t q = pos[F.p_col[e]]++;
-          rf[q] = DF.perm[f];
-          rw[q] = F.p_w[e];
+        for (int64_t e = F.p_off[f], q = cnt[f]; e < F.p_off[f + 1]; ++e, ++q) {
+          src[static_cast<size_t>(q)] = e;
+          fine_of[static_cast<size_t>(q)] = f;
         }
   }
-  // reorder parent rows into device order
-  std::vector<int32_t> inv_c(static_cast<size_t>(nc));
-  for (int32_t i = 0; i < nc; ++i) inv_c[DC.perm[i]] = i;
+  // keys (parent device row << 35 | position): distinct, so sorting them is the stable sort
+  std::vector<uint64_t> key(src.size());
+  if (static_cast<int64_t>(src.size()) >= (int64_t(1) << 35)) invalid("prolongation too large");
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < static_cast<int64_t>(src.size()); ++q)
+    key[static_cast<size_t>(q)] = static_cast<uint64_t>(DC.perm[F.p_col[src[static_cast<size_t>(q)]]]) << 35 |
+                                  static_cast<uint64_t>(q);
+  __gnu_parallel::sort(key.begin(), key.end());
+  std::vector<int64_t> ord(src.size());
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < static_cast<int64_t>(key.size()); ++i)
+    ord[static_cast<size_t>(i)] = static_cast<int64_t>(key[static_cast<size_t>(i)] & ((uint64_t(1) << 35) - 1));
+  std::vector<uint64_t>().swap(key);
   std::vector<int64_t> roff(static_cast<size_t>(nc) + 1, 0);
-  std::vector<int32_t> rcol;
-  std::vector<double> rwt;
-  rcol.reserve(rf.size());
-  rwt.reserve(rf.size());
-  for (int32_t d = 0; d < nc; ++d) {
-    const int32_t hc = inv_c[d];
-    for (int64_t q = start[hc]; q < start[hc + 1]; ++q) {
-      rcol.push_back(rf[q]);
-      rwt.push_back(rw[q]);
-    }
-    roff[d + 1] = static_cast<int64_t>(rcol.size());
+  std::vector<int32_t> rcol(ord.size());
+  std::vector<double> rwt(ord.size());
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < static_cast<int64_t>(ord.size()); ++i) {
+    const int64_t q = ord[static_cast<size_t>(i)], e = src[static_cast<size_t>(q)];
+    rcol[static_cast<size_t>(i)] = DF.perm[fine_of[static_cast<size_t>(q)]];
+    rwt[static_cast<size_t>(i)] = F.p_w[e];
   }
+  for (int64_t i = 0; i < static_cast<int64_t>(ord.size()); ++i)
+    ++roff[static_cast<size_t>(DC.perm[F.p_col[src[static_cast<size_t>(ord[static_cast<size_t>(i)])]]]) + 1];
+  for (int32_t c = 0; c < nc; ++c) roff[c + 1] += roff[c];
   sell_from_rows(nc, roff, rcol, rwt, DF.R);
 }
 
@@ -1859,10 +1941,13 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
     }
     L.total = off;
     if (off >= (int64_t(1) << 31)) invalid("level too large for int32 device indices");
+    PhaseTimer tm;
     if (l > 0)
       for (int s = 0; s < h->n_sub; ++s)
         build_transfer(L.host[s], L.sub[s], h->levels[l - 1].host[s], h->levels[l - 1].sub[s]);
+    tm("transfer", l);
     build_plans(h, l);
+    tm("plans", l);
     if (l > 0)  // the prolongation is on the device too
       for (HostLevel& H : L.host) {
         std::vector<int32_t>().swap(H.p_col);

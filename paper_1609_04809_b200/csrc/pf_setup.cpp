@@ -19,6 +19,7 @@
 #include "pf_runtime.hpp"
 
 #include <algorithm>
+#include <parallel/algorithm>
 #include <array>
 #include <chrono>
 #include <cmath>
@@ -741,6 +742,15 @@ void finest_load(const pf_setup& s, double t, double* out);
 void finish_finest(pf_setup& s);
 
 void build_level(pf_setup& s, int l) {
+  const bool timing = std::getenv("PF_TIMING") != nullptr;
+  auto tick = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pf_timing]   setup level %d %-16s %8.3f s\n", l, what,
+                 std::chrono::duration<double>(now - tick).count());
+    tick = now;
+  };
   auto L = std::make_unique<SetupLevel>();
   Geo& g = L->geo;
   g.d = s.d;
@@ -779,6 +789,7 @@ void build_level(pf_setup& s, int l) {
     for (int64_t y = vb.lo[1]; y < vb.hi[1]; ++y)
       for (int64_t z = vb.lo[2]; z < vb.hi[2]; ++z) info[vb.idx(x, y, z)] = classify(V, x, y, z, s.direct_halos);
 
+  lap("classify");
   // --- numbering: the reference's own.  build_fespace numbers vertices at first touch
   // over the local cells in gcn order, ring-slot order inside a cell (fespace.cpp:47-85);
   // build_parfemapper then stable-sorts that numbering by DofClass value
@@ -824,7 +835,7 @@ void build_level(pf_setup& s, int l) {
     order[static_cast<size_t>(k)].key =
         (static_cast<int64_t>(info[static_cast<size_t>(bi)].cls) << 59) | (best * 8 + slot);
   }
-  std::sort(order.begin(), order.end(), [](const Order& a, const Order& b) { return a.key < b.key; });
+  __gnu_parallel::sort(order.begin(), order.end(), [](const Order& a, const Order& b) { return a.key < b.key; });
   L->n = static_cast<int32_t>(total);
   L->n_own = static_cast<int32_t>(n_own);
   L->vert.resize(static_cast<size_t>(total));
@@ -860,6 +871,7 @@ void build_level(pf_setup& s, int l) {
                                               : ((x & 1) << 1) | (y & 1));
   }
 
+  lap("numbering");
   // --- element matrices per distinct cell shape
   std::vector<double> hvals;
   L->hid.assign(static_cast<size_t>(g.N), 0);
@@ -885,6 +897,7 @@ void build_level(pf_setup& s, int l) {
   const bool finest = l == s.n_levels - 1;
   const double half_dt = 0.5 * s.prob.dt;
 
+  lap("elements");
   // --- system (assembly over own + halo cells in gcn order, assembly.cpp:114-131);
   // heat: M + dt/2 K (multigrid.cpp:18-28); Dirichlet rows -> identity (:162-170)
   const int zr = d == 3 ? 1 : 0;
@@ -981,6 +994,7 @@ void build_level(pf_setup& s, int l) {
     }
   }
 
+  lap("system");
   // --- channels: my requests (recv lists), then every other rank's requests to me
   std::vector<OwnedChannel> chans;
   auto chan = [&](int kind, int peer) -> OwnedChannel& {
@@ -1017,6 +1031,7 @@ void build_level(pf_setup& s, int l) {
     L->descs.push_back(pf_channel_desc{c.kind, c.peer, static_cast<int32_t>(c.send.size()),
                                        static_cast<int32_t>(c.recv.size()), c.send.data(), c.recv.data()});
 
+  lap("channels");
   // --- prolongation from level l-1 (multigrid.cpp:35-72)
   if (l > 0) {
     const SetupLevel& C = *s.levels[static_cast<size_t>(l - 1)];
@@ -1072,8 +1087,10 @@ void build_level(pf_setup& s, int l) {
       }
   }
 
+  lap("prolongation");
   s.levels.push_back(std::move(L));
   if (l == s.n_levels - 1) finish_finest(s);
+  lap("finish");
 }
 
 void finest_load(const pf_setup& s, double t, double* out) {
@@ -1211,8 +1228,21 @@ pf_status create(int dim, int n_coarse, int n_levels, int n_ranks, int rank, int
     s->prob.seed = seed;
     s->direct_halos = direct_halos;
     s->coarse_owner = coarse_partition(dim, n_coarse, n_ranks);
+    const bool timing = std::getenv("PF_TIMING") != nullptr;
+    auto tick = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what, int l) {
+      if (!timing) return;
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[pf_timing] setup level %d %-14s %8.3f s\n", l, what,
+                   std::chrono::duration<double>(now - tick).count());
+      tick = now;
+    };
     if (problem == PF_PROBLEM_LOGNORMAL) build_coefficients(*s);
-    for (int l = 0; l < n_levels; ++l) build_level(*s, l);
+    lap("coefficients", -1);
+    for (int l = 0; l < n_levels; ++l) {
+      build_level(*s, l);
+      lap("level", l);
+    }
     s->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = s.release();
   });

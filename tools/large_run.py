@@ -30,13 +30,16 @@ h = gmg.Hierarchy.from_setups([s])
 print(f"upload {time.time() - t:.1f} s, peak RSS {rss_gb():.1f} GB, device {h.device_bytes() / 1e9:.1f} GB", flush=True)
 print({l: h.level_info(l) for l in (L - 2, L - 1)}, flush=True)
 top = L - 1
-for kind in kinds:
-    om = 1.2 if kind == 2 else 0.8
+import os  # noqa: E402
+
+sor_omegas = [float(w) for w in os.environ.get("LARGE_SOR_OMEGA", "1.2").split(",")]
+runs = [(k, w) for k in kinds for w in (sor_omegas if k == 2 else [0.8])]
+for kind, om in runs:
     c = gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=kind, damping=om), pre_smooth=2, post_smooth=2,
                             outer_tol=1e-10, outer_max_cycles=400)
     x, b = h.vector(top, s.x0), h.vector(top, s.b)
     st = gmg.solve_outer(h, x, b, c)
-    print(f"kind {kind}: cycles {st.iterations} converged {st.converged} solve {st.solve_seconds * 1e3:.1f} ms "
+    print(f"kind {kind} omega {om}: cycles {st.iterations} converged {st.converged} solve {st.solve_seconds * 1e3:.1f} ms "
           f"({s.n_global / st.solve_seconds:.3e} DOF/s), V-cycle {h.time_vcycle(x, b, c, 3):.2f} ms", flush=True)
     x.close()
     b.close()
