@@ -19,6 +19,7 @@ struct Api {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
@@ -45,6 +46,7 @@ Api& api() {
   a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
   a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
   a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+  a.CommAbort = reinterpret_cast<decltype(a.CommAbort)>(sym("ncclCommAbort"));
   a.CommGetAsyncError = reinterpret_cast<decltype(a.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
   a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
   a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
@@ -104,6 +106,10 @@ void Nccl::check_async() {
   ncclResult_t r = ncclSuccess;
   ck(api().CommGetAsyncError(static_cast<ncclComm_t>(comm), &r), "ncclCommGetAsyncError");
   ck(r, "NCCL async error");
+}
+void Nccl::abort() {
+  if (comm) api().CommAbort(static_cast<ncclComm_t>(comm));
+  comm = nullptr;
 }
 Nccl::~Nccl() {
   if (comm) api().CommDestroy(static_cast<ncclComm_t>(comm));

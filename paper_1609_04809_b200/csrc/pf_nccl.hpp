@@ -31,6 +31,10 @@ struct Transport {
   virtual void allgather(const double* send, double* recv, int64_t count, cudaStream_t s) = 0;
   virtual void check_async() {}
   virtual bool capturable() const { return true; }  // may be recorded into CUDA graphs
+  // the reference fabric's watchdog (transport.cpp:54-60): host waits on a stream that
+  // carries this transport's operations give up after this many seconds (0: never)
+  virtual double watchdog_seconds() const { return 0.0; }
+  virtual void abort() {}
 };
 
 struct Nccl final : Transport {
@@ -43,6 +47,9 @@ struct Nccl final : Transport {
   void recv(double* buf, int64_t count, int peer, cudaStream_t s) override;
   void allgather(const double* send, double* recv, int64_t count, cudaStream_t s) override;
   void check_async() override;
+  double watchdog = 300.0;  // PF_WATCHDOG_S
+  double watchdog_seconds() const override { return watchdog; }
+  void abort() override;
   ~Nccl() override;
 };
 

@@ -16,6 +16,7 @@
 #include <unordered_set>
 #include <omp.h>
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1564,8 +1565,28 @@ pf_hierarchy::GraphEntry& solve_graph(pf_hierarchy* h, pf_vector* x, const pf_ve
 }
 
 void sync(pf_hierarchy* h) {
-  PF_CUDA(cudaStreamSynchronize(h->stream));
-  if (h->xport) h->xport->check_async();
+  const double limit = h->xport ? h->xport->watchdog_seconds() : 0.0;
+  if (limit <= 0.0) {
+    PF_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->xport) h->xport->check_async();
+    return;
+  }
+  // multi-process: poll, so that a peer that never arrives (or an NCCL error) surfaces as
+  // TransportError after the watchdog period instead of a hang (transport.cpp:54-60)
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t r = cudaStreamQuery(h->stream);
+    if (r == cudaSuccess) break;
+    if (r != cudaErrorNotReady) PF_CUDA(r);
+    h->xport->check_async();
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+      h->xport->abort();
+      throw Error(PF_ERR_TRANSPORT, "watchdog: the exchange did not complete within " + std::to_string(limit) +
+                                        " s (a peer rank never arrived); communicator aborted");
+    }
+    if (spin > 1000) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  h->xport->check_async();
 }
 
 double read_norm(pf_hierarchy* h, int l) {
@@ -2062,7 +2083,11 @@ pf_status pf_hierarchy_init_nccl(pf_hierarchy* h, const void* id, int nbytes) {
   if (h->world == h->n_sub) state("NCCL is only used when ranks live in separate processes");
   PF_CUDA(cudaSetDevice(h->device));
   if (h->xport) state("transport already initialized");
-  h->xport = pf::nccl_init(h->rank_base, h->world, id, nbytes);
+  {
+    auto nc = pf::nccl_init(h->rank_base, h->world, id, nbytes);
+    if (const char* e = std::getenv("PF_WATCHDOG_S")) nc->watchdog = std::atof(e);
+    h->xport = std::move(nc);
+  }
   PF_API_END
 }
 
