@@ -175,3 +175,37 @@ def test_export_against_multigrid(cuda, tmp_path):
     assert np.abs(own - dense[:len(own)]).max() <= 1e-8 * np.abs(dense).max()
     for s in S:
         s.close()
+
+
+@pytest.mark.parametrize("K", [1, 2])
+def test_single_level_hierarchy_is_the_coarse_solve(cuda, K):
+    """multigrid.cpp:150-158: on a one-level hierarchy a V-cycle is coarse_solve; the
+    device and the oracle agree bit for bit (Q1 with 4^3 coarse cells: 27 unknowns per
+    subdomain pair), and so do the element families (one subdomain)."""
+    from oracle.restated import Oracle
+    from paper_1609_04809_b200.fe import CONSTANT, LOGNORMAL, Q2, ROTATED_Q1, FESetup
+    cases = [[StructuredSetup(3, 4, 1, K, r) for r in range(K)]]
+    if K == 1:
+        cases += [[FESetup(Q2, 3, 1)], [FESetup(ROTATED_Q1, 3, 1, LOGNORMAL, seed=2)]]
+    for setups in cases:
+        levels = [s.levels for s in setups]
+        h = gmg.Hierarchy(levels)
+        x = upload(h, 0, [s.x0 for s in setups])
+        c = cfg(tol=1e-12, max_cycles=5)
+        st = gmg.solve_outer(h, x, upload(h, 0, [s.b for s in setups]), c)
+        xo, res, ost, rc = Oracle(levels).solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
+        assert rc == 0 and st.converged and st.iterations == ost.iterations
+        assert all(np.array_equal(a, b) for a, b in zip(download(h, x, K), xo))
+
+
+def test_ragged_subdomains(cuda):
+    """K = 3, 5, 6, 7 (boxes of unequal size, partition.cpp:51-63): device == oracle."""
+    from oracle.restated import Oracle
+    for K in (3, 5, 6, 7):
+        setups, levels = structured(3, 2, 4, K)
+        h = gmg.Hierarchy(levels)
+        x = upload(h, 3, [s.x0 for s in setups])
+        st = gmg.solve_outer(h, x, upload(h, 3, [s.b for s in setups]), cfg())
+        xo, res, ost, rc = Oracle(levels).solve_outer([s.x0 for s in setups], [s.b for s in setups], cfg())
+        assert st.iterations == ost.iterations, K
+        assert all(np.array_equal(a, b) for a, b in zip(download(h, x, K), xo)), K
