@@ -32,6 +32,20 @@ namespace pf {
     asm volatile("griddepcontrol.launch_dependents;" :::);     \
   } while (0)
 
+// kVK == kVKSmem: 8-bit value indices (vkind 1) with the table staged in shared memory
+// by the kernel's prologue (vtab_stage), so the per-entry value lookup is a shared-memory
+// broadcast instead of an L1 request competing with the x gathers.
+constexpr int kVKSmem = 4;
+__shared__ double s_vtab[256];
+
+template <int kVK>
+__device__ __forceinline__ void vtab_stage(const SellView& A) {
+  if constexpr (kVK == kVKSmem) {
+    for (int i = threadIdx.x; i < A.table_n; i += blockDim.x) s_vtab[i] = A.table[i];
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
 
@@ -43,6 +57,8 @@ __device__ __forceinline__ double sell_val(const SellView& A, int64_t e) {
     return ld_stream(A.vals + e);
   } else if constexpr (kVK == 1) {
     return __ldg(A.table + __ldcs(static_cast<const unsigned char*>(A.vidx) + e));
+  } else if constexpr (kVK == kVKSmem) {
+    return s_vtab[__ldcs(static_cast<const unsigned char*>(A.vidx) + e)];
   } else if constexpr (kVK == 2) {
     return __ldg(A.table + __ldcs(static_cast<const unsigned short*>(A.vidx) + e));
   } else {
@@ -64,6 +80,10 @@ __device__ __forceinline__ void sell_group(const SellView& A, int64_t e, int32_t
     const unsigned int w = __ldcs(reinterpret_cast<const unsigned int*>(static_cast<const unsigned char*>(A.vidx) + e));
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = __ldg(A.table + ((w >> (8 * k)) & 255u));
+  } else if constexpr (kVK == kVKSmem) {
+    const unsigned int w = __ldcs(reinterpret_cast<const unsigned int*>(static_cast<const unsigned char*>(A.vidx) + e));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = s_vtab[(w >> (8 * k)) & 255u];
   } else if constexpr (kVK == 2) {
     const uint2 w = __ldcs(reinterpret_cast<const uint2*>(static_cast<const unsigned short*>(A.vidx) + e));
     v[0] = __ldg(A.table + (w.x & 0xffffu));
@@ -188,6 +208,7 @@ __global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi(SellView A, cons
                                                    double* __restrict__ x_new,
                                                    const double* __restrict__ b, int32_t n_own,
                                                    int32_t n, double omega) {
+  vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n) return;
@@ -210,6 +231,7 @@ __global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi_boundary(SellVie
                                                                     double* __restrict__ x_new,
                                                                     const double* __restrict__ b, int32_t n_own,
                                                                     int32_t n, double omega) {
+  vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
   const int32_t nb_blocks = max(1, (n_list + kBlock - 1) / kBlock);
   if (static_cast<int32_t>(blockIdx.x) >= nb_blocks) {  // non-own rows: carried over
@@ -231,6 +253,7 @@ __global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi_interior(SellVie
                                                                     double* __restrict__ x_new,
                                                                     const double* __restrict__ b, int32_t n_own,
                                                                     double omega) {
+  vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_own || is_b[row]) return;
@@ -289,6 +312,7 @@ template <bool kSor, int kVK>
 __global__ void __launch_bounds__(kBlock, PF_SOR_MINB) k_color_sweep(SellView A, double* x,
                                                         const double* __restrict__ b, int32_t row0,
                                                         int32_t row1, double omega) {
+  vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
   const int32_t row = row0 + blockIdx.x * kBlock + threadIdx.x;
   if (row >= row1) return;
@@ -315,6 +339,7 @@ __global__ void __launch_bounds__(kSplitBlock) k_color_sweep_split(SellView A, d
   extern __shared__ double prod[];  // [width][32]
   __shared__ double sdiag[32];
   __shared__ int32_t sdpos[32];
+  vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t slice = (row0 >> 5) + static_cast<int32_t>(blockIdx.x);
@@ -366,6 +391,7 @@ template <int kVK>
 __global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_residual(SellView A, const double* __restrict__ x,
                                                      const double* __restrict__ b,
                                                      double* __restrict__ r, int32_t n) {
+  vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n) return;
@@ -410,6 +436,7 @@ __global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_resnorm(SellView A, con
                                                     double* __restrict__ partials,
                                                     unsigned int* ticket, double* sumsq,
                                                     double* norm_out) {
+  vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
   __shared__ double smem[kBlock / 32];
   __shared__ bool last;
@@ -452,6 +479,7 @@ __global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_jacobi_norm(SellView A,
                                                         int32_t n, double omega,
                                                         double* __restrict__ partials,
                                                         unsigned int* ticket, double* sumsq) {
+  vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
   __shared__ double smem[kBlock / 32];
   __shared__ bool last;
@@ -502,6 +530,7 @@ __global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* o
 template <int kVK>
 __global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_prolong_add(SellView P, const double* __restrict__ xc,
                                                         double* __restrict__ xf, int32_t n_f, int add) {
+  vtab_stage<kVK>(P);
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_f) return;
@@ -521,6 +550,7 @@ __global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_restrict(SellView R, co
                                                      double* __restrict__ xc,
                                                      const uint8_t* __restrict__ is_dir_c,
                                                      int32_t n_c, int zero_dirichlet) {
+  vtab_stage<kVK>(R);
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_c) return;

@@ -109,7 +109,8 @@ Launcher launcher(pf_hierarchy* h, cudaStream_t stream = nullptr) {
 SellView view_of(const DevVals& v, const DevSell& s) {
   const void* idx = v.vkind == 1 ? static_cast<const void*>(v.vi8.p)
                   : v.vkind == 2 ? static_cast<const void*>(v.vi16.p) : nullptr;
-  return SellView{v.vals.p, s.cols.p, s.slice_ptr.p, s.row_len.p, idx, v.table.p, v.vkind};
+  return SellView{v.vals.p, s.cols.p, s.slice_ptr.p, s.row_len.p, idx, v.table.p, v.vkind,
+                  static_cast<int32_t>(v.table.n)};
 }
 SellView view(const DevSell& s) { return view_of(s.vals, s); }
 
@@ -121,6 +122,25 @@ void vk_dispatch(int vkind, F&& f) {
     case 2: f(std::integral_constant<int, 2>{}); break;
     default: f(std::integral_constant<int, 0>{}); break;
   }
+}
+
+// PF_VTAB_SMEM=0: the row kernels read an 8-bit index's value through L1 (__ldg) instead
+// of the shared-memory copy of the table.
+bool vtab_smem() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_VTAB_SMEM");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+// vk_dispatch for the operator row kernels that stage the value table (vtab_stage).
+template <typename F>
+void vk_dispatch_rows(int vkind, F&& f) {
+  if (vkind == 1 && vtab_smem())
+    f(std::integral_constant<int, kVKSmem>{});
+  else
+    vk_dispatch(vkind, f);
 }
 
 bool value_index_enabled() {
@@ -1062,7 +1082,7 @@ void enq_resnorm(pf_hierarchy* h, int l, const double* x, const double* b) {
   const bool single = h->world == 1;
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = L.sub[s];
-    vk_dispatch(D.A.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
     launch(static_cast<unsigned>(D.resnorm_blocks), kBlock, k_resnorm<decltype(V)::value>, view(D.A), x + D.offset,
            b + D.offset, D.n_own, D.partials.p, D.ticket.p, L.sumsq.p + s, single ? L.norm.p : nullptr);
     });
@@ -1074,7 +1094,7 @@ void enq_residual(pf_hierarchy* h, int l, const double* x, const double* b, doub
   Level& L = h->levels[l];
   auto launch = launcher(h);
   for (DevLevel& D : L.sub)
-    vk_dispatch(D.A.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
       launch(grid_for(D.n), kBlock, k_residual<decltype(V)::value>, view(D.A), x + D.offset, b + D.offset, r + D.offset, D.n);
     });
 }
@@ -1118,13 +1138,13 @@ void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega
   if (r1 <= r0) return;
   auto launch = launcher(h);
   const int split = split_row_len();
-  vk_dispatch(D.A.vals.vkind, [&](auto V) {
+  vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
     constexpr int vk = decltype(V)::value;
     if (split > 0 && D.A.max_len > split && D.n_own <= split_max_rows()) {
       const int32_t width = (D.A.max_len + 3) / 4 * 4;
       const size_t smem = sizeof(double) * kSlice * static_cast<size_t>(width);
       auto kern = sor ? k_color_sweep_split<true, vk> : k_color_sweep_split<false, vk>;
-      static thread_local const void* attr_set[2][4] = {};
+      static thread_local const void* attr_set[2][8] = {};
       if (smem > 48 * 1024 && attr_set[sor][vk + 1] != reinterpret_cast<const void*>(smem)) {
         PF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr_set[sor][vk + 1] = reinterpret_cast<const void*>(smem);
@@ -1159,7 +1179,7 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
         // stream overlapped with the interior rows
         const DevLevel& D = L.sub[0];
         const bool last = sweep + 1 == sc.sweeps;
-        vk_dispatch(D.A.vals.vkind, [&](auto V) {
+        vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
           constexpr int vk = decltype(V)::value;
           launch(std::max<unsigned>(grid_for(D.n_brows), 1u) + grid_for(D.n - D.n_own), kBlock, k_jacobi_boundary<vk>,
                  view(D.A), static_cast<const int32_t*>(D.brows.p), D.n_brows,
@@ -1169,7 +1189,7 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
         PF_CUDA(cudaEventRecord(h->ev_fork, h->stream));
         PF_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_fork, 0));
         enq_plan(h, last && then_h2 ? L.fused_all : L.fused_ms_h1, bufs[cur ^ 1], h->comm_stream);
-        vk_dispatch(D.A.vals.vkind, [&](auto V) {
+        vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
           constexpr int vk = decltype(V)::value;
           launch(grid_for(D.n_own), kBlock, k_jacobi_interior<vk>, view(D.A),
                  static_cast<const uint8_t*>(D.is_brow.p), static_cast<const double*>(bufs[cur] + D.offset),
@@ -1184,7 +1204,7 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
       if (sc.kind == PF_SMOOTHER_JACOBI) {
         if (!(first_done && sweep == 0 && local == 0))
           for (DevLevel& D : L.sub)
-            vk_dispatch(D.A.vals.vkind, [&](auto V) {
+            vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
               launch(grid_for(D.n), kBlock, k_jacobi<decltype(V)::value>, view(D.A),
                      static_cast<const double*>(bufs[cur] + D.offset), bufs[cur ^ 1] + D.offset, b + D.offset,
                      D.n_own, D.n, sc.damping);
@@ -1221,7 +1241,7 @@ void enq_prolong(pf_hierarchy* h, int fine, const double* xc, double* xf, int ad
   auto launch = launcher(h);
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = F.sub[s];
-    vk_dispatch(D.P.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.P.vals.vkind, [&](auto V) {
       launch(grid_for(D.n), kBlock, k_prolong_add<decltype(V)::value>, view(D.P), xc + Cl.sub[s].offset,
              xf + D.offset, D.n, add);
     });
@@ -1236,7 +1256,7 @@ void enq_restrict(pf_hierarchy* h, int fine, const double* rf, double* bc, doubl
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = F.sub[s];
     DevLevel& DC = Cl.sub[s];
-    vk_dispatch(D.R.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.R.vals.vkind, [&](auto V) {
       launch(grid_for(DC.n), kBlock, k_restrict<decltype(V)::value>, view(D.R), rf + D.offset, bc + DC.offset,
              xc ? xc + DC.offset : nullptr, static_cast<const uint8_t*>(DC.d_is_dir.p), DC.n, zero_dir);
     });
@@ -1438,7 +1458,7 @@ void enq_norm_head(pf_hierarchy* h, pf_vector* x, const double* b, const pf_mult
   auto launch = launcher(h);
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = L.sub[s];
-    vk_dispatch(D.A.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
       constexpr int vk = decltype(V)::value;
       if (fused_head(cfg))
         launch(grid_for(D.n), kBlock, k_jacobi_norm<vk>, view(D.A), static_cast<const double*>(x->cur() + D.offset),
@@ -2438,7 +2458,7 @@ pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double*
     if (kind == PF_SMOOTHER_JACOBI) {
       const double* src = (i & 1) ? x->alt() : x->cur();
       double* dst = (i & 1) ? x->cur() : x->alt();
-      vk_dispatch(D.A.vals.vkind, [&](auto V) {
+      vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
         launch(grid_for(D.n), kBlock, k_jacobi<decltype(V)::value>, view(D.A), src, dst, b, D.n_own, D.n, 0.8);
       });
     } else {

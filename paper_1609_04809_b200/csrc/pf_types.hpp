@@ -32,17 +32,21 @@ constexpr int kChunkGroups = PF_CHUNK_GROUPS;  // groups of 4 entries per chunk 
 #endif
 // colour sweeps are single-wave launches: a row's latency chain, not throughput, bounds them
 constexpr int kSorChunkGroups = PF_SOR_GROUPS;
-// Minimum resident blocks per SM of the row kernels: 4 x 256 threads leaves 64 registers,
+// Minimum resident blocks per SM of the row kernels.  4 x 256 threads leaves 64 registers,
 // enough for the software-pipelined group loop without spills (measured at C2 against 8
 // blocks / 32 registers with spills: sweep 97 -> 87 us, SOR colour sweep 153 -> 109 us).
+// With the value table in shared memory the Jacobi / residual / norm kernels fit 48
+// registers without spills, and 5 blocks (40 warps per SM) hide more of the x-gather
+// latency: finest sweep 87.9 -> 75.7 us, C2 Jacobi solve 6.66 -> 6.34 ms.  6 blocks (40
+// registers) is slower again (89 us), and the colour sweeps lose at 5 (106.5 -> 109.8 us).
 #ifndef PF_SOR_MINB
 #define PF_SOR_MINB 4
 #endif
 #ifndef PF_JAC_MINB
-#define PF_JAC_MINB 4
+#define PF_JAC_MINB 5
 #endif
 #ifndef PF_ROW_MINB
-#define PF_ROW_MINB 4
+#define PF_ROW_MINB 5
 #endif
 
 // SELL-32x4 layout: slice s holds rows 32s..32s+31; entry j of lane l sits at
@@ -68,6 +72,7 @@ struct SellView {
   const void* __restrict__ vidx;
   const double* __restrict__ table;
   int32_t vkind;
+  int32_t table_n;  // distinct values in the table
 };
 
 // One subdomain of the coarse level, for the sequential coarse solve.
