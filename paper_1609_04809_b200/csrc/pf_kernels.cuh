@@ -32,35 +32,58 @@ namespace pf {
     asm volatile("griddepcontrol.launch_dependents;" :::);     \
   } while (0)
 
-// kVK == kVKSmem: 8-bit value indices (vkind 1) with the table staged in shared memory
-// by the kernel's prologue (vtab_stage), so the per-entry value lookup is a shared-memory
-// broadcast instead of an L1 request competing with the x gathers.
+// The kernels' value-kind template argument kVK: bits 0-2 the stored value kind (0 fp64,
+// 1 8-bit index, 2 16-bit index, kVKSmem = 8-bit index with the table staged in shared
+// memory by the kernel's prologue, vtab_stage, so the per-entry value lookup is a
+// shared-memory broadcast instead of an L1 request competing with the x gathers), bit 3
+// (kVKCached) the operator-stream load policy; -1 = everything read from the view.
+//   * evict-first (ld.global.cs): levels whose operator is far larger than L2 (the finest
+//     levels) are streamed once per sweep and must not push x out of L2;
+//   * cached (ld.global.nc): the coarser levels whose operator fits L2 are re-read by every
+//     sweep of the cycle and keep living there (C2: Jacobi solve 6.33 -> 6.21 ms, SOR
+//     11.57 -> 10.91 ms).  Measured without gain: L1::no_allocate loads (Jacobi 6.37 ms,
+//     SOR unchanged), plus an L2::evict_last cache policy (6.38 ms); caching the finest
+//     level of a 64^3 hierarchy, whose 39 MB operator also fits, costs 6 %.
 constexpr int kVKSmem = 4;
+constexpr int kVKCached = 8;
+template <int kVK>
+constexpr int vk_kind() { return kVK < 0 ? kVK : (kVK & 7); }
+template <int kVK>
+constexpr bool vk_cached() { return kVK >= 0 && (kVK & kVKCached) != 0; }
 __shared__ double s_vtab[256];
 
 template <int kVK>
 __device__ __forceinline__ void vtab_stage(const SellView& A) {
-  if constexpr (kVK == kVKSmem) {
+  if constexpr (vk_kind<kVK>() == kVKSmem) {
     for (int i = threadIdx.x; i < A.table_n; i += blockDim.x) s_vtab[i] = A.table[i];
     __syncthreads();
   }
 }
 
-__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
-__device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
+#ifndef PF_LD_OP
+#define PF_LD_OP __ldcs
+#endif
+template <int kVK, typename T>
+__device__ __forceinline__ T ld_op(const T* p) {
+  if constexpr (vk_cached<kVK>())
+    return __ldg(p);
+  else
+    return PF_LD_OP(p);
+}
 
 // Value of stored entry e.  kVK = the view's value kind when known at compile time (the
 // bandwidth kernels are instantiated per kind), -1 = read it from the view.
 template <int kVK>
 __device__ __forceinline__ double sell_val(const SellView& A, int64_t e) {
-  if constexpr (kVK == 0) {
-    return ld_stream(A.vals + e);
-  } else if constexpr (kVK == 1) {
-    return __ldg(A.table + __ldcs(static_cast<const unsigned char*>(A.vidx) + e));
-  } else if constexpr (kVK == kVKSmem) {
-    return s_vtab[__ldcs(static_cast<const unsigned char*>(A.vidx) + e)];
-  } else if constexpr (kVK == 2) {
-    return __ldg(A.table + __ldcs(static_cast<const unsigned short*>(A.vidx) + e));
+  constexpr int K = vk_kind<kVK>();
+  if constexpr (K == 0) {
+    return ld_op<kVK>(A.vals + e);
+  } else if constexpr (K == 1) {
+    return __ldg(A.table + ld_op<kVK>(static_cast<const unsigned char*>(A.vidx) + e));
+  } else if constexpr (K == kVKSmem) {
+    return s_vtab[ld_op<kVK>(static_cast<const unsigned char*>(A.vidx) + e)];
+  } else if constexpr (K == 2) {
+    return __ldg(A.table + ld_op<kVK>(static_cast<const unsigned short*>(A.vidx) + e));
   } else {
     if (A.vkind == 1) return __ldg(A.table + static_cast<const unsigned char*>(A.vidx)[e]);
     if (A.vkind == 2) return __ldg(A.table + static_cast<const unsigned short*>(A.vidx)[e]);
@@ -71,28 +94,29 @@ __device__ __forceinline__ double sell_val(const SellView& A, int64_t e) {
 // One group of 4 stored entries (SELL-32x4) starting at e (e % 4 == 0): columns and values.
 template <int kVK>
 __device__ __forceinline__ void sell_group(const SellView& A, int64_t e, int32_t c[4], double v[4]) {
-  const int4 cc = __ldcs(reinterpret_cast<const int4*>(A.cols + e));
+  constexpr int K = vk_kind<kVK>();
+  const int4 cc = ld_op<kVK>(reinterpret_cast<const int4*>(A.cols + e));
   c[0] = cc.x;
   c[1] = cc.y;
   c[2] = cc.z;
   c[3] = cc.w;
-  if constexpr (kVK == 1) {
-    const unsigned int w = __ldcs(reinterpret_cast<const unsigned int*>(static_cast<const unsigned char*>(A.vidx) + e));
+  if constexpr (K == 1) {
+    const unsigned int w = ld_op<kVK>(reinterpret_cast<const unsigned int*>(static_cast<const unsigned char*>(A.vidx) + e));
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = __ldg(A.table + ((w >> (8 * k)) & 255u));
-  } else if constexpr (kVK == kVKSmem) {
-    const unsigned int w = __ldcs(reinterpret_cast<const unsigned int*>(static_cast<const unsigned char*>(A.vidx) + e));
+  } else if constexpr (K == kVKSmem) {
+    const unsigned int w = ld_op<kVK>(reinterpret_cast<const unsigned int*>(static_cast<const unsigned char*>(A.vidx) + e));
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = s_vtab[(w >> (8 * k)) & 255u];
-  } else if constexpr (kVK == 2) {
-    const uint2 w = __ldcs(reinterpret_cast<const uint2*>(static_cast<const unsigned short*>(A.vidx) + e));
+  } else if constexpr (K == 2) {
+    const uint2 w = ld_op<kVK>(reinterpret_cast<const uint2*>(static_cast<const unsigned short*>(A.vidx) + e));
     v[0] = __ldg(A.table + (w.x & 0xffffu));
     v[1] = __ldg(A.table + (w.x >> 16));
     v[2] = __ldg(A.table + (w.y & 0xffffu));
     v[3] = __ldg(A.table + (w.y >> 16));
-  } else if constexpr (kVK == 0) {
-    const double2 a = __ldcs(reinterpret_cast<const double2*>(A.vals + e));
-    const double2 b = __ldcs(reinterpret_cast<const double2*>(A.vals + e + 2));
+  } else if constexpr (K == 0) {
+    const double2 a = ld_op<kVK>(reinterpret_cast<const double2*>(A.vals + e));
+    const double2 b = ld_op<kVK>(reinterpret_cast<const double2*>(A.vals + e + 2));
     v[0] = a.x;
     v[1] = a.y;
     v[2] = b.x;

@@ -134,13 +134,34 @@ bool vtab_smem() {
   return on;
 }
 
-// vk_dispatch for the operator row kernels that stage the value table (vtab_stage).
+// Operators of the levels below the finest up to PF_CACHED_MAX_BYTES (default 48 MB, about
+// 40 % of the 126 MB L2) are read with the caching load policy (kVKCached): they stay
+// L2-resident across the sweeps of a cycle.  The finest level, and larger ones, stream
+// evict-first.
+int64_t cached_max_bytes() {
+  static const int64_t m = [] {
+    const char* e = std::getenv("PF_CACHED_MAX_BYTES");
+    return e ? std::atoll(e) : int64_t(48) << 20;
+  }();
+  return m;
+}
+
+// vk_dispatch for the operator row kernels (they stage the value table, vtab_stage, and
+// pick the load policy from the kVKCached bit).
 template <typename F>
-void vk_dispatch_rows(int vkind, F&& f) {
-  if (vkind == 1 && vtab_smem())
-    f(std::integral_constant<int, kVKSmem>{});
-  else
-    vk_dispatch(vkind, f);
+void vk_dispatch_rows(const DevSell& S, F&& f) {
+  const bool cached = S.keep_l2;
+  const int kind = S.vals.vkind == 1 && vtab_smem() ? kVKSmem : S.vals.vkind;
+  switch (kind | (cached ? kVKCached : 0)) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case kVKSmem: f(std::integral_constant<int, kVKSmem>{}); break;
+    case kVKCached: f(std::integral_constant<int, kVKCached>{}); break;
+    case 1 | kVKCached: f(std::integral_constant<int, 1 | kVKCached>{}); break;
+    case 2 | kVKCached: f(std::integral_constant<int, 2 | kVKCached>{}); break;
+    case kVKSmem | kVKCached: f(std::integral_constant<int, kVKSmem | kVKCached>{}); break;
+    default: f(std::integral_constant<int, 0>{}); break;
+  }
 }
 
 bool value_index_enabled() {
@@ -1082,7 +1103,7 @@ void enq_resnorm(pf_hierarchy* h, int l, const double* x, const double* b) {
   const bool single = h->world == 1;
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = L.sub[s];
-    vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.A, [&](auto V) {
     launch(static_cast<unsigned>(D.resnorm_blocks), kBlock, k_resnorm<decltype(V)::value>, view(D.A), x + D.offset,
            b + D.offset, D.n_own, D.partials.p, D.ticket.p, L.sumsq.p + s, single ? L.norm.p : nullptr);
     });
@@ -1094,7 +1115,7 @@ void enq_residual(pf_hierarchy* h, int l, const double* x, const double* b, doub
   Level& L = h->levels[l];
   auto launch = launcher(h);
   for (DevLevel& D : L.sub)
-    vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.A, [&](auto V) {
       launch(grid_for(D.n), kBlock, k_residual<decltype(V)::value>, view(D.A), x + D.offset, b + D.offset, r + D.offset, D.n);
     });
 }
@@ -1138,13 +1159,13 @@ void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega
   if (r1 <= r0) return;
   auto launch = launcher(h);
   const int split = split_row_len();
-  vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
+  vk_dispatch_rows(D.A, [&](auto V) {
     constexpr int vk = decltype(V)::value;
     if (split > 0 && D.A.max_len > split && D.n_own <= split_max_rows()) {
       const int32_t width = (D.A.max_len + 3) / 4 * 4;
       const size_t smem = sizeof(double) * kSlice * static_cast<size_t>(width);
       auto kern = sor ? k_color_sweep_split<true, vk> : k_color_sweep_split<false, vk>;
-      static thread_local const void* attr_set[2][8] = {};
+      static thread_local const void* attr_set[2][16] = {};
       if (smem > 48 * 1024 && attr_set[sor][vk + 1] != reinterpret_cast<const void*>(smem)) {
         PF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr_set[sor][vk + 1] = reinterpret_cast<const void*>(smem);
@@ -1179,7 +1200,7 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
         // stream overlapped with the interior rows
         const DevLevel& D = L.sub[0];
         const bool last = sweep + 1 == sc.sweeps;
-        vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
+        vk_dispatch_rows(D.A, [&](auto V) {
           constexpr int vk = decltype(V)::value;
           launch(std::max<unsigned>(grid_for(D.n_brows), 1u) + grid_for(D.n - D.n_own), kBlock, k_jacobi_boundary<vk>,
                  view(D.A), static_cast<const int32_t*>(D.brows.p), D.n_brows,
@@ -1189,7 +1210,7 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
         PF_CUDA(cudaEventRecord(h->ev_fork, h->stream));
         PF_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_fork, 0));
         enq_plan(h, last && then_h2 ? L.fused_all : L.fused_ms_h1, bufs[cur ^ 1], h->comm_stream);
-        vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
+        vk_dispatch_rows(D.A, [&](auto V) {
           constexpr int vk = decltype(V)::value;
           launch(grid_for(D.n_own), kBlock, k_jacobi_interior<vk>, view(D.A),
                  static_cast<const uint8_t*>(D.is_brow.p), static_cast<const double*>(bufs[cur] + D.offset),
@@ -1204,7 +1225,7 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
       if (sc.kind == PF_SMOOTHER_JACOBI) {
         if (!(first_done && sweep == 0 && local == 0))
           for (DevLevel& D : L.sub)
-            vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
+            vk_dispatch_rows(D.A, [&](auto V) {
               launch(grid_for(D.n), kBlock, k_jacobi<decltype(V)::value>, view(D.A),
                      static_cast<const double*>(bufs[cur] + D.offset), bufs[cur ^ 1] + D.offset, b + D.offset,
                      D.n_own, D.n, sc.damping);
@@ -1241,7 +1262,7 @@ void enq_prolong(pf_hierarchy* h, int fine, const double* xc, double* xf, int ad
   auto launch = launcher(h);
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = F.sub[s];
-    vk_dispatch_rows(D.P.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.P, [&](auto V) {
       launch(grid_for(D.n), kBlock, k_prolong_add<decltype(V)::value>, view(D.P), xc + Cl.sub[s].offset,
              xf + D.offset, D.n, add);
     });
@@ -1256,7 +1277,7 @@ void enq_restrict(pf_hierarchy* h, int fine, const double* rf, double* bc, doubl
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = F.sub[s];
     DevLevel& DC = Cl.sub[s];
-    vk_dispatch_rows(D.R.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.R, [&](auto V) {
       launch(grid_for(DC.n), kBlock, k_restrict<decltype(V)::value>, view(D.R), rf + D.offset, bc + DC.offset,
              xc ? xc + DC.offset : nullptr, static_cast<const uint8_t*>(DC.d_is_dir.p), DC.n, zero_dir);
     });
@@ -1458,7 +1479,7 @@ void enq_norm_head(pf_hierarchy* h, pf_vector* x, const double* b, const pf_mult
   auto launch = launcher(h);
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = L.sub[s];
-    vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
+    vk_dispatch_rows(D.A, [&](auto V) {
       constexpr int vk = decltype(V)::value;
       if (fused_head(cfg))
         launch(grid_for(D.n), kBlock, k_jacobi_norm<vk>, view(D.A), static_cast<const double*>(x->cur() + D.offset),
@@ -2008,6 +2029,13 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
                                    L.cp_cols, L.cp_vals);
     }
   }
+  // load policy of the operators: the levels below the finest that fit the L2 budget are
+  // read with the caching policy (vk_dispatch_rows)
+  for (int l = 0; l + 1 < h->n_levels; ++l)
+    for (DevLevel& D : h->levels[l].sub)
+      for (DevSell* S : {&D.A, &D.P, &D.R})
+        S->keep_l2 = S->vals.bytes() + S->cols.bytes() + S->row_len.bytes() + S->slice_ptr.bytes() <=
+                     cached_max_bytes();
   if (h->world != h->n_sub) build_replica(h);
   h->staging.alloc(max_total);
   for (int l = 0; l < h->n_levels; ++l) {
@@ -2458,7 +2486,7 @@ pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double*
     if (kind == PF_SMOOTHER_JACOBI) {
       const double* src = (i & 1) ? x->alt() : x->cur();
       double* dst = (i & 1) ? x->cur() : x->alt();
-      vk_dispatch_rows(D.A.vals.vkind, [&](auto V) {
+      vk_dispatch_rows(D.A, [&](auto V) {
         launch(grid_for(D.n), kBlock, k_jacobi<decltype(V)::value>, view(D.A), src, dst, b, D.n_own, D.n, 0.8);
       });
     } else {

@@ -97,6 +97,7 @@ struct DevSell {
   DevBuf<int32_t> row_len;
   int64_t nnz = 0, own_nnz = 0, stored = 0;
   int32_t max_len = 0;  // longest row
+  bool keep_l2 = false;  // read with the caching policy (kVKCached): coarse levels that fit L2
 };
 
 // One subdomain of one level on the device.
