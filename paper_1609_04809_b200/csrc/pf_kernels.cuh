@@ -71,6 +71,31 @@ __device__ __forceinline__ T ld_op(const T* p) {
     return PF_LD_OP(p);
 }
 
+// L2 prefetch of a row's groups 1..kPf (columns and value indices) at the start of the row,
+// so the software-pipelined loop's loads find them in L2 without holding registers.  Only
+// for the streamed (evict-first) operators, in the Jacobi / residual / norm kernels
+// (measured at C2: 6 groups = a whole Q1 row, finest sweep 75.7 -> 73.9 us, Jacobi solve
+// 6.18 -> 6.09 ms; the colour sweeps lose with it, 106.5 -> 117.9 us).
+#ifndef PF_PREFETCH_GROUPS
+#define PF_PREFETCH_GROUPS 6
+#endif
+constexpr int kPrefetch = PF_PREFETCH_GROUPS;
+template <int kVK, int kPf>
+__device__ __forceinline__ void row_prefetch(const SellView& A, int64_t base, int len) {
+  if constexpr (kPf > 0 && !vk_cached<kVK>() && kVK >= 0) {
+    const int ng = (len + 3) / 4;
+#pragma unroll
+    for (int g = 1; g <= kPf; ++g) {
+      if (g < ng) {
+        const int64_t e = sell_entry(base, 4 * g);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.cols + e));
+        if constexpr (vk_kind<kVK>() == 1 || vk_kind<kVK>() == kVKSmem)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const unsigned char*>(A.vidx) + e));
+      }
+    }
+  }
+}
+
 // Value of stored entry e.  kVK = the view's value kind when known at compile time (the
 // bandwidth kernels are instantiated per kind), -1 = read it from the view.
 template <int kVK>
@@ -153,7 +178,7 @@ __device__ __forceinline__ void offdiag_group(const int32_t c[4], const double v
   }
 }
 
-template <bool kReadOnlyX, bool kRes = false, int kVK = -1, int kGroups = kChunkGroups>
+template <bool kReadOnlyX, bool kRes = false, int kVK = -1, int kGroups = kChunkGroups, int kPf = 0>
 __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, const double* x,
                                             double& acc, double& diag, double* res = nullptr,
                                             double x_row = 0.0) {
@@ -161,6 +186,7 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
   // diagonal included — the reference's residual_norm row (linalg.cpp:66-70) bit for bit.
   const int64_t base = sell_row_base(A.slice_ptr, row);
   const int len = A.row_len[row];
+  row_prefetch<kVK, kPf>(A, base, len);
   double r = kRes ? *res : 0.0;
   if (len > 0) {
     int32_t c[4];
@@ -197,11 +223,12 @@ __device__ __forceinline__ void dot_group(const int32_t c[4], const double v[4],
     if (k < n) acc = kSubtract ? __dsub_rn(acc, __dmul_rn(v[k], xv[k])) : __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
 }
 
-template <bool kSubtract, bool kReadOnlyX = true, int kVK = -1, int kGroups = kChunkGroups>
+template <bool kSubtract, bool kReadOnlyX = true, int kVK = -1, int kGroups = kChunkGroups, int kPf = kPrefetch>
 __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const double* __restrict__ x,
                                           double acc) {
   const int64_t base = sell_row_base(A.slice_ptr, row);
   const int len = A.row_len[row];
+  row_prefetch<kVK, kPf>(A, base, len);
   if (len > 0) {
     int32_t c[4];
     double v[4];
@@ -242,7 +269,7 @@ __global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi(SellView A, cons
     return;
   }
   double acc = b[row], diag = 0.0;
-  row_offdiag<true, false, kVK>(A, row, x_old, acc, diag);
+  row_offdiag<true, false, kVK, kChunkGroups, kPrefetch>(A, row, x_old, acc, diag);
   x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
 }
 
@@ -267,7 +294,7 @@ __global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi_boundary(SellVie
   if (i >= n_list) return;
   const int32_t row = list[i];
   double acc = b[row], diag = 0.0;
-  row_offdiag<true, false, kVK>(A, row, x_old, acc, diag);
+  row_offdiag<true, false, kVK, kChunkGroups, kPrefetch>(A, row, x_old, acc, diag);
   x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, x_old[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
 }
 
@@ -282,7 +309,7 @@ __global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi_interior(SellVie
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
   if (row >= n_own || is_b[row]) return;
   double acc = b[row], diag = 0.0;
-  row_offdiag<true, false, kVK>(A, row, x_old, acc, diag);
+  row_offdiag<true, false, kVK, kChunkGroups, kPrefetch>(A, row, x_old, acc, diag);
   x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, x_old[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
 }
 
@@ -515,7 +542,7 @@ __global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_jacobi_norm(SellView A,
       x_new[row] = xo;
     } else {
       double acc = b[row], diag = 0.0, res = b[row];
-      row_offdiag<true, true, kVK>(A, row, x_old, acc, diag, &res, xo);
+      row_offdiag<true, true, kVK, kChunkGroups, kPrefetch>(A, row, x_old, acc, diag, &res, xo);
       sq = __dmul_rn(res, res);
       x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
     }
