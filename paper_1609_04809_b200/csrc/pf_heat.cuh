@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kBlock) k_load(LoadView L, double s, double* _
 // b = Op u + half_dt (load_now + load_next) on every non-Dirichlet row (app.cpp:191-194:
 // spmv, then b_i += 0.5 dt (ln_i + lnx_i)); Dirichlet rows are written by k_dirichlet.
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_cn_rhs(SellView Op, const double* __restrict__ u,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_cn_rhs(SellView Op, const double* __restrict__ u,
                                                    const double* __restrict__ ln,
                                                    const double* __restrict__ lnx, double half_dt,
                                                    const uint8_t* __restrict__ is_dir,

@@ -52,6 +52,12 @@ template <int kVK>
 constexpr bool vk_cached() { return kVK >= 0 && (kVK & kVKCached) != 0; }
 __shared__ double s_vtab[256];
 
+// Resident blocks per SM of a row kernel: `minb` (pf_types.hpp), except for the streamed
+// fp64 operators (kVK == 0: the per-cell-coefficient finest levels, at the HBM roofline),
+// which keep 4 blocks / 64 registers (measured: lognormal C2 sweep 114 us at 4, 117 at 5).
+template <int kVK>
+constexpr int minb_for(int minb) { return kVK == 0 ? 4 : minb; }
+
 template <int kVK>
 __device__ __forceinline__ void vtab_stage(const SellView& A) {
   if constexpr (vk_kind<kVK>() == kVKSmem) {
@@ -73,7 +79,7 @@ __device__ __forceinline__ T ld_op(const T* p) {
 
 // L2 prefetch of a row's groups 1..kPf (columns and value indices) at the start of the row,
 // so the software-pipelined loop's loads find them in L2 without holding registers.  Only
-// for the streamed (evict-first) operators, in the Jacobi / residual / norm kernels
+// for the streamed (evict-first) index-valued operators, in the Jacobi / residual / norm kernels
 // (measured at C2: 6 groups = a whole Q1 row, finest sweep 75.7 -> 73.9 us, Jacobi solve
 // 6.18 -> 6.09 ms; the colour sweeps lose with it, 106.5 -> 117.9 us).
 #ifndef PF_PREFETCH_GROUPS
@@ -82,7 +88,7 @@ __device__ __forceinline__ T ld_op(const T* p) {
 constexpr int kPrefetch = PF_PREFETCH_GROUPS;
 template <int kVK, int kPf>
 __device__ __forceinline__ void row_prefetch(const SellView& A, int64_t base, int len) {
-  if constexpr (kPf > 0 && !vk_cached<kVK>() && kVK >= 0) {
+  if constexpr (kPf > 0 && !vk_cached<kVK>() && kVK > 0) {
     const int ng = (len + 3) / 4;
 #pragma unroll
     for (int g = 1; g <= kPf; ++g) {
@@ -255,7 +261,7 @@ __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const 
 // x_new; every other row is carried over unchanged (the sweep never writes Slave,
 // Halo or Dirichlet entries, solvers.hpp:16-20).
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi(SellView A, const double* __restrict__ x_old,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_JAC_MINB)) k_jacobi(SellView A, const double* __restrict__ x_old,
                                                    double* __restrict__ x_new,
                                                    const double* __restrict__ b, int32_t n_own,
                                                    int32_t n, double omega) {
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi(SellView A, cons
 // interior rows (same per-row arithmetic as k_jacobi): the boundary rows from a list plus
 // the carry-over of the non-own rows, then the interior own rows.
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi_boundary(SellView A, const int32_t* __restrict__ list,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_JAC_MINB)) k_jacobi_boundary(SellView A, const int32_t* __restrict__ list,
                                                                     int32_t n_list, const double* __restrict__ x_old,
                                                                     double* __restrict__ x_new,
                                                                     const double* __restrict__ b, int32_t n_own,
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi_boundary(SellVie
 }
 
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_JAC_MINB) k_jacobi_interior(SellView A, const uint8_t* __restrict__ is_b,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_JAC_MINB)) k_jacobi_interior(SellView A, const uint8_t* __restrict__ is_b,
                                                                     const double* __restrict__ x_old,
                                                                     double* __restrict__ x_new,
                                                                     const double* __restrict__ b, int32_t n_own,
@@ -439,7 +445,7 @@ __global__ void __launch_bounds__(kSplitBlock) k_color_sweep_split(SellView A, d
 // Residual of the cycle (multigrid.cpp:166-167): y = A x (spmv order, acc from 0), r = b - y,
 // on rows [0, n).
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_residual(SellView A, const double* __restrict__ x,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_residual(SellView A, const double* __restrict__ x,
                                                      const double* __restrict__ b,
                                                      double* __restrict__ r, int32_t n) {
   vtab_stage<kVK>(A);
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_residual(SellView A, co
 
 // y = A x on every row (linalg.cpp:45-57).
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_spmv(SellView A, const double* __restrict__ x,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_spmv(SellView A, const double* __restrict__ x,
                                                  double* __restrict__ y, int32_t n) {
   PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
@@ -482,7 +488,7 @@ __device__ __forceinline__ double block_sum(double v, double* smem /* kBlock/32 
 // `norm_out` is set (single-subdomain case: the ascending-rank allreduce of one value
 // is 0.0 + s, transport.cpp:139-149), sqrt of it.  The ticket is reset for the next use.
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_resnorm(SellView A, const double* __restrict__ x,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_resnorm(SellView A, const double* __restrict__ x,
                                                     const double* __restrict__ b, int32_t n_own,
                                                     double* __restrict__ partials,
                                                     unsigned int* ticket, double* sumsq,
@@ -524,7 +530,7 @@ __global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_resnorm(SellView A, con
 // Deterministic block sums + last-block finish exactly as k_resnorm; *sumsq gets this
 // subdomain's sum of squares.
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_jacobi_norm(SellView A, const double* __restrict__ x_old,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_jacobi_norm(SellView A, const double* __restrict__ x_old,
                                                         double* __restrict__ x_new,
                                                         const double* __restrict__ b, int32_t n_own,
                                                         int32_t n, double omega,
@@ -579,7 +585,7 @@ __global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* o
 // x_f += P x_c over every local fine dof (multigrid.cpp:121-129 + :183-184): the
 // correction is accumulated from 0 in P's entry order, then added.
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_prolong_add(SellView P, const double* __restrict__ xc,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_prolong_add(SellView P, const double* __restrict__ xc,
                                                         double* __restrict__ xf, int32_t n_f, int add) {
   vtab_stage<kVK>(P);
   PF_PDL_ENTRY();
@@ -596,7 +602,7 @@ __global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_prolong_add(SellView P,
 // zeroed.  (Zeroing before the master/slave accumulate is equivalent: Dirichlet
 // carriers are Dirichlet on every rank, so they only ever accumulate zeros.)
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, PF_ROW_MINB) k_restrict(SellView R, const double* __restrict__ rf,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_restrict(SellView R, const double* __restrict__ rf,
                                                      double* __restrict__ bc,
                                                      double* __restrict__ xc,
                                                      const uint8_t* __restrict__ is_dir_c,
