@@ -404,7 +404,8 @@ def run_b200(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(),
                      "kernel": "k_jacobi (finest-level damped-Jacobi sweep; SELL-32x4, int32 columns, "
-                               "8-bit index into the table of distinct fp64 values)",
+                               "8-bit index into the table of distinct fp64 values staged in shared "
+                               "memory, row-start L2 prefetch, 48 registers / 5 blocks per SM)",
                      "kernel_us": sweep_ms * 1e3, "algorithmic_bytes_per_launch": alg_bytes,
                      "algorithmic_bytes_formula": "SURVEY.md 8(d): 12 z + 4 n + 8 m + 16 n (fp64 CSR)",
                      "stored_bytes_per_launch": sweep_bytes, "achieved_on_stored_bytes": achieved_stored,
