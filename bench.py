@@ -519,7 +519,7 @@ def run_b200_heat(args):
     run.t, run.step = 0.0, 0
     for _ in range(args.steps):
         run.run(1, cfg)
-        out[:] = run.u.download(0)
+        run.u.download(0, out=out)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)

@@ -1833,6 +1833,7 @@ struct pf_load {
     pf::DevBuf<double> dir_prof;   // profile at those rows
   };
   std::vector<Sub> sub;
+  std::unique_ptr<pf_vector> next;  // pf_heat_run's next-load scratch (kept across calls)
 };
 
 pf_hierarchy::~pf_hierarchy() {
@@ -2988,8 +2989,11 @@ pf_status pf_heat_run(pf_hierarchy* h, pf_operator* op, pf_load* ld, pf_vector* 
   if (steps < 0 || first_step < 0) invalid("steps must be >= 0");
   PF_CUDA(cudaSetDevice(h->device));
   Level& T = h->levels[top];
-  // the finest level's b scratch carries the step's rhs; one extra vector for the next load
-  std::unique_ptr<pf_vector> lnx(new_vector(h, top));
+  // the finest level's b scratch carries the step's rhs; one extra vector for the next load,
+  // allocated once per load object (a step-by-step caller must not pay a cudaMalloc/Free,
+  // which synchronises the device, every step)
+  if (!ld->next) ld->next.reset(new_vector(h, top));
+  pf_vector* lnx = ld->next.get();
   pf_vector* b = T.b;
   if (b == u || b == load_now) invalid("u / load_now alias the hierarchy's scratch");
   for (int k = 0; k < steps; ++k) {

@@ -101,8 +101,14 @@ class DeviceVector:
         _lib.check(_lib.lib().pf_vector_upload(self._p, sub, a.ctypes.data, a.size))
         return self
 
-    def download(self, sub: int = 0) -> np.ndarray:
-        out = np.empty(self.h.n_dofs(self.level, sub))
+    def download(self, sub: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+        """Host-order copy of subdomain `sub`; into `out` (contiguous float64, e.g. a pinned
+        buffer) when given, else into a new array."""
+        n = self.h.n_dofs(self.level, sub)
+        if out is None:
+            out = np.empty(n)
+        elif out.dtype != np.float64 or out.size != n or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a contiguous float64 array of {n} entries")
         _lib.check(_lib.lib().pf_vector_download(self._p, sub, out.ctypes.data, out.size))
         return out
 
