@@ -224,6 +224,7 @@ struct pf_hierarchy {
     void* desc = nullptr;  // device BotDesc
     void* stamps = nullptr;  // PF_BOTTOM_PROFILE phase timestamps
     std::vector<pf::DevBuf<int32_t>> color_bufs;
+    std::vector<pf::DevBuf<double>> val_bufs;  // fp64 copies of index-encoded operators
     Bottom() = default;
     Bottom(const Bottom&) = delete;
     Bottom& operator=(const Bottom&) = delete;

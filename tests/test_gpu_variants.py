@@ -1,12 +1,12 @@
 """The storage / load-policy variants of the row kernels, bit-exact against the oracle.
 
-At the default settings only operators with >= 2M stored entries get 8-bit / 16-bit value
-indices (the finest levels of C2-sized hierarchies), so the small hierarchies of the
-parity suite run the fp64 kernels on their finest level.  Here the parity suite is re-run
-in a subprocess (the settings are read once per process) with every operator
-index-encoded, so the value-table kernels — table in shared memory (kVKSmem) or read
-through L1, with the streamed (evict-first + row prefetch) or the cached load policy —
-are compared with the oracle bit for bit on the same cases as the fp64 ones.
+At the default settings every operator whose values allow it is index-encoded (8-bit /
+16-bit value indices, table in shared memory), the coarser levels that fit L2 are read
+with the caching load policy and the finest with evict-first loads + row prefetch, and
+the bottom kernel reads decoded fp64 copies.  Here the parity suite is re-run in a
+subprocess (the settings are read once per process) under the other storage / load-policy
+combinations, so every kernel variant is compared with the oracle bit for bit on the
+same cases.
 """
 import os
 import subprocess
@@ -20,10 +20,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 
 VARIANTS = {
-    # every operator index-encoded, value table in shared memory, coarse levels cached
-    "index_smem_cached": {"PF_VALUE_INDEX_MIN": "0"},
+    # only >= 2M-entry operators index-encoded: the small hierarchies run fp64 operators
+    # (cached below the finest) and the bottom kernel its native fp64 views
+    "fp64_small_levels": {"PF_VALUE_INDEX_MIN": "2097152"},
     # index-encoded, table through L1, every level streamed (evict-first + prefetch)
-    "index_l1_streamed": {"PF_VALUE_INDEX_MIN": "0", "PF_VTAB_SMEM": "0", "PF_CACHED_MAX_BYTES": "0"},
+    "index_l1_streamed": {"PF_VTAB_SMEM": "0", "PF_CACHED_MAX_BYTES": "0"},
     # fp64 everywhere, every level streamed
     "fp64_streamed": {"PF_VALUE_INDEX": "0", "PF_CACHED_MAX_BYTES": "0"},
 }
