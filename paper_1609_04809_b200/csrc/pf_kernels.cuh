@@ -616,6 +616,43 @@ __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_restrict
   if (xc) xc[row] = 0.0;
 }
 
+// Cycle residual + restriction of a small level in one launch (multigrid.cpp:166-176): one
+// warp per coarse row; lane j forms the residual of the row's j-th fine entry exactly as
+// k_residual does (b_f - A_f x, products summed from 0 in stored order), scales it by the
+// entry's weight, and lane 0 adds the products in R's stored order from 0 — k_restrict's
+// sum — then the Dirichlet zeroing and the coarse x = 0.  A fine residual shared by several
+// coarse rows is formed once per row (identical bits every time); on the latency-bound
+// small levels that redundancy is cheaper than a second launch.  R rows of <= 32 entries.
+template <int kVK>
+__global__ void __launch_bounds__(kBlock) k_residual_restrict(SellView A, SellView R, const double* __restrict__ x,
+                                                              const double* __restrict__ b, double* __restrict__ bc,
+                                                              double* __restrict__ xc,
+                                                              const uint8_t* __restrict__ is_dir_c, int32_t n_c,
+                                                              int zero_dirichlet) {
+  vtab_stage<kVK>(A);
+  PF_PDL_ENTRY();
+  const int32_t row = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_c) return;  // whole warps exit together
+  const int len = R.row_len[row];
+  double p = 0.0;
+  if (lane < len) {
+    const int64_t e = sell_entry(sell_row_base(R.slice_ptr, row), lane);
+    const int32_t f = R.cols[e];
+    const double r = __dsub_rn(b[f], row_dot<false, true, kVK>(A, f, x, 0.0));
+    p = __dmul_rn(sell_val<-1>(R, e), r);
+  }
+  double acc = 0.0;
+  for (int j = 0; j < len; ++j) {
+    const double pj = __shfl_sync(0xffffffffu, p, j);
+    acc = __dadd_rn(acc, pj);
+  }
+  if (lane == 0) {
+    bc[row] = (zero_dirichlet && is_dir_c[row]) ? 0.0 : acc;
+    if (xc) xc[row] = 0.0;
+  }
+}
+
 // Sequential coarse solve (solvers.cpp:70-92) of every subdomain held on this device:
 // per iteration, in-place Gauss-Seidel over each subdomain's own rows in the
 // reference's host order (host_of_own[i] = device row of host own dof i), then the

@@ -22,9 +22,12 @@ ROOT = os.path.dirname(HERE)
 VARIANTS = {
     # only >= 2M-entry operators index-encoded: the small hierarchies run fp64 operators
     # (cached below the finest) and the bottom kernel its native fp64 views
-    "fp64_small_levels": {"PF_VALUE_INDEX_MIN": "2097152"},
-    # index-encoded, table through L1, every level streamed (evict-first + prefetch)
-    "index_l1_streamed": {"PF_VTAB_SMEM": "0", "PF_CACHED_MAX_BYTES": "0"},
+    # (cached below the finest) and the bottom kernel its native fp64 views; the cycle
+    # residual and restriction as separate launches on every level
+    "fp64_small_levels": {"PF_VALUE_INDEX_MIN": "2097152", "PF_FUSED_RR_ROWS": "0"},
+    # index-encoded, table through L1, every level streamed (evict-first + prefetch), the
+    # fused residual + restriction on every level whose R rows fit a warp
+    "index_l1_streamed": {"PF_VTAB_SMEM": "0", "PF_CACHED_MAX_BYTES": "0", "PF_FUSED_RR_ROWS": "100000000"},
     # fp64 everywhere, every level streamed
     "fp64_streamed": {"PF_VALUE_INDEX": "0", "PF_CACHED_MAX_BYTES": "0"},
 }
