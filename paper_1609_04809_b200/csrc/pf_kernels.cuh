@@ -54,9 +54,16 @@ __shared__ double s_vtab[256];
 
 // Resident blocks per SM of a row kernel: `minb` (pf_types.hpp), except for the streamed
 // fp64 operators (kVK == 0: the per-cell-coefficient finest levels, at the HBM roofline),
-// which keep 4 blocks / 64 registers (measured: lognormal C2 sweep 114 us at 4, 117 at 5).
+// which keep 4 blocks / 64 registers (measured: lognormal C2 sweep 114 us at 4, 117 at 5),
+// and the cached (L2-resident, coarser) operators: PF_CACHED_MINB = 4 (C2 Jacobi solve
+// 5.78 -> 5.74 ms; 6 or 8 blocks: 6.24 ms).
+#ifndef PF_CACHED_MINB
+#define PF_CACHED_MINB 4
+#endif
 template <int kVK>
-constexpr int minb_for(int minb) { return kVK == 0 ? 4 : minb; }
+constexpr int minb_for(int minb) {
+  return kVK == 0 ? 4 : (PF_CACHED_MINB > 0 && vk_cached<kVK>()) ? PF_CACHED_MINB : minb;
+}
 
 template <int kVK>
 __device__ __forceinline__ void vtab_stage(const SellView& A) {
