@@ -230,6 +230,26 @@ pf_status pf_loopback_create(int world_size, void** hub);
 pf_status pf_loopback_destroy(void* hub);
 pf_status pf_hierarchy_init_loopback(pf_hierarchy* h, void* hub);
 
+/* Peer-memory transport (NVLink / NVSwitch P2P over CUDA IPC, several processes on one
+ * GPU, or several hierarchies of one process): every exchange of the V-cycle — the
+ * master/slave and halo scatters, the master accumulate, the allgathers of the norm and of
+ * the replicated coarse levels — becomes ONE kernel that stores the values straight into
+ * the receiving rank's memory and synchronises through per-pair sequence flags there
+ * (replaces Transport send/recv, transport.cpp:92-104, under fecomm.cpp:25-62, and the
+ * allgather of allreduce_sum, transport.cpp:139-165).  Capturable: solve_outer records the
+ * exchanges into its CUDA graph.  Setup, collective over the ranks, after finalize:
+ *   1. pf_hierarchy_peer_export(h, NULL, 0, &n) sizes this rank's blob (allocating the
+ *      peer-visible arena); pf_hierarchy_peer_export(h, buf, n, &n) writes it;
+ *   2. the caller allgathers the blobs (any host fabric), each padded to a common stride;
+ *   3. pf_hierarchy_init_peer(h, blobs, stride) maps every peer's arena and activates.
+ * Every rank must pass the same hierarchy shape (levels, fused exchanges, replicas).
+ * A wait that exceeds PF_WATCHDOG_S (default 120 s) raises PF_ERR_TRANSPORT at the next
+ * synchronisation (the reference fabric's watchdog, transport.cpp:54-60). */
+pf_status pf_hierarchy_peer_export(pf_hierarchy* h, void* blob, int64_t capacity, int64_t* size);
+pf_status pf_hierarchy_init_peer(pf_hierarchy* h, const void* blobs, int64_t stride);
+/* CUDA graphs the hierarchy has captured and cached (solve graphs, outer-cycle graphs). */
+pf_status pf_hierarchy_graph_count(const pf_hierarchy* h, int64_t* out);
+
 /* Device bytes held by the hierarchy (matrices, transfers, plans, scratch). */
 pf_status pf_hierarchy_device_bytes(const pf_hierarchy* h, int64_t* out);
 

@@ -22,6 +22,8 @@
 
 namespace pf {
 
+struct ExchangePlan;  // pf_runtime.hpp
+
 struct Transport {
   virtual ~Transport() = default;
   virtual void group_start() = 0;
@@ -35,6 +37,14 @@ struct Transport {
   // carries this transport's operations give up after this many seconds (0: never)
   virtual double watchdog_seconds() const { return 0.0; }
   virtual void abort() {}
+  // Direct transports (PeerTransport, pf_peer.hpp) execute a whole exchange plan as one
+  // kernel that stores straight into the peers' memory, instead of pack + send/recv +
+  // unpack.  run_plan: receivers scatter into v, or with wait_only only wait for their
+  // messages; the caller then consumes staging(P) (the master accumulate) and ack_plan()s.
+  virtual bool direct() const { return false; }
+  virtual void run_plan(const ExchangePlan&, double*, bool, cudaStream_t) {}
+  virtual const double* staging(const ExchangePlan&) const { return nullptr; }
+  virtual void ack_plan(const ExchangePlan&, cudaStream_t) {}
 };
 
 struct Nccl final : Transport {

@@ -106,6 +106,18 @@ Launcher launcher(pf_hierarchy* h, cudaStream_t stream = nullptr) {
   return Launcher{h, g_capture_counter ? g_capture_counter : &h->launches, stream};
 }
 
+}  // namespace
+
+// Kernel-launch accounting and the PDL switch for launches made outside this file
+// (pf_peer.cu).
+int64_t* launch_counter(pf_hierarchy* h) { return g_capture_counter ? g_capture_counter : &h->launches; }
+bool pdl_on() { return pdl_enabled(); }
+// pf_peer.cu
+int64_t peer_export(pf_hierarchy* h, void* buf, int64_t cap);
+void peer_import(pf_hierarchy* h, const void* blobs, int64_t stride);
+
+namespace {
+
 SellView view_of(const DevVals& v, const DevSell& s) {
   const void* idx = v.vkind == 1 ? static_cast<const void*>(v.vi8.p)
                   : v.vkind == 2 ? static_cast<const void*>(v.vi16.p) : nullptr;
@@ -1076,6 +1088,10 @@ void enq_plan(pf_hierarchy* h, ExchangePlan& P, double* v, cudaStream_t st) {
   }
   // collective on every rank, even one with nothing to move on this channel
   if (!h->xport) state("multi-process hierarchy used before pf_hierarchy_init_nccl");
+  if (h->xport->direct()) {  // one kernel: stores into the peers' staging, waits, scatters
+    h->xport->run_plan(P, v, false, st);
+    return;
+  }
   launch(grid_for(P.pack_idx.n), kBlock, k_pack, static_cast<const double*>(v),
          static_cast<const int32_t*>(P.pack_idx.p), P.sendbuf.p, static_cast<int32_t>(P.pack_idx.n));
   h->xport->group_start();
@@ -1097,6 +1113,14 @@ void enq_accumulate(pf_hierarchy* h, int l, double* v) {
     return;
   }
   if (!h->xport) state("multi-process hierarchy used before pf_hierarchy_init_nccl");
+  if (h->xport->direct()) {  // partials stored into the masters' staging, summed there in peer order
+    h->xport->run_plan(A, v, true, h->stream);
+    launch(grid_for(A.n_masters), kBlock, k_unpack_accumulate, h->xport->staging(A),
+           static_cast<const int32_t*>(A.acc_off.p), static_cast<const int32_t*>(A.acc_src.p),
+           static_cast<const int32_t*>(A.acc_dst.p), v, A.n_masters);
+    h->xport->ack_plan(A, h->stream);
+    return;
+  }
   launch(grid_for(A.pack_idx.n), kBlock, k_pack, static_cast<const double*>(v),
          static_cast<const int32_t*>(A.pack_idx.p), A.sendbuf.p, static_cast<int32_t>(A.pack_idx.n));
   h->xport->group_start();
@@ -2203,6 +2227,26 @@ pf_status pf_hierarchy_init_nccl(pf_hierarchy* h, const void* id, int nbytes) {
   PF_API_END
 }
 
+pf_status pf_hierarchy_peer_export(pf_hierarchy* h, void* blob, int64_t capacity, int64_t* size) {
+  PF_API_BEGIN
+  if (!h || !size) invalid("null argument");
+  if (!h->finalized) state("export the peer arena after pf_hierarchy_finalize");
+  if (h->world == h->n_sub) state("the peer transport is only used when ranks live in separate hierarchies");
+  PF_CUDA(cudaSetDevice(h->device));
+  *size = pf::peer_export(h, blob, capacity);
+  PF_API_END
+}
+
+pf_status pf_hierarchy_init_peer(pf_hierarchy* h, const void* blobs, int64_t stride) {
+  PF_API_BEGIN
+  if (!h || !blobs) invalid("null argument");
+  if (stride <= 0) invalid("blob stride must be positive");
+  PF_CUDA(cudaSetDevice(h->device));
+  pf::peer_import(h, blobs, stride);
+  drop_graphs(h);
+  PF_API_END
+}
+
 pf_status pf_loopback_create(int world_size, void** hub) {
   PF_API_BEGIN
   if (!hub || world_size < 1) invalid("bad argument");
@@ -2526,6 +2570,13 @@ pf_status pf_launch_count(const pf_hierarchy* h, int64_t* out) {
   PF_API_BEGIN
   if (!h || !out) invalid("null argument");
   *out = h->launches;
+  PF_API_END
+}
+
+pf_status pf_hierarchy_graph_count(const pf_hierarchy* h, int64_t* out) {
+  PF_API_BEGIN
+  if (!h || !out) invalid("null argument");
+  *out = static_cast<int64_t>(h->graphs.size());
   PF_API_END
 }
 

@@ -149,6 +149,7 @@ struct ExchangePlan {
   DevBuf<int32_t> pack_idx, unpack_idx;
   std::vector<PeerSeg> send_segs, recv_segs;
   DevBuf<double> sendbuf, recvbuf;
+  int peer_id = -1;  // index among the hierarchy's remote plans (PeerTransport)
 };
 
 struct Level {

@@ -222,6 +222,23 @@ class Hierarchy:
     def init_loopback(self, hub: "LoopbackHub"):
         _lib.check(_lib.lib().pf_hierarchy_init_loopback(self._h, hub._p))
 
+    def peer_export(self) -> bytes:
+        """This rank's peer-transport blob (pf_hierarchy_peer_export): allocates the
+        peer-visible exchange arena; allgather the blobs and pass them to init_peer."""
+        n = C.c_int64(0)
+        _lib.check(_lib.lib().pf_hierarchy_peer_export(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _lib.check(_lib.lib().pf_hierarchy_peer_export(self._h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def init_peer(self, blobs) -> None:
+        """Activate the peer-memory transport from every rank's blob (rank order): each
+        exchange becomes one kernel storing into the peers' mapped memory (CUDA IPC across
+        processes / NVLink), capturable into the solve graph."""
+        stride = max(len(b) for b in blobs)
+        buf = C.create_string_buffer(b"".join(b.ljust(stride, b"\0") for b in blobs), stride * len(blobs))
+        _lib.check(_lib.lib().pf_hierarchy_init_peer(self._h, buf, stride))
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)
@@ -270,6 +287,12 @@ class Hierarchy:
     def launch_count(self) -> int:
         out = C.c_int64()
         _lib.check(_lib.lib().pf_launch_count(self._h, C.byref(out)))
+        return out.value
+
+    def graph_count(self) -> int:
+        """CUDA graphs cached by the hierarchy (solve / outer-cycle / V-cycle captures)."""
+        out = C.c_int64()
+        _lib.check(_lib.lib().pf_hierarchy_graph_count(self._h, C.byref(out)))
         return out.value
 
     def reset_launch_count(self):
@@ -403,7 +426,11 @@ def replica_levels(dim: int, n_coarse: int, n_levels: int, world: int, problem: 
     """Every rank's bottom levels 0..top for a multi-process hierarchy (coarse_replicas):
     top is the highest level below the finest whose rows over all ranks stay <= max_rows
     (those levels then run redundantly on every GPU after one allgather)."""
-    per_rank = [StructuredSetup(dim, n_coarse, max(1, n_levels - 1), world, q, problem,
+    # only the levels that can qualify: the global vertex count bounds every rank sum
+    nl = 1
+    while nl < n_levels - 1 and (n_coarse * 2 ** nl + 1) ** dim <= max_rows:
+        nl += 1
+    per_rank = [StructuredSetup(dim, n_coarse, max(1, min(n_levels - 1, nl)), world, q, problem,
                                 direct_halos=direct_halos).levels
                 for q in range(world)]
     top = 0
