@@ -243,6 +243,9 @@ pf_status pf_hierarchy_init_loopback(pf_hierarchy* h, void* hub);
  *   2. the caller allgathers the blobs (any host fabric), each padded to a common stride;
  *   3. pf_hierarchy_init_peer(h, blobs, stride) maps every peer's arena and activates.
  * Every rank must pass the same hierarchy shape (levels, fused exchanges, replicas).
+ * Ranks that are hierarchies of ONE process share its device context: finish every
+ * allocation and device-synchronising call on all of them (a host barrier) before the first
+ * exchange, since an exchange kernel waiting for a peer is work such a call would wait for.
  * A wait that exceeds PF_WATCHDOG_S (default 120 s) raises PF_ERR_TRANSPORT at the next
  * synchronisation (the reference fabric's watchdog, transport.cpp:54-60). */
 pf_status pf_hierarchy_peer_export(pf_hierarchy* h, void* blob, int64_t capacity, int64_t* size);

@@ -21,6 +21,16 @@ bool pdl_on();
 
 namespace {
 
+// Stream-ordered upload: ranks that share a device (hierarchies of one process) may already
+// be spinning in exchange kernels, which a legacy-stream copy or a device-wide
+// synchronisation would wait for.
+template <typename T>
+void upload_on(DevBuf<T>& d, const std::vector<T>& v, cudaStream_t s) {
+  d.alloc(static_cast<int64_t>(v.size()));
+  if (!v.empty()) cuda_check(cudaMemcpyAsync(d.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s), "peer upload");
+  cuda_check(cudaStreamSynchronize(s), "peer upload");
+}
+
 constexpr uint64_t kMagic = 0x31524545504650ull;  // "PFPEER1"
 constexpr int64_t kAlign = 256;
 
@@ -174,8 +184,10 @@ void PeerTransport::recv(double*, int64_t, int, cudaStream_t) {
 void PeerTransport::check_async() {
   if (!ready) return;
   PeerCtl c;
-  cuda_check(cudaMemcpy(&c.error, &ctl()->error, sizeof(unsigned int) + sizeof(int), cudaMemcpyDeviceToHost),
+  cuda_check(cudaMemcpyAsync(&c.error, &ctl()->error, sizeof(unsigned int) + sizeof(int), cudaMemcpyDeviceToHost,
+                             h->stream),
              "peer error word");
+  cuda_check(cudaStreamSynchronize(h->stream), "peer error word");
   if (c.error)
     throw Error(PF_ERR_TRANSPORT, "peer watchdog: rank " + std::to_string(c.error_peer) +
                                       " did not deliver (or acknowledge) an exchange within " +
@@ -219,7 +231,8 @@ int64_t peer_export(pf_hierarchy* h, void* buf, int64_t cap) {
     }
     nt->arena_bytes = off;
     nt->arena.alloc(off);
-    cuda_check(cudaMemset(nt->arena.p, 0, static_cast<size_t>(off)), "peer arena");
+    cuda_check(cudaMemsetAsync(nt->arena.p, 0, static_cast<size_t>(off), h->stream), "peer arena");
+    cuda_check(cudaStreamSynchronize(h->stream), "peer arena");
     t = nt.get();
     h->xport = std::move(nt);
   }
@@ -332,7 +345,7 @@ void peer_import(pf_hierarchy* h, const void* blobs, int64_t stride) {
   }
   std::vector<PeerCtl*> rc(static_cast<size_t>(W));
   for (int r = 0; r < W; ++r) rc[static_cast<size_t>(r)] = reinterpret_cast<PeerCtl*>(base[static_cast<size_t>(r)]);
-  t->remote_ctl.upload(rc);
+  upload_on(t->remote_ctl, rc, h->stream);
   // plans: my sends pair with the peer's receives from me (k-th with k-th, NCCL order)
   for (size_t i = 0; i < ps.size(); ++i) {
     const ExchangePlan& X = *ps[i];
@@ -382,9 +395,9 @@ void peer_import(pf_hierarchy* h, const void* blobs, int64_t stride) {
     }
     o.n_sends = static_cast<int32_t>(sg.size());
     o.n_recvs = static_cast<int32_t>(rg.size());
-    o.sends.upload(sg);
-    o.recvs.upload(rg);
-    o.segs.upload(pieces);
+    upload_on(o.sends, sg, h->stream);
+    upload_on(o.recvs, rg, h->stream);
+    upload_on(o.segs, pieces, h->stream);
   }
   // allgather sites
   for (size_t j = 0; j < t->sites.size(); ++j) {
@@ -407,11 +420,10 @@ void peer_import(pf_hierarchy* h, const void* blobs, int64_t stride) {
     }
     o.n_sends = static_cast<int32_t>(sg.size());
     o.n_recvs = static_cast<int32_t>(rg.size());
-    o.sends.upload(sg);
-    o.recvs.upload(rg);
-    o.segs.upload(pieces);
+    upload_on(o.sends, sg, h->stream);
+    upload_on(o.recvs, rg, h->stream);
+    upload_on(o.segs, pieces, h->stream);
   }
-  cuda_check(cudaDeviceSynchronize(), "peer import");
   t->ready = true;
 }
 

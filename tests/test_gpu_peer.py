@@ -75,13 +75,16 @@ def test_peer_threads_captured(cuda, K, L, rep, fused, kind):
         h.init_peer(blobs)
         x = h.vector(L - 1)
         b = h.vector(L - 1, setups[r].b)
+        v = h.vector(L - 2, key_noise([levels[r][L - 2]], 3)[0])
+        # ranks sharing a device: every allocation (a device-synchronising call) is done
+        # before any rank parks a kernel waiting for a peer
+        bar.wait()
         sols = []
         for _ in range(2):
             x.upload(setups[r].x0)
             st = gmg.solve_outer(h, x, b, c)
             sols.append(x.download())
         rn = gmg.residual_norm(h, L - 1, x, b)
-        v = h.vector(L - 2, key_noise([levels[r][L - 2]], 3)[0])
         gmg.update_master_slave(h, L - 2, v, gmg.PF_UPDATE_ACCUMULATE_THEN_SCATTER)
         bar.wait()  # no rank tears its arena down while a peer may still store into it
         return st, sols, rn, v.download(), h.graph_count()
@@ -153,11 +156,12 @@ def test_peer_watchdog_raises_transport_error(cuda, monkeypatch):
         blobs[r] = h.peer_export()
         bar.wait()
         h.init_peer(blobs)
+        x = h.vector(L - 1, setups[r].x0)
+        b = h.vector(L - 1, setups[r].b)
+        bar.wait()
         if r == 1:
             bar.wait()  # rank 1 never solves
             return None
-        x = h.vector(L - 1, setups[r].x0)
-        b = h.vector(L - 1, setups[r].b)
         try:
             with pytest.raises(_lib.TransportError, match="watchdog"):
                 gmg.solve_outer(h, x, b, cfg())
