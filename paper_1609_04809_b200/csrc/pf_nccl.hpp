@@ -42,6 +42,8 @@ struct Transport {
   // unpack.  run_plan: receivers scatter into v, or with wait_only only wait for their
   // messages; the caller then consumes staging(P) (the master accumulate) and ack_plan()s.
   virtual bool direct() const { return false; }
+  // may an exchange run on the side stream, overlapped with the interior sweep
+  virtual bool overlap_ok() const { return true; }
   virtual void run_plan(const ExchangePlan&, double*, bool, cudaStream_t) {}
   virtual const double* staging(const ExchangePlan&) const { return nullptr; }
   virtual void ack_plan(const ExchangePlan&, cudaStream_t) {}

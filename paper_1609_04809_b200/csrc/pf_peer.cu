@@ -324,6 +324,20 @@ void peer_import(pf_hierarchy* h, const void* blobs, int64_t stride) {
   // map every peer's arena
   std::vector<char*> base(static_cast<size_t>(W), nullptr);
   const int64_t pid = static_cast<int64_t>(getpid());
+  int same_process = 0;
+  for (int r = 0; r < W; ++r) same_process += P[static_cast<size_t>(r)].head.pid == pid;
+  t->in_process = same_process > 1;
+  if (same_process > 1) {
+    // Ranks of one process share its context: a kernel waiting for a peer's kernel must
+    // not sit ahead of that kernel in a hardware work queue (streams beyond
+    // CUDA_DEVICE_MAX_CONNECTIONS share queues) or race a lazy module load of it.
+    const char* ml = std::getenv("CUDA_MODULE_LOADING");
+    const char* mc = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    if (!ml || std::string(ml) != "EAGER" || !mc || std::atoi(mc) < 2 * same_process)
+      throw Error(PF_ERR_STATE, "in-process peer ranks need CUDA_MODULE_LOADING=EAGER and CUDA_DEVICE_MAX_CONNECTIONS >= " +
+                                    std::to_string(2 * same_process) +
+                                    " set before CUDA initialises (or one process per rank)");
+  }
   for (int r = 0; r < W; ++r) {
     const BlobHead& hd = P[static_cast<size_t>(r)].head;
     if (r == me) {

@@ -26,6 +26,7 @@ struct PeerTransport final : Transport {
   pf_hierarchy* h = nullptr;
   int rank = 0, world = 1;
   bool ready = false;
+  bool in_process = false;           // some peers are hierarchies of this process
   DevBuf<char> arena;                // PeerCtl, then every plan's and site's staging
   int64_t arena_bytes = 0;
   std::vector<void*> opened;         // IPC-mapped peer arenas (closed at destruction)
@@ -54,6 +55,9 @@ struct PeerTransport final : Transport {
   void allgather(const double* send, double* recv, int64_t count, cudaStream_t s) override;
   void check_async() override;
   bool direct() const override { return true; }
+  // in-process peers: no side-stream overlap (a forked graph's branches may share a
+  // hardware queue with another rank's waiting exchange)
+  bool overlap_ok() const override { return !in_process; }
   void run_plan(const ExchangePlan& P, double* v, bool wait_only, cudaStream_t s) override;
   const double* staging(const ExchangePlan& P) const override;
   void ack_plan(const ExchangePlan& P, cudaStream_t s) override;

@@ -57,9 +57,15 @@ inline unsigned grid_for(int64_t n) { return static_cast<unsigned>((n + kBlock -
 [[noreturn]] void invalid(const std::string& m) { throw Error(PF_ERR_INVALID_ARGUMENT, m); }
 
 // PF_TRACE=1: one stderr line per major host step (debugging integrations).
-void trace(const char* what) {
+void trace(const char* what, int rank = -1) {
   static const bool on = std::getenv("PF_TRACE") != nullptr;
-  if (on) std::fprintf(stderr, "[pf] %s\n", what);
+  if (!on) return;
+  if (rank < 0) {
+    std::fprintf(stderr, "[pf] %s\n", what);
+  } else {
+    const double t = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    std::fprintf(stderr, "[pf %.6f r%d] %s\n", t, rank, what);
+  }
 }
 [[noreturn]] void state(const std::string& m) { throw Error(PF_ERR_STATE, m); }
 
@@ -1247,7 +1253,8 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
   bool exchanged = false;
   for (int sweep = 0; sweep < sc.sweeps; ++sweep) {
     for (int local = 0; local < sc.local_sweeps; ++local) {
-      const bool overlap = h->fused && h->world > h->n_sub && sc.kind == PF_SMOOTHER_JACOBI &&
+      const bool overlap = h->fused && h->world > h->n_sub && h->xport && h->xport->overlap_ok() &&
+                           sc.kind == PF_SMOOTHER_JACOBI &&
                            local + 1 == sc.local_sweeps && !(first_done && sweep == 0 && local == 0);
       if (overlap) {
         // boundary rows (+ the non-own carry-over) first, then the exchange on the side
@@ -1748,6 +1755,7 @@ pf_hierarchy::GraphEntry& outer_graph(pf_hierarchy* h, pf_vector* x, const pf_ve
   if (it != h->graphs.end()) return it->second;
   pf_hierarchy::GraphEntry e;
   cudaGraph_t g = nullptr;
+  trace("outer graph: capture", h->rank_base);
   PF_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   g_capture_counter = &e.kernels;
   try {
@@ -1766,7 +1774,9 @@ pf_hierarchy::GraphEntry& outer_graph(pf_hierarchy* h, pf_vector* x, const pf_ve
   }
   g_capture_counter = nullptr;
   PF_CUDA(cudaStreamEndCapture(h->stream, &g));
+  trace("outer graph: captured", h->rank_base);
   PF_CUDA(cudaGraphInstantiate(&e.exec, g, 0));
+  trace("outer graph: instantiated", h->rank_base);
   PF_CUDA(cudaGraphDestroy(g));
   return h->graphs.emplace(key, e).first->second;
 }
@@ -1807,8 +1817,10 @@ void solve_outer_dev(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf
     }
     return;
   }
+  trace("solve: initial norm", h->rank_base);
   enq_resnorm(h, top, x->cur(), b->cur());
   const double r0 = read_norm(h, top);
+  trace("solve: initial norm read", h->rank_base);
   s.initial_residual = r0;
   s.final_residual = r0;
   s.converged = 1;
@@ -1818,6 +1830,7 @@ void solve_outer_dev(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf
     pf_hierarchy::GraphEntry* g = eager ? nullptr : &outer_graph(h, x, b, cfg, true);
     for (int outer = 1; outer <= cfg.outer_max_cycles; ++outer) {
       if (g) {
+        trace("solve: cycle graph launch", h->rank_base);
         graph_launch(h, *g);
       } else {
         for (int j = 0; j < cfg.cycles; ++j) enq_vcycle(h, x, b->cur(), cfg);
@@ -1826,6 +1839,7 @@ void solve_outer_dev(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf
                                 cudaMemcpyDeviceToHost, h->stream));
       }
       sync(h);
+      trace("solve: cycle done", h->rank_base);
       const double r = h->pinned[0];
       s.iterations = outer;
       if (residuals && outer <= max_res) residuals[outer - 1] = r;
