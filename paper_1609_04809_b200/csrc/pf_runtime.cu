@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <parallel/algorithm>
 #include <unordered_set>
 #include <omp.h>
@@ -1588,7 +1589,8 @@ void enq_norm_head(pf_hierarchy* h, pf_vector* x, const double* b, const pf_mult
 }
 
 void sync(pf_hierarchy* h);
-std::string graph_key(const char* tag, const void* x, const void* b, const pf_multigrid_config& c);
+std::string graph_key(const char* tag, const pf_vector* x, const pf_vector* b, const pf_multigrid_config& c);
+void prune_graphs(pf_hierarchy* h);
 
 cudaGraphNode_t single_leaf(cudaGraph_t g) {
   size_t n = 0;
@@ -1612,12 +1614,14 @@ cudaGraphNode_t single_leaf(cudaGraph_t g) {
 // memory.  No host round trip between cycles.
 pf_hierarchy::GraphEntry& solve_graph(pf_hierarchy* h, pf_vector* x, const pf_vector* b,
                                       const pf_multigrid_config& cfg) {
-  const std::string key = graph_key("solve", x, b, cfg) + ":" + std::to_string(cfg.outer_max_cycles) +
-                          ":" + std::to_string(cfg.outer_tol);
+  const std::string key = graph_key("solve", x, b, cfg);
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) return it->second;
   trace("solve graph: build");
+  prune_graphs(h);
   pf_hierarchy::GraphEntry e;
+  e.x_uid = x->uid;
+  e.b_uid = b->uid;
   const int top = h->n_levels - 1;
   const size_t state_bytes = sizeof(SolveState) + sizeof(double) * static_cast<size_t>(cfg.outer_max_cycles);
   PF_CUDA(cudaMalloc(&e.state, state_bytes));
@@ -1738,12 +1742,41 @@ void validate_cfg(const pf_multigrid_config& c) {
   if (c.outer_max_cycles < 1) invalid("outer_max_cycles must be >= 1");
 }
 
-std::string graph_key(const char* tag, const void* x, const void* b, const pf_multigrid_config& c) {
+// Cache key of a captured graph: the vectors by id and every config field exactly (doubles
+// by their bit patterns: 1e-6 and 1e-10, or 2/3 and 0.666667, are different graphs).
+std::string graph_key(const char* tag, const pf_vector* x, const pf_vector* b, const pf_multigrid_config& c) {
+  auto bits = [](double d) {
+    uint64_t u;
+    std::memcpy(&u, &d, sizeof u);
+    return u;
+  };
   std::ostringstream os;
-  os << tag << ':' << x << ':' << b << ':' << c.cycles << ':' << c.smoother.kind << ':'
-     << c.smoother.local_sweeps << ':' << c.smoother.damping << ':' << c.pre_smooth << ':'
-     << c.post_smooth << ':' << c.coarse_tol << ':' << c.coarse_max_iter;
+  os << tag << ':' << x->uid << ':' << b->uid << ':' << c.cycles << ':' << c.smoother.kind << ':'
+     << c.smoother.local_sweeps << ':' << std::hex << bits(c.smoother.damping) << std::dec << ':' << c.pre_smooth
+     << ':' << c.post_smooth << ':' << std::hex << bits(c.coarse_tol) << std::dec << ':' << c.coarse_max_iter << ':'
+     << c.outer_max_cycles << ':' << std::hex << bits(c.outer_tol);
   return os.str();
+}
+
+// Drop the cached graphs that use a destroyed vector (their captured device pointers are
+// dangling); called before a new graph is captured.
+void prune_graphs(pf_hierarchy* h) {
+  bool synced = false;
+  for (auto it = h->graphs.begin(); it != h->graphs.end();) {
+    const auto& e = it->second;
+    if (h->vectors->alive(e.x_uid) && h->vectors->alive(e.b_uid)) {
+      ++it;
+      continue;
+    }
+    if (!synced) {
+      PF_CUDA(cudaStreamSynchronize(h->stream));
+      synced = true;
+    }
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (e.state) cudaFree(e.state);
+    if (e.host_state) cudaFreeHost(e.host_state);
+    it = h->graphs.erase(it);
+  }
 }
 
 // One outer iteration of solve_outer as a graph: cfg.cycles V-cycles, the finest
@@ -1753,7 +1786,10 @@ pf_hierarchy::GraphEntry& outer_graph(pf_hierarchy* h, pf_vector* x, const pf_ve
   const std::string key = graph_key(with_norm ? "outer" : "vcycle", x, b, cfg);
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) return it->second;
+  prune_graphs(h);
   pf_hierarchy::GraphEntry e;
+  e.x_uid = x->uid;
+  e.b_uid = b->uid;
   cudaGraph_t g = nullptr;
   trace("outer graph: capture", h->rank_base);
   PF_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
@@ -1878,7 +1914,14 @@ void download_vec(pf_hierarchy* h, const pf_vector* v, int s, double* host, int6
 }
 
 pf_vector* new_vector(pf_hierarchy* h, int level) {
+  static std::atomic<uint64_t> next_uid{1};
   auto* v = new pf_vector;
+  v->uid = next_uid++;
+  v->registry = h->vectors;
+  {
+    std::lock_guard<std::mutex> g(h->vectors->mu);
+    h->vectors->live.insert(v->uid);
+  }
   v->h = h;
   v->device = h->device;
   v->level = level;
@@ -2322,7 +2365,13 @@ pf_status pf_vector_create(pf_hierarchy* h, int level, pf_vector** out) {
 
 pf_status pf_vector_destroy(pf_vector* v) {
   PF_API_BEGIN
-  if (v) cudaSetDevice(v->device);
+  if (v) {
+    cudaSetDevice(v->device);
+    if (auto reg = v->registry.lock()) {  // the hierarchy is alive: its graphs on v go stale
+      std::lock_guard<std::mutex> g(reg->mu);
+      reg->live.erase(v->uid);
+    }
+  }
   delete v;
   PF_API_END
 }

@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <unordered_set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -181,10 +183,25 @@ namespace pf {
 void adopt_setup_level(pf_setup* s, int level, HostLevel& H);  // pf_setup.cpp
 }  // namespace pf
 
+namespace pf {
+// Ids of a hierarchy's live vectors: cached graphs are keyed by vector id (never by
+// address, which the allocator reuses) and are dropped once a vector they use is gone.
+struct VecRegistry {
+  std::mutex mu;
+  std::unordered_set<uint64_t> live;
+  bool alive(uint64_t id) {
+    std::lock_guard<std::mutex> g(mu);
+    return live.count(id) != 0;
+  }
+};
+}  // namespace pf
+
 struct pf_vector {
   pf_hierarchy* h = nullptr;
   int device = 0;  // kept here so destruction never reads the hierarchy
   int level = 0;
+  uint64_t uid = 0;                        // unique for the process lifetime
+  std::weak_ptr<pf::VecRegistry> registry;  // the hierarchy's (expired once it is destroyed)
   pf::DevBuf<double> data;  // [2 * total]: primary then Jacobi ping-pong partner
   double* cur() const { return data.p; }
   double* alt() const { return data.p + total; }
@@ -214,7 +231,9 @@ struct pf_hierarchy {
     void* state = nullptr;      // solve graph: device SolveState
     void* host_state = nullptr; // pinned copy written at the end of the graph
     size_t state_bytes = 0;
+    uint64_t x_uid = 0, b_uid = 0;  // the vectors the graph reads and writes
   };
+  std::shared_ptr<pf::VecRegistry> vectors = std::make_shared<pf::VecRegistry>();
   std::map<std::string, GraphEntry> graphs;
   // Levels 0..top of the V-cycle run in one cooperative kernel (pf_bottom.cuh).
   struct Bottom {

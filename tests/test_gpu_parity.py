@@ -439,3 +439,42 @@ def test_hierarchy_from_native_setups(cuda):
     assert exact(download(hn, xn, K), download(h, x, K))
     with pytest.raises(_lib.PfError):
         native[0].level_desc(0)  # released
+
+
+@pytest.mark.parametrize("mode", ["graph", "host"])
+def test_graph_cache_keys_every_config_bit(cuda, monkeypatch, mode):
+    """The cached solve graph is keyed by the exact bits of every config double: a second
+    solve on the same vectors with a tighter outer_tol (or a damping that prints the same
+    to 6 digits) must not replay the first graph."""
+    monkeypatch.setenv("PF_SOLVE_MODE", mode)
+    setups, levels = structured(3, 2, 4, 1)
+    h = gmg.Hierarchy(levels)
+    x = h.vector(3)
+    b = upload(h, 3, [setups[0].b])
+    o = Oracle(levels)
+    for tol, damping in ((1e-6, 0.8), (1e-10, 0.8), (1e-10, 2.0 / 3.0), (1e-10, 0.666667)):
+        c = cfg(damping=damping, tol=tol)
+        x.upload(setups[0].x0)
+        st = gmg.solve_outer(h, x, b, c)
+        xo, res, ost, rc = o.solve_outer([setups[0].x0], [setups[0].b], c)
+        assert st.iterations == ost.iterations, (tol, damping)
+        assert exact([x.download()], xo), (tol, damping)
+
+
+def test_destroyed_vector_graphs_are_dropped(cuda):
+    """Graphs are keyed by vector id, not address: destroying the solve's vectors and
+    creating new ones (the allocator may hand back the same addresses) captures a fresh
+    graph on the new device buffers, and the stale graphs are released."""
+    setups, levels = structured(3, 2, 4, 1)
+    h = gmg.Hierarchy(levels)
+    o = Oracle(levels)
+    xo, res, ost, rc = o.solve_outer([setups[0].x0], [setups[0].b], cfg())
+    for i in range(4):
+        x = h.vector(3, setups[0].x0)
+        b = h.vector(3, setups[0].b)
+        st = gmg.solve_outer(h, x, b, cfg())
+        assert st.iterations == ost.iterations
+        assert exact([x.download()], xo), i
+        x.close()
+        b.close()
+        assert h.graph_count() <= 1
