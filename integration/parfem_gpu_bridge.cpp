@@ -167,17 +167,70 @@ struct Mirror {
   std::unique_ptr<parfem_b200::DeviceVector> x, b;
   void* hub = nullptr;
   bool owns_hub = false;
+  std::uint64_t fp = 0;  // fingerprint of the hierarchy the mirror was built from
 };
 
 std::mutex g_mu;
 std::map<const MultigridHierarchy*, std::unique_ptr<Mirror>> g_mirrors;
 
+// Sampled FNV-1a fingerprint of a hierarchy's level data (sizes, row offsets, columns,
+// values, prolongation rows): a hierarchy rebuilt at the same address with other data
+// must not reuse the old device mirror.
+std::uint64_t fingerprint(const MultigridHierarchy& h) {
+  std::uint64_t f = 1469598103934665603ull;
+  auto mix = [&f](const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) f = (f ^ c[i]) * 1099511628211ull;
+  };
+  auto sample = [&mix](const auto& v) {
+    const size_t n = v.size();
+    mix(&n, sizeof n);
+    const size_t step = n > 1024 ? n / 1024 : 1;
+    for (size_t i = 0; i < n; i += step) mix(&v[i], sizeof v[i]);
+    if (n) mix(&v[n - 1], sizeof v[n - 1]);
+  };
+  const int K = h.tp->size();
+  mix(&K, sizeof K);
+  for (const MultigridLevel& L : h.levels) {
+    mix(&L.mapper->n_dofs, sizeof L.mapper->n_dofs);
+    mix(&L.mapper->n_own_dofs, sizeof L.mapper->n_own_dofs);
+    sample(L.system.row_offsets);
+    sample(L.system.col_indices);
+    sample(L.system.values);
+    const size_t np = L.prolong_map.size();
+    mix(&np, sizeof np);
+    const size_t step = np > 256 ? np / 256 : 1;
+    for (size_t i = 0; i < np; i += step)
+      for (const auto& [cd, w] : L.prolong_map[i]) {
+        mix(&cd, sizeof cd);
+        mix(&w, sizeof w);
+      }
+  }
+  return f;
+}
+
 Mirror& mirror(MultigridHierarchy& h) {
+  const std::uint64_t fp = fingerprint(h);
+  bool found = false, stale = false;
   {
     std::lock_guard<std::mutex> lock(g_mu);
     auto it = g_mirrors.find(&h);
-    if (it != g_mirrors.end()) return *it->second;
+    if (it != g_mirrors.end()) {
+      found = true;
+      stale = it->second->fp != fp;
+    }
   }
+  if (found && h.tp->size() > 1) {  // rebuilding is collective: any stale rank decides for all
+    ByteWriter w;
+    w.put_i64(stale ? 1 : 0);
+    for (Bytes& b : allgather(*h.tp, w.take()))
+      if (ByteReader(std::move(b)).get_i64()) stale = true;
+  }
+  if (found && !stale) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    return *g_mirrors.find(&h)->second;
+  }
+  if (found) release(h);
   Transport& tp = *h.tp;
   const int K = tp.size(), rank = tp.rank(), L = static_cast<int>(h.levels.size());
   int n_dev = 0;
@@ -213,6 +266,7 @@ Mirror& mirror(MultigridHierarchy& h) {
   }
   m->x = std::make_unique<parfem_b200::DeviceVector>(*m->dev, L - 1);
   m->b = std::make_unique<parfem_b200::DeviceVector>(*m->dev, L - 1);
+  m->fp = fp;
   std::lock_guard<std::mutex> lock(g_mu);
   return *(g_mirrors[&h] = std::move(m));
 }
