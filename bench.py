@@ -152,6 +152,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if args.config == "c5":
+        print(json.dumps({"impl": "reference", "unavailable": "C5 (512^3, lognormal coefficient): the reference "
+                          "assembles constant-coefficient Q1 only and its setup needs ~4 GB and 57 s per 2M "
+                          "DOFs (SURVEY.md 8d); C2 is the configuration both arms run (bench.py --config c2)"}))
+        return
     from oracle import ref
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparfem_ref.so not built"}))
@@ -432,6 +437,195 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+# --config c5: BASELINE configs[4], the north star's scaling configuration — Q1 on 512^3
+# cells (135,005,697 DOFs, 9 levels), lognormal(0,1) per-cell coefficient from a seed,
+# V(2,2) multicolour SOR, box-partitioned into N subdomains (partition.cpp:104-142), one
+# per GPU, exchanges through the peer-memory transport (CUDA IPC over NVLink: each exchange
+# one kernel storing into the peer GPUs' memory, recorded into the solve's CUDA graph) or
+# NCCL (--transport nccl).  The total problem is fixed, so N = 1, 2, 4, 8 is strong scaling.
+C5 = dict(dim=3, n_coarse=2, levels=9, pre=2, post=2, omega=1.2, tol=1e-10, seed=2024)
+C5_METRIC = "GMG solve DOFs/s (solve_outer to 1e-10 rel. residual, V(2,2) multicolour SOR w=1.2, lognormal coefficient)"
+C5_CONFIG = {
+    "workload": "C5: 3D Q1 -div(kappa grad u) = f, unit cube, 512^3 hex cells (135,005,697 DOFs), fp64, "
+                "kappa lognormal(0,1) per finest cell (seed 2024), 9 levels from 2^3, V(2,2) multicolour SOR "
+                "w=1.2, replicated coarse levels, stop at 1e-10",
+    "n_dofs": 135005697, "levels": 9, "cells": "512^3", "smoother": "multicolor_sor_1.2",
+    "l2_flush": "no flush: the finest operator (43.6 GB on one GPU, 5.4 GB per GPU at N=8) exceeds the 126 MB L2",
+}
+
+
+def c5_solve(h, setup, world, rank, args, clk, dist, local, label):
+    """Time solve_outer of an uploaded C5 hierarchy (device-resident and through host
+    buffers); returns the measurement dict (rank-local figures, max-over-ranks times)."""
+    import torch
+
+    from paper_1609_04809_b200 import gmg
+    W = C5
+    top = h.finest
+    cfg = gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=gmg.PF_SMOOTHER_MULTICOLOR_SOR, damping=W["omega"]),
+                              pre_smooth=W["pre"], post_smooth=W["post"], outer_tol=W["tol"], outer_max_cycles=400)
+    x0 = h.vector(top, setup.x0)
+    b = h.vector(top, setup.b)
+    x = h.vector(top)
+    stream = torch.cuda.ExternalStream(h.stream_handle(), device=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    st = None
+    for _ in range(args.warmup):
+        x.copy_from(x0)
+        st = gmg.solve_outer(h, x, b, cfg)
+    barrier()
+    n0 = h.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
+    e0.record(stream)
+    for _ in range(args.steps):
+        x.copy_from(x0)
+        st = gmg.solve_outer(h, x, b, cfg)
+    e1.record(stream)
+    barrier()
+    clk.window(w0, time.time())
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = h.launch_count() - n0
+    # e2e: pinned host x0 / b in, solution out, through the host-buffer entry point
+    xh = torch.empty(len(setup.x0), dtype=torch.float64).pin_memory().numpy()
+    bh = torch.from_numpy(setup.b.copy()).pin_memory().numpy()
+    e2e_ms = 0.0
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        xh[:] = setup.x0
+        barrier()
+        e0.record(stream)
+        gmg.solve_outer_host(h, [xh], [bh], cfg)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+    barrier()
+    e2e_ms = max_over_ranks(e2e_ms)
+    vc_ms = max_over_ranks(h.time_vcycle(x, b, cfg, 3))
+    sor_ms, sor_bytes = h.time_sweep(top, gmg.PF_SMOOTHER_MULTICOLOR_SOR, 5)
+    jac_ms, jac_bytes = h.time_sweep(top, gmg.PF_SMOOTHER_JACOBI, 5)
+    n = setup.n_global
+    return {"value": n * args.steps / (ms / 1e3), "ms_per_step": ms / args.steps, "cycles": st.iterations,
+            "converged": bool(st.converged), "final_rel_residual": st.final_residual / st.initial_residual,
+            "vcycle_ms": vc_ms, "launches": launches,
+            "e2e": {"value": n * e2e_steps / (e2e_ms / 1e3), "unit": "DOF/s",
+                    "h2d_bytes_per_step": 16 * len(setup.x0), "d2h_bytes_per_step": 8 * len(setup.x0),
+                    "ms_per_step": e2e_ms / e2e_steps},
+            "sor_sweep_ms": sor_ms, "sor_sweep_bytes": sor_bytes, "jacobi_sweep_ms": jac_ms,
+            "jacobi_sweep_bytes": jac_bytes, "x0": x0, "b": b, "x": x}
+
+
+def c5_hierarchy(world, rank, local, transport, dist):
+    """Rank `rank`'s box of the C5 problem on its GPU (replicated bottom levels gathered from
+    their owners, no other rank's setup built), with its transport attached."""
+    from paper_1609_04809_b200 import dist as pdist
+    from paper_1609_04809_b200 import gmg
+    from paper_1609_04809_b200.levels import StructuredSetup
+    W = C5
+    t0 = time.time()
+    setup = StructuredSetup(W["dim"], W["n_coarse"], W["levels"], world, rank, gmg._lib.PF_PROBLEM_LOGNORMAL,
+                            seed=W["seed"], direct_halos=world > 1, materialize=False)
+    setup_s = time.time() - t0
+    replicas = None
+    if world > 1:
+        def gather(obj):
+            out = [None] * world
+            dist.all_gather_object(out, obj)
+            return out
+        replicas = gmg.gather_replica_levels(setup, gather)
+    t0 = time.time()
+    h = gmg.Hierarchy.from_setups([setup], device=local, rank_base=rank, world_size=world,
+                                  coarse_replicas=replicas, fused_exchanges=world > 1)
+    upload_s = time.time() - t0
+    if world > 1:
+        if transport == "peer":
+            pdist.init_peer_transport(h, pdist.allgather_blobs_torch)
+        else:
+            uid = [gmg.Hierarchy.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, 0)
+            h.init_nccl(uid[0])
+    return h, setup, setup_s, upload_s
+
+
+def run_c5(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional checks of the multi-process path on a one-GPU box: PF_BENCH_DEVICE=0 puts
+    # every rank on device 0 (CUDA IPC between processes); PF_BENCH_C5_LEVELS shrinks the grid
+    if os.environ.get("PF_BENCH_DEVICE") is not None:
+        local = int(os.environ["PF_BENCH_DEVICE"])
+    if os.environ.get("PF_BENCH_C5_LEVELS"):
+        C5["levels"] = int(os.environ["PF_BENCH_C5_LEVELS"])
+        C5_CONFIG["workload"] += f" [REDUCED: {C5['levels']} levels]"
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    clk = Clocks(local).start()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")  # host plumbing only: the data plane is libpf_gpu.so's
+    h, setup, setup_s, upload_s = c5_hierarchy(world, rank, local, args.transport, dist)
+    m = c5_solve(h, setup, world, rank, args, clk, dist, local, "c5")
+    clk.stop()
+    peak, peak_src = peaks()
+    # per-GPU finest-level sweeps on the bytes they move (fp64 SELL-32x4: 12 B per stored
+    # entry + row lengths + x gather + b): the multicolour SOR sweep is the dominant kernel
+    sor_gbs = m["sor_sweep_bytes"] / m["sor_sweep_ms"] / 1e6
+    jac_gbs = m["jacobi_sweep_bytes"] / m["jacobi_sweep_ms"] / 1e6
+    fracs = [sor_gbs / peak, jac_gbs / peak]
+    if dist:
+        t = torch.tensor(fracs, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        fracs = t.tolist()
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": C5_METRIC, "value": m["value"], "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic manufactured problem (f = 3 pi^2 sin sin sin, g = 0, seeded lognormal kappa), "
+                    "product setup",
+            "config": dict(C5_CONFIG, parallelism=(f"{world} box subdomains (coordinate bisection), one per GPU, "
+                                                   f"{args.transport} exchanges" if world > 1 else "1 GPU"),
+                           transport=args.transport if world > 1 else None),
+            "cycles": m["cycles"], "converged": m["converged"], "final_rel_residual": m["final_rel_residual"],
+            "vcycle_ms": m["vcycle_ms"],
+            "roofline": {"bound": "hbm", "achieved": sor_gbs, "peak": peak, "unit": "GB/s", "frac": sor_gbs / peak,
+                         "traffic": None, "kernel": "k_color_sweep (finest multicolour SOR sweep, 8 colours, "
+                         "fp64 SELL-32x4), rank 0",
+                         "kernel_us": m["sor_sweep_ms"] * 1e3, "stored_bytes_per_launch": m["sor_sweep_bytes"],
+                         "min_frac_over_ranks": fracs[0], "peak_source": peak_src},
+            "finest_jacobi_sweep": {"us": m["jacobi_sweep_ms"] * 1e3, "gbs": jac_gbs, "frac": jac_gbs / peak,
+                                    "min_frac_over_ranks": fracs[1]},
+            "cpu_baseline": None,
+            "cpu_baseline_note": "the reference CPU solver cannot hold 512^3 (57 s and 4.2 GB at 128^3; "
+                                 "SURVEY.md 8d): not run",
+            "e2e": m["e2e"], "gpu_launches": m["launches"], "clocks": clocks,
+            "setup_seconds": setup_s, "upload_seconds": upload_s,
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # --workload heat: the reference's model problem (app.cpp:146-230), Crank-Nicolson on the
 # C2 grid; one step = one time step (device load assembly, CN right-hand side, solve_outer).
 HEAT = dict(dim=3, n_coarse=2, levels=7, dt=0.01, pre=2, post=2, omega=0.8, tol=1e-10)
@@ -596,13 +790,22 @@ def main():
     ap.add_argument("--no-fe", action="store_true", help="skip the Q2 / rotated-Q1 variants")
     ap.add_argument("--workload", choices=["poisson", "heat"], default="poisson",
                     help="poisson: BASELINE configs[1] (default); heat: the reference's CN run at C2")
+    ap.add_argument("--config", choices=["c2", "c5"], default=None,
+                    help="c2: BASELINE configs[1] (default on 1 GPU); c5: configs[4], 512^3 lognormal SOR "
+                         "(default on N > 1 GPUs: the scaling configuration)")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="multi-GPU exchanges: peer-memory stores (CUDA IPC/NVLink, default) or NCCL")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.config is None:
+        args.config = "c2" if args.gpus == 1 else "c5"
     if args.workload == "heat":
         (run_reference_heat if args.impl == "reference" else run_b200_heat)(args)
     elif args.impl == "reference":
         run_reference(args)
+    elif args.config == "c5":
+        run_c5(args)
     else:
         run_b200(args)
 

@@ -440,6 +440,23 @@ def replica_levels(dim: int, n_coarse: int, n_levels: int, world: int, problem: 
     return [p[:top + 1] for p in per_rank]
 
 
+def gather_replica_levels(setup, allgather, max_rows: int = 65536):
+    """coarse_replicas for a multi-process hierarchy without building any other rank's
+    setup: every rank contributes its own levels 0..top (taken from its setup before the
+    upload moves them) through `allgather(obj) -> list` (e.g. torch.distributed
+    all_gather_object).  top as in replica_levels."""
+    nl = 1
+    while nl < setup.n_levels - 1 and (setup.n_coarse * 2 ** nl + 1) ** setup.dim <= max_rows:
+        nl += 1
+    mine = [setup._level(l) for l in range(min(setup.n_levels - 1, nl))]
+    per_rank = allgather(mine)
+    top = 0
+    for l in range(len(per_rank[0])):
+        if sum(p[l].n for p in per_rank) <= max_rows:
+            top = l
+    return [p[:top + 1] for p in per_rank]
+
+
 def structured_hierarchy(dim: int, n_coarse: int, n_levels: int, n_ranks: int = 1,
                          problem: int = _lib.PF_PROBLEM_BASELINE, device: int = 0,
                          ranks: list | None = None, world_size: int | None = None):
