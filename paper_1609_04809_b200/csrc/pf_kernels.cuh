@@ -271,11 +271,11 @@ template <int kVK>
 __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_JAC_MINB)) k_jacobi(SellView A, const double* __restrict__ x_old,
                                                    double* __restrict__ x_new,
                                                    const double* __restrict__ b, int32_t n_own,
-                                                   int32_t n, double omega) {
+                                                   int32_t n, double omega, RowMap map) {
   vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
-  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
-  if (row >= n) return;
+  const int32_t row = map_row(map, blockIdx.x, threadIdx.x, n_own);
+  if (row < 0 || row >= n) return;
   const double xo = x_old[row];
   if (row >= n_own) {
     x_new[row] = xo;
@@ -454,11 +454,12 @@ __global__ void __launch_bounds__(kSplitBlock) k_color_sweep_split(SellView A, d
 template <int kVK>
 __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_residual(SellView A, const double* __restrict__ x,
                                                      const double* __restrict__ b,
-                                                     double* __restrict__ r, int32_t n) {
+                                                     double* __restrict__ r, int32_t n, int32_t n_own,
+                                                     RowMap map) {
   vtab_stage<kVK>(A);
   PF_PDL_ENTRY();
-  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
-  if (row >= n) return;
+  const int32_t row = map_row(map, blockIdx.x, threadIdx.x, n_own);
+  if (row < 0 || row >= n) return;
   r[row] = __dsub_rn(b[row], row_dot<false, true, kVK>(A, row, x, 0.0));
 }
 

@@ -34,6 +34,7 @@
 #include "pf_heat.cuh"
 #include "pf_kernels.cuh"
 #include "pf_nccl.hpp"
+#include "pf_sweep_tma.cuh"
 #include "pf_runtime.hpp"
 
 using namespace pf;
@@ -393,6 +394,17 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
 
 // Device layout of one subdomain level: own rows colour-major (stable in host order),
 // then every other row in host order; SELL-32 operator; P (rows of this level).
+// PF_INTERLEAVE_MIN_BYTES (default 64 MB): levels whose x is at least this large run their
+// full-level Jacobi / residual passes with the colour-interleaved block schedule (0: every
+// level with 2-8 colours; a huge value: never).
+int64_t interleave_min_bytes() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("PF_INTERLEAVE_MIN_BYTES");
+    return e ? std::atoll(e) : int64_t(64) << 20;
+  }();
+  return v;
+}
+
 void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
   PhaseTimer tm;
   const int32_t n = H.n, n_own = H.n_own;
@@ -486,6 +498,18 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
     for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
   }
   D.d_perm.upload(D.perm);
+  // colour-interleaved block schedule when x outgrows L2 (RowMap, pf_types.hpp)
+  D.rmap = RowMap{};
+  D.rmap_grid = grid_for(n);
+  if (n_colors >= 2 && n_colors <= 8 && 8 * static_cast<int64_t>(n) >= interleave_min_bytes()) {
+    int32_t chunks = 0;
+    for (int c = 0; c < n_colors; ++c)
+      chunks = std::max<int32_t>(chunks, static_cast<int32_t>(grid_for(D.color_start[c + 1] - D.color_start[c])));
+    D.rmap.n_col = n_colors;
+    D.rmap.chunks = chunks;
+    for (int c = 0; c <= n_colors; ++c) D.rmap.start[c] = D.color_start[c];
+    D.rmap_grid = static_cast<unsigned>(chunks) * n_colors + grid_for(n - n_own);
+  }
   tm("colours + perm", level);
   // --- SELL-32x4 operator: rows in device order, columns mapped, entries in CSR order,
   // written straight from the host CSR (no intermediate re-layout: at 512^3 the finest
@@ -1177,7 +1201,8 @@ void enq_residual(pf_hierarchy* h, int l, const double* x, const double* b, doub
   auto launch = launcher(h);
   for (DevLevel& D : L.sub)
     vk_dispatch_rows(D.A, [&](auto V) {
-      launch(grid_for(D.n), kBlock, k_residual<decltype(V)::value>, view(D.A), x + D.offset, b + D.offset, r + D.offset, D.n);
+      launch(D.rmap_grid, kBlock, k_residual<decltype(V)::value>, view(D.A), x + D.offset, b + D.offset, r + D.offset, D.n,
+             D.n_own, D.rmap);
     });
 }
 
@@ -1215,6 +1240,45 @@ int64_t split_max_rows() {
   return v;
 }
 
+// PF_SOR_TMA (default 1): colour sweeps of operators with rows of <= 28 entries (Q1,
+// rotated Q1) take the TMA-staged persistent kernel (pf_sweep_tma.cuh) on levels with at
+// least PF_SOR_TMA_MIN_ROWS own rows; PF_SOR_TMA_BPS blocks per SM (default 1, which leaves
+// room for the next colour's blocks to stream their operator chunks meanwhile).
+bool sor_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_SOR_TMA");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+int64_t sor_tma_min_rows() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("PF_SOR_TMA_MIN_ROWS");
+    return e ? std::atoll(e) : int64_t(65536);
+  }();
+  return v;
+}
+int sor_tma_bps() {
+  static const int v = [] {
+    const char* e = std::getenv("PF_SOR_TMA_BPS");
+    return e ? std::max(1, std::atoi(e)) : 2;
+  }();
+  return v;
+}
+int sor_tma_cfg() {  // experiment: 0 = 8 warps x 2 stages, 1 = 4 x 4, 2 = 8 x 3
+  static const int v = [] {
+    const char* e = std::getenv("PF_SOR_TMA_CFG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+int sm_count(int device) {
+  static int cached[64] = {};
+  if (device < 0 || device >= 64) device = 0;
+  if (!cached[device]) PF_CUDA(cudaDeviceGetAttribute(&cached[device], cudaDevAttrMultiProcessorCount, device));
+  return cached[device];
+}
+
 void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega, double* x, const double* b) {
   const int32_t r0 = D.color_start[c], r1 = D.color_start[c + 1];
   if (r1 <= r0) return;
@@ -1222,6 +1286,31 @@ void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega
   const int split = split_row_len();
   vk_dispatch_rows(D.A, [&](auto V) {
     constexpr int vk = decltype(V)::value;
+    if (sor_tma_enabled() && D.A.max_len <= 4 * kTmaMaxGroups && D.A.max_len > 0 && D.n_own >= sor_tma_min_rows()) {
+      const int32_t width = (D.A.max_len + 3) / 4 * 4;
+      const TmaStageLayout lay = tma_layout(width, tma_vbytes<vk>());
+      auto go = [&](auto W, auto S) {
+        constexpr int kw = decltype(W)::value, ks = decltype(S)::value;
+        const size_t smem = static_cast<size_t>(kw) * ks * lay.bytes;
+        auto kern = sor ? k_color_sweep_tma<true, vk, kw, ks> : k_color_sweep_tma<false, vk, kw, ks>;
+        static thread_local std::map<const void*, size_t> attr_set;
+        auto& have = attr_set[reinterpret_cast<const void*>(kern)];
+        if (smem > 48 * 1024 && have < smem) {
+          PF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+          have = smem;
+        }
+        const int64_t n_slices = ((r1 - 1) >> 5) - (r0 >> 5) + 1;
+        const int64_t grid = std::min<int64_t>((n_slices + kw - 1) / kw,
+                                               static_cast<int64_t>(sor_tma_bps()) * sm_count(h->device));
+        launch.with_smem(smem)(static_cast<unsigned>(grid), 32 * kw, kern, view(D.A), x, b, r0, r1, omega, width);
+      };
+      switch (sor_tma_cfg()) {
+        case 1: go(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}); break;
+        case 2: go(std::integral_constant<int, 8>{}, std::integral_constant<int, 3>{}); break;
+        default: go(std::integral_constant<int, 8>{}, std::integral_constant<int, 2>{}); break;
+      }
+      return;
+    }
     if (split > 0 && D.A.max_len > split && D.n_own <= split_max_rows()) {
       const int32_t width = (D.A.max_len + 3) / 4 * 4;
       const size_t smem = sizeof(double) * kSlice * static_cast<size_t>(width);
@@ -1288,9 +1377,9 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
         if (!(first_done && sweep == 0 && local == 0))
           for (DevLevel& D : L.sub)
             vk_dispatch_rows(D.A, [&](auto V) {
-              launch(grid_for(D.n), kBlock, k_jacobi<decltype(V)::value>, view(D.A),
+              launch(D.rmap_grid, kBlock, k_jacobi<decltype(V)::value>, view(D.A),
                      static_cast<const double*>(bufs[cur] + D.offset), bufs[cur ^ 1] + D.offset, b + D.offset,
-                     D.n_own, D.n, sc.damping);
+                     D.n_own, D.n, sc.damping, D.rmap);
             });
         cur ^= 1;
       } else {
@@ -2665,7 +2754,7 @@ pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double*
       const double* src = (i & 1) ? x->alt() : x->cur();
       double* dst = (i & 1) ? x->cur() : x->alt();
       vk_dispatch_rows(D.A, [&](auto V) {
-        launch(grid_for(D.n), kBlock, k_jacobi<decltype(V)::value>, view(D.A), src, dst, b, D.n_own, D.n, 0.8);
+        launch(D.rmap_grid, kBlock, k_jacobi<decltype(V)::value>, view(D.A), src, dst, b, D.n_own, D.n, 0.8, D.rmap);
       });
     } else {
       for (int c = 0; c < D.n_colors; ++c)

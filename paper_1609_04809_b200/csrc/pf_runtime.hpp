@@ -108,6 +108,8 @@ struct DevLevel {
   int64_t offset = 0;  // position of this subdomain inside the level's vectors
   int n_colors = 0;
   std::vector<int32_t> color_start;  // device rows, n_colors + 1 (own rows only)
+  RowMap rmap{};                     // block schedule of the full-level Jacobi / residual passes
+  unsigned rmap_grid = 0;            // their grid under rmap
   std::vector<int32_t> perm;         // host index -> device index
   DevBuf<int32_t> d_perm;
   DevSell A;

@@ -75,6 +75,31 @@ struct SellView {
   int32_t table_n;  // distinct values in the table
 };
 
+// Block schedule of a full-level row kernel (k_jacobi, k_residual).  Own rows sit
+// colour-major on the device (each colour in lattice order), so the identity schedule
+// sweeps colour 0 over the whole lattice, then colour 1, ...: each colour pass gathers its
+// neighbours from all the other colours across the whole x, which on a level whose x
+// exceeds L2 (512^3: 1.08 GB) re-reads x from HBM once per colour.  With n_col > 0 the
+// blocks instead take chunk k of colour c at block k * n_col + c, so the blocks resident at
+// any moment cover one lattice slab of every colour and x streams through L2 about once.
+// Rows compute exactly the same values either way (each row is independent).
+struct RowMap {
+  int32_t n_col;      // 0: identity schedule
+  int32_t chunks;     // blocks per colour (the largest colour)
+  int32_t start[9];   // colour starts over the own rows; start[n_col] = n_own
+};
+
+// The row of this thread under map m (level of n rows, n_own own rows), or -1.
+PF_HD inline int32_t map_row(const RowMap& m, int32_t block, int32_t thread, int32_t n_own) {
+  if (m.n_col == 0) return block * kBlock + thread;
+  const int32_t own_blocks = m.chunks * m.n_col;
+  if (block >= own_blocks) return n_own + (block - own_blocks) * kBlock + thread;  // non-own rows
+  const int32_t c = block % m.n_col, k = block / m.n_col;
+  const int32_t row = m.start[c] + k * kBlock + thread;
+  return row < m.start[c + 1] ? row : -1;
+}
+
+
 // One subdomain of the coarse level, for the sequential coarse solve.
 struct CoarseSub {
   SellView A;

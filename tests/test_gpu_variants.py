@@ -30,6 +30,11 @@ VARIANTS = {
     "index_l1_streamed": {"PF_VTAB_SMEM": "0", "PF_CACHED_MAX_BYTES": "0", "PF_FUSED_RR_ROWS": "100000000"},
     # fp64 everywhere, every level streamed
     "fp64_streamed": {"PF_VALUE_INDEX": "0", "PF_CACHED_MAX_BYTES": "0"},
+    # the TMA-staged colour sweep on every level whose rows fit it (default: >= 64k rows),
+    # two blocks per SM; and the register-pipelined colour sweep everywhere
+    "sor_tma_everywhere": {"PF_SOR_TMA_MIN_ROWS": "0", "PF_SOR_TMA_BPS": "2"},
+    "sor_tma_fp64": {"PF_SOR_TMA_MIN_ROWS": "0", "PF_VALUE_INDEX": "0"},
+    "sor_tma_off": {"PF_SOR_TMA": "0"},
 }
 
 

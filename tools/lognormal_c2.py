@@ -19,3 +19,5 @@ for kind, om in ((0, 0.8), (2, 1.2)):
     print(f"kind {kind}: cycles {st.iterations} converged {st.converged} solve {min(ts)*1e3:.2f} ms DOF/s {s.n_global/min(ts):.3e} vcycle {h.time_vcycle(x, b, c, 10):.3f} ms", flush=True)
 ms, by = h.time_sweep(L - 1, 0, 20)
 print(f"sweep: {ms*1e3:.1f} us {by/ms/1e6:.1f} GB/s")
+ms, by = h.time_sweep(L - 1, 2, 20)
+print(f"SOR sweep: {ms*1e3:.1f} us {by/ms/1e6:.1f} GB/s")
