@@ -218,6 +218,14 @@ pf_status pf_hierarchy_set_replica_level(pf_hierarchy* h, int level, int rank, c
  * (pf_setup_options.direct_halos; checked at finalize, PF_ERR_INVALID_ARGUMENT otherwise).
  * Must be set identically on every rank.  Results are unchanged bit for bit. */
 pf_status pf_hierarchy_set_fused_exchanges(pf_hierarchy* h, int on);
+/* Coloured smoothers (Gauss-Seidel / SOR) on several subdomains: run the master/slave and
+ * halo1 scatters after EVERY colour instead of once per sweep (solvers.cpp:56-68), so a
+ * K-subdomain coloured sweep relaxes like the single-domain coloured sweep for any K (the
+ * processor-local sweep of the reference lags the copies by one sweep, which makes
+ * over-relaxed SOR diverge on the rotated-Q1 lognormal operator at K = 8).  Off by
+ * default (reference semantics).  Must be set identically on every rank; restated in
+ * oracle/gmg_oracle.c (orc_set_colorwise). */
+pf_status pf_hierarchy_set_colorwise_exchange(pf_hierarchy* h, int on);
 pf_status pf_hierarchy_destroy(pf_hierarchy* h);
 
 /* Single-GPU test bench of the multi-process path: `world_size` single-subdomain

@@ -49,6 +49,7 @@ struct orc_hier {
   int nl, ns;
   OLev* lev;   /* [level * ns + sub] */
   double* cinv; /* orc_set_coarse_direct: inverse of level 0's own block, or NULL */
+  int colorwise; /* orc_set_colorwise */
 };
 
 static OLev* L_(orc_hier* h, int l, int s) { return &h->lev[l * h->ns + s]; }
@@ -328,10 +329,36 @@ int orc_smooth(orc_hier* h, int level, double* const* x, double* const* b, const
     if (L_(h, level, s)->n > maxn) maxn = L_(h, level, s)->n;
   double* scratch = malloc(sizeof(double) * maxn);
   int rc = 0;
+  const int colorwise = h->colorwise && (c->kind == PF_SMOOTHER_GAUSS_SEIDEL || c->kind == PF_SMOOTHER_MULTICOLOR_SOR);
+  int maxcol = 0;
+  for (int s = 0; s < h->ns; ++s)
+    if (L_(h, level, s)->ncolors > maxcol) maxcol = L_(h, level, s)->ncolors;
   for (int sweep = 0; sweep < c->sweeps && !rc; ++sweep) {
-    for (int loc = 0; loc < c->local_sweeps; ++loc)
-      for (int s = 0; s < h->ns; ++s) one_local_sweep(L_(h, level, s), x[s], b[s], c, scratch);
-    rc = orc_update_master_slave(h, level, x, PF_UPDATE_SCATTER);
+    for (int loc = 0; loc < c->local_sweeps && !rc; ++loc) {
+      if (!colorwise) {
+        for (int s = 0; s < h->ns; ++s) one_local_sweep(L_(h, level, s), x[s], b[s], c, scratch);
+        continue;
+      }
+      /* colour-wise exchange (B200 option, not in the reference): every subdomain sweeps
+       * colour col, then the master/slave and halo1 scatters refresh every copy, so the
+       * next colour sees the values a single-domain coloured sweep would */
+      const int sor = c->kind == PF_SMOOTHER_MULTICOLOR_SOR;
+      for (int col = 0; col < maxcol && !rc; ++col) {
+        for (int s = 0; s < h->ns; ++s) {
+          OLev* L = L_(h, level, s);
+          double diag;
+          for (int r = 0; r < L->n_own; ++r) {
+            if (L->color[r] != col) continue;
+            const double acc = offdiag(L, r, x[s], b[s][r], &diag);
+            x[s][r] = sor ? (1.0 - c->damping) * x[s][r] + c->damping * acc / diag : acc / diag;
+          }
+        }
+        if (loc + 1 == c->local_sweeps && col + 1 == maxcol) break; /* the sweep's own exchange follows */
+        rc = orc_update_master_slave(h, level, x, PF_UPDATE_SCATTER);
+        if (!rc) rc = scatter(h, level, PF_CH_HALO1, x);
+      }
+    }
+    if (!rc) rc = orc_update_master_slave(h, level, x, PF_UPDATE_SCATTER);
     if (!rc) rc = scatter(h, level, PF_CH_HALO1, x);
   }
   free(scratch);
@@ -341,6 +368,11 @@ int orc_smooth(orc_hier* h, int level, double* const* x, double* const* b, const
 /* Direct coarse solve of the B200 build (pf_hierarchy_set_coarse_direct): the inverse of
  * the own-own block by Gauss-Jordan elimination with partial pivoting (first row of
  * maximal |pivot|), pivot rows scaled by division. */
+int orc_set_colorwise(orc_hier* h, int on) {
+  h->colorwise = on != 0;
+  return 0;
+}
+
 int orc_set_coarse_direct(orc_hier* h, int on) {
   free(h->cinv);
   h->cinv = NULL;

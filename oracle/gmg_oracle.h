@@ -30,6 +30,8 @@ int orc_create(int n_levels, int n_sub, orc_hier** out);
 int orc_set_level(orc_hier* h, int level, int sub, const pf_level_desc* d);
 int orc_finalize(orc_hier* h);
 int orc_set_coarse_direct(orc_hier* h, int on);
+/* Colour-wise exchange of the coloured smoothers (pf_hierarchy_set_colorwise_exchange). */
+int orc_set_colorwise(orc_hier* h, int on);
 void orc_destroy(orc_hier* h);
 int orc_n_dofs(const orc_hier* h, int level, int sub);
 

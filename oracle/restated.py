@@ -31,6 +31,7 @@ def lib():
         L.orc_set_level.argtypes = [P, C.c_int, C.c_int, C.POINTER(_lib.LevelDesc)]
         L.orc_finalize.argtypes = [P]
         L.orc_set_coarse_direct.argtypes = [P, C.c_int]
+        L.orc_set_colorwise.argtypes = [P, C.c_int]
         L.orc_destroy.argtypes = [P]
         L.orc_destroy.restype = None
         vec = P  # double* const*
@@ -59,7 +60,7 @@ def _vec(arrs):
 class Oracle:
     """K subdomains (ranks 0..K-1) of one hierarchy, host order, reference semantics."""
 
-    def __init__(self, levels, coarse_direct=False):
+    def __init__(self, levels, coarse_direct=False, colorwise=False):
         L = lib()
         self.K, self.n_levels = len(levels), len(levels[0])
         self.sizes = [[lv.n for lv in sub] for sub in levels]
@@ -73,6 +74,8 @@ class Oracle:
         self._check(L.orc_finalize(self._h))
         if coarse_direct:
             self._check(L.orc_set_coarse_direct(self._h, 1))
+        if colorwise:
+            self._check(L.orc_set_colorwise(self._h, 1))
 
     @staticmethod
     def _check(rc):

@@ -73,6 +73,7 @@ struct BotCfg {
   double omega, coarse_tol;
   int block_top;  // levels 0..block_top inside block 0 (-1: none); chosen per smoother
   int calib;      // PF_BOTTOM_CALIB: empty grid-barrier phases first (profiling aid)
+  int colorwise;  // coloured smoothers: master/slave + halo1 scatter after every colour
 };
 
 // Latency-oriented row routines for the bottom levels, where each phase is a chain of
@@ -192,6 +193,18 @@ __device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps,
             }
           }
           T.sync(D, ph);
+          // colour-wise exchange: every copy refreshed before the next colour (the
+          // sweep's own exchange follows the last colour of the last local sweep)
+          if (c.colorwise && !(loc + 1 == c.local_sweeps && col + 1 == L.max_colors)) {
+            if (L.ms.n) {
+              bot_copy_plan(L.ms, x, t, stride);
+              T.sync(D, ph);
+            }
+            if (L.h1.n) {
+              bot_copy_plan(L.h1, x, t, stride);
+              T.sync(D, ph);
+            }
+          }
         }
       }
     }

@@ -1386,11 +1386,23 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
         const bool sor = sc.kind == PF_SMOOTHER_MULTICOLOR_SOR;
         int max_colors = 0;
         for (DevLevel& D : L.sub) max_colors = std::max(max_colors, D.n_colors);
-        for (int c = 0; c < max_colors; ++c)
+        for (int c = 0; c < max_colors; ++c) {
           for (DevLevel& D : L.sub) {
             if (c >= D.n_colors) continue;
             enq_color_sweep(h, D, c, sor, sor ? sc.damping : 1.0, bufs[cur] + D.offset, b + D.offset);
           }
+          // colour-wise exchange: every copy is refreshed before the next colour, so a
+          // partitioned sweep relaxes like the single-domain coloured sweep (the sweep's
+          // own exchange below follows the last colour of the last local sweep)
+          if (h->colorwise && !(local + 1 == sc.local_sweeps && c + 1 == max_colors)) {
+            if (h->fused) {
+              enq_plan(h, L.fused_ms_h1, bufs[cur]);
+            } else {
+              enq_update_ms(h, l, bufs[cur], PF_UPDATE_SCATTER);
+              enq_scatter(h, l, PF_CH_HALO1, bufs[cur]);
+            }
+          }
+        }
       }
     }
     if (exchanged) {
@@ -1594,7 +1606,8 @@ void enq_bottom(pf_hierarchy* h, const pf_hierarchy::Bottom& bot, const pf_multi
   const int block_top = cfg.smoother.kind == PF_SMOOTHER_JACOBI ? -1 : 1 << 20;
   static const int calib = std::getenv("PF_BOTTOM_CALIB") ? std::atoi(std::getenv("PF_BOTTOM_CALIB")) : 0;
   const BotCfg c{cfg.smoother.kind, cfg.pre_smooth, cfg.post_smooth, cfg.smoother.local_sweeps,
-                 cfg.coarse_max_iter, cfg.smoother.damping, cfg.coarse_tol, block_top, calib};
+                 cfg.coarse_max_iter, cfg.smoother.damping, cfg.coarse_tol, block_top, calib,
+                 h->colorwise && cfg.smoother.kind != PF_SMOOTHER_JACOBI ? 1 : 0};
   PF_CUDA(cudaLaunchKernelEx(&lc, k_bottom, static_cast<const BotDesc*>(bot.desc), c, accumulate_top));
   ++*(g_capture_counter ? g_capture_counter : &h->launches);
 }
@@ -2326,6 +2339,14 @@ pf_status pf_hierarchy_set_fused_exchanges(pf_hierarchy* h, int on) {
   if (!h) invalid("null hierarchy");
   if (h->finalized) state("set fused exchanges before pf_hierarchy_finalize");
   h->fused = on != 0;
+  PF_API_END
+}
+
+pf_status pf_hierarchy_set_colorwise_exchange(pf_hierarchy* h, int on) {
+  PF_API_BEGIN
+  if (!h) invalid("null hierarchy");
+  h->colorwise = on != 0;
+  if (h->finalized) drop_graphs(h);  // captured smoothing phases change
   PF_API_END
 }
 

@@ -215,6 +215,7 @@ struct pf_hierarchy {
   int n_levels = 0, n_sub = 1, rank_base = 0, world = 1;
   bool finalized = false;
   bool fused = false;  // master/slave + halo scatters as one message group (direct halo lists)
+  bool colorwise = false;  // coloured smoothers exchange after every colour (pf_hierarchy_set_colorwise_exchange)
   pf::DevBuf<double> coarse_inv;  // pf_hierarchy_set_coarse_direct: inverse of level 0's own block
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

@@ -262,6 +262,12 @@ class Hierarchy:
                 v.upload(values, 0)
         return v
 
+    def set_colorwise_exchange(self, on: bool = True) -> "Hierarchy":
+        """Coloured smoothers exchange after every colour (pf_hierarchy_set_colorwise_exchange):
+        a K-subdomain sweep then relaxes like the single-domain coloured sweep."""
+        _lib.check(_lib.lib().pf_hierarchy_set_colorwise_exchange(self._h, 1 if on else 0))
+        return self
+
     def set_coarse_direct(self, on: bool = True) -> "Hierarchy":
         """Direct coarse solve on level 0 (pf_hierarchy_set_coarse_direct): one subdomain."""
         _lib.check(_lib.lib().pf_hierarchy_set_coarse_direct(self._h, 1 if on else 0))

@@ -19,8 +19,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-from helpers import cfg, key_noise, structured  # noqa: E402
+from helpers import cfg, key_noise  # noqa: E402
 from paper_1609_04809_b200 import _lib, gmg  # noqa: E402
+from paper_1609_04809_b200.levels import StructuredSetup  # noqa: E402
 
 
 def main():
@@ -32,9 +33,12 @@ def main():
     ap.add_argument("--rep", default="coarse")
     ap.add_argument("--fused", action="store_true")
     ap.add_argument("--idle-rank", type=int, default=-1, help="this rank never solves (watchdog check)")
+    ap.add_argument("--colorwise", action="store_true")
+    ap.add_argument("--problem", type=int, default=0)
     a = ap.parse_args()
     K, L = a.world, a.levels
-    setups, levels = structured(3, 2, L, K, direct_halos=a.fused)
+    setups = [StructuredSetup(3, 2, L, K, r, a.problem, seed=1, direct_halos=a.fused) for r in range(K)]
+    levels = [s.levels for s in setups]
     c = cfg(a.kind, damping=1.2 if a.kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
     replicas = [s[0] for s in levels] if a.rep == "coarse" else [s[:L - 1] for s in levels]
     blobs = [None] * K
@@ -43,6 +47,8 @@ def main():
 
     def body(r):
         h = gmg.Hierarchy([levels[r]], rank_base=r, world_size=K, coarse_replicas=replicas, fused_exchanges=a.fused)
+        if a.colorwise:
+            h.set_colorwise_exchange()
         blobs[r] = h.peer_export()
         bar.wait()
         h.init_peer(blobs)
