@@ -110,13 +110,15 @@ class Clocks:
 
 
 def ncu_traffic():
-    """DRAM bytes per finest-level Jacobi launch from the committed ncu --set full capture."""
+    """(DRAM bytes per finest-level Jacobi launch, where they come from): the committed
+    ncu --set full capture of this kernel (profiles/ncu_summary.json, refreshed from the
+    current build each round; ncu cannot run inside the timed bench)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            s = json.load(f)
-        return s.get("k_jacobi_c2", {}).get("dram_bytes_per_launch")
+            s = json.load(f).get("k_jacobi_c2", {})
+        return s.get("dram_bytes_per_launch"), s.get("source")
     except Exception:
-        return None
+        return None, None
 
 
 def cpu_baseline(steps_hint: int = 1):
@@ -302,6 +304,7 @@ def run_b200(args):
     alg_bytes = 12 * z_own + 4 * fin.n_own + 8 * m_cols + 16 * fin.n_own
     achieved = alg_bytes / (sweep_ms / 1e3) / 1e9
     achieved_stored = sweep_bytes / (sweep_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic()
 
     # multicolour SOR w=1.2 variant of the same config (BASELINE configs[1])
     sor = gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=gmg.PF_SMOOTHER_MULTICOLOR_SOR, damping=1.2),
@@ -381,11 +384,62 @@ def run_b200(args):
             fh.close()
             return out
 
+        def fe_k8_colorwise(omega):
+            """configs[3] on 8 subdomains ("1 and 8 GPUs"): the partitioned rotated-Q1
+            lognormal hierarchy, all 8 subdomains on this GPU, SOR with the colour-wise
+            exchange (processor-local smoothing diverges here)."""
+            fs = [FESetup(ROTATED_Q1, 2, 7, LOGNORMAL, seed=2024, n_ranks=8, rank=r) for r in range(8)]
+            fh = gmg.Hierarchy([f.levels for f in fs], device=local).set_colorwise_exchange()
+            fc = gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=gmg.PF_SMOOTHER_MULTICOLOR_SOR, damping=omega),
+                                     pre_smooth=2, post_smooth=2, outer_tol=W["tol"], outer_max_cycles=400)
+            fx = fh.vector(6, [f.x0 for f in fs])
+            fb = fh.vector(6, [f.b for f in fs])
+            fstream = torch.cuda.ExternalStream(fh.stream_handle(), device=torch.device("cuda", local))
+            fst = gmg.solve_outer(fh, fx, fb, fc)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            w0 = time.time()
+            e0.record(fstream)
+            for _ in range(2):
+                for r, f in enumerate(fs):
+                    fx.upload(f.x0, r)
+                fst = gmg.solve_outer(fh, fx, fb, fc)
+            e1.record(fstream)
+            torch.cuda.synchronize()
+            clk.window(w0, time.time())
+            f_ms = e0.elapsed_time(e1) / 2
+            n_global = 3 * 128 * 128 * 129
+            out = {"value": n_global / (f_ms / 1e3), "unit": "DOF/s", "n_global": n_global, "subdomains": 8,
+                   "cycles": fst.iterations, "converged": bool(fst.converged), "ms_per_step": f_ms,
+                   "vcycle_ms": fh.time_vcycle(fx, fb, fc, 5), "exchange": "colour-wise",
+                   "note": "8 box subdomains of the 1-GPU configs[3] problem on one GPU (device-local "
+                           "exchanges); the processor-local reference smoothing diverges at K=8"}
+            fh.close()
+            return out
+
         fe["q2_c3_jacobi_v33"] = fe_variant(Q2, CONSTANT, 6, 3, gmg.PF_SMOOTHER_JACOBI, W["omega"])
         # omega 1.6: 68 cycles at 128^3 (1.2: 101, 1.4: 81, 1.8: 156; tools/fe_run.py)
         fe["rotated_q1_c4_lognormal_sor_1.6"] = fe_variant(ROTATED_Q1, LOGNORMAL, 7, 2,
                                                           gmg.PF_SMOOTHER_MULTICOLOR_SOR, 1.6)
+        fe["rotated_q1_c4_lognormal_sor_1.6_k8_colorwise"] = fe_k8_colorwise(1.6)
 
+    # BASELINE configs[4] (C5: 512^3, lognormal, SOR) on this one GPU: the N = 1 point of the
+    # scaling configuration (bench.py --gpus N runs it on N GPUs)
+    c5 = None
+    if world == 1 and not args.no_c5:
+        import types
+        h.close()
+        c5h, c5s, c5_setup, c5_upload = c5_hierarchy(1, 0, local, args.transport, None)
+        m = c5_solve(c5h, c5s, 1, 0, types.SimpleNamespace(steps=2, warmup=1), clk, None, local, "c5")
+        c5 = {"value": m["value"], "unit": "DOF/s", "n_global": c5s.n_global, "cycles": m["cycles"],
+              "converged": m["converged"], "ms_per_step": m["ms_per_step"], "vcycle_ms": m["vcycle_ms"],
+              "e2e": m["e2e"], "sor_sweep_us": m["sor_sweep_ms"] * 1e3,
+              "sor_sweep_frac_on_stored_bytes": m["sor_sweep_bytes"] / m["sor_sweep_ms"] / 1e6 / peak,
+              "jacobi_sweep_us": m["jacobi_sweep_ms"] * 1e3,
+              "jacobi_sweep_frac_on_stored_bytes": m["jacobi_sweep_bytes"] / m["jacobi_sweep_ms"] / 1e6 / peak,
+              "setup_seconds": c5_setup, "upload_seconds": c5_upload, "steps": 2,
+              "config": C5_CONFIG["workload"]}
+        c5h.close()
     clk.stop()
     clocks = clk.summary()
     if rank != 0:
@@ -406,17 +460,19 @@ def run_b200(args):
         "config": dict(CONFIG, parallelism=f"{world} box subdomain(s), one per GPU" if world > 1 else "1 GPU"),
         "cycles": st.iterations, "final_rel_residual": st.final_residual / st.initial_residual,
         "vcycle_ms": vcycle_ms,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(),
+        "roofline": {"bound": "hbm", "achieved": achieved_stored, "peak": peak, "unit": "GB/s",
+                     "frac": achieved_stored / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": "k_jacobi (finest-level damped-Jacobi sweep; SELL-32x4, int32 columns, "
                                "8-bit index into the table of distinct fp64 values staged in shared "
                                "memory, row-start L2 prefetch, 48 registers / 5 blocks per SM)",
-                     "kernel_us": sweep_ms * 1e3, "algorithmic_bytes_per_launch": alg_bytes,
-                     "algorithmic_bytes_formula": "SURVEY.md 8(d): 12 z + 4 n + 8 m + 16 n (fp64 CSR)",
-                     "stored_bytes_per_launch": sweep_bytes, "achieved_on_stored_bytes": achieved_stored,
-                     "frac_on_stored_bytes": achieved_stored / peak,
-                     "note": "frac > 1: the kernel streams 4 + 1 B per entry (lossless value index) "
-                             "instead of the 12 B of fp64 CSR; traffic (ncu) ~= stored bytes",
+                     "kernel_us": sweep_ms * 1e3, "bytes_per_launch": sweep_bytes,
+                     "bytes_formula": "(4 + 1) z + 4 n + 8 m + 16 n: the bytes the kernel streams (int32 "
+                                      "column + 1 B value index per own-row entry, row length, x once, b, out)",
+                     "fp64_csr_equivalent": {
+                         "bytes_per_launch": alg_bytes,
+                         "formula": "SURVEY.md 8(d): 12 z + 4 n + 8 m + 16 n (fp64 CSR)",
+                         "achieved": achieved, "note": "work-equivalent rate: the lossless value index "
+                         "moves 5 instead of 12 B per entry, so this exceeds the HBM peak"},
                      "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "DOF/s", "h2d_bytes_per_step": 16 * len(setup.x0),
@@ -430,7 +486,7 @@ def run_b200(args):
             "sweep_us": sor_ms * 1e3,
             "sweep_frac": alg_bytes / (sor_ms / 1e3) / 1e9 / peak,
             "sweep_frac_on_stored_bytes": sweep_bytes / (sor_ms / 1e3) / 1e9 / peak},
-            "lognormal_jacobi": logn, **fe},
+            "lognormal_jacobi": logn, **fe, "c5_512cubed_lognormal_sor_1.2_n1": c5},
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -788,6 +844,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fe", action="store_true", help="skip the Q2 / rotated-Q1 variants")
+    ap.add_argument("--no-c5", action="store_true", help="skip the one-GPU C5 (512^3) variant of the default run")
     ap.add_argument("--workload", choices=["poisson", "heat"], default="poisson",
                     help="poisson: BASELINE configs[1] (default); heat: the reference's CN run at C2")
     ap.add_argument("--config", choices=["c2", "c5"], default=None,

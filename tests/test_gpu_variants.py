@@ -30,11 +30,13 @@ VARIANTS = {
     "index_l1_streamed": {"PF_VTAB_SMEM": "0", "PF_CACHED_MAX_BYTES": "0", "PF_FUSED_RR_ROWS": "100000000"},
     # fp64 everywhere, every level streamed
     "fp64_streamed": {"PF_VALUE_INDEX": "0", "PF_CACHED_MAX_BYTES": "0"},
-    # the TMA-staged colour sweep on every level whose rows fit it (default: >= 64k rows),
-    # two blocks per SM; and the register-pipelined colour sweep everywhere
-    "sor_tma_everywhere": {"PF_SOR_TMA_MIN_ROWS": "0", "PF_SOR_TMA_BPS": "2"},
-    "sor_tma_fp64": {"PF_SOR_TMA_MIN_ROWS": "0", "PF_VALUE_INDEX": "0"},
-    "sor_tma_off": {"PF_SOR_TMA": "0"},
+    # the opt-in TMA-staged colour sweep (pf_sweep_tma.cuh) on every level whose rows fit it,
+    # index-encoded and fp64 operators
+    "sor_tma_everywhere": {"PF_SOR_TMA": "1", "PF_SOR_TMA_MIN_ROWS": "0", "PF_SOR_TMA_BPS": "2"},
+    "sor_tma_fp64": {"PF_SOR_TMA": "1", "PF_SOR_TMA_MIN_ROWS": "0", "PF_VALUE_INDEX": "0"},
+    # the colour-interleaved block schedule (RowMap) of the Jacobi / residual passes on every
+    # level with 2-8 colours (default: only where x exceeds 64 MB)
+    "interleave_everywhere": {"PF_INTERLEAVE_MIN_BYTES": "0"},
 }
 
 
@@ -44,7 +46,7 @@ def test_parity_suite_under_variant(cuda, name):
     env.update(VARIANTS[name])
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
            os.path.join(HERE, "test_gpu_parity.py"), os.path.join(HERE, "test_gpu_fe.py"),
-           "-k", "bit_exact or solve or lognormal"]
+           os.path.join(HERE, "test_gpu_colorwise.py"), "-k", "bit_exact or solve or lognormal or colorwise"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     tail = "\n".join((r.stdout + r.stderr).splitlines()[-25:])
     assert r.returncode == 0, f"{name}:\n{tail}"
