@@ -72,6 +72,24 @@ def solve_case(name, dim, nc, levels, K, smoother, problem=0, keep_solution=True
           f"final {res[-1]:.6e}, solve {st['solve_seconds']:.2f}s")
 
 
+def digest_case(name, dim, nc, levels, K, smoother):
+    """A whole solution pinned by a digest: sha256 of the keyed values in key order (the
+    GPU recomputes it from its own solution), plus the residual history and a sample."""
+    import hashlib
+    R = ref.build(dim, nc, levels, K, 0)
+    sizes = [R.ranks[r][-1].n_dofs for r in range(K)]
+    xs, res, st = ref.run(dim, nc, levels, K, smoother=smoother, pre=2, post=2, outer_tol=1e-10, sizes=sizes)
+    assert st["status"] == 0, st
+    keys, vals = keyed_solution(R, xs)
+    idx = np.linspace(0, len(vals) - 1, 512).astype(np.int64)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), dim=dim, n_coarse=nc, levels=levels, K=K,
+                        smoother=smoother, residuals=res, initial_residual=st["initial_residual"],
+                        iterations=st["iterations"], n_carriers=len(vals),
+                        digest=hashlib.sha256(np.ascontiguousarray(vals, np.float64).tobytes()).hexdigest(),
+                        keys=keys[idx], values=vals[idx])
+    print(f"{name}: {st['iterations']} cycles, {len(vals)} carriers, solve {st['solve_seconds']:.2f}s")
+
+
 def sweep_case(name, dim, nc, levels, K, smoother, n_ops):
     """Iterates of `n_ops` single smooth() calls from x0 (per-sweep parity)."""
     R = ref.build(dim, nc, levels, K, 0)
@@ -84,7 +102,7 @@ def sweep_case(name, dim, nc, levels, K, smoother, n_ops):
     print(f"{name}: {len(vals)} carriers")
 
 
-if __name__ == "__main__":
+def small_cases():
     # C1 (32^3, 5 levels): BASELINE configs[0], Jacobi and the reference GS, 1 and 8 ranks
     solve_case("c1_jacobi_k1", 3, 2, 5, 1, 0)
     solve_case("c1_jacobi_k8", 3, 2, 5, 8, 0)
@@ -96,7 +114,17 @@ if __name__ == "__main__":
     # per-sweep iterates
     sweep_case("sweeps_3d_l4_k2_jacobi", 3, 2, 4, 2, 0, 3)
     sweep_case("sweeps_3d_l4_k1_gs", 3, 2, 4, 1, 1, 2)
+
+
+if __name__ == "__main__":
+    if "--only-c2-digest" not in sys.argv:
+        small_cases()
     # C2 (128^3, 7 levels) residual history on 8 reference ranks (SURVEY: 9 cycles)
     if "--c2" in sys.argv:
         solve_case("c2_jacobi_k8", 3, 2, 7, 8, 0, keep_solution=False)
         solve_case("c2_gs_k8", 3, 2, 7, 8, 1, keep_solution=False)
+    # C2 whole-solution digests (1 and 8 reference ranks): the bench configuration pinned bit
+    # for bit (--c2-digest / --only-c2-digest)
+    if "--c2-digest" in sys.argv or "--only-c2-digest" in sys.argv:
+        digest_case("c2_jacobi_k1_digest", 3, 2, 7, 1, 0)
+        digest_case("c2_jacobi_k8_digest", 3, 2, 7, 8, 0)

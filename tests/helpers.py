@@ -55,3 +55,13 @@ def cfg(kind=gmg.PF_SMOOTHER_JACOBI, damping=0.8, pre=2, post=2, tol=1e-10, max_
     return gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=kind, damping=damping),
                                pre_smooth=pre, post_smooth=post, outer_tol=tol,
                                outer_max_cycles=max_cycles)
+
+
+def keyed_digest(level_arrays, values):
+    """sha256 of the authoritative (owns_row) values in Key4 order — the form of the
+    reference fixtures' whole-solution digests (tests/golden/make_golden.py digest_case)."""
+    import hashlib
+    keys = np.concatenate([lv.keys[np.flatnonzero(lv.owns_row)] for lv in level_arrays])
+    vals = np.concatenate([v[np.flatnonzero(lv.owns_row)] for lv, v in zip(level_arrays, values)])
+    order = np.lexsort(keys.T[::-1])
+    return hashlib.sha256(np.ascontiguousarray(vals[order], np.float64).tobytes()).hexdigest()

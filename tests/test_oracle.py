@@ -192,3 +192,17 @@ def test_oracle_heat_loop_matches_reference_run_heat(ref_lib, dim, nc, L, K):
             got[tuple(int(k) for k in tops[r].keys[i])] = float(u[r][i])
     assert got == rep["solution"]
     assert np.array_equal(res, rep["residuals"])
+
+
+def test_oracle_c2_solution_digest():
+    """The C restatement at the bench configuration (C2, 1 rank) reproduces the reference's
+    whole solution bit for bit (the digest fixture of make_golden.py --c2-digest)."""
+    import os
+    from helpers import cfg, keyed_digest, structured
+    from oracle.restated import Oracle
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c2_jacobi_k1_digest.npz"))
+    setups, levels = structured(3, 2, 7, 1)
+    xs, res, st, rc = Oracle(levels).solve_outer([setups[0].x0], [setups[0].b], cfg())
+    assert rc == 0 and st.iterations == int(g["iterations"])
+    np.testing.assert_array_equal(res, g["residuals"])
+    assert keyed_digest([levels[0][-1]], xs) == str(g["digest"])
