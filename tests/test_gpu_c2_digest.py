@@ -30,8 +30,10 @@ def test_c2_solution_digest_single_device(cuda, K):
     x = upload(h, 6, [s.x0 for s in setups])
     st = gmg.solve_outer(h, x, upload(h, 6, [s.b for s in setups]), cfg())
     assert st.iterations == int(g["iterations"]) == 9
-    np.testing.assert_allclose(st.residuals, g["residuals"], rtol=1e-13)
     assert keyed_digest([lv[-1] for lv in levels], download(h, x, K)) == str(g["digest"])
+    # the device norm is a tree sum of 2M squares, the reference's a sequential one: the
+    # two agree to a few ulps of the sum (n eps bounds it at 2e-10)
+    np.testing.assert_allclose(st.residuals, g["residuals"], rtol=1e-10)
 
 
 def test_c2_solution_digest_peer_ranks(cuda, tmp_path):
