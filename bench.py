@@ -202,7 +202,7 @@ def run_b200(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")  # host plumbing only: the data plane is libpf_gpu.so's
 
     W = WORKLOAD
     t0 = time.time()
@@ -216,12 +216,7 @@ def run_b200(args):
                 if multi else None)
     h = gmg.Hierarchy([setup.levels], device=local, rank_base=rank, world_size=world,
                       coarse_replicas=replicas, fused_exchanges=multi)
-    if world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(gmg.Hierarchy.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        h.init_nccl(bytes(uid.cpu().numpy().tobytes()))
+    used = attach_transport(h, world, rank, args.transport, dist) if world > 1 else None
     setup_s = time.time() - t0
     top = h.finest
     cfg = gmg.MultigridConfig(smoother=gmg.SmootherConfig(kind=gmg.PF_SMOOTHER_JACOBI, damping=W["omega"]),
@@ -253,7 +248,7 @@ def run_b200(args):
         clk.window(w0, time.time())
         ms = e0.elapsed_time(e1)
         if dist:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, st
@@ -290,7 +285,7 @@ def run_b200(args):
     clk.window(w0, time.time())
     n_headline_windows = len(clk.windows)
     if dist:
-        t = torch.tensor([e2e_ms], device="cuda")
+        t = torch.tensor([e2e_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = setup.n_global * args.steps / (e2e_ms / 1e3)
@@ -434,7 +429,7 @@ def run_b200(args):
     if world == 1 and not args.no_c5:
         import types
         h.close()
-        c5h, c5s, c5_setup, c5_upload = c5_hierarchy(1, 0, local, args.transport, None)
+        c5h, c5s, c5_setup, c5_upload, _ = c5_hierarchy(1, 0, local, args.transport, None)
         m = c5_solve(c5h, c5s, 1, 0, types.SimpleNamespace(steps=2, warmup=1), clk, None, local, "c5")
         c5 = {"value": m["value"], "unit": "DOF/s", "n_global": c5s.n_global, "cycles": m["cycles"],
               "converged": m["converged"], "ms_per_step": m["ms_per_step"], "vcycle_ms": m["vcycle_ms"],
@@ -463,7 +458,8 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic manufactured problem (f = 3 pi^2 sin sin sin, g = 0), product setup",
-        "config": dict(CONFIG, parallelism=f"{world} box subdomain(s), one per GPU" if world > 1 else "1 GPU"),
+        "config": dict(CONFIG, parallelism=f"{world} box subdomain(s), one per GPU, {used} exchanges" if world > 1
+                       else "1 GPU"),
         "cycles": st.iterations, "final_rel_residual": st.final_residual / st.initial_residual,
         "vcycle_ms": vcycle_ms,
         "roofline": {"bound": "hbm", "achieved": achieved_stored, "peak": peak, "unit": "GB/s",
@@ -589,6 +585,32 @@ def c5_solve(h, setup, world, rank, args, clk, dist, local, label):
             "jacobi_sweep_bytes": jac_bytes, "x0": x0, "b": b, "x": x}
 
 
+def attach_transport(h, world, rank, transport, dist):
+    """The multi-GPU data plane of hierarchy h: peer-memory exchanges (CUDA IPC over NVLink,
+    pf_peer.cu) by default — if any rank cannot map its peers, every rank falls back to
+    NCCL together — or NCCL.  Returns what was attached."""
+    from paper_1609_04809_b200 import dist as pdist
+    from paper_1609_04809_b200 import gmg
+    used = None
+    if transport == "peer":
+        err = None
+        try:
+            pdist.init_peer_transport(h, pdist.allgather_blobs_torch)
+        except Exception as e:  # noqa: BLE001
+            err = f"{type(e).__name__}: {e}"
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        failed = [(r, e) for r, e in enumerate(errs) if e]
+        if not failed:
+            return "peer"
+        h.drop_transport()
+        used = f"nccl (peer transport failed on rank {failed[0][0]}: {failed[0][1]})"
+    uid = [gmg.Hierarchy.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, 0)
+    h.init_nccl(uid[0])
+    return used or "nccl"
+
+
 def c5_hierarchy(world, rank, local, transport, dist):
     """Rank `rank`'s box of the C5 problem on its GPU (replicated bottom levels gathered from
     their owners, no other rank's setup built), with its transport attached."""
@@ -611,14 +633,8 @@ def c5_hierarchy(world, rank, local, transport, dist):
     h = gmg.Hierarchy.from_setups([setup], device=local, rank_base=rank, world_size=world,
                                   coarse_replicas=replicas, fused_exchanges=world > 1)
     upload_s = time.time() - t0
-    if world > 1:
-        if transport == "peer":
-            pdist.init_peer_transport(h, pdist.allgather_blobs_torch)
-        else:
-            uid = [gmg.Hierarchy.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, 0)
-            h.init_nccl(uid[0])
-    return h, setup, setup_s, upload_s
+    used = attach_transport(h, world, rank, transport, dist) if world > 1 else None
+    return h, setup, setup_s, upload_s, used
 
 
 def run_c5(args):
@@ -642,7 +658,7 @@ def run_c5(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")  # host plumbing only: the data plane is libpf_gpu.so's
-    h, setup, setup_s, upload_s = c5_hierarchy(world, rank, local, args.transport, dist)
+    h, setup, setup_s, upload_s, used = c5_hierarchy(world, rank, local, args.transport, dist)
     m = c5_solve(h, setup, world, rank, args, clk, dist, local, "c5")
     clk.stop()
     peak, peak_src = peaks()
@@ -664,8 +680,8 @@ def run_c5(args):
             "data": "synthetic manufactured problem (f = 3 pi^2 sin sin sin, g = 0, seeded lognormal kappa), "
                     "product setup",
             "config": dict(C5_CONFIG, parallelism=(f"{world} box subdomains (coordinate bisection), one per GPU, "
-                                                   f"{args.transport} exchanges" if world > 1 else "1 GPU"),
-                           transport=args.transport if world > 1 else None),
+                                                   f"{used} exchanges" if world > 1 else "1 GPU"),
+                           transport=used),
             "cycles": m["cycles"], "converged": m["converged"], "final_rel_residual": m["final_rel_residual"],
             "vcycle_ms": m["vcycle_ms"],
             "roofline": {"bound": "hbm", "achieved": sor_gbs, "peak": peak, "unit": "GB/s", "frac": sor_gbs / peak,

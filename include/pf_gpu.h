@@ -258,6 +258,10 @@ pf_status pf_hierarchy_init_loopback(pf_hierarchy* h, void* hub);
  * synchronisation (the reference fabric's watchdog, transport.cpp:54-60). */
 pf_status pf_hierarchy_peer_export(pf_hierarchy* h, void* blob, int64_t capacity, int64_t* size);
 pf_status pf_hierarchy_init_peer(pf_hierarchy* h, const void* blobs, int64_t stride);
+/* Detach the hierarchy's transport (NCCL, loopback or peer; captured graphs are dropped) so
+ * another can be attached — e.g. NCCL when peer mapping fails on some rank.  Collective in
+ * effect: every rank must switch together. */
+pf_status pf_hierarchy_drop_transport(pf_hierarchy* h);
 /* CUDA graphs the hierarchy has captured and cached (solve graphs, outer-cycle graphs). */
 pf_status pf_hierarchy_graph_count(const pf_hierarchy* h, int64_t* out);
 

@@ -130,6 +130,7 @@ EXPORTS = [
     "pf_hierarchy_destroy",
     "pf_loopback_create", "pf_loopback_destroy", "pf_hierarchy_init_loopback", "pf_hierarchy_device_bytes",
     "pf_hierarchy_peer_export", "pf_hierarchy_init_peer", "pf_hierarchy_graph_count",
+    "pf_hierarchy_drop_transport",
     "pf_vector_create", "pf_vector_destroy", "pf_vector_upload", "pf_vector_download",
     "pf_vector_fill", "pf_vector_copy", "pf_host_alloc", "pf_host_free", "pf_spmv", "pf_residual_norm", "pf_smooth",
     "pf_coarse_solve", "pf_prolongate", "pf_restrict_residual", "pf_update_master_slave",
@@ -193,6 +194,7 @@ def lib():
         "pf_hierarchy_peer_export": [P, P, C.c_int64, i64p],
         "pf_hierarchy_init_peer": [P, P, C.c_int64],
         "pf_hierarchy_graph_count": [P, i64p],
+        "pf_hierarchy_drop_transport": [P],
         "pf_hierarchy_destroy": [P],
         "pf_hierarchy_device_bytes": [P, i64p],
         "pf_vector_create": [P, C.c_int, PP],

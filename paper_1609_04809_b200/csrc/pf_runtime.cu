@@ -2414,6 +2414,16 @@ pf_status pf_hierarchy_init_peer(pf_hierarchy* h, const void* blobs, int64_t str
   PF_API_END
 }
 
+pf_status pf_hierarchy_drop_transport(pf_hierarchy* h) {
+  PF_API_BEGIN
+  if (!h) invalid("null hierarchy");
+  PF_CUDA(cudaSetDevice(h->device));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  drop_graphs(h);  // captured exchanges use the old transport
+  h->xport.reset();
+  PF_API_END
+}
+
 pf_status pf_loopback_create(int world_size, void** hub) {
   PF_API_BEGIN
   if (!hub || world_size < 1) invalid("bad argument");

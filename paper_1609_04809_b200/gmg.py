@@ -239,6 +239,10 @@ class Hierarchy:
         buf = C.create_string_buffer(b"".join(b.ljust(stride, b"\0") for b in blobs), stride * len(blobs))
         _lib.check(_lib.lib().pf_hierarchy_init_peer(self._h, buf, stride))
 
+    def drop_transport(self) -> None:
+        """Detach the transport (every rank together) so another can be attached."""
+        _lib.check(_lib.lib().pf_hierarchy_drop_transport(self._h))
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)

@@ -126,3 +126,83 @@ def test_two_process_sweep_matches_oracle(tmp_path, family):
         got = np.load(tmp_path / f"x{r}.npy")
         assert np.array_equal(got, want[r]), f"rank {r}"
         assert np.load(tmp_path / f"n{r}.npy")[0] == norm
+
+
+class _FakeHierarchy:
+    """Stands in for gmg.Hierarchy in attach_transport (no device here): records what the
+    product's transport selection did."""
+
+    def __init__(self, fail):
+        self.fail, self.calls = fail, []
+
+    def peer_export(self):
+        self.calls.append("export")
+        return b"blob-%d" % int(os.environ["RANK"])
+
+    def init_peer(self, blobs):
+        self.calls.append(("init_peer", tuple(blobs)))
+        if self.fail:
+            raise RuntimeError("cannot map peers")
+
+    def drop_transport(self):
+        self.calls.append("drop")
+
+    def init_nccl(self, uid):
+        self.calls.append(("nccl", len(uid)))
+
+
+def _plumbing_worker(rank, world, port, out_dir):
+    """The host side of bench.py --gpus 2 across real processes: replica levels gathered
+    from their owners (gmg.gather_replica_levels) equal the locally rebuilt ones; the peer
+    blobs allgather over torch.distributed and over a directory; a peer-mapping failure on
+    one rank makes every rank fall back to NCCL together (bench.attach_transport)."""
+    import sys
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    from paper_1609_04809_b200 import _lib, gmg
+    from paper_1609_04809_b200 import dist as pdist
+    from paper_1609_04809_b200.levels import StructuredSetup
+
+    def gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+    s = StructuredSetup(3, 2, 6, world, rank, _lib.PF_PROBLEM_LOGNORMAL, seed=3, direct_halos=True,
+                        materialize=False)
+    got = gmg.gather_replica_levels(s, gather)
+    want = gmg.replica_levels(3, 2, 6, world, _lib.PF_PROBLEM_LOGNORMAL, direct_halos=True)
+    # (replica_levels builds fewer levels per setup; the lognormal seed default is 1)
+    want = [[StructuredSetup(3, 2, 6, world, q, _lib.PF_PROBLEM_LOGNORMAL, seed=3, direct_halos=True).levels[l]
+             for l in range(len(want[q]))] for q in range(world)]
+    assert len(got) == world and all(len(g) == len(w) for g, w in zip(got, want))
+    for g_r, w_r in zip(got, want):
+        for a, b in zip(g_r, w_r):
+            assert a.n == b.n and np.array_equal(a.row_offsets, b.row_offsets)
+            assert np.array_equal(a.cols, b.cols) and np.array_equal(a.vals, b.vals)
+    blob = b"rank%d" % rank
+    assert pdist.allgather_blobs_torch(blob) == [b"rank0", b"rank1"]
+    assert pdist.allgather_blobs_dir(os.path.join(out_dir, "rdv"), rank, world, blob) == [b"rank0", b"rank1"]
+    gmg.Hierarchy.nccl_unique_id = staticmethod(lambda: bytes(128))  # no NCCL bootstrap on CPU
+    ok = _FakeHierarchy(fail=False)
+    assert bench.attach_transport(ok, world, rank, "peer", dist) == "peer"
+    assert ok.calls == ["export", ("init_peer", (b"blob-0", b"blob-1"))]
+    bad = _FakeHierarchy(fail=rank == 1)
+    used = bench.attach_transport(bad, world, rank, "peer", dist)
+    assert used.startswith("nccl (peer transport failed on rank 1"), used
+    assert bad.calls[-2:] == ["drop", ("nccl", 128)]
+    np.save(os.path.join(out_dir, f"ok{rank}.npy"), np.array([1]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_process_host_plumbing(tmp_path):
+    """gloo, world size 2: the multi-process host path of the product (replica gathering,
+    blob allgathers, the all-or-nothing transport fallback)."""
+    world = 2
+    mp.start_processes(_plumbing_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    for r in range(world):
+        assert np.load(tmp_path / f"ok{r}.npy")[0] == 1
