@@ -1,19 +1,24 @@
 // pf_kernels.cuh — sm_100a kernels of the GMG V-cycle hot path.
 //
-// Storage: every level operator is SELL-32 — slices of 32 consecutive device rows,
-// column-major inside a slice (entry j of the slice's lane l at
-// slice_ptr[s] + 32*j + l), so a warp's load of entry j of its 32 rows is one
-// 256 B (values) + 128 B (columns) contiguous transaction.  Entries of a row keep
-// the reference's CSR order (linalg.hpp:12-22), which fixes the summation order.
+// Storage: every level operator is SELL-32x4 (pf_types.hpp) — slices of 32 consecutive
+// device rows; inside a slice entry j of lane l sits at slice_ptr[s] + 128 (j/4) + 4 l +
+// j%4, so a lane reads four entries of its row with one 16-byte column load and a warp's
+// load of one group of four is one contiguous 512 B run.  Values are an 8/16-bit index into
+// a table of the operator's distinct doubles when it has at most 256/65,536 of them
+// (lossless; the table is staged in shared memory), else fp64: 4 + 1 B per entry for the
+// constant-coefficient Q1 stencil, 4 + 8 B with a per-cell coefficient.  Entries of a row
+// keep the reference's CSR order (linalg.hpp:12-22), which fixes the summation order.
 //
 // Arithmetic: every product and sum is rounded separately (__dmul_rn / __dadd_rn /
 // __dsub_rn / __ddiv_rn, never an FMA), reproducing the reference's x86-64 SSE2
 // evaluation of the same expressions, so Jacobi iterates match bit for bit.
 //
-// HBM behaviour: matrix values/columns are read exactly once per sweep with
-// streaming loads (evict-first: they are 12 B/nnz and never reused inside a sweep);
-// the x gather goes through the read-only path and stays L2-resident (the whole
-// finest x at 128^3 is 17 MB of a 126 MB L2).
+// HBM behaviour: the finest operator is streamed once per sweep with evict-first loads
+// (plus a row-start L2 prefetch of its groups); the operators of coarser levels that fit
+// L2 are read with the caching policy and stay resident across a cycle's sweeps; the x
+// gather goes through the read-only path and stays L2-resident (17 MB at 128^3; on levels
+// whose x outgrows L2 the colour-interleaved block schedule, RowMap, keeps it streaming
+// through L2 once per sweep).
 #pragma once
 
 #include <cstdint>
