@@ -34,6 +34,7 @@
 #include "pf_heat.cuh"
 #include "pf_kernels.cuh"
 #include "pf_nccl.hpp"
+#include "pf_sweep_dataflow.cuh"
 #include "pf_sweep_tma.cuh"
 #include "pf_runtime.hpp"
 
@@ -394,6 +395,70 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
 
 // Device layout of one subdomain level: own rows colour-major (stable in host order),
 // then every other row in host order; SELL-32 operator; P (rows of this level).
+// PF_SOR_DATAFLOW (default 1) / PF_SOR_DATAFLOW_MIN_ROWS (default 32768 own rows): the
+// coloured sweeps of such levels (2-8 colours) run as one dataflow launch per smoothing
+// phase (pf_sweep_dataflow.cuh) instead of one launch per colour.
+bool sor_dataflow_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_SOR_DATAFLOW");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+int64_t sor_dataflow_min_rows() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("PF_SOR_DATAFLOW_MIN_ROWS");
+    return e ? std::atoll(e) : int64_t(32768);
+  }();
+  return v;
+}
+
+// The task lists of the dataflow colour sweep: the neighbour reach w (in 256-row chunks)
+// from the own-row pattern, then for 1..4 sweeps per launch every (pass, chunk) in the
+// claim order t = k + (w + 1) n.
+void build_dataflow(const HostLevel& H, DevLevel& D, const std::vector<int32_t>& color, int32_t n_own) {
+  D.df = DevLevel::Dataflow{};
+  const int C = D.n_colors;
+  if (!sor_dataflow_enabled() || C < 2 || C > kDfMaxColors || n_own < sor_dataflow_min_rows()) return;
+  std::vector<int32_t> chunk(static_cast<size_t>(n_own));
+#pragma omp parallel for schedule(static)
+  for (int32_t i = 0; i < n_own; ++i)
+    chunk[static_cast<size_t>(i)] = (D.perm[i] - D.color_start[color[i]]) / kBlock;
+  int32_t w = 0;
+#pragma omp parallel for schedule(static) reduction(max : w)
+  for (int32_t i = 0; i < n_own; ++i)
+    for (int64_t e = H.rowptr[i]; e < H.rowptr[i + 1]; ++e) {
+      const int32_t j = H.cols[e];
+      if (j < n_own && color[j] != color[i]) w = std::max(w, std::abs(chunk[j] - chunk[i]));
+    }
+  DevLevel::Dataflow& F = D.df;
+  F.w = w;
+  F.kc.resize(static_cast<size_t>(C));
+  for (int c = 0; c < C; ++c) {
+    F.kc[c] = (D.color_start[c + 1] - D.color_start[c] + kBlock - 1) / kBlock;
+    F.kmax = std::max(F.kmax, F.kc[c]);
+  }
+  if (F.kmax >= (1 << kDfTaskBits)) return;
+  for (int S = 1; S <= 4; ++S) {
+    const int N = S * C;
+    std::vector<std::pair<int64_t, int32_t>> order;  // (t * 64 + n, word)
+    for (int n = 0; n < N; ++n)
+      for (int32_t k = 0; k < F.kc[n % C]; ++k)
+        order.push_back({(static_cast<int64_t>(k) + static_cast<int64_t>(w + 1) * n) * 64 + n, (n << kDfTaskBits) | k});
+    std::sort(order.begin(), order.end());
+    std::vector<int32_t> words(order.size());
+    for (size_t i = 0; i < order.size(); ++i) words[i] = order[i].second;
+    F.tasks[S - 1].upload(words);
+    F.n_tasks[S - 1] = static_cast<int32_t>(words.size());
+  }
+  F.flags.alloc(static_cast<int64_t>(4 * C) * F.kmax);
+  PF_CUDA(cudaMemset(F.flags.p, 0, sizeof(uint32_t) * static_cast<size_t>(F.flags.n)));
+  const uint32_t ctl[4] = {0, 1, 0, 0};  // next task, epoch (flags start at 0), ticket
+  F.ctl.alloc(4);
+  PF_CUDA(cudaMemcpy(F.ctl.p, ctl, sizeof ctl, cudaMemcpyHostToDevice));
+  F.on = true;
+}
+
 // PF_INTERLEAVE_MIN_BYTES (default 64 MB): levels whose x is at least this large run their
 // full-level Jacobi / residual passes with the colour-interleaved block schedule (0: every
 // level with 2-8 colours; a huge value: never).
@@ -498,6 +563,7 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
     for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
   }
   D.d_perm.upload(D.perm);
+  build_dataflow(H, D, color, n_own);
   // colour-interleaved block schedule when x outgrows L2 (RowMap, pf_types.hpp)
   D.rmap = RowMap{};
   D.rmap_grid = grid_for(n);
@@ -1330,6 +1396,34 @@ void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega
   });
 }
 
+// S sweeps of the coloured smoother on one subdomain as one dataflow launch
+// (pf_sweep_dataflow.cuh); false when the level has no dataflow plan for S.
+bool enq_dataflow(pf_hierarchy* h, DevLevel& D, int S, bool sor, double omega, double* x, const double* b) {
+  const auto& F = D.df;
+  if (!F.on || S < 1 || S > 4) return false;
+  DataflowView v{};
+  v.tasks = F.tasks[S - 1].p;
+  v.n_tasks = F.n_tasks[S - 1];
+  v.n_colors = D.n_colors;
+  v.w = F.w;
+  v.kmax = F.kmax;
+  for (int c = 0; c <= D.n_colors; ++c) v.cs[c] = D.color_start[c];
+  for (int c = 0; c < D.n_colors; ++c) v.kc[c] = F.kc[c];
+  v.flags = F.flags.p;
+  v.ctl = F.ctl.p;
+  auto launch = launcher(h);
+  vk_dispatch_rows(D.A, [&](auto V) {
+    constexpr int vk = decltype(V)::value;
+    auto kern = sor ? k_color_sweep_dataflow<true, vk> : k_color_sweep_dataflow<false, vk>;
+    static thread_local std::map<const void*, int> occ_cache;
+    int& occ = occ_cache[reinterpret_cast<const void*>(kern)];
+    if (!occ) PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0));
+    const int64_t grid = std::min<int64_t>(v.n_tasks, static_cast<int64_t>(std::max(occ, 1)) * sm_count(h->device));
+    launch(static_cast<unsigned>(grid), kBlock, kern, view(D.A), x, b, v, sor ? omega : 1.0);
+  });
+  return true;
+}
+
 // smooth (solvers.cpp:56-68) on x (primary buffer) with b.
 // first_done: the first Jacobi sweep already ran (k_jacobi_norm in the solve graph).
 // Returns true when the halo2 scatter that follows a smoothing phase in the cycle was
@@ -1384,6 +1478,21 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
         cur ^= 1;
       } else {
         const bool sor = sc.kind == PF_SMOOTHER_MULTICOLOR_SOR;
+        // one dataflow launch per smoothing phase (one subdomain, one process: the
+        // exchanges in between are empty) or per sweep (one subdomain per process)
+        if (h->n_sub == 1 && !h->colorwise && L.sub[0].df.on) {
+          DevLevel& D = L.sub[0];
+          if (h->world == 1) {
+            const int S = sc.sweeps * sc.local_sweeps;
+            if (S <= 4) {
+              if (sweep == 0 && local == 0) enq_dataflow(h, D, S, sor, sc.damping, bufs[cur] + D.offset, b + D.offset);
+              continue;
+            }
+          } else if (sc.local_sweeps <= 4) {
+            if (local == 0) enq_dataflow(h, D, sc.local_sweeps, sor, sc.damping, bufs[cur] + D.offset, b + D.offset);
+            continue;
+          }
+        }
         int max_colors = 0;
         for (DevLevel& D : L.sub) max_colors = std::max(max_colors, D.n_colors);
         for (int c = 0; c < max_colors; ++c) {
@@ -2787,7 +2896,7 @@ pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double*
       vk_dispatch_rows(D.A, [&](auto V) {
         launch(D.rmap_grid, kBlock, k_jacobi<decltype(V)::value>, view(D.A), src, dst, b, D.n_own, D.n, 0.8, D.rmap);
       });
-    } else {
+    } else if (!enq_dataflow(h, D, 1, kind == PF_SMOOTHER_MULTICOLOR_SOR, 1.2, x->cur(), b)) {
       for (int c = 0; c < D.n_colors; ++c)
         enq_color_sweep(h, D, c, true, kind == PF_SMOOTHER_MULTICOLOR_SOR ? 1.2 : 1.0, x->cur(), b);
     }

@@ -110,6 +110,16 @@ struct DevLevel {
   std::vector<int32_t> color_start;  // device rows, n_colors + 1 (own rows only)
   RowMap rmap{};                     // block schedule of the full-level Jacobi / residual passes
   unsigned rmap_grid = 0;            // their grid under rmap
+  // dataflow schedule of the coloured sweeps (pf_sweep_dataflow.cuh): tasks = 256-row
+  // chunks of one colour pass; lists for 1..kDfMaxPasses sweeps per launch
+  struct Dataflow {
+    bool on = false;
+    int32_t w = 0, kmax = 0;
+    std::vector<int32_t> kc;
+    std::array<DevBuf<int32_t>, 4> tasks;
+    std::array<int32_t, 4> n_tasks{};
+    DevBuf<uint32_t> flags, ctl;
+  } df;
   std::vector<int32_t> perm;         // host index -> device index
   DevBuf<int32_t> d_perm;
   DevSell A;
