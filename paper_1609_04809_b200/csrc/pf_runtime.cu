@@ -57,6 +57,13 @@ double wall_now() {
 
 inline unsigned grid_for(int64_t n) { return static_cast<unsigned>((n + kBlock - 1) / kBlock); }
 
+int sm_count(int device) {
+  static int cached[64] = {};
+  if (device < 0 || device >= 64) device = 0;
+  if (!cached[device]) PF_CUDA(cudaDeviceGetAttribute(&cached[device], cudaDevAttrMultiProcessorCount, device));
+  return cached[device];
+}
+
 [[noreturn]] void invalid(const std::string& m) { throw Error(PF_ERR_INVALID_ARGUMENT, m); }
 
 // PF_TRACE=1: one stderr line per major host step (debugging integrations).
@@ -395,13 +402,14 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
 
 // Device layout of one subdomain level: own rows colour-major (stable in host order),
 // then every other row in host order; SELL-32 operator; P (rows of this level).
-// PF_SOR_DATAFLOW (default 1) / PF_SOR_DATAFLOW_MIN_ROWS (default 32768 own rows): the
+// PF_SOR_DATAFLOW (default 0: measured slower at C2, profiles/r02_sweep_experiments.md) /
+// PF_SOR_DATAFLOW_MIN_ROWS (default 32768 own rows): the
 // coloured sweeps of such levels (2-8 colours) run as one dataflow launch per smoothing
 // phase (pf_sweep_dataflow.cuh) instead of one launch per colour.
 bool sor_dataflow_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PF_SOR_DATAFLOW");
-    return !(e && std::atoi(e) == 0);
+    return e && std::atoi(e) != 0;
   }();
   return on;
 }
@@ -439,12 +447,24 @@ void build_dataflow(const HostLevel& H, DevLevel& D, const std::vector<int32_t>&
     F.kmax = std::max(F.kmax, F.kc[c]);
   }
   if (F.kmax >= (1 << kDfTaskBits)) return;
+  // Claim order t = k + M n.  A task's dependency (pass n - 1, chunk k + w) is claimed
+  // M - w slots of t earlier; with R tasks resident at once the claimed-but-unfinished
+  // window spans about R M / K slots of t, so M (1 - R / K) > w + 1 keeps dependencies out
+  // of the window (no stalls) while the passes in flight stay within a band of the lattice
+  // (x stays in L2).  Twice the minimum; passes in order (M = K) when R is most of K.
+  int dev = 0;
+  PF_CUDA(cudaGetDevice(&dev));
+  const double R = 4.0 * sm_count(dev);  // resident 256-row blocks (PF_SOR_MINB = 4)
+  int64_t M = F.kmax;
+  if (R < 0.5 * F.kmax) M = std::min<int64_t>(F.kmax, 2 * static_cast<int64_t>(std::ceil((w + 1) / (1.0 - R / F.kmax))));
+  if (const char* e = std::getenv("PF_SOR_DF_TILT")) M = std::max<int64_t>(w + 1, std::atoll(e));
+  F.tilt = M;
   for (int S = 1; S <= 4; ++S) {
     const int N = S * C;
     std::vector<std::pair<int64_t, int32_t>> order;  // (t * 64 + n, word)
     for (int n = 0; n < N; ++n)
       for (int32_t k = 0; k < F.kc[n % C]; ++k)
-        order.push_back({(static_cast<int64_t>(k) + static_cast<int64_t>(w + 1) * n) * 64 + n, (n << kDfTaskBits) | k});
+        order.push_back({(static_cast<int64_t>(k) + M * n) * 64 + n, (n << kDfTaskBits) | k});
     std::sort(order.begin(), order.end());
     std::vector<int32_t> words(order.size());
     for (size_t i = 0; i < order.size(); ++i) words[i] = order[i].second;
@@ -1337,12 +1357,6 @@ int sor_tma_cfg() {  // experiment: 0 = 8 warps x 2 stages, 1 = 4 x 4, 2 = 8 x 3
     return e ? std::atoi(e) : 0;
   }();
   return v;
-}
-int sm_count(int device) {
-  static int cached[64] = {};
-  if (device < 0 || device >= 64) device = 0;
-  if (!cached[device]) PF_CUDA(cudaDeviceGetAttribute(&cached[device], cudaDevAttrMultiProcessorCount, device));
-  return cached[device];
 }
 
 void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega, double* x, const double* b) {

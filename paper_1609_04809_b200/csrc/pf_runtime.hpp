@@ -115,6 +115,7 @@ struct DevLevel {
   struct Dataflow {
     bool on = false;
     int32_t w = 0, kmax = 0;
+    int64_t tilt = 0;  // claim order t = k + tilt * pass
     std::vector<int32_t> kc;
     std::array<DevBuf<int32_t>, 4> tasks;
     std::array<int32_t, 4> n_tasks{};

@@ -37,10 +37,10 @@ VARIANTS = {
     # the colour-interleaved block schedule (RowMap) of the Jacobi / residual passes on every
     # level with 2-8 colours (default: only where x exceeds 64 MB)
     "interleave_everywhere": {"PF_INTERLEAVE_MIN_BYTES": "0"},
-    # the dataflow colour sweep (one launch per smoothing phase) on every level with 2-8
-    # colours (default: >= 32k own rows), and the per-colour launches everywhere
-    "dataflow_everywhere": {"PF_SOR_DATAFLOW_MIN_ROWS": "0"},
-    "dataflow_off": {"PF_SOR_DATAFLOW": "0"},
+    # the opt-in dataflow colour sweep (one launch per smoothing phase) on every level with
+    # 2-8 colours, in the default claim order and in a steep wavefront
+    "dataflow_everywhere": {"PF_SOR_DATAFLOW": "1", "PF_SOR_DATAFLOW_MIN_ROWS": "0"},
+    "dataflow_everywhere_ordered": {"PF_SOR_DATAFLOW": "1", "PF_SOR_DATAFLOW_MIN_ROWS": "0", "PF_SOR_DF_TILT": "17"},
 }
 
 
