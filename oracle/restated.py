@@ -77,6 +77,24 @@ class Oracle:
         if colorwise:
             self._check(L.orc_set_colorwise(self._h, 1))
 
+    @classmethod
+    def from_level_descs(cls, descs, colorwise=False):
+        """Oracle over raw pf_level_desc structs (descs[s][l]; e.g. pointers into a native
+        setup, StructuredSetup.level_desc): no numpy copy of large levels."""
+        self = cls.__new__(cls)
+        L = lib()
+        self.K, self.n_levels = len(descs), len(descs[0])
+        self.sizes = [[int(d.n_dofs) for d in sub] for sub in descs]
+        self._h = C.c_void_p()
+        self._check(L.orc_create(self.n_levels, self.K, C.byref(self._h)))
+        for s, sub in enumerate(descs):
+            for l, d in enumerate(sub):
+                self._check(L.orc_set_level(self._h, l, s, C.byref(d)))
+        self._check(L.orc_finalize(self._h))
+        if colorwise:
+            self._check(L.orc_set_colorwise(self._h, 1))
+        return self
+
     @staticmethod
     def _check(rc):
         if rc:
