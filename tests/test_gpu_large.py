@@ -6,6 +6,7 @@ level data, bit for bit: damped Jacobi, multicolour SOR, and the residual norm.
 The oracle reads the native setup's level arrays in place (Oracle.from_level_descs), then
 the hierarchy takes them over (Hierarchy.from_setups), so the host holds one copy plus the
 oracle's (~100 GB peak on the 196 GB GPU box)."""
+import ctypes
 import os
 
 import numpy as np
@@ -23,7 +24,8 @@ def test_sweeps_above_2_31_entries_bit_exact(cuda):
     L = 7
     s = StructuredSetup(3, 7, L, 1, 0, materialize=False)
     d = s.level_desc(L - 1)
-    n, z = int(d.n_dofs), int(d.row_offsets[d.n_dofs])
+    n = int(d.n_dofs)
+    z = int(ctypes.cast(d.row_offsets, ctypes.POINTER(ctypes.c_int64))[n])
     assert z > 2 ** 31
     rng = np.random.default_rng(7)
     x0 = rng.standard_normal(n)
