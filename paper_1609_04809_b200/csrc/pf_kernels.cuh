@@ -196,25 +196,46 @@ __device__ __forceinline__ void offdiag_group(const int32_t c[4], const double v
   }
 }
 
-template <bool kReadOnlyX, bool kRes = false, int kVK = -1, int kGroups = kChunkGroups, int kPf = 0>
-__device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, const double* x,
-                                            double& acc, double& diag, double* res = nullptr,
-                                            double x_row = 0.0) {
-  // kRes: *res (starting at b_r) also subtracts every product in stored order, the
-  // diagonal included — the reference's residual_norm row (linalg.cpp:66-70) bit for bit.
-  const int64_t base = sell_row_base(A.slice_ptr, row);
-  const int len = A.row_len[row];
-  row_prefetch<kVK, kPf>(A, base, len);
+// The x-independent start of a row: its SELL base, length and first group of columns and
+// values (plus the L2 prefetch of the rest).  The operator never changes after upload, so
+// the colour sweep issues this BEFORE griddepcontrol.wait: under programmatic dependent
+// launch those loads overlap the previous colour's tail instead of opening this one's
+// dependency chain (C2 SOR solve 10.63 -> 10.21 ms; the Jacobi sweep, whose predecessor
+// is itself bandwidth-heavy, loses with it: 75.0 -> 79.4 us, so it keeps the plain order).
+struct RowHead {
+  int64_t base;
+  int len;
+  int32_t c[4];
+  double v[4];
+};
+template <int kVK, int kPf = 0>
+__device__ __forceinline__ void row_head(const SellView& A, int32_t row, RowHead& h) {
+  h.base = sell_row_base(A.slice_ptr, row);
+  h.len = A.row_len[row];
+  row_prefetch<kVK, kPf>(A, h.base, h.len);
+  if (h.len > 0) sell_group<kVK>(A, h.base, h.c, h.v);
+}
+
+// The rest of row_offdiag from a RowHead.
+template <bool kReadOnlyX, bool kRes = false, int kVK = -1>
+__device__ __forceinline__ void row_offdiag_from(const SellView& A, const RowHead& h, int32_t row, const double* x,
+                                                 double& acc, double& diag, double* res = nullptr,
+                                                 double x_row = 0.0) {
   double r = kRes ? *res : 0.0;
+  const int len = h.len;
   if (len > 0) {
     int32_t c[4];
     double v[4];
-    sell_group<kVK>(A, base, c, v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      c[k] = h.c[k];
+      v[k] = h.v[k];
+    }
     int j = 0;
     for (; j + 4 < len; j += 4) {
       int32_t cn[4];
       double vn[4];
-      sell_group<kVK>(A, sell_entry(base, j + 4), cn, vn);
+      sell_group<kVK>(A, sell_entry(h.base, j + 4), cn, vn);
       offdiag_group<kReadOnlyX, kRes>(c, v, 4, row, x, x_row, acc, diag, r);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -225,6 +246,17 @@ __device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, cons
     offdiag_group<kReadOnlyX, kRes>(c, v, len - j, row, x, x_row, acc, diag, r);
   }
   if (kRes) *res = r;
+}
+
+template <bool kReadOnlyX, bool kRes = false, int kVK = -1, int kGroups = kChunkGroups, int kPf = 0>
+__device__ __forceinline__ void row_offdiag(const SellView& A, int32_t row, const double* x,
+                                            double& acc, double& diag, double* res = nullptr,
+                                            double x_row = 0.0) {
+  // kRes: *res (starting at b_r) also subtracts every product in stored order, the
+  // diagonal included — the reference's residual_norm row (linalg.cpp:66-70) bit for bit.
+  RowHead h;
+  row_head<kVK, kPf>(A, row, h);
+  row_offdiag_from<kReadOnlyX, kRes, kVK>(A, h, row, x, acc, diag, res, x_row);
 }
 
 // acc := acc op sum_c a_rc x_c over all entries in stored order.
@@ -382,13 +414,15 @@ __global__ void __launch_bounds__(kBlock, PF_SOR_MINB) k_color_sweep(SellView A,
                                                         const double* __restrict__ b, int32_t row0,
                                                         int32_t row1, double omega) {
   vtab_stage<kVK>(A);
-  PF_PDL_ENTRY();
   const int32_t row = row0 + blockIdx.x * kBlock + threadIdx.x;
+  RowHead hd;
+  if (row < row1) row_head<kVK>(A, row, hd);  // operator only: before the wait
+  PF_PDL_ENTRY();
   if (row >= row1) return;
   double acc = b[row], diag = 0.0;
   // Other colours are read-only during this launch and this row's own entry is
   // skipped by row_offdiag, so the read-only path is safe for the gather.
-  row_offdiag<true, false, kVK, kSorChunkGroups>(A, row, x, acc, diag);
+  row_offdiag_from<true, false, kVK>(A, hd, row, x, acc, diag);
   if (kSor)
     x[row] = __dadd_rn(__dmul_rn(1.0 - omega, x[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
   else
