@@ -273,6 +273,47 @@ __device__ __forceinline__ void dot_group(const int32_t c[4], const double v[4],
     if (k < n) acc = kSubtract ? __dsub_rn(acc, __dmul_rn(v[k], xv[k])) : __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
 }
 
+// The rest of row_dot from a RowHead (row_head issued before griddepcontrol.wait).
+template <bool kSubtract, bool kReadOnlyX = true, int kVK = -1>
+__device__ __forceinline__ double row_dot_from(const SellView& A, const RowHead& h, const double* __restrict__ x,
+                                               double acc) {
+  const int len = h.len;
+  if (len > 0) {
+    int32_t c[4];
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      c[k] = h.c[k];
+      v[k] = h.v[k];
+    }
+    int j = 0;
+    for (; j + 4 < len; j += 4) {
+      int32_t cn[4];
+      double vn[4];
+      sell_group<kVK>(A, sell_entry(h.base, j + 4), cn, vn);
+      dot_group<kSubtract, kReadOnlyX>(c, v, 4, x, acc);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        c[k] = cn[k];
+        v[k] = vn[k];
+      }
+    }
+    dot_group<kSubtract, kReadOnlyX>(c, v, len - j, x, acc);
+  }
+  return acc;
+}
+
+// Which row kernels issue their operator-only row start before griddepcontrol.wait
+// (PF_HEAD_EARLY, compile time): 0 the colour sweeps only, 1 also the kernels of the cached
+// (coarser, L2-resident) operators, 2 every row kernel.
+#ifndef PF_HEAD_EARLY
+#define PF_HEAD_EARLY 1
+#endif
+template <int kVK>
+constexpr bool head_early() {
+  return PF_HEAD_EARLY >= 2 || (PF_HEAD_EARLY == 1 && vk_cached<kVK>());
+}
+
 template <bool kSubtract, bool kReadOnlyX = true, int kVK = -1, int kGroups = kChunkGroups, int kPf = kPrefetch>
 __device__ __forceinline__ double row_dot(const SellView& A, int32_t row, const double* __restrict__ x,
                                           double acc) {
@@ -310,8 +351,11 @@ __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_JAC_MINB)) k_jacobi(S
                                                    const double* __restrict__ b, int32_t n_own,
                                                    int32_t n, double omega, RowMap map) {
   vtab_stage<kVK>(A);
-  PF_PDL_ENTRY();
   const int32_t row = map_row(map, blockIdx.x, threadIdx.x, n_own);
+  RowHead hd;
+  if constexpr (head_early<kVK>())
+    if (row >= 0 && row < n_own) row_head<kVK, kPrefetch>(A, row, hd);
+  PF_PDL_ENTRY();
   if (row < 0 || row >= n) return;
   const double xo = x_old[row];
   if (row >= n_own) {
@@ -319,7 +363,10 @@ __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_JAC_MINB)) k_jacobi(S
     return;
   }
   double acc = b[row], diag = 0.0;
-  row_offdiag<true, false, kVK, kChunkGroups, kPrefetch>(A, row, x_old, acc, diag);
+  if constexpr (head_early<kVK>())
+    row_offdiag_from<true, false, kVK>(A, hd, row, x_old, acc, diag);
+  else
+    row_offdiag<true, false, kVK, kChunkGroups, kPrefetch>(A, row, x_old, acc, diag);
   x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
 }
 
@@ -496,10 +543,16 @@ __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_residual
                                                      double* __restrict__ r, int32_t n, int32_t n_own,
                                                      RowMap map) {
   vtab_stage<kVK>(A);
-  PF_PDL_ENTRY();
   const int32_t row = map_row(map, blockIdx.x, threadIdx.x, n_own);
+  RowHead hd;
+  if constexpr (head_early<kVK>())
+    if (row >= 0 && row < n) row_head<kVK, kPrefetch>(A, row, hd);
+  PF_PDL_ENTRY();
   if (row < 0 || row >= n) return;
-  r[row] = __dsub_rn(b[row], row_dot<false, true, kVK>(A, row, x, 0.0));
+  if constexpr (head_early<kVK>())
+    r[row] = __dsub_rn(b[row], row_dot_from<false, true, kVK>(A, hd, x, 0.0));
+  else
+    r[row] = __dsub_rn(b[row], row_dot<false, true, kVK>(A, row, x, 0.0));
 }
 
 // y = A x on every row (linalg.cpp:45-57).
@@ -635,10 +688,17 @@ template <int kVK>
 __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_prolong_add(SellView P, const double* __restrict__ xc,
                                                         double* __restrict__ xf, int32_t n_f, int add) {
   vtab_stage<kVK>(P);
-  PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  RowHead hd;
+  if constexpr (head_early<kVK>())
+    if (row < n_f) row_head<kVK, kPrefetch>(P, row, hd);
+  PF_PDL_ENTRY();
   if (row >= n_f) return;
-  const double acc = row_dot<false, true, kVK>(P, row, xc, 0.0);
+  double acc;
+  if constexpr (head_early<kVK>())
+    acc = row_dot_from<false, true, kVK>(P, hd, xc, 0.0);
+  else
+    acc = row_dot<false, true, kVK>(P, row, xc, 0.0);
   xf[row] = add ? __dadd_rn(xf[row], acc) : acc;
 }
 
@@ -655,10 +715,17 @@ __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_restrict
                                                      const uint8_t* __restrict__ is_dir_c,
                                                      int32_t n_c, int zero_dirichlet) {
   vtab_stage<kVK>(R);
-  PF_PDL_ENTRY();
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  RowHead hd;
+  if constexpr (head_early<kVK>())
+    if (row < n_c) row_head<kVK, kPrefetch>(R, row, hd);
+  PF_PDL_ENTRY();
   if (row >= n_c) return;
-  const double acc = row_dot<false, true, kVK>(R, row, rf, 0.0);
+  double acc;
+  if constexpr (head_early<kVK>())
+    acc = row_dot_from<false, true, kVK>(R, hd, rf, 0.0);
+  else
+    acc = row_dot<false, true, kVK>(R, row, rf, 0.0);
   bc[row] = (zero_dirichlet && is_dir_c[row]) ? 0.0 : acc;
   if (xc) xc[row] = 0.0;
 }
