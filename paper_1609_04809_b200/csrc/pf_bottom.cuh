@@ -57,6 +57,24 @@ struct BotLevel {
   int32_t acc_n;
 };
 
+// Shared-memory staging of the block levels (levels 0..hs <= block_top, which block 0 runs
+// alone).  Their operators (SELL-32x4 with 8-bit value indices where the level has at
+// most 256 distinct values), colour ranges, Dirichlet flags and exchange plans are copied
+// at finalize into one global blob; the descriptor points into the blob.  At the start of
+// the block section block 0 copies the blob into shared memory, points its own copy of the
+// descriptor at it and gives the level vectors (x, xa, b, r) shared-memory slots, so every
+// dependent load of the 70-odd phases of the tiny levels is a shared-memory access instead
+// of an L2 round trip.  The blob is an exact copy, so the unstaged path (the same
+// descriptor without relocation) computes the same values from global memory.
+struct BotStage {
+  const unsigned char* blob;
+  int64_t blob_bytes;   // multiple of 16
+  int64_t arena_bytes;  // blob + the staged levels' vectors
+  int64_t smem_off;     // arena offset in the kernel's dynamic shared memory
+  int hs;               // staged levels 0..hs (-1: none)
+  int64_t vec_off[kBotMaxLevels][4];  // arena offsets of x, xa, b, r
+};
+
 struct BotDesc {
   int n_sub;
   int n_levels;   // Lc + 1
@@ -66,6 +84,7 @@ struct BotDesc {
   double* coarse_stats;
   BotLevel lev[kBotMaxLevels];
   BotSub sub[kBotMaxLevels][kBotMaxSubs];
+  BotStage stage;
 };
 
 struct BotCfg {
@@ -86,17 +105,27 @@ __device__ __forceinline__ void bot_row_offdiag(const SellView& A, int32_t row, 
                                                 double& diag) {
   const int64_t base = sell_row_base(A.slice_ptr, row);
   const int len = A.row_len[row];
-  if (len > kBotChunk) {  // long rows: the bandwidth kernel's loop
-    row_offdiag<false, false, 0>(A, row, x, acc, diag);
+  if (len > kBotChunk) {  // long rows (never staged): the bandwidth kernel's loop
+    row_offdiag<false, false, -1>(A, row, x, acc, diag);
     return;
   }
   int32_t c[kBotChunk];
   double v[kBotChunk], xv[kBotChunk];
+  if (A.vkind == 1) {  // 8-bit value index (the staged levels)
+    const unsigned char* vi = static_cast<const unsigned char*>(A.vidx);
 #pragma unroll
-  for (int k = 0; k < kBotChunk; ++k) {
-    const int64_t e = sell_entry(base, k < len ? k : 0);
-    c[k] = A.cols[e];
-    v[k] = A.vals[e];  // bottom levels are never index-encoded (fill_bottom)
+    for (int k = 0; k < kBotChunk; ++k) {
+      const int64_t e = sell_entry(base, k < len ? k : 0);
+      c[k] = A.cols[e];
+      v[k] = A.table[vi[e]];
+    }
+  } else {  // fp64 (decoded copies of the unstaged levels)
+#pragma unroll
+    for (int k = 0; k < kBotChunk; ++k) {
+      const int64_t e = sell_entry(base, k < len ? k : 0);
+      c[k] = A.cols[e];
+      v[k] = A.vals[e];
+    }
   }
 #pragma unroll
   for (int k = 0; k < kBotChunk; ++k) xv[k] = x[c[k]];
@@ -112,14 +141,93 @@ __device__ __forceinline__ void bot_row_offdiag(const SellView& A, int32_t row, 
 
 // (measured: the 28-wide unrolled form that helps the sweeps makes the residual,
 // restriction and prolongation phases 2-3x slower; they keep the bandwidth loop)
+// A staged operator (shared memory: generic loads, latency ~30 cycles) takes a plain
+// entry loop; the global ones the bandwidth kernel's group loop.
 __device__ __forceinline__ double bot_row_dot(const SellView& A, int32_t row, const double* x, double acc) {
-  return row_dot<false, false, 0>(A, row, x, acc);
+  if (!__isShared(A.cols)) return row_dot<false, false, -1>(A, row, x, acc);
+  const int64_t base = sell_row_base(A.slice_ptr, row);
+  const int len = A.row_len[row];
+  if (len == 0) return acc;  // (an empty row may sit in an all-empty slice: no entry to read)
+  if (len <= kBotChunk) {  // every load of the row first, then the products in stored order
+    int32_t c[kBotChunk];
+    double v[kBotChunk], xv[kBotChunk];
+    const unsigned char* vi = static_cast<const unsigned char*>(A.vidx);
+#pragma unroll
+    for (int k = 0; k < kBotChunk; ++k) {
+      const int64_t e = sell_entry(base, k < len ? k : 0);
+      c[k] = A.cols[e];
+      v[k] = A.vkind == 1 ? A.table[vi[e]] : A.vals[e];
+    }
+#pragma unroll
+    for (int k = 0; k < kBotChunk; ++k) xv[k] = x[c[k]];
+#pragma unroll
+    for (int k = 0; k < kBotChunk; ++k)
+      if (k < len) acc = __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
+    return acc;
+  }
+  if (A.vkind == 1) {
+    const unsigned char* vi = static_cast<const unsigned char*>(A.vidx);
+    for (int j = 0; j < len; ++j) {
+      const int64_t e = sell_entry(base, j);
+      acc = __dadd_rn(acc, __dmul_rn(A.table[vi[e]], x[A.cols[e]]));
+    }
+  } else {
+    for (int j = 0; j < len; ++j) {
+      const int64_t e = sell_entry(base, j);
+      acc = __dadd_rn(acc, __dmul_rn(A.vals[e], x[A.cols[e]]));
+    }
+  }
+  return acc;
+}
+
+// Point block 0's descriptor copy at the staged arena (pointers into the blob move to the
+// arena; the staged levels' vectors get their arena slots).
+template <class P>
+__device__ __forceinline__ void bot_reloc(P& p, const unsigned char* lo, const unsigned char* hi,
+                                          unsigned char* arena) {
+  const unsigned char* q = reinterpret_cast<const unsigned char*>(p);
+  if (q >= lo && q < hi) p = reinterpret_cast<P>(arena + (q - lo));
+}
+__device__ __forceinline__ void bot_reloc_view(SellView& A, const unsigned char* lo, const unsigned char* hi,
+                                               unsigned char* arena) {
+  bot_reloc(A.vals, lo, hi, arena);
+  bot_reloc(A.cols, lo, hi, arena);
+  bot_reloc(A.slice_ptr, lo, hi, arena);
+  bot_reloc(A.row_len, lo, hi, arena);
+  bot_reloc(A.vidx, lo, hi, arena);
+  bot_reloc(A.table, lo, hi, arena);
+}
+__device__ void bot_relocate(BotDesc& D, unsigned char* arena) {
+  const unsigned char* lo = D.stage.blob;
+  const unsigned char* hi = lo + D.stage.blob_bytes;
+  for (int l = 0; l <= D.stage.hs; ++l) {
+    BotLevel& L = D.lev[l];
+    L.x = reinterpret_cast<double*>(arena + D.stage.vec_off[l][0]);
+    L.xa = reinterpret_cast<double*>(arena + D.stage.vec_off[l][1]);
+    L.b = reinterpret_cast<double*>(arena + D.stage.vec_off[l][2]);
+    L.r = reinterpret_cast<double*>(arena + D.stage.vec_off[l][3]);
+    for (BotPlan* pl : {&L.ms, &L.h1, &L.h2}) {
+      bot_reloc(pl->dst, lo, hi, arena);
+      bot_reloc(pl->src, lo, hi, arena);
+    }
+    bot_reloc(L.acc_off, lo, hi, arena);
+    bot_reloc(L.acc_src, lo, hi, arena);
+    bot_reloc(L.acc_dst, lo, hi, arena);
+    for (int s = 0; s < D.n_sub; ++s) {
+      BotSub& S = D.sub[l][s];
+      bot_reloc_view(S.A, lo, hi, arena);
+      bot_reloc_view(S.P, lo, hi, arena);
+      bot_reloc_view(S.R, lo, hi, arena);
+      bot_reloc(S.color_start, lo, hi, arena);
+      bot_reloc(S.is_dir, lo, hi, arena);
+    }
+  }
 }
 
 // grid barrier + optional phase timestamp (block 0, thread 0)
 __device__ __forceinline__ void bsync(cg::grid_group& g, const BotDesc& D, int& phase) {
   g.sync();
-  if (D.stamps && blockIdx.x == 0 && threadIdx.x == 0 && phase < 255) {
+  if (D.stamps && blockIdx.x == 0 && threadIdx.x == 0 && phase < 127) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     D.stamps[++phase] = t;
@@ -135,7 +243,15 @@ struct GridTeam {
 };
 struct BlockTeam {
   int64_t t, stride;
-  __device__ void sync(const BotDesc&, int&) { __syncthreads(); }
+  __device__ void sync(const BotDesc& D, int& ph) {
+    __syncthreads();
+    // PF_BOTTOM_PROFILE: block-phase timestamps in stamps[128..254]
+    if (D.stamps && t == 0 && ph < 126) {
+      unsigned long long ts;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+      D.stamps[128 + ++ph] = ts;
+    }
+  }
 };
 
 __device__ __forceinline__ int bot_find(const BotDesc& D, int l, int32_t row) {
@@ -148,15 +264,16 @@ __device__ __forceinline__ void bot_copy_plan(const BotPlan& P, double* v, int64
   for (int64_t i = t; i < P.n; i += stride) v[P.dst[i]] = v[P.src[i]];
 }
 
-template <class Team>
+template <class Team, int kKind = -1>  // kKind: the smoother when known at compile time
 __device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps, Team& T, int& ph) {
+  const int kind = kKind >= 0 ? kKind : c.kind;
   const int64_t t = T.t, stride = T.stride;
   const BotLevel& L = D.lev[l];
   double* bufs[2] = {L.x, L.xa};
   int cur = 0;
   for (int sw = 0; sw < sweeps; ++sw) {
     for (int loc = 0; loc < c.local_sweeps; ++loc) {
-      if (c.kind == 0) {  // damped Jacobi, ping-pong (k_jacobi)
+      if (kind == 0) {  // damped Jacobi, ping-pong (k_jacobi)
         const double* src = bufs[cur];
         double* dst = bufs[cur ^ 1];
         for (int64_t r = t; r < L.total; r += stride) {
@@ -174,7 +291,7 @@ __device__ void bot_smooth(const BotDesc& D, int l, const BotCfg& c, int sweeps,
         cur ^= 1;
         T.sync(D, ph);
       } else {  // coloured GS / SOR, in place (k_color_sweep)
-        const bool sor = c.kind == 2;
+        const bool sor = kind == 2;
         double* x = bufs[cur];
         for (int col = 0; col < L.max_colors; ++col) {
           for (int s = 0; s < D.n_sub; ++s) {
@@ -244,11 +361,11 @@ __device__ void bot_accumulate_scatter(const BotDesc& D, int l, double* v, Team&
 
 // Descending half of cycle(l) (multigrid.cpp:160-179): pre-smooth, halo2, residual,
 // restriction to l-1 (Dirichlet zeroed, coarse x = 0), master/slave accumulate on l-1.
-template <class Team>
+template <class Team, int kKind = -1>
 __device__ void bot_descend(const BotDesc& D, int l, const BotCfg& c, Team& T, int& ph) {
   const int64_t t = T.t, stride = T.stride;
   const BotLevel& L = D.lev[l];
-  bot_smooth(D, l, c, c.pre, T, ph);
+  bot_smooth<Team, kKind>(D, l, c, c.pre, T, ph);
   if (L.h2.n) {
     bot_copy_plan(L.h2, L.x, t, stride);
     T.sync(D, ph);
@@ -276,7 +393,7 @@ __device__ void bot_descend(const BotDesc& D, int l, const BotCfg& c, Team& T, i
 }
 
 // Ascending half of cycle(l) (multigrid.cpp:183-189): x += P x_c, post-smooth, halo2.
-template <class Team>
+template <class Team, int kKind = -1>
 __device__ void bot_ascend(const BotDesc& D, int l, const BotCfg& c, Team& T, int& ph) {
   const int64_t t = T.t, stride = T.stride;
   const BotLevel& L = D.lev[l];
@@ -290,7 +407,7 @@ __device__ void bot_ascend(const BotDesc& D, int l, const BotCfg& c, Team& T, in
     L.x[r] = __dadd_rn(L.x[r], acc);
   }
   T.sync(D, ph);
-  bot_smooth(D, l, c, c.post, T, ph);
+  bot_smooth<Team, kKind>(D, l, c, c.post, T, ph);
   if (L.h2.n) {
     bot_copy_plan(L.h2, L.x, t, stride);
     T.sync(D, ph);
@@ -309,6 +426,43 @@ __device__ void bot_coarse(const BotDesc& D, const BotCfg& c, Team& T, int& ph, 
     bot_copy_plan(L0.h2, L0.x, T.t, T.stride);
     T.sync(D, ph);
   }
+}
+
+// Block 0 (every thread): copy the staged blob into the arena and point block 0's descriptor
+// at it (no-op unless levels 0..bt are staged).  stage_in_vectors then moves the interface
+// level bt's b and x in (after griddepcontrol.wait / the grid barrier that produced them),
+// stage_out its x back to global memory at the end of the block section.
+struct BotIo {
+  double* gx;        // level bt's x / b in global memory
+  const double* gb;
+  int32_t n;
+  bool staged, io;   // levels 0..bt staged; bt itself staged (interface copies needed)
+};
+__device__ BotIo bot_stage_operators(BotDesc& DB, unsigned char* smem_b, int bt) {
+  BotIo io{DB.lev[bt].x, DB.lev[bt].b, DB.lev[bt].total, DB.stage.hs >= 0 && bt == DB.block_top, false};
+  io.io = io.staged && DB.stage.hs == bt;
+  if (!io.staged) return io;
+  unsigned char* arena = smem_b + DB.stage.smem_off;
+  __syncthreads();  // everyone has read the global interface pointers
+  const int4* src = reinterpret_cast<const int4*>(DB.stage.blob);
+  int4* dst = reinterpret_cast<int4*>(arena);
+  for (int64_t i = threadIdx.x; i < DB.stage.blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
+  if (threadIdx.x == 0) bot_relocate(DB, arena);
+  __syncthreads();
+  return io;
+}
+__device__ void bot_stage_in_vectors(BotDesc& DB, const BotIo& io, int bt) {
+  if (!io.io) return;
+  for (int32_t i = threadIdx.x; i < io.n; i += blockDim.x) {
+    DB.lev[bt].b[i] = io.gb[i];
+    DB.lev[bt].x[i] = io.gx[i];
+  }
+  __syncthreads();
+}
+__device__ void bot_stage_out(BotDesc& DB, const BotIo& io, int bt) {
+  if (!io.io) return;
+  __syncthreads();
+  for (int32_t i = threadIdx.x; i < io.n; i += blockDim.x) io.gx[i] = DB.lev[bt].x[i];
 }
 
 // cycle(Lc) (multigrid.cpp:150-190) on levels 0..Lc.  On entry lev[Lc].b holds the
@@ -344,11 +498,20 @@ __global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __restrict_
   for (int l = top; l > bt && l >= 1; --l) bot_descend(D, l, c, G, ph);
   if (bt >= 0) {
     if (blockIdx.x == 0) {
+      BotDesc& DB = *reinterpret_cast<BotDesc*>(smem_b);  // block 0's own copy
+      const BotIo io = bot_stage_operators(DB, smem_b, bt);
+      bot_stage_in_vectors(DB, io, bt);
       BlockTeam B{threadIdx.x, blockDim.x};
       int bph = 0;
+      if (D.stamps && threadIdx.x == 0) {
+        unsigned long long ts;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+        D.stamps[128] = ts;
+      }
       for (int l = bt; l >= 1; --l) bot_descend(D, l, c, B, bph);
       bot_coarse(D, c, B, bph, smem_coarse);
       for (int l = 1; l <= bt; ++l) bot_ascend(D, l, c, B, bph);
+      bot_stage_out(DB, io, bt);
     }
     G.sync(D, ph);
   } else {
@@ -356,6 +519,42 @@ __global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __restrict_
   }
   for (int l = (bt >= 0 ? bt + 1 : 1); l <= top; ++l) bot_ascend(D, l, c, G, ph);
   if (D.stamps && G.t == 0) D.stamps[255] = static_cast<unsigned long long>(ph);
+}
+
+// Every bottom level staged (BotDesc::stage.hs == top == block_top): the whole bottom
+// cycle in ONE block, with the smoother known at compile time — a fraction of k_bottom's
+// code (no grid-team paths), launched as an ordinary PDL-chained kernel of one block.  The
+// descriptor and the staged operators are copied before griddepcontrol.wait (immutable),
+// the top level's b and x after it.
+template <int kKind>
+__global__ void __launch_bounds__(kBlock, 1) k_bottom_block(const BotDesc* __restrict__ Dp, BotCfg c,
+                                                            int accumulate_top) {
+  extern __shared__ __align__(16) unsigned char smem_b[];
+  {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(Dp);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(smem_b);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(BotDesc) / 8); i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+  }
+  BotDesc& DB = *reinterpret_cast<BotDesc*>(smem_b);
+  const int top = DB.n_levels - 1;
+  const BotIo io = bot_stage_operators(DB, smem_b, top);
+  PF_PDL_ENTRY();
+  bot_stage_in_vectors(DB, io, top);
+  const BotDesc& D = DB;
+  unsigned char* smem_coarse = smem_b + ((sizeof(BotDesc) + 15) / 16) * 16;
+  BlockTeam B{threadIdx.x, blockDim.x};
+  int ph = 0;
+  if (D.stamps && threadIdx.x == 0) {
+    unsigned long long ts;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+    D.stamps[128] = ts;
+  }
+  if (accumulate_top) bot_accumulate_scatter(D, top, D.lev[top].b, B, ph);
+  for (int l = top; l >= 1; --l) bot_descend<BlockTeam, kKind>(D, l, c, B, ph);
+  bot_coarse(D, c, B, ph, smem_coarse);
+  for (int l = 1; l <= top; ++l) bot_ascend<BlockTeam, kKind>(D, l, c, B, ph);
+  bot_stage_out(DB, io, top);
 }
 
 }  // namespace pf

@@ -535,6 +535,117 @@ __global__ void __launch_bounds__(kSplitBlock) k_color_sweep_split(SellView A, d
     x[row] = __ddiv_rn(acc, diag);
 }
 
+// "Wide" rows for launches that fit one wave (the mid-size levels of a cycle, where a
+// launch is bound by the latency chain of one row, not by throughput): the whole row's
+// operator — every group of 4 columns and its 8-bit value indices — is loaded into
+// registers BEFORE griddepcontrol.wait (the operator is immutable, so those loads overlap
+// the previous kernel's tail), and after the wait all of the row's x gathers are issued at
+// once: one dependent memory round trip instead of one per group.  The products are then
+// formed and subtracted in stored order, the diagonal skipped, exactly as row_offdiag does.
+// kG groups (Q1: 27 entries -> 7); rows longer than 4 kG never take these kernels.
+template <int kG>
+struct RowWide {
+  int len;
+  int32_t c[4 * kG];
+  uint32_t w[kG];  // 4 value indices per word, entry j in byte j % 4 of word j / 4
+};
+
+template <int kVK, int kG>
+__device__ __forceinline__ void row_wide_head(const SellView& A, int32_t row, RowWide<kG>& h) {
+  static_assert(vk_kind<kVK>() == 1 || vk_kind<kVK>() == kVKSmem, "wide rows: 8-bit value indices only");
+  const int64_t base = sell_row_base(A.slice_ptr, row);
+  h.len = A.row_len[row];
+#pragma unroll
+  for (int g = 0; g < kG; ++g) {
+    if (4 * g < h.len) {
+      const int64_t e = sell_entry(base, 4 * g);
+      const int4 cc = ld_op<kVK>(reinterpret_cast<const int4*>(A.cols + e));
+      h.c[4 * g] = cc.x;
+      h.c[4 * g + 1] = cc.y;
+      h.c[4 * g + 2] = cc.z;
+      h.c[4 * g + 3] = cc.w;
+      h.w[g] = ld_op<kVK>(reinterpret_cast<const unsigned int*>(static_cast<const unsigned char*>(A.vidx) + e));
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h.c[4 * g + k] = -1;
+      h.w[g] = 0;
+    }
+  }
+}
+
+template <int kVK>
+__device__ __forceinline__ double wide_val(const SellView& A, uint32_t w, int k) {
+  const uint32_t i = (w >> (8 * k)) & 255u;
+  if constexpr (vk_kind<kVK>() == kVKSmem)
+    return s_vtab[i];
+  else
+    return __ldg(A.table + i);
+}
+
+// acc := acc - sum_{c != row} a_rc x_c in stored order, diag := a_rr (row_offdiag's result).
+template <int kVK, int kG>
+__device__ __forceinline__ void row_wide_offdiag(const SellView& A, const RowWide<kG>& h, int32_t row,
+                                                 const double* __restrict__ x, double& acc, double& diag) {
+  double xv[4 * kG];
+#pragma unroll
+  for (int j = 0; j < 4 * kG; ++j) xv[j] = (j < h.len && h.c[j] != row) ? __ldg(x + h.c[j]) : 0.0;
+#pragma unroll
+  for (int j = 0; j < 4 * kG; ++j) {
+    if (j < h.len) {
+      const double v = wide_val<kVK>(A, h.w[j >> 2], j & 3);
+      if (h.c[j] == row)
+        diag = v;
+      else
+        acc = __dsub_rn(acc, __dmul_rn(v, xv[j]));
+    }
+  }
+}
+
+#ifndef PF_WIDE_MINB
+#define PF_WIDE_MINB 2
+#endif
+template <bool kSor, int kVK, int kG>
+__global__ void __launch_bounds__(kBlock, PF_WIDE_MINB) k_color_sweep_wide(SellView A, double* x,
+                                                                    const double* __restrict__ b, int32_t row0,
+                                                                    int32_t row1, double omega) {
+  vtab_stage<kVK>(A);
+  const int32_t row = row0 + blockIdx.x * kBlock + threadIdx.x;
+  RowWide<kG> hd;
+  if (row < row1) row_wide_head<kVK, kG>(A, row, hd);  // operator only: before the wait
+  PF_PDL_ENTRY();
+  if (row >= row1) return;
+  const double bb = b[row];
+  const double xo = kSor ? x[row] : 0.0;
+  double acc = bb, diag = 0.0;
+  row_wide_offdiag<kVK, kG>(A, hd, row, x, acc, diag);
+  if (kSor)
+    x[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
+  else
+    x[row] = __ddiv_rn(acc, diag);
+}
+
+// k_jacobi with wide rows (identity block schedule).
+template <int kVK, int kG>
+__global__ void __launch_bounds__(kBlock, PF_WIDE_MINB) k_jacobi_wide(SellView A, const double* __restrict__ x_old,
+                                                               double* __restrict__ x_new,
+                                                               const double* __restrict__ b, int32_t n_own,
+                                                               int32_t n, double omega) {
+  vtab_stage<kVK>(A);
+  const int32_t row = blockIdx.x * kBlock + threadIdx.x;
+  RowWide<kG> hd;
+  if (row < n_own) row_wide_head<kVK, kG>(A, row, hd);
+  PF_PDL_ENTRY();
+  if (row >= n) return;
+  const double xo = x_old[row];
+  if (row >= n_own) {
+    x_new[row] = xo;
+    return;
+  }
+  double acc = b[row], diag = 0.0;
+  row_wide_offdiag<kVK, kG>(A, hd, row, x_old, acc, diag);
+  x_new[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), diag));
+}
+
 // Residual of the cycle (multigrid.cpp:166-167): y = A x (spmv order, acc from 0), r = b - y,
 // on rows [0, n).
 template <int kVK>

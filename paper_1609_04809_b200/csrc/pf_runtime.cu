@@ -34,7 +34,6 @@
 #include "pf_heat.cuh"
 #include "pf_kernels.cuh"
 #include "pf_nccl.hpp"
-#include "pf_sweep_dataflow.cuh"
 #include "pf_sweep_tma.cuh"
 #include "pf_runtime.hpp"
 
@@ -400,85 +399,6 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
   out.stored = sptr[n_slices];
 }
 
-// Device layout of one subdomain level: own rows colour-major (stable in host order),
-// then every other row in host order; SELL-32 operator; P (rows of this level).
-// PF_SOR_DATAFLOW (default 0: measured slower at C2, profiles/r02_sweep_experiments.md) /
-// PF_SOR_DATAFLOW_MIN_ROWS (default 32768 own rows): the
-// coloured sweeps of such levels (2-8 colours) run as one dataflow launch per smoothing
-// phase (pf_sweep_dataflow.cuh) instead of one launch per colour.
-bool sor_dataflow_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PF_SOR_DATAFLOW");
-    return e && std::atoi(e) != 0;
-  }();
-  return on;
-}
-int64_t sor_dataflow_min_rows() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("PF_SOR_DATAFLOW_MIN_ROWS");
-    return e ? std::atoll(e) : int64_t(32768);
-  }();
-  return v;
-}
-
-// The task lists of the dataflow colour sweep: the neighbour reach w (in 256-row chunks)
-// from the own-row pattern, then for 1..4 sweeps per launch every (pass, chunk) in the
-// claim order t = k + (w + 1) n.
-void build_dataflow(const HostLevel& H, DevLevel& D, const std::vector<int32_t>& color, int32_t n_own) {
-  D.df = DevLevel::Dataflow{};
-  const int C = D.n_colors;
-  if (!sor_dataflow_enabled() || C < 2 || C > kDfMaxColors || n_own < sor_dataflow_min_rows()) return;
-  std::vector<int32_t> chunk(static_cast<size_t>(n_own));
-#pragma omp parallel for schedule(static)
-  for (int32_t i = 0; i < n_own; ++i)
-    chunk[static_cast<size_t>(i)] = (D.perm[i] - D.color_start[color[i]]) / kBlock;
-  int32_t w = 0;
-#pragma omp parallel for schedule(static) reduction(max : w)
-  for (int32_t i = 0; i < n_own; ++i)
-    for (int64_t e = H.rowptr[i]; e < H.rowptr[i + 1]; ++e) {
-      const int32_t j = H.cols[e];
-      if (j < n_own && color[j] != color[i]) w = std::max(w, std::abs(chunk[j] - chunk[i]));
-    }
-  DevLevel::Dataflow& F = D.df;
-  F.w = w;
-  F.kc.resize(static_cast<size_t>(C));
-  for (int c = 0; c < C; ++c) {
-    F.kc[c] = (D.color_start[c + 1] - D.color_start[c] + kBlock - 1) / kBlock;
-    F.kmax = std::max(F.kmax, F.kc[c]);
-  }
-  if (F.kmax >= (1 << kDfTaskBits)) return;
-  // Claim order t = k + M n.  A task's dependency (pass n - 1, chunk k + w) is claimed
-  // M - w slots of t earlier; with R tasks resident at once the claimed-but-unfinished
-  // window spans about R M / K slots of t, so M (1 - R / K) > w + 1 keeps dependencies out
-  // of the window (no stalls) while the passes in flight stay within a band of the lattice
-  // (x stays in L2).  Twice the minimum; passes in order (M = K) when R is most of K.
-  int dev = 0;
-  PF_CUDA(cudaGetDevice(&dev));
-  const double R = 4.0 * sm_count(dev);  // resident 256-row blocks (PF_SOR_MINB = 4)
-  int64_t M = F.kmax;
-  if (R < 0.5 * F.kmax) M = std::min<int64_t>(F.kmax, 2 * static_cast<int64_t>(std::ceil((w + 1) / (1.0 - R / F.kmax))));
-  if (const char* e = std::getenv("PF_SOR_DF_TILT")) M = std::max<int64_t>(w + 1, std::atoll(e));
-  F.tilt = M;
-  for (int S = 1; S <= 4; ++S) {
-    const int N = S * C;
-    std::vector<std::pair<int64_t, int32_t>> order;  // (t * 64 + n, word)
-    for (int n = 0; n < N; ++n)
-      for (int32_t k = 0; k < F.kc[n % C]; ++k)
-        order.push_back({(static_cast<int64_t>(k) + M * n) * 64 + n, (n << kDfTaskBits) | k});
-    std::sort(order.begin(), order.end());
-    std::vector<int32_t> words(order.size());
-    for (size_t i = 0; i < order.size(); ++i) words[i] = order[i].second;
-    F.tasks[S - 1].upload(words);
-    F.n_tasks[S - 1] = static_cast<int32_t>(words.size());
-  }
-  F.flags.alloc(static_cast<int64_t>(4 * C) * F.kmax);
-  PF_CUDA(cudaMemset(F.flags.p, 0, sizeof(uint32_t) * static_cast<size_t>(F.flags.n)));
-  const uint32_t ctl[4] = {0, 1, 0, 0};  // next task, epoch (flags start at 0), ticket
-  F.ctl.alloc(4);
-  PF_CUDA(cudaMemcpy(F.ctl.p, ctl, sizeof ctl, cudaMemcpyHostToDevice));
-  F.on = true;
-}
-
 // PF_INTERLEAVE_MIN_BYTES (default 64 MB): levels whose x is at least this large run their
 // full-level Jacobi / residual passes with the colour-interleaved block schedule (0: every
 // level with 2-8 colours; a huge value: never).
@@ -490,6 +410,8 @@ int64_t interleave_min_bytes() {
   return v;
 }
 
+// Device layout of one subdomain level: own rows colour-major (stable in host order),
+// then every other row in host order; SELL-32x4 operator; P (rows of this level).
 void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
   PhaseTimer tm;
   const int32_t n = H.n, n_own = H.n_own;
@@ -583,7 +505,6 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
     for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
   }
   D.d_perm.upload(D.perm);
-  build_dataflow(H, D, color, n_own);
   // colour-interleaved block schedule when x outgrows L2 (RowMap, pf_types.hpp)
   D.rmap = RowMap{};
   D.rmap_grid = grid_for(n);
@@ -1052,6 +973,132 @@ SellView fp64_view(pf_hierarchy::Bottom& bot, const DevSell& S) {
   return v;
 }
 
+// PF_BOTTOM_STAGE (default 1): stage the block levels in shared memory (BotStage).
+bool bottom_stage_enabled() {
+  const char* e = std::getenv("PF_BOTTOM_STAGE");  // read at build time (tests flip it)
+  return !(e && std::atoi(e) == 0);
+}
+
+// Plan and build the shared-memory staging of the block levels (BotStage, pf_bottom.cuh):
+// levels 0, 1, ... up to block_top are staged while they fit the opt-in shared memory next
+// to the descriptor and the coarse pack — each with its vectors, operator, restriction,
+// colour ranges, Dirichlet flags and plans; then the prolongations, lowest level first,
+// as far as they still fit (C2: levels 0-2 and every P but level 2's, ~200 KB).
+void stage_block_levels(pf_hierarchy* h, pf_hierarchy::Bottom& bot, BotDesc& d, const std::vector<BotSrc>& src) {
+  d.stage = BotStage{};
+  d.stage.hs = -1;
+  if (!bottom_stage_enabled() || d.block_top < 0) return;
+  int optin = 0;
+  PF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  cudaFuncAttributes fa{};
+  PF_CUDA(cudaFuncGetAttributes(&fa, k_bottom));
+  auto r16 = [](int64_t b) { return (b + 15) / 16 * 16; };
+  const int64_t smem_off = r16(sizeof(BotDesc)) + r16(static_cast<int64_t>(coarse_pack_smem(d.coarse)));
+  const int64_t budget = static_cast<int64_t>(optin) - static_cast<int64_t>(fa.sharedSizeBytes) - smem_off - 1024;
+  struct Piece {
+    const void* src;
+    int64_t bytes, off;
+  };
+  std::vector<Piece> pieces;
+  std::vector<std::pair<void**, int64_t>> fix;  // field of t -> blob offset
+  int64_t used = 0, vec_bytes = 0;
+  BotDesc t = d;
+  auto add = [&](auto* field, const void* p, int64_t bytes) {  // field: a pointer member of t
+    if (!p || bytes <= 0) return;
+    pieces.push_back(Piece{p, bytes, used});
+    fix.push_back({(void**)field, used});  // C cast: the members are __restrict__-qualified
+    used += r16(bytes);
+  };
+  auto add_view = [&](SellView& v, const DevSell& S) {
+    const int64_t n_slices = static_cast<int64_t>(S.slice_ptr.n);
+    add(&v.cols, v.cols, S.stored * 4);
+    add(&v.slice_ptr, v.slice_ptr, n_slices * 8);
+    add(&v.row_len, v.row_len, S.row_len.bytes());
+    if (S.vals.vkind == 1) {  // the 8-bit value index and its table
+      v.vals = nullptr;
+      v.vkind = 1;
+      v.vidx = S.vals.vi8.p;
+      v.table = S.vals.table.p;
+      v.table_n = static_cast<int32_t>(S.vals.table.n);
+      add(&v.vidx, v.vidx, S.stored);
+      add(&v.table, v.table, S.vals.table.bytes());
+    } else {  // the decoded fp64 copy the descriptor already holds
+      add(&v.vals, v.vals, S.stored * 8);
+    }
+  };
+  auto plan = [&](BotPlan& P) {
+    add(&P.dst, P.dst, static_cast<int64_t>(P.n) * 4);
+    add(&P.src, P.src, static_cast<int64_t>(P.n) * 4);
+  };
+  int hs = -1;
+  for (int l = 0; l <= d.block_top; ++l) {
+    const size_t p0 = pieces.size();
+    const int64_t u0 = used;
+    bool ok = true;
+    const BotSrc& L = src[static_cast<size_t>(l)];
+    BotLevel& B = t.lev[l];
+    plan(B.ms);
+    plan(B.h1);
+    plan(B.h2);
+    if (B.acc_n > 0) {
+      add(&B.acc_off, B.acc_off, (static_cast<int64_t>(B.acc_n) + 1) * 4);
+      add(&B.acc_src, B.acc_src, L.acc->acc_src.bytes());
+      add(&B.acc_dst, B.acc_dst, static_cast<int64_t>(B.acc_n) * 4);
+    }
+    for (int s = 0; s < t.n_sub; ++s) {
+      const DevLevel& D = (*L.sub)[static_cast<size_t>(s)];
+      BotSub& S = t.sub[l][s];
+      if (D.A.max_len > kBotChunk) ok = false;
+      add_view(S.A, D.A);
+      if (l > 0) add_view(S.R, D.R);
+      add(&S.color_start, S.color_start, (static_cast<int64_t>(S.n_colors) + 1) * 4);
+      add(&S.is_dir, S.is_dir, D.d_is_dir.bytes());
+    }
+    const int64_t vb = 4 * r16(L.total * 8);
+    if (!ok || used + vec_bytes + vb > budget) {  // roll back level l and stop
+      pieces.resize(p0);
+      fix.resize(p0);
+      used = u0;
+      t.lev[l] = d.lev[l];
+      for (int s = 0; s < t.n_sub; ++s) t.sub[l][s] = d.sub[l][s];
+      break;
+    }
+    vec_bytes += vb;
+    hs = l;
+  }
+  if (hs < 0) return;
+  for (int l = 1; l <= hs; ++l)  // prolongations, as far as they fit
+    for (int s = 0; s < t.n_sub; ++s) {
+      const DevLevel& D = (*src[static_cast<size_t>(l)].sub)[static_cast<size_t>(s)];
+      const size_t p0 = pieces.size();
+      const int64_t u0 = used;
+      const BotSub keep = t.sub[l][s];
+      add_view(t.sub[l][s].P, D.P);
+      if (used + vec_bytes > budget) {
+        pieces.resize(p0);
+        fix.resize(p0);
+        used = u0;
+        t.sub[l][s] = keep;
+      }
+    }
+  bot.stage_blob.alloc(used);
+  for (const Piece& q : pieces)
+    PF_CUDA(cudaMemcpy(bot.stage_blob.p + q.off, q.src, static_cast<size_t>(q.bytes), cudaMemcpyDeviceToDevice));
+  for (auto& f : fix) *f.first = bot.stage_blob.p + f.second;
+  t.stage.blob = bot.stage_blob.p;
+  t.stage.blob_bytes = used;
+  t.stage.hs = hs;
+  t.stage.smem_off = smem_off;
+  int64_t off = used;
+  for (int l = 0; l <= hs; ++l)
+    for (int k = 0; k < 4; ++k) {
+      t.stage.vec_off[l][k] = off;
+      off += r16(src[static_cast<size_t>(l)].total * 8);
+    }
+  t.stage.arena_bytes = off;
+  d = t;
+}
+
 // Fill and upload a BotDesc for levels 0..top = src.size()-1; false if unsupported.
 bool fill_bottom(pf_hierarchy* h, pf_hierarchy::Bottom& bot, const std::vector<BotSrc>& src,
                  const CoarsePack& pack, double* coarse_stats) {
@@ -1106,6 +1153,7 @@ bool fill_bottom(pf_hierarchy* h, pf_hierarchy::Bottom& bot, const std::vector<B
       S.off = static_cast<int32_t>(D.offset);
     }
   }
+  stage_block_levels(h, bot, d, src);
   if (std::getenv("PF_BOTTOM_PROFILE")) {
     PF_CUDA(cudaMalloc(&bot.stamps, 256 * sizeof(unsigned long long)));
     PF_CUDA(cudaMemset(bot.stamps, 0, 256 * sizeof(unsigned long long)));
@@ -1115,15 +1163,30 @@ bool fill_bottom(pf_hierarchy* h, pf_hierarchy::Bottom& bot, const std::vector<B
   PF_CUDA(cudaMemcpy(bot.desc, &d, sizeof d, cudaMemcpyHostToDevice));
   int sms = 0, occ = 0;
   PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-  bot.smem = ((sizeof(BotDesc) + 15) / 16) * 16 + coarse_pack_smem(d.coarse);
-  if (bot.smem > 48 * 1024)
-    PF_CUDA(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bot.smem)));
+  bot.smem = d.stage.hs >= 0 ? static_cast<size_t>(d.stage.smem_off + d.stage.arena_bytes)
+                            : ((sizeof(BotDesc) + 15) / 16) * 16 + coarse_pack_smem(d.coarse);
+  if (bot.smem > 48 * 1024) {  // the cap, not the size: several bottoms may share the kernel
+    int optin = 0;
+    PF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    auto cap = [&](auto kern) {
+      cudaFuncAttributes fa{};
+      PF_CUDA(cudaFuncGetAttributes(&fa, kern));
+      PF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   optin - static_cast<int>(fa.sharedSizeBytes)));
+    };
+    cap(k_bottom);
+    cap(k_bottom_block<0>);
+    cap(k_bottom_block<1>);
+    cap(k_bottom_block<2>);
+  }
   PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bottom, kBlock, bot.smem));
   if (occ < 1) return false;
   int64_t want = std::max<int64_t>(sms, (max_total + kBlock - 1) / kBlock);
   if (const char* e = std::getenv("PF_BOTTOM_GRID")) want = std::max<int64_t>(1, std::atoll(e));
   bot.grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(occ) * sms));
+  // every bottom level staged for block 0: the other blocks would only wait at barriers
+  bot.staged_all = d.stage.hs == top && d.block_top == top;
+  if (bot.staged_all && !std::getenv("PF_BOTTOM_GRID")) bot.grid = 1;
   bot.top = top;
   bot.active = true;
   return true;
@@ -1326,6 +1389,40 @@ int64_t split_max_rows() {
   return v;
 }
 
+// Launches of at most PF_WIDE_MAX_ROWS rows (default: one wave of the wide kernels, 2
+// blocks of 256 per SM) on operators with 8-bit value indices and rows of <= 28 entries
+// take the wide-row kernels (k_color_sweep_wide / k_jacobi_wide: the whole row's operator
+// loaded before griddepcontrol.wait, all its x gathers in flight at once after it); 0: never.
+constexpr int kWideGroups = 7;
+int64_t wide_max_rows(int device) {
+  static const int64_t env = [] {
+    const char* e = std::getenv("PF_WIDE_MAX_ROWS");
+    return e ? std::atoll(e) : int64_t(-1);
+  }();
+  return env >= 0 ? env : int64_t(PF_WIDE_MINB) * sm_count(device) * kBlock;
+}
+template <int vk>
+bool wide_ok(const pf_hierarchy* h, const DevLevel& D, int64_t rows) {
+  constexpr int K = vk_kind<vk>();
+  return (K == 1 || K == kVKSmem) && D.A.max_len > 0 && D.A.max_len <= 4 * kWideGroups && rows > 0 &&
+         rows <= wide_max_rows(h->device);
+}
+
+// One damped-Jacobi sweep of subdomain level D, src -> dst.
+void enq_jacobi_sweep(pf_hierarchy* h, DevLevel& D, const double* src, double* dst, const double* b, double omega) {
+  auto launch = launcher(h);
+  vk_dispatch_rows(D.A, [&](auto V) {
+    constexpr int vk = decltype(V)::value;
+    if constexpr (vk_kind<vk>() == 1 || vk_kind<vk>() == kVKSmem) {
+      if (D.rmap.n_col == 0 && wide_ok<vk>(h, D, D.n)) {
+        launch(grid_for(D.n), kBlock, k_jacobi_wide<vk, kWideGroups>, view(D.A), src, dst, b, D.n_own, D.n, omega);
+        return;
+      }
+    }
+    launch(D.rmap_grid, kBlock, k_jacobi<vk>, view(D.A), src, dst, b, D.n_own, D.n, omega, D.rmap);
+  });
+}
+
 // PF_SOR_TMA (default 1): colour sweeps of operators with rows of <= 28 entries (Q1,
 // rotated Q1) take the TMA-staged persistent kernel (pf_sweep_tma.cuh) on levels with at
 // least PF_SOR_TMA_MIN_ROWS own rows; PF_SOR_TMA_BPS blocks per SM (default 1, which leaves
@@ -1391,6 +1488,15 @@ void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega
       }
       return;
     }
+    if constexpr (vk_kind<vk>() == 1 || vk_kind<vk>() == kVKSmem) {
+      if (wide_ok<vk>(h, D, r1 - r0)) {
+        if (sor)
+          launch(grid_for(r1 - r0), kBlock, k_color_sweep_wide<true, vk, kWideGroups>, view(D.A), x, b, r0, r1, omega);
+        else
+          launch(grid_for(r1 - r0), kBlock, k_color_sweep_wide<false, vk, kWideGroups>, view(D.A), x, b, r0, r1, 1.0);
+        return;
+      }
+    }
     if (split > 0 && D.A.max_len > split && D.n_own <= split_max_rows()) {
       const int32_t width = (D.A.max_len + 3) / 4 * 4;
       const size_t smem = sizeof(double) * kSlice * static_cast<size_t>(width);
@@ -1408,34 +1514,6 @@ void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega
       launch(grid_for(r1 - r0), kBlock, k_color_sweep<false, vk>, view(D.A), x, b, r0, r1, 1.0);
     }
   });
-}
-
-// S sweeps of the coloured smoother on one subdomain as one dataflow launch
-// (pf_sweep_dataflow.cuh); false when the level has no dataflow plan for S.
-bool enq_dataflow(pf_hierarchy* h, DevLevel& D, int S, bool sor, double omega, double* x, const double* b) {
-  const auto& F = D.df;
-  if (!F.on || S < 1 || S > 4) return false;
-  DataflowView v{};
-  v.tasks = F.tasks[S - 1].p;
-  v.n_tasks = F.n_tasks[S - 1];
-  v.n_colors = D.n_colors;
-  v.w = F.w;
-  v.kmax = F.kmax;
-  for (int c = 0; c <= D.n_colors; ++c) v.cs[c] = D.color_start[c];
-  for (int c = 0; c < D.n_colors; ++c) v.kc[c] = F.kc[c];
-  v.flags = F.flags.p;
-  v.ctl = F.ctl.p;
-  auto launch = launcher(h);
-  vk_dispatch_rows(D.A, [&](auto V) {
-    constexpr int vk = decltype(V)::value;
-    auto kern = sor ? k_color_sweep_dataflow<true, vk> : k_color_sweep_dataflow<false, vk>;
-    static thread_local std::map<const void*, int> occ_cache;
-    int& occ = occ_cache[reinterpret_cast<const void*>(kern)];
-    if (!occ) PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0));
-    const int64_t grid = std::min<int64_t>(v.n_tasks, static_cast<int64_t>(std::max(occ, 1)) * sm_count(h->device));
-    launch(static_cast<unsigned>(grid), kBlock, kern, view(D.A), x, b, v, sor ? omega : 1.0);
-  });
-  return true;
 }
 
 // smooth (solvers.cpp:56-68) on x (primary buffer) with b.
@@ -1484,29 +1562,10 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
       if (sc.kind == PF_SMOOTHER_JACOBI) {
         if (!(first_done && sweep == 0 && local == 0))
           for (DevLevel& D : L.sub)
-            vk_dispatch_rows(D.A, [&](auto V) {
-              launch(D.rmap_grid, kBlock, k_jacobi<decltype(V)::value>, view(D.A),
-                     static_cast<const double*>(bufs[cur] + D.offset), bufs[cur ^ 1] + D.offset, b + D.offset,
-                     D.n_own, D.n, sc.damping, D.rmap);
-            });
+            enq_jacobi_sweep(h, D, bufs[cur] + D.offset, bufs[cur ^ 1] + D.offset, b + D.offset, sc.damping);
         cur ^= 1;
       } else {
         const bool sor = sc.kind == PF_SMOOTHER_MULTICOLOR_SOR;
-        // one dataflow launch per smoothing phase (one subdomain, one process: the
-        // exchanges in between are empty) or per sweep (one subdomain per process)
-        if (h->n_sub == 1 && !h->colorwise && L.sub[0].df.on) {
-          DevLevel& D = L.sub[0];
-          if (h->world == 1) {
-            const int S = sc.sweeps * sc.local_sweeps;
-            if (S <= 4) {
-              if (sweep == 0 && local == 0) enq_dataflow(h, D, S, sor, sc.damping, bufs[cur] + D.offset, b + D.offset);
-              continue;
-            }
-          } else if (sc.local_sweeps <= 4) {
-            if (local == 0) enq_dataflow(h, D, sc.local_sweeps, sor, sc.damping, bufs[cur] + D.offset, b + D.offset);
-            continue;
-          }
-        }
         int max_colors = 0;
         for (DevLevel& D : L.sub) max_colors = std::max(max_colors, D.n_colors);
         for (int c = 0; c < max_colors; ++c) {
@@ -1711,8 +1770,32 @@ bool enq_coarse(pf_hierarchy* h, int l, double* x, const double* b, double tol, 
 
 // cycle(bot.top) in one cooperative launch; lev[top].b holds the restricted residual
 // (before the master/slave accumulate when accumulate_top) and lev[top].x is zero.
+// PF_BOTTOM_BLOCK_KERNEL (default 1): a bottom whose levels are all staged runs as the
+// one-block k_bottom_block instead of the cooperative k_bottom.
+bool bottom_block_kernel() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_BOTTOM_BLOCK_KERNEL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 void enq_bottom(pf_hierarchy* h, const pf_hierarchy::Bottom& bot, const pf_multigrid_config& cfg,
                 int accumulate_top) {
+  static const int calib0 = std::getenv("PF_BOTTOM_CALIB") ? std::atoi(std::getenv("PF_BOTTOM_CALIB")) : 0;
+  if (bot.staged_all && bottom_block_kernel() && calib0 == 0) {
+    const BotCfg c{cfg.smoother.kind, cfg.pre_smooth, cfg.post_smooth, cfg.smoother.local_sweeps,
+                   cfg.coarse_max_iter, cfg.smoother.damping, cfg.coarse_tol, 1 << 20, 0,
+                   h->colorwise && cfg.smoother.kind != PF_SMOOTHER_JACOBI ? 1 : 0};
+    auto launch = launcher(h);
+    const BotDesc* d = static_cast<const BotDesc*>(bot.desc);
+    switch (cfg.smoother.kind) {
+      case PF_SMOOTHER_JACOBI: launch.with_smem(bot.smem)(1, kBlock, k_bottom_block<0>, d, c, accumulate_top); break;
+      case PF_SMOOTHER_MULTICOLOR_SOR: launch.with_smem(bot.smem)(1, kBlock, k_bottom_block<2>, d, c, accumulate_top); break;
+      default: launch.with_smem(bot.smem)(1, kBlock, k_bottom_block<1>, d, c, accumulate_top); break;
+    }
+    return;
+  }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(static_cast<unsigned>(bot.grid));
   lc.blockDim = dim3(kBlock);
@@ -1726,7 +1809,8 @@ void enq_bottom(pf_hierarchy* h, const pf_hierarchy::Bottom& bot, const pf_multi
   // measured at C2: the coloured smoothers (8 barriers per sweep) gain from running the
   // tiny levels inside one block (V-cycle 1.83 -> 1.75 ms); Jacobi (1 barrier per sweep)
   // loses parallelism there and keeps the whole grid
-  const int block_top = cfg.smoother.kind == PF_SMOOTHER_JACOBI ? -1 : 1 << 20;
+  // (with every bottom level staged in shared memory, both smoothers run them in block 0)
+  const int block_top = cfg.smoother.kind == PF_SMOOTHER_JACOBI && !bot.staged_all ? -1 : 1 << 20;
   static const int calib = std::getenv("PF_BOTTOM_CALIB") ? std::atoi(std::getenv("PF_BOTTOM_CALIB")) : 0;
   const BotCfg c{cfg.smoother.kind, cfg.pre_smooth, cfg.post_smooth, cfg.smoother.local_sweeps,
                  cfg.coarse_max_iter, cfg.smoother.damping, cfg.coarse_tol, block_top, calib,
@@ -2907,10 +2991,8 @@ pf_status pf_time_sweep(pf_hierarchy* h, int level, int kind, int iters, double*
     if (kind == PF_SMOOTHER_JACOBI) {
       const double* src = (i & 1) ? x->alt() : x->cur();
       double* dst = (i & 1) ? x->cur() : x->alt();
-      vk_dispatch_rows(D.A, [&](auto V) {
-        launch(D.rmap_grid, kBlock, k_jacobi<decltype(V)::value>, view(D.A), src, dst, b, D.n_own, D.n, 0.8, D.rmap);
-      });
-    } else if (!enq_dataflow(h, D, 1, kind == PF_SMOOTHER_MULTICOLOR_SOR, 1.2, x->cur(), b)) {
+      enq_jacobi_sweep(h, D, src, dst, b, 0.8);
+    } else {
       for (int c = 0; c < D.n_colors; ++c)
         enq_color_sweep(h, D, c, true, kind == PF_SMOOTHER_MULTICOLOR_SOR ? 1.2 : 1.0, x->cur(), b);
     }
@@ -2955,10 +3037,17 @@ pf_status pf_time_vcycle(pf_hierarchy* h, pf_vector* x, const pf_vector* b, cons
   if (h->bot.stamps) {  // PF_BOTTOM_PROFILE: per-phase times of the last bottom launch
     unsigned long long st[256];
     PF_CUDA(cudaMemcpy(st, h->bot.stamps, sizeof st, cudaMemcpyDeviceToHost));
-    const int n = static_cast<int>(st[255]);
+    const int n = static_cast<int>(st[255]) < 127 ? static_cast<int>(st[255]) : 127;
     std::fprintf(stderr, "[pf] bottom: %d phases, total %.2f us:", n, (st[n] - st[0]) / 1e3);
     for (int i = 1; i <= n; ++i) std::fprintf(stderr, " %.2f", (st[i] - st[i - 1]) / 1e3);
     std::fprintf(stderr, "\n");
+    int nb = 0;
+    while (nb < 126 && st[129 + nb] > 0) ++nb;
+    if (nb > 0) {
+      std::fprintf(stderr, "[pf] bottom block 0: %d phases, total %.2f us:", nb, (st[128 + nb] - st[128]) / 1e3);
+      for (int i = 1; i <= nb; ++i) std::fprintf(stderr, " %.2f", (st[128 + i] - st[128 + i - 1]) / 1e3);
+      std::fprintf(stderr, "\n");
+    }
   }
   PF_API_END
 }

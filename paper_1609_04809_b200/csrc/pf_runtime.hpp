@@ -110,17 +110,6 @@ struct DevLevel {
   std::vector<int32_t> color_start;  // device rows, n_colors + 1 (own rows only)
   RowMap rmap{};                     // block schedule of the full-level Jacobi / residual passes
   unsigned rmap_grid = 0;            // their grid under rmap
-  // dataflow schedule of the coloured sweeps (pf_sweep_dataflow.cuh): tasks = 256-row
-  // chunks of one colour pass; lists for 1..kDfMaxPasses sweeps per launch
-  struct Dataflow {
-    bool on = false;
-    int32_t w = 0, kmax = 0;
-    int64_t tilt = 0;  // claim order t = k + tilt * pass
-    std::vector<int32_t> kc;
-    std::array<DevBuf<int32_t>, 4> tasks;
-    std::array<int32_t, 4> n_tasks{};
-    DevBuf<uint32_t> flags, ctl;
-  } df;
   std::vector<int32_t> perm;         // host index -> device index
   DevBuf<int32_t> d_perm;
   DevSell A;
@@ -252,6 +241,7 @@ struct pf_hierarchy {
   // Levels 0..top of the V-cycle run in one cooperative kernel (pf_bottom.cuh).
   struct Bottom {
     bool active = false;
+    bool staged_all = false;  // levels 0..top all staged in block 0's shared memory
     int top = -1;
     int grid = 0;
     size_t smem = 0;       // dynamic shared memory: descriptor copy + coarse pack
@@ -259,6 +249,7 @@ struct pf_hierarchy {
     void* stamps = nullptr;  // PF_BOTTOM_PROFILE phase timestamps
     std::vector<pf::DevBuf<int32_t>> color_bufs;
     std::vector<pf::DevBuf<double>> val_bufs;  // fp64 copies of index-encoded operators
+    pf::DevBuf<unsigned char> stage_blob;       // the staged block levels (BotStage)
     Bottom() = default;
     Bottom(const Bottom&) = delete;
     Bottom& operator=(const Bottom&) = delete;

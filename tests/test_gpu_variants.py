@@ -21,7 +21,6 @@ ROOT = os.path.dirname(HERE)
 
 VARIANTS = {
     # only >= 2M-entry operators index-encoded: the small hierarchies run fp64 operators
-    # (cached below the finest) and the bottom kernel its native fp64 views
     # (cached below the finest) and the bottom kernel its native fp64 views; the cycle
     # residual and restriction as separate launches on every level
     "fp64_small_levels": {"PF_VALUE_INDEX_MIN": "2097152", "PF_FUSED_RR_ROWS": "0"},
@@ -37,10 +36,14 @@ VARIANTS = {
     # the colour-interleaved block schedule (RowMap) of the Jacobi / residual passes on every
     # level with 2-8 colours (default: only where x exceeds 64 MB)
     "interleave_everywhere": {"PF_INTERLEAVE_MIN_BYTES": "0"},
-    # the opt-in dataflow colour sweep (one launch per smoothing phase) on every level with
-    # 2-8 colours, in the default claim order and in a steep wavefront
-    "dataflow_everywhere": {"PF_SOR_DATAFLOW": "1", "PF_SOR_DATAFLOW_MIN_ROWS": "0"},
-    "dataflow_everywhere_ordered": {"PF_SOR_DATAFLOW": "1", "PF_SOR_DATAFLOW_MIN_ROWS": "0", "PF_SOR_DF_TILT": "17"},
+    # the bottom levels unstaged (operators and vectors in global memory) in the cooperative
+    # kernel, and no wide-row kernels (every mid-size launch takes the group-pipelined rows)
+    "bottom_unstaged_no_wide": {"PF_BOTTOM_STAGE": "0", "PF_WIDE_MAX_ROWS": "0"},
+    # staged bottom levels inside the cooperative kernel (not the one-block kernel), wide
+    # rows on every launch that fits them, damped Jacobi through the bottom kernel too
+    "bottom_staged_cooperative_wide_all": {"PF_BOTTOM_BLOCK_KERNEL": "0", "PF_WIDE_MAX_ROWS": "100000000",
+                                           "PF_BOTTOM_JACOBI": "1"},
+    "bottom_block_kernel_jacobi": {"PF_BOTTOM_JACOBI": "1"},
 }
 
 
