@@ -476,6 +476,46 @@ __global__ void __launch_bounds__(kBlock, PF_SOR_MINB) k_color_sweep(SellView A,
     x[row] = __ddiv_rn(acc, diag);
 }
 
+// The two halves of the last colour of a multi-process coloured sweep whose exchange
+// overlaps the interior rows (same per-row arithmetic as k_color_sweep): the rows in `list`
+// (those that send or read a non-own copy), then the other rows of [row0, row1).
+template <bool kSor, int kVK>
+__global__ void __launch_bounds__(kBlock, PF_SOR_MINB) k_color_sweep_list(SellView A, double* x,
+                                                             const double* __restrict__ b,
+                                                             const int32_t* __restrict__ list, int32_t n_list,
+                                                             double omega) {
+  vtab_stage<kVK>(A);
+  PF_PDL_ENTRY();
+  const int32_t i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= n_list) return;
+  const int32_t row = list[i];
+  double acc = b[row], diag = 0.0;
+  row_offdiag<true, false, kVK>(A, row, x, acc, diag);
+  if (kSor)
+    x[row] = __dadd_rn(__dmul_rn(1.0 - omega, x[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
+  else
+    x[row] = __ddiv_rn(acc, diag);
+}
+template <bool kSor, int kVK>
+__global__ void __launch_bounds__(kBlock, PF_SOR_MINB) k_color_sweep_skip(SellView A, double* x,
+                                                             const double* __restrict__ b, int32_t row0,
+                                                             int32_t row1, const uint8_t* __restrict__ skip,
+                                                             double omega) {
+  vtab_stage<kVK>(A);
+  const int32_t row = row0 + blockIdx.x * kBlock + threadIdx.x;
+  const bool act = row < row1 && !skip[row];
+  RowHead hd;
+  if (act) row_head<kVK>(A, row, hd);  // operator only: before the wait
+  PF_PDL_ENTRY();
+  if (!act) return;
+  double acc = b[row], diag = 0.0;
+  row_offdiag_from<true, false, kVK>(A, hd, row, x, acc, diag);
+  if (kSor)
+    x[row] = __dadd_rn(__dmul_rn(1.0 - omega, x[row]), __ddiv_rn(__dmul_rn(omega, acc), diag));
+  else
+    x[row] = __ddiv_rn(acc, diag);
+}
+
 // k_color_sweep for long rows: one block per SELL slice (32 rows), kSplitBlock / 32 warps.
 // Warp w loads groups w, w + 8, ... of all 32 rows (coalesced, as the row kernel's single
 // warp would), gathers x and forms the products a_e x_c into shared memory (entry-major,

@@ -778,6 +778,20 @@ void build_fused_plans(pf_hierarchy* h, int l) {
     D.n_brows = static_cast<int32_t>(list.size());
     D.brows.upload(list);
     D.is_brow.upload(isb);
+    // coloured smoothers: the last colour's rows that send or read a non-own copy
+    if (D.n_colors >= 1) {
+      const int32_t c0 = D.color_start[D.n_colors - 1], c1 = D.color_start[D.n_colors];
+      std::vector<uint8_t> pre(static_cast<size_t>(D.n), 0);
+      for (int32_t r = c0; r < c1; ++r)
+        pre[static_cast<size_t>(r)] = isb[static_cast<size_t>(r)] || D.reads_nonown[static_cast<size_t>(r)];
+      std::vector<int32_t> pl;
+      for (int32_t r = c0; r < c1; ++r)
+        if (pre[static_cast<size_t>(r)]) pl.push_back(r);
+      D.n_cpre = static_cast<int32_t>(pl.size());
+      D.cpre.upload(pl);
+      D.is_cpre.upload(pre);
+    }
+    std::vector<uint8_t>().swap(D.reads_nonown);
   }
   build_scatter_plan(L.host, L.sub, h->rank_base, local, {PF_CH_MASTER_SLAVE, PF_CH_HALO1}, L.fused_ms_h1);
   build_scatter_plan(L.host, L.sub, h->rank_base, local, {PF_CH_MASTER_SLAVE, PF_CH_HALO1, PF_CH_HALO2},
@@ -1556,6 +1570,52 @@ bool enq_smooth(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf
         PF_CUDA(cudaEventRecord(h->ev_join, h->comm_stream));
         PF_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
         cur ^= 1;
+        exchanged = true;
+        continue;
+      }
+      const bool overlap_c = h->fused && h->world > h->n_sub && h->xport && h->xport->overlap_ok() &&
+                             sc.kind != PF_SMOOTHER_JACOBI && !h->colorwise && local + 1 == sc.local_sweeps &&
+                             L.sub[0].n_cpre >= 0 && L.sub[0].n_colors >= 1;
+      if (overlap_c) {
+        // coloured sweep: every colour but the last as usual; the last colour's rows that
+        // send or read a non-own copy first, then the exchange on the side stream overlapped
+        // with the rest of the last colour (they touch neither the sent rows nor the copies
+        // the exchange rewrites, so the result is the reference order's bit for bit)
+        DevLevel& D = L.sub[0];
+        const bool sor = sc.kind == PF_SMOOTHER_MULTICOLOR_SOR;
+        const double om = sor ? sc.damping : 1.0;
+        double* x = bufs[cur] + D.offset;
+        const double* bb = b + D.offset;
+        for (int c = 0; c + 1 < D.n_colors; ++c) enq_color_sweep(h, D, c, sor, om, x, bb);
+        const int32_t c0 = D.color_start[D.n_colors - 1], c1 = D.color_start[D.n_colors];
+        vk_dispatch_rows(D.A, [&](auto V) {
+          constexpr int vk = decltype(V)::value;
+          if (D.n_cpre > 0) {
+            if (sor)
+              launch(grid_for(D.n_cpre), kBlock, k_color_sweep_list<true, vk>, view(D.A), x, bb,
+                     static_cast<const int32_t*>(D.cpre.p), D.n_cpre, om);
+            else
+              launch(grid_for(D.n_cpre), kBlock, k_color_sweep_list<false, vk>, view(D.A), x, bb,
+                     static_cast<const int32_t*>(D.cpre.p), D.n_cpre, om);
+          }
+        });
+        const bool last = sweep + 1 == sc.sweeps;
+        PF_CUDA(cudaEventRecord(h->ev_fork, h->stream));
+        PF_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_fork, 0));
+        enq_plan(h, last && then_h2 ? L.fused_all : L.fused_ms_h1, bufs[cur], h->comm_stream);
+        vk_dispatch_rows(D.A, [&](auto V) {
+          constexpr int vk = decltype(V)::value;
+          if (c1 > c0) {
+            if (sor)
+              launch(grid_for(c1 - c0), kBlock, k_color_sweep_skip<true, vk>, view(D.A), x, bb, c0, c1,
+                     static_cast<const uint8_t*>(D.is_cpre.p), om);
+            else
+              launch(grid_for(c1 - c0), kBlock, k_color_sweep_skip<false, vk>, view(D.A), x, bb, c0, c1,
+                     static_cast<const uint8_t*>(D.is_cpre.p), om);
+          }
+        });
+        PF_CUDA(cudaEventRecord(h->ev_join, h->comm_stream));
+        PF_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
         exchanged = true;
         continue;
       }
@@ -2447,6 +2507,17 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
       if (!L.host[s].set)
         state("level " + std::to_string(l) + " subdomain " + std::to_string(s) + " not set");
       build_dev_level(L.host[s], L.sub[s], l);
+      if (h->world != h->n_sub) {  // the own rows reading a non-own copy (build_fused_plans)
+        const HostLevel& H = L.host[s];
+        DevLevel& D = L.sub[s];
+        D.reads_nonown.assign(static_cast<size_t>(D.n), 0);
+#pragma omp parallel for schedule(static)
+        for (int32_t i = 0; i < H.n_own; ++i) {
+          bool p = false;
+          for (int64_t k = H.rowptr[i]; k < H.rowptr[i + 1] && !p; ++k) p = H.cols[k] >= H.n_own;
+          D.reads_nonown[static_cast<size_t>(D.perm[i])] = p ? 1 : 0;
+        }
+      }
       if (l > 0) {  // the operator is on the device; level 0 keeps its CSR for the coarse pack
         std::vector<int32_t>().swap(L.host[s].cols);
         std::vector<double>().swap(L.host[s].vals);

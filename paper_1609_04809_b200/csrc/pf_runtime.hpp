@@ -129,6 +129,13 @@ struct DevLevel {
   DevBuf<int32_t> brows;
   DevBuf<uint8_t> is_brow;
   int32_t n_brows = 0;
+  // ... and for the coloured smoothers: the rows of the LAST colour that must run before the
+  // exchange (boundary rows, and rows reading a non-own copy the exchange rewrites), as a
+  // list and a mask; every other row of that colour runs concurrently with the exchange
+  DevBuf<int32_t> cpre;
+  DevBuf<uint8_t> is_cpre;
+  int32_t n_cpre = -1;  // -1: not built
+  std::vector<uint8_t> reads_nonown;  // host, multi-process finalize only: own row (device order) reads a copy
   // residual-norm scratch
   int resnorm_blocks = 0;
   DevBuf<double> partials;

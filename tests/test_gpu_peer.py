@@ -94,13 +94,14 @@ def test_peer_threads_captured(cuda, tmp_path, K, L, rep, fused, kind):
 
 @pytest.mark.parametrize("K,L,rep,fused,kind", [(2, 4, "coarse", False, 0), (2, 4, "bottom", True, 0),
                                                 (4, 4, "bottom", True, 0), (4, 3, "coarse", False, 2),
-                                                (3, 3, "coarse", True, 0), (4, 4, "bottom", True, 2)],
+                                                (3, 3, "coarse", True, 0), (4, 4, "bottom", True, 2),
+                                                (2, 4, "coarse", True, 2), (3, 4, "coarse", True, 1)],
                          ids=lambda v: str(v))
 def test_peer_processes_ipc(cuda, tmp_path, K, L, rep, fused, kind):
     """K processes on cuda:0, each one rank (tests/peer_rank.py), arenas mapped with CUDA
     IPC — the path of one process per GPU over NVLink: the captured multi-process solve
-    (fused exchanges with the Jacobi sweep's side-stream overlap, replicated bottom) equals
-    the oracle's K-rank solve bit for bit."""
+    (fused exchanges with the side-stream overlap of the Jacobi sweep / the last colour of
+    the coloured sweep, replicated bottom) equals the oracle's K-rank solve bit for bit."""
     d = str(tmp_path)
     _run([[sys.executable, os.path.join(HERE, "peer_rank.py"), "--dir", d, "--rank", str(r)] + _args(K, L, rep, fused, kind)
           for r in range(K)])
