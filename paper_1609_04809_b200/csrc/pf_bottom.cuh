@@ -17,89 +17,18 @@
 
 #include <cooperative_groups.h>
 
+#include "pf_bottom_types.hpp"
 #include "pf_kernels.cuh"
 
 namespace pf {
 
 namespace cg = cooperative_groups;
 
-constexpr int kBotMaxLevels = 8;
-constexpr int kBotMaxSubs = 8;
-
-struct BotSub {
-  SellView A;
-  const int32_t* host_of_own;
-  const int32_t* color_start;  // n_colors + 1, subdomain-local device rows
-  SellView P;                  // P of this level (rows: this level; cols: parent, local)
-  SellView R;                  // R to the parent (rows: parent, local; cols: this level, local)
-  const uint8_t* is_dir;
-  int32_t n, n_own, n_colors;
-  int32_t off;                 // position in the level vectors
-};
-
-struct BotPlan {
-  const int32_t* dst;
-  const int32_t* src;
-  int32_t n;
-};
-
-struct BotLevel {
-  double* x;   // primary
-  double* xa;  // Jacobi ping-pong partner
-  double* b;
-  double* r;
-  int32_t total;
-  int32_t max_colors;
-  BotPlan ms, h1, h2;
-  const int32_t* acc_off;
-  const int32_t* acc_src;
-  const int32_t* acc_dst;
-  int32_t acc_n;
-};
-
-// Shared-memory staging of the block levels (levels 0..hs <= block_top, which block 0 runs
-// alone).  Their operators (SELL-32x4 with 8-bit value indices where the level has at
-// most 256 distinct values), colour ranges, Dirichlet flags and exchange plans are copied
-// at finalize into one global blob; the descriptor points into the blob.  At the start of
-// the block section block 0 copies the blob into shared memory, points its own copy of the
-// descriptor at it and gives the level vectors (x, xa, b, r) shared-memory slots, so every
-// dependent load of the 70-odd phases of the tiny levels is a shared-memory access instead
-// of an L2 round trip.  The blob is an exact copy, so the unstaged path (the same
-// descriptor without relocation) computes the same values from global memory.
-struct BotStage {
-  const unsigned char* blob;
-  int64_t blob_bytes;   // multiple of 16
-  int64_t arena_bytes;  // blob + the staged levels' vectors
-  int64_t smem_off;     // arena offset in the kernel's dynamic shared memory
-  int hs;               // staged levels 0..hs (-1: none)
-  int64_t vec_off[kBotMaxLevels][4];  // arena offsets of x, xa, b, r
-};
-
-struct BotDesc {
-  int n_sub;
-  int n_levels;   // Lc + 1
-  int block_top;  // highest level small enough for block 0 alone (block barriers), -1: none
-  unsigned long long* stamps;  // optional (PF_BOTTOM_PROFILE): globaltimer after each phase
-  CoarsePack coarse;        // level 0 packed for the shared-memory coarse solve
-  double* coarse_stats;
-  BotLevel lev[kBotMaxLevels];
-  BotSub sub[kBotMaxLevels][kBotMaxSubs];
-  BotStage stage;
-};
-
-struct BotCfg {
-  int kind, pre, post, local_sweeps, coarse_max_iter;
-  double omega, coarse_tol;
-  int block_top;  // levels 0..block_top inside block 0 (-1: none); chosen per smoother
-  int calib;      // PF_BOTTOM_CALIB: empty grid-barrier phases first (profiling aid)
-  int colorwise;  // coloured smoothers: master/slave + halo1 scatter after every colour
-};
-
 // Latency-oriented row routines for the bottom levels, where each phase is a chain of
 // dependent L2 round trips rather than a bandwidth problem: all entries of a row (up to
 // kBotChunk) are loaded in one round, then all x gathers in one round.  Same operations
 // in the same order as row_offdiag / row_dot, so results are bit-identical.
-constexpr int kBotChunk = 28;  // a Q1 row has 27 entries
+// (kBotChunk: pf_bottom_types.hpp)
 
 __device__ __forceinline__ void bot_row_offdiag(const SellView& A, int32_t row, const double* x, double& acc,
                                                 double& diag) {
@@ -197,7 +126,7 @@ __device__ __forceinline__ void bot_reloc_view(SellView& A, const unsigned char*
   bot_reloc(A.vidx, lo, hi, arena);
   bot_reloc(A.table, lo, hi, arena);
 }
-__device__ void bot_relocate(BotDesc& D, unsigned char* arena) {
+static __device__ void bot_relocate(BotDesc& D, unsigned char* arena) {
   const unsigned char* lo = D.stage.blob;
   const unsigned char* hi = lo + D.stage.blob_bytes;
   for (int l = 0; l <= D.stage.hs; ++l) {
@@ -438,7 +367,7 @@ struct BotIo {
   int32_t n;
   bool staged, io;   // levels 0..bt staged; bt itself staged (interface copies needed)
 };
-__device__ BotIo bot_stage_operators(BotDesc& DB, unsigned char* smem_b, int bt) {
+static __device__ BotIo bot_stage_operators(BotDesc& DB, unsigned char* smem_b, int bt) {
   BotIo io{DB.lev[bt].x, DB.lev[bt].b, DB.lev[bt].total, DB.stage.hs >= 0 && bt == DB.block_top, false};
   io.io = io.staged && DB.stage.hs == bt;
   if (!io.staged) return io;
@@ -451,7 +380,7 @@ __device__ BotIo bot_stage_operators(BotDesc& DB, unsigned char* smem_b, int bt)
   __syncthreads();
   return io;
 }
-__device__ void bot_stage_in_vectors(BotDesc& DB, const BotIo& io, int bt) {
+static __device__ void bot_stage_in_vectors(BotDesc& DB, const BotIo& io, int bt) {
   if (!io.io) return;
   for (int32_t i = threadIdx.x; i < io.n; i += blockDim.x) {
     DB.lev[bt].b[i] = io.gb[i];
@@ -459,7 +388,7 @@ __device__ void bot_stage_in_vectors(BotDesc& DB, const BotIo& io, int bt) {
   }
   __syncthreads();
 }
-__device__ void bot_stage_out(BotDesc& DB, const BotIo& io, int bt) {
+static __device__ void bot_stage_out(BotDesc& DB, const BotIo& io, int bt) {
   if (!io.io) return;
   __syncthreads();
   for (int32_t i = threadIdx.x; i < io.n; i += blockDim.x) io.gx[i] = DB.lev[bt].x[i];
@@ -469,7 +398,7 @@ __device__ void bot_stage_out(BotDesc& DB, const BotIo& io, int bt) {
 // restricted residual (Dirichlet entries zeroed, before the master/slave accumulate when
 // `accumulate_top`) and lev[Lc].x is zero.  Levels above block_top run with the whole
 // grid; levels 0..block_top (at most a few hundred rows each) run inside block 0.
-__global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __restrict__ Dp, BotCfg c,
+static __global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __restrict__ Dp, BotCfg c,
                                                       int accumulate_top) {
   PF_PDL_ENTRY();
   // The descriptor is read on every row of every phase: keep a per-block copy in

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_cn_rhs(S
 
 // apply_dirichlet_rhs (assembly.cpp:172-179) with g = scale * profile, and u_D = b_D
 // (app.cpp:196-200) when u is given.
-__global__ void __launch_bounds__(kBlock) k_dirichlet(const int32_t* __restrict__ idx,
+static __global__ void __launch_bounds__(kBlock) k_dirichlet(const int32_t* __restrict__ idx,
                                                       const double* __restrict__ prof, int32_t n_dir,
                                                       int has, double scale, double* __restrict__ b,
                                                       double* __restrict__ u) {

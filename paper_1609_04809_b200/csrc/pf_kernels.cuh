@@ -49,13 +49,8 @@ namespace pf {
 //     11.57 -> 10.91 ms).  Measured without gain: L1::no_allocate loads (Jacobi 6.37 ms,
 //     SOR unchanged), plus an L2::evict_last cache policy (6.38 ms); caching the finest
 //     level of a 64^3 hierarchy, whose 39 MB operator also fits, costs 6 %.
-constexpr int kVKSmem = 4;
-constexpr int kVKCached = 8;
-template <int kVK>
-constexpr int vk_kind() { return kVK < 0 ? kVK : (kVK & 7); }
-template <int kVK>
-constexpr bool vk_cached() { return kVK >= 0 && (kVK & kVKCached) != 0; }
-__shared__ double s_vtab[256];
+// (kVKSmem, kVKCached, vk_kind, vk_cached: pf_types.hpp, shared with the host dispatch)
+static __shared__ double s_vtab[256];
 
 // Resident blocks per SM of a row kernel: `minb` (pf_types.hpp), except for the streamed
 // fp64 operators (kVK == 0: the per-cell-coefficient finest levels, at the HBM roofline),
@@ -425,7 +420,7 @@ struct SolveState {
 // per-subdomain squares (transport.cpp:139-149) gives ||b - A x_m||; m = 0 records r0,
 // m >= 1 records the residual after cycle m and stops at <= tol * r0 or after max cycles.
 // Sets the WHILE (next iteration) and IF (rest of the cycle) conditions of the graph.
-__global__ void k_decide(const double* __restrict__ sumsq, int n_parts, double tol, int max_cycles,
+static __global__ void k_decide(const double* __restrict__ sumsq, int n_parts, double tol, int max_cycles,
                          SolveState* st, cudaGraphConditionalHandle h_while,
                          cudaGraphConditionalHandle h_if) {
   PF_PDL_ENTRY();
@@ -825,7 +820,7 @@ __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_jacobi_n
 
 // Ordered allreduce of per-subdomain sums: out = sqrt(((0 + s_0) + s_1) + ...)
 // (ascending rank, transport.cpp:139-149), optionally without the sqrt.
-__global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* out, int take_sqrt) {
+static __global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* out, int take_sqrt) {
   PF_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0.0;
@@ -835,8 +830,14 @@ __global__ void k_ordered_sum(const double* __restrict__ parts, int n, double* o
 
 // x_f += P x_c over every local fine dof (multigrid.cpp:121-129 + :183-184): the
 // correction is accumulated from 0 in P's entry order, then added.
+#ifndef PF_PROLONG_MINB
+#define PF_PROLONG_MINB PF_ROW_MINB
+#endif
+#ifndef PF_RESTRICT_MINB
+#define PF_RESTRICT_MINB PF_ROW_MINB
+#endif
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_prolong_add(SellView P, const double* __restrict__ xc,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_PROLONG_MINB)) k_prolong_add(SellView P, const double* __restrict__ xc,
                                                         double* __restrict__ xf, int32_t n_f, int add) {
   vtab_stage<kVK>(P);
   const int32_t row = blockIdx.x * kBlock + threadIdx.x;
@@ -860,7 +861,7 @@ __global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_prolong_
 // zeroed.  (Zeroing before the master/slave accumulate is equivalent: Dirichlet
 // carriers are Dirichlet on every rank, so they only ever accumulate zeros.)
 template <int kVK>
-__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_ROW_MINB)) k_restrict(SellView R, const double* __restrict__ rf,
+__global__ void __launch_bounds__(kBlock, minb_for<kVK>(PF_RESTRICT_MINB)) k_restrict(SellView R, const double* __restrict__ rf,
                                                      double* __restrict__ bc,
                                                      double* __restrict__ xc,
                                                      const uint8_t* __restrict__ is_dir_c,
@@ -926,7 +927,7 @@ __global__ void __launch_bounds__(kBlock) k_residual_restrict(SellView A, SellVi
 // ascending-rank sum; stop at <= tol * r0 or max_iter.  One thread: the coarse level of
 // the n_coarse=2 hierarchies holds one unknown, and a sequential sweep is the only way
 // to keep the reference's exact ordering.  stats: [iterations, converged, r0, final].
-__device__ void coarse_gs_body(const CoarseSub* __restrict__ subs, int n_sub, double* x,
+static __device__ void coarse_gs_body(const CoarseSub* __restrict__ subs, int n_sub, double* x,
                                const double* __restrict__ b, const int32_t* __restrict__ ms_dst,
                                const int32_t* __restrict__ ms_src, int32_t ms_n,
                                const int32_t* __restrict__ h1_dst, const int32_t* __restrict__ h1_src,
@@ -996,7 +997,7 @@ __device__ void coarse_gs_body(const CoarseSub* __restrict__ subs, int n_sub, do
 // by thread 0 in row order); the Gauss-Seidel sweep visits the rows in order with warp 0:
 // its lanes form the row's products a_e x_c from the current x, lane 0 subtracts them in
 // stored order.  Same operations in the same order as coarse_gs_body.
-__device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __restrict__ b, double tol,
+static __device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __restrict__ b, double tol,
                                int32_t max_iter, double* stats, unsigned char* smem) {
   double* sx = reinterpret_cast<double*>(smem);
   double* sb = sx + P.n_total;
@@ -1134,14 +1135,14 @@ __device__ void coarse_gs_smem(const CoarsePack& P, double* x, const double* __r
   for (int i = threadIdx.x; i < P.n_total; i += blockDim.x) x[i] = sx[i];
 }
 
-__global__ void k_coarse_smem(CoarsePack P, double* x, const double* __restrict__ b, double tol,
+static __global__ void k_coarse_smem(CoarsePack P, double* x, const double* __restrict__ b, double tol,
                               int32_t max_iter, double* stats) {
   PF_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem_c[];
   coarse_gs_smem(P, x, b, tol, max_iter, stats, smem_c);
 }
 
-__global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, double* x,
+static __global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, double* x,
                             const double* __restrict__ b, const int32_t* __restrict__ ms_dst,
                             const int32_t* __restrict__ ms_src, int32_t ms_n,
                             const int32_t* __restrict__ h1_dst, const int32_t* __restrict__ h1_src,
@@ -1154,25 +1155,25 @@ __global__ void k_coarse_gs(const CoarseSub* __restrict__ subs, int n_sub, doubl
 // ------------------------------------------------------------- vector utilities --
 
 // Host order -> device order: dev[perm[i]] = host[i].
-__global__ void k_scatter_perm(const double* __restrict__ host, const int32_t* __restrict__ perm,
+static __global__ void k_scatter_perm(const double* __restrict__ host, const int32_t* __restrict__ perm,
                                double* __restrict__ dev, int32_t n) {
   PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i < n) dev[perm[i]] = host[i];
 }
 // Device order -> host order: host[i] = dev[perm[i]].
-__global__ void k_gather_perm(const double* __restrict__ dev, const int32_t* __restrict__ perm,
+static __global__ void k_gather_perm(const double* __restrict__ dev, const int32_t* __restrict__ perm,
                               double* __restrict__ host, int32_t n) {
   PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i < n) host[i] = dev[perm[i]];
 }
-__global__ void k_fill(double* __restrict__ v, double value, int64_t n) {
+static __global__ void k_fill(double* __restrict__ v, double value, int64_t n) {
   PF_PDL_ENTRY();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
   if (i < n) v[i] = value;
 }
-__global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst, int64_t n) {
+static __global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst, int64_t n) {
   PF_PDL_ENTRY();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
   if (i < n) dst[i] = src[i];
@@ -1183,21 +1184,21 @@ __global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst,
 
 // Local transport of one scatter: v[dst[i]] = v[src[i]] (pack + send + recv + unpack of
 // fecomm.cpp:25-39 when every peer lives on this device).
-__global__ void k_copy_idx(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+static __global__ void k_copy_idx(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                            double* v, int32_t n) {
   PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i < n) v[dst[i]] = v[src[i]];
 }
 // Pack: buf[i] = v[idx[i]] (send side of scatter, fecomm.cpp:28-32).
-__global__ void k_pack(const double* __restrict__ v, const int32_t* __restrict__ idx,
+static __global__ void k_pack(const double* __restrict__ v, const int32_t* __restrict__ idx,
                        double* __restrict__ buf, int32_t n) {
   PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i < n) buf[i] = v[idx[i]];
 }
 // Unpack: v[idx[i]] = buf[i] (receive side of scatter, fecomm.cpp:33-38).
-__global__ void k_unpack(const double* __restrict__ buf, const int32_t* __restrict__ idx,
+static __global__ void k_unpack(const double* __restrict__ buf, const int32_t* __restrict__ idx,
                          double* __restrict__ v, int32_t n) {
   PF_PDL_ENTRY();
   const int32_t i = blockIdx.x * kBlock + threadIdx.x;
@@ -1206,7 +1207,7 @@ __global__ void k_unpack(const double* __restrict__ buf, const int32_t* __restri
 // Accumulate (fecomm.cpp:43-59): master entry m receives its slave partials in ascending
 // peer order: v[dst[m]] = ((v + p_a) + p_b) + ...  with the partials' buffer positions
 // listed per master in src[acc_off[m] .. acc_off[m+1]).
-__global__ void k_unpack_accumulate(const double* __restrict__ buf,
+static __global__ void k_unpack_accumulate(const double* __restrict__ buf,
                                     const int32_t* __restrict__ acc_off,
                                     const int32_t* __restrict__ src,
                                     const int32_t* __restrict__ dst, double* __restrict__ v,

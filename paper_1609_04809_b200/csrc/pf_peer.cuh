@@ -105,7 +105,7 @@ __device__ __forceinline__ bool peer_wait(const PeerArgs& a, const unsigned long
 // for its predecessor (PDL) but never releases its dependents early: a dependent grid
 // parked on griddepcontrol.wait would hold SM slots that a peer sharing this GPU needs to
 // deliver the message this kernel waits for.
-__global__ void __launch_bounds__(kPeerBlock) k_peer_exchange(PeerArgs a, double* __restrict__ v) {
+static __global__ void __launch_bounds__(kPeerBlock) k_peer_exchange(PeerArgs a, double* __restrict__ v) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ int s_ok;
   __shared__ unsigned long long s_seq;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kPeerBlock) k_peer_exchange(PeerArgs a, double
 
 // After a wait_only exchange and the kernel that consumed the staging: acknowledge every
 // receiving group (one thread per group).
-__global__ void k_peer_ack(PeerArgs a) {
+static __global__ void k_peer_ack(PeerArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n_recvs) return;

@@ -1,4 +1,6 @@
-// pf_runtime.cu — host runtime and C-ABI of the B200 GMG V-cycle hot path.
+// pf_runtime.cu — launches, CUDA graphs and the core C ABI of the B200 GMG V-cycle hot path
+// (the device layout is built by pf_build.cu, the heat / operator / load ABI lives in
+// pf_ops.cu; shared declarations in pf_internal.hpp).
 //
 // Maps the reference's hot-path API onto sm_100a kernels:
 //   spmv / residual_norm            linalg.cpp:45-74     -> k_spmv / k_resnorm
@@ -29,32 +31,35 @@
 #include <string>
 #include <vector>
 
-#include "pf_assembly.cuh"
 #include "pf_bottom.cuh"
-#include "pf_heat.cuh"
 #include "pf_kernels.cuh"
 #include "pf_nccl.hpp"
 #include "pf_sweep_tma.cuh"
+#include "pf_internal.hpp"
 #include "pf_runtime.hpp"
+
+using namespace pf;
+
 
 using namespace pf;
 
 namespace pf {
 
 thread_local std::string g_last_error;
+void set_error(const char* m) { g_last_error = m; }
 
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     throw Error(PF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-namespace {
+namespace rt {
+
+thread_local int64_t* g_capture_counter = nullptr;
 
 double wall_now() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
-
-inline unsigned grid_for(int64_t n) { return static_cast<unsigned>((n + kBlock - 1) / kBlock); }
 
 int sm_count(int device) {
   static int cached[64] = {};
@@ -66,7 +71,7 @@ int sm_count(int device) {
 [[noreturn]] void invalid(const std::string& m) { throw Error(PF_ERR_INVALID_ARGUMENT, m); }
 
 // PF_TRACE=1: one stderr line per major host step (debugging integrations).
-void trace(const char* what, int rank = -1) {
+void trace(const char* what, int rank) {
   static const bool on = std::getenv("PF_TRACE") != nullptr;
   if (!on) return;
   if (rank < 0) {
@@ -86,1180 +91,29 @@ bool pdl_enabled() {
   return on;
 }
 
-struct Launcher {
-  pf_hierarchy* h;
-  int64_t* counter;
-  cudaStream_t stream = nullptr;  // default: the hierarchy's stream
-  size_t smem = 0;                // dynamic shared memory of the next launch (with_smem)
-  Launcher& with_smem(size_t bytes) {
-    smem = bytes;
-    return *this;
-  }
-  template <typename... KArgs, typename... Args>
-  void operator()(unsigned grid, unsigned block, void (*kern)(KArgs...), Args... args) {
-    if (grid == 0) return;
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(block);
-    lc.dynamicSmemBytes = smem;
-    smem = 0;
-    lc.stream = stream ? stream : h->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    lc.attrs = attr;
-    lc.numAttrs = pdl_enabled() ? 1 : 0;
-    PF_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...));
-    ++*counter;
-  }
-};
-
-// While a graph is being captured, kernel launches are counted into the graph entry.
-thread_local int64_t* g_capture_counter = nullptr;
-
-Launcher launcher(pf_hierarchy* h, cudaStream_t stream = nullptr) {
-  return Launcher{h, g_capture_counter ? g_capture_counter : &h->launches, stream};
-}
-
-}  // namespace
-
-// Kernel-launch accounting and the PDL switch for launches made outside this file
-// (pf_peer.cu).
-int64_t* launch_counter(pf_hierarchy* h) { return g_capture_counter ? g_capture_counter : &h->launches; }
-bool pdl_on() { return pdl_enabled(); }
-// pf_peer.cu
-int64_t peer_export(pf_hierarchy* h, void* buf, int64_t cap);
-void peer_import(pf_hierarchy* h, const void* blobs, int64_t stride);
-
-namespace {
-
-SellView view_of(const DevVals& v, const DevSell& s) {
-  const void* idx = v.vkind == 1 ? static_cast<const void*>(v.vi8.p)
-                  : v.vkind == 2 ? static_cast<const void*>(v.vi16.p) : nullptr;
-  return SellView{v.vals.p, s.cols.p, s.slice_ptr.p, s.row_len.p, idx, v.table.p, v.vkind,
-                  static_cast<int32_t>(v.table.n)};
-}
-SellView view(const DevSell& s) { return view_of(s.vals, s); }
-
-// Kernel instantiation for a view's value kind: f(std::integral_constant<int, kind>).
-template <typename F>
-void vk_dispatch(int vkind, F&& f) {
-  switch (vkind) {
-    case 1: f(std::integral_constant<int, 1>{}); break;
-    case 2: f(std::integral_constant<int, 2>{}); break;
-    default: f(std::integral_constant<int, 0>{}); break;
-  }
-}
-
-// PF_VTAB_SMEM=0: the row kernels read an 8-bit index's value through L1 (__ldg) instead
-// of the shared-memory copy of the table.
-bool vtab_smem() {
-  static const bool on = [] {
-    const char* e = std::getenv("PF_VTAB_SMEM");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
-}
-
-// Operators of the levels below the finest up to PF_CACHED_MAX_BYTES (default 48 MB, about
-// 40 % of the 126 MB L2) are read with the caching load policy (kVKCached): they stay
-// L2-resident across the sweeps of a cycle.  The finest level, and larger ones, stream
-// evict-first.
-int64_t cached_max_bytes() {
-  static const int64_t m = [] {
-    const char* e = std::getenv("PF_CACHED_MAX_BYTES");
-    return e ? std::atoll(e) : int64_t(48) << 20;
-  }();
-  return m;
-}
-
-// vk_dispatch for the operator row kernels (they stage the value table, vtab_stage, and
-// pick the load policy from the kVKCached bit).
-template <typename F>
-void vk_dispatch_rows(const DevSell& S, F&& f) {
-  const bool cached = S.keep_l2;
-  const int kind = S.vals.vkind == 1 && vtab_smem() ? kVKSmem : S.vals.vkind;
-  switch (kind | (cached ? kVKCached : 0)) {
-    case 1: f(std::integral_constant<int, 1>{}); break;
-    case 2: f(std::integral_constant<int, 2>{}); break;
-    case kVKSmem: f(std::integral_constant<int, kVKSmem>{}); break;
-    case kVKCached: f(std::integral_constant<int, kVKCached>{}); break;
-    case 1 | kVKCached: f(std::integral_constant<int, 1 | kVKCached>{}); break;
-    case 2 | kVKCached: f(std::integral_constant<int, 2 | kVKCached>{}); break;
-    case kVKSmem | kVKCached: f(std::integral_constant<int, kVKSmem | kVKCached>{}); break;
-    default: f(std::integral_constant<int, 0>{}); break;
-  }
-}
-
-bool value_index_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PF_VALUE_INDEX");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
-}
-
-// Every operator with at least PF_VALUE_INDEX_MIN stored entries (default: all) is
-// index-encoded when its values allow it.  Measured at C2: encoding only the >= 2M-entry
-// operators, Jacobi solve 6.08 ms; all of them, 5.86 ms — the smaller levels' operators
-// take less L2 space and fewer L1 requests too (the shared-memory table lookup replaces
-// an 8-byte value load); the bottom kernel gets decoded fp64 copies (fp64_view).
-int64_t value_index_min_entries() {
-  static const int64_t m = [] {
-    const char* e = std::getenv("PF_VALUE_INDEX_MIN");
-    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(0);
-  }();
-  return m;
-}
-
-// Stored values (SELL order, padding included) -> device: an 8/16-bit index into the table
-// of distinct values (distinguished by bit pattern, so -0.0 and 0.0 stay apart) when there
-// are at most 65,536 of them, else fp64.
-// PF_TIMING=1: host-side phase times of pf_hierarchy_finalize on stderr (large grids)
-struct PhaseTimer {
-  bool on = std::getenv("PF_TIMING") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void operator()(const char* what, int level) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[pf_timing] level %d %-22s %8.3f s\n", level, what,
-                 std::chrono::duration<double>(now - t).count());
-    t = now;
-  }
-};
-
-void encode_values(const std::vector<double>& sv, DevVals& out) {
-  out = DevVals{};
-  if (value_index_enabled() && !sv.empty() && static_cast<int64_t>(sv.size()) >= value_index_min_entries()) {
-    // pass 1: the distinct values in first-seen order, giving up past 65,536.  Each chunk
-    // collects its own first-seen list; merging the lists in chunk order gives the
-    // sequential first-seen order.
-    const int64_t n = static_cast<int64_t>(sv.size());
-    const int nchunk = std::max(1, std::min<int>(omp_get_max_threads(), static_cast<int>(n / (1 << 20)) + 1));
-    std::vector<std::vector<uint64_t>> firsts(static_cast<size_t>(nchunk));
-    std::vector<int> overflow(static_cast<size_t>(nchunk), 0);
-#pragma omp parallel for schedule(static, 1)
-    for (int c = 0; c < nchunk; ++c) {
-      std::unordered_set<uint64_t> seen;
-      const int64_t lo = n * c / nchunk, hi = n * (c + 1) / nchunk;
-      for (int64_t i = lo; i < hi; ++i) {
-        uint64_t bits;
-        std::memcpy(&bits, &sv[static_cast<size_t>(i)], sizeof bits);
-        if (seen.insert(bits).second) {
-          firsts[static_cast<size_t>(c)].push_back(bits);
-          if (seen.size() > 65536) {
-            overflow[static_cast<size_t>(c)] = 1;
-            break;
-          }
-        }
-      }
-    }
-    std::unordered_map<uint64_t, uint32_t> ids;
-    std::vector<double> table;
-    bool fits = std::find(overflow.begin(), overflow.end(), 1) == overflow.end();
-    for (int c = 0; c < nchunk && fits; ++c)
-      for (uint64_t bits : firsts[static_cast<size_t>(c)]) {
-        if (ids.find(bits) != ids.end()) continue;
-        if (table.size() == 65536) {
-          fits = false;
-          break;
-        }
-        ids.emplace(bits, static_cast<uint32_t>(table.size()));
-        double v;
-        std::memcpy(&v, &bits, sizeof v);
-        table.push_back(v);
-      }
-    if (fits) {  // pass 2: the indices
-      out.table.upload(table);
-      if (table.size() <= 256) {
-        out.vkind = 1;
-        std::vector<uint8_t> idx(sv.size());
-#pragma omp parallel for schedule(static)
-        for (int64_t i = 0; i < n; ++i) {
-          uint64_t bits;
-          std::memcpy(&bits, &sv[static_cast<size_t>(i)], sizeof bits);
-          idx[static_cast<size_t>(i)] = static_cast<uint8_t>(ids.find(bits)->second);
-        }
-        out.vi8.upload(idx);
-      } else {
-        out.vkind = 2;
-        std::vector<uint16_t> idx(sv.size());
-#pragma omp parallel for schedule(static)
-        for (int64_t i = 0; i < n; ++i) {
-          uint64_t bits;
-          std::memcpy(&bits, &sv[static_cast<size_t>(i)], sizeof bits);
-          idx[static_cast<size_t>(i)] = static_cast<uint16_t>(ids.find(bits)->second);
-        }
-        out.vi16.upload(idx);
-      }
-      return;
-    }
-  }
-  out.vkind = 0;
-  out.vals.upload(sv);
-}
-
-void check_level(const pf_hierarchy* h, int level) {
-  if (!h) invalid("null hierarchy");
-  if (!h->finalized) state("hierarchy not finalized");
-  if (level < 0 || level >= h->n_levels) invalid("level " + std::to_string(level) + " out of range");
-}
-
-void check_vec(const pf_hierarchy* h, const pf_vector* v, int level, const char* what) {
-  if (!v) invalid(std::string(what) + ": null vector");
-  if (v->h != h) invalid(std::string(what) + ": vector belongs to another hierarchy");
-  if (v->level != level)
-    invalid(std::string("vector length does not match mapper dof count (") + what + ": level " +
-            std::to_string(v->level) + " vs " + std::to_string(level) + ")");
-}
-
-// ------------------------------------------------------------------ upload --
-
-// SELL-32 from rows already in device order (entry order inside a row is preserved).
-void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vector<int32_t>& col,
-                    const std::vector<double>& val, DevSell& out) {
-  const int64_t n_slices = (n + kSlice - 1) / kSlice;
-  std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
-  std::vector<int32_t> rlen(static_cast<size_t>(std::max<int64_t>(n_slices, 1) * kSlice), 0);
-  for (int32_t d = 0; d < n; ++d) rlen[d] = static_cast<int32_t>(off[d + 1] - off[d]);
-  for (int64_t s = 0; s < n_slices; ++s) {
-    int32_t w = 0;
-    for (int l = 0; l < kSlice; ++l) w = std::max(w, rlen[s * kSlice + l]);
-    w = (w + kGroup - 1) / kGroup * kGroup;  // SELL-32x4: whole groups of 4
-    sptr[s + 1] = sptr[s] + static_cast<int64_t>(w) * kSlice;
-  }
-  std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
-  std::vector<int32_t> sc(static_cast<size_t>(sptr[n_slices]), 0);
-#pragma omp parallel for schedule(static)
-  for (int64_t s = 0; s < n_slices; ++s) {
-    const int64_t w = (sptr[s + 1] - sptr[s]) / kSlice;
-    for (int l = 0; l < kSlice; ++l) {
-      const int64_t d = s * kSlice + l;
-      const int32_t len = d < n ? rlen[d] : 0;
-      for (int64_t j = 0; j < w; ++j) {
-        const int64_t e = sell_entry(sptr[s] + static_cast<int64_t>(l) * kGroup, static_cast<int>(j));
-        if (j < len) {
-          sc[e] = col[off[d] + j];
-          sv[e] = val[off[d] + j];
-        } else {  // padding, never read (row_len bounds every loop)
-          sc[e] = 0;
-          sv[e] = 0.0;
-        }
-      }
-    }
-  }
-  out.slice_ptr.upload(sptr);
-  out.row_len.upload(rlen);
-  out.max_len = rlen.empty() ? 0 : *std::max_element(rlen.begin(), rlen.end());
-  encode_values(sv, out.vals);
-  out.cols.upload(sc);
-  out.nnz = n > 0 ? off[n] : 0;
-  out.stored = sptr[n_slices];
-}
-
-// SELL-32x4 of a host CSR whose device row d is host row inv[d] and whose columns map
-// through perm; entry order inside a row preserved.
-void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector<int32_t>& perm,
-                   const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
-                   const std::vector<double>& vals, DevSell& out) {
-  const int64_t n_slices = (n + kSlice - 1) / kSlice;
-  std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
-  std::vector<int32_t> rlen(static_cast<size_t>(std::max<int64_t>(n_slices, 1) * kSlice), 0);
-#pragma omp parallel for schedule(static)
-  for (int32_t d = 0; d < n; ++d) rlen[d] = static_cast<int32_t>(rowptr[inv[d] + 1] - rowptr[inv[d]]);
-  for (int64_t s = 0; s < n_slices; ++s) {
-    int32_t w = 0;
-    for (int l = 0; l < kSlice; ++l) w = std::max(w, rlen[s * kSlice + l]);
-    w = (w + kGroup - 1) / kGroup * kGroup;
-    sptr[s + 1] = sptr[s] + static_cast<int64_t>(w) * kSlice;
-  }
-  // columns, then values, one host array at a time (peak host memory on large grids)
-  {
-    std::vector<int32_t> sc(static_cast<size_t>(sptr[n_slices]), 0);
-#pragma omp parallel for schedule(static)
-    for (int32_t d = 0; d < n; ++d) {
-      const int64_t base = sell_row_base(sptr.data(), d), k0 = rowptr[inv[d]];
-      for (int j = 0; j < rlen[d]; ++j) sc[static_cast<size_t>(sell_entry(base, j))] = perm[cols[static_cast<size_t>(k0 + j)]];
-    }
-    out.cols.upload(sc);
-  }
-  {
-    std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
-#pragma omp parallel for schedule(static)
-    for (int32_t d = 0; d < n; ++d) {
-      const int64_t base = sell_row_base(sptr.data(), d), k0 = rowptr[inv[d]];
-      for (int j = 0; j < rlen[d]; ++j) sv[static_cast<size_t>(sell_entry(base, j))] = vals[static_cast<size_t>(k0 + j)];
-    }
-    encode_values(sv, out.vals);
-  }
-  out.slice_ptr.upload(sptr);
-  out.row_len.upload(rlen);
-  out.max_len = rlen.empty() ? 0 : *std::max_element(rlen.begin(), rlen.end());
-  out.nnz = n > 0 ? rowptr[n] : 0;
-  out.stored = sptr[n_slices];
-}
-
-// PF_INTERLEAVE_MIN_BYTES (default 64 MB): levels whose x is at least this large run their
-// full-level Jacobi / residual passes with the colour-interleaved block schedule (0: every
-// level with 2-8 colours; a huge value: never).
-int64_t interleave_min_bytes() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("PF_INTERLEAVE_MIN_BYTES");
-    return e ? std::atoll(e) : int64_t(64) << 20;
-  }();
-  return v;
-}
-
-// Device layout of one subdomain level: own rows colour-major (stable in host order),
-// then every other row in host order; SELL-32x4 operator; P (rows of this level).
-void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
-  PhaseTimer tm;
-  const int32_t n = H.n, n_own = H.n_own;
-  D.n = n;
-  D.n_own = n_own;
-  // --- diagonal check (check_diagonal, solvers.cpp:10-15) and column sanity
-  for (int32_t r = 0; r < n; ++r) {
-    if (H.rowptr[r + 1] < H.rowptr[r]) invalid("row offsets must be non-decreasing");
-  }
-  {
-    const int64_t nnz = H.rowptr[n];
-    int bad = 0;
-#pragma omp parallel for schedule(static) reduction(| : bad)
-    for (int64_t k = 0; k < nnz; ++k) bad |= (H.cols[k] < 0 || H.cols[k] >= n) ? 1 : 0;
-    if (bad) invalid("column index out of range");
-    int32_t first_zero = INT32_MAX;
-#pragma omp parallel for schedule(static) reduction(min : first_zero)
-    for (int32_t r = 0; r < n_own; ++r) {
-      double diag = 0.0;
-      for (int64_t k = H.rowptr[r]; k < H.rowptr[r + 1]; ++k)
-        if (H.cols[k] == r) diag = H.vals[k];
-      if (diag == 0.0) first_zero = std::min(first_zero, r);
-    }
-    if (first_zero != INT32_MAX)
-      throw Error(PF_ERR_SINGULAR_DIAGONAL, "zero diagonal at own dof " + std::to_string(first_zero) +
-                                                " (level " + std::to_string(level) + ")");
-  }
-  tm("checks", level);
-  // --- colours of own rows
-  std::vector<int32_t> color(static_cast<size_t>(n_own), 0);
-  if (!H.color.empty()) {
-    for (int32_t i = 0; i < n_own; ++i) {
-      if (H.color[i] < 0) invalid("negative colour");
-      color[i] = H.color[i];
-    }
-    // a colour class must be an independent set of the own-row graph
-    int64_t first_bad = INT64_MAX;
-#pragma omp parallel for schedule(static) reduction(min : first_bad)
-    for (int32_t i = 0; i < n_own; ++i)
-      for (int64_t k = H.rowptr[i]; k < H.rowptr[i + 1]; ++k) {
-        const int32_t c = H.cols[k];
-        if (c != i && c < n_own && color[c] == color[i] && H.vals[k] != 0.0) first_bad = std::min(first_bad, k);
-      }
-    if (first_bad != INT64_MAX) {
-      const int32_t i = static_cast<int32_t>(std::upper_bound(H.rowptr.begin(), H.rowptr.end(), first_bad) - H.rowptr.begin() - 1);
-      invalid("colouring couples rows " + std::to_string(i) + " and " + std::to_string(H.cols[first_bad]));
-    }
-  } else {
-    std::vector<int32_t> seen;
-    for (int32_t i = 0; i < n_own; ++i) {
-      seen.clear();
-      for (int64_t k = H.rowptr[i]; k < H.rowptr[i + 1]; ++k) {
-        const int32_t c = H.cols[k];
-        if (c < i) seen.push_back(color[c]);
-      }
-      std::sort(seen.begin(), seen.end());
-      int32_t pick = 0;
-      for (int32_t s : seen) {
-        if (s == pick) ++pick;
-        else if (s > pick) break;
-      }
-      color[i] = pick;
-    }
-  }
-  int32_t n_colors = 0;
-  for (int32_t c : color) n_colors = std::max(n_colors, c + 1);
-  D.n_colors = n_colors;
-  D.color_start.assign(static_cast<size_t>(n_colors) + 1, 0);
-  for (int32_t c : color) ++D.color_start[c + 1];
-  for (int32_t c = 0; c < n_colors; ++c) D.color_start[c + 1] += D.color_start[c];
-  // --- permutation host -> device
-  D.perm.assign(static_cast<size_t>(n), 0);
-  std::vector<int32_t> inv(static_cast<size_t>(n), 0);
-  {
-    std::vector<int32_t> next(D.color_start.begin(), D.color_start.end() - 1);
-    if (H.order.empty()) {
-      for (int32_t i = 0; i < n_own; ++i) D.perm[i] = next[color[i]]++;
-    } else {  // placement hint: inside a colour, ascending (order, host index)
-      std::vector<int32_t> own(static_cast<size_t>(n_own));
-      std::iota(own.begin(), own.end(), 0);
-      // (colour, order, index) is a strict total order, so any sort gives the stable result
-      __gnu_parallel::sort(own.begin(), own.end(), [&](int32_t a, int32_t b) {
-        if (color[a] != color[b]) return color[a] < color[b];
-        if (H.order[a] != H.order[b]) return H.order[a] < H.order[b];
-        return a < b;
-      });
-      for (int32_t i : own) D.perm[i] = next[color[i]]++;
-    }
-    for (int32_t i = n_own; i < n; ++i) D.perm[i] = i;
-#pragma omp parallel for schedule(static)
-    for (int32_t i = 0; i < n; ++i) inv[D.perm[i]] = i;
-  }
-  D.d_perm.upload(D.perm);
-  // colour-interleaved block schedule when x outgrows L2 (RowMap, pf_types.hpp)
-  D.rmap = RowMap{};
-  D.rmap_grid = grid_for(n);
-  if (n_colors >= 2 && n_colors <= 8 && 8 * static_cast<int64_t>(n) >= interleave_min_bytes()) {
-    int32_t chunks = 0;
-    for (int c = 0; c < n_colors; ++c)
-      chunks = std::max<int32_t>(chunks, static_cast<int32_t>(grid_for(D.color_start[c + 1] - D.color_start[c])));
-    D.rmap.n_col = n_colors;
-    D.rmap.chunks = chunks;
-    for (int c = 0; c <= n_colors; ++c) D.rmap.start[c] = D.color_start[c];
-    D.rmap_grid = static_cast<unsigned>(chunks) * n_colors + grid_for(n - n_own);
-  }
-  tm("colours + perm", level);
-  // --- SELL-32x4 operator: rows in device order, columns mapped, entries in CSR order,
-  // written straight from the host CSR (no intermediate re-layout: at 512^3 the finest
-  // level alone is 44 GB of host CSR)
-  sell_from_csr(n, inv, D.perm, H.rowptr, H.cols, H.vals, D.A);
-  D.A.own_nnz = H.rowptr[n_own];
-  tm("sell", level);
-  D.csr_rowptr = H.rowptr;
-  D.sell_ptr.resize(static_cast<size_t>(D.A.slice_ptr.n));
-  if (D.A.slice_ptr.n > 0)
-    PF_CUDA(cudaMemcpy(D.sell_ptr.data(), D.A.slice_ptr.p, sizeof(int64_t) * D.sell_ptr.size(),
-                       cudaMemcpyDeviceToHost));
-  {
-    std::vector<uint8_t> touched(static_cast<size_t>(n), 0);
-    const int64_t z = H.rowptr[n_own];
-#pragma omp parallel for schedule(static)
-    for (int64_t k = 0; k < z; ++k) __atomic_store_n(&touched[static_cast<size_t>(H.cols[k])], 1, __ATOMIC_RELAXED);
-    D.own_cols_touched = std::count(touched.begin(), touched.end(), 1);
-  }
-  // --- Dirichlet mask in device order
-  std::vector<uint8_t> isdir(static_cast<size_t>(n), 0);
-  for (int32_t i = 0; i < n; ++i) isdir[D.perm[i]] = H.is_dir.empty() ? 0 : H.is_dir[i];
-  D.d_is_dir.upload(isdir);
-  // --- residual-norm scratch
-  D.resnorm_blocks = std::max<int>(1, static_cast<int>(grid_for(n_own)));
-  // partials serve k_resnorm (grid over own rows) and k_jacobi_norm (grid over all rows)
-  D.partials.alloc(std::max<int64_t>(D.resnorm_blocks, grid_for(n)));
-  D.ticket.alloc(1);
-  PF_CUDA(cudaMemset(D.ticket.p, 0, sizeof(unsigned int)));
-  tm("touched + masks", level);
-}
-
-// P rows of the fine level in device order; R = P^T over owns_row fine rows as a
-// parent-row gather with entries in ascending fine host index.
-void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const DevLevel& DC) {
-  const int32_t nf = F.n, nc = Cc.n;
-  if (F.p_off.size() != static_cast<size_t>(nf) + 1) invalid("prolongation needs n_dofs + 1 offsets");
-  for (int64_t e = 0; e < F.p_off[nf]; ++e)
-    if (F.p_col[e] < 0 || F.p_col[e] >= nc) invalid("prolongation column out of the parent level");
-  std::vector<int32_t> inv_f(static_cast<size_t>(nf));
-#pragma omp parallel for schedule(static)
-  for (int32_t i = 0; i < nf; ++i) inv_f[DF.perm[i]] = i;
-  std::vector<int64_t> poff(static_cast<size_t>(nf) + 1, 0);
-  for (int32_t d = 0; d < nf; ++d) poff[d + 1] = poff[d] + (F.p_off[inv_f[d] + 1] - F.p_off[inv_f[d]]);
-  std::vector<int32_t> pcol(static_cast<size_t>(poff[nf]));
-  std::vector<double> pw(static_cast<size_t>(poff[nf]));
-#pragma omp parallel for schedule(static)
-  for (int32_t d = 0; d < nf; ++d) {
-    const int32_t hr = inv_f[d];
-    int64_t q = poff[d];
-    for (int64_t e = F.p_off[hr]; e < F.p_off[hr + 1]; ++e, ++q) {
-      pcol[static_cast<size_t>(q)] = DC.perm[F.p_col[e]];
-      pw[static_cast<size_t>(q)] = F.p_w[e];
-    }
-  }
-  sell_from_rows(nf, poff, pcol, pw, DF.P);
-  // R rows: each parent row's contributions in ascending fine host index (the reference's
-  // scatter-add order).  The owned P entries in fine host order, sorted by (parent device
-  // row, position) — a strict order, so the parallel sort reproduces the counting sort.
-  std::vector<int64_t> src;      // positions e of owned entries, ascending (= fine host order)
-  std::vector<int32_t> fine_of;  // their fine host rows
-  {
-    std::vector<int64_t> cnt(static_cast<size_t>(nf) + 1, 0);
-#pragma omp parallel for schedule(static)
-    for (int32_t f = 0; f < nf; ++f) cnt[f + 1] = F.owns_row[f] ? F.p_off[f + 1] - F.p_off[f] : 0;
-    for (int32_t f = 0; f < nf; ++f) cnt[f + 1] += cnt[f];
-    src.resize(static_cast<size_t>(cnt[nf]));
-    fine_of.resize(static_cast<size_t>(cnt[nf]));
-#pragma omp parallel for schedule(static)
-    for (int32_t f = 0; f < nf; ++f)
-      if (F.owns_row[f])
-        for (int64_t e = F.p_off[f], q = cnt[f]; e < F.p_off[f + 1]; ++e, ++q) {
-          src[static_cast<size_t>(q)] = e;
-          fine_of[static_cast<size_t>(q)] = f;
-        }
-  }
-  // keys (parent device row << 35 | position): distinct, so sorting them is the stable sort
-  std::vector<uint64_t> key(src.size());
-  if (static_cast<int64_t>(src.size()) >= (int64_t(1) << 35)) invalid("prolongation too large");
-#pragma omp parallel for schedule(static)
-  for (int64_t q = 0; q < static_cast<int64_t>(src.size()); ++q)
-    key[static_cast<size_t>(q)] = static_cast<uint64_t>(DC.perm[F.p_col[src[static_cast<size_t>(q)]]]) << 35 |
-                                  static_cast<uint64_t>(q);
-  __gnu_parallel::sort(key.begin(), key.end());
-  std::vector<int64_t> ord(src.size());
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < static_cast<int64_t>(key.size()); ++i)
-    ord[static_cast<size_t>(i)] = static_cast<int64_t>(key[static_cast<size_t>(i)] & ((uint64_t(1) << 35) - 1));
-  std::vector<uint64_t>().swap(key);
-  std::vector<int64_t> roff(static_cast<size_t>(nc) + 1, 0);
-  std::vector<int32_t> rcol(ord.size());
-  std::vector<double> rwt(ord.size());
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < static_cast<int64_t>(ord.size()); ++i) {
-    const int64_t q = ord[static_cast<size_t>(i)], e = src[static_cast<size_t>(q)];
-    rcol[static_cast<size_t>(i)] = DF.perm[fine_of[static_cast<size_t>(q)]];
-    rwt[static_cast<size_t>(i)] = F.p_w[e];
-  }
-  for (int64_t i = 0; i < static_cast<int64_t>(ord.size()); ++i)
-    ++roff[static_cast<size_t>(DC.perm[F.p_col[src[static_cast<size_t>(ord[static_cast<size_t>(i)])]]]) + 1];
-  for (int32_t c = 0; c < nc; ++c) roff[c + 1] += roff[c];
-  sell_from_rows(nc, roff, rcol, rwt, DF.R);
-}
-
-const HostChannel* find_channel(const HostLevel& H, int kind, int peer) {
-  for (const HostChannel& c : H.channels)
-    if (c.kind == kind && c.peer == peer) return &c;
-  return nullptr;
-}
-
-// Exchange plans of one level from the per-subdomain channel lists.  local: every peer
-// is one of the subdomains in H (ranks rank_base + s); else one subdomain whose peers
-// live in other processes (NCCL segments).
-// One scatter plan over a set of channel kinds (several kinds: one message group; their
-// send and receive sets must be independent — see build_fused_plans).
-void build_scatter_plan(const std::vector<HostLevel>& H, const std::vector<DevLevel>& D, int rank_base, bool local,
-                        const std::vector<int>& kinds, ExchangePlan& P) {
-  const int n_sub = static_cast<int>(H.size());
-  {
-    auto in = [&](int k) { return std::find(kinds.begin(), kinds.end(), k) != kinds.end(); };
-    if (local) {
-      std::vector<int32_t> dst, src;
-      for (int s = 0; s < n_sub; ++s) {
-        const int R = rank_base + s;
-        for (const HostChannel& c : H[s].channels) {
-          if (!in(c.kind) || c.recv.empty()) continue;
-          const int kind = c.kind;
-          const int p = c.peer - rank_base;
-          if (p < 0 || p >= n_sub || p == s) invalid("channel peer " + std::to_string(c.peer) + " out of range");
-          const HostChannel* pc = find_channel(H[p], kind, R);
-          if (!pc || pc->send.size() != c.recv.size())
-            throw Error(PF_ERR_TRANSPORT, "channel lists of kind " + std::to_string(kind) +
-                                              " between ranks " + std::to_string(c.peer) + " and " +
-                                              std::to_string(R) + " do not pair up");
-          for (size_t i = 0; i < c.recv.size(); ++i) {
-            dst.push_back(static_cast<int32_t>(D[s].offset + D[s].perm[c.recv[i]]));
-            src.push_back(static_cast<int32_t>(D[p].offset + D[p].perm[pc->send[i]]));
-          }
-        }
-      }
-      P.n = static_cast<int64_t>(dst.size());
-      P.dst.upload(dst);
-      P.src.upload(src);
-    } else {
-      const DevLevel& D0 = D[0];
-      std::vector<int32_t> pk, up;
-      for (const HostChannel& c : H[0].channels) {
-        if (!in(c.kind)) continue;
-        if (!c.send.empty()) {
-          P.send_segs.push_back({c.peer, static_cast<int64_t>(pk.size()), static_cast<int64_t>(c.send.size())});
-          for (int32_t d : c.send) pk.push_back(D0.perm[d]);
-        }
-        if (!c.recv.empty()) {
-          P.recv_segs.push_back({c.peer, static_cast<int64_t>(up.size()), static_cast<int64_t>(c.recv.size())});
-          for (int32_t d : c.recv) up.push_back(D0.perm[d]);
-        }
-      }
-      P.n = static_cast<int64_t>(up.size());
-      P.pack_idx.upload(pk);
-      P.unpack_idx.upload(up);
-      P.sendbuf.alloc(static_cast<int64_t>(pk.size()));
-      P.recvbuf.alloc(static_cast<int64_t>(up.size()));
-    }
-  }
-}
-
-void build_exchange(const std::vector<HostLevel>& H, const std::vector<DevLevel>& D, int rank_base,
-                    bool local, std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS>& scatter, ExchangePlan& A) {
-  const int n_sub = static_cast<int>(H.size());
-  for (int kind = 0; kind < PF_NUM_CHANNEL_KINDS; ++kind) build_scatter_plan(H, D, rank_base, local, {kind}, scatter[kind]);
-  // master/slave accumulate: slaves push v[recv_dofs], masters add in ascending peer order
-  std::map<int32_t, std::vector<int32_t>> contrib;  // master dst -> sources, peer-ascending
-  if (local) {
-    for (int s = 0; s < n_sub; ++s) {
-      const int R = rank_base + s;
-      std::vector<const HostChannel*> ms;
-      for (const HostChannel& c : H[s].channels)
-        if (c.kind == PF_CH_MASTER_SLAVE && !c.send.empty()) ms.push_back(&c);
-      std::sort(ms.begin(), ms.end(), [](const HostChannel* a, const HostChannel* b) { return a->peer < b->peer; });
-      for (const HostChannel* c : ms) {
-        const int p = c->peer - rank_base;
-        const HostChannel* pc = find_channel(H[p], PF_CH_MASTER_SLAVE, R);
-        if (!pc || pc->recv.size() != c->send.size())
-          throw Error(PF_ERR_TRANSPORT, "master/slave lists do not pair up");
-        for (size_t i = 0; i < c->send.size(); ++i)
-          contrib[static_cast<int32_t>(D[s].offset + D[s].perm[c->send[i]])].push_back(
-              static_cast<int32_t>(D[p].offset + D[p].perm[pc->recv[i]]));
-      }
-    }
-  } else {
-    const DevLevel& D0 = D[0];
-    std::vector<const HostChannel*> ms;
-    for (const HostChannel& c : H[0].channels)
-      if (c.kind == PF_CH_MASTER_SLAVE) ms.push_back(&c);
-    std::sort(ms.begin(), ms.end(), [](const HostChannel* a, const HostChannel* b) { return a->peer < b->peer; });
-    std::vector<int32_t> pk;
-    int64_t rpos = 0;
-    for (const HostChannel* c : ms) {
-      if (!c->recv.empty()) {  // slave side: push partial sums to the master
-        A.send_segs.push_back({c->peer, static_cast<int64_t>(pk.size()), static_cast<int64_t>(c->recv.size())});
-        for (int32_t d : c->recv) pk.push_back(D0.perm[d]);
-      }
-      if (!c->send.empty()) {  // master side
-        A.recv_segs.push_back({c->peer, rpos, static_cast<int64_t>(c->send.size())});
-        for (size_t i = 0; i < c->send.size(); ++i)
-          contrib[D0.perm[c->send[i]]].push_back(static_cast<int32_t>(rpos + static_cast<int64_t>(i)));
-        rpos += static_cast<int64_t>(c->send.size());
-      }
-    }
-    A.pack_idx.upload(pk);
-    A.sendbuf.alloc(static_cast<int64_t>(pk.size()));
-    A.recvbuf.alloc(rpos);
-  }
-  std::vector<int32_t> off{0}, srcs, dsts;
-  for (const auto& [d, list] : contrib) {
-    dsts.push_back(d);
-    srcs.insert(srcs.end(), list.begin(), list.end());
-    off.push_back(static_cast<int32_t>(srcs.size()));
-  }
-  A.n_masters = static_cast<int32_t>(dsts.size());
-  A.n = static_cast<int64_t>(srcs.size());
-  A.acc_off.upload(off);
-  A.acc_src.upload(srcs);
-  A.acc_dst.upload(dsts);
-}
-
-// Fused exchanges (pf_hierarchy_set_fused_exchanges): master/slave + halo1 as one message
-// group per sweep, + halo2 after a smoothing phase.  Valid when no halo send entry is a
-// master/slave receive entry of the same subdomain (the halo value would otherwise be the
-// one the master/slave scatter is still delivering) — pf_setup's direct_halos lists.
-void build_fused_plans(pf_hierarchy* h, int l) {
-  Level& L = h->levels[l];
-  for (const HostLevel& H : L.host) {
-    std::vector<uint8_t> slave(static_cast<size_t>(H.n), 0);
-    for (const HostChannel& c : H.channels)
-      if (c.kind == PF_CH_MASTER_SLAVE)
-        for (int32_t d : c.recv) slave[static_cast<size_t>(d)] = 1;
-    for (const HostChannel& c : H.channels)
-      if (c.kind != PF_CH_MASTER_SLAVE)
-        for (int32_t d : c.send)
-          if (slave[static_cast<size_t>(d)])
-            invalid("fused exchanges need halo lists that never forward a Slave-held value "
-                    "(level " + std::to_string(l) + "): build them with direct_halos");
-  }
-  const bool local = h->world == h->n_sub;
-  if (!local) {
-    // multi-process: the own rows whose values leave this rank (master/slave and halo
-    // sends) form the boundary set; a Jacobi sweep computes them first, starts the
-    // exchange on the side stream, and sweeps the interior rows meanwhile
-    const HostLevel& H = L.host[0];
-    DevLevel& D = L.sub[0];
-    std::vector<uint8_t> isb(static_cast<size_t>(D.n), 0);
-    for (const HostChannel& c : H.channels)
-      for (int32_t d : c.send)
-        if (d < H.n_own) isb[static_cast<size_t>(D.perm[d])] = 1;
-    std::vector<int32_t> list;
-    for (int32_t r = 0; r < D.n_own; ++r)
-      if (isb[static_cast<size_t>(r)]) list.push_back(r);
-    D.n_brows = static_cast<int32_t>(list.size());
-    D.brows.upload(list);
-    D.is_brow.upload(isb);
-    // coloured smoothers: the last colour's rows that send or read a non-own copy
-    if (D.n_colors >= 1) {
-      const int32_t c0 = D.color_start[D.n_colors - 1], c1 = D.color_start[D.n_colors];
-      std::vector<uint8_t> pre(static_cast<size_t>(D.n), 0);
-      for (int32_t r = c0; r < c1; ++r)
-        pre[static_cast<size_t>(r)] = isb[static_cast<size_t>(r)] || D.reads_nonown[static_cast<size_t>(r)];
-      std::vector<int32_t> pl;
-      for (int32_t r = c0; r < c1; ++r)
-        if (pre[static_cast<size_t>(r)]) pl.push_back(r);
-      D.n_cpre = static_cast<int32_t>(pl.size());
-      D.cpre.upload(pl);
-      D.is_cpre.upload(pre);
-    }
-    std::vector<uint8_t>().swap(D.reads_nonown);
-  }
-  build_scatter_plan(L.host, L.sub, h->rank_base, local, {PF_CH_MASTER_SLAVE, PF_CH_HALO1}, L.fused_ms_h1);
-  build_scatter_plan(L.host, L.sub, h->rank_base, local, {PF_CH_MASTER_SLAVE, PF_CH_HALO1, PF_CH_HALO2},
-                     L.fused_all);
-}
-
-void build_plans(pf_hierarchy* h, int l) {
-  Level& L = h->levels[l];
-  build_exchange(L.host, L.sub, h->rank_base, h->world == h->n_sub, L.scatter, L.accumulate);
-  if (h->fused) build_fused_plans(h, l);
-}
-
-// Pack a coarse level (all subdomains of H/D, level-global indices) for the shared-memory
-// coarse solve: own rows per subdomain in host order, entries in stored order.
-CoarsePack make_coarse_pack(const std::vector<HostLevel>& H, const std::vector<DevLevel>& D,
-                            const std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS>& plans,
-                            DevBuf<int32_t>& sub_rows, DevBuf<int32_t>& rowptr, DevBuf<int32_t>& rowdev,
-                            DevBuf<int32_t>& cols, DevBuf<double>& vals) {
-  std::vector<int32_t> sr{0}, rp{0}, rd, cc;
-  std::vector<double> vv;
-  int64_t total = 0;
-  for (size_t s = 0; s < H.size(); ++s) {
-    const HostLevel& h = H[s];
-    const DevLevel& d = D[s];
-    for (int32_t i = 0; i < h.n_own; ++i) {
-      rd.push_back(static_cast<int32_t>(d.offset + d.perm[i]));
-      for (int64_t k = h.rowptr[i]; k < h.rowptr[i + 1]; ++k) {
-        cc.push_back(static_cast<int32_t>(d.offset + d.perm[h.cols[k]]));
-        vv.push_back(h.vals[k]);
-      }
-      rp.push_back(static_cast<int32_t>(cc.size()));
-    }
-    sr.push_back(static_cast<int32_t>(rd.size()));
-    total = std::max<int64_t>(total, d.offset + d.n);
-  }
-  sub_rows.upload(sr);
-  rowptr.upload(rp);
-  rowdev.upload(rd);
-  cols.upload(cc);
-  vals.upload(vv);
-  CoarsePack P{};
-  P.n_total = static_cast<int32_t>(total);
-  P.n_rows = static_cast<int32_t>(rd.size());
-  P.nnz = static_cast<int32_t>(cc.size());
-  P.n_sub = static_cast<int32_t>(H.size());
-  P.sub_rows = sub_rows.p;
-  P.rowptr = rowptr.p;
-  P.rowdev = rowdev.p;
-  P.cols = cols.p;
-  P.vals = vals.p;
-  P.ms_dst = plans[PF_CH_MASTER_SLAVE].dst.p;
-  P.ms_src = plans[PF_CH_MASTER_SLAVE].src.p;
-  P.ms_n = static_cast<int32_t>(plans[PF_CH_MASTER_SLAVE].n);
-  P.h1_dst = plans[PF_CH_HALO1].dst.p;
-  P.h1_src = plans[PF_CH_HALO1].src.p;
-  P.h1_n = static_cast<int32_t>(plans[PF_CH_HALO1].n);
-  P.max_row = 0;
-  for (size_t i = 0; i + 1 < rp.size(); ++i) P.max_row = std::max(P.max_row, rp[i + 1] - rp[i]);
-  return P;
-}
-
-constexpr size_t kCoarseSmemMax = 160 * 1024;  // opt-in shared memory for the coarse pack
-
-HostLevel parse_desc(const pf_level_desc& dd, int me, int world, bool need_p) {
-  const pf_level_desc* d = &dd;
-  if (d->n_dofs < 0 || d->n_own_dofs < 0 || d->n_own_dofs > d->n_dofs) invalid("bad dof counts");
-  if (!d->row_offsets || (d->n_dofs > 0 && (!d->owns_row))) invalid("missing level arrays");
-  HostLevel H;
-  H.set = true;
-  H.n = d->n_dofs;
-  H.n_own = d->n_own_dofs;
-  const int64_t nnz = d->row_offsets[d->n_dofs];
-  if (d->row_offsets[0] != 0 || nnz < 0) invalid("row offsets must start at 0");
-  if (nnz > 0 && (!d->col_indices || !d->values)) invalid("missing matrix arrays");
-  H.rowptr.assign(d->row_offsets, d->row_offsets + d->n_dofs + 1);
-  H.cols.assign(d->col_indices, d->col_indices + nnz);
-  H.vals.assign(d->values, d->values + nnz);
-  H.owns_row.assign(d->owns_row, d->owns_row + d->n_dofs);
-  if (d->is_dirichlet) H.is_dir.assign(d->is_dirichlet, d->is_dirichlet + d->n_dofs);
-  else H.is_dir.assign(static_cast<size_t>(d->n_dofs), 0);
-  if (d->color) H.color.assign(d->color, d->color + d->n_own_dofs);
-  if (d->row_order) H.order.assign(d->row_order, d->row_order + d->n_dofs);
-  for (int i = 0; i < d->n_channels; ++i) {
-    const pf_channel_desc& c = d->channels[i];
-    if (c.kind < 0 || c.kind >= PF_NUM_CHANNEL_KINDS) invalid("bad channel kind");
-    if (c.peer < 0 || c.peer >= world || c.peer == me) invalid("bad channel peer");
-    HostChannel hc;
-    hc.kind = c.kind;
-    hc.peer = c.peer;
-    hc.send.assign(c.send_dofs, c.send_dofs + c.n_send);
-    hc.recv.assign(c.recv_dofs, c.recv_dofs + c.n_recv);
-    for (int32_t v : hc.send)
-      if (v < 0 || v >= d->n_dofs) invalid("channel send dof out of range");
-    for (int32_t v : hc.recv)
-      if (v < 0 || v >= d->n_dofs) invalid("channel recv dof out of range");
-    H.channels.push_back(std::move(hc));
-  }
-  std::sort(H.channels.begin(), H.channels.end(), [](const HostChannel& a, const HostChannel& b) {
-    return a.kind != b.kind ? a.kind < b.kind : a.peer < b.peer;
-  });
-  if (need_p) {
-    if (!d->p_offsets) invalid("level > 0 needs a prolongation map");
-    H.p_off.assign(d->p_offsets, d->p_offsets + d->n_dofs + 1);
-    const int64_t pn = H.p_off.back();
-    H.p_col.assign(d->p_cols, d->p_cols + pn);
-    H.p_w.assign(d->p_weights, d->p_weights + pn);
-  }
-  return H;
-}
-
-void build_replica(pf_hierarchy* h) {
-  auto& R = h->rep;
-  if (R.lv.empty() || R.lv[0].host.size() != static_cast<size_t>(h->world))
-    state("multi-process hierarchy needs pf_hierarchy_set_coarse_replica for every rank");
-  const int top = static_cast<int>(R.lv.size()) - 1;
-  if (top >= h->n_levels) invalid("more replicated levels than the hierarchy has");
-  int64_t max_stride = 1;
-  for (int l = 0; l <= top; ++l) {
-    auto& RL = R.lv[static_cast<size_t>(l)];
-    if (RL.host.size() != static_cast<size_t>(h->world)) state("replica level " + std::to_string(l) + " incomplete");
-    RL.sub.resize(static_cast<size_t>(h->world));
-    int64_t stride = 1;
-    for (int r = 0; r < h->world; ++r) {
-      if (!RL.host[r].set)
-        state("replica of rank " + std::to_string(r) + " level " + std::to_string(l) + " not set");
-      build_dev_level(RL.host[r], RL.sub[r], l);
-      stride = std::max<int64_t>(stride, RL.sub[r].n);
-    }
-    RL.stride = stride;
-    max_stride = std::max(max_stride, stride);
-    for (int r = 0; r < h->world; ++r) RL.sub[r].offset = r * stride;
-    const DevLevel& mine = h->levels[l].sub[0];
-    if (RL.sub[h->rank_base].n != mine.n || RL.sub[h->rank_base].perm != mine.perm)
-      invalid("replica of this rank differs from its own level " + std::to_string(l));
-    if (l > 0)
-      for (int r = 0; r < h->world; ++r)
-        build_transfer(RL.host[r], RL.sub[r], R.lv[static_cast<size_t>(l - 1)].host[r],
-                       R.lv[static_cast<size_t>(l - 1)].sub[r]);
-    build_exchange(RL.host, RL.sub, 0, true, RL.scatter, RL.acc);
-    RL.x.alloc(2 * stride * h->world);
-    RL.b.alloc(stride * h->world);
-    RL.r.alloc(stride * h->world);
-    PF_CUDA(cudaMemset(RL.x.p, 0, sizeof(double) * 2 * stride * h->world));
-    PF_CUDA(cudaMemset(RL.b.p, 0, sizeof(double) * stride * h->world));
-  }
-  auto& R0 = R.lv[0];
-  std::vector<CoarseSub> cs;
-  for (DevLevel& D : R0.sub) cs.push_back(CoarseSub{view(D.A), D.d_perm.p, D.n_own, D.offset});
-  R.subs.upload(cs);
-  R.cpack = make_coarse_pack(R0.host, R0.sub, R0.scatter, R.cp_sub_rows, R.cp_rowptr, R.cp_rowdev, R.cp_cols,
-                             R.cp_vals);
-  R.send.alloc(max_stride);
-  PF_CUDA(cudaMemset(R.send.p, 0, sizeof(double) * max_stride));
-  R.coarse_stats.alloc(4);
-  PF_CUDA(cudaMemset(R.coarse_stats.p, 0, 4 * sizeof(double)));
-  R.active = true;
-}
-
-// One level as the bottom kernel sees it.
-struct BotSrc {
-  const std::vector<DevLevel>* sub;
-  int64_t total;
-  const std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS>* scatter;
-  const ExchangePlan* acc;
-  double *x, *xa, *b, *r;
-};
-
-// The bottom kernel reads fp64 values (its latency-bound rows have one dependent load
-// fewer): an index-encoded operator of a bottom level gets a decoded fp64 copy (a few KB
-// to a few MB: the bottom levels are tiny), the same doubles the table holds.
-SellView fp64_view(pf_hierarchy::Bottom& bot, const DevSell& S) {
-  SellView v = view(S);
-  if (S.vals.vkind == 0) return v;
-  std::vector<double> table(static_cast<size_t>(S.vals.table.n));
-  PF_CUDA(cudaMemcpy(table.data(), S.vals.table.p, sizeof(double) * table.size(), cudaMemcpyDeviceToHost));
-  std::vector<double> vals(static_cast<size_t>(S.stored));
-  if (S.vals.vkind == 1) {
-    std::vector<uint8_t> ix(vals.size());
-    PF_CUDA(cudaMemcpy(ix.data(), S.vals.vi8.p, ix.size(), cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < vals.size(); ++i) vals[i] = table[ix[i]];
-  } else {
-    std::vector<uint16_t> ix(vals.size());
-    PF_CUDA(cudaMemcpy(ix.data(), S.vals.vi16.p, sizeof(uint16_t) * ix.size(), cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < vals.size(); ++i) vals[i] = table[ix[i]];
-  }
-  bot.val_bufs.emplace_back();
-  bot.val_bufs.back().upload(vals);
-  v.vals = bot.val_bufs.back().p;
-  v.vidx = nullptr;
-  v.table = nullptr;
-  v.vkind = 0;
-  v.table_n = 0;
-  return v;
-}
-
-// PF_BOTTOM_STAGE (default 1): stage the block levels in shared memory (BotStage).
-bool bottom_stage_enabled() {
-  const char* e = std::getenv("PF_BOTTOM_STAGE");  // read at build time (tests flip it)
-  return !(e && std::atoi(e) == 0);
-}
-
-// Plan and build the shared-memory staging of the block levels (BotStage, pf_bottom.cuh):
-// levels 0, 1, ... up to block_top are staged while they fit the opt-in shared memory next
-// to the descriptor and the coarse pack — each with its vectors, operator, restriction,
-// colour ranges, Dirichlet flags and plans; then the prolongations, lowest level first,
-// as far as they still fit (C2: levels 0-2 and every P but level 2's, ~200 KB).
-void stage_block_levels(pf_hierarchy* h, pf_hierarchy::Bottom& bot, BotDesc& d, const std::vector<BotSrc>& src) {
-  d.stage = BotStage{};
-  d.stage.hs = -1;
-  if (!bottom_stage_enabled() || d.block_top < 0) return;
-  int optin = 0;
-  PF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+size_t bottom_kernel_static_smem() {
   cudaFuncAttributes fa{};
   PF_CUDA(cudaFuncGetAttributes(&fa, k_bottom));
-  auto r16 = [](int64_t b) { return (b + 15) / 16 * 16; };
-  const int64_t smem_off = r16(sizeof(BotDesc)) + r16(static_cast<int64_t>(coarse_pack_smem(d.coarse)));
-  const int64_t budget = static_cast<int64_t>(optin) - static_cast<int64_t>(fa.sharedSizeBytes) - smem_off - 1024;
-  struct Piece {
-    const void* src;
-    int64_t bytes, off;
+  return fa.sharedSizeBytes;
+}
+void bottom_kernel_caps(int device) {
+  int optin = 0;
+  PF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  auto cap = [&](auto kern) {
+    cudaFuncAttributes fa{};
+    PF_CUDA(cudaFuncGetAttributes(&fa, kern));
+    PF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - static_cast<int>(fa.sharedSizeBytes)));
   };
-  std::vector<Piece> pieces;
-  std::vector<std::pair<void**, int64_t>> fix;  // field of t -> blob offset
-  int64_t used = 0, vec_bytes = 0;
-  BotDesc t = d;
-  auto add = [&](auto* field, const void* p, int64_t bytes) {  // field: a pointer member of t
-    if (!p || bytes <= 0) return;
-    pieces.push_back(Piece{p, bytes, used});
-    fix.push_back({(void**)field, used});  // C cast: the members are __restrict__-qualified
-    used += r16(bytes);
-  };
-  auto add_view = [&](SellView& v, const DevSell& S) {
-    const int64_t n_slices = static_cast<int64_t>(S.slice_ptr.n);
-    add(&v.cols, v.cols, S.stored * 4);
-    add(&v.slice_ptr, v.slice_ptr, n_slices * 8);
-    add(&v.row_len, v.row_len, S.row_len.bytes());
-    if (S.vals.vkind == 1) {  // the 8-bit value index and its table
-      v.vals = nullptr;
-      v.vkind = 1;
-      v.vidx = S.vals.vi8.p;
-      v.table = S.vals.table.p;
-      v.table_n = static_cast<int32_t>(S.vals.table.n);
-      add(&v.vidx, v.vidx, S.stored);
-      add(&v.table, v.table, S.vals.table.bytes());
-    } else {  // the decoded fp64 copy the descriptor already holds
-      add(&v.vals, v.vals, S.stored * 8);
-    }
-  };
-  auto plan = [&](BotPlan& P) {
-    add(&P.dst, P.dst, static_cast<int64_t>(P.n) * 4);
-    add(&P.src, P.src, static_cast<int64_t>(P.n) * 4);
-  };
-  int hs = -1;
-  for (int l = 0; l <= d.block_top; ++l) {
-    const size_t p0 = pieces.size();
-    const int64_t u0 = used;
-    bool ok = true;
-    const BotSrc& L = src[static_cast<size_t>(l)];
-    BotLevel& B = t.lev[l];
-    plan(B.ms);
-    plan(B.h1);
-    plan(B.h2);
-    if (B.acc_n > 0) {
-      add(&B.acc_off, B.acc_off, (static_cast<int64_t>(B.acc_n) + 1) * 4);
-      add(&B.acc_src, B.acc_src, L.acc->acc_src.bytes());
-      add(&B.acc_dst, B.acc_dst, static_cast<int64_t>(B.acc_n) * 4);
-    }
-    for (int s = 0; s < t.n_sub; ++s) {
-      const DevLevel& D = (*L.sub)[static_cast<size_t>(s)];
-      BotSub& S = t.sub[l][s];
-      if (D.A.max_len > kBotChunk) ok = false;
-      add_view(S.A, D.A);
-      if (l > 0) add_view(S.R, D.R);
-      add(&S.color_start, S.color_start, (static_cast<int64_t>(S.n_colors) + 1) * 4);
-      add(&S.is_dir, S.is_dir, D.d_is_dir.bytes());
-    }
-    const int64_t vb = 4 * r16(L.total * 8);
-    if (!ok || used + vec_bytes + vb > budget) {  // roll back level l and stop
-      pieces.resize(p0);
-      fix.resize(p0);
-      used = u0;
-      t.lev[l] = d.lev[l];
-      for (int s = 0; s < t.n_sub; ++s) t.sub[l][s] = d.sub[l][s];
-      break;
-    }
-    vec_bytes += vb;
-    hs = l;
-  }
-  if (hs < 0) return;
-  for (int l = 1; l <= hs; ++l)  // prolongations, as far as they fit
-    for (int s = 0; s < t.n_sub; ++s) {
-      const DevLevel& D = (*src[static_cast<size_t>(l)].sub)[static_cast<size_t>(s)];
-      const size_t p0 = pieces.size();
-      const int64_t u0 = used;
-      const BotSub keep = t.sub[l][s];
-      add_view(t.sub[l][s].P, D.P);
-      if (used + vec_bytes > budget) {
-        pieces.resize(p0);
-        fix.resize(p0);
-        used = u0;
-        t.sub[l][s] = keep;
-      }
-    }
-  bot.stage_blob.alloc(used);
-  for (const Piece& q : pieces)
-    PF_CUDA(cudaMemcpy(bot.stage_blob.p + q.off, q.src, static_cast<size_t>(q.bytes), cudaMemcpyDeviceToDevice));
-  for (auto& f : fix) *f.first = bot.stage_blob.p + f.second;
-  t.stage.blob = bot.stage_blob.p;
-  t.stage.blob_bytes = used;
-  t.stage.hs = hs;
-  t.stage.smem_off = smem_off;
-  int64_t off = used;
-  for (int l = 0; l <= hs; ++l)
-    for (int k = 0; k < 4; ++k) {
-      t.stage.vec_off[l][k] = off;
-      off += r16(src[static_cast<size_t>(l)].total * 8);
-    }
-  t.stage.arena_bytes = off;
-  d = t;
+  cap(k_bottom);
+  cap(k_bottom_block<0>);
+  cap(k_bottom_block<1>);
+  cap(k_bottom_block<2>);
 }
-
-// Fill and upload a BotDesc for levels 0..top = src.size()-1; false if unsupported.
-bool fill_bottom(pf_hierarchy* h, pf_hierarchy::Bottom& bot, const std::vector<BotSrc>& src,
-                 const CoarsePack& pack, double* coarse_stats) {
-  const int top = static_cast<int>(src.size()) - 1;
-  const int n_sub = static_cast<int>(src[0].sub->size());
-  if (top < 1 || top >= kBotMaxLevels || n_sub > kBotMaxSubs) return false;
-  if (coarse_pack_smem(pack) > kCoarseSmemMax) return false;
-  BotDesc d;
-  std::memset(&d, 0, sizeof d);
-  d.n_sub = n_sub;
-  d.n_levels = top + 1;
-  int64_t block_rows = 1024;
-  if (const char* e = std::getenv("PF_BOTTOM_BLOCK_ROWS")) block_rows = std::atoll(e);
-  d.block_top = -1;
-  for (int l = 0; l <= top; ++l)
-    if (src[l].total <= block_rows) d.block_top = l;
-  d.coarse = pack;
-  d.coarse_stats = coarse_stats;
-  auto plan = [](const ExchangePlan& P) { return BotPlan{P.dst.p, P.src.p, static_cast<int32_t>(P.n)}; };
-  int64_t max_total = 0;
-  for (int l = 0; l <= top; ++l) {
-    const BotSrc& L = src[l];
-    BotLevel& B = d.lev[l];
-    B.x = L.x;
-    B.xa = L.xa;
-    B.b = L.b;
-    B.r = L.r;
-    B.total = static_cast<int32_t>(L.total);
-    max_total = std::max(max_total, L.total);
-    B.ms = plan((*L.scatter)[PF_CH_MASTER_SLAVE]);
-    B.h1 = plan((*L.scatter)[PF_CH_HALO1]);
-    B.h2 = plan((*L.scatter)[PF_CH_HALO2]);
-    B.acc_off = L.acc->acc_off.p;
-    B.acc_src = L.acc->acc_src.p;
-    B.acc_dst = L.acc->acc_dst.p;
-    B.acc_n = L.acc->n_masters;
-    for (int s = 0; s < n_sub; ++s) {
-      const DevLevel& D = (*L.sub)[s];
-      BotSub& S = d.sub[l][s];
-      B.max_colors = std::max(B.max_colors, D.n_colors);
-      bot.color_bufs.emplace_back();
-      bot.color_bufs.back().upload(D.color_start);
-      S.A = fp64_view(bot, D.A);
-      S.host_of_own = D.d_perm.p;
-      S.color_start = bot.color_bufs.back().p;
-      S.P = fp64_view(bot, D.P);
-      S.R = fp64_view(bot, D.R);
-      S.is_dir = D.d_is_dir.p;
-      S.n = D.n;
-      S.n_own = D.n_own;
-      S.n_colors = D.n_colors;
-      S.off = static_cast<int32_t>(D.offset);
-    }
-  }
-  stage_block_levels(h, bot, d, src);
-  if (std::getenv("PF_BOTTOM_PROFILE")) {
-    PF_CUDA(cudaMalloc(&bot.stamps, 256 * sizeof(unsigned long long)));
-    PF_CUDA(cudaMemset(bot.stamps, 0, 256 * sizeof(unsigned long long)));
-    d.stamps = static_cast<unsigned long long*>(bot.stamps);
-  }
-  PF_CUDA(cudaMalloc(&bot.desc, sizeof(BotDesc)));
-  PF_CUDA(cudaMemcpy(bot.desc, &d, sizeof d, cudaMemcpyHostToDevice));
-  int sms = 0, occ = 0;
-  PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-  bot.smem = d.stage.hs >= 0 ? static_cast<size_t>(d.stage.smem_off + d.stage.arena_bytes)
-                            : ((sizeof(BotDesc) + 15) / 16) * 16 + coarse_pack_smem(d.coarse);
-  if (bot.smem > 48 * 1024) {  // the cap, not the size: several bottoms may share the kernel
-    int optin = 0;
-    PF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-    auto cap = [&](auto kern) {
-      cudaFuncAttributes fa{};
-      PF_CUDA(cudaFuncGetAttributes(&fa, kern));
-      PF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   optin - static_cast<int>(fa.sharedSizeBytes)));
-    };
-    cap(k_bottom);
-    cap(k_bottom_block<0>);
-    cap(k_bottom_block<1>);
-    cap(k_bottom_block<2>);
-  }
-  PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bottom, kBlock, bot.smem));
-  if (occ < 1) return false;
-  int64_t want = std::max<int64_t>(sms, (max_total + kBlock - 1) / kBlock);
-  if (const char* e = std::getenv("PF_BOTTOM_GRID")) want = std::max<int64_t>(1, std::atoll(e));
-  bot.grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(occ) * sms));
-  // every bottom level staged for block 0: the other blocks would only wait at barriers
-  bot.staged_all = d.stage.hs == top && d.block_top == top;
-  if (bot.staged_all && !std::getenv("PF_BOTTOM_GRID")) bot.grid = 1;
-  bot.top = top;
-  bot.active = true;
-  return true;
-}
-
-// Single-device bottom kernel: levels up to PF_BOTTOM_ROWS rows (default 1024: at C2 the
-// coloured smoothers' V-cycle is 1.443 ms with no bottom kernel, 1.383 with levels <= 64k
-// rows, 1.356 with levels <= 1k rows).  Damped Jacobi does not use it unless
-// PF_BOTTOM_JACOBI=1: with programmatic dependent launch in the graph, separate per-level
-// kernels are faster for it (0.715 vs 0.744 ms).
-int64_t bottom_row_limit() {
-  int64_t limit = 1024;
-  if (const char* e = std::getenv("PF_BOTTOM_ROWS")) limit = std::atoll(e);
-  return limit;
-}
-bool bottom_for(const pf_multigrid_config& cfg) {
-  const char* e = std::getenv("PF_BOTTOM_JACOBI");  // read at capture time (tests flip it)
-  return cfg.smoother.kind != PF_SMOOTHER_JACOBI || (e && std::atoi(e) != 0);
-}
-// Multi-process replicated bottom (all ranks' levels on every GPU, one allgather per
-// cycle): levels up to PF_REP_BOTTOM_ROWS rows in total (default 65536).
-int64_t rep_bottom_row_limit() {
-  int64_t limit = 65536;
-  if (const char* e = std::getenv("PF_REP_BOTTOM_ROWS")) limit = std::atoll(e);
-  return limit;
-}
-
-// Levels whose total row count stays below the limit run as one cooperative kernel when
-// every rank of the level lives on this device.
-void build_bottom(pf_hierarchy* h) {
-  const int64_t limit = bottom_row_limit();
-  if (h->world != h->n_sub || limit <= 0) return;
-  int top = -1;
-  for (int l = 0; l < h->n_levels - 1 && l < kBotMaxLevels; ++l)
-    if (h->levels[l].total <= limit) top = l;
-  if (top < 1) return;
-  std::vector<BotSrc> src;
-  for (int l = 0; l <= top; ++l) {
-    Level& L = h->levels[l];
-    src.push_back(BotSrc{&L.sub, L.total, &L.scatter, &L.accumulate, L.x->cur(), L.x->alt(), L.b->cur(), L.r.p});
-  }
-  fill_bottom(h, h->bot, src, h->levels[0].cpack, h->levels[0].coarse_stats.p);
-}
-
-// Multi-process: the bottom kernel over the replicated levels (all ranks on every GPU),
-// if they are all small enough; otherwise only the coarse replica is used.
-void build_rep_bottom(pf_hierarchy* h) {
-  auto& R = h->rep;
-  const int top = static_cast<int>(R.lv.size()) - 1;
-  const int64_t limit = rep_bottom_row_limit();
-  if (top < 1 || top >= h->n_levels - 1 || limit <= 0) return;
-  std::vector<BotSrc> src;
-  for (int l = 0; l <= top; ++l) {
-    auto& RL = R.lv[static_cast<size_t>(l)];
-    const int64_t total = RL.stride * h->world;
-    if (total > limit) return;
-    src.push_back(BotSrc{&RL.sub, total, &RL.scatter, &RL.acc, RL.x.p, RL.x.p + total, RL.b.p, RL.r.p});
-  }
-  fill_bottom(h, R.bot, src, R.cpack, h->levels[0].coarse_stats.p);
+int bottom_kernel_occupancy(size_t smem) {
+  int occ = 0;
+  PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bottom, kBlock, smem));
+  return occ;
 }
 
 // ------------------------------------------------------------------ enqueue --
@@ -2300,54 +1154,19 @@ pf_vector* new_vector(pf_hierarchy* h, int level) {
   return v;
 }
 
-void set_error(const char* m) { g_last_error = m; }
+}  // namespace rt
 
-}  // namespace
+// Kernel-launch accounting and the PDL switch for launches made outside this file
+// (pf_peer.cu).
+int64_t* launch_counter(pf_hierarchy* h) { return rt::g_capture_counter ? rt::g_capture_counter : &h->launches; }
+bool pdl_on() { return rt::pdl_enabled(); }
+// pf_peer.cu
+int64_t peer_export(pf_hierarchy* h, void* buf, int64_t cap);
+void peer_import(pf_hierarchy* h, const void* blobs, int64_t stride);
+
 }  // namespace pf
 
-// A second value set on a level's operator pattern (pf_operator_create).
-struct pf_operator {
-  pf_hierarchy* h = nullptr;
-  int level = 0;
-  std::vector<pf::DevVals> vals;  // per subdomain, SELL layout of DevLevel::A
-  std::vector<bool> set;
-};
-
-// Device assembly description per subdomain (pf_assembly_create / pf_assembly_set).
-struct pf_assembly {
-  pf_hierarchy* h = nullptr;
-  int level = 0;
-  struct Sub {
-    bool set = false;
-    int dim = 3;
-    int32_t N = 0, nh = 0, n_coarse = 0, grid_level = 0;
-    pf::DevBuf<int32_t> lattice, cls;
-    pf::DevBuf<uint8_t> cell_mask;
-    pf::DevBuf<double> kappa, elem;
-    int family = 0;  // 0: Q1 (pf_assembly_desc); PF_FE_Q2 / PF_FE_ROTATED_Q1 (pf_fe_assembly_desc)
-    pf::DevBuf<uint8_t> orient;
-  };
-  std::vector<Sub> sub;
-};
-
-// The finest-level load description on the device (pf_load_create / pf_load_set).
-struct pf_load {
-  pf_hierarchy* h = nullptr;
-  int level = 0;
-  struct Sub {
-    bool set = false;
-    int dim = 3;
-    int32_t n_cells = 0;
-    double qweight = 0.0;
-    pf::DevBuf<int32_t> lattice;
-    pf::DevBuf<uint32_t> cells;
-    pf::DevBuf<double> factor, extent, phi;
-    pf::DevBuf<int32_t> dir_idx;   // Dirichlet rows, level-global device index
-    pf::DevBuf<double> dir_prof;   // profile at those rows
-  };
-  std::vector<Sub> sub;
-  std::unique_ptr<pf_vector> next;  // pf_heat_run's next-load scratch (kept across calls)
-};
+using namespace pf::rt;
 
 pf_hierarchy::~pf_hierarchy() {
   cudaSetDevice(device);
@@ -2370,27 +1189,6 @@ pf_hierarchy::~pf_hierarchy() {
   if (ev1) cudaEventDestroy(ev1);
   if (stream) cudaStreamDestroy(stream);
 }
-
-// Clear any runtime error left on this thread by unrelated code, so the launch checks
-// below report only this call's failures.
-#define PF_API_BEGIN \
-  (void)cudaGetLastError(); \
-  try {
-#define PF_API_END                                   \
-  }                                                  \
-  catch (const pf::Error& e) {                       \
-    pf::set_error(e.what());                         \
-    return e.code;                                   \
-  }                                                  \
-  catch (const std::bad_alloc&) {                    \
-    pf::set_error("host out of memory");             \
-    return PF_ERR_STATE;                             \
-  }                                                  \
-  catch (const std::exception& e) {                  \
-    pf::set_error(e.what());                         \
-    return PF_ERR_STATE;                             \
-  }                                                  \
-  return PF_OK;
 
 extern "C" {
 
@@ -3145,455 +1943,3 @@ pf_status pf_level_info(const pf_hierarchy* h, int level, int sub, int64_t* n_do
 
 }  // extern "C"
 
-// ------------------------------------------------------------ heat (Crank-Nicolson) --
-
-namespace pf {
-namespace {
-
-SellView op_view(const pf_operator* op, int s) {
-  return view_of(op->vals[s], op->h->levels[op->level].sub[s].A);
-}
-
-void check_op(const pf_operator* op) {
-  if (!op) invalid("null operator");
-  for (size_t s = 0; s < op->set.size(); ++s)
-    if (!op->set[s]) state("operator values of subdomain " + std::to_string(s) + " not set");
-}
-
-void check_load(const pf_load* ld) {
-  if (!ld) invalid("null load");
-  for (size_t s = 0; s < ld->sub.size(); ++s)
-    if (!ld->sub[s].set) state("load description of subdomain " + std::to_string(s) + " not set");
-}
-
-void enq_load(pf_load* ld, double scale, double* out) {
-  pf_hierarchy* h = ld->h;
-  Level& L = h->levels[ld->level];
-  auto launch = launcher(h);
-  for (int s = 0; s < h->n_sub; ++s) {
-    const pf_load::Sub& S = ld->sub[s];
-    const DevLevel& D = L.sub[s];
-    const LoadView v{S.lattice.p, S.cells.p, S.factor.p, S.extent.p, S.phi.p, S.qweight, S.n_cells, S.dim};
-    if (S.dim == 3)
-      launch(grid_for(D.n), kBlock, k_load<3>, v, scale, out + D.offset, D.n);
-    else
-      launch(grid_for(D.n), kBlock, k_load<2>, v, scale, out + D.offset, D.n);
-  }
-  enq_update_ms(h, ld->level, out, PF_UPDATE_ACCUMULATE_THEN_SCATTER);
-}
-
-void enq_dirichlet(pf_load* ld, int has, double scale, double* b, double* u) {
-  pf_hierarchy* h = ld->h;
-  auto launch = launcher(h);
-  for (int s = 0; s < h->n_sub; ++s) {
-    const pf_load::Sub& S = ld->sub[s];
-    launch(grid_for(S.dir_idx.n), kBlock, k_dirichlet, static_cast<const int32_t*>(S.dir_idx.p),
-           static_cast<const double*>(S.dir_prof.p), static_cast<int32_t>(S.dir_idx.n), has, scale, b, u);
-  }
-}
-
-void enq_cn_rhs(pf_operator* op, pf_load* ld, const double* u, const double* ln, const double* lnx,
-                double half_dt, int has, double gscale, double* b, double* u_out) {
-  pf_hierarchy* h = op->h;
-  Level& L = h->levels[op->level];
-  auto launch = launcher(h);
-  for (int s = 0; s < h->n_sub; ++s) {
-    const DevLevel& D = L.sub[s];
-    vk_dispatch(op->vals[s].vkind, [&](auto V) {
-      launch(grid_for(D.n), kBlock, k_cn_rhs<decltype(V)::value>, op_view(op, s), u + D.offset, ln + D.offset,
-             lnx + D.offset, half_dt, static_cast<const uint8_t*>(D.d_is_dir.p), b + D.offset, D.n);
-    });
-  }
-  enq_dirichlet(ld, has, gscale, b, u_out);
-}
-
-}  // namespace
-}  // namespace pf
-
-extern "C" {
-
-pf_status pf_operator_create(pf_hierarchy* h, int level, pf_operator** out) {
-  PF_API_BEGIN
-  check_level(h, level);
-  if (!out) invalid("null output");
-  auto op = std::make_unique<pf_operator>();
-  op->h = h;
-  op->level = level;
-  op->vals.resize(static_cast<size_t>(h->n_sub));
-  op->set.assign(static_cast<size_t>(h->n_sub), false);
-  *out = op.release();
-  PF_API_END
-}
-
-pf_status pf_operator_set_values(pf_operator* op, int sub, const double* values, int64_t nnz) {
-  PF_API_BEGIN
-  if (!op || !values) invalid("null argument");
-  pf_hierarchy* h = op->h;
-  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
-  const DevLevel& D = h->levels[op->level].sub[sub];
-  if (nnz != D.A.nnz)
-    invalid("operator nnz " + std::to_string(nnz) + " does not match the level's " + std::to_string(D.A.nnz));
-  PF_CUDA(cudaSetDevice(h->device));
-  std::vector<double> sv(static_cast<size_t>(D.A.stored), 0.0);
-  for (int32_t hr = 0; hr < D.n; ++hr) {
-    const int32_t d = D.perm[hr];
-    const int64_t base = sell_row_base(D.sell_ptr.data(), d);
-    for (int64_t k = D.csr_rowptr[hr]; k < D.csr_rowptr[hr + 1]; ++k)
-      sv[static_cast<size_t>(sell_entry(base, static_cast<int>(k - D.csr_rowptr[hr])))] = values[k];
-  }
-  encode_values(sv, op->vals[sub]);
-  op->set[sub] = true;
-  PF_API_END
-}
-
-pf_status pf_operator_apply(pf_operator* op, const pf_vector* x, pf_vector* y) {
-  PF_API_BEGIN
-  check_op(op);
-  pf_hierarchy* h = op->h;
-  check_vec(h, x, op->level, "x");
-  check_vec(h, y, op->level, "y");
-  PF_CUDA(cudaSetDevice(h->device));
-  Level& L = h->levels[op->level];
-  auto launch = launcher(h);
-  for (int s = 0; s < h->n_sub; ++s) {
-    const DevLevel& D = L.sub[s];
-    vk_dispatch(op->vals[s].vkind, [&](auto V) {
-      launch(grid_for(D.n), kBlock, k_spmv<decltype(V)::value>, op_view(op, s), x->cur() + D.offset, y->cur() + D.offset, D.n);
-    });
-  }
-  sync(h);
-  PF_API_END
-}
-
-pf_status pf_operator_get_values(const pf_operator* op, int sub, double* values, int64_t nnz) {
-  PF_API_BEGIN
-  if (!op || !values) invalid("null argument");
-  pf_hierarchy* h = op->h;
-  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
-  if (!op->set[static_cast<size_t>(sub)]) state("operator values not set");
-  const DevLevel& D = h->levels[op->level].sub[sub];
-  if (nnz != D.A.nnz) invalid("nnz does not match the level");
-  PF_CUDA(cudaSetDevice(h->device));
-  const DevVals& V = op->vals[static_cast<size_t>(sub)];
-  std::vector<double> sv(static_cast<size_t>(D.A.stored));
-  if (V.vkind == 0) {
-    PF_CUDA(cudaMemcpy(sv.data(), V.vals.p, sizeof(double) * sv.size(), cudaMemcpyDeviceToHost));
-  } else {
-    std::vector<double> table(static_cast<size_t>(V.table.n));
-    PF_CUDA(cudaMemcpy(table.data(), V.table.p, sizeof(double) * table.size(), cudaMemcpyDeviceToHost));
-    if (V.vkind == 1) {
-      std::vector<uint8_t> ix(sv.size());
-      PF_CUDA(cudaMemcpy(ix.data(), V.vi8.p, ix.size(), cudaMemcpyDeviceToHost));
-      for (size_t i = 0; i < sv.size(); ++i) sv[i] = table[ix[i]];
-    } else {
-      std::vector<uint16_t> ix(sv.size());
-      PF_CUDA(cudaMemcpy(ix.data(), V.vi16.p, 2 * ix.size(), cudaMemcpyDeviceToHost));
-      for (size_t i = 0; i < sv.size(); ++i) sv[i] = table[ix[i]];
-    }
-  }
-  for (int32_t hr = 0; hr < D.n; ++hr) {
-    const int64_t base = sell_row_base(D.sell_ptr.data(), D.perm[hr]);
-    for (int64_t k = D.csr_rowptr[hr]; k < D.csr_rowptr[hr + 1]; ++k)
-      values[k] = sv[static_cast<size_t>(sell_entry(base, static_cast<int>(k - D.csr_rowptr[hr])))];
-  }
-  PF_API_END
-}
-
-pf_status pf_assembly_create(pf_hierarchy* h, int level, pf_assembly** out) {
-  PF_API_BEGIN
-  check_level(h, level);
-  if (!out) invalid("null output");
-  auto a = std::make_unique<pf_assembly>();
-  a->h = h;
-  a->level = level;
-  a->sub.resize(static_cast<size_t>(h->n_sub));
-  *out = a.release();
-  PF_API_END
-}
-
-pf_status pf_assembly_set(pf_assembly* a, int sub, const pf_assembly_desc* d) {
-  PF_API_BEGIN
-  if (!a || !d) invalid("null argument");
-  pf_hierarchy* h = a->h;
-  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
-  const DevLevel& D = h->levels[a->level].sub[sub];
-  if (d->n_dofs != D.n) invalid("assembly description does not match the level's dof count");
-  if (d->dim != 2 && d->dim != 3) invalid("dimension must be 2 or 3");
-  if (!d->lattice || !d->cell_mask || !d->elem || !d->elem_class || d->n_classes < 1 || d->n_cells < 1)
-    invalid("null assembly array");
-  if (d->n_coarse < 1 || d->level < 0 || (static_cast<int64_t>(d->n_coarse) << d->level) != d->n_cells)
-    invalid("n_cells must be n_coarse * 2^level");
-  PF_CUDA(cudaSetDevice(h->device));
-  const int32_t n = D.n;
-  std::vector<int32_t> lat(static_cast<size_t>(3 * n));
-  std::vector<uint8_t> mask(static_cast<size_t>(n));
-  for (int32_t i = 0; i < n; ++i) {
-    const int32_t r = D.perm[i];
-    for (int k = 0; k < 3; ++k) lat[3 * static_cast<size_t>(r) + k] = d->lattice[3 * static_cast<int64_t>(i) + k];
-    mask[static_cast<size_t>(r)] = d->cell_mask[i];
-  }
-  const int64_t N = d->n_cells, ncells = d->dim == 3 ? N * N * N : N * N;
-  const int64_t nel = d->dim == 3 ? int64_t(d->n_classes) * d->n_classes * d->n_classes
-                                  : int64_t(d->n_classes) * d->n_classes;
-  pf_assembly::Sub& S = a->sub[static_cast<size_t>(sub)];
-  S.family = 0;
-  S.dim = d->dim;
-  S.N = d->n_cells;
-  S.nh = d->n_classes;
-  S.n_coarse = d->n_coarse;
-  S.grid_level = d->level;
-  S.lattice.upload(lat);
-  S.cell_mask.upload(mask);
-  S.cls.upload(std::vector<int32_t>(d->elem_class, d->elem_class + 3 * N));
-  S.elem.upload(std::vector<double>(d->elem, d->elem + 64 * nel));
-  if (d->kappa) S.kappa.upload(std::vector<double>(d->kappa, d->kappa + ncells));
-  else S.kappa.reset();
-  S.set = true;
-  PF_API_END
-}
-
-pf_status pf_fe_assembly_set(pf_assembly* a, int sub, const pf_fe_assembly_desc* d) {
-  PF_API_BEGIN
-  if (!a || !d) invalid("null argument");
-  pf_hierarchy* h = a->h;
-  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
-  const DevLevel& D = h->levels[a->level].sub[sub];
-  if (d->n_dofs != D.n) invalid("assembly description does not match the level's dof count");
-  if (d->family != PF_FE_Q2 && d->family != PF_FE_ROTATED_Q1) invalid("unknown element family");
-  if (!d->keys4 || !d->elem || d->n_cells < 1 || (d->family == PF_FE_ROTATED_Q1 && !d->kappa))
-    invalid("null assembly array");
-  PF_CUDA(cudaSetDevice(h->device));
-  const int32_t n = D.n;
-  std::vector<int32_t> lat(static_cast<size_t>(3 * n));
-  std::vector<uint8_t> ori(static_cast<size_t>(n));
-  for (int32_t i = 0; i < n; ++i) {
-    const int32_t r = D.perm[i];
-    for (int k = 0; k < 3; ++k) lat[3 * static_cast<size_t>(r) + k] = static_cast<int32_t>(d->keys4[4 * static_cast<int64_t>(i) + 1 + k]);
-    ori[static_cast<size_t>(r)] = static_cast<uint8_t>(d->keys4[4 * static_cast<int64_t>(i)]);
-  }
-  const int64_t N = d->n_cells;
-  pf_assembly::Sub& S = a->sub[static_cast<size_t>(sub)];
-  S.family = d->family;
-  S.dim = 3;
-  S.N = d->n_cells;
-  S.lattice.upload(lat);
-  S.orient.upload(ori);
-  S.elem.upload(std::vector<double>(d->elem, d->elem + (d->family == PF_FE_Q2 ? 27 * 27 : 36)));
-  if (d->kappa) S.kappa.upload(std::vector<double>(d->kappa, d->kappa + N * N * N));
-  else S.kappa.reset();
-  S.set = true;
-  PF_API_END
-}
-
-pf_status pf_assemble_operator(pf_assembly* a, pf_operator* op) {
-  PF_API_BEGIN
-  if (!a || !op) invalid("null argument");
-  pf_hierarchy* h = a->h;
-  if (op->h != h || op->level != a->level) invalid("operator of another level");
-  for (const auto& S : a->sub)
-    if (!S.set) state("assembly description not set for every subdomain");
-  PF_CUDA(cudaSetDevice(h->device));
-  auto launch = launcher(h);
-  for (int s = 0; s < h->n_sub; ++s) {
-    const DevLevel& D = h->levels[a->level].sub[s];
-    const pf_assembly::Sub& S = a->sub[static_cast<size_t>(s)];
-    DevVals& out = op->vals[static_cast<size_t>(s)];
-    if (out.vkind != 0 || out.vals.n != D.A.stored) {  // fp64 values, allocated once
-      out = DevVals{};
-      out.vkind = 0;
-      out.vals.alloc(D.A.stored);
-      PF_CUDA(cudaMemsetAsync(out.vals.p, 0, sizeof(double) * static_cast<size_t>(D.A.stored), h->stream));
-    }
-    if (S.family != 0) {
-      const FeAsmView fv{S.lattice.p, S.orient.p, D.d_is_dir.p, S.elem.p, S.kappa.p, S.N};
-      if (S.family == PF_FE_Q2)
-        launch(grid_for(D.n), kBlock, k_fe_assemble<PF_FE_Q2>, fv, view(D.A), out.vals.p, D.n);
-      else
-        launch(grid_for(D.n), kBlock, k_fe_assemble<PF_FE_ROTATED_Q1>, fv, view(D.A), out.vals.p, D.n);
-      op->set[static_cast<size_t>(s)] = true;
-      continue;
-    }
-    const AsmView v{S.lattice.p, S.cell_mask.p, D.d_is_dir.p, S.kappa.p, S.elem.p, S.cls.p, S.N, S.nh, S.n_coarse,
-                    S.grid_level};
-    if (S.dim == 3)
-      launch(grid_for(D.n), kBlock, k_assemble<3>, v, view(D.A), out.vals.p, D.n);
-    else
-      launch(grid_for(D.n), kBlock, k_assemble<2>, v, view(D.A), out.vals.p, D.n);
-    op->set[static_cast<size_t>(s)] = true;
-  }
-  sync(h);
-  PF_API_END
-}
-
-pf_status pf_assembly_destroy(pf_assembly* a) {
-  PF_API_BEGIN
-  if (a) cudaSetDevice(a->h->device);
-  delete a;
-  PF_API_END
-}
-
-pf_status pf_operator_destroy(pf_operator* op) {
-  PF_API_BEGIN
-  if (op) cudaSetDevice(op->h->device);
-  delete op;
-  PF_API_END
-}
-
-pf_status pf_load_create(pf_hierarchy* h, int level, pf_load** out) {
-  PF_API_BEGIN
-  check_level(h, level);
-  if (!out) invalid("null output");
-  auto ld = std::make_unique<pf_load>();
-  ld->h = h;
-  ld->level = level;
-  ld->sub.resize(static_cast<size_t>(h->n_sub));
-  *out = ld.release();
-  PF_API_END
-}
-
-pf_status pf_load_set(pf_load* ld, int sub, const pf_load_desc* d) {
-  PF_API_BEGIN
-  if (!ld || !d) invalid("null argument");
-  pf_hierarchy* h = ld->h;
-  if (sub < 0 || sub >= h->n_sub) invalid("subdomain out of range");
-  const DevLevel& D = h->levels[ld->level].sub[sub];
-  if (d->n_dofs != D.n) invalid("load description has " + std::to_string(d->n_dofs) + " dofs, level has " + std::to_string(D.n));
-  if (d->dim != 2 && d->dim != 3) invalid("dimension must be 2 or 3");
-  if (d->n_cells < 1) invalid("n_cells must be >= 1");
-  if (!d->lattice || !d->cells || !d->factor || !d->extent || !d->phi || !d->boundary || !d->is_dirichlet)
-    invalid("null load array");
-  PF_CUDA(cudaSetDevice(h->device));
-  const int32_t n = D.n;
-  std::vector<int32_t> lat(static_cast<size_t>(3 * n));
-  std::vector<uint32_t> cells(static_cast<size_t>(n));
-  std::vector<int32_t> didx;
-  std::vector<double> dprof;
-  const int64_t N = d->n_cells;
-  for (int32_t i = 0; i < n; ++i) {
-    const int32_t r = D.perm[i];
-    const uint32_t w = d->cells[i];
-    const int cnt = static_cast<int>(w & 15u);
-    if (cnt > (1 << d->dim)) invalid("load cell count out of range at dof " + std::to_string(i));
-    for (int a = 0; a < 3; ++a) {
-      const int32_t c = d->lattice[3 * static_cast<int64_t>(i) + a];
-      if (cnt > 0 && (a < d->dim) && (c < 0 || c > N)) invalid("lattice coordinate out of range");
-      lat[3 * static_cast<size_t>(r) + a] = c;
-    }
-    cells[static_cast<size_t>(r)] = w;
-    if (d->is_dirichlet[i]) {
-      didx.push_back(static_cast<int32_t>(D.offset) + r);
-      dprof.push_back(d->boundary[i]);
-    }
-  }
-  pf_load::Sub& S = ld->sub[static_cast<size_t>(sub)];
-  S.dim = d->dim;
-  S.n_cells = d->n_cells;
-  S.qweight = d->qweight;
-  S.lattice.upload(lat);
-  S.cells.upload(cells);
-  S.factor.upload(std::vector<double>(d->factor, d->factor + 3 * N * 2));
-  S.extent.upload(std::vector<double>(d->extent, d->extent + 3 * N));
-  S.phi.upload(std::vector<double>(d->phi, d->phi + 64));
-  S.dir_idx.upload(didx);
-  S.dir_prof.upload(dprof);
-  S.set = true;
-  PF_API_END
-}
-
-pf_status pf_load_assemble(pf_load* ld, double source_scale, pf_vector* out) {
-  PF_API_BEGIN
-  check_load(ld);
-  pf_hierarchy* h = ld->h;
-  check_vec(h, out, ld->level, "out");
-  PF_CUDA(cudaSetDevice(h->device));
-  enq_load(ld, source_scale, out->cur());
-  sync(h);
-  PF_API_END
-}
-
-pf_status pf_load_apply_dirichlet(pf_load* ld, int has_dirichlet, double scale, pf_vector* b, pf_vector* u) {
-  PF_API_BEGIN
-  check_load(ld);
-  pf_hierarchy* h = ld->h;
-  check_vec(h, b, ld->level, "b");
-  if (u) check_vec(h, u, ld->level, "u");
-  PF_CUDA(cudaSetDevice(h->device));
-  enq_dirichlet(ld, has_dirichlet, scale, b->cur(), u ? u->cur() : nullptr);
-  sync(h);
-  PF_API_END
-}
-
-pf_status pf_load_destroy(pf_load* ld) {
-  PF_API_BEGIN
-  if (ld) cudaSetDevice(ld->h->device);
-  delete ld;
-  PF_API_END
-}
-
-pf_status pf_cn_rhs(pf_operator* op, pf_load* ld, const pf_vector* u_in, const pf_vector* load_now,
-                    const pf_vector* load_next, double half_dt, int has_dirichlet, double dirichlet_scale,
-                    pf_vector* b, pf_vector* u) {
-  PF_API_BEGIN
-  check_op(op);
-  check_load(ld);
-  pf_hierarchy* h = op->h;
-  if (ld->h != h || ld->level != op->level) invalid("operator and load belong to different levels");
-  check_vec(h, u_in, op->level, "u_in");
-  check_vec(h, load_now, op->level, "load_now");
-  check_vec(h, load_next, op->level, "load_next");
-  check_vec(h, b, op->level, "b");
-  if (u) check_vec(h, u, op->level, "u");
-  if (b == u_in || b == load_now || b == load_next) invalid("b must not alias an input");
-  PF_CUDA(cudaSetDevice(h->device));
-  enq_cn_rhs(op, ld, u_in->cur(), load_now->cur(), load_next->cur(), half_dt, has_dirichlet, dirichlet_scale,
-             b->cur(), u ? u->cur() : nullptr);
-  sync(h);
-  PF_API_END
-}
-
-pf_status pf_heat_run(pf_hierarchy* h, pf_operator* op, pf_load* ld, pf_vector* u, pf_vector* load_now,
-                      int first_step, int steps, double half_dt, const double* source_scale, int has_dirichlet,
-                      const double* dirichlet_scale, const pf_multigrid_config* cfg, pf_solve_stats* stats,
-                      double* residuals, int max_residuals, int* failed_step) {
-  PF_API_BEGIN
-  if (failed_step) *failed_step = 0;
-  check_level(h, h ? h->n_levels - 1 : 0);
-  check_op(op);
-  check_load(ld);
-  const int top = h->n_levels - 1;
-  if (op->h != h || ld->h != h || op->level != top || ld->level != top)
-    invalid("operator and load must live on the hierarchy's finest level");
-  check_vec(h, u, top, "u");
-  check_vec(h, load_now, top, "load_now");
-  if (!cfg || !source_scale || (has_dirichlet && !dirichlet_scale)) invalid("null argument");
-  if (steps < 0 || first_step < 0) invalid("steps must be >= 0");
-  PF_CUDA(cudaSetDevice(h->device));
-  Level& T = h->levels[top];
-  // the finest level's b scratch carries the step's rhs; one extra vector for the next load,
-  // allocated once per load object (a step-by-step caller must not pay a cudaMalloc/Free,
-  // which synchronises the device, every step)
-  if (!ld->next) ld->next.reset(new_vector(h, top));
-  pf_vector* lnx = ld->next.get();
-  pf_vector* b = T.b;
-  if (b == u || b == load_now) invalid("u / load_now alias the hierarchy's scratch");
-  for (int k = 0; k < steps; ++k) {
-    enq_load(ld, source_scale[k], lnx->cur());
-    enq_cn_rhs(op, ld, u->cur(), load_now->cur(), lnx->cur(), half_dt, has_dirichlet,
-               has_dirichlet ? dirichlet_scale[k] : 0.0, b->cur(), u->cur());
-    try {
-      solve_outer_dev(h, u, b, *cfg, stats, residuals, max_residuals);
-    } catch (const pf::Error& e) {
-      if (e.code == PF_ERR_NO_CONVERGENCE) {
-        const int step = first_step + k + 1;
-        if (failed_step) *failed_step = step;
-        throw pf::Error(e.code, "time step " + std::to_string(step) + ": " + e.what());  // app.cpp:205-207
-      }
-      throw;
-    }
-    std::swap(load_now->data, lnx->data);  // load_now = std::move(load_next) (app.cpp:212)
-  }
-  sync(h);
-  PF_API_END
-}
-
-}  // extern "C"

@@ -49,6 +49,16 @@ constexpr int kSorChunkGroups = PF_SOR_GROUPS;
 #define PF_ROW_MINB 5
 #endif
 
+// The kernels' value-kind template argument (pf_kernels.cuh): bits 0-2 the stored value
+// kind (0 fp64, 1 8-bit index, 2 16-bit index, kVKSmem = 8-bit index with the table staged
+// in shared memory), bit 3 (kVKCached) the caching load policy; -1 = read from the view.
+constexpr int kVKSmem = 4;
+constexpr int kVKCached = 8;
+template <int kVK>
+constexpr int vk_kind() { return kVK < 0 ? kVK : (kVK & 7); }
+template <int kVK>
+constexpr bool vk_cached() { return kVK >= 0 && (kVK & kVKCached) != 0; }
+
 // SELL-32x4 layout: slice s holds rows 32s..32s+31; entry j of lane l sits at
 //   slice_ptr[s] + (j / 4) * 128 + 4 l + j % 4,
 // so a lane reads 4 entries with one 16-byte column load (one 4-byte index / 32-byte value
