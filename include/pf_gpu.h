@@ -191,6 +191,25 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h);
  * differ from the reference's at the coarse-tolerance level.  One subdomain in one
  * process; call after pf_hierarchy_finalize (captured solve graphs are rebuilt). */
 pf_status pf_hierarchy_set_coarse_direct(pf_hierarchy* h, int on);
+
+/* Tuning options of one hierarchy (the measured-best defaults, overridden by the PF_*
+ * environment variable of the same upper-case name when the hierarchy is created; the list
+ * and their meaning: DESIGN.md section 6 "Knobs").  "build" options shape the device layout
+ * and must be set before pf_hierarchy_finalize (PF_ERR_STATE after); "launch" options can be
+ * changed at any time (cached graphs are dropped).  Unknown names: PF_ERR_INVALID_ARGUMENT.
+ * Results never depend on them: every combination is bit-identical (tests/test_gpu_variants.py). */
+pf_status pf_hierarchy_set_option(pf_hierarchy* h, const char* name, int64_t value);
+pf_status pf_hierarchy_get_option(const pf_hierarchy* h, const char* name, int64_t* out);
+/* Space-separated "name:build|launch" list of every option (needs no GPU). */
+pf_status pf_option_names(char* buf, int64_t capacity);
+
+/* Memory checking (tests): with PF_GUARD=1 in the environment every device buffer of the
+ * library is followed by a 4 KB guard zone of 0xFF bytes (NaN / -1 for a kernel reading
+ * past an array), verified when the buffer is freed.  The number of guard zones found
+ * overwritten so far; and a self-test that plants one write past the end of a guarded
+ * buffer on `device` (*detected = 1 when the check catches it). */
+pf_status pf_debug_guard_failures(int64_t* out);
+pf_status pf_debug_guard_selftest(int device, int* detected);
 /* Multi-process: join the NCCL communicator of `world_size` ranks (one hierarchy per
  * process).  `unique_id` is the 128-byte ncclUniqueId from pf_nccl_unique_id() on
  * rank 0, broadcast by the caller. */

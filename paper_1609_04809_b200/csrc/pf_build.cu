@@ -30,56 +30,12 @@ namespace rt {
 
 
 
-// PF_VTAB_SMEM=0: the row kernels read an 8-bit index's value through L1 (__ldg) instead
-// of the shared-memory copy of the table.
-bool vtab_smem() {
-  static const bool on = [] {
-    const char* e = std::getenv("PF_VTAB_SMEM");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
-}
-
-// Operators of the levels below the finest up to PF_CACHED_MAX_BYTES (default 48 MB, about
-// 40 % of the 126 MB L2) are read with the caching load policy (kVKCached): they stay
-// L2-resident across the sweeps of a cycle.  The finest level, and larger ones, stream
-// evict-first.
-int64_t cached_max_bytes() {
-  static const int64_t m = [] {
-    const char* e = std::getenv("PF_CACHED_MAX_BYTES");
-    return e ? std::atoll(e) : int64_t(48) << 20;
-  }();
-  return m;
-}
-
-
-bool value_index_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PF_VALUE_INDEX");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
-}
-
-// Every operator with at least PF_VALUE_INDEX_MIN stored entries (default: all) is
-// index-encoded when its values allow it.  Measured at C2: encoding only the >= 2M-entry
-// operators, Jacobi solve 6.08 ms; all of them, 5.86 ms — the smaller levels' operators
-// take less L2 space and fewer L1 requests too (the shared-memory table lookup replaces
-// an 8-byte value load); the bottom kernel gets decoded fp64 copies (fp64_view).
-int64_t value_index_min_entries() {
-  static const int64_t m = [] {
-    const char* e = std::getenv("PF_VALUE_INDEX_MIN");
-    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(0);
-  }();
-  return m;
-}
-
 // Stored values (SELL order, padding included) -> device: an 8/16-bit index into the table
 // of distinct values (distinguished by bit pattern, so -0.0 and 0.0 stay apart) when there
 // are at most 65,536 of them, else fp64.
-void encode_values(const std::vector<double>& sv, DevVals& out) {
+void encode_values(const std::vector<double>& sv, DevVals& out, const Options& o) {
   out = DevVals{};
-  if (value_index_enabled() && !sv.empty() && static_cast<int64_t>(sv.size()) >= value_index_min_entries()) {
+  if (o.value_index && !sv.empty() && static_cast<int64_t>(sv.size()) >= o.value_index_min) {
     // pass 1: the distinct values in first-seen order, giving up past 65,536.  Each chunk
     // collects its own first-seen list; merging the lists in chunk order gives the
     // sequential first-seen order.
@@ -166,7 +122,7 @@ void check_vec(const pf_hierarchy* h, const pf_vector* v, int level, const char*
 
 // SELL-32 from rows already in device order (entry order inside a row is preserved).
 void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vector<int32_t>& col,
-                    const std::vector<double>& val, DevSell& out) {
+                    const std::vector<double>& val, DevSell& out, const Options& o) {
   const int64_t n_slices = (n + kSlice - 1) / kSlice;
   std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
   std::vector<int32_t> rlen(static_cast<size_t>(std::max<int64_t>(n_slices, 1) * kSlice), 0);
@@ -200,7 +156,8 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
   out.slice_ptr.upload(sptr);
   out.row_len.upload(rlen);
   out.max_len = rlen.empty() ? 0 : *std::max_element(rlen.begin(), rlen.end());
-  encode_values(sv, out.vals);
+  encode_values(sv, out.vals, o);
+  out.smem_table = o.vtab_smem != 0;
   out.cols.upload(sc);
   out.nnz = n > 0 ? off[n] : 0;
   out.stored = sptr[n_slices];
@@ -210,7 +167,8 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
 // through perm; entry order inside a row preserved.
 void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector<int32_t>& perm,
                    const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
-                   const std::vector<double>& vals, DevSell& out) {
+                   const std::vector<double>& vals, DevSell& out,
+                   const Options& o) {
   const int64_t n_slices = (n + kSlice - 1) / kSlice;
   std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
   std::vector<int32_t> rlen(static_cast<size_t>(std::max<int64_t>(n_slices, 1) * kSlice), 0);
@@ -239,7 +197,8 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
       const int64_t base = sell_row_base(sptr.data(), d), k0 = rowptr[inv[d]];
       for (int j = 0; j < rlen[d]; ++j) sv[static_cast<size_t>(sell_entry(base, j))] = vals[static_cast<size_t>(k0 + j)];
     }
-    encode_values(sv, out.vals);
+    encode_values(sv, out.vals, o);
+    out.smem_table = o.vtab_smem != 0;
   }
   out.slice_ptr.upload(sptr);
   out.row_len.upload(rlen);
@@ -248,20 +207,9 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
   out.stored = sptr[n_slices];
 }
 
-// PF_INTERLEAVE_MIN_BYTES (default 64 MB): levels whose x is at least this large run their
-// full-level Jacobi / residual passes with the colour-interleaved block schedule (0: every
-// level with 2-8 colours; a huge value: never).
-int64_t interleave_min_bytes() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("PF_INTERLEAVE_MIN_BYTES");
-    return e ? std::atoll(e) : int64_t(64) << 20;
-  }();
-  return v;
-}
-
 // Device layout of one subdomain level: own rows colour-major (stable in host order),
 // then every other row in host order; SELL-32x4 operator; P (rows of this level).
-void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
+void build_dev_level(const HostLevel& H, DevLevel& D, int level, const Options& o) {
   PhaseTimer tm;
   const int32_t n = H.n, n_own = H.n_own;
   D.n = n;
@@ -357,7 +305,7 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
   // colour-interleaved block schedule when x outgrows L2 (RowMap, pf_types.hpp)
   D.rmap = RowMap{};
   D.rmap_grid = grid_for(n);
-  if (n_colors >= 2 && n_colors <= 8 && 8 * static_cast<int64_t>(n) >= interleave_min_bytes()) {
+  if (n_colors >= 2 && n_colors <= 8 && 8 * static_cast<int64_t>(n) >= o.interleave_min_bytes) {
     int32_t chunks = 0;
     for (int c = 0; c < n_colors; ++c)
       chunks = std::max<int32_t>(chunks, static_cast<int32_t>(grid_for(D.color_start[c + 1] - D.color_start[c])));
@@ -370,7 +318,7 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
   // --- SELL-32x4 operator: rows in device order, columns mapped, entries in CSR order,
   // written straight from the host CSR (no intermediate re-layout: at 512^3 the finest
   // level alone is 44 GB of host CSR)
-  sell_from_csr(n, inv, D.perm, H.rowptr, H.cols, H.vals, D.A);
+  sell_from_csr(n, inv, D.perm, H.rowptr, H.cols, H.vals, D.A, o);
   D.A.own_nnz = H.rowptr[n_own];
   tm("sell", level);
   D.csr_rowptr = H.rowptr;
@@ -400,7 +348,7 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level) {
 
 // P rows of the fine level in device order; R = P^T over owns_row fine rows as a
 // parent-row gather with entries in ascending fine host index.
-void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const DevLevel& DC) {
+void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const DevLevel& DC, const Options& o) {
   const int32_t nf = F.n, nc = Cc.n;
   if (F.p_off.size() != static_cast<size_t>(nf) + 1) invalid("prolongation needs n_dofs + 1 offsets");
   for (int64_t e = 0; e < F.p_off[nf]; ++e)
@@ -421,7 +369,7 @@ void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const
       pw[static_cast<size_t>(q)] = F.p_w[e];
     }
   }
-  sell_from_rows(nf, poff, pcol, pw, DF.P);
+  sell_from_rows(nf, poff, pcol, pw, DF.P, o);
   // R rows: each parent row's contributions in ascending fine host index (the reference's
   // scatter-add order).  The owned P entries in fine host order, sorted by (parent device
   // row, position) — a strict order, so the parallel sort reproduces the counting sort.
@@ -467,7 +415,7 @@ void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const
   for (int64_t i = 0; i < static_cast<int64_t>(ord.size()); ++i)
     ++roff[static_cast<size_t>(DC.perm[F.p_col[src[static_cast<size_t>(ord[static_cast<size_t>(i)])]]]) + 1];
   for (int32_t c = 0; c < nc; ++c) roff[c + 1] += roff[c];
-  sell_from_rows(nc, roff, rcol, rwt, DF.R);
+  sell_from_rows(nc, roff, rcol, rwt, DF.R, o);
 }
 
 const HostChannel* find_channel(const HostLevel& H, int kind, int peer) {
@@ -765,7 +713,7 @@ void build_replica(pf_hierarchy* h) {
     for (int r = 0; r < h->world; ++r) {
       if (!RL.host[r].set)
         state("replica of rank " + std::to_string(r) + " level " + std::to_string(l) + " not set");
-      build_dev_level(RL.host[r], RL.sub[r], l);
+      build_dev_level(RL.host[r], RL.sub[r], l, h->opt);
       stride = std::max<int64_t>(stride, RL.sub[r].n);
     }
     RL.stride = stride;
@@ -777,7 +725,7 @@ void build_replica(pf_hierarchy* h) {
     if (l > 0)
       for (int r = 0; r < h->world; ++r)
         build_transfer(RL.host[r], RL.sub[r], R.lv[static_cast<size_t>(l - 1)].host[r],
-                       R.lv[static_cast<size_t>(l - 1)].sub[r]);
+                       R.lv[static_cast<size_t>(l - 1)].sub[r], h->opt);
     build_exchange(RL.host, RL.sub, 0, true, RL.scatter, RL.acc);
     RL.x.alloc(2 * stride * h->world);
     RL.b.alloc(stride * h->world);
@@ -835,12 +783,6 @@ SellView fp64_view(pf_hierarchy::Bottom& bot, const DevSell& S) {
   return v;
 }
 
-// PF_BOTTOM_STAGE (default 1): stage the block levels in shared memory (BotStage).
-bool bottom_stage_enabled() {
-  const char* e = std::getenv("PF_BOTTOM_STAGE");  // read at build time (tests flip it)
-  return !(e && std::atoi(e) == 0);
-}
-
 // Plan and build the shared-memory staging of the block levels (BotStage, pf_bottom.cuh):
 // levels 0, 1, ... up to block_top are staged while they fit the opt-in shared memory next
 // to the descriptor and the coarse pack — each with its vectors, operator, restriction,
@@ -849,7 +791,7 @@ bool bottom_stage_enabled() {
 void stage_block_levels(pf_hierarchy* h, pf_hierarchy::Bottom& bot, BotDesc& d, const std::vector<BotSrc>& src) {
   d.stage = BotStage{};
   d.stage.hs = -1;
-  if (!bottom_stage_enabled() || d.block_top < 0) return;
+  if (!h->opt.bottom_stage || d.block_top < 0) return;
   int optin = 0;
   PF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
   auto r16 = [](int64_t b) { return (b + 15) / 16 * 16; };
@@ -970,8 +912,7 @@ bool fill_bottom(pf_hierarchy* h, pf_hierarchy::Bottom& bot, const std::vector<B
   std::memset(&d, 0, sizeof d);
   d.n_sub = n_sub;
   d.n_levels = top + 1;
-  int64_t block_rows = 1024;
-  if (const char* e = std::getenv("PF_BOTTOM_BLOCK_ROWS")) block_rows = std::atoll(e);
+  const int64_t block_rows = h->opt.bottom_block_rows;
   d.block_top = -1;
   for (int l = 0; l <= top; ++l)
     if (src[l].total <= block_rows) d.block_top = l;
@@ -1029,42 +970,29 @@ bool fill_bottom(pf_hierarchy* h, pf_hierarchy::Bottom& bot, const std::vector<B
   occ = bottom_kernel_occupancy(bot.smem);
   if (occ < 1) return false;
   int64_t want = std::max<int64_t>(sms, (max_total + kBlock - 1) / kBlock);
-  if (const char* e = std::getenv("PF_BOTTOM_GRID")) want = std::max<int64_t>(1, std::atoll(e));
+  if (h->opt.bottom_grid > 0) want = h->opt.bottom_grid;
   bot.grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(occ) * sms));
   // every bottom level staged for block 0: the other blocks would only wait at barriers
   bot.staged_all = d.stage.hs == top && d.block_top == top;
-  if (bot.staged_all && !std::getenv("PF_BOTTOM_GRID")) bot.grid = 1;
+  if (bot.staged_all && h->opt.bottom_grid <= 0) bot.grid = 1;
   bot.top = top;
   bot.active = true;
   return true;
 }
 
-// Single-device bottom kernel: levels up to PF_BOTTOM_ROWS rows (default 1024: at C2 the
-// coloured smoothers' V-cycle is 1.443 ms with no bottom kernel, 1.383 with levels <= 64k
-// rows, 1.356 with levels <= 1k rows).  Damped Jacobi does not use it unless
-// PF_BOTTOM_JACOBI=1: with programmatic dependent launch in the graph, separate per-level
-// kernels are faster for it (0.715 vs 0.744 ms).
-int64_t bottom_row_limit() {
-  int64_t limit = 1024;
-  if (const char* e = std::getenv("PF_BOTTOM_ROWS")) limit = std::atoll(e);
-  return limit;
+// Single-device bottom kernel: levels up to Options::bottom_rows rows (default 1024: at C2
+// the coloured smoothers' V-cycle is 1.443 ms with no bottom kernel, 1.383 with levels <=
+// 64k rows, 1.356 with levels <= 1k rows).  Damped Jacobi does not use it unless
+// Options::bottom_jacobi: with programmatic dependent launch in the graph, separate
+// per-level kernels are faster for it (0.715 vs 0.744 ms).  Multi-process runs replicate
+// levels up to Options::rep_bottom_rows rows in total (one allgather per cycle).
+bool bottom_for(const pf_hierarchy* h, const pf_multigrid_config& cfg) {
+  return cfg.smoother.kind != PF_SMOOTHER_JACOBI || h->opt.bottom_jacobi != 0;
 }
-bool bottom_for(const pf_multigrid_config& cfg) {
-  const char* e = std::getenv("PF_BOTTOM_JACOBI");  // read at capture time (tests flip it)
-  return cfg.smoother.kind != PF_SMOOTHER_JACOBI || (e && std::atoi(e) != 0);
-}
-// Multi-process replicated bottom (all ranks' levels on every GPU, one allgather per
-// cycle): levels up to PF_REP_BOTTOM_ROWS rows in total (default 65536).
-int64_t rep_bottom_row_limit() {
-  int64_t limit = 65536;
-  if (const char* e = std::getenv("PF_REP_BOTTOM_ROWS")) limit = std::atoll(e);
-  return limit;
-}
-
 // Levels whose total row count stays below the limit run as one cooperative kernel when
 // every rank of the level lives on this device.
 void build_bottom(pf_hierarchy* h) {
-  const int64_t limit = bottom_row_limit();
+  const int64_t limit = h->opt.bottom_rows;
   if (h->world != h->n_sub || limit <= 0) return;
   int top = -1;
   for (int l = 0; l < h->n_levels - 1 && l < kBotMaxLevels; ++l)
@@ -1083,7 +1011,7 @@ void build_bottom(pf_hierarchy* h) {
 void build_rep_bottom(pf_hierarchy* h) {
   auto& R = h->rep;
   const int top = static_cast<int>(R.lv.size()) - 1;
-  const int64_t limit = rep_bottom_row_limit();
+  const int64_t limit = h->opt.rep_bottom_rows;
   if (top < 1 || top >= h->n_levels - 1 || limit <= 0) return;
   std::vector<BotSrc> src;
   for (int l = 0; l <= top; ++l) {

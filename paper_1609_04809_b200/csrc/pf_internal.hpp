@@ -31,7 +31,6 @@ int sm_count(int device);
 [[noreturn]] void invalid(const std::string& m);
 [[noreturn]] void state(const std::string& m);
 void trace(const char* what, int rank = -1);  // PF_TRACE=1: one stderr line per major host step
-bool pdl_enabled();
 
 // Every kernel launch of the library: programmatic dependent launch (PF_PDL) on the
 // hierarchy's stream (or `stream`), counted into the hierarchy (or, while a graph is being
@@ -58,7 +57,7 @@ struct Launcher {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
-    lc.numAttrs = pdl_enabled() ? 1 : 0;
+    lc.numAttrs = h->opt.pdl ? 1 : 0;
     PF_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...));
     ++*counter;
   }
@@ -69,9 +68,10 @@ inline Launcher launcher(pf_hierarchy* h, cudaStream_t stream = nullptr) {
   return Launcher{h, g_capture_counter ? g_capture_counter : &h->launches, stream};
 }
 
+// ---- per-hierarchy options (pf_runtime.hpp Options; pf_hierarchy_set_option)
+Options options_from_env();
+
 // ---- operator views and the kernels' value-kind dispatch
-bool vtab_smem();
-int64_t cached_max_bytes();
 inline SellView view_of(const DevVals& v, const DevSell& s) {
   const void* idx = v.vkind == 1 ? static_cast<const void*>(v.vi8.p)
                   : v.vkind == 2 ? static_cast<const void*>(v.vi16.p) : nullptr;
@@ -95,7 +95,7 @@ void vk_dispatch(int vkind, F&& f) {
 template <typename F>
 void vk_dispatch_rows(const DevSell& S, F&& f) {
   const bool cached = S.keep_l2;
-  const int kind = S.vals.vkind == 1 && vtab_smem() ? kVKSmem : S.vals.vkind;
+  const int kind = S.vals.vkind == 1 && S.smem_table ? kVKSmem : S.vals.vkind;
   switch (kind | (cached ? kVKCached : 0)) {
     case 1: f(std::integral_constant<int, 1>{}); break;
     case 2: f(std::integral_constant<int, 2>{}); break;
@@ -123,12 +123,13 @@ struct PhaseTimer {
 
 // ---- pf_build.cu
 constexpr size_t kCoarseSmemMax = 160 * 1024;  // opt-in shared memory for the coarse pack
-void encode_values(const std::vector<double>& sv, DevVals& out);
+void encode_values(const std::vector<double>& sv, DevVals& out, const Options& o);
 void check_level(const pf_hierarchy* h, int level);
 void check_vec(const pf_hierarchy* h, const pf_vector* v, int level, const char* what);
 HostLevel parse_desc(const pf_level_desc& dd, int me, int world, bool need_p);
-void build_dev_level(const HostLevel& H, DevLevel& D, int level);
-void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const DevLevel& DC);
+void build_dev_level(const HostLevel& H, DevLevel& D, int level, const Options& o);
+void build_transfer(const HostLevel& F, DevLevel& DF, const HostLevel& Cc, const DevLevel& DC,
+                    const Options& o);
 void build_plans(pf_hierarchy* h, int l);
 CoarsePack make_coarse_pack(const std::vector<HostLevel>& H, const std::vector<DevLevel>& D,
                             const std::array<ExchangePlan, PF_NUM_CHANNEL_KINDS>& plans,
@@ -137,7 +138,7 @@ CoarsePack make_coarse_pack(const std::vector<HostLevel>& H, const std::vector<D
 void build_replica(pf_hierarchy* h);
 void build_bottom(pf_hierarchy* h);
 void build_rep_bottom(pf_hierarchy* h);
-bool bottom_for(const pf_multigrid_config& cfg);
+bool bottom_for(const pf_hierarchy* h, const pf_multigrid_config& cfg);
 
 // ---- pf_runtime.cu
 size_t bottom_kernel_static_smem();

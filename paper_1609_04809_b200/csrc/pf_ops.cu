@@ -161,7 +161,7 @@ pf_status pf_operator_set_values(pf_operator* op, int sub, const double* values,
     for (int64_t k = D.csr_rowptr[hr]; k < D.csr_rowptr[hr + 1]; ++k)
       sv[static_cast<size_t>(sell_entry(base, static_cast<int>(k - D.csr_rowptr[hr])))] = values[k];
   }
-  encode_values(sv, op->vals[sub]);
+  encode_values(sv, op->vals[sub], op->h->opt);
   op->set[sub] = true;
   PF_API_END
 }

@@ -17,7 +17,7 @@ namespace pf {
 
 // pf_runtime.cu
 int64_t* launch_counter(pf_hierarchy* h);
-bool pdl_on();
+bool pdl_on(const pf_hierarchy* h);
 
 namespace {
 
@@ -131,7 +131,7 @@ void PeerTransport::launch_exchange(const Op& o, double* v, bool wait_only, cuda
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
-  lc.numAttrs = pdl_on() ? 1 : 0;
+  lc.numAttrs = pdl_on(h) ? 1 : 0;
   cuda_check(cudaLaunchKernelEx(&lc, k_peer_exchange, args(o, wait_only), v), "k_peer_exchange");
   ++*launch_counter(h);
 }
@@ -158,7 +158,7 @@ void PeerTransport::ack_plan(const ExchangePlan& P, cudaStream_t s) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
-  lc.numAttrs = pdl_on() ? 1 : 0;
+  lc.numAttrs = pdl_on(h) ? 1 : 0;
   cuda_check(cudaLaunchKernelEx(&lc, k_peer_ack, args(o, true)), "k_peer_ack");
   ++*launch_counter(h);
 }

@@ -53,6 +53,31 @@ void cuda_check(cudaError_t e, const char* what) {
     throw Error(PF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+std::atomic<int64_t> g_guard_failures{0};
+bool guard_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_GUARD");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+void guard_check(const void* zone, size_t bytes) {
+  unsigned char h[kGuardBytes];
+  // (no device-wide synchronisation: in-process peer ranks may have kernels waiting on this
+  // thread; the library synchronises its streams before it frees their buffers)
+  if (cudaMemcpy(h, zone, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return;  // a failed device (reported elsewhere), not a guard hit
+  }
+  size_t first = kGuardBytes;
+  for (size_t i = 0; i < kGuardBytes && first == kGuardBytes; ++i)
+    if (h[i] != 0xFF) first = i;
+  if (first != kGuardBytes) {
+    ++g_guard_failures;
+    std::fprintf(stderr, "[pf guard] write past the end of a %zu-byte device buffer (first at +%zu)\n", bytes, first);
+  }
+}
+
 namespace rt {
 
 thread_local int64_t* g_capture_counter = nullptr;
@@ -83,12 +108,53 @@ void trace(const char* what, int rank) {
 }
 [[noreturn]] void state(const std::string& m) { throw Error(PF_ERR_STATE, m); }
 
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PF_PDL");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
+
+// The option table: name (pf_hierarchy_set_option), environment variable, member, and
+// whether it shapes the device layout (fixed by pf_hierarchy_finalize).
+struct OptionSpec {
+  const char* name;
+  const char* env;
+  int64_t Options::*field;
+  bool build;
+};
+const OptionSpec kOptions[] = {
+    {"value_index", "PF_VALUE_INDEX", &Options::value_index, true},
+    {"value_index_min", "PF_VALUE_INDEX_MIN", &Options::value_index_min, true},
+    {"vtab_smem", "PF_VTAB_SMEM", &Options::vtab_smem, true},
+    {"cached_max_bytes", "PF_CACHED_MAX_BYTES", &Options::cached_max_bytes, true},
+    {"interleave_min_bytes", "PF_INTERLEAVE_MIN_BYTES", &Options::interleave_min_bytes, true},
+    {"bottom_rows", "PF_BOTTOM_ROWS", &Options::bottom_rows, true},
+    {"bottom_block_rows", "PF_BOTTOM_BLOCK_ROWS", &Options::bottom_block_rows, true},
+    {"bottom_grid", "PF_BOTTOM_GRID", &Options::bottom_grid, true},
+    {"bottom_stage", "PF_BOTTOM_STAGE", &Options::bottom_stage, true},
+    {"rep_bottom_rows", "PF_REP_BOTTOM_ROWS", &Options::rep_bottom_rows, true},
+    {"bottom_jacobi", "PF_BOTTOM_JACOBI", &Options::bottom_jacobi, false},
+    {"bottom_block_kernel", "PF_BOTTOM_BLOCK_KERNEL", &Options::bottom_block_kernel, false},
+    {"split_row_len", "PF_SPLIT_ROW_LEN", &Options::split_row_len, false},
+    {"split_max_rows", "PF_SPLIT_MAX_ROWS", &Options::split_max_rows, false},
+    {"wide_max_rows", "PF_WIDE_MAX_ROWS", &Options::wide_max_rows, false},
+    {"fused_rr_rows", "PF_FUSED_RR_ROWS", &Options::fused_rr_rows, false},
+    {"sor_tma", "PF_SOR_TMA", &Options::sor_tma, false},
+    {"sor_tma_min_rows", "PF_SOR_TMA_MIN_ROWS", &Options::sor_tma_min_rows, false},
+    {"sor_tma_bps", "PF_SOR_TMA_BPS", &Options::sor_tma_bps, false},
+    {"sor_tma_cfg", "PF_SOR_TMA_CFG", &Options::sor_tma_cfg, false},
+    {"pdl", "PF_PDL", &Options::pdl, false},
+    {"solve_mode_host", nullptr, &Options::solve_mode_host, false},  // env: PF_SOLVE_MODE=host
+};
+
+const OptionSpec* find_option(const char* name) {
+  for (const OptionSpec& o : kOptions)
+    if (name && std::strcmp(o.name, name) == 0) return &o;
+  return nullptr;
+}
+
+Options options_from_env() {
+  Options o;
+  for (const OptionSpec& s : kOptions)
+    if (s.env)
+      if (const char* e = std::getenv(s.env)) o.*s.field = std::atoll(e);
+  if (const char* e = std::getenv("PF_SOLVE_MODE")) o.solve_mode_host = std::string(e) == "host";
+  return o;
 }
 
 size_t bottom_kernel_static_smem() {
@@ -236,44 +302,19 @@ void enq_copy(pf_hierarchy* h, const double* src, double* dst, int64_t n) {
   launcher(h)(grid_for(n), kBlock, k_copy, src, dst, n);
 }
 
-// One colour of a coloured sweep.  Levels with long rows (Q2: up to 125 entries) take
-// the slice-split kernel: a colour has few rows there (1/27 of the level), so one thread
-// per row leaves most SMs idle while each thread walks its 32 groups.
-int split_row_len() {
-  static const int v = [] {
-    const char* e = std::getenv("PF_SPLIT_ROW_LEN");
-    return e ? std::atoi(e) : 48;
-  }();
-  return v;
-}
-
-// ... on levels up to PF_SPLIT_MAX_ROWS own rows (default 1M): on larger ones the colours
-// are big enough for the row kernel (Q2 at 64^3: 482 vs 431 us per sweep).
-int64_t split_max_rows() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("PF_SPLIT_MAX_ROWS");
-    return e ? std::atoll(e) : int64_t(1) << 20;
-  }();
-  return v;
-}
-
-// Launches of at most PF_WIDE_MAX_ROWS rows (default: one wave of the wide kernels, 2
+// Launches of at most Options::wide_max_rows rows (default: one wave of the wide kernels, 2
 // blocks of 256 per SM) on operators with 8-bit value indices and rows of <= 28 entries
 // take the wide-row kernels (k_color_sweep_wide / k_jacobi_wide: the whole row's operator
 // loaded before griddepcontrol.wait, all its x gathers in flight at once after it); 0: never.
 constexpr int kWideGroups = 7;
-int64_t wide_max_rows(int device) {
-  static const int64_t env = [] {
-    const char* e = std::getenv("PF_WIDE_MAX_ROWS");
-    return e ? std::atoll(e) : int64_t(-1);
-  }();
-  return env >= 0 ? env : int64_t(PF_WIDE_MINB) * sm_count(device) * kBlock;
+int64_t wide_max_rows(const pf_hierarchy* h) {
+  return h->opt.wide_max_rows >= 0 ? h->opt.wide_max_rows : int64_t(PF_WIDE_MINB) * sm_count(h->device) * kBlock;
 }
 template <int vk>
 bool wide_ok(const pf_hierarchy* h, const DevLevel& D, int64_t rows) {
   constexpr int K = vk_kind<vk>();
   return (K == 1 || K == kVKSmem) && D.A.max_len > 0 && D.A.max_len <= 4 * kWideGroups && rows > 0 &&
-         rows <= wide_max_rows(h->device);
+         rows <= wide_max_rows(h);
 }
 
 // One damped-Jacobi sweep of subdomain level D, src -> dst.
@@ -291,47 +332,25 @@ void enq_jacobi_sweep(pf_hierarchy* h, DevLevel& D, const double* src, double* d
   });
 }
 
-// PF_SOR_TMA (default 1): colour sweeps of operators with rows of <= 28 entries (Q1,
-// rotated Q1) take the TMA-staged persistent kernel (pf_sweep_tma.cuh) on levels with at
-// least PF_SOR_TMA_MIN_ROWS own rows; PF_SOR_TMA_BPS blocks per SM (default 1, which leaves
-// room for the next colour's blocks to stream their operator chunks meanwhile).
-bool sor_tma_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PF_SOR_TMA");
-    return e && std::atoi(e) != 0;
-  }();
-  return on;
-}
-int64_t sor_tma_min_rows() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("PF_SOR_TMA_MIN_ROWS");
-    return e ? std::atoll(e) : int64_t(65536);
-  }();
-  return v;
-}
-int sor_tma_bps() {
-  static const int v = [] {
-    const char* e = std::getenv("PF_SOR_TMA_BPS");
-    return e ? std::max(1, std::atoi(e)) : 2;
-  }();
-  return v;
-}
-int sor_tma_cfg() {  // experiment: 0 = 8 warps x 2 stages, 1 = 4 x 4, 2 = 8 x 3
-  static const int v = [] {
-    const char* e = std::getenv("PF_SOR_TMA_CFG");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
+// Options::sor_tma (default 0, measured slower): colour sweeps of operators with rows of <= 28
+// entries (Q1, rotated Q1) take the TMA-staged persistent kernel (pf_sweep_tma.cuh) on
+// levels with at least sor_tma_min_rows own rows, sor_tma_bps blocks per SM, warp layout
+// sor_tma_cfg (0 = 8 warps x 2 stages, 1 = 4 x 4, 2 = 8 x 3).
 
+// One colour of a coloured sweep.  Levels with long rows (Q2: up to 125 entries; longer
+// than Options::split_row_len, default 48) take the slice-split kernel: a colour has few
+// rows there (1/27 of the level), so one thread per row leaves most SMs idle while each
+// thread walks its 32 groups — on levels up to Options::split_max_rows own rows (default
+// 1M): on larger ones the colours are big enough for the row kernel (Q2 at 64^3: 482 vs
+// 431 us per sweep).
 void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega, double* x, const double* b) {
   const int32_t r0 = D.color_start[c], r1 = D.color_start[c + 1];
   if (r1 <= r0) return;
   auto launch = launcher(h);
-  const int split = split_row_len();
+  const int64_t split = h->opt.split_row_len;
   vk_dispatch_rows(D.A, [&](auto V) {
     constexpr int vk = decltype(V)::value;
-    if (sor_tma_enabled() && D.A.max_len <= 4 * kTmaMaxGroups && D.A.max_len > 0 && D.n_own >= sor_tma_min_rows()) {
+    if (h->opt.sor_tma && D.A.max_len <= 4 * kTmaMaxGroups && D.A.max_len > 0 && D.n_own >= h->opt.sor_tma_min_rows) {
       const int32_t width = (D.A.max_len + 3) / 4 * 4;
       const TmaStageLayout lay = tma_layout(width, tma_vbytes<vk>());
       auto go = [&](auto W, auto S) {
@@ -346,10 +365,10 @@ void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega
         }
         const int64_t n_slices = ((r1 - 1) >> 5) - (r0 >> 5) + 1;
         const int64_t grid = std::min<int64_t>((n_slices + kw - 1) / kw,
-                                               static_cast<int64_t>(sor_tma_bps()) * sm_count(h->device));
+                                               std::max<int64_t>(1, h->opt.sor_tma_bps) * sm_count(h->device));
         launch.with_smem(smem)(static_cast<unsigned>(grid), 32 * kw, kern, view(D.A), x, b, r0, r1, omega, width);
       };
-      switch (sor_tma_cfg()) {
+      switch (h->opt.sor_tma_cfg) {
         case 1: go(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}); break;
         case 2: go(std::integral_constant<int, 8>{}, std::integral_constant<int, 3>{}); break;
         default: go(std::integral_constant<int, 8>{}, std::integral_constant<int, 2>{}); break;
@@ -365,7 +384,7 @@ void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega
         return;
       }
     }
-    if (split > 0 && D.A.max_len > split && D.n_own <= split_max_rows()) {
+    if (split > 0 && D.A.max_len > split && D.n_own <= h->opt.split_max_rows) {
       const int32_t width = (D.A.max_len + 3) / 4 * 4;
       const size_t smem = sizeof(double) * kSlice * static_cast<size_t>(width);
       auto kern = sor ? k_color_sweep_split<true, vk> : k_color_sweep_split<false, vk>;
@@ -528,15 +547,12 @@ void enq_prolong(pf_hierarchy* h, int fine, const double* xc, double* xf, int ad
   }
 }
 
-// PF_FUSED_RR_ROWS (default 8192; 0 = off): levels up to that many rows form the cycle
+// Options::fused_rr_rows (default 8192; 0 = off): levels up to that many rows form the cycle
 // residual and its restriction in one launch (k_residual_restrict).  Measured at C2:
 // levels 1-3 fused, Jacobi solve 5.86 -> 5.78 ms; level 4 (36k rows) too, 5.82 ms (its
 // redundant fine-residual work outweighs the saved launch).
 bool fused_rr_for(pf_hierarchy* h, int fine) {
-  static const int64_t limit = [] {
-    const char* e = std::getenv("PF_FUSED_RR_ROWS");
-    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(8192);
-  }();
+  const int64_t limit = h->opt.fused_rr_rows;
   for (const DevLevel& D : h->levels[fine].sub)
     if (D.n > limit || D.R.max_len > 32) return false;
   return true;
@@ -684,20 +700,13 @@ bool enq_coarse(pf_hierarchy* h, int l, double* x, const double* b, double tol, 
 
 // cycle(bot.top) in one cooperative launch; lev[top].b holds the restricted residual
 // (before the master/slave accumulate when accumulate_top) and lev[top].x is zero.
-// PF_BOTTOM_BLOCK_KERNEL (default 1): a bottom whose levels are all staged runs as the
-// one-block k_bottom_block instead of the cooperative k_bottom.
-bool bottom_block_kernel() {
-  static const bool on = [] {
-    const char* e = std::getenv("PF_BOTTOM_BLOCK_KERNEL");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
-}
+// (Options::bottom_block_kernel, default 1: a bottom whose levels are all staged runs as the
+// one-block k_bottom_block instead of the cooperative k_bottom.)
 
 void enq_bottom(pf_hierarchy* h, const pf_hierarchy::Bottom& bot, const pf_multigrid_config& cfg,
                 int accumulate_top) {
   static const int calib0 = std::getenv("PF_BOTTOM_CALIB") ? std::atoi(std::getenv("PF_BOTTOM_CALIB")) : 0;
-  if (bot.staged_all && bottom_block_kernel() && calib0 == 0) {
+  if (bot.staged_all && h->opt.bottom_block_kernel && calib0 == 0) {
     const BotCfg c{cfg.smoother.kind, cfg.pre_smooth, cfg.post_smooth, cfg.smoother.local_sweeps,
                    cfg.coarse_max_iter, cfg.smoother.damping, cfg.coarse_tol, 1 << 20, 0,
                    h->colorwise && cfg.smoother.kind != PF_SMOOTHER_JACOBI ? 1 : 0};
@@ -753,7 +762,7 @@ void enq_cycle(pf_hierarchy* h, int l, pf_vector* xv, const double* b, const pf_
     enq_residual(h, l, x, b, L.r.p);
     enq_restrict(h, l, L.r.p, Cl.b->cur(), Cl.x->cur(), 1);
   }
-  if (h->bot.active && l - 1 == h->bot.top && bottom_for(cfg)) {
+  if (h->bot.active && l - 1 == h->bot.top && bottom_for(h, cfg)) {
     enq_bottom(h, h->bot, cfg, 1);  // accumulate, cycle(top) ... down to the coarse solve and back
   } else if (h->rep.bot.active && l - 1 == h->rep.bot.top) {
     // multi-process: the restricted partial sums of every rank in one allgather, then the
@@ -1052,8 +1061,7 @@ void solve_outer_dev(pf_hierarchy* h, pf_vector* x, const pf_vector* b, const pf
   const int top = h->n_levels - 1;
   const double t0 = wall_now();
   pf_solve_stats s{};
-  const char* mode = std::getenv("PF_SOLVE_MODE");
-  if (h->world == h->n_sub && !(mode && std::string(mode) == "host")) {
+  if (h->world == h->n_sub && !h->opt.solve_mode_host) {
     auto& g = solve_graph(h, x, b, cfg);
     trace("solve graph: launch");
     PF_CUDA(cudaGraphLaunch(g.exec, h->stream));
@@ -1159,7 +1167,7 @@ pf_vector* new_vector(pf_hierarchy* h, int level) {
 // Kernel-launch accounting and the PDL switch for launches made outside this file
 // (pf_peer.cu).
 int64_t* launch_counter(pf_hierarchy* h) { return rt::g_capture_counter ? rt::g_capture_counter : &h->launches; }
-bool pdl_on() { return rt::pdl_enabled(); }
+bool pdl_on(const pf_hierarchy* h) { return h->opt.pdl != 0; }
 // pf_peer.cu
 int64_t peer_export(pf_hierarchy* h, void* buf, int64_t cap);
 void peer_import(pf_hierarchy* h, const void* blobs, int64_t stride);
@@ -1240,6 +1248,7 @@ pf_status pf_hierarchy_create(int device, int n_levels, int n_subdomains, int ra
   h->n_sub = n_subdomains;
   h->rank_base = rank_base;
   h->world = world_size;
+  h->opt = options_from_env();
   h->levels.resize(static_cast<size_t>(n_levels));
   for (auto& L : h->levels) L.host.resize(static_cast<size_t>(n_subdomains));
   PF_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -1250,6 +1259,64 @@ pf_status pf_hierarchy_create(int device, int n_levels, int n_subdomains, int ra
   PF_CUDA(cudaEventCreate(&h->ev1));
   PF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->pinned), 64 * sizeof(double)));
   *out = h.release();
+  PF_API_END
+}
+
+pf_status pf_hierarchy_set_option(pf_hierarchy* h, const char* name, int64_t value) {
+  PF_API_BEGIN
+  if (!h) invalid("null hierarchy");
+  const OptionSpec* o = find_option(name);
+  if (!o) invalid(std::string("unknown option ") + (name ? name : "(null)"));
+  if (o->build && h->finalized) state(std::string("option ") + o->name + " shapes the device layout: set it before pf_hierarchy_finalize");
+  if (h->opt.*o->field != value) {
+    h->opt.*o->field = value;
+    if (h->finalized) drop_graphs(h);  // captured launches may depend on it
+  }
+  PF_API_END
+}
+
+pf_status pf_hierarchy_get_option(const pf_hierarchy* h, const char* name, int64_t* out) {
+  PF_API_BEGIN
+  if (!h || !out) invalid("null argument");
+  const OptionSpec* o = find_option(name);
+  if (!o) invalid(std::string("unknown option ") + (name ? name : "(null)"));
+  *out = h->opt.*o->field;
+  PF_API_END
+}
+
+pf_status pf_debug_guard_failures(int64_t* out) {
+  PF_API_BEGIN
+  if (!out) invalid("null output");
+  *out = g_guard_failures.load();
+  PF_API_END
+}
+
+pf_status pf_debug_guard_selftest(int device, int* detected) {
+  PF_API_BEGIN
+  if (!detected) invalid("null output");
+  PF_CUDA(cudaSetDevice(device));
+  const int64_t before = g_guard_failures.load();
+  {
+    DevBuf<double> v;
+    v.alloc(100, true);
+    k_fill<<<1, kBlock>>>(v.p, 1.0, 101);  // one element past the end
+    PF_CUDA(cudaGetLastError());
+  }
+  *detected = static_cast<int>(g_guard_failures.load() - before);
+  g_guard_failures = before;  // the planted hit is not a failure of the run
+  PF_API_END
+}
+
+pf_status pf_option_names(char* buf, int64_t capacity) {
+  PF_API_BEGIN
+  std::string all;
+  for (const OptionSpec& o : kOptions) {
+    if (!all.empty()) all += ' ';
+    all += o.name;
+    all += o.build ? ":build" : ":launch";
+  }
+  if (!buf || capacity < static_cast<int64_t>(all.size()) + 1) invalid("buffer too small for the option names");
+  std::memcpy(buf, all.c_str(), all.size() + 1);
   PF_API_END
 }
 
@@ -1304,7 +1371,7 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
     for (int s = 0; s < h->n_sub; ++s) {
       if (!L.host[s].set)
         state("level " + std::to_string(l) + " subdomain " + std::to_string(s) + " not set");
-      build_dev_level(L.host[s], L.sub[s], l);
+      build_dev_level(L.host[s], L.sub[s], l, h->opt);
       if (h->world != h->n_sub) {  // the own rows reading a non-own copy (build_fused_plans)
         const HostLevel& H = L.host[s];
         DevLevel& D = L.sub[s];
@@ -1329,7 +1396,7 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
     PhaseTimer tm;
     if (l > 0)
       for (int s = 0; s < h->n_sub; ++s)
-        build_transfer(L.host[s], L.sub[s], h->levels[l - 1].host[s], h->levels[l - 1].sub[s]);
+        build_transfer(L.host[s], L.sub[s], h->levels[l - 1].host[s], h->levels[l - 1].sub[s], h->opt);
     tm("transfer", l);
     build_plans(h, l);
     tm("plans", l);
@@ -1358,7 +1425,7 @@ pf_status pf_hierarchy_finalize(pf_hierarchy* h) {
     for (DevLevel& D : h->levels[l].sub)
       for (DevSell* S : {&D.A, &D.P, &D.R})
         S->keep_l2 = S->vals.bytes() + S->cols.bytes() + S->row_len.bytes() + S->slice_ptr.bytes() <=
-                     cached_max_bytes();
+                     h->opt.cached_max_bytes;
   if (h->world != h->n_sub) build_replica(h);
   h->staging.alloc(max_total);
   for (int l = 0; l < h->n_levels; ++l) {

@@ -27,29 +27,47 @@ struct Error : std::runtime_error {
 void cuda_check(cudaError_t e, const char* what);
 #define PF_CUDA(x) ::pf::cuda_check((x), #x)
 
+// Guard zones (PF_GUARD=1; memory checking in the tests, compute-sanitizer being closed on
+// the GPU pool): every DevBuf is followed by kGuardBytes of 0xFF — NaN as a double, -1 as an
+// index, so a kernel reading past an array feeds NaN or a wild index into a bit-exact
+// comparison with the oracle — and the zone is verified when the buffer is freed: a write
+// past the end is counted (pf_debug_guard_failures) and reported on stderr.
+constexpr size_t kGuardBytes = 4096;
+bool guard_on();
+void guard_check(const void* zone, size_t bytes);
+
 // Owning device buffer.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   int64_t n = 0;
+  bool guarded = false;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), guarded(o.guarded) { o.p = nullptr; o.n = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { reset(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) { reset(); p = o.p; n = o.n; guarded = o.guarded; o.p = nullptr; o.n = 0; }
     return *this;
   }
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (guarded) guard_check(reinterpret_cast<const char*>(p) + bytes(), static_cast<size_t>(bytes()));
+      cudaFree(p);
+    }
     p = nullptr;
     n = 0;
   }
-  void alloc(int64_t count) {
+  void alloc(int64_t count, bool force_guard = false) {
     reset();
     n = count;
-    if (count > 0) PF_CUDA(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
+    guarded = force_guard || guard_on();
+    if (count > 0) {
+      const size_t b = sizeof(T) * static_cast<size_t>(count);
+      PF_CUDA(cudaMalloc(&p, b + (guarded ? kGuardBytes : 0)));
+      if (guarded) PF_CUDA(cudaMemset(reinterpret_cast<char*>(p) + b, 0xFF, kGuardBytes));
+    }
   }
   void upload(const std::vector<T>& v) {
     alloc(static_cast<int64_t>(v.size()));
@@ -100,6 +118,7 @@ struct DevSell {
   int64_t nnz = 0, own_nnz = 0, stored = 0;
   int32_t max_len = 0;  // longest row
   bool keep_l2 = false;  // read with the caching policy (kVKCached): coarse levels that fit L2
+  bool smem_table = true;  // an 8-bit table is staged in shared memory by the row kernels (Options::vtab_smem)
 };
 
 // One subdomain of one level on the device.
@@ -217,8 +236,48 @@ struct pf_vector {
   int64_t total = 0;
 };
 
+namespace pf {
+// Tuning options of one hierarchy (DESIGN.md §6 "Knobs").  Each starts at its measured-best
+// default, is overridden by the PF_* environment variable of the same name (upper case)
+// when the hierarchy is created, and can then be set with pf_hierarchy_set_option.  Build
+// options shape the device layout and are fixed by pf_hierarchy_finalize; launch options
+// steer the enqueue (a change drops the cached graphs).
+struct Options {
+  // build
+  int64_t value_index = 1;            // index-encode operator values (8/16-bit)
+  // smallest operator (stored entries) encoded; measured at C2: encoding only the >= 2M-entry
+  // operators, Jacobi solve 6.08 ms; all of them, 5.86 ms (the smaller levels' operators take
+  // less L2 space and fewer L1 requests too)
+  int64_t value_index_min = 0;
+  int64_t vtab_smem = 1;              // 8-bit value table staged in shared memory (0: through L1)
+  // operators of the levels below the finest up to this size (about 40 % of the 126 MB L2)
+  // are read with the caching load policy and stay L2-resident across a cycle's sweeps; the
+  // finest level, and larger ones, stream evict-first
+  int64_t cached_max_bytes = int64_t(48) << 20;
+  // levels whose x is at least this large run their full-level Jacobi / residual passes with
+  // the colour-interleaved block schedule (0: every level with 2-8 colours)
+  int64_t interleave_min_bytes = int64_t(64) << 20;
+  int64_t bottom_rows = 1024;         // bottom kernel: levels up to this many rows
+  int64_t bottom_block_rows = 1024;   // ... of which block 0 runs those up to this many rows
+  int64_t bottom_grid = 0;            // bottom kernel grid (0: automatic)
+  int64_t bottom_stage = 1;           // stage the block levels in shared memory
+  int64_t rep_bottom_rows = 65536;    // multi-process replicated bottom levels
+  // launch
+  int64_t bottom_jacobi = 0;          // damped Jacobi through the bottom kernel too
+  int64_t bottom_block_kernel = 1;    // fully staged bottom as the one-block kernel
+  int64_t split_row_len = 48;         // slice-split colour sweep for rows longer than this
+  int64_t split_max_rows = int64_t(1) << 20;  // ... on levels up to this many own rows
+  int64_t wide_max_rows = -1;         // wide-row kernels for launches up to this many rows (-1: one wave)
+  int64_t fused_rr_rows = 8192;       // residual + restriction in one launch up to this many rows
+  int64_t sor_tma = 0, sor_tma_min_rows = 65536, sor_tma_bps = 2, sor_tma_cfg = 0;  // opt-in TMA colour sweep
+  int64_t pdl = 1;                    // programmatic dependent launch
+  int64_t solve_mode_host = 0;        // host-driven outer loop instead of the device WHILE graph
+};
+}  // namespace pf
+
 struct pf_hierarchy {
   int device = 0;
+  pf::Options opt;
   int n_levels = 0, n_sub = 1, rank_base = 0, world = 1;
   bool finalized = false;
   bool fused = false;  // master/slave + halo scatters as one message group (direct halo lists)

@@ -155,7 +155,8 @@ class Hierarchy:
     """
 
     def __init__(self, levels, device: int = 0, rank_base: int = 0, world_size: int | None = None,
-                 finalize: bool = True, coarse_replicas=None, fused_exchanges: bool = False):
+                 finalize: bool = True, coarse_replicas=None, fused_exchanges: bool = False,
+                 options: dict | None = None):
         n_sub = len(levels)
         n_levels = len(levels[0])
         world = n_sub if world_size is None else world_size
@@ -164,6 +165,8 @@ class Hierarchy:
         self._vectors = weakref.WeakSet()
         _lib.check(L.pf_hierarchy_create(device, n_levels, n_sub, rank_base, world, C.byref(self._h)))
         self.n_levels, self.n_sub, self.rank_base, self.world = n_levels, n_sub, rank_base, world
+        for k, v in (options or {}).items():
+            self.set_option(k, v)
         self._sizes = [[lv.n for lv in sub] for sub in levels]
         for s, sub in enumerate(levels):
             for l, lv in enumerate(sub):
@@ -185,7 +188,7 @@ class Hierarchy:
 
     @classmethod
     def from_setups(cls, setups, device: int = 0, rank_base: int = 0, world_size: int | None = None,
-                    coarse_replicas=None, fused_exchanges: bool = False) -> "Hierarchy":
+                    coarse_replicas=None, fused_exchanges: bool = False, options: dict | None = None) -> "Hierarchy":
         """A hierarchy straight from native StructuredSetups (materialize=False): the level
         arrays move from each setup into the hierarchy and on to the device, without numpy
         copies or a second host copy (large grids: 512^3 fits in host memory)."""
@@ -197,6 +200,8 @@ class Hierarchy:
         self._vectors = weakref.WeakSet()
         _lib.check(L.pf_hierarchy_create(device, n_levels, n_sub, rank_base, world, C.byref(self._h)))
         self.n_levels, self.n_sub, self.rank_base, self.world = n_levels, n_sub, rank_base, world
+        for k, v in (options or {}).items():
+            self.set_option(k, v)
         self._sizes = [list(s.sizes) for s in setups]
         for si, s in enumerate(setups):
             for l in range(n_levels):  # the arrays move from the setup: one host copy
@@ -211,6 +216,16 @@ class Hierarchy:
             _lib.check(L.pf_hierarchy_set_fused_exchanges(self._h, 1))
         self.finalize()
         return self
+
+    def set_option(self, name: str, value: int) -> "Hierarchy":
+        """pf_hierarchy_set_option: a tuning option of this hierarchy (option_names())."""
+        _lib.check(_lib.lib().pf_hierarchy_set_option(self._h, name.encode(), int(value)))
+        return self
+
+    def get_option(self, name: str) -> int:
+        out = C.c_int64()
+        _lib.check(_lib.lib().pf_hierarchy_get_option(self._h, name.encode(), C.byref(out)))
+        return out.value
 
     def finalize(self):
         _lib.check(_lib.lib().pf_hierarchy_finalize(self._h))
@@ -335,6 +350,13 @@ class Hierarchy:
 
 
 # ---------------------------------------------------------------- reference API --
+
+def option_names() -> dict:
+    """Every tuning option: {name: "build" | "launch"} (pf_option_names; no GPU needed)."""
+    buf = C.create_string_buffer(4096)
+    _lib.check(_lib.lib().pf_option_names(buf, len(buf)))
+    return dict(item.split(":") for item in buf.value.decode().split())
+
 
 def spmv(h: Hierarchy, level: int, x: DeviceVector, y: DeviceVector) -> None:
     _lib.check(_lib.lib().pf_spmv(h._h, level, x._p, y._p))

@@ -59,3 +59,19 @@ def test_argument_errors_without_a_device():
     assert (cfg.cycles, cfg.pre_smooth, cfg.post_smooth, cfg.coarse_tol, cfg.coarse_max_iter,
             cfg.outer_tol, cfg.outer_max_cycles) == (1, 3, 3, 1e-12, 20000, 1e-9, 100)
     assert (cfg.smoother.kind, cfg.smoother.sweeps, cfg.smoother.damping) == (1, 3, 0.8)
+
+
+def test_option_table_without_a_device():
+    """pf_option_names lists every tuning option with its kind; the knobs DESIGN.md §6
+    documents are all there (build options shape the device layout, launch options steer
+    the enqueue)."""
+    from paper_1609_04809_b200 import gmg
+    names = gmg.option_names()
+    assert names["value_index"] == "build" and names["bottom_stage"] == "build"
+    assert names["wide_max_rows"] == "launch" and names["solve_mode_host"] == "launch"
+    assert set(names.values()) == {"build", "launch"}
+    design = open(os.path.join(ROOT, "DESIGN.md")).read()
+    for n in names:
+        assert n in design, f"option {n} undocumented in DESIGN.md"
+    with pytest.raises(_lib.InvalidArgument):
+        _lib.check(_lib.lib().pf_option_names(C.create_string_buffer(8), 8))

@@ -25,12 +25,11 @@ def exact(a, b):
 @pytest.mark.parametrize("K,L", [(2, 4), (4, 4), (8, 4), (3, 3)])
 @pytest.mark.parametrize("kind", [gmg.PF_SMOOTHER_GAUSS_SEIDEL, gmg.PF_SMOOTHER_MULTICOLOR_SOR], ids=["gs", "sor"])
 @pytest.mark.parametrize("bottom", ["0", "1024"], ids=["multilaunch", "bottom"])
-def test_colorwise_q1_bit_exact(cuda, monkeypatch, K, L, kind, bottom):
-    monkeypatch.setenv("PF_BOTTOM_ROWS", bottom)
+def test_colorwise_q1_bit_exact(cuda, K, L, kind, bottom):
     ss = [StructuredSetup(3, 2, L, K, r, _lib.PF_PROBLEM_LOGNORMAL, seed=7) for r in range(K)]
     lv = [s.levels for s in ss]
     c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 1.0, max_cycles=100)
-    h = gmg.Hierarchy(lv).set_colorwise_exchange()
+    h = gmg.Hierarchy(lv, options={"bottom_rows": int(bottom)}).set_colorwise_exchange()
     x = upload(h, L - 1, [s.x0 for s in ss])
     st = gmg.solve_outer(h, x, upload(h, L - 1, [s.b for s in ss]), c)
     xo, res, ost, rc = Oracle(lv, colorwise=True).solve_outer([s.x0 for s in ss], [s.b for s in ss], c)

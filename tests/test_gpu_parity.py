@@ -251,17 +251,15 @@ def test_multiprocess_path_loopback(cuda, K, L, kind, rep):
 @pytest.mark.parametrize("bottom_rows", ["0", "1024", "65536", "1000000"],
                          ids=["multilaunch", "bottom", "bottom-64k", "bottom-all"])
 @pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
-def test_bottom_kernel_equals_multilaunch(cuda, monkeypatch, bottom_rows, kind):
+def test_bottom_kernel_equals_multilaunch(cuda, bottom_rows, kind):
     """The cooperative bottom-of-cycle kernel is a launch-structure change only: with it
     disabled, covering the default levels, or covering every level below the finest, the
     solve must equal the oracle bit for bit (1 and 4 subdomains).  Jacobi is forced onto
-    it too (by default it runs per-level kernels)."""
-    monkeypatch.setenv("PF_BOTTOM_ROWS", bottom_rows)
-    monkeypatch.setenv("PF_BOTTOM_JACOBI", "1")
+    it too (by default it runs per-level kernels).  Per-hierarchy options."""
     c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
     for K in (1, 4):
         setups, levels = structured(3, 2, 5, K)
-        h = gmg.Hierarchy(levels)
+        h = gmg.Hierarchy(levels, options={"bottom_rows": int(bottom_rows), "bottom_jacobi": 1})
         x = upload(h, 4, [s.x0 for s in setups])
         st = gmg.solve_outer(h, x, upload(h, 4, [s.b for s in setups]), c)
         xo, res, ost, rc = Oracle(levels).solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
@@ -271,15 +269,14 @@ def test_bottom_kernel_equals_multilaunch(cuda, monkeypatch, bottom_rows, kind):
 
 @pytest.mark.parametrize("mode", ["host", "graph"])
 @pytest.mark.parametrize("kind", KINDS, ids=["jacobi", "gs", "sor"])
-def test_solve_drivers_agree(cuda, monkeypatch, mode, kind):
+def test_solve_drivers_agree(cuda, mode, kind):
     """solve_outer driven from the host (one graph per outer cycle + host convergence
     test) and as one device-driven graph (WHILE/IF conditional nodes, the Jacobi norm
     fused into the next cycle's first sweep) give the oracle's iterate and cycle count."""
-    monkeypatch.setenv("PF_SOLVE_MODE", mode)
     c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
     for K in (1, 2):
         setups, levels = structured(3, 2, 4, K)
-        h = gmg.Hierarchy(levels)
+        h = gmg.Hierarchy(levels, options={"solve_mode_host": int(mode == "host")})
         x = upload(h, 3, [s.x0 for s in setups])
         st = gmg.solve_outer(h, x, upload(h, 3, [s.b for s in setups]), c)
         xo, res, ost, rc = Oracle(levels).solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
@@ -442,13 +439,12 @@ def test_hierarchy_from_native_setups(cuda):
 
 
 @pytest.mark.parametrize("mode", ["graph", "host"])
-def test_graph_cache_keys_every_config_bit(cuda, monkeypatch, mode):
+def test_graph_cache_keys_every_config_bit(cuda, mode):
     """The cached solve graph is keyed by the exact bits of every config double: a second
     solve on the same vectors with a tighter outer_tol (or a damping that prints the same
     to 6 digits) must not replay the first graph."""
-    monkeypatch.setenv("PF_SOLVE_MODE", mode)
     setups, levels = structured(3, 2, 4, 1)
-    h = gmg.Hierarchy(levels)
+    h = gmg.Hierarchy(levels, options={"solve_mode_host": int(mode == "host")})
     x = h.vector(3)
     b = upload(h, 3, [setups[0].b])
     o = Oracle(levels)
@@ -478,3 +474,34 @@ def test_destroyed_vector_graphs_are_dropped(cuda):
         x.close()
         b.close()
         assert h.graph_count() <= 1
+
+
+def test_options_are_per_hierarchy(cuda):
+    """Tuning options live on the hierarchy: two hierarchies of one process with opposite
+    settings of every launch-structure option both reproduce the oracle bit for bit; a
+    launch option changed between solves drops the cached graphs and the next solve is
+    again bit-exact; a build option after finalize and an unknown name are refused."""
+    setups, levels = structured(3, 2, 5, 1)
+    o = Oracle(levels)
+    alt = {"bottom_rows": 0, "vtab_smem": 0, "value_index_min": 1 << 30, "fused_rr_rows": 0, "wide_max_rows": 0,
+           "bottom_stage": 0, "pdl": 0}
+    for kind in KINDS:
+        c = cfg(kind, damping=1.2 if kind == gmg.PF_SMOOTHER_MULTICOLOR_SOR else 0.8)
+        xo, res, ost, rc = o.solve_outer([s.x0 for s in setups], [s.b for s in setups], c)
+        for opts in ({}, alt):
+            h = gmg.Hierarchy(levels, options=opts)
+            for k, v in opts.items():
+                assert h.get_option(k) == v
+            x = upload(h, 4, [setups[0].x0])
+            b = upload(h, 4, [setups[0].b])
+            st = gmg.solve_outer(h, x, b, c)
+            assert st.iterations == ost.iterations and exact(download(h, x, 1), xo)
+            h.set_option("wide_max_rows", 0 if h.get_option("wide_max_rows") != 0 else -1)
+            h.set_option("solve_mode_host", 1)
+            x.upload(setups[0].x0)
+            st = gmg.solve_outer(h, x, b, c)
+            assert st.iterations == ost.iterations and exact(download(h, x, 1), xo)
+            with pytest.raises(_lib.PfError):
+                h.set_option("value_index", 0)  # build option after finalize
+            with pytest.raises(_lib.InvalidArgument):
+                h.set_option("no_such_option", 1)

@@ -4,7 +4,8 @@ At the default settings every operator whose values allow it is index-encoded (8
 16-bit value indices, table in shared memory), the coarser levels that fit L2 are read
 with the caching load policy and the finest with evict-first loads + row prefetch, and
 the bottom kernel reads decoded fp64 copies.  Here the parity suite is re-run in a
-subprocess (the settings are read once per process) under the other storage / load-policy
+subprocess whose PF_* environment sets those options on every hierarchy it creates
+(pf_hierarchy_set_option) under the other storage / load-policy
 combinations, so every kernel variant is compared with the oracle bit for bit on the
 same cases.
 """
@@ -44,17 +45,38 @@ VARIANTS = {
     "bottom_staged_cooperative_wide_all": {"PF_BOTTOM_BLOCK_KERNEL": "0", "PF_WIDE_MAX_ROWS": "100000000",
                                            "PF_BOTTOM_JACOBI": "1"},
     "bottom_block_kernel_jacobi": {"PF_BOTTOM_JACOBI": "1"},
+    # memory checking: a 4 KB 0xFF guard zone after every device buffer (a read past an
+    # array feeds NaN / -1 into the bit-exact comparisons; a write past one is reported
+    # when the buffer is freed)
+    "guard_zones": {"PF_GUARD": "1", "_files": "test_gpu_parity.py test_gpu_fe.py test_gpu_colorwise.py "
+                    "test_gpu_heat.py test_gpu_assembly.py test_gpu_golden.py test_gpu_peer.py"},
 }
 
 
 @pytest.mark.parametrize("name", sorted(VARIANTS))
 def test_parity_suite_under_variant(cuda, name):
     env = dict(os.environ)
-    env.update(VARIANTS[name])
-    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-           os.path.join(HERE, "test_gpu_parity.py"), os.path.join(HERE, "test_gpu_fe.py"),
-           os.path.join(HERE, "test_gpu_colorwise.py"), "-k", "bit_exact or solve or lognormal or colorwise"]
+    v = dict(VARIANTS[name])
+    files = v.pop("_files", None)
+    env.update(v)
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider"]
+    if files:  # a whole-suite variant
+        cmd += [os.path.join(HERE, f) for f in files.split()]
+    else:
+        cmd += [os.path.join(HERE, "test_gpu_parity.py"), os.path.join(HERE, "test_gpu_fe.py"),
+                os.path.join(HERE, "test_gpu_colorwise.py"), "-k", "bit_exact or solve or lognormal or colorwise"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     tail = "\n".join((r.stdout + r.stderr).splitlines()[-25:])
     assert r.returncode == 0, f"{name}:\n{tail}"
     assert " passed" in r.stdout, tail
+    assert "[pf guard]" not in r.stdout + r.stderr, f"{name}: a kernel wrote past a device buffer"
+
+
+def test_guard_zone_catches_a_planted_overrun(cuda):
+    """The guard-zone check itself: one element written past a guarded buffer is caught."""
+    import ctypes as C
+
+    from paper_1609_04809_b200 import _lib
+    det = C.c_int(0)
+    _lib.check(_lib.lib().pf_debug_guard_selftest(0, C.byref(det)))
+    assert det.value == 1
