@@ -185,6 +185,15 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def share_host_cores():
+    """One process per GPU on a shared host: give this rank its share of the cores for the
+    library's OpenMP setup / upload work (torchrun sets OMP_NUM_THREADS=1 for every rank,
+    which makes the 512^3 box setup several times slower)."""
+    from paper_1609_04809_b200 import gmg
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+    return gmg.set_host_threads(max(1, (os.cpu_count() or 1) // max(1, local_world)))
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -203,6 +212,7 @@ def run_b200(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")  # host plumbing only: the data plane is libpf_gpu.so's
+        share_host_cores()
 
     W = WORKLOAD
     t0 = time.time()
@@ -658,6 +668,7 @@ def run_c5(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")  # host plumbing only: the data plane is libpf_gpu.so's
+    host_threads = share_host_cores()
     h, setup, setup_s, upload_s, used = c5_hierarchy(world, rank, local, args.transport, dist)
     m = c5_solve(h, setup, world, rank, args, clk, dist, local, "c5")
     clk.stop()
@@ -695,7 +706,7 @@ def run_c5(args):
             "cpu_baseline_note": "the reference CPU solver cannot hold 512^3 (57 s and 4.2 GB at 128^3; "
                                  "SURVEY.md 8d): not run",
             "e2e": m["e2e"], "gpu_launches": m["launches"], "clocks": clocks,
-            "setup_seconds": setup_s, "upload_seconds": upload_s,
+            "setup_seconds": setup_s, "upload_seconds": upload_s, "host_threads_per_rank": host_threads,
         }
         print(json.dumps(line), flush=True)
     h.close()

@@ -54,6 +54,11 @@ const char* pf_last_error(void);
 const char* pf_version(void);
 /* Number of CUDA devices visible to this process. */
 pf_status pf_device_count(int* out);
+/* Host threads of the library's OpenMP work (the product setup, the device-layout build):
+ * n > 0 threads, n <= 0 every processor; *out (optional) = the count now in effect.  One
+ * process per GPU on a shared host divides the cores (launchers such as torchrun default
+ * the OpenMP thread count to 1). */
+pf_status pf_set_host_threads(int n, int* out);
 
 /* ---------------------------------------------------------------- enums -- */
 

@@ -124,7 +124,7 @@ class SolveStats(C.Structure):
 
 # Every symbol include/pf_gpu.h and include/pf_setup.h declare (checked by the CPU tests).
 EXPORTS = [
-    "pf_last_error", "pf_version", "pf_device_count", "pf_default_smoother_config", "pf_default_multigrid_config",
+    "pf_last_error", "pf_version", "pf_device_count", "pf_set_host_threads", "pf_default_smoother_config", "pf_default_multigrid_config",
     "pf_hierarchy_create", "pf_hierarchy_set_level", "pf_hierarchy_finalize", "pf_nccl_unique_id",
     "pf_hierarchy_init_nccl", "pf_nccl_selftest", "pf_hierarchy_set_fused_exchanges", "pf_hierarchy_set_colorwise_exchange", "pf_hierarchy_set_coarse_direct", "pf_hierarchy_set_option", "pf_hierarchy_get_option", "pf_option_names", "pf_debug_guard_failures", "pf_debug_guard_selftest", "pf_hierarchy_set_coarse_replica", "pf_hierarchy_set_replica_level",
     "pf_hierarchy_destroy",
@@ -185,6 +185,7 @@ def lib():
         "pf_hierarchy_set_coarse_direct": [P, C.c_int],
         "pf_hierarchy_set_option": [P, C.c_char_p, C.c_int64],
         "pf_hierarchy_get_option": [P, C.c_char_p, C.POINTER(C.c_int64)],
+        "pf_set_host_threads": [C.c_int, C.POINTER(C.c_int)],
         "pf_option_names": [C.c_char_p, C.c_int64],
         "pf_debug_guard_failures": [C.POINTER(C.c_int64)],
         "pf_debug_guard_selftest": [C.c_int, C.POINTER(C.c_int)],

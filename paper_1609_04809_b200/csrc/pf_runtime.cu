@@ -1206,6 +1206,13 @@ const char* pf_version(void) {
   return "paper_1609_04809_b200 pf_gpu 0.1 (sm_100a, SELL-32 fp64)";
 }
 
+pf_status pf_set_host_threads(int n, int* out) {
+  PF_API_BEGIN
+  omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+  if (out) *out = omp_get_max_threads();
+  PF_API_END
+}
+
 pf_status pf_device_count(int* out) {
   PF_API_BEGIN
   if (!out) invalid("null output");

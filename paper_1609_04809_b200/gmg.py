@@ -351,6 +351,13 @@ class Hierarchy:
 
 # ---------------------------------------------------------------- reference API --
 
+def set_host_threads(n: int) -> int:
+    """pf_set_host_threads: the library's OpenMP host threads (n <= 0: every processor)."""
+    out = C.c_int(0)
+    _lib.check(_lib.lib().pf_set_host_threads(int(n), C.byref(out)))
+    return out.value
+
+
 def option_names() -> dict:
     """Every tuning option: {name: "build" | "launch"} (pf_option_names; no GPU needed)."""
     buf = C.create_string_buffer(4096)
