@@ -541,8 +541,16 @@ void enq_prolong(pf_hierarchy* h, int fine, const double* xc, double* xf, int ad
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = F.sub[s];
     vk_dispatch_rows(D.P, [&](auto V) {
-      launch(grid_for(D.n), kBlock, k_prolong_add<decltype(V)::value>, view(D.P), xc + Cl.sub[s].offset,
-             xf + D.offset, D.n, add);
+      constexpr int vk = decltype(V)::value;
+      // trilinear P (<= 8 entries per row, 8-bit weights): k_prolong_add8 (prolongation
+      // 31.7 -> 29.7 us at C2's finest level)
+      if constexpr (vk_kind<vk>() == 1 || vk_kind<vk>() == kVKSmem) {
+        if (D.P.max_len <= 8) {
+          launch(grid_for(D.n), kBlock, k_prolong_add8<vk>, view(D.P), xc + Cl.sub[s].offset, xf + D.offset, D.n, add);
+          return;
+        }
+      }
+      launch(grid_for(D.n), kBlock, k_prolong_add<vk>, view(D.P), xc + Cl.sub[s].offset, xf + D.offset, D.n, add);
     });
   }
 }
@@ -582,7 +590,8 @@ void enq_restrict(pf_hierarchy* h, int fine, const double* rf, double* bc, doubl
     DevLevel& D = F.sub[s];
     DevLevel& DC = Cl.sub[s];
     vk_dispatch_rows(D.R, [&](auto V) {
-      launch(grid_for(DC.n), kBlock, k_restrict<decltype(V)::value>, view(D.R), rf + D.offset, bc + DC.offset,
+      constexpr int vk = decltype(V)::value;
+      launch(grid_for(DC.n), kBlock, k_restrict<vk>, view(D.R), rf + D.offset, bc + DC.offset,
              xc ? xc + DC.offset : nullptr, static_cast<const uint8_t*>(DC.d_is_dir.p), DC.n, zero_dir);
     });
   }
