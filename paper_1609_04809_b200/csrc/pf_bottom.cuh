@@ -455,8 +455,12 @@ static __global__ void __launch_bounds__(kBlock, 1) k_bottom(const BotDesc* __re
 // code (no grid-team paths), launched as an ordinary PDL-chained kernel of one block.  The
 // descriptor and the staged operators are copied before griddepcontrol.wait (immutable),
 // the top level's b and x after it.
+#ifndef PF_BOT_BLOCK_THREADS
+#define PF_BOT_BLOCK_THREADS 256
+#endif
+constexpr int kBotBlockThreads = PF_BOT_BLOCK_THREADS;
 template <int kKind>
-__global__ void __launch_bounds__(kBlock, 1) k_bottom_block(const BotDesc* __restrict__ Dp, BotCfg c,
+__global__ void __launch_bounds__(kBotBlockThreads, 1) k_bottom_block(const BotDesc* __restrict__ Dp, BotCfg c,
                                                             int accumulate_top) {
   extern __shared__ __align__(16) unsigned char smem_b[];
   {

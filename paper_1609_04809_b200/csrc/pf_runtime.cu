@@ -722,9 +722,9 @@ void enq_bottom(pf_hierarchy* h, const pf_hierarchy::Bottom& bot, const pf_multi
     auto launch = launcher(h);
     const BotDesc* d = static_cast<const BotDesc*>(bot.desc);
     switch (cfg.smoother.kind) {
-      case PF_SMOOTHER_JACOBI: launch.with_smem(bot.smem)(1, kBlock, k_bottom_block<0>, d, c, accumulate_top); break;
-      case PF_SMOOTHER_MULTICOLOR_SOR: launch.with_smem(bot.smem)(1, kBlock, k_bottom_block<2>, d, c, accumulate_top); break;
-      default: launch.with_smem(bot.smem)(1, kBlock, k_bottom_block<1>, d, c, accumulate_top); break;
+      case PF_SMOOTHER_JACOBI: launch.with_smem(bot.smem)(1, kBotBlockThreads, k_bottom_block<0>, d, c, accumulate_top); break;
+      case PF_SMOOTHER_MULTICOLOR_SOR: launch.with_smem(bot.smem)(1, kBotBlockThreads, k_bottom_block<2>, d, c, accumulate_top); break;
+      default: launch.with_smem(bot.smem)(1, kBotBlockThreads, k_bottom_block<1>, d, c, accumulate_top); break;
     }
     return;
   }
