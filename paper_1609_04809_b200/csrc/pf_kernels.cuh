@@ -570,6 +570,73 @@ __global__ void __launch_bounds__(kSplitBlock) k_color_sweep_split(SellView A, d
     x[row] = __ddiv_rn(acc, diag);
 }
 
+// The slice-split form of the damped-Jacobi sweep (kJacobi) and of the cycle residual for
+// long rows on small levels (Q2: up to 125 entries), where one thread per row walks a
+// 32-group dependent chain: warp w of the slice's block forms the products of groups w,
+// w + 8, ... into shared memory, then lane r of warp 0 sums row r's products in stored
+// order — Jacobi: b_r minus the off-diagonal products, as k_jacobi; residual: the spmv sum
+// from 0 over every entry, r = b - sum, as k_residual.  Rows [0, n); Jacobi carries the
+// non-own rows over.
+template <bool kJacobi, int kVK>
+__global__ void __launch_bounds__(kSplitBlock) k_rows_split(SellView A, const double* __restrict__ x,
+                                                           double* __restrict__ out, const double* __restrict__ b,
+                                                           int32_t n_own, int32_t n, double omega) {
+  extern __shared__ double prod[];  // [width][32]
+  __shared__ double sdiag[32];
+  __shared__ int32_t sdpos[32];
+  vtab_stage<kVK>(A);
+  PF_PDL_ENTRY();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t slice = static_cast<int32_t>(blockIdx.x);
+  const int32_t row = slice * 32 + lane;
+  const bool active = row < n && (!kJacobi || row < n_own);
+  const int len = active ? A.row_len[row] : 0;
+  if (w == 0) {
+    sdpos[lane] = -1;
+    sdiag[lane] = 0.0;
+  }
+  __syncthreads();
+  const int64_t base = A.slice_ptr[slice] + 4 * lane;
+  for (int g = w; 4 * g < len; g += kSplitBlock / 32) {
+    int32_t c[4];
+    double v[4];
+    sell_group<kVK>(A, base + 128 * static_cast<int64_t>(g), c, v);
+    double xv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) xv[k] = (4 * g + k < len && (!kJacobi || c[k] != row)) ? __ldg(x + c[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = 4 * g + k;
+      if (j < len) {
+        if (kJacobi && c[k] == row) {
+          sdpos[lane] = j;
+          sdiag[lane] = v[k];
+        } else {
+          prod[j * 32 + lane] = __dmul_rn(v[k], xv[k]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (w != 0 || row >= n) return;
+  if (kJacobi) {
+    const double xo = x[row];
+    if (row >= n_own) {
+      out[row] = xo;
+      return;
+    }
+    const int dp = sdpos[lane];
+    double acc = b[row];
+    for (int j = 0; j < len; ++j)
+      if (j != dp) acc = __dsub_rn(acc, prod[j * 32 + lane]);
+    out[row] = __dadd_rn(__dmul_rn(1.0 - omega, xo), __ddiv_rn(__dmul_rn(omega, acc), sdiag[lane]));
+  } else {
+    double acc = 0.0;
+    for (int j = 0; j < len; ++j) acc = __dadd_rn(acc, prod[j * 32 + lane]);
+    out[row] = __dsub_rn(b[row], acc);
+  }
+}
+
 // "Wide" rows for launches that fit one wave (the mid-size levels of a cycle, where a
 // launch is bound by the latency chain of one row, not by throughput): the whole row's
 // operator — every group of 4 columns and its 8-bit value indices — is loaded into

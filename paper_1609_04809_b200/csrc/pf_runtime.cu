@@ -132,6 +132,7 @@ const OptionSpec kOptions[] = {
     {"bottom_block_kernel", "PF_BOTTOM_BLOCK_KERNEL", &Options::bottom_block_kernel, false},
     {"split_row_len", "PF_SPLIT_ROW_LEN", &Options::split_row_len, false},
     {"split_max_rows", "PF_SPLIT_MAX_ROWS", &Options::split_max_rows, false},
+    {"split_rows_max", "PF_SPLIT_ROWS_MAX", &Options::split_rows_max, false},
     {"wide_max_rows", "PF_WIDE_MAX_ROWS", &Options::wide_max_rows, false},
     {"fused_rr_rows", "PF_FUSED_RR_ROWS", &Options::fused_rr_rows, false},
     {"sor_tma", "PF_SOR_TMA", &Options::sor_tma, false},
@@ -279,9 +280,39 @@ void enq_resnorm(pf_hierarchy* h, int l, const double* x, const double* b) {
   if (!single) enq_allreduce(h, L, true);
 }
 
+// Long rows (longer than Options::split_row_len) on levels of at most
+// Options::split_rows_max rows take the slice-split Jacobi / residual (k_rows_split).
+bool rows_split_ok(const pf_hierarchy* h, const DevLevel& D) {
+  return h->opt.split_row_len > 0 && D.A.max_len > h->opt.split_row_len && D.n <= h->opt.split_rows_max;
+}
+template <bool kJacobi>
+void enq_rows_split(pf_hierarchy* h, DevLevel& D, const double* x, double* out, const double* b, double omega) {
+  const int32_t width = (D.A.max_len + 3) / 4 * 4;
+  const size_t smem = sizeof(double) * kSlice * static_cast<size_t>(width);
+  auto launch = launcher(h);
+  vk_dispatch_rows(D.A, [&](auto V) {
+    constexpr int vk = decltype(V)::value;
+    auto kern = k_rows_split<kJacobi, vk>;
+    static thread_local std::map<const void*, size_t> attr_set;
+    auto& have = attr_set[reinterpret_cast<const void*>(kern)];
+    if (smem > 48 * 1024 && have < smem) {
+      PF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      have = smem;
+    }
+    const unsigned grid = static_cast<unsigned>((static_cast<int64_t>(D.n) + kSlice - 1) / kSlice);
+    launch.with_smem(smem)(grid, kSplitBlock, kern, view(D.A), x, out, b, D.n_own, D.n, omega);
+  });
+}
+
 void enq_residual(pf_hierarchy* h, int l, const double* x, const double* b, double* r) {
   Level& L = h->levels[l];
   auto launch = launcher(h);
+  bool split = true;
+  for (DevLevel& D : L.sub) split = split && rows_split_ok(h, D);
+  if (split) {
+    for (DevLevel& D : L.sub) enq_rows_split<false>(h, D, x + D.offset, r + D.offset, b + D.offset, 0.0);
+    return;
+  }
   for (DevLevel& D : L.sub)
     vk_dispatch_rows(D.A, [&](auto V) {
       launch(D.rmap_grid, kBlock, k_residual<decltype(V)::value>, view(D.A), x + D.offset, b + D.offset, r + D.offset, D.n,
@@ -319,6 +350,10 @@ bool wide_ok(const pf_hierarchy* h, const DevLevel& D, int64_t rows) {
 
 // One damped-Jacobi sweep of subdomain level D, src -> dst.
 void enq_jacobi_sweep(pf_hierarchy* h, DevLevel& D, const double* src, double* dst, const double* b, double omega) {
+  if (rows_split_ok(h, D)) {
+    enq_rows_split<true>(h, D, src, dst, b, omega);
+    return;
+  }
   auto launch = launcher(h);
   vk_dispatch_rows(D.A, [&](auto V) {
     constexpr int vk = decltype(V)::value;

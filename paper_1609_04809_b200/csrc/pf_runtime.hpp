@@ -267,6 +267,7 @@ struct Options {
   int64_t bottom_block_kernel = 1;    // fully staged bottom as the one-block kernel
   int64_t split_row_len = 48;         // slice-split colour sweep for rows longer than this
   int64_t split_max_rows = int64_t(1) << 20;  // ... on levels up to this many own rows
+  int64_t split_rows_max = 65536;     // slice-split Jacobi / residual for long rows up to this many rows
   int64_t wide_max_rows = -1;         // wide-row kernels for launches up to this many rows (-1: one wave)
   int64_t fused_rr_rows = 8192;       // residual + restriction in one launch up to this many rows
   int64_t sor_tma = 0, sor_tma_min_rows = 65536, sor_tma_bps = 2, sor_tma_cfg = 0;  // opt-in TMA colour sweep
