@@ -38,8 +38,9 @@ VARIANTS = {
     # level with 2-8 colours (default: only where x exceeds 64 MB)
     "interleave_everywhere": {"PF_INTERLEAVE_MIN_BYTES": "0"},
     # the bottom levels unstaged (operators and vectors in global memory) in the cooperative
-    # kernel, and no wide-row kernels (every mid-size launch takes the group-pipelined rows)
-    "bottom_unstaged_no_wide": {"PF_BOTTOM_STAGE": "0", "PF_WIDE_MAX_ROWS": "0"},
+    # kernel, no wide-row kernels (every mid-size launch takes the group-pipelined rows) and
+    # no slice-split Jacobi / residual for the long (Q2) rows
+    "bottom_unstaged_no_wide": {"PF_BOTTOM_STAGE": "0", "PF_WIDE_MAX_ROWS": "0", "PF_SPLIT_ROWS_MAX": "0"},
     # staged bottom levels inside the cooperative kernel (not the one-block kernel), wide
     # rows on every launch that fits them, damped Jacobi through the bottom kernel too
     "bottom_staged_cooperative_wide_all": {"PF_BOTTOM_BLOCK_KERNEL": "0", "PF_WIDE_MAX_ROWS": "100000000",
