@@ -1247,7 +1247,7 @@ extern "C" {
 const char* pf_last_error(void) { return pf::g_last_error.c_str(); }
 
 const char* pf_version(void) {
-  return "paper_1609_04809_b200 pf_gpu 0.1 (sm_100a, SELL-32 fp64)";
+  return "paper_1609_04809_b200 pf_gpu 0.2 (sm_100a; SELL-32x4 fp64 operators, 8/16-bit lossless value index)";
 }
 
 pf_status pf_set_host_threads(int n, int* out) {
