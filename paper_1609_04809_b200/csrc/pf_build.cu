@@ -168,7 +168,7 @@ void sell_from_rows(int32_t n, const std::vector<int64_t>& off, const std::vecto
 void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector<int32_t>& perm,
                    const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
                    const std::vector<double>& vals, DevSell& out,
-                   const Options& o) {
+                   const Options& o, std::vector<int32_t>* keep_cols = nullptr) {
   const int64_t n_slices = (n + kSlice - 1) / kSlice;
   std::vector<int64_t> sptr(static_cast<size_t>(n_slices) + 1, 0);
   std::vector<int32_t> rlen(static_cast<size_t>(std::max<int64_t>(n_slices, 1) * kSlice), 0);
@@ -189,6 +189,7 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
       for (int j = 0; j < rlen[d]; ++j) sc[static_cast<size_t>(sell_entry(base, j))] = perm[cols[static_cast<size_t>(k0 + j)]];
     }
     out.cols.upload(sc);
+    if (keep_cols) keep_cols->swap(sc);
   }
   {
     std::vector<double> sv(static_cast<size_t>(sptr[n_slices]), 0.0);
@@ -205,6 +206,107 @@ void sell_from_csr(int32_t n, const std::vector<int32_t>& inv, const std::vector
   out.max_len = rlen.empty() ? 0 : *std::max_element(rlen.begin(), rlen.end());
   out.nnz = n > 0 ? rowptr[n] : 0;
   out.stored = sptr[n_slices];
+}
+
+// Block windows of the own rows (WinView, pf_types.hpp; kernels in pf_window.cuh).  For
+// every block of kBlock device rows the off-diagonal columns its own rows read, ascending,
+// are covered greedily by chunks of 16 doubles starting at a multiple of 4 (a 32-byte
+// sector); the diagonal and padding entries of a row point at the row's private slot.  A
+// block whose cover exceeds Options::win_max_chunks (at most kWinChunksCap: the launches'
+// shared memory), or with a row holding several diagonal entries, keeps an empty cover and
+// its rows take the plain path inside the window kernels; a level keeps its windows when
+// at least 90 % of its blocks have one — the structured levels do (colour-major placement:
+// a block's neighbours are a few lattice lines of each other colour); an operator without
+// that locality keeps the plain kernels.
+void build_window(DevLevel& D, const std::vector<int32_t>& sc, const std::vector<int64_t>& sptr, int level,
+                  const Options& o) {
+  D.W = DevWin{};
+  const int32_t n = D.n, n_own = D.n_own;
+  if (!o.win || n_own < o.win_min_rows || D.rmap.n_col != 0 || D.A.max_len > 255) return;
+  const int64_t blocks = grid_for(n), own_blocks = grid_for(n_own);
+  std::vector<int32_t> rlen(static_cast<size_t>(n_own));
+  PF_CUDA(cudaMemcpy(rlen.data(), D.A.row_len.p, sizeof(int32_t) * rlen.size(), cudaMemcpyDeviceToHost));
+  std::vector<std::vector<int32_t>> cover(static_cast<size_t>(own_blocks));
+  std::vector<uint16_t> c16(sc.size(), 0);
+  std::vector<uint8_t> dpos(static_cast<size_t>(n_own), 0);
+  const int64_t cap = std::min<int64_t>(o.win_max_chunks, kWinChunksCap);
+  int64_t plain = 0;
+#pragma omp parallel
+  {
+    std::vector<int32_t> cs, slot;
+#pragma omp for schedule(dynamic, 16) reduction(+ : plain)
+    for (int64_t bk = 0; bk < own_blocks; ++bk) {
+      const int32_t r0 = static_cast<int32_t>(bk * kBlock), r1 = std::min<int64_t>(n_own, r0 + kBlock);
+      cs.clear();
+      bool ok = true;
+      for (int32_t r = r0; r < r1; ++r) {
+        const int64_t base = sell_row_base(sptr.data(), r);
+        int diags = 0;
+        for (int j = 0; j < rlen[r]; ++j) {
+          const int32_t c = sc[static_cast<size_t>(sell_entry(base, j))];
+          if (c == r) {
+            dpos[r] = static_cast<uint8_t>(j);
+            ++diags;
+          } else {
+            cs.push_back(c);
+          }
+        }
+        ok = ok && diags == 1;
+      }
+      std::sort(cs.begin(), cs.end());
+      cs.erase(std::unique(cs.begin(), cs.end()), cs.end());
+      std::vector<int32_t>& ch = cover[static_cast<size_t>(bk)];
+      slot.resize(cs.size());
+      int32_t start = -kWinChunk;
+      for (size_t i = 0; i < cs.size(); ++i) {
+        if (cs[i] >= start + kWinChunk) {
+          start = cs[i] & ~3;
+          ch.push_back(start);
+        }
+        slot[i] = kBlock + static_cast<int32_t>(ch.size() - 1) * kWinChunk + (cs[i] - start);
+      }
+      if (!ok || ch.empty() || static_cast<int64_t>(ch.size()) > cap) {  // this block takes the plain row path
+        ch.clear();
+        ++plain;
+        continue;
+      }
+      for (int32_t r = r0; r < r1; ++r) {
+        const int64_t base = sell_row_base(sptr.data(), r);
+        const int padded = (rlen[r] + kGroup - 1) / kGroup * kGroup;
+        for (int j = 0; j < padded; ++j) {
+          const size_t e = static_cast<size_t>(sell_entry(base, j));
+          const int32_t c = j < rlen[r] ? sc[e] : r;
+          const int32_t sl = c == r ? r - r0 : slot[std::lower_bound(cs.begin(), cs.end(), c) - cs.begin()];
+          c16[e] = static_cast<uint16_t>(sl * 8);
+        }
+      }
+    }
+  }
+  int64_t total = 0;
+  size_t most = 0;
+  for (const auto& ch : cover) {
+    total += static_cast<int64_t>(ch.size());
+    most = std::max(most, ch.size());
+  }
+  // windows pay when nearly every block has one
+  const bool keep = 10 * plain <= own_blocks && total <= INT32_MAX;
+  if (std::getenv("PF_TIMING"))
+    std::fprintf(stderr, "[pf_window] level %d: %lld row blocks, %lld without a window, chunks per block mean %.1f max %zu%s\n",
+                 level, static_cast<long long>(own_blocks), static_cast<long long>(plain),
+                 own_blocks > plain ? double(total) / (own_blocks - plain) : 0.0, most, keep ? "" : " (plain kernels)");
+  if (!keep) return;
+  std::vector<int32_t> ptr(static_cast<size_t>(blocks) + 1, 0), flat;
+  flat.reserve(static_cast<size_t>(total));
+  for (int64_t bk = 0; bk < blocks; ++bk) {
+    if (bk < own_blocks) flat.insert(flat.end(), cover[bk].begin(), cover[bk].end());
+    ptr[static_cast<size_t>(bk) + 1] = static_cast<int32_t>(flat.size());
+  }
+  D.W.cols16.upload(c16);
+  D.W.chunk_ptr.upload(ptr);
+  D.W.chunks.upload(flat);
+  D.W.dpos.upload(dpos);
+  D.W.max_chunks = static_cast<int32_t>(most);
+  D.W.on = true;
 }
 
 // Device layout of one subdomain level: own rows colour-major (stable in host order),
@@ -318,7 +420,9 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level, const Options& 
   // --- SELL-32x4 operator: rows in device order, columns mapped, entries in CSR order,
   // written straight from the host CSR (no intermediate re-layout: at 512^3 the finest
   // level alone is 44 GB of host CSR)
-  sell_from_csr(n, inv, D.perm, H.rowptr, H.cols, H.vals, D.A, o);
+  const bool want_win = o.win && n_own >= o.win_min_rows && D.rmap.n_col == 0;
+  std::vector<int32_t> dev_cols;
+  sell_from_csr(n, inv, D.perm, H.rowptr, H.cols, H.vals, D.A, o, want_win ? &dev_cols : nullptr);
   D.A.own_nnz = H.rowptr[n_own];
   tm("sell", level);
   D.csr_rowptr = H.rowptr;
@@ -326,6 +430,11 @@ void build_dev_level(const HostLevel& H, DevLevel& D, int level, const Options& 
   if (D.A.slice_ptr.n > 0)
     PF_CUDA(cudaMemcpy(D.sell_ptr.data(), D.A.slice_ptr.p, sizeof(int64_t) * D.sell_ptr.size(),
                        cudaMemcpyDeviceToHost));
+  if (want_win) {
+    build_window(D, dev_cols, D.sell_ptr, level, o);
+    std::vector<int32_t>().swap(dev_cols);
+    tm("windows", level);
+  }
   {
     std::vector<uint8_t> touched(static_cast<size_t>(n), 0);
     const int64_t z = H.rowptr[n_own];

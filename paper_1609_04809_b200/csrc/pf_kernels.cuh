@@ -131,13 +131,20 @@ __device__ __forceinline__ double sell_val(const SellView& A, int64_t e) {
 
 // One group of 4 stored entries (SELL-32x4) starting at e (e % 4 == 0): columns and values.
 template <int kVK>
+__device__ __forceinline__ void sell_group_vals(const SellView& A, int64_t e, double v[4]);
+template <int kVK>
 __device__ __forceinline__ void sell_group(const SellView& A, int64_t e, int32_t c[4], double v[4]) {
-  constexpr int K = vk_kind<kVK>();
   const int4 cc = ld_op<kVK>(reinterpret_cast<const int4*>(A.cols + e));
   c[0] = cc.x;
   c[1] = cc.y;
   c[2] = cc.z;
   c[3] = cc.w;
+  sell_group_vals<kVK>(A, e, v);
+}
+// The four values of the group starting at e.
+template <int kVK>
+__device__ __forceinline__ void sell_group_vals(const SellView& A, int64_t e, double v[4]) {
+  constexpr int K = vk_kind<kVK>();
   if constexpr (K == 1) {
     const unsigned int w = ld_op<kVK>(reinterpret_cast<const unsigned int*>(static_cast<const unsigned char*>(A.vidx) + e));
 #pragma unroll

@@ -35,6 +35,7 @@
 #include "pf_kernels.cuh"
 #include "pf_nccl.hpp"
 #include "pf_sweep_tma.cuh"
+#include "pf_window.cuh"
 #include "pf_internal.hpp"
 #include "pf_runtime.hpp"
 
@@ -139,6 +140,10 @@ const OptionSpec kOptions[] = {
     {"sor_tma_min_rows", "PF_SOR_TMA_MIN_ROWS", &Options::sor_tma_min_rows, false},
     {"sor_tma_bps", "PF_SOR_TMA_BPS", &Options::sor_tma_bps, false},
     {"sor_tma_cfg", "PF_SOR_TMA_CFG", &Options::sor_tma_cfg, false},
+    {"win", "PF_WIN", &Options::win, true},
+    {"win_min_rows", "PF_WIN_MIN_ROWS", &Options::win_min_rows, true},
+    {"win_max_chunks", "PF_WIN_MAX_CHUNKS", &Options::win_max_chunks, true},
+    {"win_kernels", "PF_WIN_KERNELS", &Options::win_kernels, false},
     {"pdl", "PF_PDL", &Options::pdl, false},
     {"solve_mode_host", nullptr, &Options::solve_mode_host, false},  // env: PF_SOLVE_MODE=host
 };
@@ -266,6 +271,21 @@ void enq_allreduce(pf_hierarchy* h, Level& L, bool take_sqrt) {
   }
 }
 
+// Block-window kernels (pf_window.cuh) for the levels that have windows (DevWin).
+bool win_on(const pf_hierarchy* h, const DevLevel& D) { return D.W.on && h->opt.win_kernels != 0; }
+WinView win_view(const DevLevel& D) { return WinView{D.W.cols16.p, D.W.chunk_ptr.p, D.W.chunks.p, D.W.dpos.p}; }
+template <typename K>
+size_t win_smem(K kern, const DevLevel& D) {  // the launch's dynamic shared memory, cap raised once
+  const size_t smem = D.W.smem();
+  static thread_local std::map<const void*, size_t> attr_set;
+  auto& have = attr_set[reinterpret_cast<const void*>(kern)];
+  if (smem > 48 * 1024 && have < smem) {
+    PF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    have = smem;
+  }
+  return smem;
+}
+
 void enq_resnorm(pf_hierarchy* h, int l, const double* x, const double* b) {
   Level& L = h->levels[l];
   auto launch = launcher(h);
@@ -273,6 +293,14 @@ void enq_resnorm(pf_hierarchy* h, int l, const double* x, const double* b) {
   for (int s = 0; s < h->n_sub; ++s) {
     DevLevel& D = L.sub[s];
     vk_dispatch_rows(D.A, [&](auto V) {
+    constexpr int vk = decltype(V)::value;
+    if (win_on(h, D)) {
+      auto kern = k_resnorm_win<vk>;
+      launch.with_smem(win_smem(kern, D))(static_cast<unsigned>(D.resnorm_blocks), kBlock, kern, view(D.A),
+                                          win_view(D), x + D.offset, b + D.offset, D.n_own, D.n, D.partials.p,
+                                          D.ticket.p, L.sumsq.p + s, single ? L.norm.p : nullptr);
+      return;
+    }
     launch(static_cast<unsigned>(D.resnorm_blocks), kBlock, k_resnorm<decltype(V)::value>, view(D.A), x + D.offset,
            b + D.offset, D.n_own, D.partials.p, D.ticket.p, L.sumsq.p + s, single ? L.norm.p : nullptr);
     });
@@ -315,6 +343,13 @@ void enq_residual(pf_hierarchy* h, int l, const double* x, const double* b, doub
   }
   for (DevLevel& D : L.sub)
     vk_dispatch_rows(D.A, [&](auto V) {
+      constexpr int vk = decltype(V)::value;
+      if (win_on(h, D)) {
+        auto kern = k_residual_win<vk>;
+        launch.with_smem(win_smem(kern, D))(grid_for(D.n), kBlock, kern, view(D.A), win_view(D), x + D.offset,
+                                            b + D.offset, r + D.offset, D.n, D.n_own);
+        return;
+      }
       launch(D.rmap_grid, kBlock, k_residual<decltype(V)::value>, view(D.A), x + D.offset, b + D.offset, r + D.offset, D.n,
              D.n_own, D.rmap);
     });
@@ -357,6 +392,12 @@ void enq_jacobi_sweep(pf_hierarchy* h, DevLevel& D, const double* src, double* d
   auto launch = launcher(h);
   vk_dispatch_rows(D.A, [&](auto V) {
     constexpr int vk = decltype(V)::value;
+    if (win_on(h, D)) {
+      auto kern = k_jacobi_win<vk>;
+      launch.with_smem(win_smem(kern, D))(grid_for(D.n), kBlock, kern, view(D.A), win_view(D), src, dst, b, D.n_own,
+                                          D.n, omega);
+      return;
+    }
     if constexpr (vk_kind<vk>() == 1 || vk_kind<vk>() == kVKSmem) {
       if (D.rmap.n_col == 0 && wide_ok<vk>(h, D, D.n)) {
         launch(grid_for(D.n), kBlock, k_jacobi_wide<vk, kWideGroups>, view(D.A), src, dst, b, D.n_own, D.n, omega);
@@ -407,6 +448,19 @@ void enq_color_sweep(pf_hierarchy* h, DevLevel& D, int c, bool sor, double omega
         case 1: go(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}); break;
         case 2: go(std::integral_constant<int, 8>{}, std::integral_constant<int, 3>{}); break;
         default: go(std::integral_constant<int, 8>{}, std::integral_constant<int, 2>{}); break;
+      }
+      return;
+    }
+    if (win_on(h, D) && h->opt.win_kernels >= 2) {
+      const int32_t b0 = r0 / kBlock, b1 = (r1 - 1) / kBlock + 1;
+      if (sor) {
+        auto kern = k_color_sweep_win<true, vk>;
+        launch.with_smem(win_smem(kern, D))(static_cast<unsigned>(b1 - b0), kBlock, kern, view(D.A), win_view(D), x, b,
+                                            b0, r0, r1, D.n, omega);
+      } else {
+        auto kern = k_color_sweep_win<false, vk>;
+        launch.with_smem(win_smem(kern, D))(static_cast<unsigned>(b1 - b0), kBlock, kern, view(D.A), win_view(D), x, b,
+                                            b0, r0, r1, D.n, 1.0);
       }
       return;
     }
@@ -852,6 +906,22 @@ void enq_norm_head(pf_hierarchy* h, pf_vector* x, const double* b, const pf_mult
     DevLevel& D = L.sub[s];
     vk_dispatch_rows(D.A, [&](auto V) {
       constexpr int vk = decltype(V)::value;
+      if (win_on(h, D)) {
+        if (fused_head(cfg)) {
+          auto kern = k_jacobi_norm_win<vk>;
+          launch.with_smem(win_smem(kern, D))(grid_for(D.n), kBlock, kern, view(D.A), win_view(D),
+                                              static_cast<const double*>(x->cur() + D.offset), x->alt() + D.offset,
+                                              b + D.offset, D.n_own, D.n, cfg.smoother.damping, D.partials.p,
+                                              D.ticket.p, L.sumsq.p + s);
+        } else {
+          auto kern = k_resnorm_win<vk>;
+          launch.with_smem(win_smem(kern, D))(static_cast<unsigned>(D.resnorm_blocks), kBlock, kern, view(D.A),
+                                              win_view(D), static_cast<const double*>(x->cur() + D.offset),
+                                              b + D.offset, D.n_own, D.n, D.partials.p, D.ticket.p, L.sumsq.p + s,
+                                              static_cast<double*>(nullptr));
+        }
+        return;
+      }
       if (fused_head(cfg))
         launch(grid_for(D.n), kBlock, k_jacobi_norm<vk>, view(D.A), static_cast<const double*>(x->cur() + D.offset),
                x->alt() + D.offset, b + D.offset, D.n_own, D.n, cfg.smoother.damping, D.partials.p,

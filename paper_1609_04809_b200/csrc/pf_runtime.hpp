@@ -121,6 +121,16 @@ struct DevSell {
   bool smem_table = true;  // an 8-bit table is staged in shared memory by the row kernels (Options::vtab_smem)
 };
 
+// Block windows of a level operator (WinView, pf_types.hpp).
+struct DevWin {
+  bool on = false;
+  DevBuf<uint16_t> cols16;
+  DevBuf<int32_t> chunk_ptr, chunks;
+  DevBuf<uint8_t> dpos;
+  int32_t max_chunks = 0;  // largest block cover: the launches' dynamic shared memory
+  size_t smem() const { return sizeof(double) * (kBlock + kWinChunk * static_cast<size_t>(max_chunks)); }
+};
+
 // One subdomain of one level on the device.
 struct DevLevel {
   int32_t n = 0, n_own = 0;
@@ -132,6 +142,7 @@ struct DevLevel {
   std::vector<int32_t> perm;         // host index -> device index
   DevBuf<int32_t> d_perm;
   DevSell A;
+  DevWin W;  // block windows of A's own rows (Options::win)
   // host copies to place further value sets on A's pattern (pf_operator_set_values)
   std::vector<int64_t> csr_rowptr;   // the level desc's row offsets (host order)
   std::vector<int64_t> sell_ptr;     // A.slice_ptr
@@ -271,6 +282,13 @@ struct Options {
   int64_t wide_max_rows = -1;         // wide-row kernels for launches up to this many rows (-1: one wave)
   int64_t fused_rr_rows = 8192;       // residual + restriction in one launch up to this many rows
   int64_t sor_tma = 0, sor_tma_min_rows = 65536, sor_tma_bps = 2, sor_tma_cfg = 0;  // opt-in TMA colour sweep
+  // opt-in (measured slower, profiles/r02_sweep_experiments.md): block windows (pf_window.cuh)
+  // for the own rows of levels with at least win_min_rows rows; a block's cover fits
+  // win_max_chunks chunks of 16 doubles or the block takes the plain path
+  int64_t win = 0, win_min_rows = 100000, win_max_chunks = kWinChunksCap;
+  // launch: window kernels where a level has windows (1: Jacobi / residual / norm, 2: the
+  // colour sweeps too)
+  int64_t win_kernels = 1;
   int64_t pdl = 1;                    // programmatic dependent launch
   int64_t solve_mode_host = 0;        // host-driven outer loop instead of the device WHILE graph
 };

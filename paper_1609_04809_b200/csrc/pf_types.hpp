@@ -85,6 +85,30 @@ struct SellView {
   int32_t table_n;  // distinct values in the table
 };
 
+// Block-window view of an operator (pf_window.cuh): for every block of kBlock consecutive
+// device rows the x entries its own rows read off the diagonal, covered by runs ("chunks")
+// of kWinChunk consecutive doubles, and every stored column re-expressed as a 16-bit byte
+// offset into the block's shared-memory window.  The row kernels copy the cover into shared
+// memory with coalesced loads and gather from there: a stored entry costs 2 + value bytes
+// instead of 4 + value bytes, and the per-entry x gather is a shared-memory read instead
+// of an L1/L2 request.
+// Window of a block: slots [0, kBlock) belong one to each thread (slot t = the diagonal
+// entry of row block * kBlock + t, and the padding entries of its last group): the kernel
+// puts there what the diagonal term must read — x_r for the residual-type rows, a signed
+// zero for the smoothers, which leave the diagonal term out (a x 0 = +0.0 subtracts as the
+// identity); the cover chunks follow, in ascending x order.
+constexpr int kWinChunk = 16;
+// Largest cover of a block: with the kBlock private slots 40 KB of window per block, so 5
+// blocks of 256 threads fit an SM.  A block whose cover is larger keeps an empty chunk
+// range and takes the plain row path.
+constexpr int kWinChunksCap = 304;
+struct WinView {
+  const uint16_t* __restrict__ cols16;    // window byte offset of each stored entry's column (A.cols positions)
+  const int32_t* __restrict__ chunk_ptr;  // [row blocks + 1] first chunk of each block
+  const int32_t* __restrict__ chunks;     // first x index of each chunk; slot = kBlock + 16 * (chunk - first) + offset
+  const uint8_t* __restrict__ dpos;       // per own row: position of its diagonal entry in the row
+};
+
 // Block schedule of a full-level row kernel (k_jacobi, k_residual).  Own rows sit
 // colour-major on the device (each colour in lattice order), so the identity schedule
 // sweeps colour 0 over the whole lattice, then colour 1, ...: each colour pass gathers its

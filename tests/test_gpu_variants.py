@@ -46,6 +46,11 @@ VARIANTS = {
     "bottom_staged_cooperative_wide_all": {"PF_BOTTOM_BLOCK_KERNEL": "0", "PF_WIDE_MAX_ROWS": "100000000",
                                            "PF_BOTTOM_JACOBI": "1"},
     "bottom_block_kernel_jacobi": {"PF_BOTTOM_JACOBI": "1"},
+    # the opt-in block-window row kernels (pf_window.cuh: a block's x cover staged in shared
+    # memory, 16-bit window offsets, the diagonal through a private signed-zero slot) on every
+    # level, colour sweeps included; fp64 and index-encoded operators
+    "block_windows": {"PF_WIN": "1", "PF_WIN_MIN_ROWS": "0", "PF_WIN_KERNELS": "2"},
+    "block_windows_fp64": {"PF_WIN": "1", "PF_WIN_MIN_ROWS": "0", "PF_WIN_KERNELS": "2", "PF_VALUE_INDEX": "0"},
     # memory checking: a 4 KB 0xFF guard zone after every device buffer (a read past an
     # array feeds NaN / -1 into the bit-exact comparisons; a write past one is reported
     # when the buffer is freed)
@@ -57,7 +62,7 @@ VARIANTS = {
 # The opt-in TMA sweep and the pure load-policy variants run with PF_RUN_SLOW=1 (each
 # re-runs the parity suite in a subprocess; the default GPU run keeps the layout, launch
 # structure and memory-checking variants).
-SLOW = {"sor_tma_everywhere", "sor_tma_fp64", "index_l1_streamed", "interleave_everywhere"}
+SLOW = {"sor_tma_everywhere", "sor_tma_fp64", "index_l1_streamed", "interleave_everywhere", "block_windows_fp64"}
 
 
 @pytest.mark.parametrize("name", [pytest.param(n, marks=[pytest.mark.slow, pytest.mark.skipif(
