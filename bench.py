@@ -522,6 +522,22 @@ C5_CONFIG = {
 }
 
 
+def c5_n1_reference():
+    """The one-GPU value of THIS configuration, for strong-scaling efficiency: the default
+    `python bench.py` (N = 1) headlines C2 and measures C5 on one GPU as a variant, so the
+    N = 1 line's `value` is not the denominator of an N > 1 C5 line.  Read from the last
+    committed one-GPU bench line (another run, possibly another box: say so)."""
+    src = os.path.join("profiles", "r02_bench_c2_latest.json")
+    try:
+        with open(os.path.join(ROOT, src)) as f:
+            v = json.load(f)["variants"]["c5_512cubed_lognormal_sor_1.2_n1"]
+        return {"value": v["value"], "unit": "DOF/s", "ms_per_step": v["ms_per_step"], "cycles": v["cycles"],
+                "source": f"{src} variants.c5_512cubed_lognormal_sor_1.2_n1 (committed one-GPU run of the same "
+                          "configuration; `python bench.py --gpus 1 --config c5` measures it live)"}
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "source": f"{src} unreadable ({e}); run `python bench.py --gpus 1 --config c5`"}
+
+
 def c5_solve(h, setup, world, rank, args, clk, dist, local, label):
     """Time solve_outer of an uploaded C5 hierarchy (device-resident and through host
     buffers); returns the measurement dict (rank-local figures, max-over-ranks times)."""
@@ -708,6 +724,8 @@ def run_c5(args):
             "e2e": m["e2e"], "gpu_launches": m["launches"], "clocks": clocks,
             "setup_seconds": setup_s, "upload_seconds": upload_s, "host_threads_per_rank": host_threads,
         }
+        if world > 1:
+            line["n1_same_config"] = c5_n1_reference()
         print(json.dumps(line), flush=True)
     h.close()
     if dist:
@@ -832,8 +850,15 @@ def run_b200_heat(args):
     nnz = int(run.setups[0].levels[-1].row_offsets[-1])
     n = len(u0)
     rhs_bytes = 12 * nnz + 8 * n + 8 * 3 * n + n
+    # ... and the bytes the kernel streams: 4 B column + the stored value width (the rhs
+    # operator M - dt/2 K of the constant-coefficient problem has few distinct values, so it
+    # is index-encoded like the level operators: 1 or 2 B per entry)
+    import numpy as np
+    distinct = int(np.unique(np.asarray(run.setups[0].rhs_op)).size)
+    vbytes = 1 if distinct <= 256 else 2 if distinct <= 65536 else 8
+    rhs_stored = (4 + vbytes) * nnz + 8 * n + 8 * 3 * n + n
     peak, peak_src = peaks()
-    achieved = rhs_bytes / (rhs_us / 1e6) / 1e9
+    achieved = rhs_stored / (rhs_us / 1e6) / 1e9
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -854,7 +879,15 @@ def run_b200_heat(args):
         "cycles_last_step": st.iterations,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "kernel": "k_cn_rhs (+ k_dirichlet): b = (M - dt/2 K) u + dt/2 (ln + lnx)",
-                     "kernel_us": rhs_us, "algorithmic_bytes_per_launch": rhs_bytes, "peak_source": peak_src,
+                     "kernel_us": rhs_us, "bytes_per_launch": rhs_stored,
+                     "bytes_formula": f"(4 + {vbytes}) z_all + 8 n (u) + 24 n (ln, lnx, b) + n (mask): the bytes the "
+                                      f"kernel streams ({distinct} distinct operator values: {vbytes} B value index)"
+                                      if vbytes < 8 else "12 z_all + 8 n + 24 n + n (fp64 values)",
+                     "fp64_csr_equivalent": {"bytes_per_launch": rhs_bytes,
+                                             "achieved": rhs_bytes / (rhs_us / 1e6) / 1e9,
+                                             "note": "SURVEY.md 8(d) work-equivalent rate (12 B per entry), not "
+                                                     "bytes moved"},
+                     "peak_source": peak_src,
                      "note": "the solve's dominant kernel is k_jacobi as in the default workload"},
         "load_assembly_us": load_us,
         "cpu_baseline": cpu,
