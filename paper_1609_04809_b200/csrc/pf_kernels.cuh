@@ -451,7 +451,7 @@ static __global__ void k_decide(const double* __restrict__ sumsq, int n_parts, d
   st->stop = stop;
   st->converged = conv;
   cudaGraphSetConditional(h_while, stop ? 0u : 1u);
-  cudaGraphSetConditional(h_if, stop ? 0u : 1u);
+  if (h_if != h_while) cudaGraphSetConditional(h_if, stop ? 0u : 1u);
 }
 
 // One colour of multicolour Gauss-Seidel / SOR, in place, rows [row0, row1).  Rows of

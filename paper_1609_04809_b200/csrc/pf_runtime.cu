@@ -144,6 +144,7 @@ const OptionSpec kOptions[] = {
     {"win_min_rows", "PF_WIN_MIN_ROWS", &Options::win_min_rows, true},
     {"win_max_chunks", "PF_WIN_MAX_CHUNKS", &Options::win_max_chunks, true},
     {"win_kernels", "PF_WIN_KERNELS", &Options::win_kernels, false},
+    {"solve_graph_if", "PF_SOLVE_GRAPH_IF", &Options::solve_graph_if, false},
     {"pdl", "PF_PDL", &Options::pdl, false},
     {"solve_mode_host", nullptr, &Options::solve_mode_host, false},  // env: PF_SOLVE_MODE=host
 };
@@ -955,12 +956,16 @@ cudaGraphNode_t single_leaf(cudaGraph_t g) {
   return leaf;
 }
 
-// solve_outer as ONE graph launch: WHILE(continue) { halo2(x); norm head; k_decide;
-// IF(continue) { rest of the V-cycle(s) } }, then the solve state copied to pinned host
-// memory.  No host round trip between cycles.
+// solve_outer as ONE graph launch, no host round trip between cycles; the solve state is
+// copied to pinned host memory at the end.  Two shapes (Options::solve_graph_if):
+//   0 (default)  head; WHILE(continue) { rest of the V-cycle(s); head }
+//   1            WHILE(continue) { head; IF(continue) { rest of the V-cycle(s) } }
+// with head = halo2(x), the norm head and k_decide.  Both run the same kernels in the same
+// order; the first evaluates one conditional node per outer iteration instead of two and
+// keeps the programmatic-launch chain from the cycle's last kernel into the next head.
 pf_hierarchy::GraphEntry& solve_graph(pf_hierarchy* h, pf_vector* x, const pf_vector* b,
                                       const pf_multigrid_config& cfg) {
-  const std::string key = graph_key("solve", x, b, cfg);
+  const std::string key = graph_key(h->opt.solve_graph_if ? "solve_if" : "solve", x, b, cfg);
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) return it->second;
   trace("solve graph: build");
@@ -975,6 +980,31 @@ pf_hierarchy::GraphEntry& solve_graph(pf_hierarchy* h, pf_vector* x, const pf_ve
   e.state_bytes = state_bytes;
   cudaGraph_t G = nullptr;
   PF_CUDA(cudaGraphCreate(&G, 0));
+  // capture `what` into graph g after nodes `deps`, counting its kernels into *count;
+  // returns the capture's leaf nodes
+  auto capture = [&](cudaGraph_t g, const std::vector<cudaGraphNode_t>& deps, int64_t* count, auto&& what) {
+    std::vector<cudaGraphNode_t> tail;
+    PF_CUDA(cudaStreamBeginCaptureToGraph(h->stream, g, deps.empty() ? nullptr : deps.data(), nullptr, deps.size(),
+                                          cudaStreamCaptureModeThreadLocal));
+    g_capture_counter = count;
+    try {
+      what();
+      cudaStreamCaptureStatus status;
+      const cudaGraphNode_t* d = nullptr;
+      size_t nd = 0;
+      PF_CUDA(cudaStreamGetCaptureInfo(h->stream, &status, nullptr, nullptr, &d, &nd));
+      tail.assign(d, d + nd);
+    } catch (...) {
+      g_capture_counter = nullptr;
+      cudaGraph_t dummy = nullptr;
+      cudaStreamEndCapture(h->stream, &dummy);
+      throw;
+    }
+    g_capture_counter = nullptr;
+    cudaGraph_t same = nullptr;
+    PF_CUDA(cudaStreamEndCapture(h->stream, &same));
+    return tail;
+  };
   try {
     cudaGraphConditionalHandle hw, hi;
     PF_CUDA(cudaGraphConditionalHandleCreate(&hw, G, 1, cudaGraphCondAssignDefault));
@@ -986,53 +1016,51 @@ pf_hierarchy::GraphEntry& solve_graph(pf_hierarchy* h, pf_vector* x, const pf_ve
     mp.width = state_bytes;
     mp.height = 1;
     PF_CUDA(cudaGraphAddMemsetNode(&reset, G, nullptr, 0, &mp));
+    int64_t head = 0, rest = 0, head_again = 0;
+    auto enq_head = [&](cudaGraphConditionalHandle h_if) {
+      enq_scatter(h, top, PF_CH_HALO2, x->cur());
+      enq_norm_head(h, x, b->cur(), cfg);
+      launcher(h)(1, 32, k_decide, static_cast<const double*>(h->levels[top].sumsq.p), h->n_sub,
+                  cfg.outer_tol, cfg.outer_max_cycles, static_cast<SolveState*>(e.state), hw, h_if);
+    };
+    auto enq_rest = [&] {
+      enq_cycle(h, top, x, b->cur(), cfg, fused_head(cfg));
+      for (int j = 1; j < cfg.cycles; ++j) enq_vcycle(h, x, b->cur(), cfg);
+    };
     cudaGraphNodeParams wp = {};
     wp.type = cudaGraphNodeTypeConditional;
     wp.conditional.handle = hw;
     wp.conditional.type = cudaGraphCondTypeWhile;
     wp.conditional.size = 1;
     cudaGraphNode_t wnode = nullptr;
-    PF_CUDA(cudaGraphAddNode(&wnode, G, &reset, 1, &wp));
-    cudaGraph_t body = wp.conditional.phGraph_out[0];
-    PF_CUDA(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
-    // head: halo2(x) of v_cycle entry, norm head, decision
-    int64_t head = 0, rest = 0;
-    PF_CUDA(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    g_capture_counter = &head;
-    try {
-      enq_scatter(h, top, PF_CH_HALO2, x->cur());
-      enq_norm_head(h, x, b->cur(), cfg);
-      launcher(h)(1, 32, k_decide, static_cast<const double*>(h->levels[top].sumsq.p), h->n_sub,
-                  cfg.outer_tol, cfg.outer_max_cycles, static_cast<SolveState*>(e.state), hw, hi);
-    } catch (...) {
-      g_capture_counter = nullptr;
-      cudaStreamEndCapture(h->stream, &body);
-      throw;
+    if (!h->opt.solve_graph_if) {
+      std::vector<cudaGraphNode_t> tail = capture(G, {reset}, &head, [&] { enq_head(hw); });
+      trace("solve graph: head captured");
+      if (tail.empty()) tail.push_back(reset);
+      PF_CUDA(cudaGraphAddNode(&wnode, G, tail.data(), tail.size(), &wp));
+      cudaGraph_t body = wp.conditional.phGraph_out[0];
+      capture(body, {}, &rest, [&] {
+        enq_rest();
+        g_capture_counter = &head_again;  // the head again, right behind the cycle
+        enq_head(hw);
+      });
+      if (head_again != head) state("solve graph: the two captures of the head differ");
+    } else {
+      PF_CUDA(cudaGraphAddNode(&wnode, G, &reset, 1, &wp));
+      cudaGraph_t body = wp.conditional.phGraph_out[0];
+      PF_CUDA(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
+      capture(body, {}, &head, [&] { enq_head(hi); });
+      trace("solve graph: head captured");
+      cudaGraphNode_t leaf = single_leaf(body);
+      cudaGraphNodeParams ip = {};
+      ip.type = cudaGraphNodeTypeConditional;
+      ip.conditional.handle = hi;
+      ip.conditional.type = cudaGraphCondTypeIf;
+      ip.conditional.size = 1;
+      cudaGraphNode_t inode = nullptr;
+      PF_CUDA(cudaGraphAddNode(&inode, body, &leaf, 1, &ip));
+      capture(ip.conditional.phGraph_out[0], {}, &rest, enq_rest);
     }
-    g_capture_counter = nullptr;
-    PF_CUDA(cudaStreamEndCapture(h->stream, &body));
-    trace("solve graph: head captured");
-    cudaGraphNode_t leaf = single_leaf(body);
-    cudaGraphNodeParams ip = {};
-    ip.type = cudaGraphNodeTypeConditional;
-    ip.conditional.handle = hi;
-    ip.conditional.type = cudaGraphCondTypeIf;
-    ip.conditional.size = 1;
-    cudaGraphNode_t inode = nullptr;
-    PF_CUDA(cudaGraphAddNode(&inode, body, &leaf, 1, &ip));
-    cudaGraph_t rest_g = ip.conditional.phGraph_out[0];
-    PF_CUDA(cudaStreamBeginCaptureToGraph(h->stream, rest_g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    g_capture_counter = &rest;
-    try {
-      enq_cycle(h, top, x, b->cur(), cfg, fused_head(cfg));
-      for (int j = 1; j < cfg.cycles; ++j) enq_vcycle(h, x, b->cur(), cfg);
-    } catch (...) {
-      g_capture_counter = nullptr;
-      cudaStreamEndCapture(h->stream, &rest_g);
-      throw;
-    }
-    g_capture_counter = nullptr;
-    PF_CUDA(cudaStreamEndCapture(h->stream, &rest_g));
     trace("solve graph: body captured");
     cudaGraphNode_t copy = nullptr;
     PF_CUDA(cudaGraphAddMemcpyNode1D(&copy, G, &wnode, 1, e.host_state, e.state, state_bytes,

@@ -289,6 +289,7 @@ struct Options {
   // launch: window kernels where a level has windows (1: Jacobi / residual / norm, 2: the
   // colour sweeps too)
   int64_t win_kernels = 1;
+  int64_t solve_graph_if = 0;         // device solve graph with an IF node inside the WHILE body (the older shape)
   int64_t pdl = 1;                    // programmatic dependent launch
   int64_t solve_mode_host = 0;        // host-driven outer loop instead of the device WHILE graph
 };

@@ -45,7 +45,9 @@ VARIANTS = {
     # rows on every launch that fits them, damped Jacobi through the bottom kernel too
     "bottom_staged_cooperative_wide_all": {"PF_BOTTOM_BLOCK_KERNEL": "0", "PF_WIDE_MAX_ROWS": "100000000",
                                            "PF_BOTTOM_JACOBI": "1"},
-    "bottom_block_kernel_jacobi": {"PF_BOTTOM_JACOBI": "1"},
+    # ... through the one-block bottom kernel, and the solve graph's older shape (IF node
+    # inside the WHILE body)
+    "bottom_block_kernel_jacobi": {"PF_BOTTOM_JACOBI": "1", "PF_SOLVE_GRAPH_IF": "1"},
     # the opt-in block-window row kernels (pf_window.cuh: a block's x cover staged in shared
     # memory, 16-bit window offsets, the diagonal through a private signed-zero slot) on every
     # level, colour sweeps included; fp64 and index-encoded operators
