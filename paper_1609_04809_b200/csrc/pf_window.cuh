@@ -11,6 +11,11 @@
 // request per entry.  Rows do the same operations in the same order as the plain kernels
 // (row_offdiag / row_dot of pf_kernels.cuh), so results are bit-identical.
 //
+// Status: opt-in (Options::win, PF_WIN=1), parity-tested, measured SLOWER than the plain
+// kernels (C2 finest Jacobi sweep 87.4 vs 74.5 us, SOR 106.5 vs 103.8 us, fp64 values 133 vs
+// 112 us): the SM's LSU data pipe is as busy as before (shared-memory gathers, value-table
+// lookups and the staging's own loads and stores), see profiles/r02_sweep_experiments.md.
+//
 // Layout of a block's window in shared memory (WinView, pf_types.hpp): slot t < kBlock is
 // private to thread t — its row's diagonal and padding entries point there — and holds
 // x_r in the residual-type kernels and a zero of the diagonal's sign in the smoothers, whose
